@@ -1,0 +1,199 @@
+/*
+ * moe_eamc.h -- C ABI of the B200-native EAM/EAMC decision path
+ * (MoE-Infinity, arXiv 2401.14361).  libmoe_eamc.so implements every entry
+ * point below with hand-written sm_100a CUDA kernels; there is no CPU
+ * fallback: a missing or unusable GPU is reported as MOE_ERR_CUDA.
+ *
+ * The reference boundary is the C++ library API of moesim::core
+ * (/root/reference/proj/core/include/moesim/{eam,policy}.hpp).  Each entry
+ * point cites the reference symbol it replaces.  Reference C++ exceptions
+ * map to status codes; the C++ wrapper include/moesim_b200/eamc.hpp maps
+ * them back so the reference's callers compile unchanged.
+ *
+ * Conventions
+ *  - Count matrices are row-major L x E uint64 (eam.hpp:55), exactly the
+ *    reference Eam storage.  Batches are [n][L][E].
+ *  - Functions without a `_device` suffix take HOST pointers and are
+ *    synchronous.  `_device` variants take device pointers and a
+ *    cudaStream_t (passed as void*) and are stream-ordered.
+ *  - Threading: one handle per writer.  match/match_within/prefetch are
+ *    const readers (eam.hpp:89-94); insert needs exclusivity.
+ *  - Errors: the status code, plus a thread-local message from
+ *    moe_last_error().
+ */
+#ifndef MOE_EAMC_H_
+#define MOE_EAMC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_EAMC_ABI_VERSION 1
+
+typedef enum moe_status {
+  MOE_OK = 0,
+  MOE_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (eam.cpp:55-58,:109,:114,:153-158) */
+  MOE_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range (eam.cpp:43-46,:66; policy.cpp:91,:130) */
+  MOE_ERR_SNAPSHOT = 3,         /* EamcSnapshotError (eam.hpp:63-65) */
+  MOE_ERR_LOGIC = 4,            /* std::logic_error (policy.cpp:164) */
+  MOE_ERR_CUDA = 5,             /* no usable sm_100 device / kernel failure */
+  MOE_ERR_NCCL = 6,
+  MOE_ERR_OOM = 7,
+  MOE_ERR_OVERFLOW = 8 /* a count outside the range where the reference's fp64
+                          arithmetic is exact (row sum of squares >= 2^53) */
+} moe_status;
+
+/* ModelShape (model.hpp:19-29) */
+typedef struct moe_shape {
+  uint32_t n_layers;
+  uint32_t n_experts_per_layer;
+  uint32_t top_k;
+} moe_shape;
+
+typedef enum moe_phase { MOE_PHASE_PREFILL = 0, MOE_PHASE_DECODE = 1 } moe_phase; /* eam.hpp:17 */
+typedef enum moe_eam_kind { MOE_KIND_ITERATION = 0, MOE_KIND_REQUEST = 1 } moe_eam_kind; /* eam.hpp:16 */
+
+/* EamcMatch (eam.hpp:67-71).  A "none" result (empty collection / shard) is
+ * index = seq = UINT64_MAX, distance = +inf. */
+typedef struct moe_match {
+  uint64_t index;
+  uint64_t seq;
+  double distance;
+} moe_match;
+
+/* PrefetchCandidate (policy.hpp:46-50) */
+typedef struct moe_candidate {
+  uint32_t layer_idx;
+  uint32_t expert_idx;
+  double priority;
+} moe_candidate;
+
+/* SlotView (policy.hpp:96-101) */
+typedef struct moe_slot_view {
+  uint64_t slot;
+  uint32_t layer_idx;
+  uint32_t expert_idx;
+  uint8_t prefetch_protected;
+  uint8_t pinned;
+  uint8_t pad_[6];
+} moe_slot_view;
+
+typedef struct moe_eamc moe_eamc; /* opaque device-resident Eamc */
+
+int moe_abi_version(void);
+const char* moe_last_error(void);
+/* Device properties the library keys its launch geometry on. */
+moe_status moe_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
+                           size_t* l2_bytes);
+
+/* ---- collection lifecycle: Eamc(ModelShape, Phase, capacity) eam.cpp:106-111 ---- */
+/* count_bytes: storage width of one count on the device, 1 or 2 (0 = 1).
+ * The collection widens itself (1 -> 2 bytes) when an inserted EAM or a
+ * probe needs it; counts that need more are MOE_ERR_OVERFLOW. */
+moe_status moe_eamc_create(const moe_shape* shape, moe_phase phase, uint64_t capacity,
+                           int count_bytes, int device, moe_eamc** out);
+moe_status moe_eamc_destroy(moe_eamc* h);
+/* shape()/phase()/capacity()/size()/next_seq (eam.hpp:80-87) */
+moe_status moe_eamc_info(const moe_eamc* h, moe_shape* shape, int* phase, uint64_t* capacity,
+                         uint64_t* size, uint64_t* next_seq, int* count_bytes);
+/* entry(i) / entry_seq(i) (eam.hpp:86-87); counts may be NULL. */
+moe_status moe_eamc_entry(const moe_eamc* h, uint64_t index, uint64_t* counts, uint64_t* seq);
+
+/* ---- construction: Eamc::insert (eam.cpp:152-178) ---- */
+/* *evicted_slot = slot replaced (-1 when appended); evicted_counts (nullable)
+ * receives the evicted Eam. */
+moe_status moe_eamc_insert(moe_eamc* h, const uint64_t* counts, moe_eam_kind kind,
+                           moe_phase phase, int64_t* evicted_slot, uint64_t* evicted_counts);
+/* Batched construction (K7): n request-level EAMs inserted in order with the
+ * exact semantics of n sequential Eamc::insert calls (as driven by
+ * moesim_main.cpp:212-216).  evicted_slots[n] (nullable). */
+moe_status moe_eamc_build(moe_eamc* h, const uint64_t* counts, uint64_t n,
+                          int64_t* evicted_slots);
+/* Bulk append with caller-given seqs (Eamc::load semantics, eam.cpp:229-244);
+ * used for snapshots and for P-sharded collections where the global
+ * insertion number of every entry is assigned by the caller.  Entries are
+ * u64 [n][L][E]; next_seq becomes max(next_seq, max(seqs)+1). */
+moe_status moe_eamc_append(moe_eamc* h, const uint64_t* counts, const uint64_t* seqs, uint64_t n);
+/* Same, with counts already narrow on the host ([n][L][E] of count_bytes). */
+moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_bytes,
+                                  const uint64_t* seqs, uint64_t n);
+
+/* ---- matching: Eamc::match (eam.cpp:118-129) over a probe batch ---- */
+/* probes [n][L][E] u64 host; out[n]; found[n] (nullable). */
+moe_status moe_eamc_match(const moe_eamc* h, const uint64_t* probes, uint64_t n_probes,
+                          moe_match* out, uint8_t* found);
+/* Device variant: probes are device [n][L][E] of probe_bytes (1, 2 or 8)
+ * bytes per count, out is device moe_match[n]. */
+moe_status moe_eamc_match_device(const moe_eamc* h, const void* probes, int probe_bytes,
+                                 uint64_t n_probes, moe_match* out, void* stream);
+/* Eamc::match_within (eam.cpp:131-150): every entry within `window` of the
+ * best distance, sorted by (distance, seq).  *n_out = total number; at most
+ * cap are written. */
+moe_status moe_eamc_match_within(const moe_eamc* h, const uint64_t* probe, double window,
+                                 moe_match* out, uint64_t cap, uint64_t* n_out);
+/* Lexicographic (distance, seq) merge of per-shard results (P-sharded
+ * matching): parts is [n_parts][n] -> out[n]. */
+moe_status moe_match_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out);
+moe_status moe_match_merge_device(const moe_match* parts, uint64_t n_parts, uint64_t n,
+                                  moe_match* out, void* stream);
+
+/* eam_distance (eam.cpp:91-104), evaluated on the device. */
+moe_status moe_eam_distance(const moe_shape* shape, const uint64_t* a, const uint64_t* b,
+                            double* out);
+
+/* ---- policy (policy.cpp) ---- */
+/* prefetch_priorities (policy.cpp:88-126) and, if apply_floor_filter, the
+ * engine's floor filter (engine.cpp:663-668).  Candidates in the reference
+ * order (priority desc, ExpertId asc); *n_out total, at most cap written. */
+moe_status moe_prefetch_priorities(const moe_eamc* h, const uint64_t* cur_eam,
+                                   uint32_t current_layer, int apply_floor_filter,
+                                   moe_candidate* out, uint64_t cap, uint64_t* n_out);
+/* Fused decision (K5+K6): the prefetch order above and the eviction victim
+ * over `slots` priced from request_eam, in one launch. */
+moe_status moe_decide(const moe_eamc* h, const uint64_t* cur_eam, uint32_t current_layer,
+                      const uint64_t* request_eam, const moe_slot_view* slots, uint64_t n_slots,
+                      moe_candidate* out, uint64_t cap, uint64_t* n_out, int64_t* victim);
+/* cache_priority (policy.cpp:128-141) */
+moe_status moe_cache_priority(const moe_shape* shape, const uint64_t* request_eam,
+                              uint32_t layer, uint32_t expert, double* out);
+/* select_eviction_victim (policy.cpp:143-159); *victim = slot or -1. */
+moe_status moe_select_eviction_victim(const moe_shape* shape, const uint64_t* request_eam,
+                                      const moe_slot_view* slots, uint64_t n_slots,
+                                      int64_t* victim);
+
+/* ---- tracing: Eam::record (eam.cpp:41-52) from router top-k ids ---- */
+/* topk_idx [n_tokens][L][top_k] with idx_bytes in {1,2,4}; request r owns
+ * tokens [offsets[r], offsets[r+1]).  counts [R][L][E] u64 are ACCUMULATED
+ * (Eam::record adds).  All-or-nothing: any index >= E returns
+ * MOE_ERR_OUT_OF_RANGE with counts untouched (eam.cpp:42-47). */
+moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_bytes,
+                         uint64_t n_tokens, const uint64_t* offsets, uint64_t n_requests,
+                         uint64_t* counts);
+/* Device variant: all pointers device; counts_u32 [R][L][E] accumulated. */
+moe_status moe_eam_trace_device(const moe_shape* shape, const void* topk_idx, int idx_bytes,
+                                uint64_t n_tokens, const uint64_t* offsets, uint64_t n_requests,
+                                uint32_t* counts_u32, int* bad_index_flag, void* stream);
+
+/* eamc_capacity_bound (eam.cpp:258-268) */
+moe_status moe_eamc_capacity_bound(const moe_shape* shape, double similarity, uint64_t* out);
+
+/* ---- snapshots: Eamc::save / Eamc::load (eam.cpp:184-256), JSON v1 ---- */
+moe_status moe_eamc_save(const moe_eamc* h, const char* path);
+/* expected may be NULL (load(path)) or the configured shape (load(path, shape)). */
+moe_status moe_eamc_load(const char* path, const moe_shape* expected, int device,
+                         moe_eamc** out);
+
+/* ---- synthetic input families (host, bit-identical to the reference) ---- */
+/* bench_match's random_request_eam stream (bench.cpp:44-54,60-66): skips
+ * `skip` EAMs of Rng::stream(seed, 0x6265636E), then writes n EAMs as
+ * count_bytes-wide counts (1, 2 or 8) into out [n][L][E]. */
+moe_status moe_gen_bench_family(uint64_t seed, uint32_t L, uint32_t E, uint64_t skip, uint64_t n,
+                                int count_bytes, void* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_EAMC_H_ */

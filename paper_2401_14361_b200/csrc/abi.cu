@@ -1,0 +1,1102 @@
+// abi.cu -- the C ABI of include/moe_eamc.h on top of the sm_100a kernels.
+//
+// Host code here only marshals buffers, validates arguments the way the
+// reference does (and returns the status its exception maps to), sizes the
+// launch geometry and sequences kernels.  Every number the path produces
+// (counts, norms, distances, argmins, windows, aggregates, priorities,
+// orders, victims, histograms) is computed on the GPU.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "host.hpp"
+#include "kernels.cuh"
+
+using moe::DevColl;
+using moe::DevProbes;
+using moe::MatchGeom;
+using moe::MatchWork;
+
+namespace {
+
+thread_local std::string g_err;
+
+moe_status fail(moe_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? MOE_ERR_OOM : MOE_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                     \
+  } while (0)
+#define CKS(expr)                    \
+  do {                               \
+    moe_status s_ = (expr);          \
+    if (s_ != MOE_OK) return s_;     \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    const size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) n = want;
+    return e;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct PinBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMallocHost(&p, std::max<size_t>(bytes, 64));
+    if (e == cudaSuccess) n = std::max<size_t>(bytes, 64);
+    return e;
+  }
+  ~PinBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+int g_n_sm[64] = {0};
+
+moe_status device_ok(int device, int* n_sm) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(MOE_ERR_CUDA, "no CUDA device visible (libmoe_eamc has no CPU fallback)");
+  if (device < 0 || device >= n) return fail(MOE_ERR_INVALID_ARGUMENT, "bad device %d", device);
+  if (device < 64 && g_n_sm[device]) {
+    *n_sm = g_n_sm[device];
+    return MOE_OK;
+  }
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(MOE_ERR_CUDA, "device %d is sm_%d%d; libmoe_eamc is built for sm_100a only", device,
+                prop.major, prop.minor);
+  if (device < 64) g_n_sm[device] = prop.multiProcessorCount;
+  *n_sm = prop.multiProcessorCount;
+  return MOE_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+moe_status check_shape(const moe_shape* s) {
+  // ModelShape::validate (model.cpp:13-19)
+  if (!s) return fail(MOE_ERR_INVALID_ARGUMENT, "null shape");
+  if (s->n_layers < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "ModelShape: n_layers must be >= 1");
+  if (s->n_experts_per_layer < 1)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "ModelShape: n_experts_per_layer must be >= 1");
+  if (s->top_k < 1 || s->top_k > s->n_experts_per_layer)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "ModelShape: top_k must be in [1, n_experts_per_layer]");
+  return MOE_OK;
+}
+
+uint32_t row_bytes(uint32_t E, int cb) { return (E * cb + 15) / 16 * 16; }
+
+}  // namespace
+
+struct moe_eamc {
+  int device = 0;
+  int n_sm = 148;
+  moe_shape shape{};
+  int phase = 1;
+  uint64_t capacity = 0;
+  uint64_t next_seq = 0;
+  DevColl c;
+  cudaStream_t st = nullptr;
+  // workspace
+  DevBuf raw, packed, ia, sqa, T, bcnt, bucket, over_list, small, out, partials, wl, agg, cand,
+      slots, req;
+  PinBuf pin;
+
+  ~moe_eamc() {
+    if (c.counts) cudaFree(c.counts);
+    if (c.ibT) cudaFree(c.ibT);
+    if (c.sqb) cudaFree(c.sqb);
+    if (c.seq) cudaFree(c.seq);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+namespace {
+
+constexpr uint32_t kBucketCap = 64;
+
+// Grow the device collection to hold `need` entries (<= capacity).
+moe_status ensure_alloc(moe_eamc* h, uint64_t need) {
+  DevColl& c = h->c;
+  if (need <= c.cap) return MOE_OK;
+  uint64_t nc = std::max<uint64_t>(need, std::min<uint64_t>(h->capacity, std::max<uint64_t>(c.cap * 2, 1024)));
+  nc = std::min<uint64_t>(std::max(nc, need), h->capacity);
+  const uint64_t LR = (uint64_t)c.L * c.RB;
+  uint8_t* counts = nullptr;
+  float* ibT = nullptr;
+  double* sqb = nullptr;
+  uint64_t* seq = nullptr;
+  // +kNT entries of slack so TMA boxes of the last tile stay in-bounds
+  CK(cudaMalloc(&counts, (nc + moe::kNT) * LR));
+  CK(cudaMalloc(&ibT, (size_t)c.L * nc * sizeof(float)));
+  CK(cudaMalloc(&sqb, (size_t)nc * c.L * sizeof(double)));
+  CK(cudaMalloc(&seq, (size_t)nc * sizeof(uint64_t)));
+  CK(cudaMemsetAsync(counts, 0, (nc + moe::kNT) * LR, h->st));
+  if (c.size) {
+    CK(cudaMemcpyAsync(counts, c.counts, (size_t)c.size * LR, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpy2DAsync(ibT, nc * sizeof(float), c.ibT, c.cap * sizeof(float),
+                         (size_t)c.size * sizeof(float), c.L, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(sqb, c.sqb, (size_t)c.size * c.L * sizeof(double),
+                       cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(seq, c.seq, (size_t)c.size * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                       h->st));
+  }
+  CK(cudaStreamSynchronize(h->st));
+  if (c.counts) cudaFree(c.counts);
+  if (c.ibT) cudaFree(c.ibT);
+  if (c.sqb) cudaFree(c.sqb);
+  if (c.seq) cudaFree(c.seq);
+  c.counts = counts;
+  c.ibT = ibT;
+  c.sqb = sqb;
+  c.seq = seq;
+  c.cap = nc;
+  return MOE_OK;
+}
+
+// Re-encode the collection with 2-byte counts.
+moe_status widen(moe_eamc* h) {
+  DevColl& c = h->c;
+  if (c.cb == 2) return fail(MOE_ERR_OVERFLOW, "count exceeds 65535 (2-byte storage limit)");
+  const uint32_t RB2 = row_bytes(c.E, 2);
+  const uint64_t rows = c.cap ? (c.cap + moe::kNT) * c.L : 0;
+  if (c.counts) {
+    uint8_t* nc = nullptr;
+    CK(cudaMalloc(&nc, rows * RB2));
+    CK(moe::launch_widen(c.counts, nc, rows, c.RB, RB2, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    cudaFree(c.counts);
+    c.counts = nc;
+  }
+  c.cb = 2;
+  c.RB = RB2;
+  c.C = RB2 / 16;
+  return MOE_OK;
+}
+
+uint64_t width_max(int cb) { return cb == 1 ? 255ull : 65535ull; }
+
+// H2D (or D2D) + pack probes into h->packed/ia/sqa at the collection's
+// width, widening the collection if a count needs it.
+moe_status prep_probes(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bool src_device,
+                       cudaStream_t st, DevProbes* pr) {
+  DevColl& c = h->c;
+  const uint64_t cells = (uint64_t)c.L * c.E;
+  const void* dsrc = src;
+  if (!src_device) {
+    CK(h->raw.ensure(n * cells * src_bytes));
+    CK(cudaMemcpyAsync(h->raw.p, src, n * cells * src_bytes, cudaMemcpyHostToDevice, st));
+    dsrc = h->raw.p;
+  }
+  for (;;) {
+    const uint64_t LR = (uint64_t)c.L * c.RB;
+    CK(h->packed.ensure(n * LR + 16));
+    CK(h->ia.ensure(n * c.L * sizeof(float)));
+    CK(h->sqa.ensure(n * c.L * sizeof(double)));
+    CK(h->small.ensure(256));
+    CK(h->pin.ensure(256));
+    unsigned long long* dmax = h->small.as<unsigned long long>();
+    CK(cudaMemsetAsync(dmax, 0, 8, st));
+    CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, h->packed.as<uint8_t>(),
+                        h->ia.as<float>(), h->sqa.as<double>(), nullptr, 0, 0, dmax, st));
+    CK(cudaMemcpyAsync(h->pin.p, dmax, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint64_t mx = *h->pin.as<unsigned long long>();
+    if (mx <= width_max(c.cb)) break;
+    if (mx > 65535ull)
+      return fail(MOE_ERR_OVERFLOW,
+                  "count %llu exceeds the 2-byte device storage of this build", (unsigned long long)mx);
+    CKS(widen(h));
+  }
+  pr->Q = (uint32_t)n;
+  pr->packed = h->packed.as<uint8_t>();
+  pr->ia = h->ia.as<float>();
+  pr->sqa = h->sqa.as<double>();
+  return MOE_OK;
+}
+
+uint32_t pick_qt(uint64_t Q) {
+  if (const char* e = getenv("MOE_QT")) {
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) return (uint32_t)v;
+  }
+  if (Q <= 1) return 1;
+  if (Q <= 2) return 2;
+  if (Q <= 4) return 4;
+  if (Q <= 64) return 8;
+  return 16;
+}
+
+struct Plan {
+  MatchGeom g;
+  CUtensorMap map;
+};
+
+moe_status make_plan(moe_eamc* h, int mode, uint32_t QT, Plan* p) {
+  if (!moe::plan_match(h->c, h->n_sm, mode, QT, &p->g))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "shape %ux%u does not fit the matcher's shared memory",
+                h->c.L, h->c.E);
+  CK(moe::encode_tmap(h->c, p->g.G, &p->map));
+  return MOE_OK;
+}
+
+// Full matching pipeline for an already-packed probe batch; `out` is a
+// device array.  Synchronizes `st` once (overflow check).
+moe_status match_packed(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaStream_t st) {
+  const uint64_t Q = pr.Q;
+  if (Q == 0) return MOE_OK;
+  DevColl& c = h->c;
+  CK(h->T.ensure(Q * 4));
+  CK(h->bcnt.ensure(Q * 4));
+  CK(h->bucket.ensure(Q * kBucketCap * sizeof(uint2)));
+  CK(h->over_list.ensure(Q * 4));
+  CK(h->small.ensure(256));
+  CK(h->pin.ensure(256));
+  MatchWork w;
+  w.T = h->T.as<uint32_t>();
+  w.bcnt = h->bcnt.as<uint32_t>();
+  w.bucket = h->bucket.as<uint2>();
+  w.bcap = kBucketCap;
+  w.over_list = h->over_list.as<uint32_t>();
+  w.over_n = h->small.as<uint32_t>() + 4;
+  CK(cudaMemsetAsync(w.T, 0x7f, Q * 4, st));  // 0x7f7f7f7f = 3.4e38f > any distance
+  CK(cudaMemsetAsync(w.bcnt, 0, Q * 4, st));
+  CK(cudaMemsetAsync(w.over_n, 0, 4, st));
+  if (c.size == 0) {
+    CK(moe::launch_refine(c, pr, w, out, nullptr, nullptr, 0, st));
+    return MOE_OK;
+  }
+  Plan p;
+  CKS(make_plan(h, 0, pick_qt(Q), &p));
+  CK(moe::launch_screen(p.map, c, pr, p.g, w, st));
+  CK(moe::launch_refine(c, pr, w, out, nullptr, nullptr, 0, st));
+  CK(cudaMemcpyAsync(h->pin.p, w.over_n, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const uint32_t n_over = *h->pin.as<uint32_t>();
+  if (n_over) {
+    Plan pe;
+    CKS(make_plan(h, 1, 1, &pe));
+    w.part_chunk = 1024;
+    CK(h->partials.ensure((size_t)w.part_chunk * pe.g.grid * sizeof(moe_match)));
+    w.partials = h->partials.as<moe_match>();
+    CK(moe::launch_exact(pe.map, c, pr, pe.g, w, w.over_list, n_over, w.T, out, st));
+  }
+  return MOE_OK;
+}
+
+// Unpack one device entry to host u64 counts.
+moe_status read_entry(moe_eamc* h, uint64_t slot, uint64_t* counts, uint64_t* seq) {
+  DevColl& c = h->c;
+  const uint64_t LR = (uint64_t)c.L * c.RB;
+  std::vector<uint8_t> row(LR);
+  if (counts) {
+    CK(cudaMemcpy(row.data(), c.counts + slot * LR, LR, cudaMemcpyDeviceToHost));
+    for (uint32_t l = 0; l < c.L; ++l)
+      for (uint32_t e = 0; e < c.E; ++e)
+        counts[(uint64_t)l * c.E + e] =
+            c.cb == 1 ? row[l * c.RB + e]
+                      : reinterpret_cast<const uint16_t*>(row.data() + (size_t)l * c.RB)[e];
+  }
+  if (seq) CK(cudaMemcpy(seq, c.seq + slot, 8, cudaMemcpyDeviceToHost));
+  return MOE_OK;
+}
+
+// Stage n EAMs (device raw) as packed rows in a private staging set.
+struct Staged {
+  DevBuf packed, ia, sqa;
+  DevProbes pr;
+};
+
+moe_status stage_entries(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t n, Staged* s) {
+  DevColl& c = h->c;
+  for (;;) {
+    const uint64_t LR = (uint64_t)c.L * c.RB;
+    CK(s->packed.ensure(n * LR + 16));
+    CK(s->ia.ensure(n * c.L * 4));
+    CK(s->sqa.ensure(n * c.L * 8));
+    CK(h->small.ensure(256));
+    CK(h->pin.ensure(256));
+    unsigned long long* dmax = h->small.as<unsigned long long>();
+    CK(cudaMemsetAsync(dmax, 0, 8, h->st));
+    CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, s->packed.as<uint8_t>(),
+                        s->ia.as<float>(), s->sqa.as<double>(), nullptr, 0, 0, dmax, h->st));
+    CK(cudaMemcpyAsync(h->pin.p, dmax, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    const uint64_t mx = *h->pin.as<unsigned long long>();
+    if (mx <= width_max(c.cb)) break;
+    if (mx > 65535ull)
+      return fail(MOE_ERR_OVERFLOW, "count %llu exceeds the 2-byte device storage of this build",
+                  (unsigned long long)mx);
+    CKS(widen(h));
+  }
+  s->pr.Q = (uint32_t)n;
+  s->pr.packed = s->packed.as<uint8_t>();
+  s->pr.ia = s->ia.as<float>();
+  s->pr.sqa = s->sqa.as<double>();
+  return MOE_OK;
+}
+
+// Sequential Eamc::insert semantics for a staged batch (K7 replay).
+moe_status replay_staged(moe_eamc* h, Staged& s, int64_t* evicted_slots) {
+  DevColl& c = h->c;
+  const uint32_t n = s.pr.Q;
+  uint32_t i = 0;
+  // appends below capacity (eam.cpp:160-162)
+  const uint64_t room = h->capacity - c.size;
+  const uint32_t n_app = (uint32_t)std::min<uint64_t>(room, n);
+  if (n_app) {
+    CKS(ensure_alloc(h, c.size + n_app));
+    CK(moe::launch_append_staged(c, s.pr, 0, n_app, c.size, h->st));
+    std::vector<uint64_t> seqs(n_app);
+    for (uint32_t k = 0; k < n_app; ++k) seqs[k] = h->next_seq + k;
+    CK(cudaMemcpyAsync(c.seq + c.size, seqs.data(), n_app * 8, cudaMemcpyHostToDevice, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    c.size += n_app;
+    h->next_seq += n_app;
+    if (evicted_slots)
+      for (uint32_t k = 0; k < n_app; ++k) evicted_slots[k] = -1;
+    i = n_app;
+  }
+  if (i == n) return MOE_OK;
+  // at-capacity replacement steps, stream-ordered on the device; a bucket
+  // overflow halts the remaining launched steps and is resolved exactly.
+  const uint32_t n_rep = n - i;
+  CK(h->out.ensure((size_t)n * sizeof(moe_match)));
+  moe_match* vic = h->out.as<moe_match>();
+  CK(h->T.ensure(4));
+  CK(h->bcnt.ensure(4));
+  CK(h->bucket.ensure(kBucketCap * sizeof(uint2)));
+  CK(h->small.ensure(256));
+  CK(h->pin.ensure(256));
+  int* halt = h->small.as<int>() + 16;
+  CK(cudaMemsetAsync(halt, 0, 4, h->st));
+  Plan p;
+  CKS(make_plan(h, 0, 1, &p));
+  MatchWork w;
+  w.T = h->T.as<uint32_t>();
+  w.bcnt = h->bcnt.as<uint32_t>();
+  w.bucket = h->bucket.as<uint2>();
+  w.bcap = kBucketCap;
+  const uint64_t LR = (uint64_t)c.L * c.RB;
+  const uint32_t kBatch = 256;
+  uint32_t k = i;
+  while (k < n) {
+    const uint32_t kend = std::min(n, k + kBatch);
+    for (uint32_t j = k; j < kend; ++j) {
+      DevProbes one;
+      one.Q = 1;
+      one.packed = s.pr.packed + (uint64_t)j * LR;
+      one.ia = s.pr.ia + (uint64_t)j * c.L;
+      one.sqa = s.pr.sqa + (uint64_t)j * c.L;
+      CK(cudaMemsetAsync(w.T, 0x7f, 4, h->st));
+      CK(cudaMemsetAsync(w.bcnt, 0, 4, h->st));
+      CK(moe::launch_screen(p.map, c, one, p.g, w, h->st));
+      CK(moe::launch_refine(c, one, w, vic + j, halt, halt, j + 1, h->st));
+      CK(moe::launch_replace(c, s.pr, j, vic + j, h->next_seq + (j - i), halt, h->st));
+    }
+    CK(cudaMemcpyAsync(h->pin.p, halt, 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    const int hv = *h->pin.as<int>();
+    if (hv == 0) {
+      k = kend;
+      continue;
+    }
+    // step j0 overflowed its candidate bucket: resolve it with the exact
+    // pass, apply the replacement, and resume after it.
+    const uint32_t j0 = (uint32_t)hv - 1;
+    CK(cudaMemsetAsync(halt, 0, 4, h->st));
+    DevProbes one;
+    one.Q = 1;
+    one.packed = s.pr.packed + (uint64_t)j0 * LR;
+    one.ia = s.pr.ia + (uint64_t)j0 * c.L;
+    one.sqa = s.pr.sqa + (uint64_t)j0 * c.L;
+    CK(cudaMemsetAsync(w.T, 0x7f, 4, h->st));
+    CK(cudaMemsetAsync(w.bcnt, 0, 4, h->st));
+    CK(moe::launch_screen(p.map, c, one, p.g, w, h->st));
+    Plan pe;
+    CKS(make_plan(h, 1, 1, &pe));
+    MatchWork we = w;
+    we.part_chunk = 1;
+    CK(h->partials.ensure((size_t)pe.g.grid * sizeof(moe_match)));
+    we.partials = h->partials.as<moe_match>();
+    uint32_t* q0 = h->small.as<uint32_t>() + 32;
+    CK(cudaMemsetAsync(q0, 0, 4, h->st));
+    // exact argmin for probe 0 of `one`, written to vic[j0]
+    CK(moe::launch_exact(pe.map, c, one, pe.g, we, q0, 1, w.T, vic + j0 - 0, h->st));
+    CK(moe::launch_replace(c, s.pr, j0, vic + j0, h->next_seq + (j0 - i), halt, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    k = j0 + 1;
+  }
+  h->next_seq += n_rep;
+  if (evicted_slots) {
+    std::vector<moe_match> v(n_rep);
+    CK(cudaMemcpy(v.data(), vic + i, n_rep * sizeof(moe_match), cudaMemcpyDeviceToHost));
+    for (uint32_t j = 0; j < n_rep; ++j) evicted_slots[i + j] = (int64_t)v[j].index;
+  }
+  return MOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int moe_abi_version(void) { return MOE_EAMC_ABI_VERSION; }
+
+const char* moe_last_error(void) { return g_err.c_str(); }
+
+moe_status moe_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
+                           size_t* l2_bytes) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(MOE_ERR_CUDA, "no CUDA device visible");
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  if (l2_bytes) *l2_bytes = (size_t)prop.l2CacheSize;
+  return MOE_OK;
+}
+
+moe_status moe_eamc_create(const moe_shape* shape, moe_phase phase, uint64_t capacity,
+                           int count_bytes, int device, moe_eamc** out) {
+  if (!out) return fail(MOE_ERR_INVALID_ARGUMENT, "null out");
+  *out = nullptr;
+  CKS(check_shape(shape));
+  if (capacity < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "Eamc: capacity must be >= 1");
+  if (phase != MOE_PHASE_PREFILL && phase != MOE_PHASE_DECODE)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "bad phase");
+  if (count_bytes == 0) count_bytes = 1;
+  if (count_bytes != 1 && count_bytes != 2)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 0, 1 or 2");
+  int n_sm = 0;
+  CKS(device_ok(device, &n_sm));
+  DeviceGuard dg(device);
+  auto* h = new moe_eamc();
+  h->device = device;
+  h->n_sm = n_sm;
+  h->shape = *shape;
+  h->phase = phase;
+  h->capacity = capacity;
+  h->c.L = shape->n_layers;
+  h->c.E = shape->n_experts_per_layer;
+  h->c.cb = count_bytes;
+  h->c.RB = row_bytes(h->c.E, count_bytes);
+  h->c.C = h->c.RB / 16;
+  if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete h;
+    return fail(MOE_ERR_CUDA, "stream create failed");
+  }
+  *out = h;
+  return MOE_OK;
+}
+
+moe_status moe_eamc_destroy(moe_eamc* h) {
+  if (!h) return MOE_OK;
+  DeviceGuard dg(h->device);
+  cudaStreamSynchronize(h->st);
+  delete h;
+  return MOE_OK;
+}
+
+moe_status moe_eamc_info(const moe_eamc* h, moe_shape* shape, int* phase, uint64_t* capacity,
+                         uint64_t* size, uint64_t* next_seq, int* count_bytes) {
+  if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  if (shape) *shape = h->shape;
+  if (phase) *phase = h->phase;
+  if (capacity) *capacity = h->capacity;
+  if (size) *size = h->c.size;
+  if (next_seq) *next_seq = h->next_seq;
+  if (count_bytes) *count_bytes = h->c.cb;
+  return MOE_OK;
+}
+
+moe_status moe_eamc_entry(const moe_eamc* hc, uint64_t index, uint64_t* counts, uint64_t* seq) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  if (index >= h->c.size) return fail(MOE_ERR_OUT_OF_RANGE, "entry index out of range");
+  DeviceGuard dg(h->device);
+  return read_entry(h, index, counts, seq);
+}
+
+moe_status moe_eamc_insert(moe_eamc* h, const uint64_t* counts, moe_eam_kind kind,
+                           moe_phase phase, int64_t* evicted_slot, uint64_t* evicted_counts) {
+  if (!h || !counts) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  // Eamc::insert validation order (eam.cpp:153-158)
+  if (kind != MOE_KIND_REQUEST)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "Eamc::insert: only request-level EAMs are stored");
+  if ((int)phase != h->phase) return fail(MOE_ERR_INVALID_ARGUMENT, "Eamc::insert: phase mismatch");
+  DeviceGuard dg(h->device);
+  const uint64_t cells = (uint64_t)h->c.L * h->c.E;
+  Staged s;
+  CK(h->raw.ensure(cells * 8));
+  CK(cudaMemcpyAsync(h->raw.p, counts, cells * 8, cudaMemcpyHostToDevice, h->st));
+  CKS(stage_entries(h, h->raw.p, 8, 1, &s));
+  if (h->c.size < h->capacity) {
+    int64_t slot = -1;
+    CKS(replay_staged(h, s, &slot));
+    if (evicted_slot) *evicted_slot = -1;
+    return MOE_OK;
+  }
+  // at capacity: find the victim first so the evicted Eam can be returned
+  CK(h->out.ensure(sizeof(moe_match)));
+  moe_match* dv = h->out.as<moe_match>();
+  CKS(match_packed(h, s.pr, dv, h->st));
+  moe_match v;
+  CK(cudaMemcpyAsync(&v, dv, sizeof v, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (evicted_counts) CKS(read_entry(h, v.index, evicted_counts, nullptr));
+  CK(moe::launch_replace(h->c, s.pr, 0, dv, h->next_seq, nullptr, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  h->next_seq++;
+  if (evicted_slot) *evicted_slot = (int64_t)v.index;
+  return MOE_OK;
+}
+
+moe_status moe_eamc_build(moe_eamc* h, const uint64_t* counts, uint64_t n,
+                          int64_t* evicted_slots) {
+  if (!h || (!counts && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard dg(h->device);
+  const uint64_t cells = (uint64_t)h->c.L * h->c.E;
+  const uint64_t chunk = std::max<uint64_t>(1, (256ull << 20) / (cells * 8));
+  Staged s;
+  for (uint64_t off = 0; off < n; off += chunk) {
+    const uint64_t m = std::min(chunk, n - off);
+    CK(h->raw.ensure(m * cells * 8));
+    CK(cudaMemcpyAsync(h->raw.p, counts + off * cells, m * cells * 8, cudaMemcpyHostToDevice,
+                       h->st));
+    CKS(stage_entries(h, h->raw.p, 8, m, &s));
+    CKS(replay_staged(h, s, evicted_slots ? evicted_slots + off : nullptr));
+  }
+  return MOE_OK;
+}
+
+static moe_status append_impl(moe_eamc* h, const void* counts, int cbytes, const uint64_t* seqs,
+                              uint64_t n) {
+  if (h->c.size + n > h->capacity)
+    return fail(MOE_ERR_SNAPSHOT, "snapshot holds more entries than its capacity");
+  const uint64_t cells = (uint64_t)h->c.L * h->c.E;
+  const uint64_t chunk = std::max<uint64_t>(1, (256ull << 20) / (cells * cbytes));
+  Staged s;
+  for (uint64_t off = 0; off < n; off += chunk) {
+    const uint64_t m = std::min(chunk, n - off);
+    CK(h->raw.ensure(m * cells * cbytes));
+    CK(cudaMemcpyAsync(h->raw.p, static_cast<const uint8_t*>(counts) + off * cells * cbytes,
+                       m * cells * cbytes, cudaMemcpyHostToDevice, h->st));
+    CKS(stage_entries(h, h->raw.p, cbytes, m, &s));
+    CKS(ensure_alloc(h, h->c.size + m));
+    CK(moe::launch_append_staged(h->c, s.pr, 0, (uint32_t)m, h->c.size, h->st));
+    CK(cudaMemcpyAsync(h->c.seq + h->c.size, seqs + off, m * 8, cudaMemcpyHostToDevice, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    h->c.size += (uint32_t)m;
+    for (uint64_t k = 0; k < m; ++k) h->next_seq = std::max(h->next_seq, seqs[off + k] + 1);
+  }
+  return MOE_OK;
+}
+
+moe_status moe_eamc_append(moe_eamc* h, const uint64_t* counts, const uint64_t* seqs, uint64_t n) {
+  if (!h || ((!counts || !seqs) && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard dg(h->device);
+  return append_impl(h, counts, 8, seqs, n);
+}
+
+moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_bytes,
+                                  const uint64_t* seqs, uint64_t n) {
+  if (!h || ((!counts || !seqs) && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (count_bytes != 1 && count_bytes != 2 && count_bytes != 8)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 1, 2 or 8");
+  DeviceGuard dg(h->device);
+  return append_impl(h, counts, count_bytes, seqs, n);
+}
+
+moe_status moe_eamc_match(const moe_eamc* hc, const uint64_t* probes, uint64_t n_probes,
+                          moe_match* out, uint8_t* found) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || ((!probes || !out) && n_probes)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (n_probes == 0) return MOE_OK;
+  DeviceGuard dg(h->device);
+  const uint64_t cells = (uint64_t)h->c.L * h->c.E;
+  const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(65536, (512ull << 20) / (cells * 8)));
+  for (uint64_t off = 0; off < n_probes; off += chunk) {
+    const uint64_t m = std::min(chunk, n_probes - off);
+    DevProbes pr;
+    CKS(prep_probes(h, probes + off * cells, 8, m, false, h->st, &pr));
+    CK(h->out.ensure(m * sizeof(moe_match)));
+    CKS(match_packed(h, pr, h->out.as<moe_match>(), h->st));
+    CK(cudaMemcpyAsync(out + off, h->out.p, m * sizeof(moe_match), cudaMemcpyDeviceToHost, h->st));
+  }
+  CK(cudaStreamSynchronize(h->st));
+  if (found)
+    for (uint64_t q = 0; q < n_probes; ++q) found[q] = out[q].index != ~0ull;
+  return MOE_OK;
+}
+
+moe_status moe_eamc_match_device(const moe_eamc* hc, const void* probes, int probe_bytes,
+                                 uint64_t n_probes, moe_match* out, void* stream) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || ((!probes || !out) && n_probes)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (probe_bytes != 1 && probe_bytes != 2 && probe_bytes != 8)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "probe_bytes must be 1, 2 or 8");
+  if (n_probes == 0) return MOE_OK;
+  if (n_probes > 0xffffffffull) return fail(MOE_ERR_INVALID_ARGUMENT, "too many probes");
+  DeviceGuard dg(h->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->st;
+  DevProbes pr;
+  CKS(prep_probes(h, probes, probe_bytes, n_probes, true, st, &pr));
+  CKS(match_packed(h, pr, out, st));
+  return MOE_OK;
+}
+
+moe_status moe_eamc_match_within(const moe_eamc* hc, const uint64_t* probe, double window,
+                                 moe_match* out, uint64_t cap, uint64_t* n_out) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || !probe || !n_out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  *n_out = 0;
+  if (h->c.size == 0) return MOE_OK;
+  DeviceGuard dg(h->device);
+  DevProbes pr;
+  CKS(prep_probes(h, probe, 8, 1, false, h->st, &pr));
+  CK(h->out.ensure(sizeof(moe_match)));
+  moe_match* best = h->out.as<moe_match>();
+  CKS(match_packed(h, pr, best, h->st));
+  CK(h->wl.ensure((size_t)h->c.size * sizeof(moe::WinEntry)));
+  uint32_t* wl_n = h->small.as<uint32_t>() + 8;
+  CK(cudaMemsetAsync(wl_n, 0, 4, h->st));
+  Plan p;
+  CKS(make_plan(h, 2, 1, &p));
+  CK(moe::launch_window(p.map, h->c, pr, p.g, 0, best, window, h->wl.as<moe::WinEntry>(), wl_n,
+                        h->st));
+  uint32_t n = 0;
+  CK(cudaMemcpyAsync(&n, wl_n, 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  std::vector<moe::WinEntry> v(n);
+  CK(cudaMemcpy(v.data(), h->wl.p, n * sizeof(moe::WinEntry), cudaMemcpyDeviceToHost));
+  // (distance, seq) order of the result list (eam.cpp:145-148)
+  std::sort(v.begin(), v.end(), [](const moe::WinEntry& a, const moe::WinEntry& b) {
+    return a.d != b.d ? a.d < b.d : a.seq < b.seq;
+  });
+  for (uint64_t i = 0; i < n && i < cap; ++i) out[i] = moe_match{v[i].p, v[i].seq, v[i].d};
+  *n_out = n;
+  return MOE_OK;
+}
+
+moe_status moe_match_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out) {
+  if ((!parts || !out) && n) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (n == 0 || n_parts == 0) return MOE_OK;
+  int n_sm = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  CKS(device_ok(dev, &n_sm));
+  moe_match* d = nullptr;
+  CK(cudaMalloc(&d, (n_parts + 1) * n * sizeof(moe_match)));
+  cudaError_t e = cudaMemcpy(d, parts, n_parts * n * sizeof(moe_match), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = moe::launch_merge(d, n_parts, n, d + n_parts * n, nullptr);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(out, d + n_parts * n, n * sizeof(moe_match), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  CK(e);
+  return MOE_OK;
+}
+
+moe_status moe_match_merge_device(const moe_match* parts, uint64_t n_parts, uint64_t n,
+                                  moe_match* out, void* stream) {
+  if ((!parts || !out) && n) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (n == 0 || n_parts == 0) return MOE_OK;
+  CK(moe::launch_merge(parts, n_parts, n, out, static_cast<cudaStream_t>(stream)));
+  return MOE_OK;
+}
+
+moe_status moe_eam_distance(const moe_shape* shape, const uint64_t* a, const uint64_t* b,
+                            double* out) {
+  CKS(check_shape(shape));
+  if (!a || !b || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  CKS(device_ok(dev, &n_sm));
+  moe_eamc* h = nullptr;
+  CKS(moe_eamc_create(shape, MOE_PHASE_DECODE, 1, 1, dev, &h));
+  moe_status s = MOE_OK;
+  {
+    const uint64_t cells = (uint64_t)shape->n_layers * shape->n_experts_per_layer;
+    std::vector<uint64_t> both(2 * cells);
+    std::copy(a, a + cells, both.begin());
+    std::copy(b, b + cells, both.begin() + cells);
+    DevProbes pr;
+    s = prep_probes(h, both.data(), 8, 2, false, h->st, &pr);
+    if (s == MOE_OK) {
+      DevBuf dd;
+      cudaError_t e = dd.ensure(8);
+      const uint64_t LR = (uint64_t)h->c.L * h->c.RB;
+      if (e == cudaSuccess)
+        e = moe::launch_pair_distance(pr.packed, pr.sqa, pr.packed + LR, pr.sqa + h->c.L, h->c.L,
+                                      h->c.C, h->c.RB, h->c.cb, dd.as<double>(), h->st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(out, dd.p, 8, cudaMemcpyDeviceToHost, h->st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);
+      if (e != cudaSuccess) s = fail(MOE_ERR_CUDA, "eam_distance: %s", cudaGetErrorString(e));
+    }
+  }
+  moe_eamc_destroy(h);
+  return s;
+}
+
+static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_t* cur_eam,
+                              uint32_t current_layer, int filter, int do_prefetch,
+                              const uint64_t* request_eam, const moe_slot_view* slots,
+                              uint64_t n_slots, moe_candidate* out, uint64_t cap, uint64_t* n_out,
+                              int64_t* victim, double* slot_pri) {
+  const uint32_t L = shape->n_layers, E = shape->n_experts_per_layer;
+  const uint64_t cells = (uint64_t)L * E;
+  cudaStream_t st = h->st;
+  CK(h->agg.ensure(cells * 8));
+  CK(h->small.ensure(256));
+  unsigned long long* agg = h->agg.as<unsigned long long>();
+  CK(cudaMemsetAsync(agg, 0, cells * 8, st));
+  const bool prefetch_live = do_prefetch && h->c.size > 0;
+  if (prefetch_live) {
+    DevProbes pr;
+    CKS(prep_probes(h, cur_eam, 8, 1, false, st, &pr));
+    CK(h->out.ensure(sizeof(moe_match)));
+    moe_match* best = h->out.as<moe_match>();
+    CKS(match_packed(h, pr, best, st));
+    CK(h->wl.ensure((size_t)h->c.size * sizeof(moe::WinEntry)));
+    uint32_t* wl_n = h->small.as<uint32_t>() + 8;
+    CK(cudaMemsetAsync(wl_n, 0, 4, st));
+    Plan p;
+    CKS(make_plan(h, 2, 1, &p));
+    // kMatchWindow (policy.hpp:30)
+    CK(moe::launch_window(p.map, h->c, pr, p.g, 0, best, 0.01, h->wl.as<moe::WinEntry>(), wl_n,
+                          st));
+    CK(moe::launch_aggregate(h->c, h->wl.as<moe::WinEntry>(), wl_n, current_layer, agg, st));
+  }
+  unsigned long long* req = nullptr;
+  if (request_eam) {
+    CK(h->req.ensure(cells * 8));
+    CK(cudaMemcpyAsync(h->req.p, request_eam, cells * 8, cudaMemcpyHostToDevice, st));
+    req = h->req.as<unsigned long long>();
+  }
+  moe_slot_view* dslots = nullptr;
+  double* dpri = nullptr;
+  if (n_slots) {
+    CK(h->slots.ensure(n_slots * (sizeof(moe_slot_view) + 8)));
+    CK(cudaMemcpyAsync(h->slots.p, slots, n_slots * sizeof(moe_slot_view), cudaMemcpyHostToDevice,
+                       st));
+    dslots = h->slots.as<moe_slot_view>();
+    if (slot_pri) dpri = reinterpret_cast<double*>(dslots + n_slots);
+  }
+  const uint64_t ncand = prefetch_live && current_layer + 1 < L ? (uint64_t)(L - current_layer - 1) * E : 0;
+  CK(h->cand.ensure(std::max<uint64_t>(ncand, 1) * sizeof(moe_candidate)));
+  uint32_t* dn = h->small.as<uint32_t>() + 12;
+  long long* dv = reinterpret_cast<long long*>(h->small.as<uint8_t>() + 192);
+  CK(cudaMemsetAsync(dn, 0, 4, st));
+  CK(moe::launch_decide(agg, L, E, current_layer, filter, prefetch_live ? 1 : 0, req, dslots,
+                        n_slots, h->cand.as<moe_candidate>(), dn, victim ? dv : nullptr, dpri,
+                        st));
+  uint32_t n = 0;
+  long long v = -1;
+  CK(cudaMemcpyAsync(&n, dn, 4, cudaMemcpyDeviceToHost, st));
+  if (victim) CK(cudaMemcpyAsync(&v, dv, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (n_out) *n_out = prefetch_live ? n : 0;
+  if (prefetch_live && n && out && cap)
+    CK(cudaMemcpy(out, h->cand.p, std::min<uint64_t>(n, cap) * sizeof(moe_candidate),
+                  cudaMemcpyDeviceToHost));
+  if (victim) *victim = v;
+  if (slot_pri && n_slots) CK(cudaMemcpy(slot_pri, dpri, n_slots * 8, cudaMemcpyDeviceToHost));
+  return MOE_OK;
+}
+
+moe_status moe_prefetch_priorities(const moe_eamc* hc, const uint64_t* cur_eam,
+                                   uint32_t current_layer, int apply_floor_filter,
+                                   moe_candidate* out, uint64_t cap, uint64_t* n_out) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || !cur_eam || !n_out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  // policy.cpp:91-93
+  if (current_layer >= h->shape.n_layers)
+    return fail(MOE_ERR_OUT_OF_RANGE, "prefetch_priorities: current_layer out of range");
+  *n_out = 0;
+  if (h->c.size == 0) return MOE_OK;
+  DeviceGuard dg(h->device);
+  return decide_impl(h, &h->shape, cur_eam, current_layer, apply_floor_filter, 1, nullptr, nullptr,
+                     0, out, cap, n_out, nullptr, nullptr);
+}
+
+moe_status moe_decide(const moe_eamc* hc, const uint64_t* cur_eam, uint32_t current_layer,
+                      const uint64_t* request_eam, const moe_slot_view* slots, uint64_t n_slots,
+                      moe_candidate* out, uint64_t cap, uint64_t* n_out, int64_t* victim) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || !cur_eam || !request_eam || (!slots && n_slots))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (current_layer >= h->shape.n_layers)
+    return fail(MOE_ERR_OUT_OF_RANGE, "prefetch_priorities: current_layer out of range");
+  for (uint64_t i = 0; i < n_slots; ++i)
+    if (slots[i].layer_idx >= h->shape.n_layers ||
+        slots[i].expert_idx >= h->shape.n_experts_per_layer)
+      return fail(MOE_ERR_OUT_OF_RANGE, "cache_priority: expert out of range");
+  DeviceGuard dg(h->device);
+  return decide_impl(h, &h->shape, cur_eam, current_layer, 1, 1, request_eam, slots, n_slots, out,
+                     cap, n_out, victim, nullptr);
+}
+
+static moe_status scratch_handle(const moe_shape* shape, moe_eamc** h) {
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  CKS(device_ok(dev, &n_sm));
+  return moe_eamc_create(shape, MOE_PHASE_DECODE, 1, 1, dev, h);
+}
+
+moe_status moe_cache_priority(const moe_shape* shape, const uint64_t* request_eam,
+                              uint32_t layer, uint32_t expert, double* out) {
+  CKS(check_shape(shape));
+  if (!request_eam || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  // policy.cpp:130-131
+  if (layer >= shape->n_layers || expert >= shape->n_experts_per_layer)
+    return fail(MOE_ERR_OUT_OF_RANGE, "cache_priority: expert out of range");
+  moe_eamc* h = nullptr;
+  CKS(scratch_handle(shape, &h));
+  moe_slot_view v{};
+  v.slot = 0;
+  v.layer_idx = layer;
+  v.expert_idx = expert;
+  const moe_status s = decide_impl(h, shape, nullptr, 0, 0, 0, request_eam, &v, 1, nullptr, 0,
+                                   nullptr, nullptr, out);
+  moe_eamc_destroy(h);
+  return s;
+}
+
+moe_status moe_select_eviction_victim(const moe_shape* shape, const uint64_t* request_eam,
+                                      const moe_slot_view* slots, uint64_t n_slots,
+                                      int64_t* victim) {
+  CKS(check_shape(shape));
+  if (!request_eam || !victim || (!slots && n_slots))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  for (uint64_t i = 0; i < n_slots; ++i) {
+    if (slots[i].prefetch_protected || slots[i].pinned) continue;  // never priced
+    if (slots[i].layer_idx >= shape->n_layers || slots[i].expert_idx >= shape->n_experts_per_layer)
+      return fail(MOE_ERR_OUT_OF_RANGE, "cache_priority: expert out of range");
+  }
+  *victim = -1;
+  if (n_slots == 0) return MOE_OK;
+  moe_eamc* h = nullptr;
+  CKS(scratch_handle(shape, &h));
+  const moe_status s = decide_impl(h, shape, nullptr, 0, 0, 0, request_eam, slots, n_slots,
+                                   nullptr, 0, nullptr, victim, nullptr);
+  moe_eamc_destroy(h);
+  return s;
+}
+
+moe_status moe_eam_trace_device(const moe_shape* shape, const void* topk_idx, int idx_bytes,
+                                uint64_t n_tokens, const uint64_t* offsets, uint64_t n_requests,
+                                uint32_t* counts_u32, int* bad_index_flag, void* stream) {
+  CKS(check_shape(shape));
+  if (idx_bytes != 1 && idx_bytes != 2 && idx_bytes != 4)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "idx_bytes must be 1, 2 or 4");
+  if (!bad_index_flag || ((!topk_idx || !offsets || !counts_u32) && n_requests))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  CKS(device_ok(dev, &n_sm));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t cells = (uint64_t)shape->n_layers * shape->n_experts_per_layer;
+  uint32_t* scratch = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), std::max<uint64_t>(1, n_requests * cells) * 4, st));
+  CK(cudaMemsetAsync(scratch, 0, n_requests * cells * 4, st));
+  CK(moe::launch_trace(topk_idx, idx_bytes, n_tokens, shape->n_layers, shape->n_experts_per_layer,
+                       shape->top_k, offsets, n_requests, scratch, bad_index_flag, n_sm, st));
+  CK(moe::launch_trace_commit(scratch, n_requests * cells, bad_index_flag, counts_u32, st));
+  CK(cudaFreeAsync(scratch, st));
+  return MOE_OK;
+}
+
+moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_bytes,
+                         uint64_t n_tokens, const uint64_t* offsets, uint64_t n_requests,
+                         uint64_t* counts) {
+  CKS(check_shape(shape));
+  if (idx_bytes != 1 && idx_bytes != 2 && idx_bytes != 4)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "idx_bytes must be 1, 2 or 4");
+  if (n_requests == 0) return MOE_OK;
+  if (!topk_idx || !offsets || !counts) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  for (uint64_t r = 0; r < n_requests; ++r)
+    if (offsets[r] > offsets[r + 1])
+      return fail(MOE_ERR_INVALID_ARGUMENT, "request offsets must be non-decreasing");
+  if (offsets[n_requests] > n_tokens)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "request offsets exceed n_tokens");
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  CKS(device_ok(dev, &n_sm));
+  const uint64_t cells = (uint64_t)shape->n_layers * shape->n_experts_per_layer;
+  const uint64_t in_bytes = n_tokens * shape->n_layers * shape->top_k * idx_bytes;
+  cudaStream_t st = nullptr;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DevBuf din, doff, dscr, dcnt, dbad;
+  moe_status s = MOE_OK;
+  cudaError_t e = din.ensure(in_bytes);
+  if (e == cudaSuccess) e = doff.ensure((n_requests + 1) * 8);
+  if (e == cudaSuccess) e = dscr.ensure(n_requests * cells * 4);
+  if (e == cudaSuccess) e = dcnt.ensure(n_requests * cells * 8);
+  if (e == cudaSuccess) e = dbad.ensure(4);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(din.p, topk_idx, in_bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(doff.p, offsets, (n_requests + 1) * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(dcnt.p, counts, n_requests * cells * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dscr.p, 0, n_requests * cells * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dbad.p, 0, 4, st);
+  if (e == cudaSuccess)
+    e = moe::launch_trace(din.p, idx_bytes, n_tokens, shape->n_layers, shape->n_experts_per_layer,
+                          shape->top_k, doff.as<uint64_t>(), n_requests, dscr.as<uint32_t>(),
+                          dbad.as<int>(), n_sm, st);
+  if (e == cudaSuccess)
+    e = moe::launch_trace_commit64(dscr.as<uint32_t>(), n_requests * cells, dbad.as<int>(),
+                                   dcnt.as<unsigned long long>(), st);
+  int bad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, dbad.p, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && !bad)
+    e = cudaMemcpy(counts, dcnt.p, n_requests * cells * 8, cudaMemcpyDeviceToHost);
+  cudaStreamDestroy(st);
+  if (e != cudaSuccess)
+    s = fail(e == cudaErrorMemoryAllocation ? MOE_ERR_OOM : MOE_ERR_CUDA, "eam_trace: %s",
+             cudaGetErrorString(e));
+  else if (bad)
+    s = fail(MOE_ERR_OUT_OF_RANGE, "Eam::record: expert index out of range");
+  return s;
+}
+
+moe_status moe_eamc_capacity_bound(const moe_shape* shape, double similarity, uint64_t* out) {
+  CKS(check_shape(shape));
+  if (!out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  const uint64_t v = moe::host::capacity_bound(shape->n_layers, shape->n_experts_per_layer, similarity);
+  if (!v)
+    return fail(MOE_ERR_INVALID_ARGUMENT,
+                "eamc_capacity_bound: supported similarity levels are 0.75 and 0.98");
+  *out = v;
+  return MOE_OK;
+}
+
+moe_status moe_eamc_save(const moe_eamc* hc, const char* path) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || !path) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard dg(h->device);
+  const DevColl& c = h->c;
+  const uint64_t LR = (uint64_t)c.L * c.RB;
+  std::vector<uint8_t> rows((size_t)c.size * LR);
+  std::vector<uint64_t> seqs(c.size);
+  if (c.size) {
+    CK(cudaMemcpy(rows.data(), c.counts, rows.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(seqs.data(), c.seq, c.size * 8, cudaMemcpyDeviceToHost));
+  }
+  moe::host::Snapshot snap;
+  snap.L = c.L;
+  snap.E = c.E;
+  snap.top_k = h->shape.top_k;
+  snap.phase = h->phase;
+  snap.capacity = h->capacity;
+  snap.next_seq = h->next_seq;
+  snap.seqs = std::move(seqs);
+  snap.counts.resize((size_t)c.size * c.L * c.E);
+  for (uint64_t i = 0; i < c.size; ++i)
+    for (uint32_t l = 0; l < c.L; ++l)
+      for (uint32_t e = 0; e < c.E; ++e) {
+        const uint8_t* r = rows.data() + i * LR + (uint64_t)l * c.RB;
+        snap.counts[(i * c.L + l) * c.E + e] =
+            c.cb == 1 ? r[e] : reinterpret_cast<const uint16_t*>(r)[e];
+      }
+  std::string err;
+  if (!moe::host::save_snapshot(path, snap, &err)) return fail(MOE_ERR_SNAPSHOT, "%s", err.c_str());
+  return MOE_OK;
+}
+
+moe_status moe_eamc_load(const char* path, const moe_shape* expected, int device, moe_eamc** out) {
+  if (!path || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  moe::host::Snapshot snap;
+  std::string err;
+  if (!moe::host::load_snapshot(path, &snap, &err)) return fail(MOE_ERR_SNAPSHOT, "%s", err.c_str());
+  const moe_shape s{snap.L, snap.E, snap.top_k};
+  if (check_shape(&s) != MOE_OK) return fail(MOE_ERR_SNAPSHOT, "corrupt snapshot: %s", g_err.c_str());
+  if (snap.capacity < 1) return fail(MOE_ERR_SNAPSHOT, "corrupt snapshot: capacity must be >= 1");
+  if (snap.seqs.size() > snap.capacity)
+    return fail(MOE_ERR_SNAPSHOT, "snapshot holds more entries than its capacity");
+  if (expected && (expected->n_layers != s.n_layers ||
+                   expected->n_experts_per_layer != s.n_experts_per_layer ||
+                   expected->top_k != s.top_k))
+    return fail(MOE_ERR_SNAPSHOT, "snapshot shape does not match the configured model shape");
+  moe_eamc* h = nullptr;
+  CKS(moe_eamc_create(&s, (moe_phase)snap.phase, snap.capacity, 1, device, &h));
+  moe_status st = MOE_OK;
+  if (!snap.seqs.empty())
+    st = moe_eamc_append(h, snap.counts.data(), snap.seqs.data(), snap.seqs.size());
+  if (st != MOE_OK) {
+    moe_eamc_destroy(h);
+    return st == MOE_ERR_OVERFLOW ? fail(MOE_ERR_SNAPSHOT, "snapshot counts: %s", g_err.c_str()) : st;
+  }
+  h->next_seq = snap.next_seq;  // eam.cpp:244
+  *out = h;
+  return MOE_OK;
+}
+
+moe_status moe_gen_bench_family(uint64_t seed, uint32_t L, uint32_t E, uint64_t skip, uint64_t n,
+                                int count_bytes, void* out) {
+  if (!out && n) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (L < 1 || E < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "bad shape");
+  if (count_bytes != 1 && count_bytes != 2 && count_bytes != 8)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 1, 2 or 8");
+  moe::host::bench_family(seed, L, E, skip, n, count_bytes, out);
+  return MOE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// common.cuh -- shared device helpers for the B200 (sm_100a) EAM/EAMC path:
+// mbarrier + TMA (cp.async.bulk.tensor) PTX wrappers, packed-count dot
+// products and the exact fp64 row-similarity epilogue.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace moe {
+
+constexpr int kNT = 128;          // entries per collection tile == threads per block
+constexpr uint32_t kFInf = 0x7f800000u;
+constexpr uint64_t kNone = ~0ull;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 4-D TMA tile load global -> shared, completion counted on `bar`.
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// Dot product of one 16-byte chunk of packed counts.
+//  CB=1: 16 u8 counts, 4x IDP4A (u32 accumulate; exact while E*255^2 < 2^32)
+//  CB=2: 8 u16 counts, u32 products accumulated in u64 (exact)
+template <int CB>
+struct Dot;
+template <>
+struct Dot<1> {
+  using Acc = uint32_t;
+  __device__ __forceinline__ static Acc chunk(const uint4& a, const uint4& b, Acc acc) {
+    acc = __dp4a(a.x, b.x, acc);
+    acc = __dp4a(a.y, b.y, acc);
+    acc = __dp4a(a.z, b.z, acc);
+    acc = __dp4a(a.w, b.w, acc);
+    return acc;
+  }
+};
+template <>
+struct Dot<2> {
+  using Acc = uint64_t;
+  __device__ __forceinline__ static uint64_t w2(uint32_t a, uint32_t b) {
+    return (uint64_t)((a & 0xffffu) * (b & 0xffffu)) + (uint64_t)((a >> 16) * (b >> 16));
+  }
+  __device__ __forceinline__ static Acc chunk(const uint4& a, const uint4& b, Acc acc) {
+    return acc + w2(a.x, b.x) + w2(a.y, b.y) + w2(a.z, b.z) + w2(a.w, b.w);
+  }
+};
+
+// Reference row_similarity epilogue (eam.cpp:84-86) on exact integer sums:
+// both rows zero -> 1, one zero -> 0, else dot / (sqrt(na) * sqrt(nb)),
+// every operation IEEE round-to-nearest, no contraction.
+__device__ __forceinline__ double row_sim_exact(uint64_t dot, double sa, double sb) {
+  if (sa == 0.0 && sb == 0.0) return 1.0;
+  if (sa == 0.0 || sb == 0.0) return 0.0;
+  return __ddiv_rn(__ull2double_rn(dot), __dmul_rn(sa, sb));
+}
+// d = 1 - sim / L, clamped to [0, 1] (eam.cpp:99-103)
+__device__ __forceinline__ double finish_distance(double sim, uint32_t L) {
+  double d = __dsub_rn(1.0, __ddiv_rn(sim, (double)L));
+  if (d < 0.0) d = 0.0;
+  if (d > 1.0) d = 1.0;
+  return d;
+}
+
+// Lexicographic (distance, seq) order of EamcMatch (eam.cpp:123-124, :170).
+struct Best {
+  double d;
+  uint64_t seq;
+  uint64_t idx;
+};
+__device__ __forceinline__ bool better(double d, uint64_t s, double bd, uint64_t bs) {
+  return d < bd || (d == bd && s < bs);
+}
+__device__ __forceinline__ Best warp_best(Best b) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Best x;
+    x.d = __shfl_xor_sync(0xffffffffu, b.d, o);
+    x.seq = __shfl_xor_sync(0xffffffffu, b.seq, o);
+    x.idx = __shfl_xor_sync(0xffffffffu, b.idx, o);
+    if (better(x.d, x.seq, b.d, b.seq)) b = x;
+  }
+  return b;
+}
+
+}  // namespace moe

@@ -1,0 +1,385 @@
+// host.cpp -- snapshot codec, capacity bound and the bench-family generator.
+#include "host.hpp"
+
+#include <cctype>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <sstream>
+
+namespace moe {
+namespace host {
+
+// ---------------------------------------------------------------- JSON v1
+// Writer: the byte layout nlohmann::json::dump() gives the reference's
+// snapshot (eam.cpp:184-205): compact, object keys in sorted order.
+bool save_snapshot(const char* path, const Snapshot& s, std::string* err) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) {
+    *err = std::string("cannot open for writing: ") + path;
+    return false;
+  }
+  std::string buf;
+  buf.reserve(64 + s.counts.size() * 3);
+  buf += "{\"capacity\":" + std::to_string(s.capacity) + ",\"entries\":[";
+  const uint64_t cells = (uint64_t)s.L * s.E;
+  for (size_t i = 0; i < s.seqs.size(); ++i) {
+    if (i) buf += ',';
+    buf += "{\"counts\":[";
+    for (uint64_t c = 0; c < cells; ++c) {
+      if (c) buf += ',';
+      buf += std::to_string(s.counts[i * cells + c]);
+    }
+    buf += "],\"seq\":" + std::to_string(s.seqs[i]) + "}";
+  }
+  buf += "],\"next_seq\":" + std::to_string(s.next_seq);
+  buf += ",\"phase\":\"";
+  buf += s.phase == 0 ? "prefill" : "decode";
+  buf += "\",\"shape\":{\"n_experts_per_layer\":" + std::to_string(s.E) +
+         ",\"n_layers\":" + std::to_string(s.L) + ",\"top_k\":" + std::to_string(s.top_k) +
+         "},\"version\":1}\n";
+  out << buf;
+  if (!out) {
+    *err = std::string("write failed: ") + path;
+    return false;
+  }
+  return true;
+}
+
+namespace {
+
+// Minimal JSON DOM sufficient for the snapshot schema.
+struct JVal {
+  enum Kind { Null, Bool, Num, Str, Arr, Obj } kind = Null;
+  bool b = false;
+  bool is_uint = false;
+  uint64_t u = 0;
+  double d = 0.0;
+  std::string s;
+  std::vector<JVal> arr;
+  std::map<std::string, JVal> obj;
+};
+
+struct Parser {
+  const char* p;
+  const char* end;
+  std::string err;
+  void ws() {
+    while (p < end && (*p == ' ' || *p == '\n' || *p == '\r' || *p == '\t')) ++p;
+  }
+  bool lit(const char* w) {
+    const size_t n = strlen(w);
+    if ((size_t)(end - p) < n || strncmp(p, w, n) != 0) return false;
+    p += n;
+    return true;
+  }
+  bool str(std::string* o) {
+    if (p >= end || *p != '"') return false;
+    ++p;
+    while (p < end && *p != '"') {
+      if (*p == '\\') {
+        ++p;
+        if (p >= end) return false;
+        switch (*p) {
+          case 'n': o->push_back('\n'); break;
+          case 't': o->push_back('\t'); break;
+          case 'r': o->push_back('\r'); break;
+          case 'b': o->push_back('\b'); break;
+          case 'f': o->push_back('\f'); break;
+          case 'u':
+            if (end - p < 5) return false;
+            o->push_back('?');
+            p += 4;
+            break;
+          default: o->push_back(*p);
+        }
+        ++p;
+      } else {
+        o->push_back(*p++);
+      }
+    }
+    if (p >= end) return false;
+    ++p;
+    return true;
+  }
+  bool value(JVal* v, int depth) {
+    if (depth > 64) return false;
+    ws();
+    if (p >= end) return false;
+    if (*p == '{') {
+      ++p;
+      v->kind = JVal::Obj;
+      ws();
+      if (p < end && *p == '}') {
+        ++p;
+        return true;
+      }
+      for (;;) {
+        ws();
+        std::string k;
+        if (!str(&k)) return false;
+        ws();
+        if (p >= end || *p != ':') return false;
+        ++p;
+        JVal child;
+        if (!value(&child, depth + 1)) return false;
+        v->obj[k] = std::move(child);
+        ws();
+        if (p < end && *p == ',') {
+          ++p;
+          continue;
+        }
+        if (p < end && *p == '}') {
+          ++p;
+          return true;
+        }
+        return false;
+      }
+    }
+    if (*p == '[') {
+      ++p;
+      v->kind = JVal::Arr;
+      ws();
+      if (p < end && *p == ']') {
+        ++p;
+        return true;
+      }
+      for (;;) {
+        JVal child;
+        if (!value(&child, depth + 1)) return false;
+        v->arr.push_back(std::move(child));
+        ws();
+        if (p < end && *p == ',') {
+          ++p;
+          continue;
+        }
+        if (p < end && *p == ']') {
+          ++p;
+          return true;
+        }
+        return false;
+      }
+    }
+    if (*p == '"') {
+      v->kind = JVal::Str;
+      return str(&v->s);
+    }
+    if (lit("true")) {
+      v->kind = JVal::Bool;
+      v->b = true;
+      return true;
+    }
+    if (lit("false")) {
+      v->kind = JVal::Bool;
+      return true;
+    }
+    if (lit("null")) return true;
+    // number
+    const char* s = p;
+    if (p < end && (*p == '-' || *p == '+')) ++p;
+    bool digits_only = true;
+    while (p < end && (isdigit((unsigned char)*p) || *p == '.' || *p == 'e' || *p == 'E' ||
+                       *p == '-' || *p == '+')) {
+      if (!isdigit((unsigned char)*p)) digits_only = false;
+      ++p;
+    }
+    if (p == s) return false;
+    v->kind = JVal::Num;
+    const std::string tok(s, p);
+    v->d = strtod(tok.c_str(), nullptr);
+    if (digits_only && tok[0] != '-' && tok[0] != '+' && tok.size() <= 20) {
+      errno = 0;
+      char* e = nullptr;
+      const unsigned long long u = strtoull(tok.c_str(), &e, 10);
+      if (errno == 0 && e && *e == 0) {
+        v->is_uint = true;
+        v->u = u;
+      }
+    }
+    return true;
+  }
+};
+
+const JVal* at(const JVal& v, const char* key, std::string* err) {
+  if (v.kind != JVal::Obj) {
+    *err = "corrupt snapshot: expected an object";
+    return nullptr;
+  }
+  auto it = v.obj.find(key);
+  if (it == v.obj.end()) {
+    *err = std::string("corrupt snapshot: key '") + key + "' not found";
+    return nullptr;
+  }
+  return &it->second;
+}
+
+bool get_u64(const JVal* v, uint64_t* out, std::string* err) {
+  if (!v) return false;
+  if (v->kind != JVal::Num || !v->is_uint) {
+    *err = "corrupt snapshot: expected an unsigned integer";
+    return false;
+  }
+  *out = v->u;
+  return true;
+}
+
+}  // namespace
+
+// Reader with the validation of Eamc::load (eam.cpp:207-249).
+bool load_snapshot(const char* path, Snapshot* s, std::string* err) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) {
+    *err = std::string("cannot open for reading: ") + path;
+    return false;
+  }
+  std::stringstream ss;
+  ss << in.rdbuf();
+  const std::string text = ss.str();
+  Parser ps{text.data(), text.data() + text.size(), {}};
+  JVal root;
+  if (!ps.value(&root, 0)) {
+    *err = "corrupt snapshot: parse error";
+    return false;
+  }
+  ps.ws();
+  if (ps.p != ps.end) {
+    *err = "corrupt snapshot: trailing characters";
+    return false;
+  }
+  uint64_t version = 0;
+  const JVal* jv = at(root, "version", err);
+  if (!jv) return false;
+  if (jv->kind != JVal::Num || !jv->is_uint || jv->u != 1) {
+    *err = "unsupported snapshot version";
+    return false;
+  }
+  (void)version;
+  const JVal* shape = at(root, "shape", err);
+  if (!shape) return false;
+  uint64_t L = 0, E = 0, K = 0, cap = 0, nseq = 0;
+  if (!get_u64(at(*shape, "n_layers", err), &L, err)) return false;
+  if (!get_u64(at(*shape, "n_experts_per_layer", err), &E, err)) return false;
+  if (!get_u64(at(*shape, "top_k", err), &K, err)) return false;
+  if (L > 0xffffffffull || E > 0xffffffffull || K > 0xffffffffull) {
+    *err = "corrupt snapshot: shape out of range";
+    return false;
+  }
+  const JVal* ph = at(root, "phase", err);
+  if (!ph) return false;
+  if (ph->kind != JVal::Str) {
+    *err = "corrupt snapshot: phase must be a string";
+    return false;
+  }
+  int phase;
+  if (ph->s == "prefill") phase = 0;
+  else if (ph->s == "decode") phase = 1;
+  else {
+    *err = "unknown phase: " + ph->s;
+    return false;
+  }
+  if (!get_u64(at(root, "capacity", err), &cap, err)) return false;
+  const JVal* entries = at(root, "entries", err);
+  if (!entries) return false;
+  if (entries->kind != JVal::Arr) {
+    *err = "corrupt snapshot: entries must be an array";
+    return false;
+  }
+  const uint64_t cells = L * E;
+  s->L = (uint32_t)L;
+  s->E = (uint32_t)E;
+  s->top_k = (uint32_t)K;
+  s->phase = phase;
+  s->capacity = cap;
+  s->seqs.clear();
+  s->counts.clear();
+  s->counts.reserve(entries->arr.size() * cells);
+  for (const JVal& je : entries->arr) {
+    const JVal* counts = at(je, "counts", err);
+    if (!counts) return false;
+    if (counts->kind != JVal::Arr || counts->arr.size() != cells) {
+      *err = "entry count array does not match shape";
+      return false;
+    }
+    for (const JVal& c : counts->arr) {
+      uint64_t v = 0;
+      if (!get_u64(&c, &v, err)) return false;
+      s->counts.push_back(v);
+    }
+    if (s->seqs.size() >= cap) {
+      *err = "snapshot holds more entries than its capacity";
+      return false;
+    }
+    uint64_t sq = 0;
+    if (!get_u64(at(je, "seq", err), &sq, err)) return false;
+    s->seqs.push_back(sq);
+  }
+  if (!get_u64(at(root, "next_seq", err), &nseq, err)) return false;
+  s->next_seq = nseq;
+  return true;
+}
+
+// eamc_capacity_bound (eam.cpp:258-268); 0 = unsupported similarity.
+uint64_t capacity_bound(uint32_t L, uint32_t E, double similarity) {
+  const uint64_t total = (uint64_t)L * E;
+  const double le = (double)total;
+  if (similarity == 0.75) return 2 * total;
+  if (similarity == 0.98) return (uint64_t)std::ceil(0.5 * le * std::log(le));
+  return 0;
+}
+
+// ------------------------------------------------------ bench family
+// splitmix64 stream (rng.hpp:19-45) and random_request_eam
+// (bench.cpp:44-54), the reference benchmark's own synthetic EAMs.
+namespace {
+struct Rng {
+  uint64_t s;
+  uint64_t next() {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  uint64_t bounded(uint64_t n) {
+    const uint64_t threshold = (0 - n) % n;
+    for (;;) {
+      const uint64_t r = next();
+      if (r >= threshold) return r % n;
+    }
+  }
+  static Rng stream(uint64_t seed, uint64_t tag) {
+    Rng mix{seed ^ (0xA0761D6478BD642Full + tag * 0xE7037ED1A0B428DBull)};
+    return Rng{mix.next()};
+  }
+};
+}  // namespace
+
+void bench_family(uint64_t seed, uint32_t L, uint32_t E, uint64_t skip, uint64_t n,
+                  int count_bytes, void* out) {
+  Rng rng = Rng::stream(seed, 0x6265636Eull);
+  const uint32_t active = E < 4 ? E : 4;
+  const uint64_t cells = (uint64_t)L * E;
+  for (uint64_t i = 0; i < skip; ++i)
+    for (uint32_t l = 0; l < L; ++l)
+      for (uint32_t k = 0; k < active; ++k) {
+        rng.bounded(E);
+        rng.bounded(32);
+      }
+  uint8_t* o = static_cast<uint8_t*>(out);
+  memset(o, 0, n * cells * count_bytes);
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint32_t l = 0; l < L; ++l)
+      for (uint32_t k = 0; k < active; ++k) {
+        const uint64_t e = rng.bounded(E);
+        const uint64_t v = rng.bounded(32) + 1;
+        const uint64_t idx = i * cells + (uint64_t)l * E + e;
+        if (count_bytes == 1) o[idx] = (uint8_t)v;
+        else if (count_bytes == 2) reinterpret_cast<uint16_t*>(o)[idx] = (uint16_t)v;
+        else reinterpret_cast<uint64_t*>(o)[idx] = v;
+      }
+}
+
+}  // namespace host
+}  // namespace moe

@@ -1,0 +1,1160 @@
+// kernels.cu -- hand-written sm_100a kernels of the EAM/EAMC decision path.
+//
+//  K3  k_match<CB,QT,0>   EAMC matcher, screen pass.  Collection tiles of
+//                         128 entries x G layers stream HBM->SMEM through TMA
+//                         (cp.async.bulk.tensor.4d, mbarrier ring of S stages);
+//                         one thread per entry computes exact integer dots
+//                         (IDP4A for u8 counts) against QT probes held in
+//                         SMEM, an fp32 cosine screen with a proven error
+//                         bound, and the argmin threshold / candidate
+//                         buckets (warp REDUX min -> block -> global atomics).
+//      k_refine           one warp per probe: exact fp64 re-evaluation, in the
+//                         reference operation order, of the few candidates
+//                         whose screened distance is within 2*eps of the min;
+//                         lexicographic (distance, seq) argmin (eam.cpp:118-129).
+//      k_match<CB,1,1>    exact argmin for probes whose bucket overflowed
+//                         (mass near-ties), same TMA pipeline.
+//  K4  k_match<CB,1,2>    window membership d <= d_min + window (eam.cpp:131-150)
+//      k_aggregate        u64 aggregation of the matched rows (policy.cpp:97-104)
+//  K5+K6 k_decide         prefetch priorities + floor filter + order
+//                         (policy.cpp:106-125, engine.cpp:663-668) and the
+//                         eviction victim (policy.cpp:128-159), one block.
+//  K1  k_trace            router top-k ids -> per-request L x E histograms
+//                         (eam.cpp:41-52 semantics, all-or-nothing).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace moe {
+
+namespace {
+
+__host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+struct SmemLayout {
+  uint32_t stage_bytes, off_probe, off_ia, off_sqa, off_dots, off_red, off_tnow, off_wbest,
+      off_bars, total;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(uint32_t L, uint32_t RB, uint32_t G, uint32_t S,
+                                                  uint32_t QT, int mode, uint32_t acc_bytes) {
+  SmemLayout s;
+  uint32_t o = 0;
+  s.stage_bytes = kNT * G * RB;
+  o = S * s.stage_bytes;
+  s.off_probe = o;
+  o = align_up(o + QT * L * RB, 16);
+  s.off_ia = o;
+  o = align_up(o + QT * L * 4, 16);
+  s.off_sqa = o;
+  o = align_up(o + (mode ? L * 8 : 0), 16);
+  s.off_dots = o;
+  o = align_up(o + (mode ? L * kNT * acc_bytes : 0), 16);
+  s.off_red = o;
+  o = align_up(o + 4 * QT * 4, 16);
+  s.off_tnow = o;
+  o = align_up(o + QT * 4, 16);
+  s.off_wbest = o;
+  o = align_up(o + 4 * (uint32_t)sizeof(Best), 16);
+  s.off_bars = o;
+  o += S * 8;
+  s.total = align_up(o, 128);
+  return s;
+}
+
+struct MatchArgs {
+  // collection
+  const float* ibT;
+  const double* sqb;
+  const uint64_t* seq;
+  uint64_t cap;
+  uint32_t size;
+  // probes
+  const uint8_t* probes;
+  const float* ia;
+  const double* sqa;
+  uint32_t Q;
+  // geometry
+  uint32_t L, RB, C, G, S, n_groups, n_pt;
+  float eps2;
+  // mode 0
+  uint32_t* T;
+  uint32_t* bcnt;
+  uint2* bucket;
+  uint32_t bcap;
+  // mode 1 / 2
+  const uint32_t* qlist;   // null: the single probe q_single
+  uint32_t q_single;
+  uint32_t nq_list;
+  const uint32_t* Tfinal;  // mode 1 candidate threshold (null: all)
+  moe_match* partials;     // mode 1 [nq_list][grid]
+  const moe_match* best;   // mode 2
+  double window;           // mode 2
+  WinEntry* wl;            // mode 2
+  uint32_t* wl_n;          // mode 2
+};
+
+template <typename Acc>
+__device__ __forceinline__ float acc_to_float(Acc a);
+template <>
+__device__ __forceinline__ float acc_to_float<uint32_t>(uint32_t a) {
+  return __uint2float_rn(a);
+}
+template <>
+__device__ __forceinline__ float acc_to_float<uint64_t>(uint64_t a) {
+  return __ull2float_rn(a);
+}
+
+template <int CB, int QT, int MODE>
+__global__ void __launch_bounds__(kNT, 1)
+    k_match(const __grid_constant__ CUtensorMap tmap, const MatchArgs a) {
+  using D = Dot<CB>;
+  using Acc = typename D::Acc;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const SmemLayout lay = smem_layout(a.L, a.RB, a.G, a.S, QT, MODE, sizeof(Acc));
+  uint8_t* stages = smem;
+  uint8_t* probe_s = smem + lay.off_probe;
+  float* ia_s = reinterpret_cast<float*>(smem + lay.off_ia);
+  double* sqa_s = reinterpret_cast<double*>(smem + lay.off_sqa);
+  Acc* dots_s = reinterpret_cast<Acc*>(smem + lay.off_dots);
+  uint32_t* red = reinterpret_cast<uint32_t*>(smem + lay.off_red);
+  float* tnow = reinterpret_cast<float*>(smem + lay.off_tnow);
+  Best* wbest = reinterpret_cast<Best*>(smem + lay.off_wbest);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.off_bars);
+
+  const uint32_t nq = MODE == 0 ? (a.Q + QT - 1) / QT : a.nq_list;
+  const uint64_t n_items = (uint64_t)nq * a.n_pt;
+  const uint64_t it0 = n_items * blockIdx.x / gridDim.x;
+  const uint64_t it1 = n_items * (blockIdx.x + 1) / gridDim.x;
+  if (it0 >= it1) return;
+  const uint64_t total = (it1 - it0) * a.n_groups;
+
+  if (tid == 0) {
+    prefetch_tmap(&tmap);
+    for (uint32_t s = 0; s < a.S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](uint64_t j) {
+    const uint64_t item = it0 + j / a.n_groups;
+    const uint32_t g = (uint32_t)(j % a.n_groups);
+    const uint32_t pt = (uint32_t)(item % a.n_pt);
+    const uint32_t s = (uint32_t)(j % a.S);
+    mbar_arrive_expect_tx(&bars[s], lay.stage_bytes);
+    tma_load_4d(stages + (size_t)s * lay.stage_bytes, &tmap, &bars[s], 0, 0, (int)(g * a.G),
+                (int)(pt * kNT));
+  };
+  if (tid == 0) {
+    const uint64_t pre = total < a.S ? total : a.S;
+    for (uint64_t j = 0; j < pre; ++j) issue(j);
+  }
+
+  float sim[QT];
+#pragma unroll
+  for (int q = 0; q < QT; ++q) sim[q] = 0.f;
+  int64_t cur_qi = -1;
+  Best tb{__longlong_as_double(0x7ff0000000000000ll), kNone, kNone};
+  const uint32_t LR = a.L * a.RB;
+
+  auto flush_best = [&](uint32_t qi) {  // MODE 1: block argmin -> partial
+    Best b = warp_best(tb);
+    if (lane == 0) wbest[warp] = b;
+    __syncthreads();
+    if (tid == 0) {
+      Best x = wbest[0];
+      for (int w = 1; w < kNT / 32; ++w)
+        if (better(wbest[w].d, wbest[w].seq, x.d, x.seq)) x = wbest[w];
+      moe_match m;
+      m.index = x.idx;
+      m.seq = x.seq;
+      m.distance = x.d;
+      a.partials[(uint64_t)qi * gridDim.x + blockIdx.x] = m;
+    }
+    __syncthreads();
+    tb = Best{__longlong_as_double(0x7ff0000000000000ll), kNone, kNone};
+  };
+
+  for (uint64_t j = 0; j < total; ++j) {
+    const uint64_t item = it0 + j / a.n_groups;
+    const uint32_t g = (uint32_t)(j % a.n_groups);
+    const uint32_t qi = (uint32_t)(item / a.n_pt);
+    const uint32_t pt = (uint32_t)(item % a.n_pt);
+    if (g == 0 && (int64_t)qi != cur_qi) {
+      if (MODE == 1 && cur_qi >= 0) flush_best((uint32_t)cur_qi);
+      __syncthreads();
+      // Stage the probe tile: QT probes starting at q0 (mode 0) or qlist[qi].
+      const uint32_t q0 = MODE == 0 ? qi * QT : (a.qlist ? a.qlist[qi] : a.q_single);
+      const uint32_t nbytes = QT * LR;
+      for (uint32_t o = tid * 16; o < nbytes; o += kNT * 16) {
+        const uint32_t q = q0 + o / LR;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (q < a.Q) v = *reinterpret_cast<const uint4*>(a.probes + (uint64_t)q0 * LR + o);
+        *reinterpret_cast<uint4*>(probe_s + o) = v;
+      }
+      for (uint32_t o = tid; o < QT * a.L; o += kNT) {
+        const uint32_t q = q0 + o / a.L;
+        ia_s[o] = q < a.Q ? a.ia[(uint64_t)q0 * a.L + o] : 0.f;
+      }
+      if (MODE != 0)
+        for (uint32_t o = tid; o < a.L; o += kNT) sqa_s[o] = a.sqa[(uint64_t)q0 * a.L + o];
+      __syncthreads();
+      cur_qi = qi;
+    }
+
+    const uint32_t s = (uint32_t)(j % a.S);
+    mbar_wait(&bars[s], (uint32_t)((j / a.S) & 1));
+
+    const uint32_t p = pt * kNT + tid;
+    const bool valid = p < a.size;
+    const uint8_t* ebase = stages + (size_t)s * lay.stage_bytes + (size_t)tid * a.G * a.RB;
+    for (uint32_t gg = 0; gg < a.G; ++gg) {
+      const uint32_t l = g * a.G + gg;
+      if (l >= a.L) break;
+      Acc acc[QT];
+#pragma unroll
+      for (int q = 0; q < QT; ++q) acc[q] = 0;
+      const uint8_t* erow = ebase + gg * a.RB;
+      const uint8_t* prow = probe_s + l * a.RB;
+      // Per-lane chunk rotation keeps the 32 entry-row reads of a warp on
+      // distinct shared-memory bank groups (rows are RB-strided).
+      uint32_t k = lane % a.C;
+      for (uint32_t c = 0; c < a.C; ++c) {
+        const uint4 ev = *reinterpret_cast<const uint4*>(erow + 16 * k);
+#pragma unroll
+        for (int q = 0; q < QT; ++q) {
+          const uint4 pv = *reinterpret_cast<const uint4*>(prow + q * LR + 16 * k);
+          acc[q] = D::chunk(ev, pv, acc[q]);
+        }
+        if (++k == a.C) k = 0;
+      }
+      const float ib = valid ? __ldg(&a.ibT[(uint64_t)l * a.cap + p]) : 0.f;
+#pragma unroll
+      for (int q = 0; q < QT; ++q) {
+        const float ia = ia_s[q * a.L + l];
+        if (ia == 0.f && ib == 0.f)
+          sim[q] += 1.f;
+        else
+          sim[q] = fmaf(acc_to_float<Acc>(acc[q]) * ia, ib, sim[q]);
+      }
+      if (MODE != 0) dots_s[l * kNT + tid] = acc[0];
+    }
+
+    if (g == a.n_groups - 1) {
+      if (MODE == 0) {
+        float dq[QT];
+#pragma unroll
+        for (int q = 0; q < QT; ++q) {
+          float d = 1.f - sim[q] / (float)a.L;
+          d = fmaxf(d, 0.f);
+          if (!valid || qi * QT + q >= a.Q) d = __uint_as_float(kFInf);
+          dq[q] = d;
+          const uint32_t m = __reduce_min_sync(0xffffffffu, __float_as_uint(d));
+          if (lane == 0) red[warp * QT + q] = m;
+        }
+        __syncthreads();
+        if (tid < QT) {
+          const uint32_t qg = qi * QT + tid;
+          float tv = __uint_as_float(kFInf);
+          if (qg < a.Q) {
+            uint32_t m = red[tid];
+            for (int w = 1; w < kNT / 32; ++w) m = min(m, red[w * QT + tid]);
+            uint32_t t = *reinterpret_cast<volatile uint32_t*>(&a.T[qg]);
+            if (m < t) t = min(atomicMin(&a.T[qg], m), m);
+            tv = __uint_as_float(t);
+          }
+          tnow[tid] = tv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < QT; ++q) {
+          const uint32_t qg = qi * QT + q;
+          if (valid && qg < a.Q && dq[q] <= tnow[q] + a.eps2) {
+            const uint32_t pos = atomicAdd(&a.bcnt[qg], 1u);
+            if (pos < a.bcap)
+              a.bucket[(uint64_t)qg * a.bcap + pos] = make_uint2(p, __float_as_uint(dq[q]));
+          }
+        }
+      } else {
+        const uint32_t q = a.qlist ? a.qlist[qi] : a.q_single;
+        float d32 = fmaxf(1.f - sim[0] / (float)a.L, 0.f);
+        bool cand = valid;
+        double thr = 0.0;
+        if (MODE == 1) {
+          if (a.Tfinal) cand = cand && d32 <= __uint_as_float(a.Tfinal[q]) + a.eps2;
+        } else {
+          thr = __dadd_rn(a.best[q].distance, a.window);
+          cand = cand && d32 <= (float)thr + a.eps2;
+        }
+        if (cand) {
+          double sm = 0.0;
+          const double* sb = a.sqb + (uint64_t)p * a.L;
+          for (uint32_t l = 0; l < a.L; ++l)
+            sm = __dadd_rn(sm, row_sim_exact((uint64_t)dots_s[l * kNT + tid], sqa_s[l], sb[l]));
+          const double d = finish_distance(sm, a.L);
+          if (MODE == 1) {
+            const uint64_t sq = a.seq[p];
+            if (better(d, sq, tb.d, tb.seq)) tb = Best{d, sq, p};
+          } else if (d <= thr) {
+            const uint32_t pos = atomicAdd(a.wl_n, 1u);
+            a.wl[pos] = WinEntry{p, a.seq[p], d};
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < QT; ++q) sim[q] = 0.f;
+    }
+    __syncthreads();
+    if (tid == 0 && j + a.S < total) issue(j + a.S);
+  }
+  if (MODE == 1 && cur_qi >= 0) flush_best((uint32_t)cur_qi);
+}
+
+// Exact distance of packed probe row-set `pa` vs entry `pb`, warp-cooperative
+// (lane = layer), reference operation order (eam.cpp:95-103).
+template <int CB>
+__device__ double warp_exact_distance(const uint8_t* pa, const double* sqa, const uint8_t* pb,
+                                      const double* sqb, uint32_t L, uint32_t C, uint32_t RB) {
+  const uint32_t lane = threadIdx.x & 31;
+  double sim = 0.0;
+  for (uint32_t l0 = 0; l0 < L; l0 += 32) {
+    const uint32_t l = l0 + lane;
+    double r = 0.0;
+    if (l < L) {
+      typename Dot<CB>::Acc acc = 0;
+      const uint4* ra = reinterpret_cast<const uint4*>(pa + (uint64_t)l * RB);
+      const uint4* rb = reinterpret_cast<const uint4*>(pb + (uint64_t)l * RB);
+      for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(ra[c], rb[c], acc);
+      r = row_sim_exact((uint64_t)acc, sqa[l], sqb[l]);
+    }
+    const uint32_t n = min(32u, L - l0);
+    for (uint32_t i = 0; i < n; ++i) sim = __dadd_rn(sim, __shfl_sync(0xffffffffu, r, i));
+  }
+  return finish_distance(sim, L);
+}
+
+struct RefineArgs {
+  const uint8_t* counts;
+  const double* sqb;
+  const uint64_t* seq;
+  uint32_t size;
+  const uint8_t* probes;
+  const double* sqa;
+  uint32_t Q, L, C, RB;
+  float eps2;
+  const uint32_t* T;
+  const uint32_t* bcnt;
+  const uint2* bucket;
+  uint32_t bcap;
+  uint32_t* over_list;
+  uint32_t* over_n;
+  moe_match* out;
+  const int* halt;
+  int* halt_set;
+  uint32_t halt_value;
+};
+
+template <int CB>
+__global__ void k_refine(const RefineArgs r) {
+  const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (q >= r.Q) return;
+  if (r.halt && *r.halt) return;
+  moe_match none{kNone, kNone, __longlong_as_double(0x7ff0000000000000ll)};
+  if (r.size == 0) {
+    if (lane == 0) r.out[q] = none;
+    return;
+  }
+  const uint32_t n = r.bcnt[q];
+  if (n > r.bcap) {
+    if (lane == 0) {
+      if (r.over_list) r.over_list[atomicAdd(r.over_n, 1u)] = q;
+      if (r.halt_set) *r.halt_set = (int)r.halt_value;
+    }
+    return;
+  }
+  const float thr = __uint_as_float(r.T[q]) + r.eps2;
+  Best b{__longlong_as_double(0x7ff0000000000000ll), kNone, kNone};
+  const uint64_t LR = (uint64_t)r.L * r.RB;
+  for (uint32_t base = 0; base < n; base += 32) {
+    const uint32_t i = base + lane;
+    bool cand = false;
+    uint32_t p = 0;
+    if (i < n) {
+      const uint2 e = r.bucket[(uint64_t)q * r.bcap + i];
+      p = e.x;
+      cand = __uint_as_float(e.y) <= thr;
+    }
+    uint32_t mask = __ballot_sync(0xffffffffu, cand);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint32_t pp = __shfl_sync(0xffffffffu, p, src);
+      const double d = warp_exact_distance<CB>(r.probes + q * LR, r.sqa + (uint64_t)q * r.L,
+                                               r.counts + pp * LR, r.sqb + (uint64_t)pp * r.L,
+                                               r.L, r.C, r.RB);
+      const uint64_t s = r.seq[pp];
+      if (better(d, s, b.d, b.seq)) b = Best{d, s, pp};
+    }
+  }
+  if (lane == 0) r.out[q] = moe_match{b.idx, b.seq, b.d};
+}
+
+// Partial merge for mode 1: for list position qi, the blocks whose item
+// range intersects [qi*n_pt, (qi+1)*n_pt).
+__global__ void k_merge_partials(const moe_match* parts, uint32_t grid, uint32_t nq,
+                                 uint32_t n_pt, const uint32_t* qlist, moe_match* out) {
+  const uint32_t qi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (qi >= nq) return;
+  const uint64_t n_items = (uint64_t)nq * n_pt;
+  Best b{__longlong_as_double(0x7ff0000000000000ll), kNone, kNone};
+  for (uint32_t blk = lane; blk < grid; blk += 32) {
+    const uint64_t i0 = n_items * blk / grid, i1 = n_items * (blk + 1) / grid;
+    const uint64_t q0 = (uint64_t)qi * n_pt, q1 = q0 + n_pt;
+    if (i0 < i1 && i0 < q1 && i1 > q0) {
+      const moe_match m = parts[(uint64_t)qi * grid + blk];
+      if (better(m.distance, m.seq, b.d, b.seq)) b = Best{m.distance, m.seq, m.index};
+    }
+  }
+  b = warp_best(b);
+  if (lane == 0) out[qlist[qi]] = moe_match{b.idx, b.seq, b.d};
+}
+
+__global__ void k_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out) {
+  const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  moe_match b = parts[q];
+  for (uint64_t k = 1; k < n_parts; ++k) {
+    const moe_match m = parts[k * n + q];
+    if (better(m.distance, m.seq, b.distance, b.seq)) b = m;
+  }
+  out[q] = b;
+}
+
+template <int CB>
+__global__ void k_pair_distance(const uint8_t* a, const double* sqa, const uint8_t* b,
+                                const double* sqb, uint32_t L, uint32_t C, uint32_t RB,
+                                double* out) {
+  const double d = warp_exact_distance<CB>(a, sqa, b, sqb, L, C, RB);
+  if (threadIdx.x == 0) *out = d;
+}
+
+// u64 / u16 / u8 counts -> packed rows of cb-byte counts + sqrt(sum c^2)
+// and fp32 1/sqrt(sum c^2); one warp per row.
+template <int SRC>
+__device__ __forceinline__ uint64_t load_count(const void* src, uint64_t i) {
+  if (SRC == 8) return reinterpret_cast<const uint64_t*>(src)[i];
+  if (SRC == 2) return reinterpret_cast<const uint16_t*>(src)[i];
+  return reinterpret_cast<const uint8_t*>(src)[i];
+}
+
+template <int SRC>
+__global__ void k_prep(const void* src, uint64_t rows, uint32_t E, uint32_t L, uint32_t RB,
+                       int cb, uint8_t* dst, float* ia, double* sq, float* ibT, uint64_t ib_cap,
+                       uint64_t ib_base, unsigned long long* max_count) {
+  const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const uint64_t sbase = row * E;
+  uint32_t* drow = reinterpret_cast<uint32_t*>(dst + row * RB);
+  const uint32_t per_word = 4 / cb;
+  uint64_t ss = 0, mx = 0;
+  for (uint32_t w = lane; w < RB / 4; w += 32) {
+    uint32_t word = 0;
+    for (uint32_t j = 0; j < per_word; ++j) {
+      const uint32_t e = w * per_word + j;
+      if (e < E) {
+        const uint64_t c = load_count<SRC>(src, sbase + e);
+        mx = c > mx ? c : mx;
+        ss += c * c;  // exact: the caller enforces c <= 65535
+        const uint64_t cc = cb == 1 ? (c & 0xffu) : (c & 0xffffu);
+        word |= (uint32_t)cc << (8 * cb * j);
+      }
+    }
+    drow[w] = word;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const uint64_t m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = m2 > mx ? m2 : mx;
+  }
+  if (lane == 0) {
+    const double s = __dsqrt_rn(__ull2double_rn(ss));
+    const float inv = ss ? __double2float_rn(__drcp_rn(s)) : 0.f;
+    sq[row] = s;
+    if (ia) ia[row] = inv;
+    if (ibT) {
+      const uint64_t slot = ib_base + row / L;
+      const uint32_t l = (uint32_t)(row % L);
+      ibT[(uint64_t)l * ib_cap + slot] = inv;
+    }
+    if (max_count && mx) atomicMax(max_count, (unsigned long long)mx);
+  }
+}
+
+__global__ void k_replace(uint8_t* counts, float* ibT, double* sqb, uint64_t* seq, uint64_t cap,
+                          uint32_t L, uint32_t RB, const uint8_t* sp, const float* sia,
+                          const double* ssq, uint32_t i, const moe_match* victim,
+                          uint64_t append_slot, uint64_t seq_value, const int* halt) {
+  if (halt && *halt) return;
+  const uint64_t slot = victim ? victim->index : append_slot;
+  const uint64_t LR = (uint64_t)L * RB;
+  const uint4* src = reinterpret_cast<const uint4*>(sp + (uint64_t)i * LR);
+  uint4* dst = reinterpret_cast<uint4*>(counts + slot * LR);
+  for (uint32_t o = threadIdx.x; o < LR / 16; o += blockDim.x) dst[o] = src[o];
+  for (uint32_t l = threadIdx.x; l < L; l += blockDim.x) {
+    ibT[(uint64_t)l * cap + slot] = sia[(uint64_t)i * L + l];
+    sqb[slot * L + l] = ssq[(uint64_t)i * L + l];
+  }
+  if (threadIdx.x == 0) seq[slot] = seq_value;
+}
+
+__global__ void k_append_staged(uint8_t* counts, float* ibT, double* sqb, uint64_t cap, uint32_t L,
+                                uint32_t RB, const uint8_t* sp, const float* sia,
+                                const double* ssq, uint32_t first, uint32_t n, uint64_t base) {
+  const uint64_t LR = (uint64_t)L * RB;
+  const uint64_t words = (uint64_t)n * LR / 16;
+  const uint4* src = reinterpret_cast<const uint4*>(sp + (uint64_t)first * LR);
+  uint4* dst = reinterpret_cast<uint4*>(counts + base * LR);
+  for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < words;
+       o += (uint64_t)gridDim.x * blockDim.x)
+    dst[o] = src[o];
+  for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < (uint64_t)n * L;
+       o += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = o / L;
+    const uint32_t l = (uint32_t)(o % L);
+    ibT[(uint64_t)l * cap + base + e] = sia[((uint64_t)first + e) * L + l];
+    sqb[(base + e) * L + l] = ssq[((uint64_t)first + e) * L + l];
+  }
+}
+
+__global__ void k_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32_t RB_old,
+                        uint32_t RB_new) {
+  for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < rows * (RB_new / 2);
+       o += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = o / (RB_new / 2);
+    const uint32_t e = (uint32_t)(o % (RB_new / 2));
+    const uint16_t v = e < RB_old ? src[r * RB_old + e] : 0;
+    reinterpret_cast<uint16_t*>(dst + r * RB_new)[e] = v;
+  }
+}
+
+// K4 tail: aggregate rows > cur of every window member into agg (u64).
+template <int CB>
+__global__ void k_aggregate(const uint8_t* counts, uint32_t L, uint32_t E, uint32_t RB,
+                            const WinEntry* wl, const uint32_t* wl_n, uint32_t cur,
+                            unsigned long long* agg) {
+  extern __shared__ unsigned long long agg_s[];
+  const uint32_t first = (cur + 1) * E;
+  const uint32_t ncell = L * E - first;
+  for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x) agg_s[i] = 0;
+  __syncthreads();
+  const uint32_t n = *wl_n;
+  const uint32_t warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x & 31;
+  for (uint32_t m = blockIdx.x * warps + wid; m < n; m += gridDim.x * warps) {
+    const uint8_t* ent = counts + wl[m].p * (uint64_t)L * RB;
+    for (uint32_t i = lane; i < ncell; i += 32) {
+      const uint32_t cell = first + i;
+      const uint32_t l = cell / E, e = cell - l * E;
+      const uint32_t c = CB == 1 ? ent[(uint64_t)l * RB + e]
+                                 : reinterpret_cast<const uint16_t*>(ent + (uint64_t)l * RB)[e];
+      if (c) atomicAdd(&agg_s[i], (unsigned long long)c);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x)
+    if (agg_s[i]) atomicAdd(&agg[first + i], agg_s[i]);
+}
+
+// K5+K6 fused decision kernel (one block).
+__global__ void __launch_bounds__(1024)
+    k_decide(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur, int filter,
+             int do_prefetch, const unsigned long long* req, const moe_slot_view* slots,
+             uint64_t n_slots, moe_candidate* out, uint32_t* n_out, long long* victim,
+             double* slot_pri, uint32_t npow2) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(sm);
+  uint32_t* val = reinterpret_cast<uint32_t*>(key + npow2);
+  unsigned long long* rs = reinterpret_cast<unsigned long long*>(val + npow2);  // [L] agg rows
+  unsigned long long* rq = rs + L;                                             // [L] req rows
+  __shared__ uint32_t cnt;
+  __shared__ double vbest_p[32];
+  __shared__ uint64_t vbest_k[32];
+  __shared__ long long vbest_s[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const double kEps = 1e-4;  // policy.hpp:22
+  if (tid == 0) cnt = 0;
+  for (uint32_t l = wid; l < L; l += nw) {
+    unsigned long long a = 0, b = 0;
+    for (uint32_t e = lane; e < E; e += 32) {
+      if (do_prefetch && l > cur) a += agg[(uint64_t)l * E + e];
+      if (req) b += req[(uint64_t)l * E + e];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+      rs[l] = a;
+      rq[l] = b;
+    }
+  }
+  __syncthreads();
+  if (do_prefetch) {
+    const uint32_t first = (cur + 1) * E;
+    const uint32_t n = L * E - first;
+    for (uint32_t i = tid; i < n; i += blockDim.x) {
+      const uint32_t flat = first + i;
+      const uint32_t l = flat / E;
+      const unsigned long long rsum = rs[l];
+      const double ratio =
+          rsum == 0 ? 0.0 : __ddiv_rn(__ull2double_rn(agg[flat]), __ull2double_rn(rsum));
+      const double prox = __dsub_rn(1.0, __ddiv_rn((double)(l - cur), (double)L));
+      const double pri = __dmul_rn(__dadd_rn(ratio, kEps), prox);
+      if (filter && pri <= __dmul_rn(__dmul_rn(kEps, prox), __dadd_rn(1.0, 1e-9))) continue;
+      const uint32_t pos = atomicAdd(&cnt, 1u);
+      key[pos] = ~(unsigned long long)__double_as_longlong(pri);  // descending priority
+      val[pos] = flat;
+    }
+    __syncthreads();
+    const uint32_t m = cnt;
+    uint32_t np = 1;
+    while (np < m) np <<= 1;
+    for (uint32_t i = m + tid; i < np; i += blockDim.x) {
+      key[i] = ~0ull;
+      val[i] = 0xffffffffu;
+    }
+    __syncthreads();
+    // bitonic sort on (key asc, val asc)
+    for (uint32_t k = 2; k <= np; k <<= 1) {
+      for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+        for (uint32_t i = tid; i < np; i += blockDim.x) {
+          const uint32_t ixj = i ^ jj;
+          if (ixj > i) {
+            const bool up = (i & k) == 0;
+            const unsigned long long ki = key[i], kj = key[ixj];
+            const uint32_t vi = val[i], vj = val[ixj];
+            const bool gt = ki > kj || (ki == kj && vi > vj);
+            if (gt == up) {
+              key[i] = kj;
+              key[ixj] = ki;
+              val[i] = vj;
+              val[ixj] = vi;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (uint32_t i = tid; i < m; i += blockDim.x) {
+      const uint32_t flat = val[i];
+      moe_candidate c;
+      c.layer_idx = flat / E;
+      c.expert_idx = flat - c.layer_idx * E;
+      c.priority = __longlong_as_double((long long)~key[i]);
+      out[i] = c;
+    }
+    if (tid == 0) *n_out = m;
+  }
+  if (victim || slot_pri) {
+    // select_eviction_victim: argmin (cache_priority, ExpertId) over
+    // unprotected, unpinned slots (policy.cpp:143-159).
+    double bp = 0.0;
+    uint64_t bk = ~0ull;
+    long long bs = -1;
+    for (uint64_t i = tid; i < n_slots; i += blockDim.x) {
+      const moe_slot_view v = slots[i];
+      if (!slot_pri && (v.prefetch_protected || v.pinned)) continue;
+      const unsigned long long rsum = rq[v.layer_idx];
+      const double ratio =
+          rsum == 0 ? 0.0
+                    : __ddiv_rn(__ull2double_rn(req[(uint64_t)v.layer_idx * E + v.expert_idx]),
+                                __ull2double_rn(rsum));
+      const double w = __dsub_rn(1.0, __ddiv_rn((double)v.layer_idx, (double)L));
+      const double p = __dmul_rn(__dadd_rn(ratio, kEps), w);
+      if (slot_pri) slot_pri[i] = p;
+      if (v.prefetch_protected || v.pinned) continue;
+      const uint64_t k = ((uint64_t)v.layer_idx << 32) | v.expert_idx;
+      if (bs < 0 || p < bp || (p == bp && k < bk)) {
+        bp = p;
+        bk = k;
+        bs = (long long)v.slot;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const long long os = __shfl_xor_sync(0xffffffffu, bs, o);
+      if (os >= 0 && (bs < 0 || op < bp || (op == bp && ok < bk))) {
+        bp = op;
+        bk = ok;
+        bs = os;
+      }
+    }
+    if (lane == 0) {
+      vbest_p[wid] = bp;
+      vbest_k[wid] = bk;
+      vbest_s[wid] = bs;
+    }
+    __syncthreads();
+    if (tid == 0 && victim) {
+      for (uint32_t w = 1; w < nw; ++w) {
+        if (vbest_s[w] >= 0 &&
+            (bs < 0 || vbest_p[w] < bp || (vbest_p[w] == bp && vbest_k[w] < bk))) {
+          bp = vbest_p[w];
+          bk = vbest_k[w];
+          bs = vbest_s[w];
+        }
+      }
+      *victim = bs;
+    }
+  }
+}
+
+// K1: top-k ids -> per-request histograms in shared memory.
+template <int IB>
+__device__ __forceinline__ uint32_t load_idx(const void* p, uint64_t i) {
+  if (IB == 1) return reinterpret_cast<const uint8_t*>(p)[i];
+  if (IB == 2) return reinterpret_cast<const uint16_t*>(p)[i];
+  return reinterpret_cast<const uint32_t*>(p)[i];
+}
+
+template <int IB>
+__global__ void __launch_bounds__(512)
+    k_trace(const void* topk, uint64_t T, uint32_t L, uint32_t E, uint32_t k,
+            const uint64_t* offsets, uint64_t R, uint32_t* scratch, int* bad, uint32_t chunk) {
+  extern __shared__ uint32_t hist[];
+  const uint32_t ncell = L * E;
+  const uint64_t n_chunks = (T + chunk - 1) / chunk;
+  for (uint64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    const uint64_t t0 = ch * chunk;
+    const uint64_t t1 = min(T, t0 + chunk);
+    // first request whose range ends after t0 (offsets is non-decreasing)
+    uint64_t lo = 0, hi = R;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      if (offsets[mid + 1] <= t0) lo = mid + 1; else hi = mid;
+    }
+    for (uint64_t r = lo; r < R && offsets[r] < t1; ++r) {
+      const uint64_t s0 = max(t0, offsets[r]), s1 = min(t1, offsets[r + 1]);
+      if (s0 >= s1) continue;
+      for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      const uint64_t pairs = (s1 - s0) * L;
+      for (uint64_t u = threadIdx.x; u < pairs; u += blockDim.x) {
+        const uint64_t tok = s0 + u / L;
+        const uint32_t l = (uint32_t)(u % L);
+        const uint64_t base = (tok * L + l) * k;
+        for (uint32_t j = 0; j < k; ++j) {
+          const uint32_t e = load_idx<IB>(topk, base + j);
+          if (e < E)
+            atomicAdd(&hist[l * E + e], 1u);
+          else
+            *bad = 1;
+        }
+      }
+      __syncthreads();
+      uint32_t* dst = scratch + r * (uint64_t)ncell;
+      for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x)
+        if (hist[i]) atomicAdd(&dst[i], hist[i]);
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void k_trace_commit(const uint32_t* scratch, uint64_t n, const int* bad,
+                               uint32_t* counts) {
+  if (*bad) return;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    counts[i] += scratch[i];
+}
+
+__global__ void k_trace_commit64(const uint32_t* scratch, uint64_t n, const int* bad,
+                                 unsigned long long* counts) {
+  if (*bad) return;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    counts[i] += scratch[i];
+}
+
+template <int CB, int QT, int MODE>
+cudaError_t set_smem_attr(size_t smem) {
+  return cudaFuncSetAttribute(k_match<CB, QT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem);
+}
+
+template <int CB, int QT, int MODE>
+cudaError_t launch_match_t(const CUtensorMap& map, const MatchArgs& a, const MatchGeom& g,
+                           cudaStream_t st) {
+  cudaError_t e = set_smem_attr<CB, QT, MODE>(g.smem);
+  if (e != cudaSuccess) return e;
+  k_match<CB, QT, MODE><<<g.grid, kNT, g.smem, st>>>(map, a);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t dispatch_match(int cb, uint32_t QT, const CUtensorMap& map, const MatchArgs& a,
+                           const MatchGeom& g, cudaStream_t st) {
+  if (MODE != 0) {
+    return cb == 1 ? launch_match_t<1, 1, MODE>(map, a, g, st)
+                   : launch_match_t<2, 1, MODE>(map, a, g, st);
+  }
+#define MOE_QT_CASE(q)                                                      \
+  case q:                                                                   \
+    return cb == 1 ? launch_match_t<1, q, 0>(map, a, g, st)                 \
+                   : launch_match_t<2, q, 0>(map, a, g, st);
+  switch (QT) {
+    MOE_QT_CASE(1)
+    MOE_QT_CASE(2)
+    MOE_QT_CASE(4)
+    MOE_QT_CASE(8)
+    MOE_QT_CASE(16)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef MOE_QT_CASE
+}
+
+MatchArgs base_args(const DevColl& c, const DevProbes& pr, const MatchGeom& g) {
+  MatchArgs a{};
+  a.ibT = c.ibT;
+  a.sqb = c.sqb;
+  a.seq = c.seq;
+  a.cap = c.cap;
+  a.size = c.size;
+  a.probes = pr.packed;
+  a.ia = pr.ia;
+  a.sqa = pr.sqa;
+  a.Q = pr.Q;
+  a.L = c.L;
+  a.RB = c.RB;
+  a.C = c.C;
+  a.G = g.G;
+  a.S = g.S;
+  a.n_groups = g.n_groups;
+  a.n_pt = g.n_pt;
+  a.eps2 = screen_eps2(c.L);
+  return a;
+}
+
+}  // namespace
+
+float screen_eps2(uint32_t L) {
+  // |d32 - d_ref| <= u * (6 + (L+1)/2) with u = 2^-24 (see DESIGN.md
+  // "screen bound"); 1.5x safety margin plus an absolute floor.
+  const double u = 1.0 / 16777216.0;
+  const double eps = 1.5 * u * (6.0 + 0.5 * (L + 1.0)) + 1e-9;
+  return (float)(2.0 * eps);
+}
+
+bool plan_match(const DevColl& c, int n_sm, int mode, uint32_t QT, MatchGeom* g) {
+  const size_t kMaxSmem = 220 * 1024;
+  const uint32_t acc_bytes = c.cb == 1 ? 4 : 8;
+  // Choose the layer-group depth G: prefer conflict-free shared-memory
+  // banking for the per-lane rotated row reads, then the deepest stage
+  // that fits 3 (else 2) pipeline stages.
+  double best_score = -1.0;
+  MatchGeom best;
+  for (uint32_t S = 3; S >= 2; --S) {
+    for (uint32_t G = 1; G <= std::min<uint32_t>(c.L, 16); ++G) {
+      const SmemLayout lay = smem_layout(c.L, c.RB, G, S, QT, mode, acc_bytes);
+      if (lay.total > kMaxSmem) continue;
+      // bank-group wavefronts of one warp-wide 16-byte row read
+      double wf = 0.0;
+      for (uint32_t cc = 0; cc < c.C; ++cc) {
+        int cnt[8] = {0};
+        for (uint32_t ln = 0; ln < 32; ++ln) {
+          const uint32_t k = (cc + ln) % c.C;
+          const uint64_t chunk = (uint64_t)ln * G * c.C + k;
+          cnt[chunk % 8]++;
+        }
+        int m = 4;
+        for (int b = 0; b < 8; ++b) m = std::max(m, cnt[b]);
+        wf += m;
+      }
+      wf /= c.C;
+      const uint32_t ng = (c.L + G - 1) / G;
+      const double waste = (double)(ng * G) / c.L;  // OOB layers still cost TMA bandwidth
+      const double score = (4.0 / wf) / waste + 0.01 * G + 0.001 * S;
+      if (score > best_score) {
+        best_score = score;
+        best.G = G;
+        best.S = S;
+        best.smem = lay.total;
+      }
+    }
+    if (best_score > 0) break;
+  }
+  if (best_score < 0) return false;
+  best.QT = QT;
+  best.n_groups = (c.L + best.G - 1) / best.G;
+  best.n_pt = (c.size + kNT - 1) / kNT;
+  best.grid = (uint32_t)n_sm;
+  *g = best;
+  return true;
+}
+
+cudaError_t encode_tmap(const DevColl& c, uint32_t G, CUtensorMap* map) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[4] = {16, c.C, c.L, c.cap};
+  const cuuint64_t strides[3] = {16, c.RB, (cuuint64_t)c.L * c.RB};
+  const cuuint32_t box[4] = {16, c.C, G, (cuuint32_t)kNT};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, c.counts, dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, uint32_t E,
+                        uint32_t RB, int cb, uint8_t* dst, float* ia, double* sq, float* ibT,
+                        uint64_t ib_cap, uint64_t ib_base, unsigned long long* max_count,
+                        cudaStream_t st) {
+  const uint64_t rows = n * L;
+  if (rows == 0) return cudaSuccess;
+  const uint32_t threads = 256;
+  const uint64_t blocks = (rows * 32 + threads - 1) / threads;
+  switch (src_bytes) {
+    case 8:
+      k_prep<8><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,
+                                                      ib_cap, ib_base, max_count);
+      break;
+    case 2:
+      k_prep<2><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,
+                                                      ib_cap, ib_base, max_count);
+      break;
+    case 1:
+      k_prep<1><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,
+                                                      ib_cap, ib_base, max_count);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_screen(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
+                          const MatchGeom& g, const MatchWork& w, cudaStream_t st) {
+  if (c.size == 0 || pr.Q == 0) return cudaSuccess;
+  MatchArgs a = base_args(c, pr, g);
+  a.T = w.T;
+  a.bcnt = w.bcnt;
+  a.bucket = w.bucket;
+  a.bcap = w.bcap;
+  return dispatch_match<0>(c.cb, g.QT, map, a, g, st);
+}
+
+cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork& w,
+                          moe_match* out, const int* halt, int* halt_set, uint32_t halt_value,
+                          cudaStream_t st) {
+  if (pr.Q == 0) return cudaSuccess;
+  RefineArgs r{};
+  r.counts = c.counts;
+  r.sqb = c.sqb;
+  r.seq = c.seq;
+  r.size = c.size;
+  r.probes = pr.packed;
+  r.sqa = pr.sqa;
+  r.Q = pr.Q;
+  r.L = c.L;
+  r.C = c.C;
+  r.RB = c.RB;
+  r.eps2 = screen_eps2(c.L);
+  r.T = w.T;
+  r.bcnt = w.bcnt;
+  r.bucket = w.bucket;
+  r.bcap = w.bcap;
+  r.over_list = w.over_list;
+  r.over_n = w.over_n;
+  r.out = out;
+  r.halt = halt;
+  r.halt_set = halt_set;
+  r.halt_value = halt_value;
+  const uint32_t threads = 256;
+  const uint32_t blocks = (uint32_t)(((uint64_t)pr.Q * 32 + threads - 1) / threads);
+  if (c.cb == 1)
+    k_refine<1><<<blocks, threads, 0, st>>>(r);
+  else
+    k_refine<2><<<blocks, threads, 0, st>>>(r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
+                         const MatchGeom& g, const MatchWork& w, const uint32_t* qlist,
+                         uint32_t qlist_n, const uint32_t* T, moe_match* out, cudaStream_t st) {
+  if (qlist_n == 0) return cudaSuccess;
+  for (uint32_t off = 0; off < qlist_n; off += w.part_chunk) {
+    const uint32_t n = std::min(w.part_chunk, qlist_n - off);
+    MatchArgs a = base_args(c, pr, g);
+    a.qlist = qlist + off;
+    a.nq_list = n;
+    a.Tfinal = T;
+    a.partials = w.partials;
+    cudaError_t e = dispatch_match<1>(c.cb, 1, map, a, g, st);
+    if (e != cudaSuccess) return e;
+    const uint32_t threads = 256;
+    const uint32_t blocks = (uint32_t)(((uint64_t)n * 32 + threads - 1) / threads);
+    k_merge_partials<<<blocks, threads, 0, st>>>(w.partials, g.grid, n, g.n_pt, qlist + off, out);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_window(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
+                          const MatchGeom& g, uint32_t q0, const moe_match* best, double window,
+                          WinEntry* wl, uint32_t* wl_n, cudaStream_t st) {
+  MatchArgs a = base_args(c, pr, g);
+  a.qlist = nullptr;
+  a.q_single = q0;
+  a.nq_list = 1;
+  a.best = best;
+  a.window = window;
+  a.wl = wl;
+  a.wl_n = wl_n;
+  return dispatch_match<2>(c.cb, 1, map, a, g, st);
+}
+
+cudaError_t launch_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out,
+                         cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_merge<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(parts, n_parts, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pair_distance(const uint8_t* a, const double* sqa, const uint8_t* b,
+                                 const double* sqb, uint32_t L, uint32_t C, uint32_t RB, int cb,
+                                 double* out, cudaStream_t st) {
+  if (cb == 1)
+    k_pair_distance<1><<<1, 32, 0, st>>>(a, sqa, b, sqb, L, C, RB, out);
+  else
+    k_pair_distance<2><<<1, 32, 0, st>>>(a, sqa, b, sqb, L, C, RB, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_replace(const DevColl& c, const DevProbes& staged, uint32_t i,
+                           const moe_match* victim, uint64_t seq_value, const int* halt,
+                           cudaStream_t st) {
+  k_replace<<<1, 256, 0, st>>>(c.counts, c.ibT, c.sqb, c.seq, c.cap, c.L, c.RB, staged.packed,
+                               staged.ia, staged.sqa, i, victim, c.size, seq_value, halt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_append_staged(const DevColl& c, const DevProbes& staged, uint32_t first,
+                                 uint32_t n, uint64_t base, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_append_staged<<<256, 256, 0, st>>>(c.counts, c.ibT, c.sqb, c.cap, c.L, c.RB, staged.packed,
+                                       staged.ia, staged.sqa, first, n, base);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32_t RB_old,
+                         uint32_t RB_new, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  k_widen<<<1024, 256, 0, st>>>(src, dst, rows, RB_old, RB_new);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_aggregate(const DevColl& c, const WinEntry* wl, const uint32_t* wl_n,
+                             uint32_t cur, unsigned long long* agg, cudaStream_t st) {
+  if (cur + 1 >= c.L) return cudaSuccess;
+  const size_t smem = (size_t)(c.L - cur - 1) * c.E * 8;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e;
+  if (c.cb == 1) {
+    e = cudaFuncSetAttribute(k_aggregate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    k_aggregate<1><<<148, 512, smem, st>>>(c.counts, c.L, c.E, c.RB, wl, wl_n, cur, agg);
+  } else {
+    e = cudaFuncSetAttribute(k_aggregate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    k_aggregate<2><<<148, 512, smem, st>>>(c.counts, c.L, c.E, c.RB, wl, wl_n, cur, agg);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decide(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur,
+                          int filter, int do_prefetch, const unsigned long long* req,
+                          const moe_slot_view* slots, uint64_t n_slots, moe_candidate* out,
+                          uint32_t* n_out, long long* victim, double* slot_pri,
+                          cudaStream_t st) {
+  uint32_t n = do_prefetch && cur + 1 < L ? (L - cur - 1) * E : 1;
+  uint32_t np = 2;
+  while (np < n) np <<= 1;
+  const size_t smem = (size_t)np * 12 + (size_t)L * 16 + 16;
+  if (smem > 220 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e =
+      cudaFuncSetAttribute(k_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_decide<<<1, 1024, smem, st>>>(agg, L, E, cur, filter, do_prefetch && cur + 1 < L, req, slots,
+                                  n_slots, out, n_out, victim, slot_pri, np);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace(const void* topk, int idx_bytes, uint64_t T, uint32_t L, uint32_t E,
+                         uint32_t k, const uint64_t* offsets, uint64_t R, uint32_t* scratch,
+                         int* bad, int n_sm, cudaStream_t st) {
+  if (T == 0 || R == 0) return cudaSuccess;
+  const size_t smem = (size_t)L * E * 4;
+  if (smem > 220 * 1024) return cudaErrorInvalidValue;
+  const uint32_t chunk = 512;
+  const uint64_t n_chunks = (T + chunk - 1) / chunk;
+  const unsigned grid = (unsigned)std::min<uint64_t>(n_chunks, (uint64_t)n_sm * 4);
+  cudaError_t e;
+  switch (idx_bytes) {
+    case 1:
+      e = cudaFuncSetAttribute(k_trace<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      k_trace<1><<<grid, 512, smem, st>>>(topk, T, L, E, k, offsets, R, scratch, bad, chunk);
+      break;
+    case 2:
+      e = cudaFuncSetAttribute(k_trace<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      k_trace<2><<<grid, 512, smem, st>>>(topk, T, L, E, k, offsets, R, scratch, bad, chunk);
+      break;
+    case 4:
+      e = cudaFuncSetAttribute(k_trace<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      k_trace<4><<<grid, 512, smem, st>>>(topk, T, L, E, k, offsets, R, scratch, bad, chunk);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace_commit(const uint32_t* scratch, uint64_t n, const int* bad,
+                                uint32_t* counts, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_trace_commit<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+      scratch, n, bad, counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace_commit64(const uint32_t* scratch, uint64_t n, const int* bad,
+                                  unsigned long long* counts, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_trace_commit64<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+      scratch, n, bad, counts);
+  return cudaGetLastError();
+}
+
+}  // namespace moe

@@ -1,0 +1,124 @@
+// kernels.cuh -- host-visible launch interface of the sm_100a kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/moe_eamc.h"
+
+namespace moe {
+
+// Device-resident collection (AoS counts [cap][L][RB], SoA metadata).
+struct DevColl {
+  uint32_t L = 0, E = 0, RB = 0, C = 0;
+  int cb = 1;              // bytes per stored count
+  uint64_t cap = 0;
+  uint32_t size = 0;
+  uint8_t* counts = nullptr;  // [cap][L][RB]
+  float* ibT = nullptr;       // [L][cap] fp32 1/sqrt(sum c^2) (0 on zero rows)
+  double* sqb = nullptr;      // [cap][L] sqrt(sum c^2)
+  uint64_t* seq = nullptr;    // [cap]
+};
+
+// Packed probe batch.
+struct DevProbes {
+  uint32_t Q = 0;
+  uint8_t* packed = nullptr;  // [Q][L][RB]
+  float* ia = nullptr;        // [Q][L]
+  double* sqa = nullptr;      // [Q][L]
+};
+
+struct MatchGeom {
+  uint32_t G = 1, S = 2, QT = 1, n_groups = 1, n_pt = 0, grid = 1;
+  size_t smem = 0;
+};
+
+struct MatchWork {  // scratch for one match pipeline
+  uint32_t* T = nullptr;       // [Q]
+  uint32_t* bcnt = nullptr;    // [Q]
+  uint2* bucket = nullptr;     // [Q][bcap]
+  uint32_t bcap = 0;
+  uint32_t* over_list = nullptr;  // [Q]
+  uint32_t* over_n = nullptr;     // [1]
+  moe_match* partials = nullptr;  // [chunk][grid]
+  uint32_t part_chunk = 0;
+};
+
+struct WinEntry {
+  uint64_t p;
+  uint64_t seq;
+  double d;
+};
+
+float screen_eps2(uint32_t L);
+
+// Geometry for a matcher launch (mode 0 screen with QT probes / tile, or
+// QT=1 exact modes).  Returns false if the shape does not fit shared memory.
+bool plan_match(const DevColl& c, int n_sm, int mode, uint32_t QT, MatchGeom* g);
+
+cudaError_t encode_tmap(const DevColl& c, uint32_t G, CUtensorMap* map);
+
+// u64/u16/u8 counts -> packed rows + norms.  rows = n*L.  When ibT != null
+// the row norms are written as collection metadata at slots base..base+n.
+cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, uint32_t E,
+                        uint32_t RB, int cb, uint8_t* dst, float* ia, double* sq, float* ibT,
+                        uint64_t ib_cap, uint64_t ib_base, unsigned long long* max_count,
+                        cudaStream_t st);
+
+// mode 0: screen all Q probes; then refine.
+cudaError_t launch_screen(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
+                          const MatchGeom& g, const MatchWork& w, cudaStream_t st);
+cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork& w,
+                          moe_match* out, const int* halt, int* halt_set, uint32_t halt_value,
+                          cudaStream_t st);
+// mode 1: exact argmin for the probes listed in qlist[0..*qlist_n) (at most
+// chunk of them starting at qlist_off); T may be null (evaluate all).
+cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
+                         const MatchGeom& g, const MatchWork& w, const uint32_t* qlist,
+                         uint32_t qlist_n, const uint32_t* T, moe_match* out, cudaStream_t st);
+// mode 2: window membership for probe q0 (exact d <= best.distance + window).
+cudaError_t launch_window(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
+                          const MatchGeom& g, uint32_t q0, const moe_match* best, double window,
+                          WinEntry* wl, uint32_t* wl_n, cudaStream_t st);
+
+cudaError_t launch_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out,
+                         cudaStream_t st);
+cudaError_t launch_pair_distance(const uint8_t* a, const double* sqa, const uint8_t* b,
+                                 const double* sqb, uint32_t L, uint32_t C, uint32_t RB, int cb,
+                                 double* out, cudaStream_t st);
+
+// Build replay step: copy staged probe i into the slot chosen by out->index
+// (or append slot), seq = seq_value.  Skips when *halt != 0.
+cudaError_t launch_replace(const DevColl& c, const DevProbes& staged, uint32_t i,
+                           const moe_match* victim, uint64_t seq_value, const int* halt,
+                           cudaStream_t st);
+// Bulk copy staged probes [first, first+n) into slots [base, base+n).
+cudaError_t launch_append_staged(const DevColl& c, const DevProbes& staged, uint32_t first,
+                                 uint32_t n, uint64_t base, cudaStream_t st);
+
+// Window aggregation: agg[L][E] (u64) += rows > cur of every listed entry.
+cudaError_t launch_aggregate(const DevColl& c, const WinEntry* wl, const uint32_t* wl_n,
+                             uint32_t cur, unsigned long long* agg, cudaStream_t st);
+// Fused K5+K6: priorities, floor filter, sort, eviction victim.
+cudaError_t launch_decide(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur,
+                          int filter, int do_prefetch, const unsigned long long* req,
+                          const moe_slot_view* slots, uint64_t n_slots, moe_candidate* out,
+                          uint32_t* n_out, long long* victim, double* slot_pri,
+                          cudaStream_t st);
+
+// K1 tracing: scratch[R][L][E] (u32, zeroed) += histogram; *bad |= 1 on
+// an out-of-range index.
+cudaError_t launch_trace(const void* topk, int idx_bytes, uint64_t T, uint32_t L, uint32_t E,
+                         uint32_t k, const uint64_t* offsets, uint64_t R, uint32_t* scratch,
+                         int* bad, int n_sm, cudaStream_t st);
+cudaError_t launch_trace_commit(const uint32_t* scratch, uint64_t n, const int* bad,
+                                uint32_t* counts, cudaStream_t st);
+
+cudaError_t launch_trace_commit64(const uint32_t* scratch, uint64_t n, const int* bad,
+                                  unsigned long long* counts, cudaStream_t st);
+
+cudaError_t launch_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32_t RB_old,
+                         uint32_t RB_new, cudaStream_t st);
+
+}  // namespace moe

@@ -1,0 +1,475 @@
+"""Python mirror of the reference's EAM/EAMC/policy API over libmoe_eamc.
+
+Names, argument meaning and error behaviour follow moesim's C++ API
+(proj/core/include/moesim/eam.hpp, policy.hpp, model.hpp) so that parity
+tests read like the reference's own tests:
+
+  reference (C++)                          here
+  ---------------------------------------  -----------------------------------
+  ModelShape / ExpertId (model.hpp:19-41)  ModelShape / ExpertId
+  Eam (eam.hpp:25-56)                      Eam (host value type, u64 counts)
+  eam_distance (eam.hpp:61)                eam_distance           [GPU]
+  Eamc (eam.hpp:76-116)                    Eamc (device-resident) [GPU]
+  prefetch_priorities (policy.hpp:87)      prefetch_priorities    [GPU]
+  cache_priority (policy.hpp:93)           cache_priority         [GPU]
+  select_eviction_victim (policy.hpp:105)  select_eviction_victim [GPU]
+  TransferQueue (policy.hpp:55-80)         TransferQueue (host, as in the reference)
+  eamc_capacity_bound (eam.hpp:121)        eamc_capacity_bound
+  std::invalid_argument / out_of_range     ValueError / IndexError
+
+`Eam` stays a host value type like the reference's (record/accumulate/set
+are bookkeeping on one L x E matrix); the batched tracer that turns router
+top-k ids into count matrices is `trace_requests` (GPU kernel K1).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import (CAND_DTYPE, MATCH_DTYPE, NONE, SLOT_DTYPE, CountOverflowError, CudaError,
+                   EamcSnapshotError, check, lib, ptr)
+
+kEpsilon = 1e-4          # policy.hpp:22
+kMaxPriority = float("inf")  # policy.hpp:26
+kMatchWindow = 0.01      # policy.hpp:30
+
+
+class EamKind(enum.IntEnum):
+    iteration = 0
+    request = 1
+
+
+class Phase(enum.IntEnum):
+    prefill = 0
+    decode = 1
+
+
+@dataclasses.dataclass(frozen=True)
+class ModelShape:
+    """model.hpp:19-29"""
+    n_layers: int
+    n_experts_per_layer: int
+    top_k: int = 1
+
+    def validate(self) -> None:  # model.cpp:13-19
+        if self.n_layers < 1:
+            raise ValueError("ModelShape: n_layers must be >= 1")
+        if self.n_experts_per_layer < 1:
+            raise ValueError("ModelShape: n_experts_per_layer must be >= 1")
+        if self.top_k < 1 or self.top_k > self.n_experts_per_layer:
+            raise ValueError("ModelShape: top_k must be in [1, n_experts_per_layer]")
+
+    def total_experts(self) -> int:
+        return self.n_layers * self.n_experts_per_layer
+
+    def c(self) -> _lib.moe_shape:
+        return _lib.moe_shape(self.n_layers, self.n_experts_per_layer, self.top_k)
+
+
+@dataclasses.dataclass(frozen=True, order=True)
+class ExpertId:
+    """model.hpp:33-41 (lexicographic order is the tie-breaker everywhere)"""
+    layer_idx: int = 0
+    expert_idx: int = 0
+
+    def flat(self, shape: ModelShape) -> int:
+        return self.layer_idx * shape.n_experts_per_layer + self.expert_idx
+
+
+@dataclasses.dataclass
+class RoutingEvent:
+    """model.hpp:50-54: assignments are (expert_idx, token_count) pairs."""
+    layer_idx: int
+    assignments: List[Tuple[int, int]]
+
+
+class Eam:
+    """Expert Activation Matrix (eam.hpp:25-56): L x E uint64 counts."""
+
+    def __init__(self, shape: ModelShape, kind: EamKind = EamKind.request,
+                 phase: Phase = Phase.decode, counts=None):
+        shape.validate()
+        self.shape = shape
+        self.kind = EamKind(kind)
+        self.phase = Phase(phase)
+        if counts is None:
+            self.counts = np.zeros((shape.n_layers, shape.n_experts_per_layer), np.uint64)
+        else:
+            self.counts = np.array(counts, dtype=np.uint64).reshape(
+                shape.n_layers, shape.n_experts_per_layer)
+
+    def at(self, layer: int, expert: int) -> int:
+        return int(self.counts[layer, expert])
+
+    def row_sum(self, layer: int) -> int:
+        return int(self.counts[layer].sum())
+
+    def row(self, layer: int) -> np.ndarray:
+        return self.counts[layer]
+
+    def set(self, layer: int, expert: int, count: int) -> None:  # eam.cpp:64-68
+        if not (0 <= layer < self.shape.n_layers and 0 <= expert < self.shape.n_experts_per_layer):
+            raise IndexError("Eam::set: index out of range")
+        self.counts[layer, expert] = count
+
+    def record(self, event: RoutingEvent) -> None:
+        """eam.cpp:41-52: validate every index, then add (no partial writes)."""
+        if not 0 <= event.layer_idx < self.shape.n_layers:
+            raise IndexError("Eam::record: layer index out of range")
+        for e, _ in event.assignments:
+            if not 0 <= e < self.shape.n_experts_per_layer:
+                raise IndexError("Eam::record: expert index out of range")
+        for e, t in event.assignments:
+            self.counts[event.layer_idx, e] += np.uint64(t)
+
+    def accumulate(self, other: "Eam") -> None:  # eam.cpp:54-60
+        if self.shape != other.shape:
+            raise ValueError("Eam::accumulate: shape mismatch")
+        if self.phase != other.phase:
+            raise ValueError("Eam::accumulate: phase mismatch")
+        self.counts += other.counts
+
+    def reset(self) -> None:
+        self.counts[:] = 0
+
+    def copy(self) -> "Eam":
+        return Eam(self.shape, self.kind, self.phase, self.counts.copy())
+
+    def __eq__(self, other) -> bool:  # eam.hpp:49 (defaulted ==)
+        return (isinstance(other, Eam) and self.shape == other.shape and self.kind == other.kind
+                and self.phase == other.phase and np.array_equal(self.counts, other.counts))
+
+    def _buf(self) -> np.ndarray:
+        return np.ascontiguousarray(self.counts, np.uint64)
+
+
+def eam_distance(a: Eam, b: Eam) -> float:
+    """eam.cpp:91-104, evaluated on the GPU."""
+    if a.shape != b.shape:
+        raise ValueError("eam_distance: shape mismatch")
+    out = C.c_double()
+    sh = a.shape.c()
+    check(lib.moe_eam_distance(C.byref(sh), ptr(a._buf()), ptr(b._buf()), C.byref(out)))
+    return out.value
+
+
+@dataclasses.dataclass
+class EamcMatch:
+    """eam.hpp:67-71"""
+    index: int
+    seq: int
+    distance: float
+
+
+class Eamc:
+    """Fixed-capacity, device-resident collection (eam.hpp:76-116)."""
+
+    def __init__(self, shape: ModelShape, phase: Phase = Phase.decode, capacity: int = 1,
+                 device: int = 0, count_bytes: int = 0, _handle=None):
+        self.shape = shape
+        self._h = C.c_void_p()
+        if _handle is not None:
+            self._h = _handle
+        else:
+            sh = shape.c()
+            check(lib.moe_eamc_create(C.byref(sh), int(phase), capacity, count_bytes, device,
+                                      C.byref(self._h)))
+        self.device = device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.moe_eamc_destroy(h)
+            self._h = C.c_void_p()
+
+    # -- accessors (eam.hpp:80-87) -------------------------------------
+    def _info(self):
+        sh = _lib.moe_shape()
+        ph = C.c_int()
+        cap = C.c_uint64()
+        size = C.c_uint64()
+        nxt = C.c_uint64()
+        cb = C.c_int()
+        check(lib.moe_eamc_info(self._h, C.byref(sh), C.byref(ph), C.byref(cap), C.byref(size),
+                                C.byref(nxt), C.byref(cb)))
+        return sh, ph.value, cap.value, size.value, nxt.value, cb.value
+
+    def phase(self) -> Phase:
+        return Phase(self._info()[1])
+
+    def capacity(self) -> int:
+        return self._info()[2]
+
+    def size(self) -> int:
+        return self._info()[3]
+
+    def empty(self) -> bool:
+        return self.size() == 0
+
+    def next_seq(self) -> int:
+        return self._info()[4]
+
+    def count_bytes(self) -> int:
+        return self._info()[5]
+
+    def entry(self, index: int) -> Eam:
+        out = np.zeros((self.shape.n_layers, self.shape.n_experts_per_layer), np.uint64)
+        seq = C.c_uint64()
+        check(lib.moe_eamc_entry(self._h, index, ptr(out), C.byref(seq)))
+        return Eam(self.shape, EamKind.request, self.phase(), out)
+
+    def entry_seq(self, index: int) -> int:
+        seq = C.c_uint64()
+        check(lib.moe_eamc_entry(self._h, index, None, C.byref(seq)))
+        return seq.value
+
+    # -- construction ---------------------------------------------------
+    def insert(self, eam: Eam) -> Optional[Eam]:
+        """eam.cpp:152-178: returns the evicted entry when full."""
+        if eam.shape != self.shape:
+            raise ValueError("Eamc::insert: shape mismatch")
+        slot = C.c_int64()
+        ev = np.zeros((self.shape.n_layers, self.shape.n_experts_per_layer), np.uint64)
+        check(lib.moe_eamc_insert(self._h, ptr(eam._buf()), int(eam.kind), int(eam.phase),
+                                  C.byref(slot), ptr(ev)))
+        if slot.value < 0:
+            return None
+        return Eam(self.shape, EamKind.request, self.phase(), ev)
+
+    def build(self, counts: np.ndarray) -> np.ndarray:
+        """Batched construction: n sequential inserts; returns evicted slots (-1 = appended)."""
+        counts = np.ascontiguousarray(counts, np.uint64)
+        n = counts.shape[0]
+        slots = np.zeros(max(n, 1), np.int64)
+        check(lib.moe_eamc_build(self._h, ptr(counts), n, ptr(slots)))
+        return slots[:n]
+
+    def append(self, counts: np.ndarray, seqs: np.ndarray) -> None:
+        """Bulk load with caller-assigned seqs (snapshot / shard semantics)."""
+        seqs = np.ascontiguousarray(seqs, np.uint64)
+        counts = np.ascontiguousarray(counts)
+        if counts.dtype == np.uint64:
+            check(lib.moe_eamc_append(self._h, ptr(counts), ptr(seqs), len(seqs)))
+        else:
+            check(lib.moe_eamc_append_packed(self._h, ptr(counts), counts.dtype.itemsize,
+                                             ptr(seqs), len(seqs)))
+
+    # -- matching ---------------------------------------------------------
+    def match_batch(self, probes: np.ndarray) -> np.ndarray:
+        """Eamc::match over [Q][L][E] probes -> structured array (index, seq, distance)."""
+        probes = np.ascontiguousarray(probes, np.uint64)
+        if probes.shape[1:] != (self.shape.n_layers, self.shape.n_experts_per_layer):
+            raise ValueError("Eamc: probe shape mismatch")
+        Q = probes.shape[0]
+        out = np.zeros(max(Q, 1), MATCH_DTYPE)
+        check(lib.moe_eamc_match(self._h, ptr(probes), Q, ptr(out), None))
+        return out[:Q]
+
+    def match(self, probe: Eam) -> Optional[EamcMatch]:
+        """eam.cpp:118-129"""
+        if probe.shape != self.shape:
+            raise ValueError("Eamc: probe shape mismatch")
+        m = self.match_batch(probe.counts[None])[0]
+        if int(m["index"]) == NONE:
+            return None
+        return EamcMatch(int(m["index"]), int(m["seq"]), float(m["distance"]))
+
+    def match_within(self, probe: Eam, window: float) -> List[EamcMatch]:
+        """eam.cpp:131-150"""
+        if probe.shape != self.shape:
+            raise ValueError("Eamc: probe shape mismatch")
+        cap = max(self.size(), 1)
+        out = np.zeros(cap, MATCH_DTYPE)
+        n = C.c_uint64()
+        check(lib.moe_eamc_match_within(self._h, ptr(probe._buf()), window, ptr(out), cap,
+                                        C.byref(n)))
+        return [EamcMatch(int(m["index"]), int(m["seq"]), float(m["distance"]))
+                for m in out[:n.value]]
+
+    # -- snapshots (eam.cpp:184-256) ------------------------------------
+    def save(self, path: str) -> None:
+        check(lib.moe_eamc_save(self._h, str(path).encode()))
+
+    @staticmethod
+    def load(path: str, expected: Optional[ModelShape] = None, device: int = 0) -> "Eamc":
+        h = C.c_void_p()
+        sh = expected.c() if expected is not None else None
+        check(lib.moe_eamc_load(str(path).encode(), C.byref(sh) if sh is not None else None,
+                                device, C.byref(h)))
+        s = _lib.moe_shape()
+        check(lib.moe_eamc_info(h, C.byref(s), None, None, None, None, None))
+        return Eamc(ModelShape(s.n_layers, s.n_experts_per_layer, s.top_k), _handle=h,
+                    device=device)
+
+
+@dataclasses.dataclass
+class PrefetchCandidate:
+    """policy.hpp:46-50"""
+    expert: ExpertId
+    priority: float
+
+
+def _cands(arr: np.ndarray) -> List[PrefetchCandidate]:
+    return [PrefetchCandidate(ExpertId(int(c["layer_idx"]), int(c["expert_idx"])),
+                              float(c["priority"])) for c in arr]
+
+
+def prefetch_priorities(cur_eam: Eam, eamc: Eamc, current_layer: int,
+                        apply_floor_filter: bool = False) -> List[PrefetchCandidate]:
+    """policy.cpp:88-126 (+ the engine floor filter, engine.cpp:663-668)."""
+    if current_layer < 0:
+        raise IndexError("prefetch_priorities: current_layer out of range")
+    cap = max(cur_eam.shape.total_experts(), 1)
+    out = np.zeros(cap, CAND_DTYPE)
+    n = C.c_uint64()
+    check(lib.moe_prefetch_priorities(eamc._h, ptr(cur_eam._buf()), current_layer,
+                                      int(apply_floor_filter), ptr(out), cap, C.byref(n)))
+    return _cands(out[:n.value])
+
+
+def prefetch_order(cur_eam: Eam, eamc: Eamc, current_layer: int,
+                   apply_floor_filter: bool = True) -> np.ndarray:
+    """Same as prefetch_priorities, as a structured array (layer, expert, priority)."""
+    cap = max(cur_eam.shape.total_experts(), 1)
+    out = np.zeros(cap, CAND_DTYPE)
+    n = C.c_uint64()
+    check(lib.moe_prefetch_priorities(eamc._h, ptr(cur_eam._buf()), current_layer,
+                                      int(apply_floor_filter), ptr(out), cap, C.byref(n)))
+    return out[:n.value]
+
+
+def cache_priority(request_eam: Eam, expert: ExpertId) -> float:
+    """policy.cpp:128-141"""
+    out = C.c_double()
+    sh = request_eam.shape.c()
+    if expert.layer_idx < 0 or expert.expert_idx < 0:
+        raise IndexError("cache_priority: expert out of range")
+    check(lib.moe_cache_priority(C.byref(sh), ptr(request_eam._buf()), expert.layer_idx,
+                                 expert.expert_idx, C.byref(out)))
+    return out.value
+
+
+@dataclasses.dataclass
+class SlotView:
+    """policy.hpp:96-101"""
+    slot: int
+    occupant: ExpertId
+    prefetch_protected: bool = False
+    pinned: bool = False
+
+
+def _slot_array(slots: Sequence[SlotView]) -> np.ndarray:
+    a = np.zeros(max(len(slots), 1), SLOT_DTYPE)
+    for i, s in enumerate(slots):
+        a[i]["slot"] = s.slot
+        a[i]["layer_idx"] = s.occupant.layer_idx
+        a[i]["expert_idx"] = s.occupant.expert_idx
+        a[i]["prefetch_protected"] = int(s.prefetch_protected)
+        a[i]["pinned"] = int(s.pinned)
+    return a
+
+
+def select_eviction_victim(slots: Sequence[SlotView], request_eam: Eam) -> Optional[int]:
+    """policy.cpp:143-159"""
+    a = _slot_array(slots)
+    v = C.c_int64()
+    sh = request_eam.shape.c()
+    check(lib.moe_select_eviction_victim(C.byref(sh), ptr(request_eam._buf()), ptr(a), len(slots),
+                                         C.byref(v)))
+    return None if v.value < 0 else int(v.value)
+
+
+def decide(cur_eam: Eam, eamc: Eamc, current_layer: int, request_eam: Eam,
+           slots: Sequence[SlotView]) -> Tuple[np.ndarray, Optional[int]]:
+    """Fused K5+K6: floor-filtered prefetch order and eviction victim in one launch."""
+    a = _slot_array(slots)
+    cap = max(cur_eam.shape.total_experts(), 1)
+    out = np.zeros(cap, CAND_DTYPE)
+    n = C.c_uint64()
+    v = C.c_int64()
+    check(lib.moe_decide(eamc._h, ptr(cur_eam._buf()), current_layer, ptr(request_eam._buf()),
+                         ptr(a), len(slots), ptr(out), cap, C.byref(n), C.byref(v)))
+    return out[:n.value], (None if v.value < 0 else int(v.value))
+
+
+def eamc_capacity_bound(shape: ModelShape, similarity: float) -> int:
+    """eam.cpp:258-268"""
+    out = C.c_uint64()
+    sh = shape.c()
+    check(lib.moe_eamc_capacity_bound(C.byref(sh), similarity, C.byref(out)))
+    return out.value
+
+
+def trace_requests(shape: ModelShape, topk_idx: np.ndarray, offsets: np.ndarray,
+                   counts: Optional[np.ndarray] = None) -> np.ndarray:
+    """K1: router top-k ids [T][L][k] -> per-request L x E counts (accumulated into
+    `counts` when given).  All-or-nothing like Eam::record (eam.cpp:41-52)."""
+    topk_idx = np.ascontiguousarray(topk_idx)
+    if topk_idx.dtype not in (np.uint8, np.uint16, np.uint32, np.int32):
+        raise ValueError("topk_idx must be uint8/uint16/uint32/int32")
+    offsets = np.ascontiguousarray(offsets, np.uint64)
+    R = len(offsets) - 1
+    if counts is None:
+        counts = np.zeros((max(R, 0), shape.n_layers, shape.n_experts_per_layer), np.uint64)
+    counts = np.ascontiguousarray(counts, np.uint64)
+    sh = shape.c()
+    T = topk_idx.shape[0] if topk_idx.ndim else 0
+    check(lib.moe_eam_trace(C.byref(sh), ptr(topk_idx), topk_idx.dtype.itemsize, T, ptr(offsets),
+                            R, ptr(counts)))
+    return counts
+
+
+class TransferQueue:
+    """policy.cpp:43-86.  Host-side by design: a priority
+    queue keyed by expert with overwrite-on-resubmit; pop order is priority
+    descending, (layer, expert) ascending."""
+
+    def __init__(self):
+        self._by_expert = {}
+
+    def submit(self, expert: ExpertId, priority: float) -> None:
+        self._by_expert[expert] = priority
+
+    def cancel(self, expert: ExpertId) -> bool:
+        return self._by_expert.pop(expert, None) is not None
+
+    def cancel_all(self) -> int:
+        n = len(self._by_expert)
+        self._by_expert.clear()
+        return n
+
+    def _order(self):
+        return sorted(self._by_expert.items(), key=lambda kv: (-kv[1], kv[0]))
+
+    def peek(self) -> Optional[PrefetchCandidate]:
+        if not self._by_expert:
+            return None
+        e, p = self._order()[0]
+        return PrefetchCandidate(e, p)
+
+    def pop(self) -> Optional[PrefetchCandidate]:
+        top = self.peek()
+        if top is not None:
+            del self._by_expert[top.expert]
+        return top
+
+    def contains(self, expert: ExpertId) -> bool:
+        return expert in self._by_expert
+
+    def priority_of(self, expert: ExpertId) -> Optional[float]:
+        return self._by_expert.get(expert)
+
+    def size(self) -> int:
+        return len(self._by_expert)
+
+    def empty(self) -> bool:
+        return not self._by_expert
+
+    def __iter__(self):
+        for e, p in self._order():
+            yield PrefetchCandidate(e, p)

@@ -1,0 +1,438 @@
+"""GPU parity: libmoe_eamc (sm_100a kernels, through its C ABI) vs the oracle.
+
+Bar (BASELINE.json north_star): bit-exact counts, match indices / seqs,
+distances, window sets, prefetch order and victims.  Distances are compared
+BITWISE (stricter than the 1e-5 relative the north star allows), because
+the device path reproduces the reference's fp64 operation order on exact
+integer sums ("exactness contract").
+"""
+import numpy as np
+import pytest
+
+from oracle import Workload
+
+pytestmark = pytest.mark.gpu
+
+
+def seqs_of(n):
+    return np.arange(n, dtype=np.uint64)
+
+
+def filled(m, L, E, entries, capacity=None, top_k=1, count_bytes=0):
+    e = m.Eamc(m.ModelShape(L, E, top_k), m.Phase.decode, capacity or max(len(entries), 1),
+               count_bytes=count_bytes)
+    if len(entries):
+        slots = e.build(entries)
+        assert (slots == -1).all()
+    return e
+
+
+def check_match(m, orc, e, entries, seqs, probes):
+    got = e.match_batch(probes)
+    idx, seq, d, found = orc.match(entries, seqs, probes)
+    assert found.all()
+    assert np.array_equal(got["index"], idx), np.nonzero(got["index"] != idx)
+    assert np.array_equal(got["seq"], seq)
+    assert np.array_equal(got["distance"], d)  # bitwise
+    return got
+
+
+# ---------------------------------------------------------------- distance
+def test_distance_golden(m, golden):
+    g = golden("distance.npz")
+    oa = 0
+    for i, (L, E) in enumerate(g["shapes"]):
+        n = int(L) * int(E)
+        s = m.ModelShape(int(L), int(E))
+        a = m.Eam(s, counts=g["a"][oa:oa + n])
+        b = m.Eam(s, counts=g["b"][oa:oa + n])
+        oa += n
+        assert m.eam_distance(a, b) == g["d"][i]
+    with pytest.raises(ValueError):
+        m.eam_distance(m.Eam(m.ModelShape(1, 2)), m.Eam(m.ModelShape(2, 2)))
+
+
+# ------------------------------------------------------------------- match
+def test_empty_collection_matches_nothing(m):
+    e = m.Eamc(m.ModelShape(2, 4), m.Phase.decode, 200)
+    assert e.match(m.Eam(m.ModelShape(2, 4), counts=np.ones((2, 4)))) is None
+    assert e.match_within(m.Eam(m.ModelShape(2, 4)), 0.01) == []
+    with pytest.raises(ValueError):
+        e.match(m.Eam(m.ModelShape(3, 4)))
+
+
+def test_bench_checksums_golden(m, golden):
+    for P, L, E, Q, seed, ck in golden("bench_checksum.npz")["rows"]:
+        P, L, E, Q, seed = int(P), int(L), int(E), int(Q), int(seed)
+        fam = m.gen_bench_family(seed, L, E, P + Q)
+        e = filled(m, L, E, fam[:P])
+        got = e.match_batch(fam[P:])
+        assert int((got["index"] + 1).sum()) == int(ck)
+
+
+def test_match_golden_mix(m, golden):
+    g = golden("match_mix.npz")
+    P, L, E, Q, seed = (int(x) for x in g["params"])
+    fam = m.gen_bench_family(seed, L, E, P + Q)
+    e = filled(m, L, E, fam[:P])
+    got = e.match_batch(fam[P:])
+    assert np.array_equal(got["index"], g["idx"]) and np.array_equal(got["seq"], g["seq"])
+    assert np.array_equal(got["distance"], g["d"])
+    o = 0
+    for q in range(len(g["w_n"])):
+        n = int(g["w_n"][q])
+        w = e.match_within(m.Eam(m.ModelShape(L, E), counts=fam[P + q]), 0.01)
+        assert [x.index for x in w] == list(g["w_idx"][o:o + n])
+        assert [x.seq for x in w] == list(g["w_seq"][o:o + n])
+        assert [x.distance for x in w] == list(g["w_d"][o:o + n])
+        o += n
+
+
+@pytest.mark.parametrize("L,E,P,Q,seed", [
+    (12, 128, 2000, 96, 55),    # Switch shape (SW), streaming + batch tiles
+    (32, 8, 300, 200, 7),       # Mixtral shape (MIX)
+    (59, 160, 300, 12, 9),      # DeepSeek-V2 shape (DS)
+    (24, 128, 500, 20, 3),      # NLLB shape (NL)
+    (3, 5, 77, 33, 1),          # odd tiny shape
+    (1, 1, 10, 5, 2),
+])
+def test_match_bench_family(m, orc, L, E, P, Q, seed):
+    fam = m.gen_bench_family(seed, L, E, P + Q)
+    e = filled(m, L, E, fam[:P])
+    check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
+
+
+@pytest.mark.parametrize("Q", [1, 2, 3, 4, 7, 8, 9, 64, 65, 130])
+def test_match_probe_batch_sizes(m, orc, Q):
+    L, E, P = 12, 128, 700
+    fam = m.gen_bench_family(11, L, E, P + Q)
+    e = filled(m, L, E, fam[:P])
+    check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
+
+
+def test_match_random_eam_family(m, orc):
+    """random_eam family (test_eam.cpp:58-66): dense Bernoulli(0.4) rows."""
+    rng = orc.rng(23)
+    ents = np.stack([orc.random_eam(rng, 2, 4) for _ in range(100)])
+    probes = np.stack([orc.random_eam(rng, 2, 4) for _ in range(20)])
+    e = filled(m, 2, 4, ents, capacity=200)
+    check_match(m, orc, e, ents, seqs_of(100), probes)
+    # a contained entry matches itself at distance 0 (test_eam.cpp:257-261)
+    r = e.match(m.Eam(m.ModelShape(2, 4), counts=ents[42]))
+    assert r.distance == 0.0
+    first = min(i for i in range(100) if np.array_equal(ents[i], ents[42]))
+    assert r.index == first
+
+
+def test_match_ties_and_duplicates(m, orc):
+    """Many exact ties: the oldest seq must win (eam.cpp:123-124); exceeds the
+    candidate bucket and exercises the exact fallback pass."""
+    L, E = 12, 128
+    base = m.gen_bench_family(5, L, E, 40)
+    ents = np.concatenate([np.repeat(base[:3], 150, axis=0), base[3:30]])
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(len(ents))
+    ents = ents[perm]
+    e = filled(m, L, E, ents)
+    probes = np.concatenate([base[:3], base[30:36], base[:3] * 2])  # scaled rows: distance 0
+    check_match(m, orc, e, ents, seqs_of(len(ents)), probes)
+
+
+def test_match_zero_rows(m, orc):
+    L, E, P = 6, 16, 400
+    fam = m.gen_bench_family(8, L, E, P + 40).copy()
+    rng = np.random.default_rng(1)
+    z = rng.random((P + 40, L)) < 0.3
+    fam[z] = 0
+    fam[P + 35:] = 0  # all-zero probes
+    fam[:5] = 0       # all-zero entries
+    e = filled(m, L, E, fam[:P])
+    check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
+
+
+def test_match_wide_counts(m, orc):
+    """Counts above 255 widen the device collection to 2-byte storage."""
+    L, E, P = 4, 32, 300
+    fam = m.gen_bench_family(21, L, E, P + 30).copy()
+    e = filled(m, L, E, fam[:P])
+    assert e.count_bytes() == 1
+    probes = fam[P:] * 37  # up to 1184 > 255
+    check_match(m, orc, e, fam[:P], seqs_of(P), probes)
+    assert e.count_bytes() == 2
+    big = fam[:P].copy()
+    big[::7] *= 1500
+    e2 = filled(m, L, E, big)
+    check_match(m, orc, e2, big, seqs_of(P), fam[P:])
+    with pytest.raises(m.CountOverflowError):
+        e2.match_batch(fam[P:P + 1] * 70000)
+
+
+def test_match_f2_workload(m, orc):
+    """Realistic grouped/skewed request EAMs (F2) and iteration probes."""
+    w = Workload(12, 64, 1, seed=1001)
+    ents = orc.request_eams(w, 300)
+    probes = np.stack([orc.iteration_probe(w, 500 + i, 1 + i % 8, i % 12) for i in range(40)])
+    e = filled(m, 12, 64, ents)
+    check_match(m, orc, e, ents, seqs_of(300), probes)
+
+
+def test_match_large_collection(m, orc):
+    """P = 100k at the Switch shape (> one wave of tiles on every SM)."""
+    L, E, P, Q = 12, 128, 100_000, 3
+    fam = m.gen_bench_family(55, L, E, P + Q, dtype=np.uint8)
+    e = m.Eamc(m.ModelShape(L, E), m.Phase.decode, P)
+    e.append(fam[:P], seqs_of(P))
+    got = e.match_batch(fam[P:].astype(np.uint64))
+    idx, seq, d, _ = orc.match(fam[:P].astype(np.uint64), seqs_of(P), fam[P:].astype(np.uint64))
+    assert np.array_equal(got["index"], idx) and np.array_equal(got["distance"], d)
+
+
+def test_match_device_api(m, orc):
+    import ctypes as C
+    import torch
+    from paper_2401_14361_b200 import _lib
+    L, E, P, Q = 12, 128, 1000, 50
+    fam = m.gen_bench_family(3, L, E, P + Q)
+    e = filled(m, L, E, fam[:P])
+    for dt in (torch.uint8, torch.int16, torch.int64):
+        pr = torch.from_numpy(fam[P:].astype(np.int64)).to(dt).cuda()
+        out = torch.zeros((Q, 3), dtype=torch.float64, device="cuda")  # 24 B per moe_match
+        stream = torch.cuda.current_stream().cuda_stream
+        _lib.check(_lib.lib.moe_eamc_match_device(e._h, pr.data_ptr(), pr.element_size(), Q,
+                                                  out.data_ptr(), C.c_void_p(stream)))
+        torch.cuda.synchronize()
+        res = out.cpu().numpy().view(np.uint8).reshape(Q, 24).copy().view(_lib.MATCH_DTYPE)[:, 0]
+        idx, seq, d, _ = orc.match(fam[:P], seqs_of(P), fam[P:])
+        assert np.array_equal(res["index"], idx) and np.array_equal(res["distance"], d)
+
+
+# ------------------------------------------------------------ construction
+def test_insert_replay_golden(m, golden):
+    g = golden("insert_replay.npz")
+    s = m.ModelShape(2, 4)
+    e = m.Eamc(s, m.Phase.decode, 10)
+    slots = e.build(g["eams"])
+    assert np.array_equal(slots, g["slots"])
+    for i in range(e.size()):
+        assert np.array_equal(e.entry(i).counts, g["entries"][i])
+        assert e.entry_seq(i) == g["seqs"][i]
+    # one-at-a-time inserts return the evicted Eam (eam.cpp:175-177)
+    e1 = m.Eamc(m.ModelShape(1, 4), m.Phase.decode, 3)
+    ex = g["ex"]
+    for x in ex[:3]:
+        assert e1.insert(m.Eam(m.ModelShape(1, 4), counts=x)) is None
+    ev = e1.insert(m.Eam(m.ModelShape(1, 4), counts=ex[3]))
+    assert ev is not None and np.array_equal(ev.counts, ex[2])
+    assert e1.size() == 3
+    assert e1.match(m.Eam(m.ModelShape(1, 4), counts=ex[3])).distance == 0.0
+
+
+def test_insert_validation(m):
+    s = m.ModelShape(1, 2)
+    e = m.Eamc(s, m.Phase.decode, 2)
+    with pytest.raises(ValueError):
+        e.insert(m.Eam(s, m.EamKind.iteration, m.Phase.decode))
+    with pytest.raises(ValueError):
+        e.insert(m.Eam(s, m.EamKind.request, m.Phase.prefill))
+    with pytest.raises(ValueError):
+        e.insert(m.Eam(m.ModelShape(2, 2)))
+
+
+@pytest.mark.parametrize("L,E,cap,n,seed", [(24, 128, 50, 400, 3), (12, 128, 200, 900, 55),
+                                            (2, 4, 10, 600, 1)])
+def test_build_replay_vs_oracle(m, orc, L, E, cap, n, seed):
+    eams = m.gen_bench_family(seed, L, E, n)
+    e = m.Eamc(m.ModelShape(L, E), m.Phase.decode, cap)
+    slots = e.build(eams)
+    ent, sq, want = orc.insert_replay(L, E, cap, eams)
+    assert np.array_equal(slots, want)
+    for i in range(cap):
+        assert e.entry_seq(i) == sq[i]
+    assert np.array_equal(e.entry(cap // 2).counts, ent[cap // 2])
+
+
+def test_build_replay_f2_nllb_shape(m, orc):
+    w = Workload(24, 128, 2, seed=1234)
+    eams = orc.request_eams(w, 260)
+    e = m.Eamc(m.ModelShape(24, 128, 2), m.Phase.decode, 60)
+    slots = e.build(eams)
+    _, _, want = orc.insert_replay(24, 128, 60, eams)
+    assert np.array_equal(slots, want)
+
+
+def test_build_with_duplicates(m, orc):
+    """Tied victims (duplicate entries) resolve to the oldest seq."""
+    base = m.gen_bench_family(17, 4, 16, 6)
+    eams = np.concatenate([np.repeat(base[:2], 40, axis=0), base[2:], base[:2]])
+    e = m.Eamc(m.ModelShape(4, 16), m.Phase.decode, 70)
+    slots = e.build(eams)
+    _, _, want = orc.insert_replay(4, 16, 70, eams)
+    assert np.array_equal(slots, want)
+
+
+def test_snapshot_round_trip(m, tmp_path):
+    s = m.ModelShape(3, 6, 1)
+    empty = m.Eamc(s, m.Phase.prefill, 5)
+    p = str(tmp_path / "snap.json")
+    empty.save(p)
+    back = m.Eamc.load(p)
+    assert back.size() == 0 and back.capacity() == 5 and back.phase() == m.Phase.prefill
+    full = m.Eamc(s, m.Phase.decode, 64)
+    fam = m.gen_bench_family(41, 3, 6, 101)
+    full.build(fam[:100])
+    full.save(p)
+    b1 = m.Eamc.load(p, s)
+    assert b1.size() == full.size() and b1.next_seq() == full.next_seq()
+    for i in range(b1.size()):
+        assert np.array_equal(b1.entry(i).counts, full.entry(i).counts)
+        assert b1.entry_seq(i) == full.entry_seq(i)
+    b2 = m.Eamc.load(p, s)
+    x = m.Eam(s, counts=fam[100])
+    assert b1.insert(x) == b2.insert(x)
+    with pytest.raises(m.EamcSnapshotError):
+        m.Eamc.load(p, m.ModelShape(4, 6, 1))
+    open(p, "w").write('{"version": 99}\n')
+    with pytest.raises(m.EamcSnapshotError):
+        m.Eamc.load(p)
+    open(p, "w").write("not json\n")
+    with pytest.raises(m.EamcSnapshotError):
+        m.Eamc.load(p)
+
+
+# ---------------------------------------------------------------- policy
+def test_prefetch_worked_example(m, golden):
+    g = golden("prefetch.npz")
+    s = m.ModelShape(4, 2)
+    e = m.Eamc(s, m.Phase.decode, 4)
+    e.insert(m.Eam(s, counts=[[1, 0], [1, 0], [2, 1], [0, 3]]))
+    cur = m.Eam(s, m.EamKind.iteration, counts=[[1, 0], [1, 0], [0, 0], [0, 0]])
+    out = m.prefetch_priorities(cur, e, 1)
+    assert [c.expert.layer_idx for c in out] == list(g["worked_l"])
+    assert [c.expert.expert_idx for c in out] == list(g["worked_e"])
+    assert [c.priority for c in out] == list(g["worked_p"])
+    assert out[0].expert == m.ExpertId(2, 0) and abs(out[0].priority - 0.500075) < 1e-12
+    with pytest.raises(IndexError):
+        m.prefetch_priorities(cur, e, 4)
+    assert m.prefetch_priorities(cur, m.Eamc(s, m.Phase.decode, 2), 0) == []
+
+
+def test_prefetch_zero_rows_floor(m):
+    """test_policy.cpp:67-82: zero rows -> epsilon floor, ties in ExpertId order."""
+    s = m.ModelShape(3, 2)
+    e = m.Eamc(s, m.Phase.decode, 2)
+    e.insert(m.Eam(s, counts=[[1, 0], [0, 0], [0, 0]]))
+    cur = m.Eam(s, m.EamKind.iteration, counts=[[1, 0], [0, 0], [0, 0]])
+    out = m.prefetch_priorities(cur, e, 0)
+    assert len(out) == 4
+    assert out[0].expert == m.ExpertId(1, 0) and out[1].expert == m.ExpertId(1, 1)
+    assert m.prefetch_priorities(cur, e, 0, apply_floor_filter=True) == []
+
+
+def test_prefetch_f2_golden(m, golden):
+    g = golden("prefetch.npz")
+    s = m.ModelShape(32, 8, 2)
+    e = m.Eamc(s, m.Phase.decode, 60)
+    e.build(g["f2_entries"])
+    o = 0
+    for i in range(len(g["f2_n"])):
+        n = int(g["f2_n"][i])
+        cur = m.Eam(s, m.EamKind.iteration, counts=g["f2_probes"][i])
+        out = m.prefetch_order(cur, e, int(g["f2_layers"][i]), bool(g["f2_filter"][i]))
+        assert np.array_equal(out["layer_idx"], g["f2_l"][o:o + n])
+        assert np.array_equal(out["expert_idx"], g["f2_e"][o:o + n])
+        assert np.array_equal(out["priority"], g["f2_p"][o:o + n])  # bitwise
+        o += n
+
+
+@pytest.mark.parametrize("L,E,P,seed", [(59, 160, 200, 5), (12, 128, 1000, 7), (24, 128, 300, 9)])
+def test_prefetch_vs_oracle(m, orc, L, E, P, seed):
+    w = Workload(L, E, min(6, E), n_groups=12, prompt_len=3, decode_len=4, batch_size=2,
+                 seed=seed)
+    ents = orc.request_eams(w, P)
+    s = m.ModelShape(L, E, min(6, E))
+    e = m.Eamc(s, m.Phase.decode, P)
+    e.build(ents)
+    for r, it, layer in [(900, 1, 0), (901, 2, L // 2), (902, 3, L - 2), (903, 4, L - 1)]:
+        pr = orc.iteration_probe(w, r, it, layer)
+        for flt in (True, False):
+            l, x, p = orc.prefetch(ents, seqs_of(P), pr, layer, flt)
+            out = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), e, layer, flt)
+            assert np.array_equal(out["layer_idx"], l)
+            assert np.array_equal(out["expert_idx"], x)
+            assert np.array_equal(out["priority"], p)
+
+
+def test_eviction_golden(m, golden):
+    g = golden("eviction.npz")
+    s = m.ModelShape(4, 8)
+    for req, v, want in zip(g["reqs"], g["views"], g["victims"]):
+        slots = [m.SlotView(int(v[0][i]), m.ExpertId(int(v[1][i]), int(v[2][i])), bool(v[3][i]),
+                            bool(v[4][i])) for i in range(v.shape[1])]
+        got = m.select_eviction_victim(slots, m.Eam(s, counts=req))
+        assert (got if got is not None else -1) == want
+    cs = m.ModelShape(3, 2)
+    req = m.Eam(cs, counts=g["cp_req"])
+    got = [m.cache_priority(req, m.ExpertId(0, 1)), m.cache_priority(req, m.ExpertId(1, 0)),
+           m.cache_priority(req, m.ExpertId(2, 1))]
+    assert got == list(g["cp"])
+    with pytest.raises(IndexError):
+        m.cache_priority(req, m.ExpertId(3, 0))
+    assert m.select_eviction_victim([], req) is None
+
+
+def test_fused_decide(m, orc):
+    """K5+K6 in one launch equals prefetch_priorities+filter and the victim."""
+    w = Workload(12, 64, 2, seed=31)
+    ents = orc.request_eams(w, 100)
+    s = m.ModelShape(12, 64, 2)
+    e = m.Eamc(s, m.Phase.decode, 100)
+    e.build(ents)
+    pr = orc.iteration_probe(w, 555, 2, 4)
+    req = orc.request_eams(w, 1, start=777)[0]
+    slots = [m.SlotView(i, m.ExpertId(i % 12, (7 * i) % 64), i % 5 == 0, i % 7 == 0)
+             for i in range(40)]
+    order, victim = m.decide(m.Eam(s, m.EamKind.iteration, counts=pr), e, 4, m.Eam(s, counts=req),
+                             slots)
+    l, x, p = orc.prefetch(ents, seqs_of(100), pr, 4, True)
+    assert np.array_equal(order["layer_idx"], l) and np.array_equal(order["priority"], p)
+    want = orc.select_victim(req, [v.slot for v in slots],
+                             [v.occupant.layer_idx for v in slots],
+                             [v.occupant.expert_idx for v in slots],
+                             [int(v.prefetch_protected) for v in slots],
+                             [int(v.pinned) for v in slots])
+    assert (victim if victim is not None else -1) == want
+
+
+# ---------------------------------------------------------------- tracing
+@pytest.mark.parametrize("name,w", [
+    ("mix", Workload(32, 8, 2, seed=99)),
+    ("ds", Workload(59, 160, 6, n_groups=8, prompt_len=40, decode_len=25, batch_size=2, seed=5)),
+])
+def test_trace_vs_oracle(m, orc, name, w):
+    p = w.params
+    picks, offs = [], [0]
+    for r in range(6):
+        _, pk = orc.trace_picks(w, r)
+        picks.append(pk)
+        offs.append(offs[-1] + pk.shape[0])
+    picks = np.concatenate(picks)
+    offs = np.array(offs, np.uint64)
+    rc, want = orc.trace(p["L"], p["E"], p["top_k"], picks, offs)
+    assert rc == 0
+    s = m.ModelShape(p["L"], p["E"], p["top_k"])
+    for dt in (np.uint8, np.uint16, np.uint32):
+        got = m.trace_requests(s, picks.astype(dt), offs)
+        assert np.array_equal(got, want)
+    # accumulate semantics (Eam::record adds)
+    base = np.ones_like(want)
+    got = m.trace_requests(s, picks.astype(np.uint8), offs, counts=base.copy())
+    assert np.array_equal(got, want + 1)
+
+
+def test_trace_all_or_nothing(m):
+    s = m.ModelShape(2, 4, 2)
+    picks = np.array([[[0, 1], [2, 3]], [[1, 2], [3, 9]]], np.uint8)
+    base = np.full((1, 2, 4), 5, np.uint64)
+    with pytest.raises(IndexError):
+        m.trace_requests(s, picks, np.array([0, 2], np.uint64), counts=base)
+    assert (base == 5).all()
