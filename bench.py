@@ -1,0 +1,464 @@
+#!/usr/bin/env python
+"""bench.py -- EAM-vs-EAMC distance evals/s on B200 (BASELINE.json `metric`).
+
+Default workload (BASELINE.json configs[1], "SW"): Switch-Transformers-base-128
+shape (L=12, E=128, top-1), an EAMC of P=10,000 entries per GPU matched
+against a 4,096-probe batch.  Inputs are the reference benchmark's own
+synthetic EAM family (bench.cpp:44-54, seed 55): the first P*N EAMs of the
+stream are the collection (rank r owns [r*P, (r+1)*P)), the next Q are the
+probes.  A step = one Eamc::match pass of the probe batch over the whole
+collection; at N>1 the collection is P-sharded and the per-shard argmins are
+merged over NCCL (all_gather + device lexicographic merge): weak scaling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EAM-vs-EAMC distance evals/sec + % HBM roofline at 1/2/4/8 B200"
+L, E, TOPK = 12, 128, 1
+P_PER_GPU, Q = 10_000, 4096
+SEED = 55
+STREAM_P, STREAM_Q = 1 << 20, 8   # SC streaming regime (P >= 1M), north-star HBM target
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def ncu_traffic(key):
+    """dram bytes/launch of the named kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = d.get(key, {})
+    return v.get("dram_bytes_per_launch")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_14361_b200 as m
+    from paper_2401_14361_b200 import _lib
+
+    rank, world, local = dist_env()
+    N = world
+    torch.cuda.set_device(local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+
+    def barrier():
+        if N > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- collection shard + probes (host-generated, reference bench stream)
+    P = P_PER_GPU
+    shard = m.gen_bench_family(SEED, L, E, P, skip=rank * P, dtype=np.uint8)
+    probes_u8 = m.gen_bench_family(SEED, L, E, Q, skip=N * P, dtype=np.uint8)
+    eamc = m.Eamc(m.ModelShape(L, E, TOPK), m.Phase.decode, P, device=local)
+    eamc.append(shard, np.arange(rank * P, (rank + 1) * P, dtype=np.uint64))
+    _lib.check(_lib.lib.moe_eamc_set_index_base(eamc._h, rank * P))
+
+    d_probes = torch.from_numpy(probes_u8).to(dev)
+    d_out = torch.empty((Q, 3), dtype=torch.float64, device=dev)      # moe_match[Q]
+    d_parts = torch.empty((N, Q, 3), dtype=torch.float64, device=dev)
+    d_final = torch.empty((Q, 3), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step_device():
+        _lib.check(_lib.lib.moe_eamc_match_device(eamc._h, d_probes.data_ptr(), 1, Q,
+                                                  d_out.data_ptr(), sp))
+        if N > 1:
+            dist.all_gather_into_tensor(d_parts, d_out)
+            _lib.check(_lib.lib.moe_match_merge_device(d_parts.data_ptr(), N, Q,
+                                                       d_final.data_ptr(), sp))
+            return d_final
+        return d_out
+
+    # warmup
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+
+    # ---- timed region: K steps, L2 flushed between steps (outside the events)
+    clocks = ClockSampler(local)
+    time.sleep(0.05)
+    _lib.check(_lib.lib.moe_eamc_set_profiling(eamc._h, 1))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        step_device()
+        evs[i][1].record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms_steps = [a.elapsed_time(b) for a, b in evs]
+    kms = (C.c_double * 3)()
+    kcalls = (C.c_uint64 * 3)()
+    _lib.check(_lib.lib.moe_eamc_kernel_times(eamc._h, kms, kcalls))
+    _lib.check(_lib.lib.moe_eamc_set_profiling(eamc._h, 0))
+    t_total = torch.tensor([sum(ms_steps)], dtype=torch.float64, device=dev)
+    if N > 1:
+        dist.all_reduce(t_total, op=dist.ReduceOp.MAX)
+    t_ms = float(t_total.item())
+    evals_per_step = P * N * Q
+    value = evals_per_step * args.steps / (t_ms / 1e3)
+    gpu_launches = int(kcalls[0] + kcalls[1] + kcalls[2]) + (args.steps if N > 1 else 0)
+
+    # result of the last step, for the parity sample
+    res = step_device().cpu().numpy().view(np.uint8).reshape(Q, 24).copy().view(
+        _lib.MATCH_DTYPE)[:, 0]
+
+    # ---- roofline of the dominant kernel (screen pass), live CUDA events
+    hbm_peak, tf_peak, peak_kind = load_peaks()
+    screen_ms = kms[1] / max(kcalls[1], 1)
+    ops_alg = 2.0 * L * E * P * Q
+    bytes_alg = P * L * E * 1 + Q * L * E * 1 + 24 * Q
+    roofline = {
+        "bound": "tensor", "kernel": "k_match<1,16,0> (screen pass)",
+        "achieved": ops_alg / (screen_ms / 1e3) / 1e12, "peak": tf_peak, "unit": "TFLOP/s",
+        "frac": ops_alg / (screen_ms / 1e3) / 1e12 / tf_peak,
+        "traffic": ncu_traffic("sw_screen"),
+        "alg_ops_per_launch": ops_alg, "alg_bytes_per_launch": bytes_alg,
+        "launch_ms": screen_ms,
+        "share_of_step": screen_ms / (t_ms / args.steps),
+        "note": (f"peak = {peak_kind} dense bf16 (MEASURED_PEAKS.json); ops = 2*L*E*P*Q integer "
+                 "MACs on u8 counts (IDP4A, CUDA cores). SW at Q=4096 is compute-bound by "
+                 "construction (SURVEY.md 8d); HBM view: "
+                 f"{bytes_alg / (screen_ms / 1e3) / 1e9:.1f} GB/s of {hbm_peak:.0f}"),
+    }
+
+    # ---- e2e: public host API, pinned u64 probes in, results out, every step
+    import torch as _t
+    h_probes = _t.from_numpy(probes_u8.astype(np.uint64)).pin_memory()
+    h_out = np.zeros(Q, _lib.MATCH_DTYPE)
+    h_parts = _t.empty((N, Q, 3), dtype=_t.float64, device=dev)
+
+    def step_e2e():
+        _lib.check(_lib.lib.moe_eamc_match(eamc._h, h_probes.data_ptr(), Q, h_out.ctypes.data,
+                                           None))
+        if N > 1:
+            mine = _t.from_numpy(h_out.view(np.float64).reshape(Q, 3)).to(dev)
+            dist.all_gather_into_tensor(h_parts, mine)
+            _lib.check(_lib.lib.moe_match_merge_device(h_parts.data_ptr(), N, Q,
+                                                       d_final.data_ptr(), sp))
+            return d_final.cpu()
+        return h_out
+
+    for _ in range(min(args.warmup, 3)):
+        step_e2e()
+    barrier()
+    e2e_steps = max(3, min(args.steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step_e2e()
+    if N > 1:
+        dist.barrier()
+    t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if N > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_val = evals_per_step * e2e_steps / float(t_e2e.item())
+
+    # ---- streaming regime (north-star target: >= 60% HBM roofline at P >= 1M)
+    streaming = None
+    if not args.no_streaming:
+        streaming = run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak,
+                                  peak_kind)
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic: reference bench family F1 (bench.cpp:44-54, seed 55)",
+            "config": {
+                "workload": (f"SW (BASELINE configs[1]): Switch-base-128 shape L={L} E={E} "
+                             f"top-{TOPK}, EAMC P={P} per GPU (P_total={P * N}), Q={Q} probes"),
+                "L": L, "E": E, "P_per_gpu": P, "P_total": P * N, "Q": Q, "count_bytes": 1,
+                "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                "parallelism": (f"P-sharded x{N}, NCCL all_gather + device lexicographic merge"
+                                if N > 1 else "single GPU"),
+            },
+            "roofline": roofline,
+            "e2e": {"value": e2e_val, "unit": "evals/s", "steps": e2e_steps,
+                    "api": "moe_eamc_match (host u64 probes, pinned) + D2H results",
+                    "h2d_bytes_per_step": int(Q * L * E * 8),
+                    "d2h_bytes_per_step": int(Q * 24)},
+            "gpu_launches": gpu_launches,
+            "kernel_ms_per_step": {"prep": kms[0] / max(kcalls[0], 1), "screen": screen_ms,
+                                   "refine": kms[2] / max(kcalls[2], 1)},
+            "clocks": clk,
+        }
+        if streaming:
+            out["streaming"] = streaming
+        if N == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"], out["parity_sample"] = cpu_baseline(args, probes_u8, res)
+    if N > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak, peak_kind):
+    """SC streaming regime: P = 2^20 entries (sharded P/N), Q = 8 probes."""
+    P = STREAM_P // N
+    shard = m.gen_bench_family(SEED, L, E, P, skip=rank * P, dtype=np.uint8)
+    probes = m.gen_bench_family(SEED, L, E, STREAM_Q, skip=STREAM_P, dtype=np.uint8)
+    e = m.Eamc(m.ModelShape(L, E, TOPK), m.Phase.decode, P, device=dev.index)
+    e.append(shard, np.arange(rank * P, (rank + 1) * P, dtype=np.uint64))
+    del shard
+    _lib.check(_lib.lib.moe_eamc_set_index_base(e._h, rank * P))
+    d_pr = torch.from_numpy(probes).to(dev)
+    d_out = torch.empty((STREAM_Q, 3), dtype=torch.float64, device=dev)
+    d_parts = torch.empty((N, STREAM_Q, 3), dtype=torch.float64, device=dev)
+    d_fin = torch.empty((STREAM_Q, 3), dtype=torch.float64, device=dev)
+
+    def step():
+        _lib.check(_lib.lib.moe_eamc_match_device(e._h, d_pr.data_ptr(), 1, STREAM_Q,
+                                                  d_out.data_ptr(), sp))
+        if N > 1:
+            dist.all_gather_into_tensor(d_parts, d_out)
+            _lib.check(_lib.lib.moe_match_merge_device(d_parts.data_ptr(), N, STREAM_Q,
+                                                       d_fin.data_ptr(), sp))
+
+    for _ in range(3):
+        step()
+    if N > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    steps = 30
+    _lib.check(_lib.lib.moe_eamc_set_profiling(e._h, 1))
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    kms = (C.c_double * 3)()
+    kc = (C.c_uint64 * 3)()
+    _lib.check(_lib.lib.moe_eamc_kernel_times(e._h, kms, kc))
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+    if N > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    screen_ms = kms[1] / max(kc[1], 1)
+    bytes_alg = P * L * E * 1 + STREAM_Q * L * E * 1 + 24 * STREAM_Q
+    ach = bytes_alg / (screen_ms / 1e3) / 1e9
+    return {
+        "workload": f"SC streaming: P={STREAM_P} (P/GPU={P}), Q={STREAM_Q}, L={L} E={E}, u8",
+        "value": P * N * STREAM_Q * steps / (t_ms / 1e3), "unit": "evals/s",
+        "ms_per_step": t_ms / steps, "steps": steps,
+        "roofline": {"bound": "hbm", "kernel": "k_match<1,8,0> (screen pass)", "achieved": ach,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                     "traffic": ncu_traffic("sc_screen"), "launch_ms": screen_ms,
+                     "alg_bytes_per_launch": bytes_alg,
+                     "note": f"peak = {peak_kind} HBM copy bandwidth (MEASURED_PEAKS.json)"},
+    }
+
+
+def cpu_baseline(args, probes_u8, gpu_res):
+    """The reference CPU path (oracle/_ref = moesim compiled from its sources) on
+    this box's host cores, bounded sample of the SW workload; also checks the
+    sampled probes against the GPU result bit for bit."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import REF_SO, Oracle, RefLib
+    import paper_2401_14361_b200 as m
+    fam = m.gen_bench_family(SEED, L, E, P_PER_GPU, dtype=np.uint64)
+    cores = os.cpu_count() or 1
+    if os.path.exists(REF_SO):
+        ref = RefLib()
+        kind = "reference"
+        e = ref.eamc(L, E, TOPK, 1, P_PER_GPU)
+        for x in fam:
+            e.insert(x)
+
+        def run(pr):
+            idx, seq, d, f, secs = e.match(pr, threads=cores)
+            return idx, d, secs
+    else:
+        orc = Oracle()
+        kind = "port"
+        cores = 1
+
+        def run(pr):
+            t0 = time.perf_counter()
+            idx, seq, d, f = orc.match(fam, np.arange(P_PER_GPU, dtype=np.uint64), pr)
+            return idx, d, time.perf_counter() - t0
+    chunk = max(cores * 2, 8)
+    done, secs = 0, 0.0
+    ok = True
+    while done < Q and secs < args.cpu_seconds:
+        pr = probes_u8[done:done + chunk].astype(np.uint64)
+        idx, d, s = run(pr)
+        secs += s
+        ok &= bool(np.array_equal(idx, gpu_res["index"][done:done + chunk]) and
+                   np.array_equal(d, gpu_res["distance"][done:done + chunk]))
+        done += len(pr)
+    val = P_PER_GPU * done / secs
+    return ({"value": val, "unit": "evals/s", "cores": cores, "kind": kind,
+             "sample": (f"{done} of {Q} SW probes vs P={P_PER_GPU} (Eamc::match, "
+                        f"{'std::thread over the const matcher' if cores > 1 else 'one thread'}), "
+                        f"{secs:.1f} s")},
+            {"probes": done, "bitwise_equal_index_and_distance": ok})
+
+
+# --------------------------------------------------------------- reference
+def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref) on this box's host
+    cores, on our arm's config; rank 0 only."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import REF_SO, Oracle, RefLib
+    import paper_2401_14361_b200 as m
+    N = max(world, args.gpus)
+    P = P_PER_GPU * N
+    fam = m.gen_bench_family(SEED, L, E, P + Q, dtype=np.uint64)
+    cores = os.cpu_count() or 1
+    if os.path.exists(REF_SO):
+        kind = "reference"
+        e = RefLib().eamc(L, E, TOPK, 1, P)
+        for x in fam[:P]:
+            e.insert(x)
+
+        def run(pr):
+            return e.match(pr, threads=cores)[4]
+    else:
+        kind = "port"
+        orc = Oracle()
+        cores = 1
+
+        def run(pr):
+            t0 = time.perf_counter()
+            orc.match(fam[:P], np.arange(P, dtype=np.uint64), pr)
+            return time.perf_counter() - t0
+    per_step = max(cores, 4)
+    probes = fam[P:]
+    for i in range(args.warmup):
+        run(probes[:per_step])
+    secs = 0.0
+    for i in range(args.steps):
+        s0 = (i * per_step) % (Q - per_step)
+        secs += run(probes[s0:s0 + per_step])
+    val = P * per_step * args.steps / secs
+    return {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": N,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference bench family F1 (bench.cpp:44-54, seed 55)",
+        "config": {"workload": (f"SW (BASELINE configs[1]): L={L} E={E} top-{TOPK}, EAMC "
+                                f"P={P}, Q={Q}; each step a {per_step}-probe sample"),
+                   "L": L, "E": E, "P_total": P, "Q": Q},
+        "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": kind,
+                         "sample": f"{per_step} probes per step x {args.steps} steps"},
+        "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-streaming", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,17 @@ moe_status moe_match_merge(const moe_match* parts, uint64_t n_parts, uint64_t n,
 moe_status moe_match_merge_device(const moe_match* parts, uint64_t n_parts, uint64_t n,
                                   moe_match* out, void* stream);
 
+/* P-sharded collections: results report index = base + local slot, so the
+ * per-shard outputs merge into global slot numbers. */
+moe_status moe_eamc_set_index_base(moe_eamc* h, uint64_t base);
+
+/* Instrumentation: when enabled, matching records CUDA events around its
+ * kernels on the launching stream; ms[0..2] = accumulated device time of
+ * probe packing, the screen pass and the refine pass, calls[0..2] their
+ * launch counts (reset by moe_eamc_set_profiling). */
+moe_status moe_eamc_set_profiling(moe_eamc* h, int enable);
+moe_status moe_eamc_kernel_times(const moe_eamc* h, double* ms, uint64_t* calls);
+
 /* eam_distance (eam.cpp:91-104), evaluated on the device. */
 moe_status moe_eam_distance(const moe_shape* shape, const uint64_t* a, const uint64_t* b,
                             double* out);

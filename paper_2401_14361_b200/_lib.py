@@ -88,6 +88,9 @@ _sig("moe_eamc_match_device", C.c_int, vp, vp, C.c_int, u64, vp, vp)
 _sig("moe_eamc_match_within", C.c_int, vp, vp, C.c_double, vp, u64, P(u64))
 _sig("moe_match_merge", C.c_int, vp, u64, u64, vp)
 _sig("moe_match_merge_device", C.c_int, vp, u64, u64, vp, vp)
+_sig("moe_eamc_set_index_base", C.c_int, vp, u64)
+_sig("moe_eamc_set_profiling", C.c_int, vp, C.c_int)
+_sig("moe_eamc_kernel_times", C.c_int, vp, vp, vp)
 _sig("moe_eam_distance", C.c_int, P(moe_shape), vp, vp, P(C.c_double))
 _sig("moe_prefetch_priorities", C.c_int, vp, vp, C.c_uint32, C.c_int, vp, u64, P(u64))
 _sig("moe_decide", C.c_int, vp, vp, C.c_uint32, vp, vp, u64, vp, u64, P(u64), P(C.c_int64))
@@ -105,7 +108,9 @@ EXPORTS = [
     "moe_abi_version", "moe_last_error", "moe_device_info", "moe_eamc_create",
     "moe_eamc_destroy", "moe_eamc_info", "moe_eamc_entry", "moe_eamc_insert", "moe_eamc_build",
     "moe_eamc_append", "moe_eamc_append_packed", "moe_eamc_match", "moe_eamc_match_device",
-    "moe_eamc_match_within", "moe_match_merge", "moe_match_merge_device", "moe_eam_distance",
+    "moe_eamc_match_within", "moe_match_merge", "moe_match_merge_device",
+    "moe_eamc_set_index_base", "moe_eamc_set_profiling", "moe_eamc_kernel_times",
+    "moe_eam_distance",
     "moe_prefetch_priorities", "moe_decide", "moe_cache_priority",
     "moe_select_eviction_victim", "moe_eam_trace", "moe_eam_trace_device",
     "moe_eamc_capacity_bound", "moe_eamc_save", "moe_eamc_load", "moe_gen_bench_family",

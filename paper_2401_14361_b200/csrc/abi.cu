@@ -155,12 +155,19 @@ struct moe_eamc {
   DevBuf raw, packed, ia, sqa, T, bcnt, bucket, over_list, small, out, partials, wl, agg, cand,
       slots, req;
   PinBuf pin;
+  // instrumentation (moe_eamc_set_profiling)
+  bool prof = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double ms[3] = {0, 0, 0};
+  uint64_t calls[3] = {0, 0, 0};
 
   ~moe_eamc() {
     if (c.counts) cudaFree(c.counts);
     if (c.ibT) cudaFree(c.ibT);
     if (c.sqb) cudaFree(c.sqb);
     if (c.seq) cudaFree(c.seq);
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -251,10 +258,18 @@ moe_status prep_probes(moe_eamc* h, const void* src, int src_bytes, uint64_t n, 
     CK(h->pin.ensure(256));
     unsigned long long* dmax = h->small.as<unsigned long long>();
     CK(cudaMemsetAsync(dmax, 0, 8, st));
+    if (h->prof) CK(cudaEventRecord(h->ev[0], st));
     CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, h->packed.as<uint8_t>(),
                         h->ia.as<float>(), h->sqa.as<double>(), nullptr, 0, 0, dmax, st));
+    if (h->prof) CK(cudaEventRecord(h->ev[1], st));
     CK(cudaMemcpyAsync(h->pin.p, dmax, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (h->prof) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, h->ev[0], h->ev[1]));
+      h->ms[0] += t;
+      h->calls[0]++;
+    }
     const uint64_t mx = *h->pin.as<unsigned long long>();
     if (mx <= width_max(c.cb)) break;
     if (mx > 65535ull)
@@ -322,10 +337,22 @@ moe_status match_packed(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaSt
   }
   Plan p;
   CKS(make_plan(h, 0, pick_qt(Q), &p));
+  if (h->prof) CK(cudaEventRecord(h->ev[1], st));
   CK(moe::launch_screen(p.map, c, pr, p.g, w, st));
+  if (h->prof) CK(cudaEventRecord(h->ev[2], st));
   CK(moe::launch_refine(c, pr, w, out, nullptr, nullptr, 0, st));
+  if (h->prof) CK(cudaEventRecord(h->ev[3], st));
   CK(cudaMemcpyAsync(h->pin.p, w.over_n, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (h->prof) {
+    float t1 = 0.f, t2 = 0.f;
+    CK(cudaEventElapsedTime(&t1, h->ev[1], h->ev[2]));
+    CK(cudaEventElapsedTime(&t2, h->ev[2], h->ev[3]));
+    h->ms[1] += t1;
+    h->ms[2] += t2;
+    h->calls[1]++;
+    h->calls[2]++;
+  }
   const uint32_t n_over = *h->pin.as<uint32_t>();
   if (n_over) {
     Plan pe;
@@ -485,7 +512,8 @@ moe_status replay_staged(moe_eamc* h, Staged& s, int64_t* evicted_slots) {
   if (evicted_slots) {
     std::vector<moe_match> v(n_rep);
     CK(cudaMemcpy(v.data(), vic + i, n_rep * sizeof(moe_match), cudaMemcpyDeviceToHost));
-    for (uint32_t j = 0; j < n_rep; ++j) evicted_slots[i + j] = (int64_t)v[j].index;
+    for (uint32_t j = 0; j < n_rep; ++j)
+      evicted_slots[i + j] = (int64_t)(v[j].index - h->c.index_base);
   }
   return MOE_OK;
 }
@@ -599,11 +627,11 @@ moe_status moe_eamc_insert(moe_eamc* h, const uint64_t* counts, moe_eam_kind kin
   moe_match v;
   CK(cudaMemcpyAsync(&v, dv, sizeof v, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
-  if (evicted_counts) CKS(read_entry(h, v.index, evicted_counts, nullptr));
+  if (evicted_counts) CKS(read_entry(h, v.index - h->c.index_base, evicted_counts, nullptr));
   CK(moe::launch_replace(h->c, s.pr, 0, dv, h->next_seq, nullptr, h->st));
   CK(cudaStreamSynchronize(h->st));
   h->next_seq++;
-  if (evicted_slot) *evicted_slot = (int64_t)v.index;
+  if (evicted_slot) *evicted_slot = (int64_t)(v.index - h->c.index_base);
   return MOE_OK;
 }
 
@@ -729,7 +757,8 @@ moe_status moe_eamc_match_within(const moe_eamc* hc, const uint64_t* probe, doub
   std::sort(v.begin(), v.end(), [](const moe::WinEntry& a, const moe::WinEntry& b) {
     return a.d != b.d ? a.d < b.d : a.seq < b.seq;
   });
-  for (uint64_t i = 0; i < n && i < cap; ++i) out[i] = moe_match{v[i].p, v[i].seq, v[i].d};
+  for (uint64_t i = 0; i < n && i < cap; ++i)
+    out[i] = moe_match{v[i].p + h->c.index_base, v[i].seq, v[i].d};
   *n_out = n;
   return MOE_OK;
 }
@@ -757,6 +786,34 @@ moe_status moe_match_merge_device(const moe_match* parts, uint64_t n_parts, uint
   if ((!parts || !out) && n) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (n == 0 || n_parts == 0) return MOE_OK;
   CK(moe::launch_merge(parts, n_parts, n, out, static_cast<cudaStream_t>(stream)));
+  return MOE_OK;
+}
+
+moe_status moe_eamc_set_index_base(moe_eamc* h, uint64_t base) {
+  if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  h->c.index_base = base;
+  return MOE_OK;
+}
+
+moe_status moe_eamc_set_profiling(moe_eamc* h, int enable) {
+  if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  DeviceGuard dg(h->device);
+  for (cudaEvent_t& e : h->ev)
+    if (!e) CK(cudaEventCreate(&e));
+  h->prof = enable != 0;
+  for (int i = 0; i < 3; ++i) {
+    h->ms[i] = 0.0;
+    h->calls[i] = 0;
+  }
+  return MOE_OK;
+}
+
+moe_status moe_eamc_kernel_times(const moe_eamc* h, double* ms, uint64_t* calls) {
+  if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  for (int i = 0; i < 3; ++i) {
+    if (ms) ms[i] = h->ms[i];
+    if (calls) calls[i] = h->calls[i];
+  }
   return MOE_OK;
 }
 

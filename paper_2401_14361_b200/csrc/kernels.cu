@@ -357,6 +357,7 @@ struct RefineArgs {
   const int* halt;
   int* halt_set;
   uint32_t halt_value;
+  uint64_t index_base;
 };
 
 template <int CB>
@@ -402,13 +403,14 @@ __global__ void k_refine(const RefineArgs r) {
       if (better(d, s, b.d, b.seq)) b = Best{d, s, pp};
     }
   }
-  if (lane == 0) r.out[q] = moe_match{b.idx, b.seq, b.d};
+  if (lane == 0) r.out[q] = moe_match{b.idx == kNone ? kNone : b.idx + r.index_base, b.seq, b.d};
 }
 
 // Partial merge for mode 1: for list position qi, the blocks whose item
 // range intersects [qi*n_pt, (qi+1)*n_pt).
 __global__ void k_merge_partials(const moe_match* parts, uint32_t grid, uint32_t nq,
-                                 uint32_t n_pt, const uint32_t* qlist, moe_match* out) {
+                                 uint32_t n_pt, const uint32_t* qlist, moe_match* out,
+                                 uint64_t index_base) {
   const uint32_t qi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (qi >= nq) return;
@@ -423,7 +425,8 @@ __global__ void k_merge_partials(const moe_match* parts, uint32_t grid, uint32_t
     }
   }
   b = warp_best(b);
-  if (lane == 0) out[qlist[qi]] = moe_match{b.idx, b.seq, b.d};
+  if (lane == 0)
+    out[qlist[qi]] = moe_match{b.idx == kNone ? kNone : b.idx + index_base, b.seq, b.d};
 }
 
 __global__ void k_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out) {
@@ -502,9 +505,10 @@ __global__ void k_prep(const void* src, uint64_t rows, uint32_t E, uint32_t L, u
 __global__ void k_replace(uint8_t* counts, float* ibT, double* sqb, uint64_t* seq, uint64_t cap,
                           uint32_t L, uint32_t RB, const uint8_t* sp, const float* sia,
                           const double* ssq, uint32_t i, const moe_match* victim,
-                          uint64_t append_slot, uint64_t seq_value, const int* halt) {
+                          uint64_t append_slot, uint64_t seq_value, const int* halt,
+                          uint64_t index_base) {
   if (halt && *halt) return;
-  const uint64_t slot = victim ? victim->index : append_slot;
+  const uint64_t slot = victim ? victim->index - index_base : append_slot;
   const uint64_t LR = (uint64_t)L * RB;
   const uint4* src = reinterpret_cast<const uint4*>(sp + (uint64_t)i * LR);
   uint4* dst = reinterpret_cast<uint4*>(counts + slot * LR);
@@ -986,6 +990,7 @@ cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork
   r.halt = halt;
   r.halt_set = halt_set;
   r.halt_value = halt_value;
+  r.index_base = c.index_base;
   const uint32_t threads = 256;
   const uint32_t blocks = (uint32_t)(((uint64_t)pr.Q * 32 + threads - 1) / threads);
   if (c.cb == 1)
@@ -1010,7 +1015,8 @@ cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProb
     if (e != cudaSuccess) return e;
     const uint32_t threads = 256;
     const uint32_t blocks = (uint32_t)(((uint64_t)n * 32 + threads - 1) / threads);
-    k_merge_partials<<<blocks, threads, 0, st>>>(w.partials, g.grid, n, g.n_pt, qlist + off, out);
+    k_merge_partials<<<blocks, threads, 0, st>>>(w.partials, g.grid, n, g.n_pt, qlist + off, out,
+                                                 c.index_base);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -1052,7 +1058,8 @@ cudaError_t launch_replace(const DevColl& c, const DevProbes& staged, uint32_t i
                            const moe_match* victim, uint64_t seq_value, const int* halt,
                            cudaStream_t st) {
   k_replace<<<1, 256, 0, st>>>(c.counts, c.ibT, c.sqb, c.seq, c.cap, c.L, c.RB, staged.packed,
-                               staged.ia, staged.sqa, i, victim, c.size, seq_value, halt);
+                               staged.ia, staged.sqa, i, victim, c.size, seq_value, halt,
+                               c.index_base);
   return cudaGetLastError();
 }
 

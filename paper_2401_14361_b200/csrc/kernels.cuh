@@ -15,6 +15,7 @@ struct DevColl {
   int cb = 1;              // bytes per stored count
   uint64_t cap = 0;
   uint32_t size = 0;
+  uint64_t index_base = 0;    // reported index = index_base + slot (P-sharding)
   uint8_t* counts = nullptr;  // [cap][L][RB]
   float* ibT = nullptr;       // [L][cap] fp32 1/sqrt(sum c^2) (0 on zero rows)
   double* sqb = nullptr;      // [cap][L] sqrt(sum c^2)
