@@ -141,7 +141,7 @@ def run_ours(args):
 
     d_probes = torch.from_numpy(probes_u8).to(dev)
     d_out = torch.empty((Q, 3), dtype=torch.float64, device=dev)      # moe_match[Q]
-    d_parts = torch.empty((N, Q, 3), dtype=torch.float64, device=dev)
+    d_parts = torch.empty((N * Q, 3), dtype=torch.float64, device=dev)
     d_final = torch.empty((Q, 3), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -214,7 +214,7 @@ def run_ours(args):
     import torch as _t
     h_probes = _t.from_numpy(probes_u8.astype(np.uint64)).pin_memory()
     h_out = np.zeros(Q, _lib.MATCH_DTYPE)
-    h_parts = _t.empty((N, Q, 3), dtype=_t.float64, device=dev)
+    h_parts = _t.empty((N * Q, 3), dtype=_t.float64, device=dev)
 
     def step_e2e():
         _lib.check(_lib.lib.moe_eamc_match(eamc._h, h_probes.data_ptr(), Q, h_out.ctypes.data,
@@ -293,7 +293,7 @@ def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak,
     _lib.check(_lib.lib.moe_eamc_set_index_base(e._h, rank * P))
     d_pr = torch.from_numpy(probes).to(dev)
     d_out = torch.empty((STREAM_Q, 3), dtype=torch.float64, device=dev)
-    d_parts = torch.empty((N, STREAM_Q, 3), dtype=torch.float64, device=dev)
+    d_parts = torch.empty((N * STREAM_Q, 3), dtype=torch.float64, device=dev)
     d_fin = torch.empty((STREAM_Q, 3), dtype=torch.float64, device=dev)
 
     def step():

@@ -25,6 +25,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <tuple>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -859,20 +861,56 @@ float screen_eps2(uint32_t L) {
   return (float)(2.0 * eps);
 }
 
+namespace {
+template <int CB, int QT, int MODE>
+int occ_blocks_t(size_t smem) {
+  if (set_smem_attr<CB, QT, MODE>(smem) != cudaSuccess) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_match<CB, QT, MODE>, kNT, smem) !=
+      cudaSuccess)
+    return 0;
+  return n;
+}
+int occ_blocks(int cb, uint32_t QT, int mode, size_t smem) {
+  if (mode == 1) return cb == 1 ? occ_blocks_t<1, 1, 1>(smem) : occ_blocks_t<2, 1, 1>(smem);
+  if (mode == 2) return cb == 1 ? occ_blocks_t<1, 1, 2>(smem) : occ_blocks_t<2, 1, 2>(smem);
+  switch (QT) {
+    case 1: return cb == 1 ? occ_blocks_t<1, 1, 0>(smem) : occ_blocks_t<2, 1, 0>(smem);
+    case 2: return cb == 1 ? occ_blocks_t<1, 2, 0>(smem) : occ_blocks_t<2, 2, 0>(smem);
+    case 4: return cb == 1 ? occ_blocks_t<1, 4, 0>(smem) : occ_blocks_t<2, 4, 0>(smem);
+    case 8: return cb == 1 ? occ_blocks_t<1, 8, 0>(smem) : occ_blocks_t<2, 8, 0>(smem);
+    case 16: return cb == 1 ? occ_blocks_t<1, 16, 0>(smem) : occ_blocks_t<2, 16, 0>(smem);
+  }
+  return 0;
+}
+}  // namespace
+
+// Launch geometry of the matcher: the layer-group depth G (rows per TMA box),
+// pipeline depth S and resident blocks per SM are chosen together to maximize
+//   (resident warps, capped at 16/SM) x (shared-memory bank efficiency of the
+//   per-lane rotated row reads) / (TMA bytes wasted on out-of-range layers)
+// subject to keeping >= ~32 KB of TMA traffic in flight per SM.
 bool plan_match(const DevColl& c, int n_sm, int mode, uint32_t QT, MatchGeom* g) {
-  const size_t kMaxSmem = 220 * 1024;
+  static std::map<std::tuple<uint32_t, uint32_t, int, int, uint32_t>, MatchGeom> cache;
+  const auto key = std::make_tuple(c.L, c.RB, c.cb, mode, QT);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *g = it->second;
+    g->n_pt = (c.size + kNT - 1) / kNT;
+    g->grid = (uint32_t)n_sm * g->blocks_per_sm;
+    return true;
+  }
+  const size_t kMaxSmem = 227 * 1024;
   const uint32_t acc_bytes = c.cb == 1 ? 4 : 8;
-  // Choose the layer-group depth G: prefer conflict-free shared-memory
-  // banking for the per-lane rotated row reads, then the deepest stage
-  // that fits 3 (else 2) pipeline stages.
   double best_score = -1.0;
   MatchGeom best;
-  for (uint32_t S = 3; S >= 2; --S) {
+  for (uint32_t S = 2; S <= 4; ++S) {
     for (uint32_t G = 1; G <= std::min<uint32_t>(c.L, 16); ++G) {
       const SmemLayout lay = smem_layout(c.L, c.RB, G, S, QT, mode, acc_bytes);
       if (lay.total > kMaxSmem) continue;
-      // bank-group wavefronts of one warp-wide 16-byte row read
-      double wf = 0.0;
+      const int blocks = occ_blocks(c.cb, QT, mode, lay.total);
+      if (blocks < 1) continue;
+      double wf = 0.0;  // bank-group wavefronts of one warp-wide 16-byte row read
       for (uint32_t cc = 0; cc < c.C; ++cc) {
         int cnt[8] = {0};
         for (uint32_t ln = 0; ln < 32; ++ln) {
@@ -886,22 +924,26 @@ bool plan_match(const DevColl& c, int n_sm, int mode, uint32_t QT, MatchGeom* g)
       }
       wf /= c.C;
       const uint32_t ng = (c.L + G - 1) / G;
-      const double waste = (double)(ng * G) / c.L;  // OOB layers still cost TMA bandwidth
-      const double score = (4.0 / wf) / waste + 0.01 * G + 0.001 * S;
+      const double waste = (double)(ng * G) / c.L;
+      const double warps = std::min(16.0, 4.0 * blocks) / 16.0;
+      const double inflight = (double)(S - 1) * lay.stage_bytes * blocks;
+      const double score = warps * (4.0 / wf) / waste * std::min(1.0, inflight / 32768.0) +
+                           1e-3 * G + 1e-4 * S;
       if (score > best_score) {
         best_score = score;
         best.G = G;
         best.S = S;
         best.smem = lay.total;
+        best.blocks_per_sm = (uint32_t)blocks;
       }
     }
-    if (best_score > 0) break;
   }
   if (best_score < 0) return false;
   best.QT = QT;
   best.n_groups = (c.L + best.G - 1) / best.G;
+  cache[key] = best;
   best.n_pt = (c.size + kNT - 1) / kNT;
-  best.grid = (uint32_t)n_sm;
+  best.grid = (uint32_t)n_sm * best.blocks_per_sm;
   *g = best;
   return true;
 }

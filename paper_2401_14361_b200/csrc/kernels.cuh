@@ -31,7 +31,7 @@ struct DevProbes {
 };
 
 struct MatchGeom {
-  uint32_t G = 1, S = 2, QT = 1, n_groups = 1, n_pt = 0, grid = 1;
+  uint32_t G = 1, S = 2, QT = 1, n_groups = 1, n_pt = 0, grid = 1, blocks_per_sm = 1;
   size_t smem = 0;
 };
 
