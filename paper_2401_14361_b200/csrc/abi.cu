@@ -152,8 +152,8 @@ struct moe_eamc {
   DevColl c;
   cudaStream_t st = nullptr;
   // workspace
-  DevBuf raw, packed, ia, sqa, T, bcnt, bucket, over_list, small, out, partials, wl, agg, cand,
-      slots, req;
+  DevBuf raw, packed, ia, sqa, nrm, zq, T, bcnt, bucket, over_list, small, out, partials, wl,
+      agg, cand, slots, req;
   PinBuf pin;
   // instrumentation (moe_eamc_set_profiling)
   bool prof = false;
@@ -166,6 +166,8 @@ struct moe_eamc {
     if (c.ibT) cudaFree(c.ibT);
     if (c.sqb) cudaFree(c.sqb);
     if (c.seq) cudaFree(c.seq);
+    if (c.nrm) cudaFree(c.nrm);
+    if (c.zmask) cudaFree(c.zmask);
     for (cudaEvent_t e : ev)
       if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
@@ -187,6 +189,17 @@ moe_status ensure_alloc(moe_eamc* h, uint64_t need) {
   float* ibT = nullptr;
   double* sqb = nullptr;
   uint64_t* seq = nullptr;
+  __half* nrm = nullptr;
+  uint64_t* zmask = nullptr;
+  if (c.Kp) {
+    CK(cudaMalloc(&nrm, (size_t)nc * c.Kp * sizeof(__half)));
+    CK(cudaMalloc(&zmask, (size_t)nc * sizeof(uint64_t)));
+    if (c.size) {
+      CK(cudaMemcpyAsync(nrm, c.nrm, (size_t)c.size * c.Kp * sizeof(__half),
+                         cudaMemcpyDeviceToDevice, h->st));
+      CK(cudaMemcpyAsync(zmask, c.zmask, (size_t)c.size * 8, cudaMemcpyDeviceToDevice, h->st));
+    }
+  }
   // +kNT entries of slack so TMA boxes of the last tile stay in-bounds
   CK(cudaMalloc(&counts, (nc + moe::kNT) * LR));
   CK(cudaMalloc(&ibT, (size_t)c.L * nc * sizeof(float)));
@@ -207,10 +220,14 @@ moe_status ensure_alloc(moe_eamc* h, uint64_t need) {
   if (c.ibT) cudaFree(c.ibT);
   if (c.sqb) cudaFree(c.sqb);
   if (c.seq) cudaFree(c.seq);
+  if (c.nrm) cudaFree(c.nrm);
+  if (c.zmask) cudaFree(c.zmask);
   c.counts = counts;
   c.ibT = ibT;
   c.sqb = sqb;
   c.seq = seq;
+  c.nrm = nrm;
+  c.zmask = zmask;
   c.cap = nc;
   return MOE_OK;
 }
@@ -237,6 +254,17 @@ moe_status widen(moe_eamc* h) {
 
 uint64_t width_max(int cb) { return cb == 1 ? 255ull : 65535ull; }
 
+// Tensor-core screen for probe batches that fill its 128-row M tile
+// (MOE_TC=0 disables it, MOE_TC=1 forces it for any batch size).
+bool use_tc(const moe_eamc* h, uint64_t Q) {
+  if (!h->c.Kp) return false;
+  if (const char* e = getenv("MOE_TC")) {
+    if (e[0] == '0') return false;
+    if (e[0] == '1') return true;
+  }
+  return Q >= 128;
+}
+
 // H2D (or D2D) + pack probes into h->packed/ia/sqa at the collection's
 // width, widening the collection if a count needs it.
 moe_status prep_probes(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bool src_device,
@@ -259,8 +287,21 @@ moe_status prep_probes(moe_eamc* h, const void* src, int src_bytes, uint64_t n, 
     unsigned long long* dmax = h->small.as<unsigned long long>();
     CK(cudaMemsetAsync(dmax, 0, 8, st));
     if (h->prof) CK(cudaEventRecord(h->ev[0], st));
+    __half* nrm = nullptr;
+    uint64_t* zq = nullptr;
+    if (c.Kp && use_tc(h, n)) {
+      CK(h->nrm.ensure(n * c.Kp * sizeof(__half)));
+      CK(h->zq.ensure(n * 8));
+      nrm = h->nrm.as<__half>();
+      zq = h->zq.as<uint64_t>();
+      CK(cudaMemsetAsync(nrm, 0, n * c.Kp * sizeof(__half), st));
+      CK(cudaMemsetAsync(zq, 0, n * 8, st));
+    }
     CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, h->packed.as<uint8_t>(),
-                        h->ia.as<float>(), h->sqa.as<double>(), nullptr, 0, 0, dmax, st));
+                        h->ia.as<float>(), h->sqa.as<double>(), nullptr, 0, 0, dmax, nrm, c.Kp,
+                        zq, st));
+    pr->nrm = nrm;
+    pr->zmask = zq;
     if (h->prof) CK(cudaEventRecord(h->ev[1], st));
     CK(cudaMemcpyAsync(h->pin.p, dmax, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -335,10 +376,16 @@ moe_status match_packed(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaSt
     CK(moe::launch_refine(c, pr, w, out, nullptr, nullptr, 0, st));
     return MOE_OK;
   }
-  Plan p;
-  CKS(make_plan(h, 0, pick_qt(Q), &p));
+  const bool tc = pr.nrm != nullptr && moe::tc_supported(c);
+  w.eps2 = tc ? moe::tc_eps2(c.L, c.E, c.Kp) : moe::screen_eps2(c.L);
   if (h->prof) CK(cudaEventRecord(h->ev[1], st));
-  CK(moe::launch_screen(p.map, c, pr, p.g, w, st));
+  if (tc) {
+    CK(moe::launch_tc_screen(c, pr, w, h->n_sm, st));
+  } else {
+    Plan p;
+    CKS(make_plan(h, 0, pick_qt(Q), &p));
+    CK(moe::launch_screen(p.map, c, pr, p.g, w, st));
+  }
   if (h->prof) CK(cudaEventRecord(h->ev[2], st));
   CK(moe::launch_refine(c, pr, w, out, nullptr, nullptr, 0, st));
   if (h->prof) CK(cudaEventRecord(h->ev[3], st));
@@ -384,7 +431,7 @@ moe_status read_entry(moe_eamc* h, uint64_t slot, uint64_t* counts, uint64_t* se
 
 // Stage n EAMs (device raw) as packed rows in a private staging set.
 struct Staged {
-  DevBuf packed, ia, sqa;
+  DevBuf packed, ia, sqa, nrm, zmask;
   DevProbes pr;
 };
 
@@ -399,8 +446,16 @@ moe_status stage_entries(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t 
     CK(h->pin.ensure(256));
     unsigned long long* dmax = h->small.as<unsigned long long>();
     CK(cudaMemsetAsync(dmax, 0, 8, h->st));
+    if (c.Kp) {
+      CK(s->nrm.ensure(n * c.Kp * sizeof(__half)));
+      CK(s->zmask.ensure(n * 8));
+      CK(cudaMemsetAsync(s->nrm.p, 0, n * c.Kp * sizeof(__half), h->st));
+      CK(cudaMemsetAsync(s->zmask.p, 0, n * 8, h->st));
+    }
     CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, s->packed.as<uint8_t>(),
-                        s->ia.as<float>(), s->sqa.as<double>(), nullptr, 0, 0, dmax, h->st));
+                        s->ia.as<float>(), s->sqa.as<double>(), nullptr, 0, 0, dmax,
+                        c.Kp ? s->nrm.as<__half>() : nullptr, c.Kp,
+                        c.Kp ? s->zmask.as<uint64_t>() : nullptr, h->st));
     CK(cudaMemcpyAsync(h->pin.p, dmax, 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     const uint64_t mx = *h->pin.as<unsigned long long>();
@@ -414,6 +469,8 @@ moe_status stage_entries(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t 
   s->pr.packed = s->packed.as<uint8_t>();
   s->pr.ia = s->ia.as<float>();
   s->pr.sqa = s->sqa.as<double>();
+  s->pr.nrm = c.Kp ? s->nrm.as<__half>() : nullptr;
+  s->pr.zmask = c.Kp ? s->zmask.as<uint64_t>() : nullptr;
   return MOE_OK;
 }
 
@@ -565,6 +622,7 @@ moe_status moe_eamc_create(const moe_shape* shape, moe_phase phase, uint64_t cap
   h->c.cb = count_bytes;
   h->c.RB = row_bytes(h->c.E, count_bytes);
   h->c.C = h->c.RB / 16;
+  if (h->c.L <= 64) h->c.Kp = (h->c.L * h->c.E + 63) / 64 * 64;
   if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) {
     delete h;
     return fail(MOE_ERR_CUDA, "stream create failed");

@@ -462,7 +462,8 @@ __device__ __forceinline__ uint64_t load_count(const void* src, uint64_t i) {
 template <int SRC>
 __global__ void k_prep(const void* src, uint64_t rows, uint32_t E, uint32_t L, uint32_t RB,
                        int cb, uint8_t* dst, float* ia, double* sq, float* ibT, uint64_t ib_cap,
-                       uint64_t ib_base, unsigned long long* max_count) {
+                       uint64_t ib_base, unsigned long long* max_count, __half* nrm, uint32_t Kp,
+                       uint64_t* zmask) {
   const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -490,9 +491,9 @@ __global__ void k_prep(const void* src, uint64_t rows, uint32_t E, uint32_t L, u
     const uint64_t m2 = __shfl_xor_sync(0xffffffffu, mx, o);
     mx = m2 > mx ? m2 : mx;
   }
+  const double s = __dsqrt_rn(__ull2double_rn(ss));
+  const float inv = ss ? __double2float_rn(__drcp_rn(s)) : 0.f;
   if (lane == 0) {
-    const double s = __dsqrt_rn(__ull2double_rn(ss));
-    const float inv = ss ? __double2float_rn(__drcp_rn(s)) : 0.f;
     sq[row] = s;
     if (ia) ia[row] = inv;
     if (ibT) {
@@ -501,6 +502,15 @@ __global__ void k_prep(const void* src, uint64_t rows, uint32_t E, uint32_t L, u
       ibT[(uint64_t)l * ib_cap + slot] = inv;
     }
     if (max_count && mx) atomicMax(max_count, (unsigned long long)mx);
+    if (zmask && ss == 0) atomicOr(reinterpret_cast<unsigned long long*>(&zmask[row / L]),
+                                   1ull << (row % L));
+  }
+  if (nrm && ss) {  // unit-normalised fp16 row of the tensor-core screen operand
+    __half* o = nrm + (row / L) * (uint64_t)Kp + (row % L) * (uint64_t)E;
+    for (uint32_t e = lane; e < E; e += 32) {
+      const uint64_t c = load_count<SRC>(src, sbase + e);
+      o[e] = __float2half_rn(__uint2float_rn((uint32_t)c) * inv);
+    }
   }
 }
 
@@ -508,9 +518,16 @@ __global__ void k_replace(uint8_t* counts, float* ibT, double* sqb, uint64_t* se
                           uint32_t L, uint32_t RB, const uint8_t* sp, const float* sia,
                           const double* ssq, uint32_t i, const moe_match* victim,
                           uint64_t append_slot, uint64_t seq_value, const int* halt,
-                          uint64_t index_base) {
+                          uint64_t index_base, __half* nrm, const __half* snrm, uint32_t Kp,
+                          uint64_t* zmask, const uint64_t* szmask) {
   if (halt && *halt) return;
   const uint64_t slot = victim ? victim->index - index_base : append_slot;
+  if (nrm) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(snrm + (uint64_t)i * Kp);
+    uint4* d4 = reinterpret_cast<uint4*>(nrm + slot * Kp);
+    for (uint32_t o = threadIdx.x; o < Kp / 8; o += blockDim.x) d4[o] = s4[o];
+    if (threadIdx.x == 0) zmask[slot] = szmask[i];
+  }
   const uint64_t LR = (uint64_t)L * RB;
   const uint4* src = reinterpret_cast<const uint4*>(sp + (uint64_t)i * LR);
   uint4* dst = reinterpret_cast<uint4*>(counts + slot * LR);
@@ -524,7 +541,20 @@ __global__ void k_replace(uint8_t* counts, float* ibT, double* sqb, uint64_t* se
 
 __global__ void k_append_staged(uint8_t* counts, float* ibT, double* sqb, uint64_t cap, uint32_t L,
                                 uint32_t RB, const uint8_t* sp, const float* sia,
-                                const double* ssq, uint32_t first, uint32_t n, uint64_t base) {
+                                const double* ssq, uint32_t first, uint32_t n, uint64_t base,
+                                __half* nrm, const __half* snrm, uint32_t Kp, uint64_t* zmask,
+                                const uint64_t* szmask) {
+  if (nrm) {
+    const uint64_t w16 = (uint64_t)n * Kp / 8;
+    const uint4* s4 = reinterpret_cast<const uint4*>(snrm + (uint64_t)first * Kp);
+    uint4* d4 = reinterpret_cast<uint4*>(nrm + base * Kp);
+    for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < w16;
+         o += (uint64_t)gridDim.x * blockDim.x)
+      d4[o] = s4[o];
+    for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < n;
+         o += (uint64_t)gridDim.x * blockDim.x)
+      zmask[base + o] = szmask[first + o];
+  }
   const uint64_t LR = (uint64_t)L * RB;
   const uint64_t words = (uint64_t)n * LR / 16;
   const uint4* src = reinterpret_cast<const uint4*>(sp + (uint64_t)first * LR);
@@ -971,7 +1001,7 @@ cudaError_t encode_tmap(const DevColl& c, uint32_t G, CUtensorMap* map) {
 cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, uint32_t E,
                         uint32_t RB, int cb, uint8_t* dst, float* ia, double* sq, float* ibT,
                         uint64_t ib_cap, uint64_t ib_base, unsigned long long* max_count,
-                        cudaStream_t st) {
+                        __half* nrm, uint32_t Kp, uint64_t* zmask, cudaStream_t st) {
   const uint64_t rows = n * L;
   if (rows == 0) return cudaSuccess;
   const uint32_t threads = 256;
@@ -979,15 +1009,18 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
   switch (src_bytes) {
     case 8:
       k_prep<8><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,
-                                                      ib_cap, ib_base, max_count);
+                                                      ib_cap, ib_base, max_count, nrm, Kp,
+                                                      zmask);
       break;
     case 2:
       k_prep<2><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,
-                                                      ib_cap, ib_base, max_count);
+                                                      ib_cap, ib_base, max_count, nrm, Kp,
+                                                      zmask);
       break;
     case 1:
       k_prep<1><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,
-                                                      ib_cap, ib_base, max_count);
+                                                      ib_cap, ib_base, max_count, nrm, Kp,
+                                                      zmask);
       break;
     default:
       return cudaErrorInvalidValue;
@@ -1021,7 +1054,7 @@ cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork
   r.L = c.L;
   r.C = c.C;
   r.RB = c.RB;
-  r.eps2 = screen_eps2(c.L);
+  r.eps2 = w.eps2 > 0.f ? w.eps2 : screen_eps2(c.L);
   r.T = w.T;
   r.bcnt = w.bcnt;
   r.bucket = w.bucket;
@@ -1049,6 +1082,7 @@ cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProb
   for (uint32_t off = 0; off < qlist_n; off += w.part_chunk) {
     const uint32_t n = std::min(w.part_chunk, qlist_n - off);
     MatchArgs a = base_args(c, pr, g);
+    a.eps2 = std::max(a.eps2, w.eps2);  // band of whichever screen produced T
     a.qlist = qlist + off;
     a.nq_list = n;
     a.Tfinal = T;
@@ -1101,7 +1135,7 @@ cudaError_t launch_replace(const DevColl& c, const DevProbes& staged, uint32_t i
                            cudaStream_t st) {
   k_replace<<<1, 256, 0, st>>>(c.counts, c.ibT, c.sqb, c.seq, c.cap, c.L, c.RB, staged.packed,
                                staged.ia, staged.sqa, i, victim, c.size, seq_value, halt,
-                               c.index_base);
+                               c.index_base, c.nrm, staged.nrm, c.Kp, c.zmask, staged.zmask);
   return cudaGetLastError();
 }
 
@@ -1109,7 +1143,8 @@ cudaError_t launch_append_staged(const DevColl& c, const DevProbes& staged, uint
                                  uint32_t n, uint64_t base, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   k_append_staged<<<256, 256, 0, st>>>(c.counts, c.ibT, c.sqb, c.cap, c.L, c.RB, staged.packed,
-                                       staged.ia, staged.sqa, first, n, base);
+                                       staged.ia, staged.sqa, first, n, base, c.nrm, staged.nrm,
+                                       c.Kp, c.zmask, staged.zmask);
   return cudaGetLastError();
 }
 

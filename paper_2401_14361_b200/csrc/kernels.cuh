@@ -3,6 +3,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "../../include/moe_eamc.h"
@@ -20,6 +21,11 @@ struct DevColl {
   float* ibT = nullptr;       // [L][cap] fp32 1/sqrt(sum c^2) (0 on zero rows)
   double* sqb = nullptr;      // [cap][L] sqrt(sum c^2)
   uint64_t* seq = nullptr;    // [cap]
+  // tensor-core screen operands (L <= 64): rows normalised to unit length,
+  // fp16, K-major [cap][Kp] with Kp = roundup(L*E, 64); zero-row bitmasks
+  uint32_t Kp = 0;
+  __half* nrm = nullptr;
+  uint64_t* zmask = nullptr;
 };
 
 // Packed probe batch.
@@ -28,6 +34,8 @@ struct DevProbes {
   uint8_t* packed = nullptr;  // [Q][L][RB]
   float* ia = nullptr;        // [Q][L]
   double* sqa = nullptr;      // [Q][L]
+  __half* nrm = nullptr;      // [Q][Kp] (tensor-core screen operand) or null
+  uint64_t* zmask = nullptr;  // [Q]
 };
 
 struct MatchGeom {
@@ -44,6 +52,7 @@ struct MatchWork {  // scratch for one match pipeline
   uint32_t* over_n = nullptr;     // [1]
   moe_match* partials = nullptr;  // [chunk][grid]
   uint32_t part_chunk = 0;
+  float eps2 = 0.f;               // screen band the refine pass must honour
 };
 
 struct WinEntry {
@@ -65,7 +74,13 @@ cudaError_t encode_tmap(const DevColl& c, uint32_t G, CUtensorMap* map);
 cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, uint32_t E,
                         uint32_t RB, int cb, uint8_t* dst, float* ia, double* sq, float* ibT,
                         uint64_t ib_cap, uint64_t ib_base, unsigned long long* max_count,
-                        cudaStream_t st);
+                        __half* nrm, uint32_t Kp, uint64_t* zmask, cudaStream_t st);
+
+// Tensor-core (tcgen05 kind::f16) screen pass for large probe batches.
+float tc_eps2(uint32_t L, uint32_t E, uint32_t Kp);
+bool tc_supported(const DevColl& c);
+cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchWork& w, int n_sm,
+                             cudaStream_t st);
 
 // mode 0: screen all Q probes; then refine.
 cudaError_t launch_screen(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,

@@ -1,0 +1,347 @@
+// tc_screen.cu -- tensor-core (tcgen05) screen pass of the EAMC matcher for
+// large probe batches (batch regime: SW Q=4096, SC Q=65,536).
+//
+// Every probe row and collection row is stored a second time, normalised
+// (c * RN32(1/sqrt(sum c^2))) and rounded to fp16, K-major, K = L*E padded to
+// a multiple of 64.  One GEMM D[q][p] = sum_k A'[q][k] * B'[p][k] then gives
+// the summed per-layer cosine similarities of every (probe, entry) pair
+// directly -- the per-layer epilogue of the SIMT screen disappears.  The
+// both-zero-row convention (eam.cpp:84) is added exactly as
+// popc(zmask_q & zmask_p).  fp16 rounding of the operands and the fp32
+// tensor-core accumulation give a screen distance within tc_eps of the
+// reference distance ("tensor-core screen bound"); the argmin
+// threshold / candidate-bucket logic and the exact fp64 refine are shared
+// with the SIMT path, so results stay bit-exact.
+//
+// Kernel anatomy (one CTA per SM, persistent over 128x256 output tiles):
+//   warp 0      TMA producer: A' 128x64 and B' 256x64 fp16 tiles, 128B swizzle,
+//               4-stage mbarrier ring (48 KB per stage)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma.cta_group::1.kind::f16
+//               issuer (M=128, N=256, K=16), double-buffered fp32 accumulators
+//               (2 x 256 TMEM columns), tcgen05.commit -> mbarriers
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 (thread = probe row), screen
+//               distance, row min -> global per-probe threshold (atomicMin),
+//               candidate push into the per-probe bucket
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace moe {
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK * 2;  // 16 KB
+constexpr uint32_t B_BYTES = BN * BK * 2;  // 32 KB
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr uint32_t TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
+constexpr int THREADS = 192;
+
+struct TcArgs {
+  const uint64_t* zq;  // [Q] zero-row masks of the probes
+  const uint64_t* zp;  // [cap] zero-row masks of the entries
+  uint32_t Q, P, L;
+  uint32_t n_m, n_n, n_k;
+  float eps2;
+  uint32_t* T;
+  uint32_t* bcnt;
+  uint2* bucket;
+  uint32_t bcap;
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// K-major operand tile, 128-byte swizzle: 8-row atoms of 128 B, atoms 1024 B
+// apart (SBO), LBO unused for swizzled K-major; version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor: A,B = F16 K-major, D = F32, M=128, N=256.
+constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | (0u << 15) | (0u << 16) |
+                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_tc_screen(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                const TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* zp_s = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);  // [2][BN]
+  uint64_t* full = zp_s + 2 * BN;
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n_tiles = a.n_m * a.n_n;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&ta);
+    prefetch_tmap(&tb);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t s = 0, ph = 0;
+      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const uint32_t m = t % a.n_m, n = t / a.n_m;
+        for (uint32_t kb = 0; kb < a.n_k; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(sA + s * A_BYTES, &ta, &full[s], (int)(kb * BK), (int)(m * BM));
+          tma_load_2d(sB + s * B_BYTES, &tb, &full[s], (int)(kb * BK), (int)(n * BN));
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t s = 0, ph = 0, i = 0;
+      for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+        const uint32_t acc = i & 1;
+        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (uint32_t kb = 0; kb < a.n_k; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint8_t* pa = sA + s * A_BYTES;
+          const uint8_t* pb = sB + s * B_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_f16(d, smem_desc_sw128(pa + 32 * k), smem_desc_sw128(pb + 32 * k),
+                    (kb | k) != 0 ? 1u : 0u);
+          mma_commit(&empty[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // epilogue: 4 warps, thread = accumulator lane = probe row of the tile
+    const uint32_t quarter = warp & 3;
+    const uint32_t row = quarter * 32 + lane;
+    const uint32_t et = threadIdx.x - 64;  // 0..127
+    const float invL = 1.0f / (float)a.L;
+    uint32_t i = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      const uint32_t acc = i & 1;
+      const uint32_t m = t % a.n_m, n = t / a.n_m;
+      uint64_t* zt = zp_s + acc * BN;
+      for (uint32_t j = et; j < BN; j += 128) {
+        const uint32_t p = n * BN + j;
+        zt[j] = p < a.P ? a.zp[p] : 0ull;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const uint32_t q = m * BM + row;
+      const bool qvalid = q < a.Q;
+      const uint64_t zq = qvalid ? a.zq[q] : 0ull;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((quarter * 32) << 16) + acc * BN;
+      float rmin = __uint_as_float(kFInf);
+      uint32_t r[32];
+#pragma unroll 1
+      for (uint32_t c = 0; c < BN / 32; ++c) {
+        tmem_ld32(tbase + c * 32, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t col = c * 32 + j;
+          const float sim = __uint_as_float(r[j]) + (float)__popcll(zq & zt[col]);
+          const float d = fmaxf(fmaf(-sim, invL, 1.0f), 0.0f);
+          if (n * BN + col < a.P) rmin = fminf(rmin, d);
+        }
+      }
+      float thr = __uint_as_float(kFInf);
+      if (qvalid) {
+        const uint32_t mb = __float_as_uint(rmin);
+        uint32_t tv = *reinterpret_cast<volatile uint32_t*>(&a.T[q]);
+        if (mb < tv) tv = min(atomicMin(&a.T[q], mb), mb);
+        thr = __uint_as_float(tv) + a.eps2;
+      }
+#pragma unroll 1
+      for (uint32_t c = 0; c < BN / 32; ++c) {
+        tmem_ld32(tbase + c * 32, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t col = c * 32 + j;
+          const float sim = __uint_as_float(r[j]) + (float)__popcll(zq & zt[col]);
+          const float d = fmaxf(fmaf(-sim, invL, 1.0f), 0.0f);
+          const uint32_t p = n * BN + col;
+          if (qvalid && p < a.P && d <= thr) {
+            const uint32_t pos = atomicAdd(&a.bcnt[q], 1u);
+            if (pos < a.bcap) a.bucket[(uint64_t)q * a.bcap + pos] = make_uint2(p, __float_as_uint(d));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+cudaError_t encode_2d_f16(const void* base, uint64_t rows, uint64_t Kp, uint32_t box_rows,
+                          CUtensorMap* map) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr);
+    if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {Kp, rows};
+  const cuuint64_t strides[1] = {Kp * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+float tc_eps2(uint32_t L, uint32_t E, uint32_t Kp) {
+  // |d16 - d_ref| <= 2.2*2^-11 (fp16 operand rounding, relative, per term;
+  // cos <= 1 per layer) + 2*E*2^-25 (subnormal floor) + Kp*2^-22 (fp32
+  // accumulation with truncation, partial sums <= L) -- DESIGN.md.
+  (void)L;
+  const double eps = 2.2 / 2048.0 + 2.0 * E / 33554432.0 + (double)Kp / 4194304.0 + 1e-6;
+  return (float)(2.0 * 1.25 * eps);
+}
+
+bool tc_supported(const DevColl& c) { return c.L <= 64 && c.nrm != nullptr && c.Kp > 0; }
+
+cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchWork& w, int n_sm,
+                             cudaStream_t st) {
+  if (c.size == 0 || pr.Q == 0) return cudaSuccess;
+  CUtensorMap ta, tb;
+  cudaError_t e = encode_2d_f16(pr.nrm, pr.Q, c.Kp, BM, &ta);
+  if (e != cudaSuccess) return e;
+  e = encode_2d_f16(c.nrm, c.cap, c.Kp, BN, &tb);
+  if (e != cudaSuccess) return e;
+  TcArgs a{};
+  a.zq = pr.zmask;
+  a.zp = c.zmask;
+  a.Q = pr.Q;
+  a.P = c.size;
+  a.L = c.L;
+  a.n_m = (pr.Q + BM - 1) / BM;
+  a.n_n = (c.size + BN - 1) / BN;
+  a.n_k = c.Kp / BK;
+  a.eps2 = w.eps2;
+  a.T = w.T;
+  a.bcnt = w.bcnt;
+  a.bucket = w.bucket;
+  a.bcap = w.bcap;
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + 2 * BN * 8 + (2 * STAGES + 4) * 8 + 16;
+  e = cudaFuncSetAttribute(k_tc_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t tiles = a.n_m * a.n_n;
+  const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)n_sm);
+  k_tc_screen<<<grid, THREADS, smem, st>>>(ta, tb, a);
+  return cudaGetLastError();
+}
+
+}  // namespace moe

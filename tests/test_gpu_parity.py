@@ -437,3 +437,58 @@ def test_trace_all_or_nothing(m):
     with pytest.raises(IndexError):
         m.trace_requests(s, picks, np.array([0, 2], np.uint64), counts=base)
     assert (base == 5).all()
+
+
+# ------------------------------------------------- tensor-core screen path
+@pytest.mark.parametrize("L,E,P,Q,seed", [
+    (12, 128, 2000, 300, 55),   # SW shape, ragged M and N tiles
+    (32, 8, 300, 200, 7),       # MIX
+    (59, 160, 300, 130, 9),     # DS (L=59 <= 64 zero-row mask bits)
+    (24, 128, 777, 256, 3),     # NL
+    (3, 5, 77, 129, 1),
+])
+def test_match_tensor_core_path(m, orc, monkeypatch, L, E, P, Q, seed):
+    monkeypatch.setenv("MOE_TC", "1")
+    fam = m.gen_bench_family(seed, L, E, P + Q)
+    e = filled(m, L, E, fam[:P])
+    check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
+
+
+def test_tensor_core_small_batches_and_edge_cases(m, orc, monkeypatch):
+    monkeypatch.setenv("MOE_TC", "1")
+    L, E, P = 6, 16, 600
+    fam = m.gen_bench_family(8, L, E, P + 200).copy()
+    rng = np.random.default_rng(3)
+    fam[rng.random((P + 200, L)) < 0.3] = 0
+    fam[P + 190:] = 0
+    fam[:5] = 0
+    fam[100:400] = fam[100]  # mass duplicates -> bucket overflow -> exact pass
+    e = filled(m, L, E, fam[:P])
+    for Q in (1, 7, 200):
+        check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:P + Q])
+    check_match(m, orc, e, fam[:P], seqs_of(P), fam[100:160])
+
+
+def test_tensor_core_wide_counts(m, orc, monkeypatch):
+    monkeypatch.setenv("MOE_TC", "1")
+    L, E, P = 4, 32, 500
+    fam = m.gen_bench_family(21, L, E, P + 150).copy()
+    fam[::5] *= 1900  # 2-byte storage, subnormal fp16 normalised values
+    e = filled(m, L, E, fam[:P])
+    check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
+
+
+def test_tensor_core_f2_and_build(m, orc, monkeypatch):
+    monkeypatch.setenv("MOE_TC", "1")
+    w = Workload(12, 64, 1, seed=1001)
+    ents = orc.request_eams(w, 400)
+    probes = np.stack([orc.iteration_probe(w, 500 + i, 1 + i % 8, i % 12) for i in range(150)])
+    e = filled(m, 12, 64, ents)
+    check_match(m, orc, e, ents, seqs_of(400), probes)
+    # replacement steps after a tensor-core-screened build keep the fp16 copy in sync
+    e2 = m.Eamc(m.ModelShape(12, 64), m.Phase.decode, 150)
+    slots = e2.build(ents)
+    _, _, want = orc.insert_replay(12, 64, 150, ents)
+    assert np.array_equal(slots, want)
+    cur_e, cur_s, _ = orc.insert_replay(12, 64, 150, ents)
+    check_match(m, orc, e2, cur_e, cur_s, probes)
