@@ -126,7 +126,9 @@ moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_byt
 moe_status moe_eamc_match(const moe_eamc* h, const uint64_t* probes, uint64_t n_probes,
                           moe_match* out, uint8_t* found);
 /* Device variant: probes are device [n][L][E] of probe_bytes (1, 2 or 8)
- * bytes per count, out is device moe_match[n]. */
+ * bytes per count, out is device moe_match[n].  stream NULL = the handle's
+ * internal stream (NOT the legacy default stream); pass the caller's stream
+ * to order the work with the caller's kernels and events. */
 moe_status moe_eamc_match_device(const moe_eamc* h, const void* probes, int probe_bytes,
                                  uint64_t n_probes, moe_match* out, void* stream);
 /* Eamc::match_within (eam.cpp:131-150): every entry within `window` of the

@@ -157,7 +157,7 @@ struct moe_eamc {
   PinBuf pin;
   // instrumentation (moe_eamc_set_profiling)
   bool prof = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   double ms[3] = {0, 0, 0};
   uint64_t calls[3] = {0, 0, 0};
 
@@ -176,7 +176,7 @@ struct moe_eamc {
 
 namespace {
 
-constexpr uint32_t kBucketCap = 64;
+constexpr uint32_t kBucketCap = 256;  // early tiles push before the shared threshold tightens
 
 // Grow the device collection to hold `need` entries (<= capacity).
 moe_status ensure_alloc(moe_eamc* h, uint64_t need) {
@@ -265,64 +265,77 @@ bool use_tc(const moe_eamc* h, uint64_t Q) {
   return Q >= 128;
 }
 
-// H2D (or D2D) + pack probes into h->packed/ia/sqa at the collection's
-// width, widening the collection if a count needs it.
-moe_status prep_probes(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bool src_device,
-                       cudaStream_t st, DevProbes* pr) {
+// Launch the packing of n probes (device source) at the collection's current
+// width; *dmax (device) receives the largest count.  No synchronisation.
+moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t n,
+                             cudaStream_t st, DevProbes* pr) {
   DevColl& c = h->c;
-  const uint64_t cells = (uint64_t)c.L * c.E;
-  const void* dsrc = src;
-  if (!src_device) {
-    CK(h->raw.ensure(n * cells * src_bytes));
-    CK(cudaMemcpyAsync(h->raw.p, src, n * cells * src_bytes, cudaMemcpyHostToDevice, st));
-    dsrc = h->raw.p;
+  const uint64_t LR = (uint64_t)c.L * c.RB;
+  CK(h->packed.ensure(n * LR + 16));
+  CK(h->ia.ensure(n * c.L * sizeof(float)));
+  CK(h->sqa.ensure(n * c.L * sizeof(double)));
+  CK(h->small.ensure(256));
+  CK(h->pin.ensure(256));
+  unsigned long long* dmax = h->small.as<unsigned long long>();
+  __half* nrm = nullptr;
+  uint64_t* zq = nullptr;
+  if (c.Kp && use_tc(h, n)) {
+    CK(h->nrm.ensure(n * c.Kp * sizeof(__half)));
+    CK(h->zq.ensure(n * 8));
+    nrm = h->nrm.as<__half>();
+    zq = h->zq.as<uint64_t>();
   }
-  for (;;) {
-    const uint64_t LR = (uint64_t)c.L * c.RB;
-    CK(h->packed.ensure(n * LR + 16));
-    CK(h->ia.ensure(n * c.L * sizeof(float)));
-    CK(h->sqa.ensure(n * c.L * sizeof(double)));
-    CK(h->small.ensure(256));
-    CK(h->pin.ensure(256));
-    unsigned long long* dmax = h->small.as<unsigned long long>();
-    CK(cudaMemsetAsync(dmax, 0, 8, st));
-    if (h->prof) CK(cudaEventRecord(h->ev[0], st));
-    __half* nrm = nullptr;
-    uint64_t* zq = nullptr;
-    if (c.Kp && use_tc(h, n)) {
-      CK(h->nrm.ensure(n * c.Kp * sizeof(__half)));
-      CK(h->zq.ensure(n * 8));
-      nrm = h->nrm.as<__half>();
-      zq = h->zq.as<uint64_t>();
-      CK(cudaMemsetAsync(nrm, 0, n * c.Kp * sizeof(__half), st));
-      CK(cudaMemsetAsync(zq, 0, n * 8, st));
-    }
-    CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, h->packed.as<uint8_t>(),
-                        h->ia.as<float>(), h->sqa.as<double>(), nullptr, 0, 0, dmax, nrm, c.Kp,
-                        zq, st));
-    pr->nrm = nrm;
-    pr->zmask = zq;
-    if (h->prof) CK(cudaEventRecord(h->ev[1], st));
-    CK(cudaMemcpyAsync(h->pin.p, dmax, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (h->prof) {
-      float t = 0.f;
-      CK(cudaEventElapsedTime(&t, h->ev[0], h->ev[1]));
-      h->ms[0] += t;
-      h->calls[0]++;
-    }
-    const uint64_t mx = *h->pin.as<unsigned long long>();
-    if (mx <= width_max(c.cb)) break;
-    if (mx > 65535ull)
-      return fail(MOE_ERR_OVERFLOW,
-                  "count %llu exceeds the 2-byte device storage of this build", (unsigned long long)mx);
-    CKS(widen(h));
-  }
+  CK(cudaMemsetAsync(dmax, 0, 8, st));
+  if (h->prof) CK(cudaEventRecord(h->ev[0], st));
+  CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, h->packed.as<uint8_t>(),
+                      h->ia.as<float>(), h->sqa.as<double>(), nullptr, 0, 0, dmax, nrm, c.Kp, zq,
+                      st));
+  if (h->prof) CK(cudaEventRecord(h->ev[1], st));
   pr->Q = (uint32_t)n;
   pr->packed = h->packed.as<uint8_t>();
   pr->ia = h->ia.as<float>();
   pr->sqa = h->sqa.as<double>();
+  pr->nrm = nrm;
+  pr->zmask = zq;
   return MOE_OK;
+}
+
+// Width check after the caller's synchronisation: widen if needed.  Returns
+// true when the packed probes are exact (nothing to redo).
+moe_status check_width(moe_eamc* h, uint64_t mx, bool* ok) {
+  *ok = mx <= width_max(h->c.cb);
+  if (*ok) return MOE_OK;
+  if (mx > 65535ull)
+    return fail(MOE_ERR_OVERFLOW, "count %llu exceeds the 2-byte device storage of this build",
+                (unsigned long long)mx);
+  return widen(h);
+}
+
+const void* stage_source(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bool src_device,
+                         cudaStream_t st, moe_status* status) {
+  *status = MOE_OK;
+  if (src_device) return src;
+  const uint64_t bytes = n * (uint64_t)h->c.L * h->c.E * src_bytes;
+  cudaError_t e = h->raw.ensure(bytes);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->raw.p, src, bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) *status = fail(MOE_ERR_CUDA, "probe upload: %s", cudaGetErrorString(e));
+  return h->raw.p;
+}
+
+// H2D (or D2D) + pack probes, synchronously width-checked.
+moe_status prep_probes(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bool src_device,
+                       cudaStream_t st, DevProbes* pr) {
+  moe_status ss;
+  const void* dsrc = stage_source(h, src, src_bytes, n, src_device, st, &ss);
+  CKS(ss);
+  for (;;) {
+    CKS(launch_probe_prep(h, dsrc, src_bytes, n, st, pr));
+    CK(cudaMemcpyAsync(h->pin.p, h->small.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bool ok = false;
+    CKS(check_width(h, *h->pin.as<unsigned long long>(), &ok));
+    if (ok) return MOE_OK;
+  }
 }
 
 uint32_t pick_qt(uint64_t Q) {
@@ -352,9 +365,10 @@ moe_status make_plan(moe_eamc* h, int mode, uint32_t QT, Plan* p) {
 
 // Full matching pipeline for an already-packed probe batch; `out` is a
 // device array.  Synchronizes `st` once (overflow check).
-moe_status match_packed(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaStream_t st) {
+// Screen + refine launches for packed probes (no synchronisation).
+moe_status launch_match(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaStream_t st,
+                        MatchWork* wout) {
   const uint64_t Q = pr.Q;
-  if (Q == 0) return MOE_OK;
   DevColl& c = h->c;
   CK(h->T.ensure(Q * 4));
   CK(h->bcnt.ensure(Q * 4));
@@ -372,42 +386,85 @@ moe_status match_packed(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaSt
   CK(cudaMemsetAsync(w.T, 0x7f, Q * 4, st));  // 0x7f7f7f7f = 3.4e38f > any distance
   CK(cudaMemsetAsync(w.bcnt, 0, Q * 4, st));
   CK(cudaMemsetAsync(w.over_n, 0, 4, st));
-  if (c.size == 0) {
-    CK(moe::launch_refine(c, pr, w, out, nullptr, nullptr, 0, st));
-    return MOE_OK;
-  }
   const bool tc = pr.nrm != nullptr && moe::tc_supported(c);
   w.eps2 = tc ? moe::tc_eps2(c.L, c.E, c.Kp) : moe::screen_eps2(c.L);
-  if (h->prof) CK(cudaEventRecord(h->ev[1], st));
-  if (tc) {
-    CK(moe::launch_tc_screen(c, pr, w, h->n_sm, st));
-  } else {
-    Plan p;
-    CKS(make_plan(h, 0, pick_qt(Q), &p));
-    CK(moe::launch_screen(p.map, c, pr, p.g, w, st));
-  }
   if (h->prof) CK(cudaEventRecord(h->ev[2], st));
-  CK(moe::launch_refine(c, pr, w, out, nullptr, nullptr, 0, st));
-  if (h->prof) CK(cudaEventRecord(h->ev[3], st));
-  CK(cudaMemcpyAsync(h->pin.p, w.over_n, 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (h->prof) {
-    float t1 = 0.f, t2 = 0.f;
-    CK(cudaEventElapsedTime(&t1, h->ev[1], h->ev[2]));
-    CK(cudaEventElapsedTime(&t2, h->ev[2], h->ev[3]));
-    h->ms[1] += t1;
-    h->ms[2] += t2;
-    h->calls[1]++;
-    h->calls[2]++;
+  if (c.size > 0) {
+    if (tc) {
+      CK(moe::launch_tc_screen(c, pr, w, h->n_sm, st));
+    } else {
+      Plan p;
+      CKS(make_plan(h, 0, pick_qt(Q), &p));
+      CK(moe::launch_screen(p.map, c, pr, p.g, w, st));
+    }
   }
-  const uint32_t n_over = *h->pin.as<uint32_t>();
+  if (h->prof) CK(cudaEventRecord(h->ev[3], st));
+  CK(moe::launch_refine(c, pr, w, out, nullptr, nullptr, 0, st));
+  if (h->prof) CK(cudaEventRecord(h->ev[4], st));
+  *wout = w;
+  return MOE_OK;
+}
+
+// Full matching pipeline with optimistic execution: probe packing, screen and
+// refine are launched back to back and ONE synchronisation then checks both
+// the probe count width (rare widening -> redo) and candidate-bucket overflow
+// (rare -> exact pass).  `out` is a device array; `pr` receives the packed
+// probes for follow-up passes.
+moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bool src_device,
+                     moe_match* out, cudaStream_t st, DevProbes* pr) {
+  if (n == 0) return MOE_OK;
+  moe_status ss;
+  const void* dsrc = stage_source(h, src, src_bytes, n, src_device, st, &ss);
+  CKS(ss);
+  for (;;) {
+    CKS(launch_probe_prep(h, dsrc, src_bytes, n, st, pr));
+    MatchWork w;
+    CKS(launch_match(h, *pr, out, st, &w));
+    CK(cudaMemcpyAsync(h->pin.p, h->small.p, 32, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h->prof) {
+      float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+      CK(cudaEventElapsedTime(&t0, h->ev[0], h->ev[1]));
+      CK(cudaEventElapsedTime(&t1, h->ev[2], h->ev[3]));
+      CK(cudaEventElapsedTime(&t2, h->ev[3], h->ev[4]));
+      h->ms[0] += t0;
+      h->ms[1] += t1;
+      h->ms[2] += t2;
+      h->calls[0]++;
+      h->calls[1]++;
+      h->calls[2]++;
+    }
+    bool ok = false;
+    CKS(check_width(h, *h->pin.as<unsigned long long>(), &ok));
+    if (!ok) continue;  // collection widened: redo with the wider packing
+    const uint32_t n_over = h->pin.as<uint32_t>()[4];  // w.over_n = small + 16 B
+    if (n_over) {
+      Plan pe;
+      CKS(make_plan(h, 1, 1, &pe));
+      w.part_chunk = 1024;
+      CK(h->partials.ensure((size_t)w.part_chunk * pe.g.grid * sizeof(moe_match)));
+      w.partials = h->partials.as<moe_match>();
+      CK(moe::launch_exact(pe.map, h->c, *pr, pe.g, w, w.over_list, n_over, w.T, out, st));
+    }
+    return MOE_OK;
+  }
+}
+
+// Compatibility wrapper used by the insert path: packed probes in hand.
+moe_status match_packed(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaStream_t st) {
+  if (pr.Q == 0) return MOE_OK;
+  MatchWork w;
+  CKS(launch_match(h, pr, out, st, &w));
+  CK(cudaMemcpyAsync(h->pin.p, h->small.p, 32, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const uint32_t n_over = h->pin.as<uint32_t>()[4];  // w.over_n = small + 16 B
   if (n_over) {
     Plan pe;
     CKS(make_plan(h, 1, 1, &pe));
     w.part_chunk = 1024;
     CK(h->partials.ensure((size_t)w.part_chunk * pe.g.grid * sizeof(moe_match)));
     w.partials = h->partials.as<moe_match>();
-    CK(moe::launch_exact(pe.map, c, pr, pe.g, w, w.over_list, n_over, w.T, out, st));
+    CK(moe::launch_exact(pe.map, h->c, pr, pe.g, w, w.over_list, n_over, w.T, out, st));
   }
   return MOE_OK;
 }
@@ -449,8 +506,6 @@ moe_status stage_entries(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t 
     if (c.Kp) {
       CK(s->nrm.ensure(n * c.Kp * sizeof(__half)));
       CK(s->zmask.ensure(n * 8));
-      CK(cudaMemsetAsync(s->nrm.p, 0, n * c.Kp * sizeof(__half), h->st));
-      CK(cudaMemsetAsync(s->zmask.p, 0, n * 8, h->st));
     }
     CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, s->packed.as<uint8_t>(),
                         s->ia.as<float>(), s->sqa.as<double>(), nullptr, 0, 0, dmax,
@@ -760,9 +815,8 @@ moe_status moe_eamc_match(const moe_eamc* hc, const uint64_t* probes, uint64_t n
   for (uint64_t off = 0; off < n_probes; off += chunk) {
     const uint64_t m = std::min(chunk, n_probes - off);
     DevProbes pr;
-    CKS(prep_probes(h, probes + off * cells, 8, m, false, h->st, &pr));
     CK(h->out.ensure(m * sizeof(moe_match)));
-    CKS(match_packed(h, pr, h->out.as<moe_match>(), h->st));
+    CKS(match_all(h, probes + off * cells, 8, m, false, h->out.as<moe_match>(), h->st, &pr));
     CK(cudaMemcpyAsync(out + off, h->out.p, m * sizeof(moe_match), cudaMemcpyDeviceToHost, h->st));
   }
   CK(cudaStreamSynchronize(h->st));
@@ -782,8 +836,7 @@ moe_status moe_eamc_match_device(const moe_eamc* hc, const void* probes, int pro
   DeviceGuard dg(h->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->st;
   DevProbes pr;
-  CKS(prep_probes(h, probes, probe_bytes, n_probes, true, st, &pr));
-  CKS(match_packed(h, pr, out, st));
+  CKS(match_all(h, probes, probe_bytes, n_probes, true, out, st, &pr));
   return MOE_OK;
 }
 
@@ -795,10 +848,9 @@ moe_status moe_eamc_match_within(const moe_eamc* hc, const uint64_t* probe, doub
   if (h->c.size == 0) return MOE_OK;
   DeviceGuard dg(h->device);
   DevProbes pr;
-  CKS(prep_probes(h, probe, 8, 1, false, h->st, &pr));
   CK(h->out.ensure(sizeof(moe_match)));
   moe_match* best = h->out.as<moe_match>();
-  CKS(match_packed(h, pr, best, h->st));
+  CKS(match_all(h, probe, 8, 1, false, best, h->st, &pr));
   CK(h->wl.ensure((size_t)h->c.size * sizeof(moe::WinEntry)));
   uint32_t* wl_n = h->small.as<uint32_t>() + 8;
   CK(cudaMemsetAsync(wl_n, 0, 4, h->st));
@@ -923,10 +975,9 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
   const bool prefetch_live = do_prefetch && h->c.size > 0;
   if (prefetch_live) {
     DevProbes pr;
-    CKS(prep_probes(h, cur_eam, 8, 1, false, st, &pr));
     CK(h->out.ensure(sizeof(moe_match)));
     moe_match* best = h->out.as<moe_match>();
-    CKS(match_packed(h, pr, best, st));
+    CKS(match_all(h, cur_eam, 8, 1, false, best, st, &pr));
     CK(h->wl.ensure((size_t)h->c.size * sizeof(moe::WinEntry)));
     uint32_t* wl_n = h->small.as<uint32_t>() + 8;
     CK(cudaMemsetAsync(wl_n, 0, 4, st));

@@ -362,13 +362,25 @@ struct RefineArgs {
   uint64_t index_base;
 };
 
+// One warp per probe.  The bucket's candidates that survive the final
+// threshold are evaluated exactly: (candidate, layer) pairs are spread over
+// the 32 lanes (integer row dots + the fp64 row similarity), the per-layer
+// values land in shared memory, and one lane per candidate then sums them in
+// layer order (eam.cpp:95-98) -- so the critical path grows with
+// candidates*L/32 instead of with the candidate count.
+constexpr int kRefineWarps = 4;
+constexpr int kRefineBuf = 256;  // doubles of per-warp scratch
+
 template <int CB>
-__global__ void k_refine(const RefineArgs r) {
-  const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r) {
+  __shared__ double rbuf[kRefineWarps][kRefineBuf];
+  __shared__ uint32_t cand[kRefineWarps][256];
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint32_t q = blockIdx.x * kRefineWarps + wib;
   const uint32_t lane = threadIdx.x & 31;
   if (q >= r.Q) return;
   if (r.halt && *r.halt) return;
-  moe_match none{kNone, kNone, __longlong_as_double(0x7ff0000000000000ll)};
+  const moe_match none{kNone, kNone, __longlong_as_double(0x7ff0000000000000ll)};
   if (r.size == 0) {
     if (lane == 0) r.out[q] = none;
     return;
@@ -381,31 +393,54 @@ __global__ void k_refine(const RefineArgs r) {
     }
     return;
   }
+  // compact the candidates that pass the final threshold
   const float thr = __uint_as_float(r.T[q]) + r.eps2;
-  Best b{__longlong_as_double(0x7ff0000000000000ll), kNone, kNone};
-  const uint64_t LR = (uint64_t)r.L * r.RB;
+  uint32_t nc = 0;
   for (uint32_t base = 0; base < n; base += 32) {
     const uint32_t i = base + lane;
-    bool cand = false;
+    bool pass = false;
     uint32_t p = 0;
     if (i < n) {
       const uint2 e = r.bucket[(uint64_t)q * r.bcap + i];
       p = e.x;
-      cand = __uint_as_float(e.y) <= thr;
+      pass = __uint_as_float(e.y) <= thr;
     }
-    uint32_t mask = __ballot_sync(0xffffffffu, cand);
-    while (mask) {
-      const int src = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const uint32_t pp = __shfl_sync(0xffffffffu, p, src);
-      const double d = warp_exact_distance<CB>(r.probes + q * LR, r.sqa + (uint64_t)q * r.L,
-                                               r.counts + pp * LR, r.sqb + (uint64_t)pp * r.L,
-                                               r.L, r.C, r.RB);
-      const uint64_t s = r.seq[pp];
-      if (better(d, s, b.d, b.seq)) b = Best{d, s, pp};
-    }
+    const uint32_t m = __ballot_sync(0xffffffffu, pass);
+    if (pass) cand[wib][nc + __popc(m & ((1u << lane) - 1))] = p;
+    nc += __popc(m);
   }
-  if (lane == 0) r.out[q] = moe_match{b.idx == kNone ? kNone : b.idx + r.index_base, b.seq, b.d};
+  __syncwarp();
+  const uint64_t LR = (uint64_t)r.L * r.RB;
+  const uint8_t* pa = r.probes + q * LR;
+  const double* sqa = r.sqa + (uint64_t)q * r.L;
+  Best b{__longlong_as_double(0x7ff0000000000000ll), kNone, kNone};
+  const uint32_t G = max(1u, (uint32_t)kRefineBuf / r.L);  // candidates per group
+  for (uint32_t g0 = 0; g0 < nc; g0 += G) {
+    const uint32_t gn = min(G, nc - g0);
+    const uint32_t pairs = gn * r.L;
+    for (uint32_t id = lane; id < pairs; id += 32) {
+      const uint32_t ci = id / r.L, l = id - ci * r.L;
+      const uint32_t p = cand[wib][g0 + ci];
+      typename Dot<CB>::Acc acc = 0;
+      const uint4* ra = reinterpret_cast<const uint4*>(pa + (uint64_t)l * r.RB);
+      const uint4* rb = reinterpret_cast<const uint4*>(r.counts + p * LR + (uint64_t)l * r.RB);
+      for (uint32_t c = 0; c < r.C; ++c) acc = Dot<CB>::chunk(ra[c], rb[c], acc);
+      rbuf[wib][ci * r.L + l] = row_sim_exact((uint64_t)acc, sqa[l], r.sqb[(uint64_t)p * r.L + l]);
+    }
+    __syncwarp();
+    if (lane < gn) {
+      const uint32_t p = cand[wib][g0 + lane];
+      const uint64_t sq = r.seq[p];
+      double sm = 0.0;
+      for (uint32_t l = 0; l < r.L; ++l) sm = __dadd_rn(sm, rbuf[wib][lane * r.L + l]);
+      const double d = finish_distance(sm, r.L);
+      if (better(d, sq, b.d, b.seq)) b = Best{d, sq, p};
+    }
+    __syncwarp();
+  }
+  b = warp_best(b);
+  if (lane == 0)
+    r.out[q] = moe_match{b.idx == kNone ? kNone : b.idx + r.index_base, b.seq, b.d};
 }
 
 // Partial merge for mode 1: for list position qi, the blocks whose item
@@ -460,56 +495,85 @@ __device__ __forceinline__ uint64_t load_count(const void* src, uint64_t i) {
 }
 
 template <int SRC>
-__global__ void k_prep(const void* src, uint64_t rows, uint32_t E, uint32_t L, uint32_t RB,
-                       int cb, uint8_t* dst, float* ia, double* sq, float* ibT, uint64_t ib_cap,
-                       uint64_t ib_base, unsigned long long* max_count, __half* nrm, uint32_t Kp,
-                       uint64_t* zmask) {
+__global__ void __launch_bounds__(256)
+    k_prep(const void* src, uint64_t rows, uint32_t E, uint32_t L, uint32_t RB, int cb,
+           uint8_t* dst, float* ia, double* sq, float* ibT, uint64_t ib_cap, uint64_t ib_base,
+           unsigned long long* max_count, uint64_t width_limit, __half* nrm, uint32_t Kp,
+           uint64_t* zmask) {
+  // One warp per row (max parallelism, short latency chain).  The host only
+  // needs to know whether some count exceeds the storage width, so the global
+  // max is touched only by rows that actually do (no atomics in the common
+  // case).  Zero rows set their bit in the (pre-zeroed) per-EAM mask; the last
+  // row of an EAM also writes the operand's K padding.
   const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (row >= rows) return;
+  const uint64_t it = row / L;
+  const uint32_t l = (uint32_t)(row - it * L);
   const uint64_t sbase = row * E;
   uint32_t* drow = reinterpret_cast<uint32_t*>(dst + row * RB);
   const uint32_t per_word = 4 / cb;
+  const uint32_t nwords = RB / 4;
+  constexpr int kWords = 4;
+  uint32_t words[kWords] = {0, 0, 0, 0};
   uint64_t ss = 0, mx = 0;
-  for (uint32_t w = lane; w < RB / 4; w += 32) {
+  for (uint32_t w = lane, k = 0; w < nwords; w += 32, ++k) {
     uint32_t word = 0;
-    for (uint32_t j = 0; j < per_word; ++j) {
-      const uint32_t e = w * per_word + j;
-      if (e < E) {
-        const uint64_t c = load_count<SRC>(src, sbase + e);
+    if (SRC == 1 && cb == 1 && (E & 3) == 0 && 4 * w + 3 < E) {
+      word = reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(src) + sbase)[w];
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t c = (word >> (8 * j)) & 0xffu;
         mx = c > mx ? c : mx;
-        ss += c * c;  // exact: the caller enforces c <= 65535
-        const uint64_t cc = cb == 1 ? (c & 0xffu) : (c & 0xffffu);
-        word |= (uint32_t)cc << (8 * cb * j);
+        ss += c * c;
+      }
+    } else {
+      for (uint32_t j = 0; j < per_word; ++j) {
+        const uint32_t e = w * per_word + j;
+        if (e < E) {
+          const uint64_t c = load_count<SRC>(src, sbase + e);
+          mx = c > mx ? c : mx;
+          ss += c * c;  // exact: counts above 65535 are rejected by the caller
+          const uint64_t cc = cb == 1 ? (c & 0xffu) : (c & 0xffffu);
+          word |= (uint32_t)cc << (8 * cb * j);
+        }
       }
     }
     drow[w] = word;
+    if (k < kWords) words[k] = word;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    const uint64_t m2 = __shfl_xor_sync(0xffffffffu, mx, o);
-    mx = m2 > mx ? m2 : mx;
-  }
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (max_count && mx > width_limit) atomicMax(max_count, (unsigned long long)mx);
   const double s = __dsqrt_rn(__ull2double_rn(ss));
   const float inv = ss ? __double2float_rn(__drcp_rn(s)) : 0.f;
   if (lane == 0) {
     sq[row] = s;
     if (ia) ia[row] = inv;
-    if (ibT) {
-      const uint64_t slot = ib_base + row / L;
-      const uint32_t l = (uint32_t)(row % L);
-      ibT[(uint64_t)l * ib_cap + slot] = inv;
-    }
-    if (max_count && mx) atomicMax(max_count, (unsigned long long)mx);
-    if (zmask && ss == 0) atomicOr(reinterpret_cast<unsigned long long*>(&zmask[row / L]),
-                                   1ull << (row % L));
+    if (ibT) ibT[(uint64_t)l * ib_cap + ib_base + it] = inv;
+    if (zmask && ss == 0)
+      atomicOr(reinterpret_cast<unsigned long long*>(&zmask[it]), 1ull << (l & 63));
   }
-  if (nrm && ss) {  // unit-normalised fp16 row of the tensor-core screen operand
-    __half* o = nrm + (row / L) * (uint64_t)Kp + (row % L) * (uint64_t)E;
-    for (uint32_t e = lane; e < E; e += 32) {
-      const uint64_t c = load_count<SRC>(src, sbase + e);
-      o[e] = __float2half_rn(__uint2float_rn((uint32_t)c) * inv);
+  if (nrm) {  // unit-normalised fp16 row of the tensor-core screen operand
+    __half* o = nrm + it * (uint64_t)Kp + (uint64_t)l * E;
+    if (nwords <= 32 * kWords) {
+      for (uint32_t w = lane, k = 0; w < nwords; w += 32, ++k) {
+        const uint32_t word = k < kWords ? words[k] : 0u;
+        for (uint32_t j = 0; j < per_word; ++j) {
+          const uint32_t e = w * per_word + j;
+          if (e < E) {
+            const uint32_t c =
+                cb == 1 ? (word >> (8 * j)) & 0xffu : (word >> (16 * j)) & 0xffffu;
+            o[e] = __float2half_rn(__uint2float_rn(c) * inv);
+          }
+        }
+      }
+    } else {
+      for (uint32_t e = lane; e < E; e += 32)
+        o[e] = __float2half_rn(__uint2float_rn((uint32_t)load_count<SRC>(src, sbase + e)) * inv);
+    }
+    if (l == L - 1) {
+      __half* orow = nrm + it * (uint64_t)Kp;
+      for (uint32_t k = L * E + lane; k < Kp; k += 32) orow[k] = __float2half_rn(0.f);
     }
   }
 }
@@ -823,8 +887,12 @@ __global__ void k_trace_commit64(const uint32_t* scratch, uint64_t n, const int*
 
 template <int CB, int QT, int MODE>
 cudaError_t set_smem_attr(size_t smem) {
-  return cudaFuncSetAttribute(k_match<CB, QT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem);
+  static size_t set = 0;  // cudaFuncSetAttribute only when the requirement grows
+  if (smem <= set) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_match<CB, QT, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) set = smem;
+  return e;
 }
 
 template <int CB, int QT, int MODE>
@@ -1002,29 +1070,26 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
                         uint32_t RB, int cb, uint8_t* dst, float* ia, double* sq, float* ibT,
                         uint64_t ib_cap, uint64_t ib_base, unsigned long long* max_count,
                         __half* nrm, uint32_t Kp, uint64_t* zmask, cudaStream_t st) {
-  const uint64_t rows = n * L;
-  if (rows == 0) return cudaSuccess;
+  if (n == 0) return cudaSuccess;
   const uint32_t threads = 256;
+  const uint64_t rows = n * L;
   const uint64_t blocks = (rows * 32 + threads - 1) / threads;
-  switch (src_bytes) {
-    case 8:
-      k_prep<8><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,
-                                                      ib_cap, ib_base, max_count, nrm, Kp,
-                                                      zmask);
-      break;
-    case 2:
-      k_prep<2><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,
-                                                      ib_cap, ib_base, max_count, nrm, Kp,
-                                                      zmask);
-      break;
-    case 1:
-      k_prep<1><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,
-                                                      ib_cap, ib_base, max_count, nrm, Kp,
-                                                      zmask);
-      break;
-    default:
-      return cudaErrorInvalidValue;
+  const uint64_t limit = cb == 1 ? 255ull : 65535ull;
+  if (zmask) {
+    cudaError_t e = cudaMemsetAsync(zmask, 0, n * sizeof(uint64_t), st);
+    if (e != cudaSuccess) return e;
   }
+#define MOE_PREP(S)                                                                            \
+  k_prep<S><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,    \
+                                                  ib_cap, ib_base, max_count, limit, nrm, Kp,  \
+                                                  zmask)
+  switch (src_bytes) {
+    case 8: MOE_PREP(8); break;
+    case 2: MOE_PREP(2); break;
+    case 1: MOE_PREP(1); break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef MOE_PREP
   return cudaGetLastError();
 }
 
@@ -1066,12 +1131,11 @@ cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork
   r.halt_set = halt_set;
   r.halt_value = halt_value;
   r.index_base = c.index_base;
-  const uint32_t threads = 256;
-  const uint32_t blocks = (uint32_t)(((uint64_t)pr.Q * 32 + threads - 1) / threads);
+  const uint32_t blocks = (pr.Q + kRefineWarps - 1) / kRefineWarps;
   if (c.cb == 1)
-    k_refine<1><<<blocks, threads, 0, st>>>(r);
+    k_refine<1><<<blocks, kRefineWarps * 32, 0, st>>>(r);
   else
-    k_refine<2><<<blocks, threads, 0, st>>>(r);
+    k_refine<2><<<blocks, kRefineWarps * 32, 0, st>>>(r);
   return cudaGetLastError();
 }
 

@@ -316,11 +316,30 @@ bool tc_supported(const DevColl& c) { return c.L <= 64 && c.nrm != nullptr && c.
 cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchWork& w, int n_sm,
                              cudaStream_t st) {
   if (c.size == 0 || pr.Q == 0) return cudaSuccess;
-  CUtensorMap ta, tb;
-  cudaError_t e = encode_2d_f16(pr.nrm, pr.Q, c.Kp, BM, &ta);
-  if (e != cudaSuccess) return e;
-  e = encode_2d_f16(c.nrm, c.cap, c.Kp, BN, &tb);
-  if (e != cudaSuccess) return e;
+  // tensor maps are re-encoded only when the operand buffers change
+  struct MapCache {
+    const void* base = nullptr;
+    uint64_t rows = 0, Kp = 0;
+    CUtensorMap map;
+  };
+  static thread_local MapCache ca, cb;
+  cudaError_t e = cudaSuccess;
+  if (ca.base != pr.nrm || ca.rows != pr.Q || ca.Kp != c.Kp) {
+    e = encode_2d_f16(pr.nrm, pr.Q, c.Kp, BM, &ca.map);
+    if (e != cudaSuccess) return e;
+    ca.base = pr.nrm;
+    ca.rows = pr.Q;
+    ca.Kp = c.Kp;
+  }
+  if (cb.base != c.nrm || cb.rows != c.cap || cb.Kp != c.Kp) {
+    e = encode_2d_f16(c.nrm, c.cap, c.Kp, BN, &cb.map);
+    if (e != cudaSuccess) return e;
+    cb.base = c.nrm;
+    cb.rows = c.cap;
+    cb.Kp = c.Kp;
+  }
+  const CUtensorMap& ta = ca.map;
+  const CUtensorMap& tb = cb.map;
   TcArgs a{};
   a.zq = pr.zmask;
   a.zp = c.zmask;
@@ -336,8 +355,12 @@ cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchW
   a.bucket = w.bucket;
   a.bcap = w.bcap;
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 2 * BN * 8 + (2 * STAGES + 4) * 8 + 16;
-  e = cudaFuncSetAttribute(k_tc_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(k_tc_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   const uint32_t tiles = a.n_m * a.n_n;
   const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)n_sm);
   k_tc_screen<<<grid, THREADS, smem, st>>>(ta, tb, a);

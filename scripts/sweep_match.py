@@ -34,7 +34,9 @@ def main():
     e.append(fam, np.arange(P, dtype=np.uint64))
     del fam
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sp = C.c_void_p(stream.cuda_stream)
     for Q in [int(x) for x in a.qs.split(",")]:
         pr = torch.from_numpy(m.gen_bench_family(55, L, E, Q, skip=P, dtype=np.uint8)).cuda()
         out = torch.empty((Q, 3), dtype=torch.float64, device="cuda")
