@@ -155,11 +155,19 @@ struct moe_eamc {
   DevBuf raw, packed, ia, sqa, nrm, zq, T, bcnt, bucket, over_list, small, out, partials, wl,
       agg, cand, slots, req;
   PinBuf pin;
-  // instrumentation (moe_eamc_set_profiling)
+  // instrumentation (moe_eamc_set_profiling): a ring of event sets so the
+  // asynchronous device path can be timed without synchronising per call
+  struct EvSet {
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool pending = false;
+  };
   bool prof = false;
-  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  std::vector<EvSet> ring;
+  size_t ring_i = 0;
+  cudaEvent_t* ev = nullptr;  // events of the call in flight
   double ms[3] = {0, 0, 0};
   uint64_t calls[3] = {0, 0, 0};
+  DevBuf wide;
 
   ~moe_eamc() {
     if (c.counts) cudaFree(c.counts);
@@ -168,8 +176,9 @@ struct moe_eamc {
     if (c.seq) cudaFree(c.seq);
     if (c.nrm) cudaFree(c.nrm);
     if (c.zmask) cudaFree(c.zmask);
-    for (cudaEvent_t e : ev)
-      if (e) cudaEventDestroy(e);
+    for (EvSet& es : ring)
+      for (cudaEvent_t e : es.ev)
+        if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -265,6 +274,35 @@ bool use_tc(const moe_eamc* h, uint64_t Q) {
   return Q >= 128;
 }
 
+// Fold a completed event set into the per-kernel totals.
+moe_status prof_collect(moe_eamc* h, moe_eamc::EvSet& es) {
+  if (!es.pending) return MOE_OK;
+  CK(cudaEventSynchronize(es.ev[4]));
+  float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+  CK(cudaEventElapsedTime(&t0, es.ev[0], es.ev[1]));
+  CK(cudaEventElapsedTime(&t1, es.ev[2], es.ev[3]));
+  CK(cudaEventElapsedTime(&t2, es.ev[3], es.ev[4]));
+  h->ms[0] += t0;
+  h->ms[1] += t1;
+  h->ms[2] += t2;
+  h->calls[0]++;
+  h->calls[1]++;
+  h->calls[2]++;
+  es.pending = false;
+  return MOE_OK;
+}
+
+// Pick the event set for the next matching call (collecting whatever it held).
+moe_status prof_begin(moe_eamc* h) {
+  if (!h->prof) return MOE_OK;
+  moe_eamc::EvSet& es = h->ring[h->ring_i];
+  h->ring_i = (h->ring_i + 1) % h->ring.size();
+  CKS(prof_collect(h, es));
+  es.pending = true;
+  h->ev = es.ev;
+  return MOE_OK;
+}
+
 // Launch the packing of n probes (device source) at the collection's current
 // width; *dmax (device) receives the largest count.  No synchronisation.
 moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t n,
@@ -285,11 +323,12 @@ moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint6
     nrm = h->nrm.as<__half>();
     zq = h->zq.as<uint64_t>();
   }
+  CK(h->wide.ensure(n));
   CK(cudaMemsetAsync(dmax, 0, 8, st));
   if (h->prof) CK(cudaEventRecord(h->ev[0], st));
   CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, h->packed.as<uint8_t>(),
                       h->ia.as<float>(), h->sqa.as<double>(), nullptr, 0, 0, dmax, nrm, c.Kp, zq,
-                      st));
+                      h->wide.as<uint8_t>(), st));
   if (h->prof) CK(cudaEventRecord(h->ev[1], st));
   pr->Q = (uint32_t)n;
   pr->packed = h->packed.as<uint8_t>();
@@ -297,6 +336,7 @@ moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint6
   pr->sqa = h->sqa.as<double>();
   pr->nrm = nrm;
   pr->zmask = zq;
+  pr->wide = h->wide.as<uint8_t>();
   return MOE_OK;
 }
 
@@ -329,7 +369,11 @@ moe_status prep_probes(moe_eamc* h, const void* src, int src_bytes, uint64_t n, 
   const void* dsrc = stage_source(h, src, src_bytes, n, src_device, st, &ss);
   CKS(ss);
   for (;;) {
-    CKS(launch_probe_prep(h, dsrc, src_bytes, n, st, pr));
+    const bool prof = h->prof;
+    h->prof = false;  // standalone packing is not part of the matcher's timing
+    const moe_status ps = launch_probe_prep(h, dsrc, src_bytes, n, st, pr);
+    h->prof = prof;
+    CKS(ps);
     CK(cudaMemcpyAsync(h->pin.p, h->small.p, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     bool ok = false;
@@ -405,35 +449,40 @@ moe_status launch_match(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaSt
   return MOE_OK;
 }
 
-// Full matching pipeline with optimistic execution: probe packing, screen and
-// refine are launched back to back and ONE synchronisation then checks both
-// the probe count width (rare widening -> redo) and candidate-bucket overflow
-// (rare -> exact pass).  `out` is a device array; `pr` receives the packed
-// probes for follow-up passes.
+// Full matching pipeline.  Probe packing, screen and refine are launched back
+// to back.  Synchronous mode (host API): ONE synchronisation then checks the
+// probe count width (rare widening -> redo) and candidate-bucket overflow
+// (rare -> exact pass).  Asynchronous mode (device API): nothing waits on the
+// host -- the exact pass is launched device-gated on the overflow count, and
+// probes whose counts exceed the storage width get the sentinel result
+// {UINT64_MAX-1, UINT64_MAX, NaN}.  `out` is a device array; `pr` receives
+// the packed probes for follow-up passes.
 moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bool src_device,
-                     moe_match* out, cudaStream_t st, DevProbes* pr) {
+                     moe_match* out, cudaStream_t st, DevProbes* pr, bool async = false) {
   if (n == 0) return MOE_OK;
   moe_status ss;
   const void* dsrc = stage_source(h, src, src_bytes, n, src_device, st, &ss);
   CKS(ss);
   for (;;) {
+    CKS(prof_begin(h));
     CKS(launch_probe_prep(h, dsrc, src_bytes, n, st, pr));
     MatchWork w;
     CKS(launch_match(h, *pr, out, st, &w));
+    if (async) {
+      if (h->c.size) {
+        Plan pe;
+        CKS(make_plan(h, 1, 1, &pe));
+        w.part_chunk = (uint32_t)std::min<uint64_t>(n, 8192);
+        CK(h->partials.ensure((size_t)w.part_chunk * pe.g.grid * sizeof(moe_match)));
+        w.partials = h->partials.as<moe_match>();
+        CK(moe::launch_exact(pe.map, h->c, *pr, pe.g, w, w.over_list, (uint32_t)n, w.T, out, st,
+                             w.over_n));
+      }
+      return MOE_OK;
+    }
     CK(cudaMemcpyAsync(h->pin.p, h->small.p, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (h->prof) {
-      float t0 = 0.f, t1 = 0.f, t2 = 0.f;
-      CK(cudaEventElapsedTime(&t0, h->ev[0], h->ev[1]));
-      CK(cudaEventElapsedTime(&t1, h->ev[2], h->ev[3]));
-      CK(cudaEventElapsedTime(&t2, h->ev[3], h->ev[4]));
-      h->ms[0] += t0;
-      h->ms[1] += t1;
-      h->ms[2] += t2;
-      h->calls[0]++;
-      h->calls[1]++;
-      h->calls[2]++;
-    }
+    if (h->prof) CKS(prof_collect(h, h->ring[(h->ring_i + h->ring.size() - 1) % h->ring.size()]));
     bool ok = false;
     CKS(check_width(h, *h->pin.as<unsigned long long>(), &ok));
     if (!ok) continue;  // collection widened: redo with the wider packing
@@ -454,7 +503,11 @@ moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bo
 moe_status match_packed(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaStream_t st) {
   if (pr.Q == 0) return MOE_OK;
   MatchWork w;
-  CKS(launch_match(h, pr, out, st, &w));
+  const bool prof = h->prof;
+  h->prof = false;
+  const moe_status ls = launch_match(h, pr, out, st, &w);
+  h->prof = prof;
+  CKS(ls);
   CK(cudaMemcpyAsync(h->pin.p, h->small.p, 32, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const uint32_t n_over = h->pin.as<uint32_t>()[4];  // w.over_n = small + 16 B
@@ -510,7 +563,7 @@ moe_status stage_entries(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t 
     CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, s->packed.as<uint8_t>(),
                         s->ia.as<float>(), s->sqa.as<double>(), nullptr, 0, 0, dmax,
                         c.Kp ? s->nrm.as<__half>() : nullptr, c.Kp,
-                        c.Kp ? s->zmask.as<uint64_t>() : nullptr, h->st));
+                        c.Kp ? s->zmask.as<uint64_t>() : nullptr, nullptr, h->st));
     CK(cudaMemcpyAsync(h->pin.p, dmax, 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     const uint64_t mx = *h->pin.as<unsigned long long>();
@@ -836,7 +889,7 @@ moe_status moe_eamc_match_device(const moe_eamc* hc, const void* probes, int pro
   DeviceGuard dg(h->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->st;
   DevProbes pr;
-  CKS(match_all(h, probes, probe_bytes, n_probes, true, out, st, &pr));
+  CKS(match_all(h, probes, probe_bytes, n_probes, true, out, st, &pr, /*async=*/true));
   return MOE_OK;
 }
 
@@ -908,8 +961,12 @@ moe_status moe_eamc_set_index_base(moe_eamc* h, uint64_t base) {
 moe_status moe_eamc_set_profiling(moe_eamc* h, int enable) {
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
   DeviceGuard dg(h->device);
-  for (cudaEvent_t& e : h->ev)
-    if (!e) CK(cudaEventCreate(&e));
+  if (h->ring.empty()) {
+    h->ring.resize(256);
+    for (auto& es : h->ring)
+      for (cudaEvent_t& e : es.ev) CK(cudaEventCreate(&e));
+  }
+  for (auto& es : h->ring) es.pending = false;
   h->prof = enable != 0;
   for (int i = 0; i < 3; ++i) {
     h->ms[i] = 0.0;
@@ -918,8 +975,11 @@ moe_status moe_eamc_set_profiling(moe_eamc* h, int enable) {
   return MOE_OK;
 }
 
-moe_status moe_eamc_kernel_times(const moe_eamc* h, double* ms, uint64_t* calls) {
+moe_status moe_eamc_kernel_times(const moe_eamc* hc, double* ms, uint64_t* calls) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  DeviceGuard dg(h->device);
+  for (auto& es : h->ring) CKS(prof_collect(h, es));
   for (int i = 0; i < 3; ++i) {
     if (ms) ms[i] = h->ms[i];
     if (calls) calls[i] = h->calls[i];

@@ -92,6 +92,8 @@ struct MatchArgs {
   const uint32_t* qlist;   // null: the single probe q_single
   uint32_t q_single;
   uint32_t nq_list;
+  const uint32_t* nq_dev;  // mode 1: list length read on the device (minus q_off, capped)
+  uint32_t q_off;
   const uint32_t* Tfinal;  // mode 1 candidate threshold (null: all)
   moe_match* partials;     // mode 1 [nq_list][grid]
   const moe_match* best;   // mode 2
@@ -129,7 +131,11 @@ __global__ void __launch_bounds__(kNT, 1)
   Best* wbest = reinterpret_cast<Best*>(smem + lay.off_wbest);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.off_bars);
 
-  const uint32_t nq = MODE == 0 ? (a.Q + QT - 1) / QT : a.nq_list;
+  uint32_t nq = MODE == 0 ? (a.Q + QT - 1) / QT : a.nq_list;
+  if (MODE == 1 && a.nq_dev) {  // device-gated exact pass: no work unless buckets overflowed
+    const uint32_t tot = *a.nq_dev;
+    nq = tot > a.q_off ? min(tot - a.q_off, a.nq_list) : 0u;
+  }
   const uint64_t n_items = (uint64_t)nq * a.n_pt;
   const uint64_t it0 = n_items * blockIdx.x / gridDim.x;
   const uint64_t it1 = n_items * (blockIdx.x + 1) / gridDim.x;
@@ -355,6 +361,7 @@ struct RefineArgs {
   uint32_t bcap;
   uint32_t* over_list;
   uint32_t* over_n;
+  const uint8_t* wide;  // probes whose counts exceed the storage width
   moe_match* out;
   const int* halt;
   int* halt_set;
@@ -383,6 +390,10 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
   const moe_match none{kNone, kNone, __longlong_as_double(0x7ff0000000000000ll)};
   if (r.size == 0) {
     if (lane == 0) r.out[q] = none;
+    return;
+  }
+  if (r.wide && r.wide[q]) {  // cannot be matched at this width: explicit sentinel
+    if (lane == 0) r.out[q] = moe_match{kNone - 1, kNone, __longlong_as_double(0x7ff8000000000000ll)};
     return;
   }
   const uint32_t n = r.bcnt[q];
@@ -447,7 +458,11 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
 // range intersects [qi*n_pt, (qi+1)*n_pt).
 __global__ void k_merge_partials(const moe_match* parts, uint32_t grid, uint32_t nq,
                                  uint32_t n_pt, const uint32_t* qlist, moe_match* out,
-                                 uint64_t index_base) {
+                                 uint64_t index_base, const uint32_t* nq_dev, uint32_t q_off) {
+  if (nq_dev) {
+    const uint32_t tot = *nq_dev;
+    nq = tot > q_off ? min(tot - q_off, nq) : 0u;
+  }
   const uint32_t qi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (qi >= nq) return;
@@ -499,7 +514,7 @@ __global__ void __launch_bounds__(256)
     k_prep(const void* src, uint64_t rows, uint32_t E, uint32_t L, uint32_t RB, int cb,
            uint8_t* dst, float* ia, double* sq, float* ibT, uint64_t ib_cap, uint64_t ib_base,
            unsigned long long* max_count, uint64_t width_limit, __half* nrm, uint32_t Kp,
-           uint64_t* zmask) {
+           uint64_t* zmask, uint8_t* wide) {
   // One warp per row (max parallelism, short latency chain).  The host only
   // needs to know whether some count exceeds the storage width, so the global
   // max is touched only by rows that actually do (no atomics in the common
@@ -543,7 +558,10 @@ __global__ void __launch_bounds__(256)
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (max_count && mx > width_limit) atomicMax(max_count, (unsigned long long)mx);
+  if (mx > width_limit) {
+    if (max_count) atomicMax(max_count, (unsigned long long)mx);
+    if (wide) wide[it] = 1;  // this EAM does not fit the storage width
+  }
   const double s = __dsqrt_rn(__ull2double_rn(ss));
   const float inv = ss ? __double2float_rn(__drcp_rn(s)) : 0.f;
   if (lane == 0) {
@@ -1069,7 +1087,8 @@ cudaError_t encode_tmap(const DevColl& c, uint32_t G, CUtensorMap* map) {
 cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, uint32_t E,
                         uint32_t RB, int cb, uint8_t* dst, float* ia, double* sq, float* ibT,
                         uint64_t ib_cap, uint64_t ib_base, unsigned long long* max_count,
-                        __half* nrm, uint32_t Kp, uint64_t* zmask, cudaStream_t st) {
+                        __half* nrm, uint32_t Kp, uint64_t* zmask, uint8_t* wide,
+                        cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const uint32_t threads = 256;
   const uint64_t rows = n * L;
@@ -1079,10 +1098,14 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
     cudaError_t e = cudaMemsetAsync(zmask, 0, n * sizeof(uint64_t), st);
     if (e != cudaSuccess) return e;
   }
+  if (wide) {
+    cudaError_t e = cudaMemsetAsync(wide, 0, n, st);
+    if (e != cudaSuccess) return e;
+  }
 #define MOE_PREP(S)                                                                            \
   k_prep<S><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,    \
                                                   ib_cap, ib_base, max_count, limit, nrm, Kp,  \
-                                                  zmask)
+                                                  zmask, wide)
   switch (src_bytes) {
     case 8: MOE_PREP(8); break;
     case 2: MOE_PREP(2); break;
@@ -1126,6 +1149,7 @@ cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork
   r.bcap = w.bcap;
   r.over_list = w.over_list;
   r.over_n = w.over_n;
+  r.wide = pr.wide;
   r.out = out;
   r.halt = halt;
   r.halt_set = halt_set;
@@ -1141,7 +1165,8 @@ cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork
 
 cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
                          const MatchGeom& g, const MatchWork& w, const uint32_t* qlist,
-                         uint32_t qlist_n, const uint32_t* T, moe_match* out, cudaStream_t st) {
+                         uint32_t qlist_n, const uint32_t* T, moe_match* out, cudaStream_t st,
+                         const uint32_t* nq_dev) {
   if (qlist_n == 0) return cudaSuccess;
   for (uint32_t off = 0; off < qlist_n; off += w.part_chunk) {
     const uint32_t n = std::min(w.part_chunk, qlist_n - off);
@@ -1149,6 +1174,8 @@ cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProb
     a.eps2 = std::max(a.eps2, w.eps2);  // band of whichever screen produced T
     a.qlist = qlist + off;
     a.nq_list = n;
+    a.nq_dev = nq_dev;
+    a.q_off = off;
     a.Tfinal = T;
     a.partials = w.partials;
     cudaError_t e = dispatch_match<1>(c.cb, 1, map, a, g, st);
@@ -1156,7 +1183,7 @@ cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProb
     const uint32_t threads = 256;
     const uint32_t blocks = (uint32_t)(((uint64_t)n * 32 + threads - 1) / threads);
     k_merge_partials<<<blocks, threads, 0, st>>>(w.partials, g.grid, n, g.n_pt, qlist + off, out,
-                                                 c.index_base);
+                                                 c.index_base, nq_dev, off);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

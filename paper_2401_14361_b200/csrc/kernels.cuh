@@ -36,6 +36,7 @@ struct DevProbes {
   double* sqa = nullptr;      // [Q][L]
   __half* nrm = nullptr;      // [Q][Kp] (tensor-core screen operand) or null
   uint64_t* zmask = nullptr;  // [Q]
+  uint8_t* wide = nullptr;    // [Q] 1 = a count exceeds the collection's storage width
 };
 
 struct MatchGeom {
@@ -74,7 +75,8 @@ cudaError_t encode_tmap(const DevColl& c, uint32_t G, CUtensorMap* map);
 cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, uint32_t E,
                         uint32_t RB, int cb, uint8_t* dst, float* ia, double* sq, float* ibT,
                         uint64_t ib_cap, uint64_t ib_base, unsigned long long* max_count,
-                        __half* nrm, uint32_t Kp, uint64_t* zmask, cudaStream_t st);
+                        __half* nrm, uint32_t Kp, uint64_t* zmask, uint8_t* wide,
+                        cudaStream_t st);
 
 // Tensor-core (tcgen05 kind::f16) screen pass for large probe batches.
 float tc_eps2(uint32_t L, uint32_t E, uint32_t Kp);
@@ -92,7 +94,8 @@ cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork
 // chunk of them starting at qlist_off); T may be null (evaluate all).
 cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
                          const MatchGeom& g, const MatchWork& w, const uint32_t* qlist,
-                         uint32_t qlist_n, const uint32_t* T, moe_match* out, cudaStream_t st);
+                         uint32_t qlist_n, const uint32_t* T, moe_match* out, cudaStream_t st,
+                         const uint32_t* nq_dev = nullptr);
 // mode 2: window membership for probe q0 (exact d <= best.distance + window).
 cudaError_t launch_window(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
                           const MatchGeom& g, uint32_t q0, const moe_match* best, double window,

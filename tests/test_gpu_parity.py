@@ -492,3 +492,34 @@ def test_tensor_core_f2_and_build(m, orc, monkeypatch):
     assert np.array_equal(slots, want)
     cur_e, cur_s, _ = orc.insert_replay(12, 64, 150, ents)
     check_match(m, orc, e2, cur_e, cur_s, probes)
+
+
+def test_device_api_async_width_sentinel_and_overflow(m, orc):
+    """The device path never waits on the host: a probe wider than the storage
+    width gets the sentinel, and mass ties are resolved by the device-gated
+    exact pass."""
+    import ctypes as C
+    import torch
+    from paper_2401_14361_b200 import _lib
+    L, E, P = 6, 32, 400
+    fam = m.gen_bench_family(12, L, E, P + 10).copy()
+    fam[50:300] = fam[50]  # 250 exact duplicates -> bucket overflow for probe 0
+    e = filled(m, L, E, fam[:P])
+    probes = np.concatenate([fam[50:51], fam[P:P + 8], fam[P + 8:P + 9] * 300])  # last: > 255
+    st = torch.cuda.Stream()
+    pr = torch.from_numpy(probes.astype(np.int64)).cuda()
+    out = torch.zeros((len(probes), 3), dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(st):
+        _lib.check(_lib.lib.moe_eamc_match_device(e._h, pr.data_ptr(), 8, len(probes),
+                                                  out.data_ptr(), C.c_void_p(st.cuda_stream)))
+    st.synchronize()
+    res = out.cpu().numpy().view(np.uint8).reshape(len(probes), 24).copy().view(
+        _lib.MATCH_DTYPE)[:, 0]
+    idx, seq, d, _ = orc.match(fam[:P], seqs_of(P), probes[:-1])
+    assert np.array_equal(res["index"][:-1], idx) and np.array_equal(res["distance"][:-1], d)
+    assert int(res["index"][-1]) == 0xFFFFFFFFFFFFFFFE and np.isnan(res["distance"][-1])
+    assert e.count_bytes() == 1  # the device path never widens behind the caller's back
+    # the host API widens and answers the same probe exactly
+    got = e.match_batch(probes[-1:])
+    i2, s2, d2, _ = orc.match(fam[:P], seqs_of(P), probes[-1:])
+    assert got["index"][0] == i2[0] and got["distance"][0] == d2[0]
