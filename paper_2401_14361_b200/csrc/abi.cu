@@ -153,7 +153,7 @@ struct moe_eamc {
   cudaStream_t st = nullptr;
   // workspace
   DevBuf raw, packed, ia, sqa, nrm, zq, T, bcnt, bucket, over_list, small, out, partials, wl,
-      agg, cand, slots, req;
+      agg, cand, slots, req, dist, rsim, keys, mem;
   PinBuf pin;
   // instrumentation (moe_eamc_set_profiling): a ring of event sets so the
   // asynchronous device path can be timed without synchronising per call
@@ -497,6 +497,29 @@ moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bo
     }
     return MOE_OK;
   }
+}
+
+// Exact distance of one host probe to every entry (dist[p] in h->dist) and
+// the minimum (*h->small @224) -- the single collection pass behind
+// match_within and prefetch_priorities.  Asynchronous; the caller checks the
+// probe width (dmax @0) after its synchronisation.
+moe_status launch_exact_distances(moe_eamc* h, const uint64_t* probe, cudaStream_t st,
+                                  DevProbes* pr) {
+  moe_status ss;
+  const void* dsrc = stage_source(h, probe, 8, 1, false, st, &ss);
+  CKS(ss);
+  const bool prof = h->prof;
+  h->prof = false;
+  ss = launch_probe_prep(h, dsrc, 8, 1, st, pr);
+  h->prof = prof;
+  CKS(ss);
+  CK(h->dist.ensure((size_t)std::max<uint32_t>(h->c.size, 1) * sizeof(double)));
+  CK(h->rsim.ensure((size_t)std::max<uint32_t>(h->c.size, 1) * h->c.L * sizeof(double)));
+  unsigned long long* dmin = reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224);
+  CK(cudaMemsetAsync(dmin, 0xff, 8, st));  // > every distance bit pattern
+  CK(moe::launch_exact_rows(h->c, *pr, 0, 0, h->c.L, h->rsim.as<double>(), h->dist.as<double>(),
+                            dmin, h->n_sm, st));
+  return MOE_OK;
 }
 
 // Compatibility wrapper used by the insert path: packed probes in hand.
@@ -900,30 +923,34 @@ moe_status moe_eamc_match_within(const moe_eamc* hc, const uint64_t* probe, doub
   *n_out = 0;
   if (h->c.size == 0) return MOE_OK;
   DeviceGuard dg(h->device);
-  DevProbes pr;
-  CK(h->out.ensure(sizeof(moe_match)));
-  moe_match* best = h->out.as<moe_match>();
-  CKS(match_all(h, probe, 8, 1, false, best, h->st, &pr));
-  CK(h->wl.ensure((size_t)h->c.size * sizeof(moe::WinEntry)));
-  uint32_t* wl_n = h->small.as<uint32_t>() + 8;
-  CK(cudaMemsetAsync(wl_n, 0, 4, h->st));
-  Plan p;
-  CKS(make_plan(h, 2, 1, &p));
-  CK(moe::launch_window(p.map, h->c, pr, p.g, 0, best, window, h->wl.as<moe::WinEntry>(), wl_n,
-                        h->st));
-  uint32_t n = 0;
-  CK(cudaMemcpyAsync(&n, wl_n, 4, cudaMemcpyDeviceToHost, h->st));
-  CK(cudaStreamSynchronize(h->st));
-  std::vector<moe::WinEntry> v(n);
-  CK(cudaMemcpy(v.data(), h->wl.p, n * sizeof(moe::WinEntry), cudaMemcpyDeviceToHost));
-  // (distance, seq) order of the result list (eam.cpp:145-148)
-  std::sort(v.begin(), v.end(), [](const moe::WinEntry& a, const moe::WinEntry& b) {
-    return a.d != b.d ? a.d < b.d : a.seq < b.seq;
-  });
-  for (uint64_t i = 0; i < n && i < cap; ++i)
-    out[i] = moe_match{v[i].p + h->c.index_base, v[i].seq, v[i].d};
-  *n_out = n;
-  return MOE_OK;
+  cudaStream_t st = h->st;
+  for (;;) {
+    DevProbes pr;
+    CKS(launch_exact_distances(h, probe, st, &pr));
+    CK(h->wl.ensure((size_t)h->c.size * sizeof(moe::WinEntry)));
+    uint32_t* wl_n = h->small.as<uint32_t>() + 8;
+    CK(cudaMemsetAsync(wl_n, 0, 4, st));
+    CK(moe::launch_window_list(
+        h->c, h->dist.as<double>(),
+        reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224), window,
+        h->wl.as<moe::WinEntry>(), wl_n, st));
+    CK(cudaMemcpyAsync(h->pin.p, h->small.p, 64, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bool ok = false;
+    CKS(check_width(h, *h->pin.as<unsigned long long>(), &ok));
+    if (!ok) continue;
+    const uint32_t n = h->pin.as<uint32_t>()[8];
+    std::vector<moe::WinEntry> v(n);
+    CK(cudaMemcpy(v.data(), h->wl.p, n * sizeof(moe::WinEntry), cudaMemcpyDeviceToHost));
+    // (distance, seq) order of the result list (eam.cpp:145-148)
+    std::sort(v.begin(), v.end(), [](const moe::WinEntry& a, const moe::WinEntry& b) {
+      return a.d != b.d ? a.d < b.d : a.seq < b.seq;
+    });
+    for (uint64_t i = 0; i < n && i < cap; ++i)
+      out[i] = moe_match{v[i].p + h->c.index_base, v[i].seq, v[i].d};
+    *n_out = n;
+    return MOE_OK;
+  }
 }
 
 moe_status moe_match_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out) {
@@ -1030,24 +1057,32 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
   cudaStream_t st = h->st;
   CK(h->agg.ensure(cells * 8));
   CK(h->small.ensure(256));
+  CK(h->pin.ensure(256));
   unsigned long long* agg = h->agg.as<unsigned long long>();
   CK(cudaMemsetAsync(agg, 0, cells * 8, st));
   const bool prefetch_live = do_prefetch && h->c.size > 0;
+  const uint64_t ncand = prefetch_live && current_layer + 1 < L ? (uint64_t)(L - current_layer - 1) * E : 0;
+  CK(h->cand.ensure(std::max<uint64_t>(ncand, 1) * sizeof(moe_candidate)));
+  uint32_t* dn = h->small.as<uint32_t>() + 12;
   if (prefetch_live) {
+    // one exact pass over the collection (row-parallel), window membership
+    // (kMatchWindow, policy.hpp:30) + u64 aggregation of the members' rows > l,
+    // then priorities / floor filter / order
     DevProbes pr;
-    CK(h->out.ensure(sizeof(moe_match)));
-    moe_match* best = h->out.as<moe_match>();
-    CKS(match_all(h, cur_eam, 8, 1, false, best, st, &pr));
-    CK(h->wl.ensure((size_t)h->c.size * sizeof(moe::WinEntry)));
-    uint32_t* wl_n = h->small.as<uint32_t>() + 8;
-    CK(cudaMemsetAsync(wl_n, 0, 4, st));
-    Plan p;
-    CKS(make_plan(h, 2, 1, &p));
-    // kMatchWindow (policy.hpp:30)
-    CK(moe::launch_window(p.map, h->c, pr, p.g, 0, best, 0.01, h->wl.as<moe::WinEntry>(), wl_n,
-                          st));
-    CK(moe::launch_aggregate(h->c, h->wl.as<moe::WinEntry>(), wl_n, current_layer, agg, st));
+    CKS(launch_exact_distances(h, cur_eam, st, &pr));
+    CK(h->mem.ensure((size_t)h->c.size * 4));
+    CK(moe::launch_member_agg(h->c, h->dist.as<double>(),
+                              reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224),
+                              0.01, current_layer, h->mem.as<uint32_t>(),
+                              h->small.as<uint32_t>() + 10, agg, h->n_sm, st));
+    CK(h->keys.ensure(std::max<uint64_t>(ncand, 1) * 12));
+    CK(moe::launch_prefetch_order(agg, L, E, current_layer, filter,
+                                  h->keys.as<unsigned long long>(), dn,
+                                  h->cand.as<moe_candidate>(), h->n_sm, st));
+  } else {
+    CK(cudaMemsetAsync(h->small.p, 0, 8, st));  // no probe: nothing to width-check
   }
+  if (!prefetch_live || current_layer + 1 >= L) CK(cudaMemsetAsync(dn, 0, 4, st));
   unsigned long long* req = nullptr;
   if (request_eam) {
     CK(h->req.ensure(cells * 8));
@@ -1063,19 +1098,21 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
     dslots = h->slots.as<moe_slot_view>();
     if (slot_pri) dpri = reinterpret_cast<double*>(dslots + n_slots);
   }
-  const uint64_t ncand = prefetch_live && current_layer + 1 < L ? (uint64_t)(L - current_layer - 1) * E : 0;
-  CK(h->cand.ensure(std::max<uint64_t>(ncand, 1) * sizeof(moe_candidate)));
-  uint32_t* dn = h->small.as<uint32_t>() + 12;
   long long* dv = reinterpret_cast<long long*>(h->small.as<uint8_t>() + 192);
-  CK(cudaMemsetAsync(dn, 0, 4, st));
-  CK(moe::launch_decide(agg, L, E, current_layer, filter, prefetch_live ? 1 : 0, req, dslots,
-                        n_slots, h->cand.as<moe_candidate>(), dn, victim ? dv : nullptr, dpri,
-                        st));
-  uint32_t n = 0;
-  long long v = -1;
-  CK(cudaMemcpyAsync(&n, dn, 4, cudaMemcpyDeviceToHost, st));
-  if (victim) CK(cudaMemcpyAsync(&v, dv, 8, cudaMemcpyDeviceToHost, st));
+  if (victim || slot_pri)
+    CK(moe::launch_decide(agg, L, E, current_layer, filter, 0, req, dslots, n_slots, nullptr,
+                          nullptr, victim ? dv : nullptr, dpri, st));
+  CK(cudaMemcpyAsync(h->pin.p, h->small.p, 256, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (prefetch_live) {
+    bool ok = false;
+    CKS(check_width(h, *h->pin.as<unsigned long long>(), &ok));
+    if (!ok)  // collection widened for this probe: decide again at the new width
+      return decide_impl(h, shape, cur_eam, current_layer, filter, do_prefetch, request_eam, slots,
+                         n_slots, out, cap, n_out, victim, slot_pri);
+  }
+  const uint32_t n = h->pin.as<uint32_t>()[12];
+  const long long v = *reinterpret_cast<const long long*>(h->pin.as<uint8_t>() + 192);
   if (n_out) *n_out = prefetch_live ? n : 0;
   if (prefetch_live && n && out && cap)
     CK(cudaMemcpy(out, h->cand.p, std::min<uint64_t>(n, cap) * sizeof(moe_candidate),

@@ -100,6 +100,8 @@ struct MatchArgs {
   double window;           // mode 2
   WinEntry* wl;            // mode 2
   uint32_t* wl_n;          // mode 2
+  double* dist;            // mode 3: exact distance of every entry to probe q_single
+  unsigned long long* dmin;  // mode 3: bit pattern of the minimum distance (>= 0)
 };
 
 template <typename Acc>
@@ -288,6 +290,25 @@ __global__ void __launch_bounds__(kNT, 1)
               a.bucket[(uint64_t)qg * a.bcap + pos] = make_uint2(p, __float_as_uint(dq[q]));
           }
         }
+      } else if (MODE == 3) {
+        // exact distance of every entry (reference operation order), stored,
+        // plus the collection-wide minimum for the match_within window
+        double d = __longlong_as_double(0x7ff0000000000000ll);
+        if (valid) {
+          double sm = 0.0;
+          const double* sb = a.sqb + (uint64_t)p * a.L;
+          for (uint32_t l = 0; l < a.L; ++l)
+            sm = __dadd_rn(sm, row_sim_exact((uint64_t)dots_s[l * kNT + tid], sqa_s[l], sb[l]));
+          d = finish_distance(sm, a.L);
+          a.dist[p] = d;
+        }
+        unsigned long long b = (unsigned long long)__double_as_longlong(d);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+          b = x < b ? x : b;
+        }
+        if (lane == 0 && b != 0x7ff0000000000000ull) atomicMin(a.dmin, b);
       } else {
         const uint32_t q = a.qlist ? a.qlist[qi] : a.q_single;
         float d32 = fmaxf(1.f - sim[0] / (float)a.L, 0.f);
@@ -691,6 +712,264 @@ __global__ void k_aggregate(const uint8_t* counts, uint32_t L, uint32_t E, uint3
     if (agg_s[i]) atomicAdd(&agg[first + i], agg_s[i]);
 }
 
+// K4 (window from the exact distances of mode 3): member = d <= d_min + window
+// (eam.cpp:143); rows > cur of every member are summed into agg (u64).
+template <int CB>
+__global__ void __launch_bounds__(512)
+    k_window_aggregate(const uint8_t* counts, uint32_t L, uint32_t E, uint32_t RB, uint32_t size,
+                       const double* dist, const unsigned long long* dmin, double window,
+                       uint32_t cur, unsigned long long* agg) {
+  extern __shared__ uint32_t aggs[];
+  const uint32_t first = (cur + 1) * E;
+  const uint32_t ncell = L * E - first;
+  for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x) aggs[i] = 0;
+  __syncthreads();
+  const double thr = __dadd_rn(__longlong_as_double((long long)*dmin), window);
+  const uint32_t warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x & 31;
+  for (uint32_t p = blockIdx.x * warps + wid; p < size; p += gridDim.x * warps) {
+    if (!(dist[p] <= thr)) continue;
+    const uint8_t* ent = counts + (uint64_t)p * L * RB;
+    for (uint32_t i = lane; i < ncell; i += 32) {
+      const uint32_t cell = first + i;
+      const uint32_t l = cell / E, e = cell - l * E;
+      const uint32_t c = CB == 1 ? ent[(uint64_t)l * RB + e]
+                                 : reinterpret_cast<const uint16_t*>(ent + (uint64_t)l * RB)[e];
+      if (c) atomicAdd(&aggs[i], c);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x)
+    if (aggs[i]) atomicAdd(&agg[first + i], (unsigned long long)aggs[i]);
+}
+
+__global__ void k_window_list(const double* dist, const unsigned long long* dmin, double window,
+                              const uint64_t* seq, uint32_t size, WinEntry* wl, uint32_t* wl_n) {
+  const double thr = __dadd_rn(__longlong_as_double((long long)*dmin), window);
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < size; p += gridDim.x * blockDim.x) {
+    const double d = dist[p];
+    if (d <= thr) wl[atomicAdd(wl_n, 1u)] = WinEntry{p, seq[p], d};
+  }
+}
+
+// ---- single-probe decision path (match_within / prefetch_priorities) ------
+// Row-parallel exact similarities: thread per (entry, layer) row, reading the
+// row (RB bytes, warp-contiguous in the AoS layout) and the probe row; the
+// per-row fp64 similarity goes to r[p*L + l].
+template <int CB>
+__global__ void __launch_bounds__(256)
+    k_rowsim(const uint8_t* counts, const double* sqb, uint32_t size, uint32_t L, uint32_t C,
+             uint32_t RB, const uint8_t* probe, const double* sqa, uint32_t l0, uint32_t l1,
+             double* r) {
+  const uint32_t nl = l1 - l0;
+  const uint64_t n = (uint64_t)size * nl;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = i / nl;
+    const uint32_t l = l0 + (uint32_t)(i - p * nl);
+    const uint4* ra = reinterpret_cast<const uint4*>(probe + (uint64_t)l * RB);
+    const uint4* rb = reinterpret_cast<const uint4*>(counts + (p * L + l) * RB);
+    typename Dot<CB>::Acc acc = 0;
+    for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(ra[c], __ldg(&rb[c]), acc);
+    r[p * L + l] = row_sim_exact((uint64_t)acc, sqa[l], sqb[p * L + l]);
+  }
+}
+
+// In-order layer sum (eam.cpp:95-103) -> dist[p]; warp min -> atomicMin(*dmin).
+__global__ void __launch_bounds__(256)
+    k_rowsum(const double* r, uint32_t size, uint32_t L, double* dist, unsigned long long* dmin) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  double d = __longlong_as_double(0x7ff0000000000000ll);
+  if (p < size) {
+    double sm = 0.0;
+    const double* rr = r + (uint64_t)p * L;
+    for (uint32_t l = 0; l < L; ++l) sm = __dadd_rn(sm, rr[l]);
+    d = finish_distance(sm, L);
+    dist[p] = d;
+  }
+  unsigned long long b = (unsigned long long)__double_as_longlong(d);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+    b = x < b ? x : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b != 0x7ff0000000000000ull) atomicMin(dmin, b);
+}
+
+// Window members (dist <= d_min + window, eam.cpp:143) -> compact list.
+__global__ void k_members(const double* dist, const unsigned long long* dmin, double window,
+                          uint32_t size, uint32_t* mem, uint32_t* n_mem) {
+  const double thr = __dadd_rn(__longlong_as_double((long long)*dmin), window);
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < size; p += gridDim.x * blockDim.x)
+    if (dist[p] <= thr) mem[atomicAdd(n_mem, 1u)] = p;
+}
+
+// u64 aggregation of the members' rows > cur (policy.cpp:97-104): thread per
+// 4-byte word of the row region, a chunk of members per blockIdx.y, loads
+// unrolled for memory-level parallelism, one atomic per nonzero cell.
+template <int CB>
+__global__ void __launch_bounds__(256)
+    k_member_agg(const uint8_t* counts, uint32_t L, uint32_t E, uint32_t RB, uint32_t cur,
+                 const uint32_t* mem, const uint32_t* n_mem, uint32_t chunk,
+                 unsigned long long* agg) {
+  const uint32_t rows = L - cur - 1;
+  const uint32_t wpr = RB / 4;  // words per row
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t n = *n_mem;
+  const uint32_t m0 = blockIdx.y * chunk;
+  if (w >= rows * wpr || m0 >= n) return;
+  const uint32_t m1 = min(n, m0 + chunk);
+  const uint32_t r = w / wpr, wi = w - r * wpr;
+  const uint64_t off = (uint64_t)(cur + 1 + r) * RB + 4ull * wi;
+  const uint64_t LR = (uint64_t)L * RB;
+  uint32_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;  // per-cell partial sums (<= chunk * 65535)
+  uint32_t m = m0;
+  for (; m + 4 <= m1; m += 4) {
+    uint32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      v[k] = __ldg(reinterpret_cast<const uint32_t*>(counts + mem[m + k] * LR + off));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (CB == 1) {
+        s0 += v[k] & 0xffu;
+        s1 += (v[k] >> 8) & 0xffu;
+        s2 += (v[k] >> 16) & 0xffu;
+        s3 += v[k] >> 24;
+      } else {
+        s0 += v[k] & 0xffffu;
+        s1 += v[k] >> 16;
+      }
+    }
+  }
+  for (; m < m1; ++m) {
+    const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(counts + mem[m] * LR + off));
+    if (CB == 1) {
+      s0 += v & 0xffu;
+      s1 += (v >> 8) & 0xffu;
+      s2 += (v >> 16) & 0xffu;
+      s3 += v >> 24;
+    } else {
+      s0 += v & 0xffffu;
+      s1 += v >> 16;
+    }
+  }
+  const uint32_t per = 4 / CB;
+  const uint32_t e0 = wi * per;
+  const uint64_t base = (uint64_t)(cur + 1 + r) * E;
+  const uint32_t sums[4] = {s0, s1, s2, s3};
+  for (uint32_t k = 0; k < per; ++k)
+    if (e0 + k < E && sums[k]) atomicAdd(&agg[base + e0 + k], (unsigned long long)sums[k]);
+}
+
+// Priorities (policy.cpp:106-120) + floor filter (engine.cpp:663-668) of
+// every expert of layer cur+1+blockIdx.x; the block then sorts its layer by
+// (priority desc, expert asc) -- within one layer priority is monotone in the
+// aggregated count -- and writes the sorted keys (filtered-out experts get
+// the max key) to the layer's segment.  Keys are ~bits(priority): ascending
+// key = descending priority; priorities are > 0 so no real key is ~0.
+__global__ void __launch_bounds__(1024)
+    k_layer_sort(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur, int filter,
+                 unsigned long long* keys, uint32_t* n_out) {
+  extern __shared__ unsigned long long sk[];  // [np] keys, then [np] u32 expert ids
+  uint32_t np = 1;
+  while (np < E) np <<= 1;
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + np);
+  __shared__ unsigned long long rsum;
+  __shared__ uint32_t cnt;
+  const uint32_t l = cur + 1 + blockIdx.x;
+  const double kEps = 1e-4;  // policy.hpp:22
+  if (threadIdx.x == 0) {
+    rsum = 0;
+    cnt = 0;
+  }
+  __syncthreads();
+  unsigned long long part = 0;
+  for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) part += agg[(uint64_t)l * E + e];
+  if (part) atomicAdd(&rsum, part);
+  __syncthreads();
+  const double prox = __dsub_rn(1.0, __ddiv_rn((double)(l - cur), (double)L));
+  for (uint32_t e = threadIdx.x; e < np; e += blockDim.x) {
+    unsigned long long key = ~0ull;
+    if (e < E) {
+      const double ratio =
+          rsum == 0 ? 0.0
+                    : __ddiv_rn(__ull2double_rn(agg[(uint64_t)l * E + e]), __ull2double_rn(rsum));
+      const double pri = __dmul_rn(__dadd_rn(ratio, kEps), prox);
+      if (!(filter && pri <= __dmul_rn(__dmul_rn(kEps, prox), __dadd_rn(1.0, 1e-9)))) {
+        key = ~(unsigned long long)__double_as_longlong(pri);
+        atomicAdd(&cnt, 1u);
+      }
+    }
+    sk[e] = key;
+    sv[e] = e;
+  }
+  __syncthreads();
+  for (uint32_t k = 2; k <= np; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long ki = sk[i], kj = sk[ixj];
+          const uint32_t vi = sv[i], vj = sv[ixj];
+          if ((ki > kj || (ki == kj && vi > vj)) == up) {
+            sk[i] = kj;
+            sk[ixj] = ki;
+            sv[i] = vj;
+            sv[ixj] = vi;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  unsigned long long* out = keys + (uint64_t)blockIdx.x * E;
+  uint32_t* ids = reinterpret_cast<uint32_t*>(keys + (uint64_t)(L - cur - 1) * E) +
+                  (uint64_t)blockIdx.x * E;
+  for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
+    out[e] = sk[e];
+    ids[e] = sv[e];
+  }
+  if (threadIdx.x == 0) atomicAdd(n_out, cnt);
+}
+
+// Merge-rank of the per-layer sorted segments: a candidate's output position
+// is its position in its own layer plus, for every other layer, the number
+// of that layer's candidates that precede it (binary search).  Keys tie only
+// across layers (ids are unique), where the lower layer -- the smaller
+// ExpertId -- goes first.
+__global__ void __launch_bounds__(256)
+    k_merge_rank(const unsigned long long* keys, uint32_t L, uint32_t E, uint32_t cur,
+                 moe_candidate* out) {
+  extern __shared__ unsigned long long kss[];  // all sorted segments (binary searches stay on chip)
+  const uint32_t nl = L - cur - 1;
+  const uint32_t n = nl * E;
+  for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) kss[j] = keys[j];
+  __syncthreads();
+  const uint32_t* ids = reinterpret_cast<const uint32_t*>(keys + (uint64_t)n);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long k = kss[i];
+    if (k == ~0ull) continue;
+    const uint32_t li = i / E;
+    uint32_t rank = i - li * E;
+    for (uint32_t lj = 0; lj < nl; ++lj) {
+      if (lj == li) continue;
+      const unsigned long long* seg = kss + (uint64_t)lj * E;
+      uint32_t lo = 0, hi = E;  // count of seg < k (lj > li) or <= k (lj < li)
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const bool before = lj < li ? seg[mid] <= k : seg[mid] < k;
+        if (before) lo = mid + 1; else hi = mid;
+      }
+      rank += lo;
+    }
+    moe_candidate c;
+    c.layer_idx = cur + 1 + li;
+    c.expert_idx = ids[i];
+    c.priority = __longlong_as_double((long long)~k);
+    out[rank] = c;
+  }
+}
+
 // K5+K6 fused decision kernel (one block).
 __global__ void __launch_bounds__(1024)
     k_decide(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur, int filter,
@@ -990,6 +1269,7 @@ int occ_blocks_t(size_t smem) {
 int occ_blocks(int cb, uint32_t QT, int mode, size_t smem) {
   if (mode == 1) return cb == 1 ? occ_blocks_t<1, 1, 1>(smem) : occ_blocks_t<2, 1, 1>(smem);
   if (mode == 2) return cb == 1 ? occ_blocks_t<1, 1, 2>(smem) : occ_blocks_t<2, 1, 2>(smem);
+  if (mode == 3) return cb == 1 ? occ_blocks_t<1, 1, 3>(smem) : occ_blocks_t<2, 1, 3>(smem);
   switch (QT) {
     case 1: return cb == 1 ? occ_blocks_t<1, 1, 0>(smem) : occ_blocks_t<2, 1, 0>(smem);
     case 2: return cb == 1 ? occ_blocks_t<1, 2, 0>(smem) : occ_blocks_t<2, 2, 0>(smem);
@@ -1276,9 +1556,13 @@ cudaError_t launch_decide(const unsigned long long* agg, uint32_t L, uint32_t E,
   while (np < n) np <<= 1;
   const size_t smem = (size_t)np * 12 + (size_t)L * 16 + 16;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e =
-      cudaFuncSetAttribute(k_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static size_t set = 0;
+  if (smem > set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k_decide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = smem;
+  }
   k_decide<<<1, 1024, smem, st>>>(agg, L, E, cur, filter, do_prefetch && cur + 1 < L, req, slots,
                                   n_slots, out, n_out, victim, slot_pri, np);
   return cudaGetLastError();
@@ -1329,6 +1613,123 @@ cudaError_t launch_trace_commit64(const uint32_t* scratch, uint64_t n, const int
   if (n == 0) return cudaSuccess;
   k_trace_commit64<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
       scratch, n, bad, counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exact_all(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
+                             const MatchGeom& g, uint32_t q0, double* dist,
+                             unsigned long long* dmin, cudaStream_t st) {
+  if (c.size == 0) return cudaSuccess;
+  MatchArgs a = base_args(c, pr, g);
+  a.qlist = nullptr;
+  a.q_single = q0;
+  a.nq_list = 1;
+  a.dist = dist;
+  a.dmin = dmin;
+  return dispatch_match<3>(c.cb, 1, map, a, g, st);
+}
+
+cudaError_t launch_window_aggregate(const DevColl& c, const double* dist,
+                                    const unsigned long long* dmin, double window, uint32_t cur,
+                                    unsigned long long* agg, int n_sm, cudaStream_t st) {
+  if (cur + 1 >= c.L || c.size == 0) return cudaSuccess;
+  const size_t smem = (size_t)(c.L - cur - 1) * c.E * 4;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  static size_t set1 = 0, set2 = 0;
+  size_t& set = c.cb == 1 ? set1 : set2;
+  if (smem > set) {
+    cudaError_t e = c.cb == 1
+                        ? cudaFuncSetAttribute(k_window_aggregate<1>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                        : cudaFuncSetAttribute(k_window_aggregate<2>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = smem;
+  }
+  const unsigned grid = (unsigned)std::min<uint64_t>((c.size + 15) / 16, (uint64_t)n_sm * 2);
+  if (c.cb == 1)
+    k_window_aggregate<1><<<grid, 512, smem, st>>>(c.counts, c.L, c.E, c.RB, c.size, dist, dmin,
+                                                   window, cur, agg);
+  else
+    k_window_aggregate<2><<<grid, 512, smem, st>>>(c.counts, c.L, c.E, c.RB, c.size, dist, dmin,
+                                                   window, cur, agg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_window_list(const DevColl& c, const double* dist,
+                               const unsigned long long* dmin, double window, WinEntry* wl,
+                               uint32_t* wl_n, cudaStream_t st) {
+  if (c.size == 0) return cudaSuccess;
+  k_window_list<<<(c.size + 255) / 256, 256, 0, st>>>(dist, dmin, window, c.seq, c.size, wl, wl_n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exact_rows(const DevColl& c, const DevProbes& pr, uint32_t q0, uint32_t l0,
+                              uint32_t l1, double* r, double* dist, unsigned long long* dmin,
+                              int n_sm, cudaStream_t st) {
+  if (c.size == 0) return cudaSuccess;
+  const uint64_t LR = (uint64_t)c.L * c.RB;
+  const uint64_t n = (uint64_t)c.size * (l1 - l0);
+  if (n) {
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)n_sm * 16);
+    if (c.cb == 1)
+      k_rowsim<1><<<grid, 256, 0, st>>>(c.counts, c.sqb, c.size, c.L, c.C, c.RB,
+                                        pr.packed + q0 * LR, pr.sqa + (uint64_t)q0 * c.L, l0, l1, r);
+    else
+      k_rowsim<2><<<grid, 256, 0, st>>>(c.counts, c.sqb, c.size, c.L, c.C, c.RB,
+                                        pr.packed + q0 * LR, pr.sqa + (uint64_t)q0 * c.L, l0, l1, r);
+  }
+  k_rowsum<<<(c.size + 255) / 256, 256, 0, st>>>(r, c.size, c.L, dist, dmin);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_member_agg(const DevColl& c, const double* dist,
+                              const unsigned long long* dmin, double window, uint32_t cur,
+                              uint32_t* mem, uint32_t* n_mem, unsigned long long* agg, int n_sm,
+                              cudaStream_t st) {
+  if (c.size == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(n_mem, 0, 4, st);
+  if (e != cudaSuccess) return e;
+  k_members<<<std::min<uint32_t>((c.size + 255) / 256, (uint32_t)n_sm * 4), 256, 0, st>>>(
+      dist, dmin, window, c.size, mem, n_mem);
+  if (cur + 1 >= c.L) return cudaGetLastError();
+  const uint32_t words = (c.L - cur - 1) * (c.RB / 4);
+  const uint32_t bx = (words + 255) / 256;
+  const uint32_t by = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)n_sm * 8 / bx + 1,
+                                                               (c.size + 31) / 32));
+  const uint32_t chunk = (c.size + by - 1) / by;
+  dim3 grid(bx, by);
+  if (c.cb == 1)
+    k_member_agg<1><<<grid, 256, 0, st>>>(c.counts, c.L, c.E, c.RB, cur, mem, n_mem, chunk, agg);
+  else
+    k_member_agg<2><<<grid, 256, 0, st>>>(c.counts, c.L, c.E, c.RB, cur, mem, n_mem, chunk, agg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefetch_order(const unsigned long long* agg, uint32_t L, uint32_t E,
+                                  uint32_t cur, int filter, unsigned long long* keys,
+                                  uint32_t* n_dev, moe_candidate* out, int n_sm,
+                                  cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(n_dev, 0, 4, st);
+  if (e != cudaSuccess || cur + 1 >= L) return e;
+  if (E > 4096) return cudaErrorInvalidValue;
+  uint32_t np = 1;
+  while (np < E) np <<= 1;
+  const size_t smem = (size_t)np * 12;
+  const uint32_t nl = L - cur - 1;
+  k_layer_sort<<<nl, std::min<uint32_t>(1024, np), smem, st>>>(agg, L, E, cur, filter, keys,
+                                                                n_dev);
+  const uint32_t n = nl * E;
+  const size_t ksmem = (size_t)n * 8;
+  if (ksmem > 220 * 1024) return cudaErrorInvalidValue;
+  static size_t kset = 0;
+  if (ksmem > kset) {
+    e = cudaFuncSetAttribute(k_merge_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksmem);
+    if (e != cudaSuccess) return e;
+    kset = ksmem;
+  }
+  k_merge_rank<<<std::min<uint32_t>((n + 255) / 256, (uint32_t)n_sm), 256, ksmem, st>>>(
+      keys, L, E, cur, out);
   return cudaGetLastError();
 }
 

@@ -101,6 +101,37 @@ cudaError_t launch_window(const CUtensorMap& map, const DevColl& c, const DevPro
                           const MatchGeom& g, uint32_t q0, const moe_match* best, double window,
                           WinEntry* wl, uint32_t* wl_n, cudaStream_t st);
 
+// mode 3: exact distance of every entry to probe q0 -> dist[p], atomic min
+// of the distance bits -> *dmin (pre-set to +inf bits).
+cudaError_t launch_exact_all(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
+                             const MatchGeom& g, uint32_t q0, double* dist,
+                             unsigned long long* dmin, cudaStream_t st);
+// agg[L][E] += rows > cur of every entry with dist <= d_min + window.
+cudaError_t launch_window_aggregate(const DevColl& c, const double* dist,
+                                    const unsigned long long* dmin, double window, uint32_t cur,
+                                    unsigned long long* agg, int n_sm, cudaStream_t st);
+cudaError_t launch_window_list(const DevColl& c, const double* dist,
+                               const unsigned long long* dmin, double window, WinEntry* wl,
+                               uint32_t* wl_n, cudaStream_t st);
+
+// Single-probe exact distances, row-parallel: r[p][l] for l in [l0, l1), then
+// the in-order layer sum of all L rows -> dist[p] and atomic min -> *dmin.
+cudaError_t launch_exact_rows(const DevColl& c, const DevProbes& pr, uint32_t q0, uint32_t l0,
+                              uint32_t l1, double* r, double* dist, unsigned long long* dmin,
+                              int n_sm, cudaStream_t st);
+// Window members (dist <= d_min + window) -> mem list; agg[L][E] += their
+// rows > cur (u64).
+cudaError_t launch_member_agg(const DevColl& c, const double* dist,
+                              const unsigned long long* dmin, double window, uint32_t cur,
+                              uint32_t* mem, uint32_t* n_mem, unsigned long long* agg, int n_sm,
+                              cudaStream_t st);
+// Priorities + floor filter + order of the experts in layers > cur; keys is
+// scratch of (L-cur-1)*E*12 bytes, *n_dev = number of candidates emitted.
+cudaError_t launch_prefetch_order(const unsigned long long* agg, uint32_t L, uint32_t E,
+                                  uint32_t cur, int filter, unsigned long long* keys,
+                                  uint32_t* n_dev, moe_candidate* out, int n_sm,
+                                  cudaStream_t st);
+
 cudaError_t launch_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out,
                          cudaStream_t st);
 cudaError_t launch_pair_distance(const uint8_t* a, const double* sqa, const uint8_t* b,
