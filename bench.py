@@ -245,6 +245,11 @@ def run_ours(args):
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_val = evals_per_step * e2e_steps / float(t_e2e.item())
 
+    # ---- the other SURVEY 8 rows (prefetch decisions, construction, tracing, MIX)
+    rows = None
+    if N == 1 and not args.no_rows:
+        rows = run_rows(args, m, _lib, torch, dev, sp, stream)
+
     # ---- streaming regime (north-star target: >= 60% HBM roofline at P >= 1M)
     streaming = None
     if not args.no_streaming:
@@ -278,11 +283,179 @@ def run_ours(args):
         }
         if streaming:
             out["streaming"] = streaming
+        if rows:
+            out["rows"] = rows
         if N == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"], out["parity_sample"] = cpu_baseline(args, probes_u8, res)
     if N > 1:
         dist.barrier()
         dist.destroy_process_group()
+    return out
+
+
+def _ref_or_none():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import REF_SO, Oracle, RefLib
+    return (RefLib() if os.path.exists(REF_SO) else None), Oracle()
+
+
+def run_rows(args, m, _lib, torch, dev, sp, stream):
+    """Measured lines for SURVEY 8 rows beyond the headline matcher, each with
+    the reference CPU path (oracle/_ref) timed on this box beside it."""
+    from concurrent.futures import ThreadPoolExecutor
+    hbm_peak, _, peak_kind = load_peaks()
+    ref, orc = _ref_or_none()
+    cores = os.cpu_count() or 1
+    out = {}
+
+    # -- A10/A11 prefetch decisions, DS shape (L=59, E=160, top-6): one decode
+    #    step = 58 prefetch_priorities calls (l = 0..57) + floor filter
+    L2, E2, P2 = 59, 160, 10_000
+    fam = m.gen_bench_family(SEED, L2, E2, P2 + 1, dtype=np.uint8)
+    s2 = m.ModelShape(L2, E2, 6)
+    e2 = m.Eamc(s2, m.Phase.decode, P2)
+    e2.append(fam[:P2], np.arange(P2, dtype=np.uint64))
+    base = fam[P2].astype(np.uint64)
+    probes = []
+    for l in range(L2 - 1):
+        pr = base.copy()
+        pr[l + 1:] = 0  # the engine's iteration EAM at layer l (engine.cpp:546, :587)
+        probes.append(pr)
+    orders = [m.prefetch_order(m.Eam(s2, m.EamKind.iteration, counts=probes[0]), e2, 0)]
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        orders = [m.prefetch_order(m.Eam(s2, m.EamKind.iteration, counts=probes[l]), e2, l)
+                  for l in range(L2 - 1)]
+    t_gpu = (time.perf_counter() - t0) / reps
+    row = {"workload": f"DS decode step: L={L2} E={E2} top-6, EAMC P={P2} (F1), 58 "
+                       "prefetch_priorities calls + floor filter, host API",
+           "gpu_ms_per_step": t_gpu * 1e3, "gpu_decisions_per_s": (L2 - 1) / t_gpu}
+    if ref is not None:
+        er = ref.eamc(L2, E2, 6, 1, P2)
+        for x in fam[:P2]:
+            er.insert(x.astype(np.uint64))
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(cores) as ex:
+            refs = list(ex.map(lambda l: er.prefetch(probes[l], l, True), range(L2 - 1)))
+        t_cpu = time.perf_counter() - t0
+        same = all(np.array_equal(o["layer_idx"], r[0]) and np.array_equal(o["expert_idx"], r[1])
+                   and np.array_equal(o["priority"], r[2]) for o, r in zip(orders, refs))
+        row.update({"cpu_ms_per_step": t_cpu * 1e3, "cpu_cores": cores, "cpu_kind": "reference",
+                    "speedup": t_cpu / t_gpu, "parity_bitwise_order": bool(same)})
+    out["prefetch_decode_step"] = row
+
+    # -- A9/K7 EAMC construction, NL shape (L=24, E=128): insert replay at
+    #    capacity P=10k (each step: argmin over P, replace in place)
+    L3, E3, P3, n3 = 24, 128, 10_000, 2000
+    fam3 = m.gen_bench_family(3, L3, E3, P3 + n3, dtype=np.uint8)
+    e3 = m.Eamc(m.ModelShape(L3, E3), m.Phase.decode, P3)
+    e3.append(fam3[:P3], np.arange(P3, dtype=np.uint64))  # = P3 inserts below capacity
+    steps = fam3[P3:].astype(np.uint64)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    slots = e3.build(steps)
+    t_gpu = time.perf_counter() - t0
+    row = {"workload": f"NL construction replay: L={L3} E={E3}, capacity P={P3}, {n3} "
+                       "at-capacity Eamc::insert steps (F1), host API",
+           "gpu_us_per_step": t_gpu / n3 * 1e6, "gpu_evals_per_s": n3 * P3 / t_gpu,
+           "extrapolated_N100k_s": 90_000 * t_gpu / n3}
+    if ref is not None:
+        er = ref.eamc(L3, E3, 1, 1, P3)
+        for x in fam3[:P3]:
+            er.insert(x.astype(np.uint64))
+        ns = 20
+        t0 = time.perf_counter()
+        rs = [er.insert(x) for x in steps[:ns]]
+        t_cpu = (time.perf_counter() - t0) / ns
+        row.update({"cpu_us_per_step": t_cpu * 1e6, "cpu_cores": 1, "cpu_kind": "reference",
+                    "speedup": t_cpu / (t_gpu / n3),
+                    "parity_first_steps": bool(list(slots[:ns]) == rs)})
+    out["construction"] = row
+
+    # -- A2/K1 tracing, DS shape: T = 1M router tokens x 59 layers x top-6 ids
+    #    (u8, resident) -> R = 1000 per-request count matrices
+    L4, E4, k4, T4 = 59, 160, 6, 1_000_000
+    R4 = T4 // 1000
+    rng = np.random.default_rng(1001)
+    zipf = 1.0 / np.arange(1, E4 + 1) ** 1.2
+    basei = rng.choice(E4, size=(T4, L4), p=zipf / zipf.sum()).astype(np.uint16)
+    picks = ((basei[:, :, None] + np.arange(k4, dtype=np.uint16)[None, None, :]) % E4).astype(np.uint8)
+    offs = np.arange(0, T4 + 1, 1000, dtype=np.uint64)
+    d_picks = torch.from_numpy(picks).to(dev)
+    d_offs = torch.from_numpy(offs.astype(np.int64)).to(dev)
+    d_counts = torch.zeros((R4, L4, E4), dtype=torch.int32, device=dev)
+    d_bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    s4 = m.ModelShape(L4, E4, k4)
+    import ctypes as C
+    sh = s4.c()
+
+    def trace_dev():
+        _lib.check(_lib.lib.moe_eam_trace_device(C.byref(sh), d_picks.data_ptr(), 1, T4,
+                                                 d_offs.data_ptr(), R4, d_counts.data_ptr(),
+                                                 d_bad.data_ptr(), sp))
+    for _ in range(3):
+        trace_dev()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(10)]
+    for a, b in evs:
+        a.record(stream)
+        trace_dev()
+        b.record(stream)
+    torch.cuda.synchronize()
+    t_dev = sum(a.elapsed_time(b) for a, b in evs) / len(evs) / 1e3
+    bytes_alg = T4 * L4 * k4 * 1 + R4 * L4 * E4 * 4 + 8 * (R4 + 1)
+    t0 = time.perf_counter()
+    host_counts = m.trace_requests(s4, picks, offs)
+    t_e2e = time.perf_counter() - t0
+    row = {"workload": f"DS tracing: T={T4} tokens x L={L4} x top-{k4} u8 ids, R={R4} requests",
+           "gpu_ms": t_dev * 1e3, "picks_per_s": T4 * L4 * k4 / t_dev,
+           "roofline": {"bound": "hbm", "achieved": bytes_alg / t_dev / 1e9, "peak": hbm_peak,
+                        "unit": "GB/s", "frac": bytes_alg / t_dev / 1e9 / hbm_peak,
+                        "alg_bytes": bytes_alg, "note": f"peak = {peak_kind} HBM"},
+           "e2e_ms": t_e2e * 1e3, "e2e_api": "moe_eam_trace (host u8 ids, H2D inside)"}
+    ns = 20_000
+    t0 = time.perf_counter()
+    rc, ref_counts = orc.trace(L4, E4, k4, picks[:ns].astype(np.uint32),
+                               np.arange(0, ns + 1, 1000, dtype=np.uint64))
+    t_cpu = time.perf_counter() - t0
+    row.update({"cpu_picks_per_s": ns * L4 * k4 / t_cpu, "cpu_cores": 1, "cpu_kind": "port",
+                "cpu_sample": f"{ns} tokens (oracle restatement of workload.cpp:166-181 + "
+                              "Eam::record)",
+                "parity_sample": bool(rc == 0 and np.array_equal(host_counts[:ns // 1000],
+                                                                 ref_counts))})
+    out["tracing"] = row
+    del d_picks, d_counts
+
+    # -- MIX matcher (configs[0] shape): P=300, Q=1000 probes, latency regime
+    L5, E5, P5, Q5 = 32, 8, 300, 1000
+    fam5 = m.gen_bench_family(SEED, L5, E5, P5 + Q5)
+    e5 = m.Eamc(m.ModelShape(L5, E5, 2), m.Phase.decode, P5)
+    e5.append(fam5[:P5], np.arange(P5, dtype=np.uint64))
+    d5 = torch.from_numpy(fam5[P5:].astype(np.uint8)).to(dev)
+    o5 = torch.empty((Q5, 3), dtype=torch.float64, device=dev)
+    for _ in range(5):
+        _lib.check(_lib.lib.moe_eamc_match_device(e5._h, d5.data_ptr(), 1, Q5, o5.data_ptr(), sp))
+    torch.cuda.synchronize()
+    a5, b5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a5.record(stream)
+    for _ in range(50):
+        _lib.check(_lib.lib.moe_eamc_match_device(e5._h, d5.data_ptr(), 1, Q5, o5.data_ptr(), sp))
+    b5.record(stream)
+    torch.cuda.synchronize()
+    t5 = a5.elapsed_time(b5) / 50 / 1e3
+    row = {"workload": f"MIX: L={L5} E={E5} top-2, EAMC P={P5}, Q={Q5} probes (F1), device API",
+           "gpu_us_per_batch": t5 * 1e6, "evals_per_s": P5 * Q5 / t5,
+           "us_per_query": t5 / Q5 * 1e6}
+    if ref is not None:
+        er = ref.eamc(L5, E5, 2, 1, P5)
+        for x in fam5[:P5]:
+            er.insert(x)
+        idx, seq, d, f, secs = er.match(fam5[P5:], threads=cores)
+        row.update({"cpu_evals_per_s": P5 * Q5 / secs, "cpu_cores": cores, "cpu_kind": "reference",
+                    "speedup": (P5 * Q5 / t5) / (P5 * Q5 / secs)})
+    out["mix_match"] = row
     return out
 
 
@@ -456,6 +629,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-streaming", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rows", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
