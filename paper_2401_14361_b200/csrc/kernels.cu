@@ -446,7 +446,8 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
   const uint8_t* pa = r.probes + q * LR;
   const double* sqa = r.sqa + (uint64_t)q * r.L;
   Best b{__longlong_as_double(0x7ff0000000000000ll), kNone, kNone};
-  const uint32_t G = max(1u, (uint32_t)kRefineBuf / r.L);  // candidates per group
+  // candidates per group: one summing lane each, and their L values in rbuf
+  const uint32_t G = max(1u, min(32u, (uint32_t)kRefineBuf / r.L));
   for (uint32_t g0 = 0; g0 < nc; g0 += G) {
     const uint32_t gn = min(G, nc - g0);
     const uint32_t pairs = gn * r.L;

@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -41,9 +42,11 @@ constexpr uint32_t A_BYTES = BM * BK * 2;  // 16 KB
 constexpr uint32_t B_BYTES = BN * BK * 2;  // 32 KB
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
-constexpr int THREADS = 192;
+constexpr int THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+constexpr uint32_t EPI_THREADS = 256;
 
 struct TcArgs {
+  float invL;          // 1/L (fp32)
   const uint64_t* zq;  // [Q] zero-row masks of the probes
   const uint64_t* zp;  // [cap] zero-row masks of the entries
   uint32_t Q, P, L;
@@ -124,6 +127,61 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Epilogue of one accumulator tile for one probe row and 128 of its 256
+// columns (two warps of the same TMEM lane quarter split the columns).
+// Pass 1 (branch-free): screen distances -> row minimum -> global per-probe
+// threshold.  Pass 2 only runs when the row minimum can still produce a
+// candidate (rare once the threshold has converged) and walks a bitmask.
+__device__ __forceinline__ void epilogue_half(uint32_t tcol, uint32_t col0, uint64_t zq,
+                                              const uint64_t* zt, uint32_t q, bool qvalid,
+                                              uint32_t p0, const TcArgs& a, float invL) {
+  uint32_t r[32];
+  const bool full_tile = p0 + col0 + 128 <= a.P;
+  float rmin = __uint_as_float(kFInf);
+#pragma unroll 1
+  for (uint32_t c = 0; c < 4; ++c) {
+    tmem_ld32(tcol + c * 32, r);
+    if (zq == 0 && full_tile) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) rmin = fminf(rmin, fmaf(-__uint_as_float(r[j]), invL, 1.0f));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t col = col0 + c * 32 + j;
+        const float sim = __uint_as_float(r[j]) + (float)__popcll(zq & zt[col]);
+        const float d = fmaf(-sim, invL, 1.0f);
+        rmin = (p0 + col < a.P) ? fminf(rmin, d) : rmin;
+      }
+    }
+  }
+  rmin = fmaxf(rmin, 0.0f);
+  float thr = -1.0f;  // invalid rows never qualify
+  if (qvalid) {
+    const uint32_t mb = __float_as_uint(rmin);
+    uint32_t tv = *reinterpret_cast<volatile uint32_t*>(&a.T[q]);
+    if (mb < tv) tv = min(atomicMin(&a.T[q], mb), mb);
+    thr = __uint_as_float(tv) + a.eps2;
+  }
+  // tcgen05.ld is warp-collective: the (rare) candidate pass is taken by the
+  // whole warp whenever any of its rows can still produce a candidate
+  if (!__any_sync(0xffffffffu, rmin <= thr)) return;
+#pragma unroll 1
+  for (uint32_t c = 0; c < 4; ++c) {
+    tmem_ld32(tcol + c * 32, r);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {  // rare pass: a branch per column is fine here
+      const uint32_t col = col0 + c * 32 + j;
+      const float sim = __uint_as_float(r[j]) + (float)__popcll(zq & zt[col]);
+      const float d = fmaxf(fmaf(-sim, invL, 1.0f), 0.0f);
+      if (qvalid && d <= thr && p0 + col < a.P) {
+        const uint32_t pos = atomicAdd(&a.bcnt[q], 1u);
+        if (pos < a.bcap)
+          a.bucket[(uint64_t)q * a.bcap + pos] = make_uint2(p0 + col, __float_as_uint(d));
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     k_tc_screen(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                 const TcArgs a) {
@@ -149,7 +207,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], EPI_THREADS);
     }
     fence_mbar_init();
   }
@@ -209,62 +267,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    // epilogue: 4 warps, thread = accumulator lane = probe row of the tile
+    // epilogue: 8 warps; warp w serves TMEM lane quarter w%4 (probe rows) and
+    // column half (w-2)/4 of the 256-column accumulator
     const uint32_t quarter = warp & 3;
+    const uint32_t half = (warp - 2) >> 2;
     const uint32_t row = quarter * 32 + lane;
-    const uint32_t et = threadIdx.x - 64;  // 0..127
-    const float invL = 1.0f / (float)a.L;
+    const uint32_t et = threadIdx.x - 64;  // 0..255
     uint32_t i = 0;
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const uint32_t acc = i & 1;
       const uint32_t m = t % a.n_m, n = t / a.n_m;
       uint64_t* zt = zp_s + acc * BN;
-      for (uint32_t j = et; j < BN; j += 128) {
-        const uint32_t p = n * BN + j;
-        zt[j] = p < a.P ? a.zp[p] : 0ull;
+      {
+        const uint32_t p = n * BN + et;
+        zt[et] = p < a.P ? a.zp[p] : 0ull;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       const uint32_t q = m * BM + row;
       const bool qvalid = q < a.Q;
       const uint64_t zq = qvalid ? a.zq[q] : 0ull;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
-      const uint32_t tbase = tmem + ((quarter * 32) << 16) + acc * BN;
-      float rmin = __uint_as_float(kFInf);
-      uint32_t r[32];
-#pragma unroll 1
-      for (uint32_t c = 0; c < BN / 32; ++c) {
-        tmem_ld32(tbase + c * 32, r);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const uint32_t col = c * 32 + j;
-          const float sim = __uint_as_float(r[j]) + (float)__popcll(zq & zt[col]);
-          const float d = fmaxf(fmaf(-sim, invL, 1.0f), 0.0f);
-          if (n * BN + col < a.P) rmin = fminf(rmin, d);
-        }
-      }
-      float thr = __uint_as_float(kFInf);
-      if (qvalid) {
-        const uint32_t mb = __float_as_uint(rmin);
-        uint32_t tv = *reinterpret_cast<volatile uint32_t*>(&a.T[q]);
-        if (mb < tv) tv = min(atomicMin(&a.T[q], mb), mb);
-        thr = __uint_as_float(tv) + a.eps2;
-      }
-#pragma unroll 1
-      for (uint32_t c = 0; c < BN / 32; ++c) {
-        tmem_ld32(tbase + c * 32, r);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const uint32_t col = c * 32 + j;
-          const float sim = __uint_as_float(r[j]) + (float)__popcll(zq & zt[col]);
-          const float d = fmaxf(fmaf(-sim, invL, 1.0f), 0.0f);
-          const uint32_t p = n * BN + col;
-          if (qvalid && p < a.P && d <= thr) {
-            const uint32_t pos = atomicAdd(&a.bcnt[q], 1u);
-            if (pos < a.bcap) a.bucket[(uint64_t)q * a.bcap + pos] = make_uint2(p, __float_as_uint(d));
-          }
-        }
-      }
+      const uint32_t tcol = tmem + ((quarter * 32) << 16) + acc * BN + half * 128;
+      epilogue_half(tcol, half * 128, zq, zt, q, qvalid, n * BN, a, a.invL);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -274,6 +299,186 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2-CTA variant (cta_group::2, cluster of 2): one MMA covers a 256x256 tile.
+// CTA r of the pair loads A rows [256m + 128r, +128) and B rows
+// [256n + 128r, +128) (half the N tile); the leader (r=0) issues
+// tcgen05.mma.cta_group::2 over both CTAs' shared memory, accumulating the
+// pair's 256x256 tile as 128 TMEM lanes x 256 columns in each CTA.  Per SM
+// this halves the B bytes staged per FLOP relative to the 1-CTA kernel.
+constexpr int S2 = 6;                         // pipeline stages
+constexpr uint32_t A2_BYTES = 128 * BK * 2;   // 16 KB
+constexpr uint32_t B2_BYTES = 128 * BK * 2;   // 16 KB (half of the N tile)
+constexpr uint32_t STAGE2 = A2_BYTES + B2_BYTES;
+constexpr uint32_t kIdesc2 = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // leader-CTA address of a pair barrier
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_tc2_screen(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                 const TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S2 * A2_BYTES;
+  uint64_t* zp_s = reinterpret_cast<uint64_t*>(sB + S2 * B2_BYTES);  // [2][BN]
+  uint64_t* full = zp_s + 2 * BN;
+  uint64_t* empty = full + S2;
+  uint64_t* tfull = empty + S2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const uint32_t cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const uint32_t n_tiles = a.n_m * a.n_n;  // n_m counts 256-row M tiles here
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&ta);
+    prefetch_tmap(&tb);
+    for (int s = 0; s < S2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * EPI_THREADS);  // both CTAs' epilogue threads (leader's copy)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t s = 0, ph = 0;
+      for (uint32_t t = cluster; t < n_tiles; t += n_clusters) {
+        const uint32_t m = t % a.n_m, n = t / a.n_m;
+        for (uint32_t kb = 0; kb < a.n_k; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2);
+          tma_load_2d_pair(sA + s * A2_BYTES, &ta, &full[s], (int)(kb * BK),
+                           (int)(m * 256 + rank * 128));
+          tma_load_2d_pair(sB + s * B2_BYTES, &tb, &full[s], (int)(kb * BK),
+                           (int)(n * BN + rank * 128));
+          if (++s == S2) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      uint32_t s = 0, ph = 0, i = 0;
+      for (uint32_t t = cluster; t < n_tiles; t += n_clusters, ++i) {
+        const uint32_t acc = i & 1;
+        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (uint32_t kb = 0; kb < a.n_k; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint8_t* pa = sA + s * A2_BYTES;
+          const uint8_t* pb = sB + s * B2_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_f16_pair(d, smem_desc_sw128(pa + 32 * k), smem_desc_sw128(pb + 32 * k),
+                         (kb | k) != 0 ? 1u : 0u);
+          mma_commit_pair(&empty[s]);
+          if (++s == S2) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else {
+    // epilogue: 8 warps; warp w serves TMEM lane quarter w%4 (probe rows) and
+    // column half (w-2)/4 of the 256-column accumulator
+    const uint32_t quarter = warp & 3;
+    const uint32_t half = (warp - 2) >> 2;
+    const uint32_t row = quarter * 32 + lane;
+    const uint32_t et = threadIdx.x - 64;  // 0..255
+    uint32_t i = 0;
+    for (uint32_t t = cluster; t < n_tiles; t += n_clusters, ++i) {
+      const uint32_t acc = i & 1;
+      const uint32_t m = t % a.n_m, n = t / a.n_m;
+      uint64_t* zt = zp_s + acc * BN;
+      {
+        const uint32_t p = n * BN + et;
+        zt[et] = p < a.P ? a.zp[p] : 0ull;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const uint32_t q = m * 256 + rank * 128 + row;
+      const bool qvalid = q < a.Q;
+      const uint64_t zq = qvalid ? a.zq[q] : 0ull;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tcol = tmem + ((quarter * 32) << 16) + acc * BN + half * 128;
+      epilogue_half(tcol, half * 128, zq, zt, q, qvalid, n * BN, a, a.invL);
+      tc_fence_before();
+      mbar_arrive_leader(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS)
                  : "memory");
   }
@@ -320,6 +525,7 @@ cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchW
   struct MapCache {
     const void* base = nullptr;
     uint64_t rows = 0, Kp = 0;
+    uint32_t box = 0;
     CUtensorMap map;
   };
   static thread_local MapCache ca, cb;
@@ -337,10 +543,12 @@ cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchW
     cb.base = c.nrm;
     cb.rows = c.cap;
     cb.Kp = c.Kp;
+    cb.box = BN;
   }
   const CUtensorMap& ta = ca.map;
   const CUtensorMap& tb = cb.map;
   TcArgs a{};
+  a.invL = 1.0f / (float)c.L;
   a.zq = pr.zmask;
   a.zp = c.zmask;
   a.Q = pr.Q;
@@ -354,6 +562,36 @@ cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchW
   a.bcnt = w.bcnt;
   a.bucket = w.bucket;
   a.bcap = w.bcap;
+  const char* e2 = getenv("MOE_TC2");
+  const bool pair = (e2 ? e2[0] != '0' : true) && pr.Q > 128;
+  if (pair) {  // 2-CTA pairs: 256-row M tiles, half the B tile per CTA
+    if (cb.rows != c.cap || cb.base != c.nrm || cb.Kp != c.Kp || cb.box != 128) {
+      e = encode_2d_f16(c.nrm, c.cap, c.Kp, 128, &cb.map);
+      if (e != cudaSuccess) return e;
+      cb.base = c.nrm;
+      cb.rows = c.cap;
+      cb.Kp = c.Kp;
+      cb.box = 128;
+    }
+    a.n_m = (pr.Q + 255) / 256;
+    const size_t smem2 = (size_t)S2 * STAGE2 + 2 * BN * 8 + (2 * S2 + 4) * 8 + 16;
+    static bool attr2 = false;
+    if (!attr2) {
+      e = cudaFuncSetAttribute(k_tc2_screen, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem2);
+      if (e != cudaSuccess) return e;
+      attr2 = true;
+    }
+    const uint32_t tiles = a.n_m * a.n_n;
+    const uint32_t clusters = std::min<uint32_t>(tiles, (uint32_t)n_sm / 2);
+    k_tc2_screen<<<clusters * 2, THREADS, smem2, st>>>(ta, cb.map, a);
+    return cudaGetLastError();
+  }
+  if (cb.box != BN) {
+    e = encode_2d_f16(c.nrm, c.cap, c.Kp, BN, &cb.map);
+    if (e != cudaSuccess) return e;
+    cb.box = BN;
+  }
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 2 * BN * 8 + (2 * STAGES + 4) * 8 + 16;
   static bool attr = false;
   if (!attr) {

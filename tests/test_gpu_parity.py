@@ -523,3 +523,18 @@ def test_device_api_async_width_sentinel_and_overflow(m, orc):
     got = e.match_batch(probes[-1:])
     i2, s2, d2, _ = orc.match(fam[:P], seqs_of(P), probes[-1:])
     assert got["index"][0] == i2[0] and got["distance"][0] == d2[0]
+
+
+@pytest.mark.parametrize("L,dups", [(6, 250), (3, 200), (12, 70), (1, 240)])
+def test_refine_many_tied_candidates(m, orc, L, dups):
+    """More than 32 exact ties inside the candidate bucket (<= 256): every one
+    must be evaluated; the oldest seq wins (eam.cpp:123-124)."""
+    E, P = 32, 400
+    fam = m.gen_bench_family(12 + L, L, E, P + 4).copy()
+    fam[37:37 + dups] = fam[37]
+    rng = np.random.default_rng(L)
+    perm = rng.permutation(P)
+    ents = fam[:P][perm]
+    e = filled(m, L, E, ents)
+    for _ in range(3):  # bucket push order is nondeterministic: repeat
+        check_match(m, orc, e, ents, seqs_of(P), np.concatenate([fam[37:38], fam[P:P + 3]]))
