@@ -168,6 +168,10 @@ struct moe_eamc {
   double ms[3] = {0, 0, 0};
   uint64_t calls[3] = {0, 0, 0};
   DevBuf wide;
+  // pipelined host matching: copy stream, double-buffered u64 staging
+  cudaStream_t st2 = nullptr;
+  DevBuf raw2[2], outall;
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
 
   ~moe_eamc() {
     if (c.counts) cudaFree(c.counts);
@@ -179,6 +183,11 @@ struct moe_eamc {
     for (EvSet& es : ring)
       for (cudaEvent_t e : es.ev)
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i) {
+      if (ev_copy[i]) cudaEventDestroy(ev_copy[i]);
+      if (ev_free[i]) cudaEventDestroy(ev_free[i]);
+    }
+    if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -458,7 +467,8 @@ moe_status launch_match(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaSt
 // {UINT64_MAX-1, UINT64_MAX, NaN}.  `out` is a device array; `pr` receives
 // the packed probes for follow-up passes.
 moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bool src_device,
-                     moe_match* out, cudaStream_t st, DevProbes* pr, bool async = false) {
+                     moe_match* out, cudaStream_t st, DevProbes* pr, bool async = false,
+                     cudaEvent_t after_prep = nullptr) {
   if (n == 0) return MOE_OK;
   moe_status ss;
   const void* dsrc = stage_source(h, src, src_bytes, n, src_device, st, &ss);
@@ -466,6 +476,7 @@ moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bo
   for (;;) {
     CKS(prof_begin(h));
     CKS(launch_probe_prep(h, dsrc, src_bytes, n, st, pr));
+    if (after_prep) CK(cudaEventRecord(after_prep, st));  // the source buffer may be reused
     MatchWork w;
     CKS(launch_match(h, *pr, out, st, &w));
     if (async) {
@@ -887,15 +898,71 @@ moe_status moe_eamc_match(const moe_eamc* hc, const uint64_t* probes, uint64_t n
   if (n_probes == 0) return MOE_OK;
   DeviceGuard dg(h->device);
   const uint64_t cells = (uint64_t)h->c.L * h->c.E;
-  const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(65536, (512ull << 20) / (cells * 8)));
-  for (uint64_t off = 0; off < n_probes; off += chunk) {
-    const uint64_t m = std::min(chunk, n_probes - off);
+  const uint64_t bytes = n_probes * cells * 8;
+  uint64_t pipe_chunk = 0;  // probes per pipelined chunk (0 = one shot)
+  if (const char* pc = getenv("MOE_PIPE_CHUNK")) pipe_chunk = strtoull(pc, nullptr, 10);
+  else if (bytes >= (16ull << 20)) pipe_chunk = std::max<uint64_t>(1024, (n_probes + 3) / 4);
+  if (pipe_chunk == 0 || pipe_chunk >= n_probes) {  // one shot
     DevProbes pr;
-    CK(h->out.ensure(m * sizeof(moe_match)));
-    CKS(match_all(h, probes + off * cells, 8, m, false, h->out.as<moe_match>(), h->st, &pr));
-    CK(cudaMemcpyAsync(out + off, h->out.p, m * sizeof(moe_match), cudaMemcpyDeviceToHost, h->st));
+    CK(h->out.ensure(n_probes * sizeof(moe_match)));
+    CKS(match_all(h, probes, 8, n_probes, false, h->out.as<moe_match>(), h->st, &pr));
+    CK(cudaMemcpyAsync(out, h->out.p, n_probes * sizeof(moe_match), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  } else {
+    // Pipelined: the H2D copy of chunk k+1 (copy stream) overlaps the matching
+    // of chunk k (compute stream); two staging buffers, event-ordered reuse.
+    // Probes that do not fit the storage width come back as sentinels and
+    // are redone below (the collection widens then).
+    if (!h->st2) {
+      CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_free[i], cudaEventDisableTiming));
+      }
+    }
+    const uint64_t chunk = std::max<uint64_t>(
+        128, std::min<uint64_t>(pipe_chunk, (128ull << 20) / (cells * 8)));
+    CK(h->raw2[0].ensure(chunk * cells * 8));
+    CK(h->raw2[1].ensure(chunk * cells * 8));
+    CK(h->outall.ensure(n_probes * sizeof(moe_match)));
+    moe_match* dout = h->outall.as<moe_match>();
+    uint64_t k = 0;
+    for (uint64_t off = 0; off < n_probes; off += chunk, ++k) {
+      const uint64_t m = std::min(chunk, n_probes - off);
+      const int b = (int)(k & 1);
+      if (k >= 2) CK(cudaStreamWaitEvent(h->st2, h->ev_free[b], 0));
+      CK(cudaMemcpyAsync(h->raw2[b].p, probes + off * cells, m * cells * 8, cudaMemcpyHostToDevice,
+                         h->st2));
+      CK(cudaEventRecord(h->ev_copy[b], h->st2));
+      CK(cudaStreamWaitEvent(h->st, h->ev_copy[b], 0));
+      DevProbes pr;
+      CKS(match_all(h, h->raw2[b].p, 8, m, true, dout + off, h->st, &pr, /*async=*/true,
+                    h->ev_free[b]));
+    }
+    CK(cudaMemcpyAsync(out, dout, n_probes * sizeof(moe_match), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    std::vector<uint64_t> redo;
+    for (uint64_t q = 0; q < n_probes; ++q)
+      if (out[q].index == ~0ull - 1) redo.push_back(q);
+    if (!redo.empty()) {
+      std::vector<uint64_t> sub(redo.size() * cells);
+      for (size_t i = 0; i < redo.size(); ++i)
+        std::copy(probes + redo[i] * cells, probes + (redo[i] + 1) * cells, sub.begin() + i * cells);
+      // synchronous path: widens the collection, then matches exactly
+      const uint64_t step = std::max<uint64_t>(1, (8ull << 20) / (cells * 8));
+      for (uint64_t o = 0; o < redo.size(); o += step) {
+        const uint64_t m = std::min<uint64_t>(step, redo.size() - o);
+        DevProbes pr;
+        CK(h->out.ensure(m * sizeof(moe_match)));
+        CKS(match_all(h, sub.data() + o * cells, 8, m, false, h->out.as<moe_match>(), h->st, &pr));
+        std::vector<moe_match> res(m);
+        CK(cudaMemcpyAsync(res.data(), h->out.p, m * sizeof(moe_match), cudaMemcpyDeviceToHost,
+                           h->st));
+        CK(cudaStreamSynchronize(h->st));
+        for (uint64_t i = 0; i < m; ++i) out[redo[o + i]] = res[i];
+      }
+    }
   }
-  CK(cudaStreamSynchronize(h->st));
   if (found)
     for (uint64_t q = 0; q < n_probes; ++q) found[q] = out[q].index != ~0ull;
   return MOE_OK;

@@ -538,3 +538,16 @@ def test_refine_many_tied_candidates(m, orc, L, dups):
     e = filled(m, L, E, ents)
     for _ in range(3):  # bucket push order is nondeterministic: repeat
         check_match(m, orc, e, ents, seqs_of(P), np.concatenate([fam[37:38], fam[P:P + 3]]))
+
+
+def test_host_api_pipelined_large_batch(m, orc):
+    """> 16 MB of u64 probes: chunked H2D overlapped with matching; probes that
+    need a wider storage width are redone synchronously after widening."""
+    L, E, P, Q = 12, 128, 600, 2200
+    fam = m.gen_bench_family(77, L, E, P + Q).copy()
+    probes = fam[P:].copy()
+    probes[5::97] *= 300  # > 255: forces the widening redo path
+    e = filled(m, L, E, fam[:P])
+    check_match(m, orc, e, fam[:P], seqs_of(P), probes)
+    assert e.count_bytes() == 2
+    check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
