@@ -153,7 +153,7 @@ struct moe_eamc {
   cudaStream_t st = nullptr;
   // workspace
   DevBuf raw, packed, ia, sqa, nrm, zq, T, bcnt, bucket, over_list, small, out, partials, wl,
-      agg, cand, slots, req, dist, rsim, keys, mem;
+      agg, cand, slots, req, dist, rsim, keys, mem, bdiag;
   PinBuf pin;
   // instrumentation (moe_eamc_set_profiling): a ring of event sets so the
   // asynchronous device path can be timed without synchronising per call
@@ -272,6 +272,21 @@ moe_status widen(moe_eamc* h) {
 
 uint64_t width_max(int cb) { return cb == 1 ? 255ull : 65535ull; }
 
+// Exact-integer tensor-core screen for small batches (MOE_I8=0 disables,
+// MOE_I8=1 forces it for any batch size it supports).
+bool use_i8(const moe_eamc* h, uint64_t Q) {
+  if (!moe::i8_supported(h->c)) return false;
+  if (const char* e = getenv("MOE_I8")) {
+    if (e[0] == '0') return false;
+    if (e[0] == '1') return true;
+  }
+  // one 128-row block-diagonal M tile (128/R probes) streams the collection
+  // once; beyond that the fp16 screen is cheaper
+  uint32_t R = 1;
+  while (R < h->c.L) R <<= 1;
+  return Q <= 128 / R;
+}
+
 // Tensor-core screen for probe batches that fill its 128-row M tile
 // (MOE_TC=0 disables it, MOE_TC=1 forces it for any batch size).
 bool use_tc(const moe_eamc* h, uint64_t Q) {
@@ -280,7 +295,7 @@ bool use_tc(const moe_eamc* h, uint64_t Q) {
     if (e[0] == '0') return false;
     if (e[0] == '1') return true;
   }
-  return Q >= 128;
+  return !use_i8(h, Q) && Q >= 8;
 }
 
 // Fold a completed event set into the per-kernel totals.
@@ -326,10 +341,13 @@ moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint6
   unsigned long long* dmax = h->small.as<unsigned long long>();
   __half* nrm = nullptr;
   uint64_t* zq = nullptr;
-  if (c.Kp && use_tc(h, n)) {
+  const bool tc = c.Kp && use_tc(h, n);
+  if (tc) {
     CK(h->nrm.ensure(n * c.Kp * sizeof(__half)));
-    CK(h->zq.ensure(n * 8));
     nrm = h->nrm.as<__half>();
+  }
+  if (tc || (c.Kp && use_i8(h, n))) {
+    CK(h->zq.ensure(n * 8));
     zq = h->zq.as<uint64_t>();
   }
   CK(h->wide.ensure(n));
@@ -440,11 +458,15 @@ moe_status launch_match(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaSt
   CK(cudaMemsetAsync(w.bcnt, 0, Q * 4, st));
   CK(cudaMemsetAsync(w.over_n, 0, 4, st));
   const bool tc = pr.nrm != nullptr && moe::tc_supported(c);
+  const bool i8 = !tc && pr.zmask != nullptr && use_i8(h, Q);
   w.eps2 = tc ? moe::tc_eps2(c.L, c.E, c.Kp) : moe::screen_eps2(c.L);
   if (h->prof) CK(cudaEventRecord(h->ev[2], st));
   if (c.size > 0) {
     if (tc) {
       CK(moe::launch_tc_screen(c, pr, w, h->n_sm, st));
+    } else if (i8) {
+      CK(h->bdiag.ensure(moe::i8_blockdiag_bytes(c, (uint32_t)Q)));
+      CK(moe::launch_tci8_screen(c, pr, w, h->bdiag.as<uint8_t>(), h->n_sm, st));
     } else {
       Plan p;
       CKS(make_plan(h, 0, pick_qt(Q), &p));

@@ -83,6 +83,12 @@ float tc_eps2(uint32_t L, uint32_t E, uint32_t Kp);
 bool tc_supported(const DevColl& c);
 cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchWork& w, int n_sm,
                              cudaStream_t st);
+// Exact-integer tensor-core (tcgen05 kind::i8) screen for small probe batches
+// (u8 collections, L <= 32); blockdiag is scratch of i8_blockdiag_bytes().
+bool i8_supported(const DevColl& c);
+size_t i8_blockdiag_bytes(const DevColl& c, uint32_t Q);
+cudaError_t launch_tci8_screen(const DevColl& c, const DevProbes& pr, const MatchWork& w,
+                               uint8_t* blockdiag, int n_sm, cudaStream_t st);
 
 // mode 0: screen all Q probes; then refine.
 cudaError_t launch_screen(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
