@@ -201,7 +201,8 @@ def run_ours(args):
     ops_alg = 2.0 * L * E * P * Q
     bytes_alg = P * L * E * 1 + Q * L * E * 1 + 24 * Q
     roofline = {
-        "bound": "tensor", "kernel": "k_tc_screen (tcgen05.mma kind::f16 screen pass)",
+        "bound": "tensor",
+        "kernel": "k_tc2_screen (tcgen05.mma.cta_group::2 kind::f16, 256x256 tiles, screen pass)",
         "achieved": ops_alg / (screen_ms / 1e3) / 1e12, "peak": tf_peak, "unit": "TFLOP/s",
         "frac": ops_alg / (screen_ms / 1e3) / 1e12 / tf_peak,
         "traffic": ncu_traffic("sw_screen"),
@@ -210,7 +211,8 @@ def run_ours(args):
         "share_of_step": screen_ms / (t_ms / args.steps),
         "note": (f"peak = {peak_kind} dense bf16 (MEASURED_PEAKS.json); ops = 2*L*E*P*Q "
                  "(SURVEY.md 8d), executed as one fp16 tensor-core GEMM over unit-normalised "
-                 "rows (K=L*E), fp32 accumulate in TMEM. HBM view: "
+                 "rows (K=L*E), fp32 accumulate in TMEM; the operands are the fp16 copies "
+                 "(2 B/count), so ncu traffic is ~2x the u8 algorithmic bytes. HBM view: "
                  f"{bytes_alg / (screen_ms / 1e3) / 1e9:.1f} GB/s of {hbm_peak:.0f}"),
     }
 
@@ -512,7 +514,9 @@ def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak,
         "workload": f"SC streaming: P={STREAM_P} (P/GPU={P}), Q={STREAM_Q}, L={L} E={E}, u8",
         "value": P * N * STREAM_Q * steps / (t_ms / 1e3), "unit": "evals/s",
         "ms_per_step": t_ms / steps, "steps": steps,
-        "roofline": {"bound": "hbm", "kernel": "k_match<1,8,0> (screen pass)", "achieved": ach,
+        "roofline": {"bound": "hbm",
+                     "kernel": "k_tci8_screen<4> (tcgen05.mma kind::i8, block-diagonal probes)",
+                     "achieved": ach,
                      "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                      "traffic": ncu_traffic("sc_screen"), "launch_ms": screen_ms,
                      "alg_bytes_per_launch": bytes_alg,
