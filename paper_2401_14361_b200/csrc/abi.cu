@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1303,13 +1304,17 @@ moe_status moe_eam_trace_device(const moe_shape* shape, const void* topk_idx, in
   CKS(device_ok(dev, &n_sm));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t cells = (uint64_t)shape->n_layers * shape->n_experts_per_layer;
-  uint32_t* scratch = nullptr;
-  CK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), std::max<uint64_t>(1, n_requests * cells) * 4, st));
-  CK(cudaMemsetAsync(scratch, 0, n_requests * cells * 4, st));
+  // persistent per-device scratch (a stream-ordered pool allocation would be
+  // unmapped and remapped around every synchronisation)
+  static std::mutex mu;
+  static DevBuf scratch_buf[64];
+  std::lock_guard<std::mutex> lock(mu);
+  CK(scratch_buf[dev & 63].ensure(std::max<uint64_t>(1, n_requests * cells) * 4));
+  uint32_t* scratch = scratch_buf[dev & 63].as<uint32_t>();
+  // k_trace writes (or zeroes) every request's rows itself
   CK(moe::launch_trace(topk_idx, idx_bytes, n_tokens, shape->n_layers, shape->n_experts_per_layer,
                        shape->top_k, offsets, n_requests, scratch, bad_index_flag, n_sm, st));
   CK(moe::launch_trace_commit(scratch, n_requests * cells, bad_index_flag, counts_u32, st));
-  CK(cudaFreeAsync(scratch, st));
   return MOE_OK;
 }
 
@@ -1345,7 +1350,6 @@ moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_b
     e = cudaMemcpyAsync(doff.p, offsets, (n_requests + 1) * 8, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(dcnt.p, counts, n_requests * cells * 8, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(dscr.p, 0, n_requests * cells * 4, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(dbad.p, 0, 4, st);
   if (e == cudaSuccess)
     e = moe::launch_trace(din.p, idx_bytes, n_tokens, shape->n_layers, shape->n_experts_per_layer,

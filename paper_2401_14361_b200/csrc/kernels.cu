@@ -96,12 +96,6 @@ struct MatchArgs {
   uint32_t q_off;
   const uint32_t* Tfinal;  // mode 1 candidate threshold (null: all)
   moe_match* partials;     // mode 1 [nq_list][grid]
-  const moe_match* best;   // mode 2
-  double window;           // mode 2
-  WinEntry* wl;            // mode 2
-  uint32_t* wl_n;          // mode 2
-  double* dist;            // mode 3: exact distance of every entry to probe q_single
-  unsigned long long* dmin;  // mode 3: bit pattern of the minimum distance (>= 0)
 };
 
 template <typename Acc>
@@ -290,49 +284,20 @@ __global__ void __launch_bounds__(kNT, 1)
               a.bucket[(uint64_t)qg * a.bcap + pos] = make_uint2(p, __float_as_uint(dq[q]));
           }
         }
-      } else if (MODE == 3) {
-        // exact distance of every entry (reference operation order), stored,
-        // plus the collection-wide minimum for the match_within window
-        double d = __longlong_as_double(0x7ff0000000000000ll);
-        if (valid) {
-          double sm = 0.0;
-          const double* sb = a.sqb + (uint64_t)p * a.L;
-          for (uint32_t l = 0; l < a.L; ++l)
-            sm = __dadd_rn(sm, row_sim_exact((uint64_t)dots_s[l * kNT + tid], sqa_s[l], sb[l]));
-          d = finish_distance(sm, a.L);
-          a.dist[p] = d;
-        }
-        unsigned long long b = (unsigned long long)__double_as_longlong(d);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
-          b = x < b ? x : b;
-        }
-        if (lane == 0 && b != 0x7ff0000000000000ull) atomicMin(a.dmin, b);
       } else {
+        // MODE 1: exact evaluation of the candidates below the final threshold
         const uint32_t q = a.qlist ? a.qlist[qi] : a.q_single;
-        float d32 = fmaxf(1.f - sim[0] / (float)a.L, 0.f);
+        const float d32 = fmaxf(1.f - sim[0] / (float)a.L, 0.f);
         bool cand = valid;
-        double thr = 0.0;
-        if (MODE == 1) {
-          if (a.Tfinal) cand = cand && d32 <= __uint_as_float(a.Tfinal[q]) + a.eps2;
-        } else {
-          thr = __dadd_rn(a.best[q].distance, a.window);
-          cand = cand && d32 <= (float)thr + a.eps2;
-        }
+        if (a.Tfinal) cand = cand && d32 <= __uint_as_float(a.Tfinal[q]) + a.eps2;
         if (cand) {
           double sm = 0.0;
           const double* sb = a.sqb + (uint64_t)p * a.L;
           for (uint32_t l = 0; l < a.L; ++l)
             sm = __dadd_rn(sm, row_sim_exact((uint64_t)dots_s[l * kNT + tid], sqa_s[l], sb[l]));
           const double d = finish_distance(sm, a.L);
-          if (MODE == 1) {
-            const uint64_t sq = a.seq[p];
-            if (better(d, sq, tb.d, tb.seq)) tb = Best{d, sq, p};
-          } else if (d <= thr) {
-            const uint32_t pos = atomicAdd(a.wl_n, 1u);
-            a.wl[pos] = WinEntry{p, a.seq[p], d};
-          }
+          const uint64_t sq = a.seq[p];
+          if (better(d, sq, tb.d, tb.seq)) tb = Best{d, sq, p};
         }
       }
 #pragma unroll
@@ -684,63 +649,6 @@ __global__ void k_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32_
     const uint16_t v = e < RB_old ? src[r * RB_old + e] : 0;
     reinterpret_cast<uint16_t*>(dst + r * RB_new)[e] = v;
   }
-}
-
-// K4 tail: aggregate rows > cur of every window member into agg (u64).
-template <int CB>
-__global__ void k_aggregate(const uint8_t* counts, uint32_t L, uint32_t E, uint32_t RB,
-                            const WinEntry* wl, const uint32_t* wl_n, uint32_t cur,
-                            unsigned long long* agg) {
-  extern __shared__ unsigned long long agg_s[];
-  const uint32_t first = (cur + 1) * E;
-  const uint32_t ncell = L * E - first;
-  for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x) agg_s[i] = 0;
-  __syncthreads();
-  const uint32_t n = *wl_n;
-  const uint32_t warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x & 31;
-  for (uint32_t m = blockIdx.x * warps + wid; m < n; m += gridDim.x * warps) {
-    const uint8_t* ent = counts + wl[m].p * (uint64_t)L * RB;
-    for (uint32_t i = lane; i < ncell; i += 32) {
-      const uint32_t cell = first + i;
-      const uint32_t l = cell / E, e = cell - l * E;
-      const uint32_t c = CB == 1 ? ent[(uint64_t)l * RB + e]
-                                 : reinterpret_cast<const uint16_t*>(ent + (uint64_t)l * RB)[e];
-      if (c) atomicAdd(&agg_s[i], (unsigned long long)c);
-    }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x)
-    if (agg_s[i]) atomicAdd(&agg[first + i], agg_s[i]);
-}
-
-// K4 (window from the exact distances of mode 3): member = d <= d_min + window
-// (eam.cpp:143); rows > cur of every member are summed into agg (u64).
-template <int CB>
-__global__ void __launch_bounds__(512)
-    k_window_aggregate(const uint8_t* counts, uint32_t L, uint32_t E, uint32_t RB, uint32_t size,
-                       const double* dist, const unsigned long long* dmin, double window,
-                       uint32_t cur, unsigned long long* agg) {
-  extern __shared__ uint32_t aggs[];
-  const uint32_t first = (cur + 1) * E;
-  const uint32_t ncell = L * E - first;
-  for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x) aggs[i] = 0;
-  __syncthreads();
-  const double thr = __dadd_rn(__longlong_as_double((long long)*dmin), window);
-  const uint32_t warps = blockDim.x / 32, wid = threadIdx.x / 32, lane = threadIdx.x & 31;
-  for (uint32_t p = blockIdx.x * warps + wid; p < size; p += gridDim.x * warps) {
-    if (!(dist[p] <= thr)) continue;
-    const uint8_t* ent = counts + (uint64_t)p * L * RB;
-    for (uint32_t i = lane; i < ncell; i += 32) {
-      const uint32_t cell = first + i;
-      const uint32_t l = cell / E, e = cell - l * E;
-      const uint32_t c = CB == 1 ? ent[(uint64_t)l * RB + e]
-                                 : reinterpret_cast<const uint16_t*>(ent + (uint64_t)l * RB)[e];
-      if (c) atomicAdd(&aggs[i], c);
-    }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x)
-    if (aggs[i]) atomicAdd(&agg[first + i], (unsigned long long)aggs[i]);
 }
 
 __global__ void k_window_list(const double* dist, const unsigned long long* dmin, double window,
@@ -1124,44 +1032,115 @@ __device__ __forceinline__ uint32_t load_idx(const void* p, uint64_t i) {
   return reinterpret_cast<const uint32_t*>(p)[i];
 }
 
+// Histogram of the ids of tokens [s0, s1) into the shared histogram (odd row
+// stride ES), position-major: a token's L*k ids are "positions"; thread
+// (phase, pi) owns position pair pi (2 consecutive ids when L*k is even, so
+// one 16-bit load) of tokens phase, phase+phases, ...  Its histogram row
+// offsets are loop-invariant registers; per id: extract, range check, add,
+// shared-memory reduction.  Lanes of a warp read consecutive bytes of a
+// token (coalesced) and hit distinct rows (banks).  Out-of-range ids raise *bad.
+template <int IB>
+__device__ __forceinline__ void trace_tokens(const void* topk, uint64_t s0, uint64_t s1,
+                                             uint32_t L, uint32_t E, uint32_t k, uint32_t ES,
+                                             uint32_t* hist, int* bad) {
+  const uint32_t per_tok = L * k;
+  const uint32_t span = (IB == 1 && (per_tok & 1) == 0) ? 2u : 1u;
+  const uint32_t npos = per_tok / span;
+  const uint32_t phases = npos <= blockDim.x ? blockDim.x / npos : 1u;
+  const uint32_t tid = threadIdx.x;
+  if (tid >= phases * npos && npos <= blockDim.x) return;
+  const uint32_t phase = npos <= blockDim.x ? tid / npos : 0u;
+  for (uint32_t pi = npos <= blockDim.x ? tid - phase * npos : tid; pi < npos;
+       pi += npos <= blockDim.x ? npos : blockDim.x) {
+    const uint32_t pos = pi * span;
+    const uint32_t b0 = (pos / k) * ES, b1 = ((pos + 1) / k) * ES;
+    auto load = [&](uint64_t t) -> uint32_t {
+      const uint64_t i = t * per_tok + pos;
+      return span == 2 ? (uint32_t)reinterpret_cast<const uint16_t*>(topk)[i >> 1]
+                       : load_idx<IB>(topk, i);
+    };
+    auto count = [&](uint32_t w) {
+      if (span == 2) {
+        const uint32_t e0 = w & 0xffu, e1 = w >> 8;
+        if (e0 < E) atomicAdd(&hist[b0 + e0], 1u); else *bad = 1;
+        if (e1 < E) atomicAdd(&hist[b1 + e1], 1u); else *bad = 1;
+      } else {
+        if (w < E) atomicAdd(&hist[b0 + w], 1u); else *bad = 1;
+      }
+    };
+    constexpr int kU = 8;  // loads in flight per thread
+    uint64_t t = s0 + phase;
+    for (; t + (kU - 1) * (uint64_t)phases < s1; t += kU * (uint64_t)phases) {
+      uint32_t w[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) w[u] = load(t + u * (uint64_t)phases);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) count(w[u]);
+    }
+    for (; t < s1; t += phases) count(load(t));
+  }
+}
+
+constexpr uint64_t kTraceOwnedMax = 16384;  // tokens a single block owns outright
+
+// Requests of <= kTraceOwnedMax tokens: one block owns the request and writes
+// its whole L x E histogram with plain stores (no zeroing, no global
+// atomics).  Longer requests only get their scratch rows zeroed here.
 template <int IB>
 __global__ void __launch_bounds__(512)
-    k_trace(const void* topk, uint64_t T, uint32_t L, uint32_t E, uint32_t k,
-            const uint64_t* offsets, uint64_t R, uint32_t* scratch, int* bad, uint32_t chunk) {
+    k_trace(const void* topk, uint32_t L, uint32_t E, uint32_t k, const uint64_t* offsets,
+            uint64_t R, uint32_t* scratch, int* bad) {
   extern __shared__ uint32_t hist[];
-  const uint32_t ncell = L * E;
-  const uint64_t n_chunks = (T + chunk - 1) / chunk;
+  const uint32_t ES = E | 1;  // odd row stride: rows of the same expert on distinct banks
+  for (uint64_t r = blockIdx.x; r < R; r += gridDim.x) {
+    const uint64_t s0 = offsets[r], s1 = offsets[r + 1];
+    uint32_t* dst = scratch + r * (uint64_t)L * E;
+    if (s1 - s0 > kTraceOwnedMax) {
+      for (uint32_t i = threadIdx.x; i < L * E; i += blockDim.x) dst[i] = 0;
+      continue;
+    }
+    for (uint32_t i = threadIdx.x; i < L * ES; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    trace_tokens<IB>(topk, s0, s1, L, E, k, ES, hist, bad);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < L * E; i += blockDim.x) {
+      const uint32_t l = i / E;
+      dst[i] = hist[l * ES + (i - l * E)];
+    }
+    __syncthreads();
+  }
+}
+
+// Requests longer than kTraceOwnedMax: split into token chunks across blocks,
+// flushed with global atomics (runs after k_trace, which zeroed their rows).
+template <int IB>
+__global__ void __launch_bounds__(512)
+    k_trace_long(const void* topk, uint64_t T, uint32_t L, uint32_t E, uint32_t k,
+                 const uint64_t* offsets, uint64_t R, uint32_t* scratch, int* bad) {
+  extern __shared__ uint32_t hist[];
+  const uint32_t ES = E | 1;
+  const uint64_t n_chunks = (T + kTraceOwnedMax - 1) / kTraceOwnedMax;
   for (uint64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    const uint64_t t0 = ch * chunk;
-    const uint64_t t1 = min(T, t0 + chunk);
-    // first request whose range ends after t0 (offsets is non-decreasing)
-    uint64_t lo = 0, hi = R;
+    const uint64_t t0 = ch * kTraceOwnedMax, t1 = min(T, t0 + kTraceOwnedMax);
+    uint64_t lo = 0, hi = R;  // first request whose range ends after t0
     while (lo < hi) {
       const uint64_t mid = (lo + hi) / 2;
       if (offsets[mid + 1] <= t0) lo = mid + 1; else hi = mid;
     }
     for (uint64_t r = lo; r < R && offsets[r] < t1; ++r) {
+      if (offsets[r + 1] - offsets[r] <= kTraceOwnedMax) continue;  // owned by k_trace
       const uint64_t s0 = max(t0, offsets[r]), s1 = min(t1, offsets[r + 1]);
       if (s0 >= s1) continue;
-      for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x) hist[i] = 0;
+      for (uint32_t i = threadIdx.x; i < L * ES; i += blockDim.x) hist[i] = 0;
       __syncthreads();
-      const uint64_t pairs = (s1 - s0) * L;
-      for (uint64_t u = threadIdx.x; u < pairs; u += blockDim.x) {
-        const uint64_t tok = s0 + u / L;
-        const uint32_t l = (uint32_t)(u % L);
-        const uint64_t base = (tok * L + l) * k;
-        for (uint32_t j = 0; j < k; ++j) {
-          const uint32_t e = load_idx<IB>(topk, base + j);
-          if (e < E)
-            atomicAdd(&hist[l * E + e], 1u);
-          else
-            *bad = 1;
-        }
+      trace_tokens<IB>(topk, s0, s1, L, E, k, ES, hist, bad);
+      __syncthreads();
+      uint32_t* dst = scratch + r * (uint64_t)L * E;
+      for (uint32_t i = threadIdx.x; i < L * E; i += blockDim.x) {
+        const uint32_t l = i / E;
+        const uint32_t v = hist[l * ES + (i - l * E)];
+        if (v) atomicAdd(&dst[i], v);
       }
-      __syncthreads();
-      uint32_t* dst = scratch + r * (uint64_t)ncell;
-      for (uint32_t i = threadIdx.x; i < ncell; i += blockDim.x)
-        if (hist[i]) atomicAdd(&dst[i], hist[i]);
       __syncthreads();
     }
   }
@@ -1269,8 +1248,6 @@ int occ_blocks_t(size_t smem) {
 }
 int occ_blocks(int cb, uint32_t QT, int mode, size_t smem) {
   if (mode == 1) return cb == 1 ? occ_blocks_t<1, 1, 1>(smem) : occ_blocks_t<2, 1, 1>(smem);
-  if (mode == 2) return cb == 1 ? occ_blocks_t<1, 1, 2>(smem) : occ_blocks_t<2, 1, 2>(smem);
-  if (mode == 3) return cb == 1 ? occ_blocks_t<1, 1, 3>(smem) : occ_blocks_t<2, 1, 3>(smem);
   switch (QT) {
     case 1: return cb == 1 ? occ_blocks_t<1, 1, 0>(smem) : occ_blocks_t<2, 1, 0>(smem);
     case 2: return cb == 1 ? occ_blocks_t<1, 2, 0>(smem) : occ_blocks_t<2, 2, 0>(smem);
@@ -1471,20 +1448,6 @@ cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProb
   return cudaSuccess;
 }
 
-cudaError_t launch_window(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
-                          const MatchGeom& g, uint32_t q0, const moe_match* best, double window,
-                          WinEntry* wl, uint32_t* wl_n, cudaStream_t st) {
-  MatchArgs a = base_args(c, pr, g);
-  a.qlist = nullptr;
-  a.q_single = q0;
-  a.nq_list = 1;
-  a.best = best;
-  a.window = window;
-  a.wl = wl;
-  a.wl_n = wl_n;
-  return dispatch_match<2>(c.cb, 1, map, a, g, st);
-}
-
 cudaError_t launch_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out,
                          cudaStream_t st) {
   if (n == 0) return cudaSuccess;
@@ -1527,26 +1490,6 @@ cudaError_t launch_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32
   return cudaGetLastError();
 }
 
-cudaError_t launch_aggregate(const DevColl& c, const WinEntry* wl, const uint32_t* wl_n,
-                             uint32_t cur, unsigned long long* agg, cudaStream_t st) {
-  if (cur + 1 >= c.L) return cudaSuccess;
-  const size_t smem = (size_t)(c.L - cur - 1) * c.E * 8;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e;
-  if (c.cb == 1) {
-    e = cudaFuncSetAttribute(k_aggregate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return e;
-    k_aggregate<1><<<148, 512, smem, st>>>(c.counts, c.L, c.E, c.RB, wl, wl_n, cur, agg);
-  } else {
-    e = cudaFuncSetAttribute(k_aggregate<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return e;
-    k_aggregate<2><<<148, 512, smem, st>>>(c.counts, c.L, c.E, c.RB, wl, wl_n, cur, agg);
-  }
-  return cudaGetLastError();
-}
-
 cudaError_t launch_decide(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur,
                           int filter, int do_prefetch, const unsigned long long* req,
                           const moe_slot_view* slots, uint64_t n_slots, moe_candidate* out,
@@ -1573,31 +1516,33 @@ cudaError_t launch_trace(const void* topk, int idx_bytes, uint64_t T, uint32_t L
                          uint32_t k, const uint64_t* offsets, uint64_t R, uint32_t* scratch,
                          int* bad, int n_sm, cudaStream_t st) {
   if (T == 0 || R == 0) return cudaSuccess;
-  const size_t smem = (size_t)L * E * 4;
+  const size_t smem = (size_t)L * (E | 1) * 4;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
-  const uint32_t chunk = 512;
-  const uint64_t n_chunks = (T + chunk - 1) / chunk;
-  const unsigned grid = (unsigned)std::min<uint64_t>(n_chunks, (uint64_t)n_sm * 4);
-  cudaError_t e;
-  switch (idx_bytes) {
-    case 1:
-      e = cudaFuncSetAttribute(k_trace<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      k_trace<1><<<grid, 512, smem, st>>>(topk, T, L, E, k, offsets, R, scratch, bad, chunk);
-      break;
-    case 2:
-      e = cudaFuncSetAttribute(k_trace<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      k_trace<2><<<grid, 512, smem, st>>>(topk, T, L, E, k, offsets, R, scratch, bad, chunk);
-      break;
-    case 4:
-      e = cudaFuncSetAttribute(k_trace<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      k_trace<4><<<grid, 512, smem, st>>>(topk, T, L, E, k, offsets, R, scratch, bad, chunk);
-      break;
-    default:
-      return cudaErrorInvalidValue;
+  const unsigned grid = (unsigned)std::min<uint64_t>(R, (uint64_t)n_sm * 4);
+  const unsigned grid_long =
+      (unsigned)std::min<uint64_t>((T + kTraceOwnedMax - 1) / kTraceOwnedMax, (uint64_t)n_sm * 4);
+#define MOE_TRACE(IB)                                                                          \
+  {                                                                                            \
+    static size_t set = 0;                                                                     \
+    if (smem > set) {                                                                          \
+      cudaError_t e =                                                                          \
+          cudaFuncSetAttribute(k_trace<IB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e == cudaSuccess)                                                                    \
+        e = cudaFuncSetAttribute(k_trace_long<IB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)smem);                                                   \
+      if (e != cudaSuccess) return e;                                                          \
+      set = smem;                                                                              \
+    }                                                                                          \
+    k_trace<IB><<<grid, 512, smem, st>>>(topk, L, E, k, offsets, R, scratch, bad);             \
+    k_trace_long<IB><<<grid_long, 512, smem, st>>>(topk, T, L, E, k, offsets, R, scratch, bad); \
   }
+  switch (idx_bytes) {
+    case 1: MOE_TRACE(1) break;
+    case 2: MOE_TRACE(2) break;
+    case 4: MOE_TRACE(4) break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef MOE_TRACE
   return cudaGetLastError();
 }
 
@@ -1614,46 +1559,6 @@ cudaError_t launch_trace_commit64(const uint32_t* scratch, uint64_t n, const int
   if (n == 0) return cudaSuccess;
   k_trace_commit64<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
       scratch, n, bad, counts);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_exact_all(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
-                             const MatchGeom& g, uint32_t q0, double* dist,
-                             unsigned long long* dmin, cudaStream_t st) {
-  if (c.size == 0) return cudaSuccess;
-  MatchArgs a = base_args(c, pr, g);
-  a.qlist = nullptr;
-  a.q_single = q0;
-  a.nq_list = 1;
-  a.dist = dist;
-  a.dmin = dmin;
-  return dispatch_match<3>(c.cb, 1, map, a, g, st);
-}
-
-cudaError_t launch_window_aggregate(const DevColl& c, const double* dist,
-                                    const unsigned long long* dmin, double window, uint32_t cur,
-                                    unsigned long long* agg, int n_sm, cudaStream_t st) {
-  if (cur + 1 >= c.L || c.size == 0) return cudaSuccess;
-  const size_t smem = (size_t)(c.L - cur - 1) * c.E * 4;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  static size_t set1 = 0, set2 = 0;
-  size_t& set = c.cb == 1 ? set1 : set2;
-  if (smem > set) {
-    cudaError_t e = c.cb == 1
-                        ? cudaFuncSetAttribute(k_window_aggregate<1>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                        : cudaFuncSetAttribute(k_window_aggregate<2>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = smem;
-  }
-  const unsigned grid = (unsigned)std::min<uint64_t>((c.size + 15) / 16, (uint64_t)n_sm * 2);
-  if (c.cb == 1)
-    k_window_aggregate<1><<<grid, 512, smem, st>>>(c.counts, c.L, c.E, c.RB, c.size, dist, dmin,
-                                                   window, cur, agg);
-  else
-    k_window_aggregate<2><<<grid, 512, smem, st>>>(c.counts, c.L, c.E, c.RB, c.size, dist, dmin,
-                                                   window, cur, agg);
   return cudaGetLastError();
 }
 

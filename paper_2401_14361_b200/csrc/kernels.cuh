@@ -102,20 +102,6 @@ cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProb
                          const MatchGeom& g, const MatchWork& w, const uint32_t* qlist,
                          uint32_t qlist_n, const uint32_t* T, moe_match* out, cudaStream_t st,
                          const uint32_t* nq_dev = nullptr);
-// mode 2: window membership for probe q0 (exact d <= best.distance + window).
-cudaError_t launch_window(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
-                          const MatchGeom& g, uint32_t q0, const moe_match* best, double window,
-                          WinEntry* wl, uint32_t* wl_n, cudaStream_t st);
-
-// mode 3: exact distance of every entry to probe q0 -> dist[p], atomic min
-// of the distance bits -> *dmin (pre-set to +inf bits).
-cudaError_t launch_exact_all(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
-                             const MatchGeom& g, uint32_t q0, double* dist,
-                             unsigned long long* dmin, cudaStream_t st);
-// agg[L][E] += rows > cur of every entry with dist <= d_min + window.
-cudaError_t launch_window_aggregate(const DevColl& c, const double* dist,
-                                    const unsigned long long* dmin, double window, uint32_t cur,
-                                    unsigned long long* agg, int n_sm, cudaStream_t st);
 cudaError_t launch_window_list(const DevColl& c, const double* dist,
                                const unsigned long long* dmin, double window, WinEntry* wl,
                                uint32_t* wl_n, cudaStream_t st);
@@ -153,10 +139,8 @@ cudaError_t launch_replace(const DevColl& c, const DevProbes& staged, uint32_t i
 cudaError_t launch_append_staged(const DevColl& c, const DevProbes& staged, uint32_t first,
                                  uint32_t n, uint64_t base, cudaStream_t st);
 
-// Window aggregation: agg[L][E] (u64) += rows > cur of every listed entry.
-cudaError_t launch_aggregate(const DevColl& c, const WinEntry* wl, const uint32_t* wl_n,
-                             uint32_t cur, unsigned long long* agg, cudaStream_t st);
-// Fused K5+K6: priorities, floor filter, sort, eviction victim.
+// Eviction scoring (K6): cache priorities and the victim over slot views; the
+// prefetch half of this kernel is superseded by launch_prefetch_order.
 cudaError_t launch_decide(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur,
                           int filter, int do_prefetch, const unsigned long long* req,
                           const moe_slot_view* slots, uint64_t n_slots, moe_candidate* out,

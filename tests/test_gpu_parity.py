@@ -551,3 +551,20 @@ def test_host_api_pipelined_large_batch(m, orc):
     check_match(m, orc, e, fam[:P], seqs_of(P), probes)
     assert e.count_bytes() == 2
     check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
+
+
+def test_trace_long_and_empty_requests(m, orc):
+    """Requests longer than one block's ownership limit (chunked, atomics),
+    empty requests, unaligned id ranges, and tokens outside any request."""
+    L, E, k = 7, 40, 3
+    rng = np.random.default_rng(9)
+    T = 41_000
+    base = rng.integers(0, E, size=(T, L))
+    picks = ((base[:, :, None] + np.arange(k)[None, None, :]) % E).astype(np.uint8)
+    offs = np.array([0, 20_001, 20_001, 20_006, 40_999], np.uint64)  # long, empty, short, long
+    rc, want = orc.trace(L, E, k, picks.astype(np.uint32), offs)
+    assert rc == 0
+    s = m.ModelShape(L, E, k)
+    for dt in (np.uint8, np.uint16, np.uint32):
+        got = m.trace_requests(s, picks.astype(dt), offs)
+        assert np.array_equal(got, want)
