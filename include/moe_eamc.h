@@ -99,6 +99,9 @@ moe_status moe_eamc_destroy(moe_eamc* h);
 /* shape()/phase()/capacity()/size()/next_seq (eam.hpp:80-87) */
 moe_status moe_eamc_info(const moe_eamc* h, moe_shape* shape, int* phase, uint64_t* capacity,
                          uint64_t* size, uint64_t* next_seq, int* count_bytes);
+/* Deep copy (Eamc's implicit copy constructor, eam.hpp:76-116): same slots,
+ * seqs, next_seq, capacity and device. */
+moe_status moe_eamc_clone(const moe_eamc* h, moe_eamc** out);
 /* entry(i) / entry_seq(i) (eam.hpp:86-87); counts may be NULL. */
 moe_status moe_eamc_entry(const moe_eamc* h, uint64_t index, uint64_t* counts, uint64_t* seq);
 

@@ -78,6 +78,7 @@ _sig("moe_eamc_create", C.c_int, P(moe_shape), C.c_int, u64, C.c_int, C.c_int, P
 _sig("moe_eamc_destroy", C.c_int, vp)
 _sig("moe_eamc_info", C.c_int, vp, P(moe_shape), P(C.c_int), P(u64), P(u64), P(u64),
      P(C.c_int))
+_sig("moe_eamc_clone", C.c_int, vp, P(vp))
 _sig("moe_eamc_entry", C.c_int, vp, u64, vp, P(u64))
 _sig("moe_eamc_insert", C.c_int, vp, vp, C.c_int, C.c_int, P(C.c_int64), vp)
 _sig("moe_eamc_build", C.c_int, vp, vp, u64, vp)
@@ -106,7 +107,7 @@ _sig("moe_gen_bench_family", C.c_int, u64, C.c_uint32, C.c_uint32, u64, u64, C.c
 # every symbol include/moe_eamc.h declares
 EXPORTS = [
     "moe_abi_version", "moe_last_error", "moe_device_info", "moe_eamc_create",
-    "moe_eamc_destroy", "moe_eamc_info", "moe_eamc_entry", "moe_eamc_insert", "moe_eamc_build",
+    "moe_eamc_destroy", "moe_eamc_info", "moe_eamc_clone", "moe_eamc_entry", "moe_eamc_insert", "moe_eamc_build",
     "moe_eamc_append", "moe_eamc_append_packed", "moe_eamc_match", "moe_eamc_match_device",
     "moe_eamc_match_within", "moe_match_merge", "moe_match_merge_device",
     "moe_eamc_set_index_base", "moe_eamc_set_profiling", "moe_eamc_kernel_times",

@@ -1069,6 +1069,29 @@ moe_status moe_match_merge_device(const moe_match* parts, uint64_t n_parts, uint
   return MOE_OK;
 }
 
+moe_status moe_eamc_clone(const moe_eamc* hc, moe_eamc** out) {
+  moe_eamc* src = const_cast<moe_eamc*>(hc);
+  if (!src || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard dg(src->device);
+  const uint64_t cells = (uint64_t)src->c.L * src->c.E, n = src->c.size;
+  std::vector<uint64_t> counts(n * cells), seqs(n);
+  for (uint64_t i = 0; i < n; ++i) CKS(read_entry(src, i, counts.data() + i * cells, &seqs[i]));
+  moe_eamc* h = nullptr;
+  CKS(moe_eamc_create(&src->shape, (moe_phase)src->phase, src->capacity, src->c.cb, src->device,
+                      &h));
+  if (n) {
+    const moe_status s = moe_eamc_append(h, counts.data(), seqs.data(), n);
+    if (s != MOE_OK) {
+      moe_eamc_destroy(h);
+      return s;
+    }
+  }
+  h->next_seq = src->next_seq;
+  h->c.index_base = src->c.index_base;
+  *out = h;
+  return MOE_OK;
+}
+
 moe_status moe_eamc_set_index_base(moe_eamc* h, uint64_t base) {
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
   h->c.index_base = base;
@@ -1104,37 +1127,68 @@ moe_status moe_eamc_kernel_times(const moe_eamc* hc, double* ms, uint64_t* calls
   return MOE_OK;
 }
 
+// Scalar entry points (eam_distance, cache_priority, select_eviction_victim)
+// run on a persistent per-(device, shape) scratch collection: creating a
+// handle costs device allocations and streams, which would dominate a call
+// the engine makes per slot (engine.cpp:443,:472,:644).  The lease holds the
+// cache lock, so concurrent scalar calls serialise on it.
+struct ScratchLease {
+  std::unique_lock<std::mutex> lock;
+  moe_eamc* h = nullptr;
+};
+
+static moe_status scratch_handle(const moe_shape* shape, ScratchLease* lease) {
+  struct Slot {
+    int dev;
+    uint32_t L, E;
+    moe_eamc* h;
+  };
+  static std::mutex mu;
+  static std::vector<Slot> cache;  // never destroyed: lives until process exit
+  int dev = 0, n_sm = 0;
+  cudaGetDevice(&dev);
+  CKS(device_ok(dev, &n_sm));
+  std::unique_lock<std::mutex> lk(mu);
+  for (const Slot& c : cache)
+    if (c.dev == dev && c.L == shape->n_layers && c.E == shape->n_experts_per_layer) {
+      lease->h = c.h;
+      lease->lock = std::move(lk);
+      return MOE_OK;
+    }
+  moe_eamc* h = nullptr;
+  CKS(moe_eamc_create(shape, MOE_PHASE_DECODE, 1, 1, dev, &h));
+  if (cache.size() >= 8) {
+    moe_eamc_destroy(cache.front().h);
+    cache.erase(cache.begin());
+  }
+  cache.push_back({dev, shape->n_layers, shape->n_experts_per_layer, h});
+  lease->h = h;
+  lease->lock = std::move(lk);
+  return MOE_OK;
+}
+
 moe_status moe_eam_distance(const moe_shape* shape, const uint64_t* a, const uint64_t* b,
                             double* out) {
   CKS(check_shape(shape));
   if (!a || !b || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
-  int dev = 0, n_sm = 0;
-  cudaGetDevice(&dev);
-  CKS(device_ok(dev, &n_sm));
-  moe_eamc* h = nullptr;
-  CKS(moe_eamc_create(shape, MOE_PHASE_DECODE, 1, 1, dev, &h));
-  moe_status s = MOE_OK;
-  {
-    const uint64_t cells = (uint64_t)shape->n_layers * shape->n_experts_per_layer;
-    std::vector<uint64_t> both(2 * cells);
-    std::copy(a, a + cells, both.begin());
-    std::copy(b, b + cells, both.begin() + cells);
-    DevProbes pr;
-    s = prep_probes(h, both.data(), 8, 2, false, h->st, &pr);
-    if (s == MOE_OK) {
-      DevBuf dd;
-      cudaError_t e = dd.ensure(8);
-      const uint64_t LR = (uint64_t)h->c.L * h->c.RB;
-      if (e == cudaSuccess)
-        e = moe::launch_pair_distance(pr.packed, pr.sqa, pr.packed + LR, pr.sqa + h->c.L, h->c.L,
-                                      h->c.C, h->c.RB, h->c.cb, dd.as<double>(), h->st);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(out, dd.p, 8, cudaMemcpyDeviceToHost, h->st);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);
-      if (e != cudaSuccess) s = fail(MOE_ERR_CUDA, "eam_distance: %s", cudaGetErrorString(e));
-    }
-  }
-  moe_eamc_destroy(h);
-  return s;
+  ScratchLease lease;
+  CKS(scratch_handle(shape, &lease));
+  moe_eamc* h = lease.h;
+  const uint64_t cells = (uint64_t)shape->n_layers * shape->n_experts_per_layer;
+  std::vector<uint64_t> both(2 * cells);
+  std::copy(a, a + cells, both.begin());
+  std::copy(b, b + cells, both.begin() + cells);
+  DevProbes pr;
+  CKS(prep_probes(h, both.data(), 8, 2, false, h->st, &pr));
+  cudaError_t e = h->dist.ensure(8);
+  const uint64_t LR = (uint64_t)h->c.L * h->c.RB;
+  if (e == cudaSuccess)
+    e = moe::launch_pair_distance(pr.packed, pr.sqa, pr.packed + LR, pr.sqa + h->c.L, h->c.L,
+                                  h->c.C, h->c.RB, h->c.cb, h->dist.as<double>(), h->st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, h->dist.p, 8, cudaMemcpyDeviceToHost, h->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);
+  if (e != cudaSuccess) return fail(MOE_ERR_CUDA, "eam_distance: %s", cudaGetErrorString(e));
+  return MOE_OK;
 }
 
 static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_t* cur_eam,
@@ -1244,13 +1298,6 @@ moe_status moe_decide(const moe_eamc* hc, const uint64_t* cur_eam, uint32_t curr
                      cap, n_out, victim, nullptr);
 }
 
-static moe_status scratch_handle(const moe_shape* shape, moe_eamc** h) {
-  int dev = 0, n_sm = 0;
-  cudaGetDevice(&dev);
-  CKS(device_ok(dev, &n_sm));
-  return moe_eamc_create(shape, MOE_PHASE_DECODE, 1, 1, dev, h);
-}
-
 moe_status moe_cache_priority(const moe_shape* shape, const uint64_t* request_eam,
                               uint32_t layer, uint32_t expert, double* out) {
   CKS(check_shape(shape));
@@ -1258,16 +1305,15 @@ moe_status moe_cache_priority(const moe_shape* shape, const uint64_t* request_ea
   // policy.cpp:130-131
   if (layer >= shape->n_layers || expert >= shape->n_experts_per_layer)
     return fail(MOE_ERR_OUT_OF_RANGE, "cache_priority: expert out of range");
-  moe_eamc* h = nullptr;
-  CKS(scratch_handle(shape, &h));
+  ScratchLease lease;
+  CKS(scratch_handle(shape, &lease));
+  moe_eamc* h = lease.h;
   moe_slot_view v{};
   v.slot = 0;
   v.layer_idx = layer;
   v.expert_idx = expert;
-  const moe_status s = decide_impl(h, shape, nullptr, 0, 0, 0, request_eam, &v, 1, nullptr, 0,
-                                   nullptr, nullptr, out);
-  moe_eamc_destroy(h);
-  return s;
+  return decide_impl(h, shape, nullptr, 0, 0, 0, request_eam, &v, 1, nullptr, 0, nullptr, nullptr,
+                     out);
 }
 
 moe_status moe_select_eviction_victim(const moe_shape* shape, const uint64_t* request_eam,
@@ -1283,12 +1329,10 @@ moe_status moe_select_eviction_victim(const moe_shape* shape, const uint64_t* re
   }
   *victim = -1;
   if (n_slots == 0) return MOE_OK;
-  moe_eamc* h = nullptr;
-  CKS(scratch_handle(shape, &h));
-  const moe_status s = decide_impl(h, shape, nullptr, 0, 0, 0, request_eam, slots, n_slots,
-                                   nullptr, 0, nullptr, victim, nullptr);
-  moe_eamc_destroy(h);
-  return s;
+  ScratchLease lease;
+  CKS(scratch_handle(shape, &lease));
+  return decide_impl(lease.h, shape, nullptr, 0, 0, 0, request_eam, slots, n_slots, nullptr, 0,
+                     nullptr, victim, nullptr);
 }
 
 moe_status moe_eam_trace_device(const moe_shape* shape, const void* topk_idx, int idx_bytes,

@@ -187,6 +187,18 @@ class Eamc:
             lib.moe_eamc_destroy(h)
             self._h = C.c_void_p()
 
+    def copy(self) -> "Eamc":
+        """Deep copy (the reference's implicit copy constructor): same slots,
+        seqs and next_seq, a new device collection."""
+        h = C.c_void_p()
+        check(lib.moe_eamc_clone(self._h, C.byref(h)))
+        return Eamc(self.shape, device=self.device, _handle=h)
+
+    __copy__ = copy
+
+    def __deepcopy__(self, memo):
+        return self.copy()
+
     # -- accessors (eam.hpp:80-87) -------------------------------------
     def _info(self):
         sh = _lib.moe_shape()
