@@ -246,6 +246,7 @@ def run_ours(args):
     if N > 1:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_val = evals_per_step * e2e_steps / float(t_e2e.item())
+    host_threads = int(_lib.lib.moe_host_threads())
 
     # ---- the other SURVEY 8 rows (prefetch decisions, construction, tracing, MIX)
     rows = None
@@ -275,8 +276,9 @@ def run_ours(args):
             },
             "roofline": roofline,
             "e2e": {"value": e2e_val, "unit": "evals/s", "steps": e2e_steps,
-                    "api": "moe_eamc_match (host u64 probes, pinned) + D2H results",
-                    "h2d_bytes_per_step": int(Q * L * E * 8),
+                    "api": ("moe_eamc_match (host u64 probes, pinned) + D2H results; u64 "
+                            f"narrowed to u8 on {host_threads} host threads inside the call"),
+                    "h2d_bytes_per_step": int(Q * L * E * 1),
                     "d2h_bytes_per_step": int(Q * 24)},
             "gpu_launches": gpu_launches,
             "kernel_ms_per_step": {"prep": kms[0] / max(kcalls[0], 1), "screen": screen_ms,

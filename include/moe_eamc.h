@@ -84,6 +84,9 @@ typedef struct moe_slot_view {
 typedef struct moe_eamc moe_eamc; /* opaque device-resident Eamc */
 
 int moe_abi_version(void);
+/* Host threads of the marshalling pool used by the host-pointer entry points
+ * (u64 -> storage-width narrowing; MOE_HOST_THREADS overrides). */
+int moe_host_threads(void);
 const char* moe_last_error(void);
 /* Device properties the library keys its launch geometry on. */
 moe_status moe_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,

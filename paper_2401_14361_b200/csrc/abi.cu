@@ -19,6 +19,8 @@
 
 #include "common.cuh"
 #include "host.hpp"
+
+#include <atomic>
 #include "kernels.cuh"
 
 using moe::DevColl;
@@ -172,6 +174,7 @@ struct moe_eamc {
   // pipelined host matching: copy stream, double-buffered u64 staging
   cudaStream_t st2 = nullptr;
   DevBuf raw2[2], outall;
+  PinBuf hpack;  // host-narrowed probes (moe_eamc_match, match_host_packed)
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
 
   ~moe_eamc() {
@@ -748,6 +751,8 @@ int moe_abi_version(void) { return MOE_EAMC_ABI_VERSION; }
 
 const char* moe_last_error(void) { return g_err.c_str(); }
 
+int moe_host_threads(void) { return moe::host::pool_threads(); }
+
 moe_status moe_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
                            size_t* l2_bytes) {
   int n = 0;
@@ -914,6 +919,101 @@ moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_byt
   return append_impl(h, counts, count_bytes, seqs, n);
 }
 
+// Host-narrowed matching for large host batches.  The reference API hands over
+// u64 counts (eam.hpp:55); shipping them as is makes the call PCIe-bound
+// (8 B/count).  Each host-pool task narrows one chunk to the storage width
+// into a pinned buffer (the OR of the chunk is the exact width check) and
+// enqueues that chunk's DMA on the copy stream itself, so transfers start
+// while other chunks are still being narrowed (MOE_MATCH_GROUPS > 1 also
+// splits the batch into groups matched as they arrive).
+// *done = false (nothing usable written) when some count exceeds the storage
+// width: the caller then takes the u64 path, which widens the collection.
+struct PackJob {
+  const uint64_t* src;
+  uint8_t *hp, *dp;
+  uint64_t cells, row_b, g0, g1, chunk;
+  int cb, device;
+  cudaStream_t st;
+  std::atomic<int> bad{0};
+  std::atomic<int> err{0};
+};
+
+static void pack_chunk_task(void* vj, int t) {
+  PackJob* j = static_cast<PackJob*>(vj);
+  const uint64_t off = j->g0 + (uint64_t)t * j->chunk;
+  const uint64_t m = std::min(j->chunk, j->g1 - off);
+  if (j->bad.load(std::memory_order_relaxed)) return;
+  const uint64_t o = moe::host::pack_counts_serial(j->src + off * j->cells, m * j->cells, j->cb,
+                                                   j->hp + off * j->row_b);
+  if (o > width_max(j->cb)) {
+    j->bad.store(1);
+    return;
+  }
+  if (cudaSetDevice(j->device) != cudaSuccess ||
+      cudaMemcpyAsync(j->dp + off * j->row_b, j->hp + off * j->row_b, m * j->row_b,
+                      cudaMemcpyHostToDevice, j->st) != cudaSuccess)
+    j->err.store(1);
+}
+
+static moe_status match_host_packed(moe_eamc* h, const uint64_t* probes, uint64_t n,
+                                    moe_match* out, bool* done) {
+  *done = false;
+  const int cb = h->c.cb;
+  const uint64_t cells = (uint64_t)h->c.L * h->c.E;
+  const uint64_t row_b = cells * cb;
+  if (!h->st2) {
+    CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_free[i], cudaEventDisableTiming));
+    }
+  }
+  CK(h->hpack.ensure(n * row_b));
+  CK(h->raw.ensure(n * row_b));
+  CK(h->outall.ensure(n * sizeof(moe_match)));
+  moe_match* dout = h->outall.as<moe_match>();
+  // one group measured fastest at SW (splitting the batch costs screen
+  // efficiency and per-group launches more than the overlap gains)
+  uint64_t groups = 1;
+  if (const char* e = getenv("MOE_MATCH_GROUPS")) groups = std::max(1, atoi(e));
+  groups = std::min<uint64_t>(groups, n);
+  const uint64_t threads = (uint64_t)moe::host::pool_threads();
+  PackJob j;
+  j.src = probes;
+  j.hp = h->hpack.as<uint8_t>();
+  j.dp = h->raw.as<uint8_t>();
+  j.cells = cells;
+  j.row_b = row_b;
+  j.cb = cb;
+  j.device = h->device;
+  j.st = h->st2;
+  for (uint64_t g = 0; g < groups; ++g) {
+    j.g0 = n * g / groups;
+    j.g1 = n * (g + 1) / groups;
+    // one chunk per pool thread (>= 64 KiB of input each)
+    j.chunk = std::max<uint64_t>((j.g1 - j.g0 + threads - 1) / threads,
+                                 std::max<uint64_t>(1, 8192 / cells));
+    if (const char* e = getenv("MOE_PACK_CHUNK")) j.chunk = std::max(1, atoi(e));
+    const int tasks = (int)((j.g1 - j.g0 + j.chunk - 1) / j.chunk);
+    moe::host::pool_run(tasks, pack_chunk_task, &j);
+    if (j.err.load()) return fail(MOE_ERR_CUDA, "probe upload failed");
+    if (j.bad.load()) {  // rare: widen through the u64 path
+      CK(cudaStreamSynchronize(h->st2));
+      CK(cudaStreamSynchronize(h->st));
+      return MOE_OK;
+    }
+    CK(cudaEventRecord(h->ev_copy[g & 1], h->st2));
+    CK(cudaStreamWaitEvent(h->st, h->ev_copy[g & 1], 0));
+    DevProbes pr;
+    CKS(match_all(h, j.dp + j.g0 * row_b, cb, j.g1 - j.g0, true, dout + j.g0, h->st, &pr,
+                  /*async=*/true));
+  }
+  CK(cudaMemcpyAsync(out, dout, n * sizeof(moe_match), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  *done = true;
+  return MOE_OK;
+}
+
 moe_status moe_eamc_match(const moe_eamc* hc, const uint64_t* probes, uint64_t n_probes,
                           moe_match* out, uint8_t* found) {
   moe_eamc* h = const_cast<moe_eamc*>(hc);
@@ -922,6 +1022,16 @@ moe_status moe_eamc_match(const moe_eamc* hc, const uint64_t* probes, uint64_t n
   DeviceGuard dg(h->device);
   const uint64_t cells = (uint64_t)h->c.L * h->c.E;
   const uint64_t bytes = n_probes * cells * 8;
+  const char* hp_env = getenv("MOE_HOST_PACK");
+  if (bytes >= (4ull << 20) && !(hp_env && hp_env[0] == '0')) {
+    bool done = false;
+    CKS(match_host_packed(h, probes, n_probes, out, &done));
+    if (done) {
+      if (found)
+        for (uint64_t q = 0; q < n_probes; ++q) found[q] = out[q].index != ~0ull;
+      return MOE_OK;
+    }
+  }
   uint64_t pipe_chunk = 0;  // probes per pipelined chunk (0 = one shot)
   if (const char* pc = getenv("MOE_PIPE_CHUNK")) pipe_chunk = strtoull(pc, nullptr, 10);
   else if (bytes >= (16ull << 20)) pipe_chunk = std::max<uint64_t>(1024, (n_probes + 3) / 4);

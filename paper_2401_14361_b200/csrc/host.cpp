@@ -1,14 +1,21 @@
 // host.cpp -- snapshot codec, capacity bound and the bench-family generator.
 #include "host.hpp"
 
+#include <algorithm>
+#include <atomic>
 #include <cctype>
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <sstream>
+#include <thread>
 
 namespace moe {
 namespace host {
@@ -379,6 +386,150 @@ void bench_family(uint64_t seed, uint32_t L, uint32_t E, uint64_t skip, uint64_t
         else if (count_bytes == 2) reinterpret_cast<uint16_t*>(o)[idx] = (uint16_t)v;
         else reinterpret_cast<uint64_t*>(o)[idx] = v;
       }
+}
+
+}  // namespace host
+}  // namespace moe
+
+// ---------------------------------------------------------------- host pool
+namespace moe {
+namespace host {
+namespace {
+
+class Pool {
+ public:
+  Pool() {
+    int n = (int)std::thread::hardware_concurrency();
+    if (const char* e = std::getenv("MOE_HOST_THREADS")) n = std::atoi(e);
+    n_ = std::max(1, std::min(n, 64));
+    for (int i = 1; i < n_; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~Pool() {
+    stop_.store(true);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  int size() const { return n_; }
+
+  void run(int n, void (*fn)(void*, int), void* ctx) {
+    if (n <= 0) return;
+    std::lock_guard<std::mutex> serial(run_mu_);  // one job at a time
+    if (n_ == 1 || n == 1) {
+      for (int i = 0; i < n; ++i) fn(ctx, i);
+      return;
+    }
+    fn_ = fn;
+    ctx_ = ctx;
+    n_tasks_ = n;
+    done_.store(0, std::memory_order_relaxed);
+    next_.store(0, std::memory_order_release);
+    {
+      std::lock_guard<std::mutex> g(mu_);  // no lost wake-up for a sleeping worker
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+    work();
+    while (done_.load(std::memory_order_acquire) < n) std::this_thread::yield();
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      const int i = next_.fetch_add(1, std::memory_order_acq_rel);
+      if (i >= n_tasks_) return;
+      fn_(ctx_, i);
+      done_.fetch_add(1, std::memory_order_release);
+    }
+  }
+  // Workers spin for a while after each job (back-to-back jobs of one call
+  // then start without a futex wake-up), and sleep on the condvar after.
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      const auto t0 = std::chrono::steady_clock::now();
+      int k = 0;
+      while (gen_.load(std::memory_order_acquire) == seen) {
+        if ((++k & 63) == 0 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(300)) {
+          std::unique_lock<std::mutex> g(mu_);
+          cv_.wait(g, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+          break;
+        }
+        std::this_thread::yield();
+      }
+      seen = gen_.load(std::memory_order_acquire);
+      if (stop_.load()) return;
+      work();
+    }
+  }
+  int n_ = 1;
+  std::vector<std::thread> workers_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<bool> stop_{false};
+  void (*fn_)(void*, int) = nullptr;
+  void* ctx_ = nullptr;
+  int n_tasks_ = 0;
+  std::atomic<int> next_{0}, done_{0};
+};
+
+Pool& pool() {
+  static Pool* p = new Pool();  // leaked: workers outlive static destruction order
+  return *p;
+}
+
+struct PackCtx {
+  const uint64_t* src;
+  uint64_t n;
+  int cb, parts;
+  void* dst;
+  uint64_t ors[64];
+};
+
+template <typename T>
+uint64_t pack_range(const uint64_t* __restrict s, T* __restrict d, uint64_t n) {
+  uint64_t o = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t v = s[i];
+    o |= v;
+    d[i] = (T)v;
+  }
+  return o;
+}
+
+void pack_task(void* vc, int t) {
+  PackCtx* c = static_cast<PackCtx*>(vc);
+  // 64-element aligned piece boundaries
+  const uint64_t a = (c->n * t / c->parts) & ~63ull;
+  const uint64_t b = t + 1 == c->parts ? c->n : (c->n * (t + 1) / c->parts) & ~63ull;
+  c->ors[t] = c->cb == 1 ? pack_range(c->src + a, static_cast<uint8_t*>(c->dst) + a, b - a)
+                         : pack_range(c->src + a, static_cast<uint16_t*>(c->dst) + a, b - a);
+}
+
+}  // namespace
+
+uint64_t pack_counts_serial(const uint64_t* src, uint64_t n, int cb, void* dst) {
+  return cb == 1 ? pack_range(src, static_cast<uint8_t*>(dst), n)
+                 : pack_range(src, static_cast<uint16_t*>(dst), n);
+}
+
+int pool_threads() { return pool().size(); }
+
+void pool_run(int n, void (*fn)(void*, int), void* ctx) { pool().run(n, fn, ctx); }
+
+uint64_t pack_counts(const uint64_t* src, uint64_t n, int cb, void* dst) {
+  PackCtx c{src, n, cb, 1, dst, {}};
+  // >= 256 KiB of input per piece keeps the pool's fork/join cost negligible
+  c.parts = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)pool().size(), n / 32768));
+  pool().run(c.parts, pack_task, &c);
+  uint64_t o = 0;
+  for (int t = 0; t < c.parts; ++t) o |= c.ors[t];
+  return o;
 }
 
 }  // namespace host

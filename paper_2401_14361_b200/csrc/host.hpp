@@ -29,3 +29,25 @@ void bench_family(uint64_t seed, uint32_t L, uint32_t E, uint64_t skip, uint64_t
 
 }  // namespace host
 }  // namespace moe
+
+namespace moe {
+namespace host {
+
+// Persistent worker pool for host-side marshalling of the host-pointer entry
+// points (the reference's API hands over u64 count matrices; narrowing them
+// to the device storage width on the host cuts the PCIe bytes 8x).  Workers
+// are created once per process; run() executes fn(0..n-1) on the pool plus
+// the calling thread and returns when all are done.  MOE_HOST_THREADS
+// overrides the size (default: hardware_concurrency, at most 64).
+int pool_threads();
+void pool_run(int n, void (*fn)(void*, int), void* ctx);
+
+// Narrow n u64 counts to cb (1 or 2) bytes, in parallel on the pool.
+// Returns the bitwise OR of all inputs: the caller's width check is
+// `or > width_max(cb)` (exactly "some count exceeds the width").
+uint64_t pack_counts(const uint64_t* src, uint64_t n, int cb, void* dst);
+// The same on the calling thread only (for use inside a pool task).
+uint64_t pack_counts_serial(const uint64_t* src, uint64_t n, int cb, void* dst);
+
+}  // namespace host
+}  // namespace moe

@@ -553,6 +553,30 @@ def test_host_api_pipelined_large_batch(m, orc):
     check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
 
 
+@pytest.mark.parametrize("groups,chunk", [(None, None), ("3", "77"), ("1", "5000")])
+def test_host_api_narrowed_batch(m, orc, monkeypatch, groups, chunk):
+    """>= 4 MB of u64 probes: narrowed to the storage width on the host pool,
+    chunked DMA, matched in groups; both storage widths; identical to the
+    u64 path."""
+    if groups:
+        monkeypatch.setenv("MOE_MATCH_GROUPS", groups)
+        monkeypatch.setenv("MOE_PACK_CHUNK", chunk)
+    L, E, P, Q = 12, 128, 700, 2111
+    fam = m.gen_bench_family(78, L, E, P + Q).copy()
+    e = filled(m, L, E, fam[:P])
+    got = check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
+    assert e.count_bytes() == 1
+    monkeypatch.setenv("MOE_HOST_PACK", "0")
+    ref = e.match_batch(fam[P:])
+    assert np.array_equal(ref["index"], got["index"]) and np.array_equal(ref["distance"], got["distance"])
+    monkeypatch.delenv("MOE_HOST_PACK")
+    wide = fam[:P].copy()
+    wide[::5] *= 400  # 2-byte storage: probes narrowed to u16 on the host
+    e2 = filled(m, L, E, wide)
+    assert e2.count_bytes() == 2
+    check_match(m, orc, e2, wide, seqs_of(P), fam[P:] * 3)
+
+
 def test_trace_long_and_empty_requests(m, orc):
     """Requests longer than one block's ownership limit (chunked, atomics),
     empty requests, unaligned id ranges, and tokens outside any request."""
