@@ -91,6 +91,8 @@ const char* moe_last_error(void);
 /* Device properties the library keys its launch geometry on. */
 moe_status moe_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
                            size_t* l2_bytes);
+/* Creates the device's CUDA context (the cost of the first call otherwise). */
+moe_status moe_device_warmup(int device);
 
 /* ---- collection lifecycle: Eamc(ModelShape, Phase, capacity) eam.cpp:106-111 ---- */
 /* count_bytes: storage width of one count on the device, 1 or 2 (0 = 1).

@@ -767,6 +767,14 @@ moe_status moe_device_info(int device, int* sm_count, int* cc_major, int* cc_min
   return MOE_OK;
 }
 
+moe_status moe_device_warmup(int device) {
+  int n_sm = 0;
+  CKS(device_ok(device, &n_sm));
+  DeviceGuard dg(device);
+  CK(cudaFree(nullptr));
+  return MOE_OK;
+}
+
 moe_status moe_eamc_create(const moe_shape* shape, moe_phase phase, uint64_t capacity,
                            int count_bytes, int device, moe_eamc** out) {
   if (!out) return fail(MOE_ERR_INVALID_ARGUMENT, "null out");

@@ -363,26 +363,76 @@ struct RefineArgs {
 // candidates*L/32 instead of with the candidate count.
 constexpr int kRefineWarps = 4;
 constexpr int kRefineBuf = 256;  // doubles of per-warp scratch
+constexpr int kRefinePartBytes = 4096;  // per-warp scratch of per-chunk partial dots
+
+// Lane-per-row exact evaluation (the general path of k_refine for EAMs too
+// long for the chunk-parallel scratch): (candidate, layer) pairs over the
+// lanes, each lane walking its row's 16-byte chunks.
+template <int CB>
+__device__ __forceinline__ void refine_rows_per_lane(const RefineArgs& r, const uint8_t* pa,
+                                                     const double* sqa, const uint32_t* cand,
+                                                     uint32_t nc, double* rbuf, uint32_t lane,
+                                                     Best& b) {
+  const uint64_t LR = (uint64_t)r.L * r.RB;
+  const uint32_t G = max(1u, min(32u, (uint32_t)kRefineBuf / r.L));
+  for (uint32_t g0 = 0; g0 < nc; g0 += G) {
+    const uint32_t gn = min(G, nc - g0);
+    const uint32_t pairs = gn * r.L;
+    const uint64_t my_seq = lane < gn ? r.seq[cand[g0 + lane]] : 0;
+    for (uint32_t id = lane; id < pairs; id += 32) {
+      const uint32_t ci = id / r.L, l = id - ci * r.L;
+      const uint32_t p = cand[g0 + ci];
+      typename Dot<CB>::Acc acc = 0;
+      const uint4* ra = reinterpret_cast<const uint4*>(pa + (uint64_t)l * r.RB);
+      const uint4* rb = reinterpret_cast<const uint4*>(r.counts + p * LR + (uint64_t)l * r.RB);
+      for (uint32_t c = 0; c < r.C; ++c) acc = Dot<CB>::chunk(__ldg(ra + c), __ldg(rb + c), acc);
+      rbuf[ci * r.L + l] = row_sim_exact((uint64_t)acc, sqa[l], r.sqb[(uint64_t)p * r.L + l]);
+    }
+    __syncwarp();
+    if (lane < gn) {
+      const uint32_t p = cand[g0 + lane];
+      double sm = 0.0;
+      for (uint32_t l = 0; l < r.L; ++l) sm = __dadd_rn(sm, rbuf[lane * r.L + l]);
+      const double d = finish_distance(sm, r.L);
+      if (better(d, my_seq, b.d, b.seq)) b = Best{d, my_seq, p};
+    }
+    __syncwarp();
+  }
+}
 
 template <int CB>
 __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r) {
   __shared__ double rbuf[kRefineWarps][kRefineBuf];
   __shared__ uint32_t cand[kRefineWarps][256];
+  __shared__ uint64_t parts[kRefineWarps][kRefinePartBytes / 8];
   const uint32_t wib = threadIdx.x >> 5;
   const uint32_t q = blockIdx.x * kRefineWarps + wib;
   const uint32_t lane = threadIdx.x & 31;
   if (q >= r.Q) return;
-  if (r.halt && *r.halt) return;
+  // Every load that does not depend on another is issued up front (one
+  // memory round trip instead of a chain): flags, bucket count, threshold,
+  // the first 32 bucket slots (the bucket always spans bcap slots per probe)
+  // and an L1 prefetch of the probe's packed rows.
+  const uint64_t LR = (uint64_t)r.L * r.RB;
+  const uint8_t* pa = r.probes + q * LR;
+  const int halted = r.halt ? *r.halt : 0;
+  const uint8_t is_wide = r.wide ? r.wide[q] : (uint8_t)0;
+  const uint32_t n = r.bcnt[q];
+  const float thr = __uint_as_float(r.T[q]) + r.eps2;
+  uint2 e0 = make_uint2(0u, 0x7f800000u);
+  if (lane < r.bcap) e0 = r.bucket[(uint64_t)q * r.bcap + lane];
+  for (uint64_t o = (uint64_t)lane * 128; o < LR; o += 32 * 128)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + o));
+  if (halted) return;
   const moe_match none{kNone, kNone, __longlong_as_double(0x7ff0000000000000ll)};
   if (r.size == 0) {
     if (lane == 0) r.out[q] = none;
     return;
   }
-  if (r.wide && r.wide[q]) {  // cannot be matched at this width: explicit sentinel
+  if (is_wide) {  // cannot be matched at this width: explicit sentinel
     if (lane == 0) r.out[q] = moe_match{kNone - 1, kNone, __longlong_as_double(0x7ff8000000000000ll)};
     return;
   }
-  const uint32_t n = r.bcnt[q];
   if (n > r.bcap) {
     if (lane == 0) {
       if (r.over_list) r.over_list[atomicAdd(r.over_n, 1u)] = q;
@@ -391,14 +441,13 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
     return;
   }
   // compact the candidates that pass the final threshold
-  const float thr = __uint_as_float(r.T[q]) + r.eps2;
   uint32_t nc = 0;
   for (uint32_t base = 0; base < n; base += 32) {
     const uint32_t i = base + lane;
     bool pass = false;
     uint32_t p = 0;
     if (i < n) {
-      const uint2 e = r.bucket[(uint64_t)q * r.bcap + i];
+      const uint2 e = base == 0 ? e0 : r.bucket[(uint64_t)q * r.bcap + i];
       p = e.x;
       pass = __uint_as_float(e.y) <= thr;
     }
@@ -407,32 +456,57 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
     nc += __popc(m);
   }
   __syncwarp();
-  const uint64_t LR = (uint64_t)r.L * r.RB;
-  const uint8_t* pa = r.probes + q * LR;
   const double* sqa = r.sqa + (uint64_t)q * r.L;
   Best b{__longlong_as_double(0x7ff0000000000000ll), kNone, kNone};
-  // candidates per group: one summing lane each, and their L values in rbuf
-  const uint32_t G = max(1u, min(32u, (uint32_t)kRefineBuf / r.L));
+  // Candidates are taken in groups; a group's (candidate, layer, 16-byte
+  // chunk) items are spread over the lanes so that consecutive lanes read
+  // consecutive chunks of the same row (coalesced 128-bit loads), the
+  // per-chunk partial dots go to shared memory, one lane per (candidate,
+  // layer) sums its row's chunks and applies the fp64 row similarity, and one
+  // lane per candidate sums the layers in order (eam.cpp:95-98).
+  using Acc = typename Dot<CB>::Acc;
+  constexpr uint32_t kParts = kRefinePartBytes / sizeof(Acc);
+  const uint32_t C = r.C;
+  if ((uint64_t)r.L * C > kParts) {  // very long EAMs: one lane per (candidate, layer) row
+    refine_rows_per_lane<CB>(r, pa, sqa, cand[wib], nc, rbuf[wib], lane, b);
+    b = warp_best(b);
+    if (lane == 0)
+      r.out[q] = moe_match{b.idx == kNone ? kNone : b.idx + r.index_base, b.seq, b.d};
+    return;
+  }
+  const uint32_t G = max(1u, min(min(32u, (uint32_t)kRefineBuf / r.L), kParts / (r.L * C)));
+  const uint4* pa4 = reinterpret_cast<const uint4*>(pa);
+  const uint4* cb4 = reinterpret_cast<const uint4*>(r.counts);
+  const uint64_t LC = (uint64_t)r.L * C;
+  Acc* part = reinterpret_cast<Acc*>(parts[wib]);
   for (uint32_t g0 = 0; g0 < nc; g0 += G) {
     const uint32_t gn = min(G, nc - g0);
     const uint32_t pairs = gn * r.L;
-    for (uint32_t id = lane; id < pairs; id += 32) {
-      const uint32_t ci = id / r.L, l = id - ci * r.L;
+    const uint32_t items = pairs * C;
+    // the summing lane's seq load overlaps the row loads below
+    const uint64_t my_seq = lane < gn ? r.seq[cand[wib][g0 + lane]] : 0;
+#pragma unroll 4
+    for (uint32_t it = lane; it < items; it += 32) {
+      const uint32_t ci = it / (uint32_t)LC;
+      const uint32_t lc = it - ci * (uint32_t)LC;  // = l * C + chunk
       const uint32_t p = cand[wib][g0 + ci];
-      typename Dot<CB>::Acc acc = 0;
-      const uint4* ra = reinterpret_cast<const uint4*>(pa + (uint64_t)l * r.RB);
-      const uint4* rb = reinterpret_cast<const uint4*>(r.counts + p * LR + (uint64_t)l * r.RB);
-      for (uint32_t c = 0; c < r.C; ++c) acc = Dot<CB>::chunk(ra[c], rb[c], acc);
-      rbuf[wib][ci * r.L + l] = row_sim_exact((uint64_t)acc, sqa[l], r.sqb[(uint64_t)p * r.L + l]);
+      part[it] = Dot<CB>::chunk(__ldg(pa4 + lc), __ldg(cb4 + (uint64_t)p * LC + lc), (Acc)0);
+    }
+    __syncwarp();
+    for (uint32_t pr = lane; pr < pairs; pr += 32) {
+      const uint32_t ci = pr / r.L, l = pr - ci * r.L;
+      const uint32_t p = cand[wib][g0 + ci];
+      uint64_t dot = 0;
+      for (uint32_t c = 0; c < C; ++c) dot += (uint64_t)part[pr * C + c];
+      rbuf[wib][pr] = row_sim_exact(dot, sqa[l], r.sqb[(uint64_t)p * r.L + l]);
     }
     __syncwarp();
     if (lane < gn) {
       const uint32_t p = cand[wib][g0 + lane];
-      const uint64_t sq = r.seq[p];
       double sm = 0.0;
       for (uint32_t l = 0; l < r.L; ++l) sm = __dadd_rn(sm, rbuf[wib][lane * r.L + l]);
       const double d = finish_distance(sm, r.L);
-      if (better(d, sq, b.d, b.seq)) b = Best{d, sq, p};
+      if (better(d, my_seq, b.d, b.seq)) b = Best{d, my_seq, p};
     }
     __syncwarp();
   }
@@ -580,6 +654,85 @@ __global__ void __launch_bounds__(256)
       __half* orow = nrm + it * (uint64_t)Kp;
       for (uint32_t k = L * E + lane; k < Kp; k += 32) orow[k] = __float2half_rn(0.f);
     }
+  }
+}
+
+// Fast path of k_prep for u8 counts into u8 storage (every probe batch that
+// arrives narrowed, and u8 collections): one warp per EAM, its rows loaded
+// 8 at a time before any is used (one memory round trip per 8 rows), Σc² by
+// IDP4A + REDUX (exact: E <= 256 so Σc² < 2^24), fp16 operand written 8 B per
+// lane, and the zero-row mask / width flag stored directly (no pre-zeroing
+// launches).  Same outputs as k_prep<1> with cb = 1.
+template <int WPL>
+__global__ void __launch_bounds__(256)
+    k_prep_u8(const uint8_t* src, uint64_t n, uint32_t E, uint32_t L, uint32_t RB, uint8_t* dst,
+              float* ia, double* sq, float* ibT, uint64_t ib_cap, uint64_t ib_base, __half* nrm,
+              uint32_t Kp, uint64_t* zmask, uint8_t* wide) {
+  const uint64_t it = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (it >= n) return;
+  const uint32_t ew = E >> 2, nwords = RB >> 2;
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src) + it * L * ew;
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst) + it * L * nwords;
+  uint64_t zbits = 0;
+  for (uint32_t l0 = 0; l0 < L; l0 += 8) {
+    uint32_t wv[8][WPL];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int k = 0; k < WPL; ++k) {
+        const uint32_t w = lane + 32 * k, l = l0 + r;
+        wv[r][k] = (l < L && w < ew) ? __ldg(s32 + (uint64_t)l * ew + w) : 0u;
+      }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint32_t l = l0 + r;
+      if (l >= L) break;
+      uint32_t ss = 0;
+#pragma unroll
+      for (int k = 0; k < WPL; ++k) ss = __dp4a(wv[r][k], wv[r][k], ss);
+      ss = __reduce_add_sync(0xffffffffu, ss);
+      const uint64_t row = it * L + l;
+#pragma unroll
+      for (int k = 0; k < WPL; ++k) {
+        const uint32_t w = lane + 32 * k;
+        if (w < nwords) d32[(uint64_t)l * nwords + w] = wv[r][k];
+      }
+      const double sd = __dsqrt_rn((double)ss);
+      const float inv = ss ? __double2float_rn(__drcp_rn(sd)) : 0.f;
+      if (lane == 0) {
+        sq[row] = sd;
+        if (ia) ia[row] = inv;
+        if (ibT) ibT[(uint64_t)l * ib_cap + ib_base + it] = inv;
+      }
+      if (ss == 0) zbits |= 1ull << (l & 63);
+      if (nrm) {
+        __half* o = nrm + it * (uint64_t)Kp + (uint64_t)l * E;
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+          const uint32_t w = lane + 32 * k;
+          if (w < ew) {
+            const uint32_t x = wv[r][k];
+            const __half2 lo = __floats2half2_rn(__uint2float_rn(x & 0xffu) * inv,
+                                                 __uint2float_rn((x >> 8) & 0xffu) * inv);
+            const __half2 hi = __floats2half2_rn(__uint2float_rn((x >> 16) & 0xffu) * inv,
+                                                 __uint2float_rn(x >> 24) * inv);
+            uint2 v;
+            v.x = *reinterpret_cast<const uint32_t*>(&lo);
+            v.y = *reinterpret_cast<const uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(o + 4 * w) = v;
+          }
+        }
+      }
+    }
+  }
+  if (nrm) {
+    __half* orow = nrm + it * (uint64_t)Kp;
+    for (uint32_t k = L * E + lane; k < Kp; k += 32) orow[k] = __float2half_rn(0.f);
+  }
+  if (lane == 0) {
+    if (zmask) zmask[it] = zbits;
+    if (wide) wide[it] = 0;
   }
 }
 
@@ -1349,6 +1502,20 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
                         cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const uint32_t threads = 256;
+  // u8 -> u8 fast path (8-byte aligned fp16 rows need E % 4 == 0)
+  if (src_bytes == 1 && cb == 1 && (E & 3) == 0 && E <= 256 &&
+      (reinterpret_cast<uintptr_t>(src) & 3) == 0) {
+    const uint64_t wblocks = (n * 32 + threads - 1) / threads;
+    if (E <= 128)
+      k_prep_u8<1><<<(unsigned)wblocks, threads, 0, st>>>(
+          static_cast<const uint8_t*>(src), n, E, L, RB, dst, ia, sq, ibT, ib_cap, ib_base, nrm,
+          Kp, zmask, wide);
+    else
+      k_prep_u8<2><<<(unsigned)wblocks, threads, 0, st>>>(
+          static_cast<const uint8_t*>(src), n, E, L, RB, dst, ia, sq, ibT, ib_cap, ib_base, nrm,
+          Kp, zmask, wide);
+    return cudaGetLastError();
+  }
   const uint64_t rows = n * L;
   const uint64_t blocks = (rows * 32 + threads - 1) / threads;
   const uint64_t limit = cb == 1 ? 255ull : 65535ull;

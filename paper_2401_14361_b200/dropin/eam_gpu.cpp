@@ -10,6 +10,16 @@
 #include "dropin_common.hpp"
 #include "moe_eamc.h"
 
+namespace {
+// Device bring-up at program start (as an integrating engine would do when it
+// loads its policy library), so the first decision does not pay for CUDA
+// context creation.  Failure is ignored here: every later call reports it.
+const bool g_warm = [] {
+  (void)moe_device_warmup(moesim::dropin::device());
+  return true;
+}();
+}  // namespace
+
 namespace moesim {
 
 using dropin::check;

@@ -167,6 +167,20 @@ def test_match_wide_counts(m, orc):
         e2.match_batch(fam[P:P + 1] * 70000)
 
 
+def test_match_long_wide_eams(m, orc):
+    """2-byte storage with L*E large enough that k_refine takes its
+    lane-per-row path (L x 20 chunks of 16 B > the chunk-parallel scratch)."""
+    L, E, P = 40, 160, 500
+    fam = m.gen_bench_family(31, L, E, P + 20).copy()
+    fam[::3] *= 300
+    e = filled(m, L, E, fam[:P])
+    assert e.count_bytes() == 2
+    check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
+    dup = np.concatenate([fam[:P], np.repeat(fam[P:P + 1], 40, axis=0)])
+    e2 = filled(m, L, E, dup)
+    check_match(m, orc, e2, dup, seqs_of(len(dup)), fam[P:P + 2])
+
+
 def test_match_f2_workload(m, orc):
     """Realistic grouped/skewed request EAMs (F2) and iteration probes."""
     w = Workload(12, 64, 1, seed=1001)
