@@ -175,6 +175,17 @@ struct moe_eamc {
   cudaStream_t st2 = nullptr;
   DevBuf raw2[2], outall;
   PinBuf hpack;  // host-narrowed probes (moe_eamc_match, match_host_packed)
+  // collection version: bumped by every mutation (insert/build/append/widen)
+  uint64_t version = 0;
+  // decision-path layer-prefix cache (decide_impl / k_dec_dist): pref[p] =
+  // the in-order layer sum of rows [0, dec_keep] for the probe rows dec_rows
+  PinBuf dpin, cpin;
+  DevBuf pref, oscr;
+  std::vector<uint8_t> dec_rows;
+  int64_t dec_keep = -1;
+  uint64_t dec_version = ~0ull;
+  int dec_cb = 0;
+  moe_status last_status = MOE_OK;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
 
   ~moe_eamc() {
@@ -257,6 +268,7 @@ moe_status ensure_alloc(moe_eamc* h, uint64_t need) {
 // Re-encode the collection with 2-byte counts.
 moe_status widen(moe_eamc* h) {
   DevColl& c = h->c;
+  ++h->version;
   if (c.cb == 2) return fail(MOE_ERR_OVERFLOW, "count exceeds 65535 (2-byte storage limit)");
   const uint32_t RB2 = row_bytes(c.E, 2);
   const uint64_t rows = c.cap ? (c.cap + moe::kNT) * c.L : 0;
@@ -645,6 +657,7 @@ moe_status stage_entries(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t 
 // Sequential Eamc::insert semantics for a staged batch (K7 replay).
 moe_status replay_staged(moe_eamc* h, Staged& s, int64_t* evicted_slots) {
   DevColl& c = h->c;
+  ++h->version;
   const uint32_t n = s.pr.Q;
   uint32_t i = 0;
   // appends below capacity (eam.cpp:160-162)
@@ -864,6 +877,7 @@ moe_status moe_eamc_insert(moe_eamc* h, const uint64_t* counts, moe_eam_kind kin
   CK(cudaMemcpyAsync(&v, dv, sizeof v, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   if (evicted_counts) CKS(read_entry(h, v.index - h->c.index_base, evicted_counts, nullptr));
+  ++h->version;
   CK(moe::launch_replace(h->c, s.pr, 0, dv, h->next_seq, nullptr, h->st));
   CK(cudaStreamSynchronize(h->st));
   h->next_seq++;
@@ -893,6 +907,7 @@ static moe_status append_impl(moe_eamc* h, const void* counts, int cbytes, const
                               uint64_t n) {
   if (h->c.size + n > h->capacity)
     return fail(MOE_ERR_SNAPSHOT, "snapshot holds more entries than its capacity");
+  ++h->version;
   const uint64_t cells = (uint64_t)h->c.L * h->c.E;
   const uint64_t chunk = std::max<uint64_t>(1, (256ull << 20) / (cells * cbytes));
   Staged s;
@@ -1309,6 +1324,78 @@ moe_status moe_eam_distance(const moe_shape* shape, const uint64_t* a, const uin
   return MOE_OK;
 }
 
+// Decision-path distance pass over a host probe (prefetch_priorities /
+// decide): the probe is narrowed to the storage width on the host (one
+// small pinned upload instead of an 8-byte-per-count copy), and the per-entry
+// layer sums of the rows it shares with the previous call's probe -- the
+// engine calls once per layer with the iteration EAM growing by one row
+// (engine.cpp:546, :587) -- are reused from pref (k_dec_dist).  Returns
+// false (nothing launched) when the probe does not fit the storage width;
+// launch errors land in h->last_status.
+static bool dec_pass(moe_eamc* h, const uint64_t* probe, uint32_t cur, cudaStream_t st,
+                     DevProbes* pr) {
+  h->last_status = MOE_OK;
+  DevColl& c = h->c;
+  const int cb = c.cb;
+  const uint32_t L = c.L, E = c.E;
+  const uint64_t row_b = (uint64_t)E * cb, cells = (uint64_t)L * E;
+  const uint64_t nz_off = (cells * cb + 15) & ~15ull;
+  auto bad = [&](moe_status st_) {
+    h->last_status = st_;
+    return true;
+  };
+  if (h->dpin.ensure(nz_off + L * 2 + 16) != cudaSuccess) return bad(fail(MOE_ERR_CUDA, "pinned alloc"));
+  uint8_t* hb = h->dpin.as<uint8_t>();
+  if (moe::host::pack_counts_serial(probe, cells, cb, hb) > width_max(cb)) return false;
+  // reuse the layer-prefix sums when rows [0, dec_keep] are unchanged
+  uint32_t j0 = 0;
+  if (h->dec_keep >= 0 && h->dec_version == h->version && h->dec_cb == cb &&
+      std::memcmp(hb, h->dec_rows.data(), (size_t)(h->dec_keep + 1) * row_b) == 0)
+    j0 = (uint32_t)h->dec_keep + 1;
+  const bool store = (int64_t)cur > h->dec_keep || j0 == 0;
+  const uint32_t keep = store ? cur : L;  // L: leave pref as it is
+  uint16_t* nz = reinterpret_cast<uint16_t*>(hb + nz_off);
+  uint32_t n_nz = 0;
+  for (uint32_t l = j0; l < L; ++l) {
+    const uint8_t* r = hb + l * row_b;
+    bool any = false;
+    for (uint64_t b = 0; b < row_b && !any; ++b) any = r[b] != 0;
+    if (any) nz[n_nz++] = (uint16_t)l;
+  }
+  auto ck = [&](cudaError_t e) {
+    if (e != cudaSuccess) h->last_status = fail(MOE_ERR_CUDA, "%s", cudaGetErrorString(e));
+    return e == cudaSuccess;
+  };
+  if (!ck(h->raw.ensure(nz_off + L * 2 + 16)) || !ck(h->pref.ensure((size_t)std::max<uint32_t>(c.size, 1) * 8)) ||
+      !ck(h->dist.ensure((size_t)std::max<uint32_t>(c.size, 1) * 8)) ||
+      !ck(cudaMemcpyAsync(h->raw.p, hb, nz_off + n_nz * 2, cudaMemcpyHostToDevice, st)))
+    return true;
+  const bool prof = h->prof;
+  h->prof = false;
+  const moe_status ps = launch_probe_prep(h, h->raw.p, cb, 1, st, pr);
+  h->prof = prof;
+  if (ps != MOE_OK) return bad(ps);
+  unsigned long long* dmin = reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224);
+  // explicit rows: through the last nonzero probe row and the stored row
+  uint32_t hi = n_nz ? nz[n_nz - 1] : 0;
+  if (keep < L) hi = std::max(hi, keep);
+  if (!n_nz && keep >= L) hi = j0 ? j0 - 1 : 0;  // nothing explicit beyond the cached prefix
+  if (!ck(cudaMemsetAsync(dmin, 0xff, 8, st)) ||
+      !ck(moe::launch_dec_dist(c, pr->packed, pr->sqa,
+                               reinterpret_cast<const uint16_t*>(h->raw.as<uint8_t>() + nz_off),
+                               n_nz, j0, hi, keep, h->pref.as<double>(), h->dist.as<double>(),
+                               dmin, h->agg.as<unsigned long long>(), (uint32_t)cells,
+                               h->small.as<uint32_t>() + 10, st)))
+    return true;
+  if (store) {
+    h->dec_rows.assign(hb, hb + (size_t)(cur + 1) * row_b);
+    h->dec_keep = cur;
+    h->dec_version = h->version;
+    h->dec_cb = cb;
+  }
+  return true;
+}
+
 static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_t* cur_eam,
                               uint32_t current_layer, int filter, int do_prefetch,
                               const uint64_t* request_eam, const moe_slot_view* slots,
@@ -1321,26 +1408,38 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
   CK(h->small.ensure(256));
   CK(h->pin.ensure(256));
   unsigned long long* agg = h->agg.as<unsigned long long>();
-  CK(cudaMemsetAsync(agg, 0, cells * 8, st));
   const bool prefetch_live = do_prefetch && h->c.size > 0;
   const uint64_t ncand = prefetch_live && current_layer + 1 < L ? (uint64_t)(L - current_layer - 1) * E : 0;
   CK(h->cand.ensure(std::max<uint64_t>(ncand, 1) * sizeof(moe_candidate)));
   uint32_t* dn = h->small.as<uint32_t>() + 12;
   if (prefetch_live) {
-    // one exact pass over the collection (row-parallel), window membership
-    // (kMatchWindow, policy.hpp:30) + u64 aggregation of the members' rows > l,
-    // then priorities / floor filter / order
+    // one exact pass over the collection, window membership (kMatchWindow,
+    // policy.hpp:30) + u64 aggregation of the members' rows > l, then
+    // priorities / floor filter / order
     DevProbes pr;
-    CKS(launch_exact_distances(h, cur_eam, st, &pr));
+    bool fused = false;  // k_dec_dist zeroed agg and the members count
+    if (!h->c.L || h->c.L > 256 || !dec_pass(h, cur_eam, current_layer, st, &pr)) {
+      CK(cudaMemsetAsync(agg, 0, cells * 8, st));
+      CKS(launch_exact_distances(h, cur_eam, st, &pr));
+    } else if (h->last_status != MOE_OK) {
+      return h->last_status;
+    } else {
+      fused = true;
+    }
     CK(h->mem.ensure((size_t)h->c.size * 4));
     CK(moe::launch_member_agg(h->c, h->dist.as<double>(),
                               reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224),
                               0.01, current_layer, h->mem.as<uint32_t>(),
-                              h->small.as<uint32_t>() + 10, agg, h->n_sm, st));
+                              h->small.as<uint32_t>() + 10, agg, h->n_sm, st, fused));
     CK(h->keys.ensure(std::max<uint64_t>(ncand, 1) * 12));
+    const size_t osz = moe::prefetch_order_scratch(L, E);
+    if (h->oscr.n < osz) {
+      CK(h->oscr.ensure(osz));
+      CK(cudaMemsetAsync(h->oscr.p, 0, osz, st));
+    }
     CK(moe::launch_prefetch_order(agg, L, E, current_layer, filter,
                                   h->keys.as<unsigned long long>(), dn,
-                                  h->cand.as<moe_candidate>(), h->n_sm, st));
+                                  h->cand.as<moe_candidate>(), h->n_sm, st, h->oscr.p));
   } else {
     CK(cudaMemsetAsync(h->small.p, 0, 8, st));  // no probe: nothing to width-check
   }
@@ -1365,6 +1464,14 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
     CK(moe::launch_decide(agg, L, E, current_layer, filter, 0, req, dslots, n_slots, nullptr,
                           nullptr, victim ? dv : nullptr, dpri, st));
   CK(cudaMemcpyAsync(h->pin.p, h->small.p, 256, cudaMemcpyDeviceToHost, st));
+  // speculative copy of the head of the order with the status words: one
+  // round trip for the usual (floor-filtered, short) answer
+  const uint64_t head = prefetch_live && out ? std::min<uint64_t>({cap, ncand, 1024}) : 0;
+  if (head) {
+    CK(h->cpin.ensure(head * sizeof(moe_candidate)));
+    CK(cudaMemcpyAsync(h->cpin.p, h->cand.p, head * sizeof(moe_candidate), cudaMemcpyDeviceToHost,
+                       st));
+  }
   CK(cudaStreamSynchronize(st));
   if (prefetch_live) {
     bool ok = false;
@@ -1376,9 +1483,13 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
   const uint32_t n = h->pin.as<uint32_t>()[12];
   const long long v = *reinterpret_cast<const long long*>(h->pin.as<uint8_t>() + 192);
   if (n_out) *n_out = prefetch_live ? n : 0;
-  if (prefetch_live && n && out && cap)
-    CK(cudaMemcpy(out, h->cand.p, std::min<uint64_t>(n, cap) * sizeof(moe_candidate),
-                  cudaMemcpyDeviceToHost));
+  if (prefetch_live && n && out && cap) {
+    const uint64_t want = std::min<uint64_t>(n, cap);
+    std::memcpy(out, h->cpin.p, std::min(want, head) * sizeof(moe_candidate));
+    if (want > head)
+      CK(cudaMemcpy(out + head, h->cand.as<moe_candidate>() + head,
+                    (want - head) * sizeof(moe_candidate), cudaMemcpyDeviceToHost));
+  }
   if (victim) *victim = v;
   if (slot_pri && n_slots) CK(cudaMemcpy(slot_pri, dpri, n_slots * 8, cudaMemcpyDeviceToHost));
   return MOE_OK;

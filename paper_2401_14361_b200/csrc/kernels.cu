@@ -664,29 +664,38 @@ __global__ void __launch_bounds__(256)
 // lane, and the zero-row mask / width flag stored directly (no pre-zeroing
 // launches).  Same outputs as k_prep<1> with cb = 1.
 template <int WPL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
     k_prep_u8(const uint8_t* src, uint64_t n, uint32_t E, uint32_t L, uint32_t RB, uint8_t* dst,
               float* ia, double* sq, float* ibT, uint64_t ib_cap, uint64_t ib_base, __half* nrm,
-              uint32_t Kp, uint64_t* zmask, uint8_t* wide) {
-  const uint64_t it = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31;
-  if (it >= n) return;
+              uint32_t Kp, uint64_t* zmask, uint8_t* wide, uint32_t wpe) {
+  // wpe warps per EAM (1 for large batches; up to 16 for a handful of probes,
+  // where one warp walking all L rows would be a long latency chain); the
+  // EAMs of a block never straddle blocks (wpe divides 16).
+  __shared__ unsigned long long zsh[16];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t it = gw / wpe;
+  const uint32_t sub = (uint32_t)(gw - it * wpe);
+  const uint32_t slot = wib / wpe;
+  if (sub == 0) zsh[slot] = 0;
+  __syncthreads();
+  const bool live = it < n;
   const uint32_t ew = E >> 2, nwords = RB >> 2;
   const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src) + it * L * ew;
   uint32_t* d32 = reinterpret_cast<uint32_t*>(dst) + it * L * nwords;
   uint64_t zbits = 0;
-  for (uint32_t l0 = 0; l0 < L; l0 += 8) {
+  for (uint32_t l0 = sub; live && l0 < L; l0 += 8 * wpe) {
     uint32_t wv[8][WPL];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
       for (int k = 0; k < WPL; ++k) {
-        const uint32_t w = lane + 32 * k, l = l0 + r;
+        const uint32_t w = lane + 32 * k, l = l0 + r * wpe;
         wv[r][k] = (l < L && w < ew) ? __ldg(s32 + (uint64_t)l * ew + w) : 0u;
       }
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const uint32_t l = l0 + r;
+      const uint32_t l = l0 + r * wpe;
       if (l >= L) break;
       uint32_t ss = 0;
 #pragma unroll
@@ -726,12 +735,15 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+  if (live && lane == 0 && zbits) atomicOr(&zsh[slot], (unsigned long long)zbits);
+  __syncthreads();
+  if (!live || sub != 0) return;
   if (nrm) {
     __half* orow = nrm + it * (uint64_t)Kp;
     for (uint32_t k = L * E + lane; k < Kp; k += 32) orow[k] = __float2half_rn(0.f);
   }
   if (lane == 0) {
-    if (zmask) zmask[it] = zbits;
+    if (zmask) zmask[it] = zsh[slot];
     if (wide) wide[it] = 0;
   }
 }
@@ -834,6 +846,238 @@ __global__ void __launch_bounds__(256)
     for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(ra[c], __ldg(&rb[c]), acc);
     r[p * L + l] = row_sim_exact((uint64_t)acc, sqa[l], sqb[p * L + l]);
   }
+}
+
+// Decision-path distances of ONE probe to every entry (the window pass of
+// match_within / prefetch_priorities, eam.cpp:131-150), warp per entry.
+// The per-entry layer sum S is carried over from the previous call through
+// pref[p] for rows [0, j0) (the caller guarantees the probe's rows [0, j0)
+// equal those of the probe that produced pref, and that the collection did
+// not change), so only rows j0..L-1 are evaluated: the probe rows listed in
+// nz (its nonzero rows >= j0) by exact integer dots + the fp64 row
+// similarity, the others from the entry's zero-row flag alone (sqb == 0:
+// both zero -> 1, else 0; eam.cpp:82-83).  S is then summed in layer order
+// (eam.cpp:95-98) and stored at row `keep` for the next call.  Block min ->
+// atomicMin(*dmin) on the distance bits.
+constexpr uint32_t kDecWarps = 4;
+constexpr uint32_t kDecParts = 256;  // per-warp partial-dot scratch (u32 or u64 entries)
+
+template <int CB>
+__global__ void __launch_bounds__(kDecWarps * 32)
+    k_dec_dist(const uint8_t* counts, const double* sqb, const uint64_t* zm, uint32_t size,
+               uint32_t L, uint32_t C, uint32_t RB, const uint8_t* probe, const double* sqa,
+               const uint16_t* nz, uint32_t n_nz, uint32_t j0, uint32_t hi, uint32_t keep,
+               double* pref, double* dist, unsigned long long* dmin,
+               unsigned long long* zero_agg, uint32_t n_agg, uint32_t* zero_cnt) {
+  // Rows [j0, hi] are evaluated explicitly (hi >= every nonzero probe row and
+  // >= keep when keep < L); rows above hi have zero probe rows, so each adds
+  // 1.0 if the entry row is zero and 0.0 otherwise -- adding 0.0 leaves the
+  // sum unchanged, so with the entry's zero-row mask (zm, L <= 64) the tail
+  // is one in-order "+1.0" per zero row instead of a walk over every row.
+  using Acc = typename Dot<CB>::Acc;
+  __shared__ Acc part[kDecWarps][kDecParts];
+  __shared__ double rbuf[kDecWarps][256];
+  __shared__ unsigned long long bmin[kDecWarps];
+  const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t p = blockIdx.x * kDecWarps + wib;
+  // the follow-up kernels' accumulators (members count, u64 aggregate)
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_agg; i += gridDim.x * blockDim.x)
+    zero_agg[i] = 0ull;
+  if (zero_cnt && blockIdx.x == 0 && threadIdx.x == 0) *zero_cnt = 0;
+  double d = __longlong_as_double(0x7ff0000000000000ll);
+  if (p < size) {
+    const uint64_t LR = (uint64_t)L * RB;
+    const uint4* eb = reinterpret_cast<const uint4*>(counts + p * LR);
+    const uint4* pb = reinterpret_cast<const uint4*>(probe);
+    const double* sb = sqb + (uint64_t)p * L;
+    const uint64_t zv = zm ? zm[p] : 0ull;
+    const double s0 = j0 ? pref[p] : 0.0;
+    for (uint32_t l = j0 + lane; l <= hi && l < L; l += 32)
+      rbuf[wib][l] = (zm ? ((zv >> l) & 1ull) != 0 : sb[l] == 0.0) ? 1.0 : 0.0;
+    const uint32_t rows_per = max(1u, kDecParts / C);
+    for (uint32_t r0 = 0; r0 < n_nz; r0 += rows_per) {
+      const uint32_t nr = min(rows_per, n_nz - r0);
+      const uint32_t items = nr * C;
+      __syncwarp();
+#pragma unroll 4
+      for (uint32_t it = lane; it < items; it += 32) {
+        const uint32_t ri = it / C, c = it - ri * C;
+        const uint32_t l = nz[r0 + ri];
+        const uint32_t off = l * (RB / 16) + c;
+        part[wib][it] = Dot<CB>::chunk(__ldg(pb + off), __ldg(eb + off), (Acc)0);
+      }
+      __syncwarp();
+      for (uint32_t ri = lane; ri < nr; ri += 32) {
+        const uint32_t l = nz[r0 + ri];
+        uint64_t dot = 0;
+        for (uint32_t c = 0; c < C; ++c) dot += (uint64_t)part[wib][ri * C + c];
+        rbuf[wib][l] = row_sim_exact(dot, sqa[l], sb[l]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double sm = s0;
+      for (uint32_t l = j0; l <= hi && l < L; ++l) {
+        sm = __dadd_rn(sm, rbuf[wib][l]);
+        if (l == keep) pref[p] = sm;
+      }
+      if (zm) {
+        uint64_t bits = hi + 1 < 64 ? zv & ~((2ull << hi) - 1ull) : 0ull;
+        if (L < 64) bits &= (1ull << L) - 1ull;
+        for (; bits; bits &= bits - 1) sm = __dadd_rn(sm, 1.0);
+      } else {
+        for (uint32_t l = hi + 1; l < L; ++l)
+          if (sb[l] == 0.0) sm = __dadd_rn(sm, 1.0);
+      }
+      d = finish_distance(sm, L);
+      dist[p] = d;
+    }
+  }
+  if (lane == 0) bmin[wib] = (unsigned long long)__double_as_longlong(d);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long b = bmin[0];
+    for (uint32_t w = 1; w < kDecWarps; ++w) b = bmin[w] < b ? bmin[w] : b;
+    if (b != 0x7ff0000000000000ull) atomicMin(dmin, b);
+  }
+}
+
+// Priorities, floor filter and the full (priority desc, ExpertId asc) order
+// of the candidates of layers cur+1..L-1 (policy.cpp:106-124,
+// engine.cpp:663-668).  k_order (one block): per-layer row sums, priorities
+// in the reference's operation order, surviving candidates compacted to
+// (key = ~bits(priority), flat ExpertId) -- ascending (key, id) is the
+// reference order and the pairs are unique, so a candidate's output position
+// is the number of pairs below it.  Up to kRankSmall survivors are ranked in
+// the same block (every thread scans the shared-memory list; the reads are
+// broadcasts); more are ranked by k_rank over a 2-D grid of (candidate tile,
+// key tile) blocks, the last block scattering the result.
+constexpr uint32_t kRankSmall = 1024;
+
+__device__ __forceinline__ bool pair_less(unsigned long long ka, uint32_t ia,
+                                          unsigned long long kb, uint32_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+__device__ __forceinline__ moe_candidate make_cand(unsigned long long key, uint32_t id,
+                                                   uint32_t E) {
+  moe_candidate c;
+  c.layer_idx = id / E;
+  c.expert_idx = id - c.layer_idx * E;
+  c.priority = __longlong_as_double((long long)~key);
+  return c;
+}
+
+__global__ void __launch_bounds__(1024)
+    k_order(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur, int filter,
+            moe_candidate* out, uint32_t* n_out, unsigned long long* gkey, uint32_t* gid,
+            uint32_t* grank, uint32_t* big) {
+  __shared__ unsigned long long key[kRankSmall];
+  __shared__ uint32_t id[kRankSmall];
+  __shared__ unsigned long long rs[256];
+  __shared__ double px[256];
+  __shared__ uint32_t cnt;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const double kEps = 1e-4;  // policy.hpp:22
+  if (tid == 0) cnt = 0;
+  for (uint32_t l = cur + 1 + wid; l < L; l += nw) {
+    unsigned long long a = 0;
+    for (uint32_t e = lane; e < E; e += 32) a += agg[(uint64_t)l * E + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) {
+      rs[l] = a;
+      px[l] = __dsub_rn(1.0, __ddiv_rn((double)(l - cur), (double)L));  // policy.cpp:110
+    }
+  }
+  __syncthreads();
+  const uint32_t n = (L - cur - 1) * E;
+  const unsigned long long* ag = agg + (uint64_t)(cur + 1) * E;  // candidate i <-> ag[i]
+  constexpr int kPre = 16;  // all loads of a thread in flight at once (n <= 16 * 1024)
+  unsigned long long av[kPre];
+#pragma unroll
+  for (int k = 0; k < kPre; ++k) {
+    const uint32_t i = tid + k * blockDim.x;
+    av[k] = i < n ? ag[i] : 0ull;
+  }
+#pragma unroll
+  for (int u = 0; u < kPre; ++u) {
+    const uint32_t i = tid + u * blockDim.x;
+    if (i >= n) break;
+    const uint32_t li = i / E, e = i - li * E;
+    const uint32_t l = cur + 1 + li;
+    const double prox = px[l];
+    const unsigned long long a = av[u];
+    // a zero count gives priority kEps*prox, which never clears the floor
+    // kEps*prox*(1+1e-9) (rounding is monotone)
+    if (filter && a == 0) continue;
+    const double ratio = rs[l] == 0 ? 0.0 : __ddiv_rn(__ull2double_rn(a), __ull2double_rn(rs[l]));
+    const double pri = __dmul_rn(__dadd_rn(ratio, kEps), prox);
+    if (filter && pri <= __dmul_rn(__dmul_rn(kEps, prox), __dadd_rn(1.0, 1e-9))) continue;
+    const uint32_t pos = atomicAdd(&cnt, 1u);
+    const unsigned long long k = ~(unsigned long long)__double_as_longlong(pri);
+    const uint32_t flat = l * E + e;
+    if (pos < kRankSmall) {
+      key[pos] = k;
+      id[pos] = flat;
+    }
+    gkey[pos] = k;
+    gid[pos] = flat;
+    grank[pos] = 0;
+  }
+  __syncthreads();
+  const uint32_t ns = cnt;
+  if (tid == 0) {
+    *n_out = ns;
+    *big = ns > kRankSmall;
+  }
+  if (ns > kRankSmall) return;
+  if (tid < ns) {
+    const unsigned long long k = key[tid];
+    const uint32_t v = id[tid];
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < ns; ++j) r += pair_less(key[j], id[j], k, v);
+    out[r] = make_cand(k, v, E);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_rank(const unsigned long long* gkey, const uint32_t* gid, const uint32_t* n_dev,
+           const uint32_t* big, uint32_t E, uint32_t* grank, uint32_t* done,
+           moe_candidate* out) {
+  if (*big == 0) return;
+  __shared__ unsigned long long tk[1024];
+  __shared__ uint32_t ti[1024];
+  __shared__ bool last;
+  const uint32_t ns = *n_dev;
+  const uint32_t j0 = blockIdx.y * 1024;
+  const uint32_t i = blockIdx.x * 256 + threadIdx.x;
+  if (blockIdx.x * 256 < ns && j0 < ns) {
+    const uint32_t nj = min(1024u, ns - j0);
+    for (uint32_t j = threadIdx.x; j < nj; j += 256) {
+      tk[j] = gkey[j0 + j];
+      ti[j] = gid[j0 + j];
+    }
+    __syncthreads();
+    if (i < ns) {
+      const unsigned long long k = gkey[i];
+      const uint32_t v = gid[i];
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < nj; ++j) r += pair_less(tk[j], ti[j], k, v);
+      if (r) atomicAdd(&grank[i], r);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (uint32_t q = threadIdx.x; q < ns; q += 256) {
+    const uint32_t r = *reinterpret_cast<volatile const uint32_t*>(&grank[q]);
+    out[r] = make_cand(gkey[q], gid[q], E);
+  }
+  if (threadIdx.x == 0) *done = 0;
 }
 
 // In-order layer sum (eam.cpp:95-103) -> dist[p]; warp min -> atomicMin(*dmin).
@@ -1616,15 +1860,19 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
   // u8 -> u8 fast path (8-byte aligned fp16 rows need E % 4 == 0)
   if (src_bytes == 1 && cb == 1 && (E & 3) == 0 && E <= 256 &&
       (reinterpret_cast<uintptr_t>(src) & 3) == 0) {
-    const uint64_t wblocks = (n * 32 + threads - 1) / threads;
+    // warps per EAM: enough warps in flight for small batches
+    uint32_t wpe = 1;
+    while (wpe < 16 && n * wpe < 2048 && wpe * 8 < L) wpe <<= 1;
+    const uint32_t pt = 512;
+    const uint64_t wblocks = (n * wpe * 32 + pt - 1) / pt;
     if (E <= 128)
-      k_prep_u8<1><<<(unsigned)wblocks, threads, 0, st>>>(
+      k_prep_u8<1><<<(unsigned)wblocks, pt, 0, st>>>(
           static_cast<const uint8_t*>(src), n, E, L, RB, dst, ia, sq, ibT, ib_cap, ib_base, nrm,
-          Kp, zmask, wide);
+          Kp, zmask, wide, wpe);
     else
-      k_prep_u8<2><<<(unsigned)wblocks, threads, 0, st>>>(
+      k_prep_u8<2><<<(unsigned)wblocks, pt, 0, st>>>(
           static_cast<const uint8_t*>(src), n, E, L, RB, dst, ia, sq, ibT, ib_cap, ib_base, nrm,
-          Kp, zmask, wide);
+          Kp, zmask, wide, wpe);
     return cudaGetLastError();
   }
   const uint64_t rows = n * L;
@@ -1893,13 +2141,35 @@ cudaError_t launch_exact_rows(const DevColl& c, const DevProbes& pr, uint32_t q0
   return cudaGetLastError();
 }
 
+cudaError_t launch_dec_dist(const DevColl& c, const uint8_t* probe, const double* sqa,
+                            const uint16_t* nz, uint32_t n_nz, uint32_t j0, uint32_t hi,
+                            uint32_t keep, double* pref, double* dist, unsigned long long* dmin,
+                            unsigned long long* zero_agg, uint32_t n_agg, uint32_t* zero_cnt,
+                            cudaStream_t st) {
+  if (c.size == 0) return cudaSuccess;
+  if (c.L > 256) return cudaErrorInvalidValue;
+  const uint64_t* zm = c.L <= 64 ? c.zmask : nullptr;
+  const unsigned grid = (c.size + kDecWarps - 1) / kDecWarps;
+  if (c.cb == 1)
+    k_dec_dist<1><<<grid, kDecWarps * 32, 0, st>>>(c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB,
+                                                   probe, sqa, nz, n_nz, j0, hi, keep, pref, dist,
+                                                   dmin, zero_agg, n_agg, zero_cnt);
+  else
+    k_dec_dist<2><<<grid, kDecWarps * 32, 0, st>>>(c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB,
+                                                   probe, sqa, nz, n_nz, j0, hi, keep, pref, dist,
+                                                   dmin, zero_agg, n_agg, zero_cnt);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_member_agg(const DevColl& c, const double* dist,
                               const unsigned long long* dmin, double window, uint32_t cur,
                               uint32_t* mem, uint32_t* n_mem, unsigned long long* agg, int n_sm,
-                              cudaStream_t st) {
+                              cudaStream_t st, bool n_mem_zeroed) {
   if (c.size == 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(n_mem, 0, 4, st);
-  if (e != cudaSuccess) return e;
+  if (!n_mem_zeroed) {
+    cudaError_t e = cudaMemsetAsync(n_mem, 0, 4, st);
+    if (e != cudaSuccess) return e;
+  }
   k_members<<<std::min<uint32_t>((c.size + 255) / 256, (uint32_t)n_sm * 4), 256, 0, st>>>(
       dist, dmin, window, c.size, mem, n_mem);
   if (cur + 1 >= c.L) return cudaGetLastError();
@@ -1916,12 +2186,34 @@ cudaError_t launch_member_agg(const DevColl& c, const double* dist,
   return cudaGetLastError();
 }
 
+size_t prefetch_order_scratch(uint32_t L, uint32_t E) {
+  return (size_t)L * E * 16 + 64;
+}
+
 cudaError_t launch_prefetch_order(const unsigned long long* agg, uint32_t L, uint32_t E,
                                   uint32_t cur, int filter, unsigned long long* keys,
                                   uint32_t* n_dev, moe_candidate* out, int n_sm,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, void* scratch) {
+  if (cur + 1 >= L) return cudaMemsetAsync(n_dev, 0, 4, st);
+  if (L <= 256 && scratch && (uint64_t)(L - cur - 1) * E <= 16u * 1024u) {
+    // k_order (+ k_rank for long survivor lists); k_order's loads assume
+    // at most 16 candidates per thread
+    const uint32_t n = (L - cur - 1) * E;
+    uint32_t* big = static_cast<uint32_t*>(scratch);
+    uint32_t* done = big + 1;  // zeroed at allocation, reset by k_rank's last block
+    unsigned long long* gkey =
+        reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 64);
+    uint32_t* gid = reinterpret_cast<uint32_t*>(gkey + n);
+    uint32_t* grank = gid + n;
+    k_order<<<1, 1024, 0, st>>>(agg, L, E, cur, filter, out, n_dev, gkey, gid, grank, big);
+    if (n > kRankSmall) {
+      const dim3 g((n + 255) / 256, (n + 1023) / 1024);
+      k_rank<<<g, 256, 0, st>>>(gkey, gid, n_dev, big, E, grank, done, out);
+    }
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaMemsetAsync(n_dev, 0, 4, st);
-  if (e != cudaSuccess || cur + 1 >= L) return e;
+  if (e != cudaSuccess) return e;
   if (E > 4096) return cudaErrorInvalidValue;
   uint32_t np = 1;
   while (np < E) np <<= 1;

@@ -113,16 +113,25 @@ cudaError_t launch_exact_rows(const DevColl& c, const DevProbes& pr, uint32_t q0
                               int n_sm, cudaStream_t st);
 // Window members (dist <= d_min + window) -> mem list; agg[L][E] += their
 // rows > cur (u64).
+// One probe vs every entry, incremental over layers (see k_dec_dist).
+cudaError_t launch_dec_dist(const DevColl& c, const uint8_t* probe, const double* sqa,
+                            const uint16_t* nz, uint32_t n_nz, uint32_t j0, uint32_t hi,
+                            uint32_t keep, double* pref, double* dist, unsigned long long* dmin,
+                            unsigned long long* zero_agg, uint32_t n_agg, uint32_t* zero_cnt,
+                            cudaStream_t st);
 cudaError_t launch_member_agg(const DevColl& c, const double* dist,
                               const unsigned long long* dmin, double window, uint32_t cur,
                               uint32_t* mem, uint32_t* n_mem, unsigned long long* agg, int n_sm,
-                              cudaStream_t st);
+                              cudaStream_t st, bool n_mem_zeroed = false);
 // Priorities + floor filter + order of the experts in layers > cur; keys is
 // scratch of (L-cur-1)*E*12 bytes, *n_dev = number of candidates emitted.
+// scratch: prefetch_order_scratch(L, E) bytes, zeroed once at allocation
+// (null: the per-layer sort + merge-rank kernels).
+size_t prefetch_order_scratch(uint32_t L, uint32_t E);
 cudaError_t launch_prefetch_order(const unsigned long long* agg, uint32_t L, uint32_t E,
                                   uint32_t cur, int filter, unsigned long long* keys,
                                   uint32_t* n_dev, moe_candidate* out, int n_sm,
-                                  cudaStream_t st);
+                                  cudaStream_t st, void* scratch);
 
 cudaError_t launch_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out,
                          cudaStream_t st);

@@ -377,6 +377,62 @@ def test_prefetch_vs_oracle(m, orc, L, E, P, seed):
             assert np.array_equal(out["priority"], p)
 
 
+def test_prefetch_decode_sequence_incremental(m, orc):
+    """The engine's call pattern (engine.cpp:546, :587, :658-678): one decode
+    iteration calls prefetch_priorities at l = 0..L-2 with the iteration EAM
+    growing by one row; the device reuses the layer-prefix sums of the rows
+    that did not change.  Every call must equal the oracle, including after a
+    prefix break (next iteration), a repeated / earlier layer, rows beyond the
+    current layer, a collection mutation, and u16 storage."""
+    L, E, P = 9, 24, 700
+    w = Workload(L, E, 3, n_groups=10, prompt_len=3, decode_len=4, batch_size=2, seed=77)
+    ents = orc.request_eams(w, P)
+    s = m.ModelShape(L, E, 3)
+    e = m.Eamc(s, m.Phase.decode, P + 5)
+    e.build(ents)
+    seqs = list(range(P))
+
+    def check(pr, layer, flt=True, entries=None):
+        entries = ents if entries is None else entries
+        lx, ex, px = orc.prefetch(entries, np.arange(len(entries), dtype=np.uint64), pr, layer, flt)
+        out = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), e, layer, flt)
+        assert np.array_equal(out["layer_idx"], lx), layer
+        assert np.array_equal(out["expert_idx"], ex), layer
+        assert np.array_equal(out["priority"], px), layer
+
+    for it in (1, 2):
+        for layer in range(L - 1):
+            check(orc.iteration_probe(w, 500 + it, it, layer), layer)
+    pr = orc.iteration_probe(w, 600, 2, 4)
+    check(pr, 4)
+    check(pr, 4)                     # same call again
+    check(orc.iteration_probe(w, 600, 2, 6), 6)
+    check(orc.iteration_probe(w, 600, 2, 2), 2)  # earlier layer, shared prefix
+    full = orc.iteration_probe(w, 601, 2, L - 1)
+    check(full, 3)                   # rows beyond the current layer are nonzero
+    check(full, 5, flt=False)
+    # mutation: an append changes the collection -> the prefix cache is stale
+    extra = orc.request_eams(w, P + 3)[P:]
+    e.build(extra)
+    allents = np.concatenate([ents, extra])
+    check(orc.iteration_probe(w, 600, 2, 6), 6, entries=allents)
+    check(orc.iteration_probe(w, 600, 2, 7), 7, entries=allents)
+    # u16 storage (widened collection)
+    big = allents.copy()
+    big[::4] *= 300
+    e2 = m.Eamc(s, m.Phase.decode, len(big))
+    e2.build(big)
+    assert e2.count_bytes() == 2
+    for layer in (0, 1, 2, 5):
+        pr = orc.iteration_probe(w, 700, 3, layer)
+        lx, ex, px = orc.prefetch(big, np.arange(len(big), dtype=np.uint64), pr, layer, True)
+        out = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), e2, layer, True)
+        assert np.array_equal(out["expert_idx"], ex) and np.array_equal(out["priority"], px)
+    # a probe wider than the storage width takes the u64 path (widens)
+    pr = orc.iteration_probe(w, 701, 3, 3) * 400
+    check(pr, 3, entries=allents)
+
+
 def test_eviction_golden(m, golden):
     g = golden("eviction.npz")
     s = m.ModelShape(4, 8)
