@@ -181,6 +181,7 @@ struct moe_eamc {
   // the in-order layer sum of rows [0, dec_keep] for the probe rows dec_rows
   PinBuf dpin, cpin;
   DevBuf pref, oscr;
+  DevBuf rdc, rdx, rocc;  // blocked construction replay: screen matrices, slot occupants
   std::vector<uint8_t> dec_rows;
   int64_t dec_keep = -1;
   uint64_t dec_version = ~0ull;
@@ -677,11 +678,67 @@ moe_status replay_staged(moe_eamc* h, Staged& s, int64_t* evicted_slots) {
     i = n_app;
   }
   if (i == n) return MOE_OK;
-  // at-capacity replacement steps, stream-ordered on the device; a bucket
-  // overflow halts the remaining launched steps and is resolved exactly.
   const uint32_t n_rep = n - i;
   CK(h->out.ensure((size_t)n * sizeof(moe_match)));
   moe_match* vic = h->out.as<moe_match>();
+  const char* rs_env = getenv("MOE_REPLAY_STEPWISE");
+  if (c.nrm && c.Kp && moe::tc_supported(c) && c.L <= 64 && c.size <= 16384 && n_rep >= 16 &&
+      moe::replay_block_smem(c) <= 220 * 1024 && !(rs_env && rs_env[0] == '1')) {
+    // blocked replay: screen matrices on the tensor cores, the sequential
+    // decisions in one CTA per block of steps (launch_replay_block)
+    uint32_t B = 512;
+    if (const char* e = getenv("MOE_REPLAY_BLOCK")) B = std::max(16, atoi(e));
+    const uint32_t ldc = (c.size + 3) & ~3u, ldx = (B + 3) & ~3u;
+    CK(h->rdc.ensure((size_t)B * ldc * 4));
+    CK(h->rdx.ensure((size_t)B * ldx * 4));
+    if (h->rocc.n < (size_t)c.size * 4) {
+      CK(h->rocc.ensure((size_t)c.cap * 4));
+      CK(cudaMemsetAsync(h->rocc.p, 0xff, h->rocc.n, h->st));
+    }
+    const float eps2 = moe::tc_eps2(c.L, c.E, c.Kp);
+    unsigned long long* rprof = nullptr;
+    if (getenv("MOE_REPLAY_PROF")) {
+      CK(h->partials.ensure(64));
+      rprof = h->partials.as<unsigned long long>();
+      CK(cudaMemsetAsync(rprof, 0, 64, h->st));
+    }
+    MatchWork w;
+    for (uint32_t b0 = i; b0 < n; b0 += B) {
+      const uint32_t nb = std::min(B, n - b0);
+      DevProbes xb;
+      xb.Q = nb;
+      xb.nrm = s.pr.nrm + (uint64_t)b0 * c.Kp;
+      xb.zmask = s.pr.zmask + b0;
+      CK(moe::launch_tc_screen(c, xb, w, h->n_sm, h->st, h->rdc.as<float>(), ldc));
+      DevColl cx = c;
+      cx.nrm = xb.nrm;
+      cx.zmask = xb.zmask;
+      cx.size = nb;
+      cx.cap = nb;
+      CK(moe::launch_tc_screen(cx, xb, w, h->n_sm, h->st, h->rdx.as<float>(), ldx));
+      CK(moe::launch_replay_block(c, s.pr, b0, nb, h->rdc.as<float>(), ldc, h->rdx.as<float>(),
+                                  ldx, eps2, h->rocc.as<int>(), h->next_seq + (b0 - i), vic + b0,
+                                  h->st, rprof));
+    }
+    if (rprof) {  // MOE_REPLAY_PROF: phase cycles of the sequential kernel
+      unsigned long long pc[5];
+      CK(cudaMemcpy(pc, rprof, sizeof pc, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "replay phases (cycles/step): screen-min %.0f band %.0f refine %.0f (warp1 %.0f) pick %.0f\n",
+              pc[0] / (double)n_rep, pc[1] / (double)n_rep, pc[2] / (double)n_rep,
+              pc[4] / (double)n_rep, pc[3] / (double)n_rep);
+    }
+    h->next_seq += n_rep;
+    std::vector<moe_match> v(n_rep);
+    CK(cudaMemcpyAsync(v.data(), vic + i, n_rep * sizeof(moe_match), cudaMemcpyDeviceToHost,
+                       h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (evicted_slots)
+      for (uint32_t j = 0; j < n_rep; ++j)
+        evicted_slots[i + j] = (int64_t)(v[j].index - h->c.index_base);
+    return MOE_OK;
+  }
+  // stepwise: at-capacity replacement steps, stream-ordered on the device; a
+  // bucket overflow halts the remaining launched steps and is resolved exactly.
   CK(h->T.ensure(4));
   CK(h->bcnt.ensure(4));
   CK(h->bucket.ensure(kBucketCap * sizeof(uint2)));
@@ -885,6 +942,30 @@ moe_status moe_eamc_insert(moe_eamc* h, const uint64_t* counts, moe_eam_kind kin
   return MOE_OK;
 }
 
+// Upload m host u64 EAMs for staging: narrowed to the storage width on the
+// host pool into pinned memory (1-2 B per count over PCIe instead of 8),
+// or, when some count does not fit that width, as u64 (stage_entries then
+// widens the collection).  *src_bytes = the width now in h->raw.
+static moe_status upload_host_counts(moe_eamc* h, const uint64_t* src, uint64_t m,
+                                     int* src_bytes) {
+  const uint64_t cells = (uint64_t)h->c.L * h->c.E;
+  const int cb = h->c.cb;
+  CK(h->hpack.ensure(m * cells * cb));
+  const uint64_t o = moe::host::pack_counts(src, m * cells, cb, h->hpack.p);
+  if (o <= width_max(cb)) {
+    CK(h->raw.ensure(m * cells * cb));
+    CK(cudaMemcpyAsync(h->raw.p, h->hpack.p, m * cells * cb, cudaMemcpyHostToDevice, h->st));
+    // the pinned staging buffer is reused by the next chunk
+    CK(cudaStreamSynchronize(h->st));
+    *src_bytes = cb;
+    return MOE_OK;
+  }
+  CK(h->raw.ensure(m * cells * 8));
+  CK(cudaMemcpyAsync(h->raw.p, src, m * cells * 8, cudaMemcpyHostToDevice, h->st));
+  *src_bytes = 8;
+  return MOE_OK;
+}
+
 moe_status moe_eamc_build(moe_eamc* h, const uint64_t* counts, uint64_t n,
                           int64_t* evicted_slots) {
   if (!h || (!counts && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
@@ -894,10 +975,9 @@ moe_status moe_eamc_build(moe_eamc* h, const uint64_t* counts, uint64_t n,
   Staged s;
   for (uint64_t off = 0; off < n; off += chunk) {
     const uint64_t m = std::min(chunk, n - off);
-    CK(h->raw.ensure(m * cells * 8));
-    CK(cudaMemcpyAsync(h->raw.p, counts + off * cells, m * cells * 8, cudaMemcpyHostToDevice,
-                       h->st));
-    CKS(stage_entries(h, h->raw.p, 8, m, &s));
+    int sb = 8;
+    CKS(upload_host_counts(h, counts + off * cells, m, &sb));
+    CKS(stage_entries(h, h->raw.p, sb, m, &s));
     CKS(replay_staged(h, s, evicted_slots ? evicted_slots + off : nullptr));
   }
   return MOE_OK;
@@ -913,10 +993,15 @@ static moe_status append_impl(moe_eamc* h, const void* counts, int cbytes, const
   Staged s;
   for (uint64_t off = 0; off < n; off += chunk) {
     const uint64_t m = std::min(chunk, n - off);
-    CK(h->raw.ensure(m * cells * cbytes));
-    CK(cudaMemcpyAsync(h->raw.p, static_cast<const uint8_t*>(counts) + off * cells * cbytes,
-                       m * cells * cbytes, cudaMemcpyHostToDevice, h->st));
-    CKS(stage_entries(h, h->raw.p, cbytes, m, &s));
+    int sb = cbytes;
+    if (cbytes == 8) {
+      CKS(upload_host_counts(h, static_cast<const uint64_t*>(counts) + off * cells, m, &sb));
+    } else {
+      CK(h->raw.ensure(m * cells * cbytes));
+      CK(cudaMemcpyAsync(h->raw.p, static_cast<const uint8_t*>(counts) + off * cells * cbytes,
+                         m * cells * cbytes, cudaMemcpyHostToDevice, h->st));
+    }
+    CKS(stage_entries(h, h->raw.p, sb, m, &s));
     CKS(ensure_alloc(h, h->c.size + m));
     CK(moe::launch_append_staged(h->c, s.pr, 0, (uint32_t)m, h->c.size, h->st));
     CK(cudaMemcpyAsync(h->c.seq + h->c.size, seqs + off, m * 8, cudaMemcpyHostToDevice, h->st));

@@ -773,6 +773,305 @@ __global__ void k_replace(uint8_t* counts, float* ibT, double* sqb, uint64_t* se
   if (threadIdx.x == 0) seq[slot] = seq_value;
 }
 
+// Blocked construction replay (K7, Eamc::insert at capacity, eam.cpp:164-177).
+// For a block of nb incoming EAMs x_0..x_{nb-1} the screen distances to the
+// collection as it stood before the block (dc [nb][P]) and to each other
+// (dx [nb][nb]) come from one tensor-core GEMM each; this ONE-CTA kernel then
+// replays the nb sequential decisions: at step t the occupant of slot p is
+// the original entry (occ[p] < 0) or x_occ[p], with screen distance
+// dc[t][p] or dx[t][occ[p]]; every slot within the screen band
+// (<= min + eps2, the same proof as the matcher's) is re-evaluated exactly
+// in the reference operation order and the lexicographic (distance, seq)
+// minimum is the victim.  k_apply_block then writes each replaced slot's
+// final occupant into the collection.
+constexpr uint32_t kReplayThreads = 512;
+constexpr uint32_t kReplayCand = 512;  // >= kReplayThreads (the slice walk relies on it)
+
+struct ReplayArgs {
+  const uint8_t* counts;
+  const double* sqb;
+  const uint64_t* seq;
+  uint32_t P, L, C, RB;
+  uint64_t index_base;
+  const uint8_t* xp;    // [nb][L][RB] packed incoming EAMs of the block
+  const double* xsq;    // [nb][L] their row norms
+  uint32_t nb;
+  const float* dc;      // [nb][ldc]
+  const float* dx;      // [nb][ldx]
+  uint32_t ldc, ldx;
+  float eps2;
+  int* occ;             // [P], -1 = original entry (all -1 on entry and exit of a block)
+  unsigned long long* prof;  // optional [4] phase cycle totals (thread 0's view)
+  uint64_t seq0;        // seq given to step 0 of the block
+  moe_match* vic;       // [nb] victims
+};
+
+__device__ __forceinline__ float block_min_f(float v, float* sbuf) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sbuf[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < (blockDim.x >> 5) ? sbuf[lane] : __uint_as_float(0x7f800000u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sbuf[32] = v;
+  }
+  __syncthreads();
+  return sbuf[32];
+}
+
+constexpr uint32_t kReplayMaxP = 16384;  // slots held in registers / shared memory per step
+constexpr uint32_t kRW = 8;              // refine warps (each stages one candidate's rows)
+constexpr int kReplayRT = kReplayMaxP / (4 * kReplayThreads);  // float4 groups per thread
+
+template <int CB>
+__global__ void __launch_bounds__(kReplayThreads, 1) k_replay_block(const ReplayArgs a) {
+  // dynamic: occ_s [P4*4] int16 | xs [L*RB] (x_t) | es [kRW][L*RB] | esq [kRW][64] f64
+  extern __shared__ __align__(16) uint8_t rsm[];
+  int16_t* occ_s = reinterpret_cast<int16_t*>(rsm);
+  __shared__ float sbuf[33];
+  __shared__ uint32_t cand[kReplayCand];
+  __shared__ uint32_t ncand;
+  __shared__ double rbuf[kReplayThreads / 32][64];
+  __shared__ double xsq_s[64];
+  __shared__ double bd[kReplayThreads / 32];
+  __shared__ unsigned long long bs[kReplayThreads / 32];
+  __shared__ uint32_t bp[kReplayThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  const uint64_t LR = (uint64_t)a.L * a.RB;
+  const uint32_t P4 = (a.P + 3) >> 2;  // float4 groups of a dc row (ldc % 4 == 0)
+  const uint32_t LR16 = (uint32_t)(LR / 16);
+  uint4* xs = reinterpret_cast<uint4*>(rsm + (((size_t)P4 * 8 + 15) & ~(size_t)15));
+  uint4* es = xs + LR16;
+  double* esq = reinterpret_cast<double*>(es + (size_t)kRW * LR16);
+  for (uint32_t p = tid; p < ((a.P + 3) & ~3u); p += blockDim.x) occ_s[p] = -1;
+  __syncthreads();
+  unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+  for (uint32_t t = 0; t < a.nb; ++t) {
+    if (a.prof) c0 = clock64();
+    const float4* dct4 = reinterpret_cast<const float4*>(a.dc + (uint64_t)t * a.ldc);
+    const float* dxt = a.dx + (uint64_t)t * a.ldx;
+    {  // the step's incoming EAM and its row norms -> shared memory
+      const uint4* src = reinterpret_cast<const uint4*>(a.xp + (uint64_t)t * LR);
+      for (uint32_t k = tid; k < LR16; k += blockDim.x) xs[k] = src[k];
+      if (tid < a.L) xsq_s[tid] = a.xsq[(uint64_t)t * a.L + tid];
+    }
+    // pass 1: the step's screen row, all loads in flight at once, kept in
+    // registers for pass 2; slots replaced earlier in the block take their
+    // occupant's row of dx instead
+    float v[kReplayRT][4];
+#pragma unroll
+    for (int r = 0; r < kReplayRT; ++r) {
+      const uint32_t g = tid + r * kReplayThreads;
+      const float4 x = g < P4 ? __ldcs(dct4 + g) : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+      v[r][0] = x.x;
+      v[r][1] = x.y;
+      v[r][2] = x.z;
+      v[r][3] = x.w;
+    }
+    float m = __uint_as_float(0x7f800000u);
+#pragma unroll
+    for (int r = 0; r < kReplayRT; ++r) {
+      const uint32_t g = tid + r * kReplayThreads;
+      if (g >= P4) break;
+      const uint2 oc = *reinterpret_cast<const uint2*>(occ_s + 4 * g);  // 4 x int16
+      const int o4[4] = {(int)(int16_t)(oc.x & 0xffffu), (int)(int16_t)(oc.x >> 16),
+                         (int)(int16_t)(oc.y & 0xffffu), (int)(int16_t)(oc.y >> 16)};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (4 * g + j >= a.P) v[r][j] = INFINITY;
+        else if (o4[j] >= 0) v[r][j] = dxt[o4[j]];
+        m = fminf(m, v[r][j]);
+      }
+    }
+    if (tid == 0) ncand = 0;
+    const float thr = block_min_f(m, sbuf) + a.eps2;
+    if (a.prof) c1 = clock64();
+    // pass 2: candidates inside the band
+#pragma unroll
+    for (int r = 0; r < kReplayRT; ++r) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (v[r][j] <= thr) {
+          const uint32_t pos = atomicAdd(&ncand, 1u);
+          if (pos < kReplayCand) cand[pos] = 4 * (tid + r * kReplayThreads) + j;
+        }
+    }
+    __syncthreads();
+    if (a.prof) c2 = clock64();
+    const uint32_t nc = ncand;
+    double best_d = __longlong_as_double(0x7ff0000000000000ll);
+    unsigned long long best_s = ~0ull;
+    uint32_t best_p = 0xffffffffu;
+    const double* sqt = xsq_s;
+    // exact re-evaluation, one candidate per refine warp: the candidate's
+    // rows and row norms are first copied to shared memory with every load
+    // of the warp in flight (one memory round trip), then each row's dot is
+    // taken over C lanes (consecutive chunks) and reduced by shuffles when C
+    // is a power of two, or by one lane per layer otherwise.
+    const bool seg = (a.C & (a.C - 1)) == 0 && a.C <= 32;
+    const uint32_t lpi = seg ? 32 / a.C : 0;  // layers per warp iteration
+    auto refine = [&](uint32_t n_list) {
+      if (w >= kRW) return;
+      uint4* er = es + (size_t)w * LR16;
+      double* eq = esq + (size_t)w * 64;
+      const uint8_t* xb = reinterpret_cast<const uint8_t*>(xs);
+      for (uint32_t ci = w; ci < n_list; ci += kRW) {
+        const uint32_t p = cand[ci];
+        const int o = occ_s[p];
+        const unsigned long long sq = o < 0 ? a.seq[p] : a.seq0 + (uint64_t)o;  // early
+        const uint4* eg = reinterpret_cast<const uint4*>(o < 0 ? a.counts + (uint64_t)p * LR
+                                                                : a.xp + (uint64_t)o * LR);
+        const double* sg = o < 0 ? a.sqb + (uint64_t)p * a.L : a.xsq + (uint64_t)o * a.L;
+        // all loads first (up to 8 per lane in flight), then the stores
+        for (uint32_t k0 = 0; k0 < LR16; k0 += 8 * 32) {
+          uint4 tmp[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t k = k0 + u * 32 + lane;
+            if (k < LR16) tmp[u] = __ldg(eg + k);
+          }
+          const double q0 = lane < a.L && k0 == 0 ? sg[lane] : 0.0;
+          const double q1 = lane + 32 < a.L && k0 == 0 ? sg[lane + 32] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t k = k0 + u * 32 + lane;
+            if (k < LR16) er[k] = tmp[u];
+          }
+          if (k0 == 0) {
+            if (lane < a.L) eq[lane] = q0;
+            if (lane + 32 < a.L) eq[lane + 32] = q1;
+          }
+        }
+        __syncwarp();
+        const uint8_t* ebb = reinterpret_cast<const uint8_t*>(er);
+        if (seg) {
+          const uint32_t c = lane & (a.C - 1);
+          for (uint32_t l0 = 0; l0 < a.L; l0 += lpi) {
+            const uint32_t l = l0 + lane / a.C;
+            typename Dot<CB>::Acc acc = 0;
+            if (l < a.L)
+              acc = Dot<CB>::chunk(reinterpret_cast<const uint4*>(xb + (uint64_t)l * a.RB)[c],
+                                   reinterpret_cast<const uint4*>(ebb + (uint64_t)l * a.RB)[c], acc);
+            for (uint32_t off = 1; off < a.C; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (c == 0 && l < a.L) rbuf[w][l] = __longlong_as_double((long long)(uint64_t)acc);
+          }
+          __syncwarp();
+          // the fp64 row similarities of all layers in parallel (one ddiv latency)
+          for (uint32_t l = lane; l < a.L; l += 32)
+            rbuf[w][l] = row_sim_exact((uint64_t)__double_as_longlong(rbuf[w][l]), sqt[l], eq[l]);
+        } else {
+          for (uint32_t l = lane; l < a.L; l += 32) {
+            const uint4* ra = reinterpret_cast<const uint4*>(xb + (uint64_t)l * a.RB);
+            const uint4* rb = reinterpret_cast<const uint4*>(ebb + (uint64_t)l * a.RB);
+            typename Dot<CB>::Acc acc = 0;
+            for (uint32_t cc = 0; cc < a.C; ++cc) acc = Dot<CB>::chunk(ra[cc], rb[cc], acc);
+            rbuf[w][l] = row_sim_exact((uint64_t)acc, sqt[l], eq[l]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          double sm = 0.0;
+          for (uint32_t l = 0; l < a.L; ++l) sm = __dadd_rn(sm, rbuf[w][l]);
+          const double d = finish_distance(sm, a.L);
+          if (better(d, sq, best_d, best_s)) {
+            best_d = d;
+            best_s = sq;
+            best_p = p;
+          }
+        }
+        __syncwarp();
+      }
+    };
+    if (nc <= kReplayCand) {
+      refine(nc);
+    } else {
+      // mass near-ties: walk the band in slot order, one slice of
+      // kReplayThreads slots at a time (each slice has at most kReplayCand members)
+      for (uint32_t r0 = 0; r0 < a.P; r0 += blockDim.x) {
+        __syncthreads();
+        if (tid == 0) ncand = 0;
+        __syncthreads();
+        const uint32_t p = r0 + tid;
+        if (p < a.P) {
+          const int o = occ_s[p];
+          if ((o < 0 ? a.dc[(uint64_t)t * a.ldc + p] : dxt[o]) <= thr)
+            cand[atomicAdd(&ncand, 1u)] = p;
+        }
+        __syncthreads();
+        refine(ncand);
+      }
+    }
+    if (a.prof) {
+      c3 = clock64();
+      acc0 += c1 - c0;
+      acc1 += c2 - c1;
+      acc2 += c3 - c2;
+    }
+    if (lane == 0) {
+      bd[w] = best_d;
+      bs[w] = best_s;
+      bp[w] = best_p;
+    }
+    __syncthreads();
+    if (w == 0) {  // lexicographic (distance, seq) minimum over the warps
+      Best b{__longlong_as_double(0x7ff0000000000000ll), ~0ull, 0xffffffffull};
+      if (lane < nw) b = Best{bd[lane], bs[lane], bp[lane]};
+      b = warp_best(b);
+      if (lane == 0) {
+        const uint32_t pp = (uint32_t)b.idx;
+        a.vic[t] = moe_match{pp + a.index_base, b.seq, b.d};
+        a.occ[pp] = (int)t;
+        occ_s[pp] = (int16_t)t;
+      }
+    }
+    __syncthreads();
+    if (a.prof) acc3 += clock64() - c3;
+  }
+  if (a.prof && tid == 0) {
+    atomicAdd(a.prof + 0, acc0);
+    atomicAdd(a.prof + 1, acc1);
+    atomicAdd(a.prof + 2, acc2);
+    atomicAdd(a.prof + 3, acc3);
+  }
+  if (a.prof && tid == 32) atomicAdd(a.prof + 4, acc2);  // a refine warp's view
+}
+
+// Final occupants of the slots replaced in a block -> the collection (the
+// data k_replace writes for a single step); resets occ for the next block.
+__global__ void k_apply_block(uint8_t* counts, float* ibT, double* sqb, uint64_t* seq,
+                              uint64_t cap, uint32_t L, uint32_t RB, const uint8_t* sp,
+                              const float* sia, const double* ssq, const moe_match* vic,
+                              int* occ, uint64_t seq0, uint64_t index_base, __half* nrm,
+                              const __half* snrm, uint32_t Kp, uint64_t* zmask,
+                              const uint64_t* szmask) {
+  const uint32_t t = blockIdx.x;
+  const uint64_t slot = vic[t].index - index_base;
+  if (occ[slot] != (int)t) return;  // a later step of the block replaced it again
+  __syncthreads();
+  if (nrm) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(snrm + (uint64_t)t * Kp);
+    uint4* d4 = reinterpret_cast<uint4*>(nrm + slot * Kp);
+    for (uint32_t o = threadIdx.x; o < Kp / 8; o += blockDim.x) d4[o] = s4[o];
+    if (threadIdx.x == 0) zmask[slot] = szmask[t];
+  }
+  const uint64_t LR = (uint64_t)L * RB;
+  const uint4* src = reinterpret_cast<const uint4*>(sp + (uint64_t)t * LR);
+  uint4* dst = reinterpret_cast<uint4*>(counts + slot * LR);
+  for (uint32_t o = threadIdx.x; o < LR / 16; o += blockDim.x) dst[o] = src[o];
+  for (uint32_t l = threadIdx.x; l < L; l += blockDim.x) {
+    ibT[(uint64_t)l * cap + slot] = sia[(uint64_t)t * L + l];
+    sqb[slot * L + l] = ssq[(uint64_t)t * L + l];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    seq[slot] = seq0 + t;
+    occ[slot] = -1;
+  }
+}
+
 __global__ void k_append_staged(uint8_t* counts, float* ibT, double* sqb, uint64_t cap, uint32_t L,
                                 uint32_t RB, const uint8_t* sp, const float* sia,
                                 const double* ssq, uint32_t first, uint32_t n, uint64_t base,
@@ -1997,6 +2296,66 @@ cudaError_t launch_replace(const DevColl& c, const DevProbes& staged, uint32_t i
   k_replace<<<1, 256, 0, st>>>(c.counts, c.ibT, c.sqb, c.seq, c.cap, c.L, c.RB, staged.packed,
                                staged.ia, staged.sqa, i, victim, c.size, seq_value, halt,
                                c.index_base, c.nrm, staged.nrm, c.Kp, c.zmask, staged.zmask);
+  return cudaGetLastError();
+}
+
+size_t replay_block_smem(const DevColl& c) {
+  const size_t P4 = (c.size + 3) / 4;
+  const size_t LR = (size_t)c.L * c.RB;
+  return ((P4 * 8 + 15) & ~(size_t)15) + LR + kRW * LR + kRW * 64 * 8;
+}
+
+cudaError_t launch_replay_block(const DevColl& c, const DevProbes& staged, uint32_t first,
+                                uint32_t nb, const float* dc, uint32_t ldc, const float* dx,
+                                uint32_t ldx, float eps2, int* occ, uint64_t seq0,
+                                moe_match* vic, cudaStream_t st, unsigned long long* prof) {
+  if (nb == 0) return cudaSuccess;
+  if (c.L > 64 || c.size > kReplayMaxP || nb > 32767 || (ldc & 3)) return cudaErrorInvalidValue;
+  ReplayArgs a;
+  a.counts = c.counts;
+  a.sqb = c.sqb;
+  a.seq = c.seq;
+  a.P = c.size;
+  a.L = c.L;
+  a.C = c.C;
+  a.RB = c.RB;
+  a.index_base = c.index_base;
+  const uint64_t LR = (uint64_t)c.L * c.RB;
+  a.xp = staged.packed + (uint64_t)first * LR;
+  a.xsq = staged.sqa + (uint64_t)first * c.L;
+  a.nb = nb;
+  a.dc = dc;
+  a.dx = dx;
+  a.ldc = ldc;
+  a.ldx = ldx;
+  a.eps2 = eps2;
+  a.occ = occ;
+  a.seq0 = seq0;
+  a.vic = vic;
+  a.prof = prof;
+  const size_t smem = replay_block_smem(c);
+  if (smem > 220 * 1024) return cudaErrorInvalidValue;
+  static size_t set = 0;
+  if (smem > set) {
+    cudaError_t e1 = cudaFuncSetAttribute(k_replay_block<1>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e1 == cudaSuccess)
+      e1 = cudaFuncSetAttribute(k_replay_block<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
+    if (e1 != cudaSuccess) return e1;
+    set = smem;
+  }
+  if (c.cb == 1)
+    k_replay_block<1><<<1, kReplayThreads, smem, st>>>(a);
+  else
+    k_replay_block<2><<<1, kReplayThreads, smem, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_apply_block<<<nb, 256, 0, st>>>(c.counts, c.ibT, c.sqb, c.seq, c.cap, c.L, c.RB,
+                                    a.xp, staged.ia + (uint64_t)first * c.L, a.xsq, vic, occ,
+                                    seq0, c.index_base, c.nrm,
+                                    staged.nrm ? staged.nrm + (uint64_t)first * c.Kp : nullptr,
+                                    c.Kp, c.zmask, staged.zmask ? staged.zmask + first : nullptr);
   return cudaGetLastError();
 }
 

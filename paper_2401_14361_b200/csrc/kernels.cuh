@@ -81,8 +81,20 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
 // Tensor-core (tcgen05 kind::f16) screen pass for large probe batches.
 float tc_eps2(uint32_t L, uint32_t E, uint32_t Kp);
 bool tc_supported(const DevColl& c);
+// dmat != null: matrix mode, every screen distance -> dmat[q * ldd + p]
+// (no threshold / buckets; ldd a multiple of 4).
 cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchWork& w, int n_sm,
-                             cudaStream_t st);
+                             cudaStream_t st, float* dmat = nullptr, uint32_t ldd = 0);
+// Blocked construction replay of staged entries [first, first+nb): screen
+// matrices dc [nb][c.size] and dx [nb][nb] -> victims vic[nb] (slot +
+// index_base, evicted seq, exact distance), collection updated; occ[c.size]
+// must be all -1 (it is again on return).
+size_t replay_block_smem(const DevColl& c);  // must be <= 220 KB for the blocked replay
+cudaError_t launch_replay_block(const DevColl& c, const DevProbes& staged, uint32_t first,
+                                uint32_t nb, const float* dc, uint32_t ldc, const float* dx,
+                                uint32_t ldx, float eps2, int* occ, uint64_t seq0,
+                                moe_match* vic, cudaStream_t st,
+                                unsigned long long* prof = nullptr);
 // Exact-integer tensor-core (tcgen05 kind::i8) screen for small probe batches
 // (u8 collections, L <= 32); blockdiag is scratch of i8_blockdiag_bytes().
 bool i8_supported(const DevColl& c);

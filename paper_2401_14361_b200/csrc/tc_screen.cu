@@ -56,6 +56,8 @@ struct TcArgs {
   uint32_t* bcnt;
   uint2* bucket;
   uint32_t bcap;
+  float* dmat;    // matrix mode: every screen distance -> dmat[q * ldd + p]
+  uint32_t ldd;
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
@@ -137,6 +139,31 @@ __device__ __forceinline__ void epilogue_half(uint32_t tcol, uint32_t col0, uint
                                               uint32_t p0, const TcArgs& a, float invL) {
   uint32_t r[32];
   const bool full_tile = p0 + col0 + 128 <= a.P;
+  if (a.dmat) {  // matrix mode (blocked construction replay): store, no threshold
+#pragma unroll 1
+    for (uint32_t c = 0; c < 4; ++c) {
+      tmem_ld32(tcol + c * 32, r);
+      if (!qvalid) continue;
+      float* o = a.dmat + (uint64_t)q * a.ldd + p0 + col0 + c * 32;
+      float dv[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t col = col0 + c * 32 + j;
+        const float sim = __uint_as_float(r[j]) + (float)__popcll(zq & zt[col]);
+        dv[j] = fmaxf(fmaf(-sim, invL, 1.0f), 0.0f);
+      }
+      if (full_tile) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(o + j) = make_float4(dv[j], dv[j + 1], dv[j + 2], dv[j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (p0 + col0 + c * 32 + j < a.P) o[j] = dv[j];
+      }
+    }
+    return;
+  }
   float rmin = __uint_as_float(kFInf);
 #pragma unroll 1
   for (uint32_t c = 0; c < 4; ++c) {
@@ -519,7 +546,7 @@ float tc_eps2(uint32_t L, uint32_t E, uint32_t Kp) {
 bool tc_supported(const DevColl& c) { return c.L <= 64 && c.nrm != nullptr && c.Kp > 0; }
 
 cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchWork& w, int n_sm,
-                             cudaStream_t st) {
+                             cudaStream_t st, float* dmat, uint32_t ldd) {
   if (c.size == 0 || pr.Q == 0) return cudaSuccess;
   // tensor maps are re-encoded only when the operand buffers change
   struct MapCache {
@@ -562,6 +589,8 @@ cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchW
   a.bcnt = w.bcnt;
   a.bucket = w.bucket;
   a.bcap = w.bcap;
+  a.dmat = dmat;
+  a.ldd = ldd;
   const char* e2 = getenv("MOE_TC2");
   const bool pair = (e2 ? e2[0] != '0' : true) && pr.Q > 128;
   if (pair) {  // 2-CTA pairs: 256-row M tiles, half the B tile per CTA

@@ -285,6 +285,46 @@ def test_build_with_duplicates(m, orc):
     assert np.array_equal(slots, want)
 
 
+@pytest.mark.parametrize("block", [None, "16", "37"])
+def test_blocked_replay_edge_cases(m, orc, monkeypatch, block):
+    """Blocked construction replay (screen matrices + one-CTA sequential
+    decisions): re-replacement of a slot inside one block, steps that pick
+    an entry inserted earlier in the same block, block boundaries, u16
+    storage, and a band wider than the candidate list (> 1024 tied slots)."""
+    if block:
+        monkeypatch.setenv("MOE_REPLAY_BLOCK", block)
+    base = m.gen_bench_family(23, 6, 32, 40)
+    # repeated incoming EAMs: the same slot is replaced again and again
+    eams = np.concatenate([base[:30], np.repeat(base[30:32], 25, axis=0), base[32:], base[:8]])
+    for cap in (30, 31):
+        e = m.Eamc(m.ModelShape(6, 32), m.Phase.decode, cap)
+        slots = e.build(eams)
+        ent, sq, want = orc.insert_replay(6, 32, cap, eams)
+        assert np.array_equal(slots, want)
+        for i in range(cap):
+            assert e.entry_seq(i) == sq[i]
+            assert np.array_equal(e.entry(i).counts, ent[i])
+    wide = m.gen_bench_family(24, 5, 40, 300).copy()
+    wide[::3] *= 500  # 2-byte storage
+    e = m.Eamc(m.ModelShape(5, 40), m.Phase.decode, 90)
+    slots = e.build(wide)
+    assert e.count_bytes() == 2
+    _, _, want = orc.insert_replay(5, 40, 90, wide)
+    assert np.array_equal(slots, want)
+
+
+def test_blocked_replay_mass_ties(m, orc):
+    """1,100 identical entries: every incoming EAM's screen band holds more
+    slots than the one-CTA candidate list; the slot-order walk resolves the
+    (distance, seq) minimum exactly."""
+    base = m.gen_bench_family(25, 3, 16, 4)
+    eams = np.concatenate([np.repeat(base[:1], 1100, axis=0), base[1:3], np.repeat(base[:1], 20, axis=0)])
+    e = m.Eamc(m.ModelShape(3, 16), m.Phase.decode, 1100)
+    slots = e.build(eams)
+    _, _, want = orc.insert_replay(3, 16, 1100, eams)
+    assert np.array_equal(slots, want)
+
+
 def test_snapshot_round_trip(m, tmp_path):
     s = m.ModelShape(3, 6, 1)
     empty = m.Eamc(s, m.Phase.prefill, 5)
