@@ -42,8 +42,10 @@ typedef enum moe_status {
   MOE_ERR_CUDA = 5,             /* no usable sm_100 device / kernel failure */
   MOE_ERR_NCCL = 6,
   MOE_ERR_OOM = 7,
-  MOE_ERR_OVERFLOW = 8 /* a count outside the range where the reference's fp64
+  MOE_ERR_OVERFLOW = 8, /* a count outside the range where the reference's fp64
                           arithmetic is exact (row sum of squares >= 2^53) */
+  MOE_ERR_TRACE = 9     /* TraceIngestError (workload.hpp:55-59): a bad trace line;
+                           moe_last_error() holds the reference's "line N: ..." text */
 } moe_status;
 
 /* ModelShape (model.hpp:19-29) */
@@ -197,6 +199,18 @@ moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_b
 moe_status moe_eam_trace_device(const moe_shape* shape, const void* topk_idx, int idx_bytes,
                                 uint64_t n_tokens, const uint64_t* offsets, uint64_t n_requests,
                                 uint32_t* counts_u32, int* bad_index_flag, void* stream);
+
+/* ---- trace ingest: ingest_traces (workload.cpp:209-232) + validate_trace
+ * (model.cpp:32-71) + request_level_eam (moesim_main.cpp:192-201) ---- */
+/* Request-level EAMs of one phase from a JSONL trace file (model.hpp:103-114):
+ * prefill = iteration 0, decode = iterations 1.. (requests with < 2
+ * iterations skipped, moesim_main.cpp:212-214).  Writes up to cap EAMs
+ * [n][L][E] u64 (counts may be NULL with cap 0); *n_eams = total. */
+moe_status moe_traces_request_eams(const char* path, const moe_shape* shape, moe_phase phase,
+                                   uint64_t* counts, uint64_t cap, uint64_t* n_eams);
+/* `moesim eamc save` (moesim_main.cpp:203-221) minus the file write: the
+ * request EAMs of the collection's phase inserted in file order (K7). */
+moe_status moe_eamc_build_from_traces(moe_eamc* h, const char* path, uint64_t* n_inserted);
 
 /* eamc_capacity_bound (eam.cpp:258-268) */
 moe_status moe_eamc_capacity_bound(const moe_shape* shape, double similarity, uint64_t* out);

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -291,6 +292,61 @@ uint32_t ref_generate_trace_counts(uint32_t L, uint32_t E, uint32_t top_k, uint3
     std::copy(c.begin(), c.end(), iter_counts + it * cells);
   }
   return static_cast<uint32_t>(t.iterations.size());
+}
+
+// The reference's own JSONL writer over its own corpus generator
+// (workload.cpp generate_corpus, model.cpp write_traces_jsonl): trace fixtures.
+int ref_write_corpus_jsonl(const char* path, uint32_t L, uint32_t E, uint32_t top_k,
+                           uint32_t n_groups, double fidelity, double skew, uint32_t prompt_len,
+                           uint32_t decode_len, uint32_t batch, uint64_t seed, uint64_t n) {
+  try {
+    WorkloadSpec w;
+    w.shape = ModelShape{L, E, top_k};
+    w.n_groups = n_groups;
+    w.group_fidelity = fidelity;
+    w.reuse_skew = skew;
+    w.prompt_len = DiscreteDist::constant(prompt_len);
+    w.decode_len = DiscreteDist::constant(decode_len);
+    w.batch_size = batch;
+    w.seed = seed;
+    const auto traces = generate_corpus(w, n);
+    write_traces_jsonl(path, traces);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// `moesim eamc save` (tools/moesim_main.cpp:203-221) on the reference
+// library: ingest_traces (validated), request_level_eam (restated verbatim
+// from moesim_main.cpp:192-201, which lives in that file's anonymous
+// namespace), Eamc::insert in file order, Eamc::save.  Returns 0, or 9 with
+// the TraceIngestError text in err.
+int ref_eamc_save_from_traces(const char* trace_path, uint32_t L, uint32_t E, uint32_t top_k,
+                              int phase, uint64_t capacity, const char* out_path, char* err,
+                              uint64_t err_len) {
+  try {
+    const ModelShape shape{L, E, top_k};
+    const Phase ph = phase == 0 ? Phase::prefill : Phase::decode;
+    const auto traces = ingest_traces(trace_path, shape);
+    Eamc eamc(shape, ph, capacity);
+    for (const auto& trace : traces) {
+      if (ph == Phase::decode && trace.iterations.size() < 2) continue;
+      Eam eam(shape, EamKind::request, ph);
+      const std::size_t begin = ph == Phase::prefill ? 0 : 1;
+      const std::size_t end = ph == Phase::prefill ? 1 : trace.iterations.size();
+      for (std::size_t it = begin; it < end && it < trace.iterations.size(); ++it)
+        for (const RoutingEvent& ev : trace.iterations[it]) eam.record(ev);
+      eamc.insert(std::move(eam));
+    }
+    eamc.save(out_path);
+    return 0;
+  } catch (const TraceIngestError& e) {
+    std::snprintf(err, err_len, "%s", e.what());
+    return 9;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
 }
 
 }  // extern "C"

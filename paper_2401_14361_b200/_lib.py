@@ -31,6 +31,7 @@ MOE_ERR_CUDA = 5
 MOE_ERR_NCCL = 6
 MOE_ERR_OOM = 7
 MOE_ERR_OVERFLOW = 8
+MOE_ERR_TRACE = 9
 
 NONE = 0xFFFFFFFFFFFFFFFF
 
@@ -101,6 +102,8 @@ _sig("moe_cache_priority", C.c_int, P(moe_shape), vp, C.c_uint32, C.c_uint32, P(
 _sig("moe_select_eviction_victim", C.c_int, P(moe_shape), vp, vp, u64, P(C.c_int64))
 _sig("moe_eam_trace", C.c_int, P(moe_shape), vp, C.c_int, u64, vp, u64, vp)
 _sig("moe_eam_trace_device", C.c_int, P(moe_shape), vp, C.c_int, u64, vp, u64, vp, vp, vp)
+_sig("moe_traces_request_eams", C.c_int, C.c_char_p, P(moe_shape), C.c_int, vp, u64, P(u64))
+_sig("moe_eamc_build_from_traces", C.c_int, vp, C.c_char_p, P(u64))
 _sig("moe_eamc_capacity_bound", C.c_int, P(moe_shape), C.c_double, P(u64))
 _sig("moe_eamc_save", C.c_int, vp, C.c_char_p)
 _sig("moe_eamc_load", C.c_int, C.c_char_p, P(moe_shape), C.c_int, P(vp))
@@ -116,7 +119,8 @@ EXPORTS = [
     "moe_eam_distance",
     "moe_prefetch_priorities", "moe_decide", "moe_cache_priority",
     "moe_select_eviction_victim", "moe_eam_trace", "moe_eam_trace_device",
-    "moe_eamc_capacity_bound", "moe_eamc_save", "moe_eamc_load", "moe_gen_bench_family",
+    "moe_eamc_capacity_bound", "moe_traces_request_eams", "moe_eamc_build_from_traces",
+    "moe_eamc_save", "moe_eamc_load", "moe_gen_bench_family",
 ]
 
 
@@ -126,6 +130,10 @@ class EamcSnapshotError(RuntimeError):
 
 class CudaError(RuntimeError):
     """MOE_ERR_CUDA / MOE_ERR_OOM / MOE_ERR_NCCL: no usable sm_100 device or a kernel failure."""
+
+
+class TraceIngestError(RuntimeError):
+    """MOE_ERR_TRACE: workload.hpp:55-59 -- a bad trace line ("line N: ...")."""
 
 
 class CountOverflowError(OverflowError):
@@ -144,6 +152,8 @@ def check(status: int) -> None:
         raise EamcSnapshotError(msg)
     if status == MOE_ERR_LOGIC:
         raise RuntimeError(msg)          # std::logic_error
+    if status == MOE_ERR_TRACE:
+        raise TraceIngestError(msg)
     if status == MOE_ERR_OVERFLOW:
         raise CountOverflowError(msg)
     raise CudaError(f"status {status}: {msg}")

@@ -1730,6 +1730,35 @@ moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_b
   return s;
 }
 
+moe_status moe_traces_request_eams(const char* path, const moe_shape* shape, moe_phase phase,
+                                   uint64_t* counts, uint64_t cap, uint64_t* n_eams) {
+  if (!path || !shape || !n_eams || (cap && !counts))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  CKS(check_shape(shape));
+  std::vector<uint64_t> c;
+  uint64_t n = 0;
+  std::string err;
+  if (!moe::host::ingest_request_eams(path, shape->n_layers, shape->n_experts_per_layer,
+                                      phase == MOE_PHASE_PREFILL ? 0 : 1, &c, &n, &err))
+    return fail(MOE_ERR_TRACE, "%s", err.c_str());
+  *n_eams = n;
+  if (cap) std::copy(c.begin(), c.begin() + std::min(n, cap) * shape->n_layers *
+                                               shape->n_experts_per_layer, counts);
+  return MOE_OK;
+}
+
+moe_status moe_eamc_build_from_traces(moe_eamc* h, const char* path, uint64_t* n_inserted) {
+  if (!h || !path) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<uint64_t> c;
+  uint64_t n = 0;
+  std::string err;
+  if (!moe::host::ingest_request_eams(path, h->c.L, h->c.E, h->phase, &c, &n, &err))
+    return fail(MOE_ERR_TRACE, "%s", err.c_str());
+  CKS(moe_eamc_build(h, c.data(), n, nullptr));
+  if (n_inserted) *n_inserted = n;
+  return MOE_OK;
+}
+
 moe_status moe_eamc_capacity_bound(const moe_shape* shape, double similarity, uint64_t* out) {
   CKS(check_shape(shape));
   if (!out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");

@@ -391,6 +391,146 @@ void bench_family(uint64_t seed, uint32_t L, uint32_t E, uint64_t skip, uint64_t
 }  // namespace host
 }  // namespace moe
 
+// ---------------------------------------------------------------- traces
+namespace moe {
+namespace host {
+namespace {
+
+// One parsed RequestTrace (model.hpp:58-66) as flat events.
+struct TraceEvent {
+  uint32_t layer;
+  std::vector<std::pair<uint64_t, uint64_t>> assign;  // (expert, tokens)
+};
+
+bool as_u64(const JVal& v, uint64_t* o) {
+  if (v.kind != JVal::Num || !v.is_uint) return false;
+  *o = v.u;
+  return true;
+}
+
+// trace_from_jsonl (model.cpp:92-121): request_id string, prompt_tokens
+// number, iterations [[[layer, [[expert, tokens], ...]], ...], ...]; unknown
+// fields ignored.  Returns "" or the structure error.
+std::string parse_trace(const JVal& j, std::string* id,
+                        std::vector<std::vector<TraceEvent>>* iters) {
+  if (j.kind != JVal::Obj) return "bad trace structure: not an object";
+  auto rid = j.obj.find("request_id");
+  auto pt = j.obj.find("prompt_tokens");
+  auto it = j.obj.find("iterations");
+  if (rid == j.obj.end() || rid->second.kind != JVal::Str)
+    return "bad trace structure: request_id";
+  uint64_t ptok = 0;
+  if (pt == j.obj.end() || !as_u64(pt->second, &ptok)) return "bad trace structure: prompt_tokens";
+  if (it == j.obj.end() || it->second.kind != JVal::Arr) return "bad trace structure: iterations";
+  *id = rid->second.s;
+  iters->clear();
+  for (const JVal& ji : it->second.arr) {
+    if (ji.kind != JVal::Arr) return "bad trace structure: iteration";
+    std::vector<TraceEvent> evs;
+    for (const JVal& je : ji.arr) {
+      if (je.kind != JVal::Arr || je.arr.size() < 2 || je.arr[1].kind != JVal::Arr)
+        return "bad trace structure: routing event";
+      uint64_t layer = 0;
+      if (!as_u64(je.arr[0], &layer) || layer > 0xffffffffull)
+        return "bad trace structure: layer";
+      TraceEvent ev;
+      ev.layer = (uint32_t)layer;
+      for (const JVal& ja : je.arr[1].arr) {
+        uint64_t ex = 0, tok = 0;
+        if (ja.kind != JVal::Arr || ja.arr.size() < 2 || !as_u64(ja.arr[0], &ex) ||
+            ex > 0xffffffffull || !as_u64(ja.arr[1], &tok))
+          return "bad trace structure: assignment";
+        ev.assign.emplace_back(ex, tok);
+      }
+      evs.push_back(std::move(ev));
+    }
+    iters->push_back(std::move(evs));
+  }
+  return "";
+}
+
+// validate_trace (model.cpp:32-71), same order and messages.
+std::string validate(const std::string& id, const std::vector<std::vector<TraceEvent>>& iters,
+                     uint32_t L, uint32_t E) {
+  std::ostringstream os;
+  if (iters.empty()) return "EmptyIterationList: request '" + id + "' has no iterations";
+  for (size_t it = 0; it < iters.size(); ++it) {
+    if (iters[it].size() != L) {
+      os << "LayerCountMismatch: iteration " << it << " has " << iters[it].size()
+         << " routing events, expected " << L;
+      return os.str();
+    }
+    for (uint32_t l = 0; l < L; ++l) {
+      const TraceEvent& ev = iters[it][l];
+      if (ev.layer != l) {
+        os << "LayerCountMismatch: iteration " << it << " position " << l << " carries layer "
+           << ev.layer;
+        return os.str();
+      }
+      for (const auto& a : ev.assign) {
+        if (a.first >= E) {
+          os << "ExpertIndexOutOfRange: iteration " << it << " layer " << l << " routes expert "
+             << a.first << " outside [0, " << E << ")";
+          return os.str();
+        }
+        if (a.second < 1) {
+          os << "InvalidTokenCount: iteration " << it << " layer " << l << " expert " << a.first
+             << " has zero token count";
+          return os.str();
+        }
+      }
+    }
+  }
+  return "";
+}
+
+}  // namespace
+
+bool ingest_request_eams(const char* path, uint32_t L, uint32_t E, int phase,
+                         std::vector<uint64_t>* counts, uint64_t* n, std::string* err) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) {
+    *err = std::string("cannot open for reading: ") + path;
+    return false;
+  }
+  counts->clear();
+  *n = 0;
+  const uint64_t cells = (uint64_t)L * E;
+  std::string line, id;
+  std::vector<std::vector<TraceEvent>> iters;
+  uint64_t line_no = 0;
+  while (std::getline(in, line)) {
+    ++line_no;
+    if (line.empty()) continue;
+    Parser ps{line.data(), line.data() + line.size(), {}};
+    JVal j;
+    ps.ws();
+    bool ok = ps.value(&j, 0);
+    ps.ws();
+    if (ok && ps.p != ps.end) ok = false;
+    std::string e = ok ? parse_trace(j, &id, &iters) : "bad JSON: " + ps.err;
+    if (e.empty()) e = validate(id, iters, L, E);
+    if (!e.empty()) {
+      *err = "line " + std::to_string(line_no) + ": " + e;
+      return false;
+    }
+    // request_level_eam (moesim_main.cpp:192-201) + the decode skip (:212-214)
+    if (phase == 1 && iters.size() < 2) continue;
+    const size_t b = phase == 0 ? 0 : 1, e_it = phase == 0 ? 1 : iters.size();
+    const size_t base = counts->size();
+    counts->resize(base + cells, 0);
+    uint64_t* c = counts->data() + base;
+    for (size_t it = b; it < e_it && it < iters.size(); ++it)
+      for (const TraceEvent& ev : iters[it])
+        for (const auto& a : ev.assign) c[(uint64_t)ev.layer * E + a.first] += a.second;
+    ++*n;
+  }
+  return true;
+}
+
+}  // namespace host
+}  // namespace moe
+
 // ---------------------------------------------------------------- host pool
 namespace moe {
 namespace host {

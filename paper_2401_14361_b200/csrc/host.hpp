@@ -33,6 +33,15 @@ void bench_family(uint64_t seed, uint32_t L, uint32_t E, uint64_t skip, uint64_t
 namespace moe {
 namespace host {
 
+// Trace ingest (workload.cpp:209-232 + model.cpp:32-71 validation) folded
+// into request-level EAM counts for one phase (moesim_main.cpp:192-201,
+// :212-216): phase 0 = prefill (iteration 0), 1 = decode (iterations 1..;
+// requests with fewer than 2 iterations are skipped, as `eamc save` does).
+// counts gets [n][L][E] u64 in file order.  On a bad line returns false
+// with the reference's TraceIngestError text ("line N: Kind: detail").
+bool ingest_request_eams(const char* path, uint32_t L, uint32_t E, int phase,
+                         std::vector<uint64_t>* counts, uint64_t* n, std::string* err);
+
 // Persistent worker pool for host-side marshalling of the host-pointer entry
 // points (the reference's API hands over u64 count matrices; narrowing them
 // to the device storage width on the host cuts the PCIe bytes 8x).  Workers

@@ -24,6 +24,7 @@ top-k ids into count matrices is `trace_requests` (GPU kernel K1).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import dataclasses
 import enum
 from typing import Iterable, List, Optional, Sequence, Tuple
@@ -32,6 +33,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import (CAND_DTYPE, MATCH_DTYPE, NONE, SLOT_DTYPE, CountOverflowError, CudaError,
+                   TraceIngestError,
                    EamcSnapshotError, check, lib, ptr)
 
 kEpsilon = 1e-4          # policy.hpp:22
@@ -261,6 +263,14 @@ class Eamc:
         check(lib.moe_eamc_build(self._h, ptr(counts), n, ptr(slots)))
         return slots[:n]
 
+    def build_from_traces(self, trace_path: str) -> int:
+        """`moesim eamc save` minus the write (moesim_main.cpp:203-221): the request
+        EAMs of this collection's phase, from a JSONL trace file, inserted in file
+        order.  Returns the number inserted; raises TraceIngestError on a bad line."""
+        n = C.c_uint64()
+        check(lib.moe_eamc_build_from_traces(self._h, os.fsencode(trace_path), C.byref(n)))
+        return n.value
+
     def append(self, counts: np.ndarray, seqs: np.ndarray) -> None:
         """Bulk load with caller-assigned seqs (snapshot / shard semantics)."""
         seqs = np.ascontiguousarray(seqs, np.uint64)
@@ -485,3 +495,25 @@ class TransferQueue:
     def __iter__(self):
         for e, p in self._order():
             yield PrefetchCandidate(e, p)
+
+
+def ingest_request_eams(trace_path: str, shape: ModelShape, phase: Phase) -> np.ndarray:
+    """ingest_traces (workload.cpp:209-232) + request_level_eam
+    (moesim_main.cpp:192-201) for one phase: [n][L][E] u64 in file order."""
+    sh = shape.c()
+    n = C.c_uint64()
+    check(lib.moe_traces_request_eams(os.fsencode(trace_path), C.byref(sh), int(phase), None, 0,
+                                      C.byref(n)))
+    out = np.zeros((max(n.value, 1), shape.n_layers, shape.n_experts_per_layer), np.uint64)
+    check(lib.moe_traces_request_eams(os.fsencode(trace_path), C.byref(sh), int(phase),
+                                      ptr(out), n.value, C.byref(n)))
+    return out[:n.value]
+
+
+def eamc_save_from_traces(trace_path: str, shape: ModelShape, phase: Phase, capacity: int,
+                          out_path: str, device: int = 0) -> "Eamc":
+    """`moesim eamc save --trace T --out O` (moesim_main.cpp:203-221)."""
+    e = Eamc(shape, phase, capacity, device=device)
+    e.build_from_traces(trace_path)
+    e.save(out_path)
+    return e

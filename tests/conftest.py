@@ -57,3 +57,10 @@ def m():
         pytest.skip("no GPU")
     import paper_2401_14361_b200 as pkg
     return pkg
+
+
+@pytest.fixture(scope="session")
+def host_pkg():
+    """The product package for host-only entry points (trace ingest): no GPU."""
+    import paper_2401_14361_b200 as pkg
+    return pkg
