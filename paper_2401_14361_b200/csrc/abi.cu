@@ -1676,6 +1676,95 @@ moe_status moe_eam_trace_device(const moe_shape* shape, const void* topk_idx, in
   return MOE_OK;
 }
 
+// Pageable host <-> device transfers through a ring of pinned staging
+// buffers: the host pool copies chunk k into its slot while the DMA of chunk
+// k-1 runs (a pageable cudaMemcpy moves ~3-5 GB/s; this runs at PCIe rate).
+struct StagingRing {
+  static constexpr int kSlots = 4;
+  static constexpr size_t kChunk = 16u << 20;
+  PinBuf slot[kSlots];
+  cudaEvent_t ev[kSlots] = {};
+  bool init = false;
+  moe_status setup() {
+    if (init) return MOE_OK;
+    for (int i = 0; i < kSlots; ++i) {
+      CK(slot[i].ensure(kChunk));
+      CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    init = true;
+    return MOE_OK;
+  }
+};
+
+struct CopyJob {
+  uint8_t* dst;
+  const uint8_t* src;
+  size_t n;
+  int parts;
+};
+
+static void copy_task(void* vj, int t) {
+  CopyJob* j = static_cast<CopyJob*>(vj);
+  const size_t a = j->n * t / j->parts, b = j->n * (t + 1) / j->parts;
+  std::memcpy(j->dst + a, j->src + a, b - a);
+}
+
+static void pool_memcpy(void* dst, const void* src, size_t n) {
+  CopyJob j{static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), n,
+            (int)std::max<size_t>(1, std::min<size_t>((size_t)moe::host::pool_threads(),
+                                                      n / (1u << 20)))};
+  moe::host::pool_run(j.parts, copy_task, &j);
+}
+
+static moe_status h2d_staged(StagingRing& r, void* dst, const void* src, size_t n,
+                             cudaStream_t st) {
+  CKS(r.setup());
+  size_t k = 0;
+  for (size_t off = 0; off < n; off += StagingRing::kChunk, ++k) {
+    const int sl = (int)(k % StagingRing::kSlots);
+    const size_t m = std::min(StagingRing::kChunk, n - off);
+    CK(cudaEventSynchronize(r.ev[sl]));  // the slot's previous DMA (this or an earlier call)
+    pool_memcpy(r.slot[sl].p, static_cast<const uint8_t*>(src) + off, m);
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, r.slot[sl].p, m, cudaMemcpyHostToDevice,
+                       st));
+    CK(cudaEventRecord(r.ev[sl], st));
+  }
+  return MOE_OK;
+}
+
+static moe_status d2h_staged(StagingRing& r, void* dst, const void* src, size_t n,
+                             cudaStream_t st) {
+  CKS(r.setup());
+  const size_t nchunks = (n + StagingRing::kChunk - 1) / StagingRing::kChunk;
+  // keep kSlots DMAs in flight; drain chunk k - kSlots + 1 once its slot is needed
+  for (size_t k = 0; k < nchunks + StagingRing::kSlots - 1; ++k) {
+    if (k < nchunks) {
+      const int sl = (int)(k % StagingRing::kSlots);
+      if (k >= StagingRing::kSlots) {  // slot busy with chunk k - kSlots: drain it first
+        const size_t kd = k - StagingRing::kSlots;
+        CK(cudaEventSynchronize(r.ev[sl]));
+        const size_t off = kd * StagingRing::kChunk;
+        pool_memcpy(static_cast<uint8_t*>(dst) + off, r.slot[sl].p,
+                    std::min(StagingRing::kChunk, n - off));
+      }
+      const size_t off = k * StagingRing::kChunk;
+      CK(cudaMemcpyAsync(r.slot[sl].p, static_cast<const uint8_t*>(src) + off,
+                         std::min(StagingRing::kChunk, n - off), cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(r.ev[sl], st));
+    }
+  }
+  // drain the last min(nchunks, kSlots) chunks
+  const size_t first = nchunks > (size_t)StagingRing::kSlots ? nchunks - StagingRing::kSlots : 0;
+  for (size_t kd = first; kd < nchunks; ++kd) {
+    const int sl = (int)(kd % StagingRing::kSlots);
+    CK(cudaEventSynchronize(r.ev[sl]));
+    const size_t off = kd * StagingRing::kChunk;
+    pool_memcpy(static_cast<uint8_t*>(dst) + off, r.slot[sl].p,
+                std::min(StagingRing::kChunk, n - off));
+  }
+  return MOE_OK;
+}
+
 moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_bytes,
                          uint64_t n_tokens, const uint64_t* offsets, uint64_t n_requests,
                          uint64_t* counts) {
@@ -1694,40 +1783,40 @@ moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_b
   CKS(device_ok(dev, &n_sm));
   const uint64_t cells = (uint64_t)shape->n_layers * shape->n_experts_per_layer;
   const uint64_t in_bytes = n_tokens * shape->n_layers * shape->top_k * idx_bytes;
-  cudaStream_t st = nullptr;
-  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  DevBuf din, doff, dscr, dcnt, dbad;
-  moe_status s = MOE_OK;
-  cudaError_t e = din.ensure(in_bytes);
-  if (e == cudaSuccess) e = doff.ensure((n_requests + 1) * 8);
-  if (e == cudaSuccess) e = dscr.ensure(n_requests * cells * 4);
-  if (e == cudaSuccess) e = dcnt.ensure(n_requests * cells * 8);
-  if (e == cudaSuccess) e = dbad.ensure(4);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(din.p, topk_idx, in_bytes, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(doff.p, offsets, (n_requests + 1) * 8, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(dcnt.p, counts, n_requests * cells * 8, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(dbad.p, 0, 4, st);
-  if (e == cudaSuccess)
-    e = moe::launch_trace(din.p, idx_bytes, n_tokens, shape->n_layers, shape->n_experts_per_layer,
-                          shape->top_k, doff.as<uint64_t>(), n_requests, dscr.as<uint32_t>(),
-                          dbad.as<int>(), n_sm, st);
-  if (e == cudaSuccess)
-    e = moe::launch_trace_commit64(dscr.as<uint32_t>(), n_requests * cells, dbad.as<int>(),
-                                   dcnt.as<unsigned long long>(), st);
-  int bad = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, dbad.p, 4, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess && !bad)
-    e = cudaMemcpy(counts, dcnt.p, n_requests * cells * 8, cudaMemcpyDeviceToHost);
-  cudaStreamDestroy(st);
-  if (e != cudaSuccess)
-    s = fail(e == cudaErrorMemoryAllocation ? MOE_ERR_OOM : MOE_ERR_CUDA, "eam_trace: %s",
-             cudaGetErrorString(e));
-  else if (bad)
-    s = fail(MOE_ERR_OUT_OF_RANGE, "Eam::record: expert index out of range");
-  return s;
+  // persistent per-device state: stream, buffers, pinned staging ring
+  struct TraceState {
+    cudaStream_t st = nullptr;
+    DevBuf din, doff, dscr, dcnt, dbad;
+    PinBuf hbad;
+    StagingRing ring;
+  };
+  static std::mutex mu;
+  static TraceState states[64];
+  std::lock_guard<std::mutex> lock(mu);
+  TraceState& S = states[dev & 63];
+  if (!S.st) CK(cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking));
+  cudaStream_t st = S.st;
+  CK(S.din.ensure(std::max<uint64_t>(in_bytes, 16)));
+  CK(S.doff.ensure((n_requests + 1) * 8));
+  CK(S.dscr.ensure(n_requests * cells * 4));
+  CK(S.dcnt.ensure(n_requests * cells * 8));
+  CK(S.dbad.ensure(4));
+  CK(S.hbad.ensure(4));
+  CKS(h2d_staged(S.ring, S.din.p, topk_idx, in_bytes, st));
+  CK(cudaMemcpyAsync(S.doff.p, offsets, (n_requests + 1) * 8, cudaMemcpyHostToDevice, st));
+  CKS(h2d_staged(S.ring, S.dcnt.p, counts, n_requests * cells * 8, st));
+  CK(cudaMemsetAsync(S.dbad.p, 0, 4, st));
+  CK(moe::launch_trace(S.din.p, idx_bytes, n_tokens, shape->n_layers,
+                       shape->n_experts_per_layer, shape->top_k, S.doff.as<uint64_t>(),
+                       n_requests, S.dscr.as<uint32_t>(), S.dbad.as<int>(), n_sm, st));
+  CK(moe::launch_trace_commit64(S.dscr.as<uint32_t>(), n_requests * cells, S.dbad.as<int>(),
+                                S.dcnt.as<unsigned long long>(), st));
+  CK(cudaMemcpyAsync(S.hbad.p, S.dbad.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (*S.hbad.as<int>())  // all-or-nothing (eam.cpp:42-47): the caller's counts untouched
+    return fail(MOE_ERR_OUT_OF_RANGE, "Eam::record: expert index out of range");
+  CKS(d2h_staged(S.ring, counts, S.dcnt.p, n_requests * cells * 8, st));
+  return MOE_OK;
 }
 
 moe_status moe_traces_request_eams(const char* path, const moe_shape* shape, moe_phase phase,
