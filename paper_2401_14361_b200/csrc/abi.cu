@@ -1080,22 +1080,30 @@ static moe_status match_host_packed(moe_eamc* h, const uint64_t* probes, uint64_
   CK(h->raw.ensure(n * row_b));
   CK(h->outall.ensure(n * sizeof(moe_match)));
   moe_match* dout = h->outall.as<moe_match>();
-  // one group measured fastest at SW (splitting the batch costs screen
-  // efficiency and per-group launches more than the overlap gains)
+  // one group measured fastest at SW (0.53 vs 0.55 ms for two: host narrowing
+  // is bound by host memory bandwidth, the GPU tail is short)
   uint64_t groups = 1;
   if (const char* e = getenv("MOE_MATCH_GROUPS")) groups = std::max(1, atoi(e));
   groups = std::min<uint64_t>(groups, n);
   const uint64_t threads = (uint64_t)moe::host::pool_threads();
-  PackJob j;
-  j.src = probes;
-  j.hp = h->hpack.as<uint8_t>();
-  j.dp = h->raw.as<uint8_t>();
-  j.cells = cells;
-  j.row_b = row_b;
-  j.cb = cb;
-  j.device = h->device;
-  j.st = h->st2;
-  for (uint64_t g = 0; g < groups; ++g) {
+  // group g is narrowed by the pool workers while this thread launches the
+  // matching of group g-1 (its DMAs were issued by the tasks themselves)
+  PackJob jobs[2];
+  for (int k = 0; k < 2; ++k) {
+    PackJob& j = jobs[k];
+    j.src = probes;
+    j.hp = h->hpack.as<uint8_t>();
+    j.dp = h->raw.as<uint8_t>();
+    j.cells = cells;
+    j.row_b = row_b;
+    j.cb = cb;
+    j.device = h->device;
+    j.st = h->st2;
+  }
+  auto submit = [&](uint64_t g) {
+    PackJob& j = jobs[g & 1];
+    j.bad.store(0);
+    j.err.store(0);
     j.g0 = n * g / groups;
     j.g1 = n * (g + 1) / groups;
     // one chunk per pool thread (>= 64 KiB of input each)
@@ -1103,19 +1111,41 @@ static moe_status match_host_packed(moe_eamc* h, const uint64_t* probes, uint64_
                                  std::max<uint64_t>(1, 8192 / cells));
     if (const char* e = getenv("MOE_PACK_CHUNK")) j.chunk = std::max(1, atoi(e));
     const int tasks = (int)((j.g1 - j.g0 + j.chunk - 1) / j.chunk);
-    moe::host::pool_run(tasks, pack_chunk_task, &j);
+    if (groups == 1) moe::host::pool_run(tasks, pack_chunk_task, &j);
+    else moe::host::pool_submit(tasks, pack_chunk_task, &j);
+  };
+  auto finish = [&](uint64_t g) -> moe_status {  // after the group's tasks are done
+    PackJob& j = jobs[g & 1];
     if (j.err.load()) return fail(MOE_ERR_CUDA, "probe upload failed");
-    if (j.bad.load()) {  // rare: widen through the u64 path
-      CK(cudaStreamSynchronize(h->st2));
-      CK(cudaStreamSynchronize(h->st));
-      return MOE_OK;
-    }
+    if (j.bad.load()) return MOE_ERR_OVERFLOW;  // sentinel for the caller below
     CK(cudaEventRecord(h->ev_copy[g & 1], h->st2));
+    return MOE_OK;
+  };
+  auto launch = [&](uint64_t g) -> moe_status {
+    PackJob& j = jobs[g & 1];
     CK(cudaStreamWaitEvent(h->st, h->ev_copy[g & 1], 0));
     DevProbes pr;
     CKS(match_all(h, j.dp + j.g0 * row_b, cb, j.g1 - j.g0, true, dout + j.g0, h->st, &pr,
                   /*async=*/true));
+    return MOE_OK;
+  };
+  moe_status fs = MOE_OK;
+  submit(0);
+  if (groups > 1) moe::host::pool_wait();
+  fs = finish(0);
+  for (uint64_t g = 1; g <= groups && fs == MOE_OK; ++g) {
+    if (g < groups) submit(g);
+    const moe_status ls = launch(g - 1);
+    if (g < groups) moe::host::pool_wait();
+    if (ls != MOE_OK) return ls;
+    if (g < groups) fs = finish(g);
   }
+  if (fs == MOE_ERR_OVERFLOW) {  // rare: widen through the u64 path
+    CK(cudaStreamSynchronize(h->st2));
+    CK(cudaStreamSynchronize(h->st));
+    return MOE_OK;
+  }
+  CKS(fs);
   CK(cudaMemcpyAsync(out, dout, n * sizeof(moe_match), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   *done = true;

@@ -555,6 +555,35 @@ class Pool {
   }
   int size() const { return n_; }
 
+  // Asynchronous job: the workers only (the caller keeps going); wait()
+  // returns when every task is done.  Jobs are serialised across callers.
+  void submit(int n, void (*fn)(void*, int), void* ctx) {
+    run_mu_.lock();
+    async_n_ = n;
+    if (n <= 0) return;
+    if (n_ == 1) {  // no workers: run inline
+      for (int i = 0; i < n; ++i) fn(ctx, i);
+      done_.store(n, std::memory_order_release);
+      return;
+    }
+    fn_ = fn;
+    ctx_ = ctx;
+    n_tasks_ = n;
+    done_.store(0, std::memory_order_relaxed);
+    next_.store(0, std::memory_order_release);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+  }
+  void wait() {
+    if (async_n_ > 0)
+      while (done_.load(std::memory_order_acquire) < async_n_) std::this_thread::yield();
+    async_n_ = 0;
+    run_mu_.unlock();
+  }
+
   void run(int n, void (*fn)(void*, int), void* ctx) {
     if (n <= 0) return;
     std::lock_guard<std::mutex> serial(run_mu_);  // one job at a time
@@ -615,6 +644,7 @@ class Pool {
   void (*fn_)(void*, int) = nullptr;
   void* ctx_ = nullptr;
   int n_tasks_ = 0;
+  int async_n_ = 0;
   std::atomic<int> next_{0}, done_{0};
 };
 
@@ -661,6 +691,10 @@ uint64_t pack_counts_serial(const uint64_t* src, uint64_t n, int cb, void* dst) 
 int pool_threads() { return pool().size(); }
 
 void pool_run(int n, void (*fn)(void*, int), void* ctx) { pool().run(n, fn, ctx); }
+
+void pool_submit(int n, void (*fn)(void*, int), void* ctx) { pool().submit(n, fn, ctx); }
+
+void pool_wait() { pool().wait(); }
 
 uint64_t pack_counts(const uint64_t* src, uint64_t n, int cb, void* dst) {
   PackCtx c{src, n, cb, 1, dst, {}};

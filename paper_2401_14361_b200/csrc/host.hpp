@@ -50,6 +50,10 @@ bool ingest_request_eams(const char* path, uint32_t L, uint32_t E, int phase,
 // overrides the size (default: hardware_concurrency, at most 64).
 int pool_threads();
 void pool_run(int n, void (*fn)(void*, int), void* ctx);
+// Asynchronous variant: fn(0..n-1) on the workers only; the caller continues
+// and must call pool_wait() before the next job (jobs are serialised).
+void pool_submit(int n, void (*fn)(void*, int), void* ctx);
+void pool_wait();
 
 // Narrow n u64 counts to cb (1 or 2) bytes, in parallel on the pool.
 // Returns the bitwise OR of all inputs: the caller's width check is
