@@ -1498,7 +1498,7 @@ static bool dec_pass(moe_eamc* h, const uint64_t* probe, uint32_t cur, cudaStrea
   if (!ck(cudaMemsetAsync(dmin, 0xff, 8, st)) ||
       !ck(moe::launch_dec_dist(c, pr->packed, pr->sqa,
                                reinterpret_cast<const uint16_t*>(h->raw.as<uint8_t>() + nz_off),
-                               n_nz, j0, hi, keep, h->pref.as<double>(), h->dist.as<double>(),
+                               nz, n_nz, j0, hi, keep, h->pref.as<double>(), h->dist.as<double>(),
                                dmin, h->agg.as<unsigned long long>(), (uint32_t)cells,
                                h->small.as<uint32_t>() + 10, st)))
     return true;

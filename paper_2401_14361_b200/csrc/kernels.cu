@@ -1241,6 +1241,63 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   }
 }
 
+// Thread-per-entry variant of k_dec_dist for the engine's common case: at
+// most a few explicit rows (the probe's new row, L <= 64, entry zero-row
+// masks available).  One thread walks rows [j0, hi] of its entry (dots only
+// for the rows in nzmask) and the zero-row tail; no shared memory, no
+// per-warp fixed cost.  Same arithmetic and order as k_dec_dist.
+template <int CB>
+__global__ void __launch_bounds__(256)
+    k_dec_dist_t(const uint8_t* counts, const double* sqb, const uint64_t* zm, uint32_t size,
+                 uint32_t L, uint32_t C, uint32_t RB, const uint8_t* probe, const double* sqa,
+                 uint64_t nzmask, uint32_t j0, uint32_t hi, uint32_t keep, double* pref,
+                 double* dist, unsigned long long* dmin, unsigned long long* zero_agg,
+                 uint32_t n_agg, uint32_t* zero_cnt) {
+  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint32_t i = gtid; i < n_agg; i += gridDim.x * blockDim.x) zero_agg[i] = 0ull;
+  if (zero_cnt && gtid == 0) *zero_cnt = 0;
+  const uint32_t p = gtid;
+  double d = __longlong_as_double(0x7ff0000000000000ll);
+  if (p < size) {
+    const uint64_t LR = (uint64_t)L * RB;
+    const uint64_t zv = zm[p];
+    double sm = j0 ? pref[p] : 0.0;
+    for (uint32_t l = j0; l <= hi && l < L; ++l) {
+      double r;
+      if ((nzmask >> l) & 1ull) {
+        const uint4* ra = reinterpret_cast<const uint4*>(probe + (uint64_t)l * RB);
+        const uint4* rb = reinterpret_cast<const uint4*>(counts + p * LR + (uint64_t)l * RB);
+        typename Dot<CB>::Acc acc = 0;
+        for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(__ldg(ra + c), __ldg(rb + c), acc);
+        r = row_sim_exact((uint64_t)acc, sqa[l], sqb[(uint64_t)p * L + l]);
+      } else {
+        r = ((zv >> l) & 1ull) ? 1.0 : 0.0;
+      }
+      sm = __dadd_rn(sm, r);
+      if (l == keep) pref[p] = sm;
+    }
+    uint64_t bits = hi + 1 < 64 ? zv & ~((2ull << hi) - 1ull) : 0ull;
+    if (L < 64) bits &= (1ull << L) - 1ull;
+    for (; bits; bits &= bits - 1) sm = __dadd_rn(sm, 1.0);
+    d = finish_distance(sm, L);
+    dist[p] = d;
+  }
+  unsigned long long b = (unsigned long long)__double_as_longlong(d);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
+    b = x < b ? x : b;
+  }
+  __shared__ unsigned long long wmin[8];
+  if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < (blockDim.x >> 5); ++w) b = wmin[w] < b ? wmin[w] : b;
+    b = wmin[0] < b ? wmin[0] : b;
+    if (b != 0x7ff0000000000000ull) atomicMin(dmin, b);
+  }
+}
+
 // Priorities, floor filter and the full (priority desc, ExpertId asc) order
 // of the candidates of layers cur+1..L-1 (policy.cpp:106-124,
 // engine.cpp:663-668).  k_order (one block): per-layer row sums, priorities
@@ -1331,13 +1388,32 @@ __global__ void __launch_bounds__(1024)
     *big = ns > kRankSmall;
   }
   if (ns > kRankSmall) return;
-  if (tid < ns) {
-    const unsigned long long k = key[tid];
-    const uint32_t v = id[tid];
-    uint32_t r = 0;
-    for (uint32_t j = 0; j < ns; ++j) r += pair_less(key[j], id[j], k, v);
-    out[r] = make_cand(k, v, E);
+  // bitonic sort of the (key, id) pairs in shared memory (np <= 1024: one
+  // compare-exchange per thread per stage)
+  uint32_t np = 1;
+  while (np < ns) np <<= 1;
+  if (tid >= ns && tid < np) {
+    key[tid] = ~0ull;
+    id[tid] = 0xffffffffu;
   }
+  __syncthreads();
+  for (uint32_t k = 2; k <= np; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t i = tid, ixj = i ^ j;
+      if (i < np && ixj > i) {
+        const bool up = (i & k) == 0;
+        const unsigned long long ki = key[i], kj = key[ixj];
+        const uint32_t vi = id[i], vj = id[ixj];
+        if (pair_less(kj, vj, ki, vi) == up) {
+          key[i] = kj;
+          key[ixj] = ki;
+          id[i] = vj;
+          id[ixj] = vi;
+        }
+      }
+      __syncthreads();
+    }
+  if (tid < ns) out[tid] = make_cand(key[tid], id[tid], E);
 }
 
 __global__ void __launch_bounds__(256)
@@ -2501,13 +2577,28 @@ cudaError_t launch_exact_rows(const DevColl& c, const DevProbes& pr, uint32_t q0
 }
 
 cudaError_t launch_dec_dist(const DevColl& c, const uint8_t* probe, const double* sqa,
-                            const uint16_t* nz, uint32_t n_nz, uint32_t j0, uint32_t hi,
+                            const uint16_t* nz, const uint16_t* nz_host, uint32_t n_nz,
+                            uint32_t j0, uint32_t hi,
                             uint32_t keep, double* pref, double* dist, unsigned long long* dmin,
                             unsigned long long* zero_agg, uint32_t n_agg, uint32_t* zero_cnt,
                             cudaStream_t st) {
   if (c.size == 0) return cudaSuccess;
   if (c.L > 256) return cudaErrorInvalidValue;
   const uint64_t* zm = c.L <= 64 ? c.zmask : nullptr;
+  if (zm && n_nz <= 4 && hi + 1 - j0 <= 8) {  // few explicit rows: thread per entry
+    uint64_t nzmask = 0;
+    for (uint32_t i = 0; i < n_nz; ++i) nzmask |= 1ull << nz_host[i];
+    const unsigned g = (c.size + 255) / 256;
+    if (c.cb == 1)
+      k_dec_dist_t<1><<<g, 256, 0, st>>>(c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB, probe, sqa,
+                                         nzmask, j0, hi, keep, pref, dist, dmin, zero_agg, n_agg,
+                                         zero_cnt);
+    else
+      k_dec_dist_t<2><<<g, 256, 0, st>>>(c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB, probe, sqa,
+                                         nzmask, j0, hi, keep, pref, dist, dmin, zero_agg, n_agg,
+                                         zero_cnt);
+    return cudaGetLastError();
+  }
   const unsigned grid = (c.size + kDecWarps - 1) / kDecWarps;
   if (c.cb == 1)
     k_dec_dist<1><<<grid, kDecWarps * 32, 0, st>>>(c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB,

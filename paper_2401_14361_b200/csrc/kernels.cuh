@@ -127,7 +127,8 @@ cudaError_t launch_exact_rows(const DevColl& c, const DevProbes& pr, uint32_t q0
 // rows > cur (u64).
 // One probe vs every entry, incremental over layers (see k_dec_dist).
 cudaError_t launch_dec_dist(const DevColl& c, const uint8_t* probe, const double* sqa,
-                            const uint16_t* nz, uint32_t n_nz, uint32_t j0, uint32_t hi,
+                            const uint16_t* nz, const uint16_t* nz_host, uint32_t n_nz,
+                            uint32_t j0, uint32_t hi,
                             uint32_t keep, double* pref, double* dist, unsigned long long* dmin,
                             unsigned long long* zero_agg, uint32_t n_agg, uint32_t* zero_cnt,
                             cudaStream_t st);
