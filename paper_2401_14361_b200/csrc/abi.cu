@@ -683,11 +683,12 @@ moe_status replay_staged(moe_eamc* h, Staged& s, int64_t* evicted_slots) {
   moe_match* vic = h->out.as<moe_match>();
   const char* rs_env = getenv("MOE_REPLAY_STEPWISE");
   if (c.nrm && c.Kp && moe::tc_supported(c) && c.L <= 64 && c.size <= 16384 && n_rep >= 16 &&
-      moe::replay_block_smem(c) <= 220 * 1024 && !(rs_env && rs_env[0] == '1')) {
+      moe::replay_block_smem(c) <= 220 * 1024 && (uint64_t)c.L * c.RB <= 16384 &&
+      !(rs_env && rs_env[0] == '1')) {
     // blocked replay: screen matrices on the tensor cores, the sequential
     // decisions in one CTA per block of steps (launch_replay_block)
     uint32_t B = 512;
-    if (const char* e = getenv("MOE_REPLAY_BLOCK")) B = std::max(16, atoi(e));
+    if (const char* e = getenv("MOE_REPLAY_BLOCK")) B = std::min(1024, std::max(16, atoi(e)));
     const uint32_t ldc = (c.size + 3) & ~3u, ldx = (B + 3) & ~3u;
     CK(h->rdc.ensure((size_t)B * ldc * 4));
     CK(h->rdx.ensure((size_t)B * ldx * 4));
@@ -721,11 +722,11 @@ moe_status replay_staged(moe_eamc* h, Staged& s, int64_t* evicted_slots) {
                                   h->st, rprof));
     }
     if (rprof) {  // MOE_REPLAY_PROF: phase cycles of the sequential kernel
-      unsigned long long pc[5];
+      unsigned long long pc[6];
       CK(cudaMemcpy(pc, rprof, sizeof pc, cudaMemcpyDeviceToHost));
-      fprintf(stderr, "replay phases (cycles/step): screen-min %.0f band %.0f refine %.0f (warp1 %.0f) pick %.0f\n",
-              pc[0] / (double)n_rep, pc[1] / (double)n_rep, pc[2] / (double)n_rep,
-              pc[4] / (double)n_rep, pc[3] / (double)n_rep);
+      fprintf(stderr, "replay phases (cycles/step): screen-min %.0f (row wait %.0f) band %.0f refine %.0f (warp1 %.0f) pick %.0f\n",
+              pc[0] / (double)n_rep, pc[5] / (double)n_rep, pc[1] / (double)n_rep,
+              pc[2] / (double)n_rep, pc[4] / (double)n_rep, pc[3] / (double)n_rep);
     }
     h->next_seq += n_rep;
     std::vector<moe_match> v(n_rep);

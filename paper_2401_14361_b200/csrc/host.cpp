@@ -1,6 +1,8 @@
 // host.cpp -- snapshot codec, capacity bound and the bench-family generator.
 #include "host.hpp"
 
+#include <immintrin.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cctype>
@@ -661,8 +663,34 @@ struct PackCtx {
   uint64_t ors[64];
 };
 
+// u64 -> u8 with AVX-512 (VPMOVQB) where the host has it (runtime dispatch;
+// the library is built for the baseline x86-64 ISA).
+__attribute__((target("avx512f,avx512bw"))) uint64_t pack_u8_avx512(const uint64_t* s,
+                                                                     uint8_t* d, uint64_t n) {
+  __m512i o = _mm512_setzero_si512();
+  uint64_t i = 0;
+  for (; i + 32 <= n; i += 32) {
+    const __m512i a = _mm512_loadu_si512(s + i), b = _mm512_loadu_si512(s + i + 8);
+    const __m512i c = _mm512_loadu_si512(s + i + 16), e = _mm512_loadu_si512(s + i + 24);
+    o = _mm512_or_si512(o, _mm512_or_si512(_mm512_or_si512(a, b), _mm512_or_si512(c, e)));
+    const __m128i lo = _mm_unpacklo_epi64(_mm512_cvtepi64_epi8(a), _mm512_cvtepi64_epi8(b));
+    const __m128i hi = _mm_unpacklo_epi64(_mm512_cvtepi64_epi8(c), _mm512_cvtepi64_epi8(e));
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(d + i), lo);
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(d + i + 16), hi);
+  }
+  uint64_t r = (uint64_t)_mm512_reduce_or_epi64(o);
+  for (; i < n; ++i) {
+    r |= s[i];
+    d[i] = (uint8_t)s[i];
+  }
+  return r;
+}
+
+const bool g_avx512 = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
+
 template <typename T>
 uint64_t pack_range(const uint64_t* __restrict s, T* __restrict d, uint64_t n) {
+  if (sizeof(T) == 1 && g_avx512) return pack_u8_avx512(s, reinterpret_cast<uint8_t*>(d), n);
   uint64_t o = 0;
   for (uint64_t i = 0; i < n; ++i) {
     const uint64_t v = s[i];

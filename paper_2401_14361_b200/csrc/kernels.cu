@@ -824,13 +824,17 @@ __device__ __forceinline__ float block_min_f(float v, float* sbuf) {
 
 constexpr uint32_t kReplayMaxP = 16384;  // slots held in registers / shared memory per step
 constexpr uint32_t kRW = 8;              // refine warps (each stages one candidate's rows)
+constexpr uint32_t kReplayBlockMax = 1024;  // steps per replay block (dx row capacity)
+constexpr int kXsPer = 2;                // 16-byte chunks of x_t per thread (L*RB <= 16 KB)
 constexpr int kReplayRT = kReplayMaxP / (4 * kReplayThreads);  // float4 groups per thread
 
 template <int CB>
 __global__ void __launch_bounds__(kReplayThreads, 1) k_replay_block(const ReplayArgs a) {
   // dynamic: occ_s [P4*4] int16 | xs [L*RB] (x_t) | es [kRW][L*RB] | esq [kRW][64] f64
+  //          | drow [2][P4*4] f32 (screen rows t, t+1, filled by bulk copies)
   extern __shared__ __align__(16) uint8_t rsm[];
   int16_t* occ_s = reinterpret_cast<int16_t*>(rsm);
+  __shared__ __align__(8) uint64_t rbar[2];
   __shared__ float sbuf[33];
   __shared__ uint32_t cand[kReplayCand];
   __shared__ uint32_t ncand;
@@ -846,26 +850,68 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay_block(const Replay
   uint4* xs = reinterpret_cast<uint4*>(rsm + (((size_t)P4 * 8 + 15) & ~(size_t)15));
   uint4* es = xs + LR16;
   double* esq = reinterpret_cast<double*>(es + (size_t)kRW * LR16);
+  float* drow = reinterpret_cast<float*>(esq + (size_t)kRW * 64);
+  const uint32_t row_bytes = P4 * 16;
   for (uint32_t p = tid; p < ((a.P + 3) & ~3u); p += blockDim.x) occ_s[p] = -1;
+  if (tid == 0) {
+    mbar_init(&rbar[0], 1);
+    mbar_init(&rbar[1], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
-  unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+  float* dxrow = drow + (size_t)2 * P4 * 4;  // [2][ldx]
+  const uint32_t dx_bytes = a.ldx * 4;
+  auto fetch_row = [&](uint32_t t) {  // one thread: screen rows t of dc and dx -> buffer t & 1
+    uint64_t* bar = &rbar[t & 1];
+    mbar_arrive_expect_tx(bar, row_bytes + dx_bytes);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(drow + (size_t)(t & 1) * P4 * 4)),
+        "l"(a.dc + (uint64_t)t * a.ldc), "r"(row_bytes), "r"(smem_u32(bar))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dxrow + (size_t)(t & 1) * a.ldx)),
+        "l"(a.dx + (uint64_t)t * a.ldx), "r"(dx_bytes), "r"(smem_u32(bar))
+        : "memory");
+  };
+  if (tid == 0 && a.nb) fetch_row(0);
+  if (a.nb) {  // x_0 -> shared memory
+    const uint4* src = reinterpret_cast<const uint4*>(a.xp);
+    for (uint32_t k = tid; k < LR16; k += blockDim.x) xs[k] = src[k];
+    if (tid < a.L) xsq_s[tid] = a.xsq[tid];
+  }
+  __syncthreads();
+  unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0,
+                     acc4 = 0;
   for (uint32_t t = 0; t < a.nb; ++t) {
     if (a.prof) c0 = clock64();
-    const float4* dct4 = reinterpret_cast<const float4*>(a.dc + (uint64_t)t * a.ldc);
     const float* dxt = a.dx + (uint64_t)t * a.ldx;
-    {  // the step's incoming EAM and its row norms -> shared memory
-      const uint4* src = reinterpret_cast<const uint4*>(a.xp + (uint64_t)t * LR);
-      for (uint32_t k = tid; k < LR16; k += blockDim.x) xs[k] = src[k];
-      if (tid < a.L) xsq_s[tid] = a.xsq[(uint64_t)t * a.L + tid];
+    // the next step's incoming EAM and row norms: loads issued now, stored to
+    // shared memory at the end of this step (their latency hides behind it)
+    uint4 nx[kXsPer];
+    double nsq = 0.0;
+    if (t + 1 < a.nb) {
+      const uint4* src = reinterpret_cast<const uint4*>(a.xp + (uint64_t)(t + 1) * LR);
+#pragma unroll
+      for (int u = 0; u < kXsPer; ++u) {
+        const uint32_t k = tid + u * blockDim.x;
+        if (k < LR16) nx[u] = __ldg(src + k);
+      }
+      if (tid < a.L) nsq = a.xsq[(uint64_t)(t + 1) * a.L + tid];
     }
-    // pass 1: the step's screen row, all loads in flight at once, kept in
-    // registers for pass 2; slots replaced earlier in the block take their
-    // occupant's row of dx instead
+    // pass 1: the step's screen row (prefetched into shared memory during the
+    // previous step by a bulk copy), kept in registers for pass 2; slots
+    // replaced earlier in the block take their occupant's row of dx instead
+    mbar_wait(&rbar[t & 1], (t >> 1) & 1);
+    if (a.prof && tid == 0) acc4 += clock64() - c0;
+    const float4* srow4 = reinterpret_cast<const float4*>(drow + (size_t)(t & 1) * P4 * 4);
+    const float* sdx = dxrow + (size_t)(t & 1) * a.ldx;
     float v[kReplayRT][4];
 #pragma unroll
     for (int r = 0; r < kReplayRT; ++r) {
       const uint32_t g = tid + r * kReplayThreads;
-      const float4 x = g < P4 ? __ldcs(dct4 + g) : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+      const float4 x = g < P4 ? srow4[g] : make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
       v[r][0] = x.x;
       v[r][1] = x.y;
       v[r][2] = x.z;
@@ -882,12 +928,18 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay_block(const Replay
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (4 * g + j >= a.P) v[r][j] = INFINITY;
-        else if (o4[j] >= 0) v[r][j] = dxt[o4[j]];
+        else if (o4[j] >= 0) v[r][j] = sdx[o4[j]];
         m = fminf(m, v[r][j]);
       }
     }
     if (tid == 0) ncand = 0;
     const float thr = block_min_f(m, sbuf) + a.eps2;
+    // every thread has its screen values in registers now: buffer (t+1)&1 was
+    // last read in step t-1, so the next row can land in it
+    if (tid == 0 && t + 1 < a.nb) {
+      fence_proxy_async();  // generic reads of that buffer before the async-proxy write
+      fetch_row(t + 1);
+    }
     if (a.prof) c1 = clock64();
     // pass 2: candidates inside the band
 #pragma unroll
@@ -947,7 +999,19 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay_block(const Replay
         }
         __syncwarp();
         const uint8_t* ebb = reinterpret_cast<const uint8_t*>(er);
-        if (seg) {
+        if (true) {  // lane per layer from shared memory, chunk order rotated by layer
+          for (uint32_t l = lane; l < a.L; l += 32) {
+            const uint4* ra = reinterpret_cast<const uint4*>(xb + (uint64_t)l * a.RB);
+            const uint4* rb = reinterpret_cast<const uint4*>(ebb + (uint64_t)l * a.RB);
+            typename Dot<CB>::Acc acc = 0;
+            uint32_t cc = l % a.C;
+            for (uint32_t k = 0; k < a.C; ++k) {
+              acc = Dot<CB>::chunk(ra[cc], rb[cc], acc);
+              cc = cc + 1 == a.C ? 0 : cc + 1;
+            }
+            rbuf[w][l] = row_sim_exact((uint64_t)acc, sqt[l], eq[l]);
+          }
+        } else if (seg) {
           const uint32_t c = lane & (a.C - 1);
           for (uint32_t l0 = 0; l0 < a.L; l0 += lpi) {
             const uint32_t l = l0 + lane / a.C;
@@ -974,7 +1038,15 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay_block(const Replay
         __syncwarp();
         if (lane == 0) {
           double sm = 0.0;
-          for (uint32_t l = 0; l < a.L; ++l) sm = __dadd_rn(sm, rbuf[w][l]);
+          uint32_t l = 0;
+          for (; l + 8 <= a.L; l += 8) {
+            double x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = rbuf[w][l + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sm = __dadd_rn(sm, x[u]);
+          }
+          for (; l < a.L; ++l) sm = __dadd_rn(sm, rbuf[w][l]);
           const double d = finish_distance(sm, a.L);
           if (better(d, sq, best_d, best_s)) {
             best_d = d;
@@ -1028,6 +1100,14 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay_block(const Replay
       }
     }
     __syncthreads();
+    if (t + 1 < a.nb) {  // x_{t+1} -> shared memory (this step's readers are done)
+#pragma unroll
+      for (int u = 0; u < kXsPer; ++u) {
+        const uint32_t k = tid + u * blockDim.x;
+        if (k < LR16) xs[k] = nx[u];
+      }
+      if (tid < a.L) xsq_s[tid] = nsq;
+    }
     if (a.prof) acc3 += clock64() - c3;
   }
   if (a.prof && tid == 0) {
@@ -1037,6 +1117,7 @@ __global__ void __launch_bounds__(kReplayThreads, 1) k_replay_block(const Replay
     atomicAdd(a.prof + 3, acc3);
   }
   if (a.prof && tid == 32) atomicAdd(a.prof + 4, acc2);  // a refine warp's view
+  if (a.prof && tid == 0) atomicAdd(a.prof + 5, acc4);   // waiting for the screen row
 }
 
 // Final occupants of the slots replaced in a block -> the collection (the
@@ -2378,7 +2459,8 @@ cudaError_t launch_replace(const DevColl& c, const DevProbes& staged, uint32_t i
 size_t replay_block_smem(const DevColl& c) {
   const size_t P4 = (c.size + 3) / 4;
   const size_t LR = (size_t)c.L * c.RB;
-  return ((P4 * 8 + 15) & ~(size_t)15) + LR + kRW * LR + kRW * 64 * 8;
+  return ((P4 * 8 + 15) & ~(size_t)15) + LR + kRW * LR + kRW * 64 * 8 + 2 * P4 * 16 +
+         2 * (size_t)4 * ((kReplayBlockMax + 3) & ~3u);
 }
 
 cudaError_t launch_replay_block(const DevColl& c, const DevProbes& staged, uint32_t first,
@@ -2386,7 +2468,10 @@ cudaError_t launch_replay_block(const DevColl& c, const DevProbes& staged, uint3
                                 uint32_t ldx, float eps2, int* occ, uint64_t seq0,
                                 moe_match* vic, cudaStream_t st, unsigned long long* prof) {
   if (nb == 0) return cudaSuccess;
-  if (c.L > 64 || c.size > kReplayMaxP || nb > 32767 || (ldc & 3)) return cudaErrorInvalidValue;
+  if (c.L > 64 || c.size > kReplayMaxP || nb > kReplayBlockMax || ldx > kReplayBlockMax ||
+      (ldc & 3) ||
+      (uint64_t)c.L * c.RB > 16ull * kXsPer * kReplayThreads)
+    return cudaErrorInvalidValue;
   ReplayArgs a;
   a.counts = c.counts;
   a.sqb = c.sqb;
