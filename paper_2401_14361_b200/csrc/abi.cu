@@ -347,7 +347,8 @@ moe_status prof_begin(moe_eamc* h) {
 // Launch the packing of n probes (device source) at the collection's current
 // width; *dmax (device) receives the largest count.  No synchronisation.
 moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t n,
-                             cudaStream_t st, DevProbes* pr) {
+                             cudaStream_t st, DevProbes* pr,
+                             moe::MatchInit init = moe::MatchInit{}) {
   DevColl& c = h->c;
   const uint64_t LR = (uint64_t)c.L * c.RB;
   CK(h->packed.ensure(n * LR + 16));
@@ -368,11 +369,10 @@ moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint6
     zq = h->zq.as<uint64_t>();
   }
   CK(h->wide.ensure(n));
-  CK(cudaMemsetAsync(dmax, 0, 8, st));
   if (h->prof) CK(cudaEventRecord(h->ev[0], st));
   CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, h->packed.as<uint8_t>(),
                       h->ia.as<float>(), h->sqa.as<double>(), nullptr, 0, 0, dmax, nrm, c.Kp, zq,
-                      h->wide.as<uint8_t>(), st));
+                      h->wide.as<uint8_t>(), st, init));
   if (h->prof) CK(cudaEventRecord(h->ev[1], st));
   pr->Q = (uint32_t)n;
   pr->packed = h->packed.as<uint8_t>();
@@ -451,13 +451,9 @@ moe_status make_plan(moe_eamc* h, int mode, uint32_t QT, Plan* p) {
   return MOE_OK;
 }
 
-// Full matching pipeline for an already-packed probe batch; `out` is a
-// device array.  Synchronizes `st` once (overflow check).
-// Screen + refine launches for packed probes (no synchronisation).
-moe_status launch_match(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaStream_t st,
-                        MatchWork* wout) {
-  const uint64_t Q = pr.Q;
-  DevColl& c = h->c;
+// Scratch of one match pipeline for Q probes (allocated before the probe prep
+// that initialises it).
+moe_status match_work(moe_eamc* h, uint64_t Q, MatchWork* wout) {
   CK(h->T.ensure(Q * 4));
   CK(h->bcnt.ensure(Q * 4));
   CK(h->bucket.ensure(Q * kBucketCap * sizeof(uint2)));
@@ -471,9 +467,26 @@ moe_status launch_match(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaSt
   w.bcap = kBucketCap;
   w.over_list = h->over_list.as<uint32_t>();
   w.over_n = h->small.as<uint32_t>() + 4;
-  CK(cudaMemsetAsync(w.T, 0x7f, Q * 4, st));  // 0x7f7f7f7f = 3.4e38f > any distance
-  CK(cudaMemsetAsync(w.bcnt, 0, Q * 4, st));
-  CK(cudaMemsetAsync(w.over_n, 0, 4, st));
+  *wout = w;
+  return MOE_OK;
+}
+
+// Screen + refine launches for packed probes (no synchronisation).  `inited`:
+// the probe prep already initialised w's threshold / bucket counters
+// (MatchInit); otherwise they are reset here.
+moe_status launch_match(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaStream_t st,
+                        MatchWork* wout, bool inited = false) {
+  const uint64_t Q = pr.Q;
+  DevColl& c = h->c;
+  MatchWork w;
+  if (inited) {
+    w = *wout;
+  } else {
+    CKS(match_work(h, Q, &w));
+    CK(cudaMemsetAsync(w.T, 0x7f, Q * 4, st));  // 0x7f7f7f7f = 3.4e38f > any distance
+    CK(cudaMemsetAsync(w.bcnt, 0, Q * 4, st));
+    CK(cudaMemsetAsync(w.over_n, 0, 4, st));
+  }
   const bool tc = pr.nrm != nullptr && moe::tc_supported(c);
   const bool i8 = !tc && pr.zmask != nullptr && use_i8(h, Q);
   w.eps2 = tc ? moe::tc_eps2(c.L, c.E, c.Kp) : moe::screen_eps2(c.L);
@@ -514,10 +527,11 @@ moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bo
   CKS(ss);
   for (;;) {
     CKS(prof_begin(h));
-    CKS(launch_probe_prep(h, dsrc, src_bytes, n, st, pr));
-    if (after_prep) CK(cudaEventRecord(after_prep, st));  // the source buffer may be reused
     MatchWork w;
-    CKS(launch_match(h, *pr, out, st, &w));
+    CKS(match_work(h, n, &w));
+    CKS(launch_probe_prep(h, dsrc, src_bytes, n, st, pr, moe::MatchInit{w.T, w.bcnt, w.over_n}));
+    if (after_prep) CK(cudaEventRecord(after_prep, st));  // the source buffer may be reused
+    CKS(launch_match(h, *pr, out, st, &w, /*inited=*/true));
     if (async) {
       if (h->c.size) {
         Plan pe;
@@ -627,8 +641,7 @@ moe_status stage_entries(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t 
     CK(s->sqa.ensure(n * c.L * 8));
     CK(h->small.ensure(256));
     CK(h->pin.ensure(256));
-    unsigned long long* dmax = h->small.as<unsigned long long>();
-    CK(cudaMemsetAsync(dmax, 0, 8, h->st));
+    unsigned long long* dmax = h->small.as<unsigned long long>();  // reset by launch_prep
     if (c.Kp) {
       CK(s->nrm.ensure(n * c.Kp * sizeof(__half)));
       CK(s->zmask.ensure(n * 8));

@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 namespace moe {
 
 constexpr int kNT = 128;          // entries per collection tile == threads per block
@@ -53,6 +56,43 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// Programmatic dependent launch.  The kernels of one match pipeline (probe
+// prep -> screen -> refine -> gated exact pass -> gated merge) are launched
+// with programmatic stream serialisation: grid n+1 is scheduled while grid n
+// drains, runs only its shared-memory / TMEM / barrier set-up, and then
+// blocks in pdl_wait() (griddepcontrol.wait returns once the preceding grid
+// has completed and its writes are visible; a no-op for a normal launch).
+// Every such kernel touches global memory only after pdl_wait().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// MOE_PDL=0 disables it (A/B measurement).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MOE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // Dot product of one 16-byte chunk of packed counts.

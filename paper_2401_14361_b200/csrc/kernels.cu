@@ -127,6 +127,8 @@ __global__ void __launch_bounds__(kNT, 1)
   Best* wbest = reinterpret_cast<Best*>(smem + lay.off_wbest);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + lay.off_bars);
 
+  pdl_wait();
+  pdl_trigger();
   uint32_t nq = MODE == 0 ? (a.Q + QT - 1) / QT : a.nq_list;
   if (MODE == 1 && a.nq_dev) {  // device-gated exact pass: no work unless buckets overflowed
     const uint32_t tot = *a.nq_dev;
@@ -408,6 +410,8 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
   const uint32_t wib = threadIdx.x >> 5;
   const uint32_t q = blockIdx.x * kRefineWarps + wib;
   const uint32_t lane = threadIdx.x & 31;
+  pdl_wait();
+  pdl_trigger();
   if (q >= r.Q) return;
   // Every load that does not depend on another is issued up front (one
   // memory round trip instead of a chain): flags, bucket count, threshold,
@@ -520,6 +524,8 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
 __global__ void k_merge_partials(const moe_match* parts, uint32_t grid, uint32_t nq,
                                  uint32_t n_pt, const uint32_t* qlist, moe_match* out,
                                  uint64_t index_base, const uint32_t* nq_dev, uint32_t q_off) {
+  pdl_wait();
+  pdl_trigger();
   if (nq_dev) {
     const uint32_t tot = *nq_dev;
     nq = tot > q_off ? min(tot - q_off, nq) : 0u;
@@ -575,17 +581,24 @@ __global__ void __launch_bounds__(256)
     k_prep(const void* src, uint64_t rows, uint32_t E, uint32_t L, uint32_t RB, int cb,
            uint8_t* dst, float* ia, double* sq, float* ibT, uint64_t ib_cap, uint64_t ib_base,
            unsigned long long* max_count, uint64_t width_limit, __half* nrm, uint32_t Kp,
-           uint64_t* zmask, uint8_t* wide) {
+           uint64_t* zmask, uint8_t* wide, MatchInit init) {
   // One warp per row (max parallelism, short latency chain).  The host only
   // needs to know whether some count exceeds the storage width, so the global
   // max is touched only by rows that actually do (no atomics in the common
   // case).  Zero rows set their bit in the (pre-zeroed) per-EAM mask; the last
   // row of an EAM also writes the operand's K padding.
+  pdl_wait();
+  pdl_trigger();
   const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  if (row == 0 && lane == 0 && init.over_n) *init.over_n = 0;
   if (row >= rows) return;
   const uint64_t it = row / L;
   const uint32_t l = (uint32_t)(row - it * L);
+  if (l == 0 && lane == 0 && init.T) {
+    init.T[it] = 0x7f7f7f7fu;  // 3.4e38f > any distance
+    init.bcnt[it] = 0;
+  }
   const uint64_t sbase = row * E;
   uint32_t* drow = reinterpret_cast<uint32_t*>(dst + row * RB);
   const uint32_t per_word = 4 / cb;
@@ -667,19 +680,30 @@ template <int WPL>
 __global__ void __launch_bounds__(512)
     k_prep_u8(const uint8_t* src, uint64_t n, uint32_t E, uint32_t L, uint32_t RB, uint8_t* dst,
               float* ia, double* sq, float* ibT, uint64_t ib_cap, uint64_t ib_base, __half* nrm,
-              uint32_t Kp, uint64_t* zmask, uint8_t* wide, uint32_t wpe) {
+              uint32_t Kp, uint64_t* zmask, uint8_t* wide, uint32_t wpe,
+              unsigned long long* max_count, MatchInit init) {
   // wpe warps per EAM (1 for large batches; up to 16 for a handful of probes,
   // where one warp walking all L rows would be a long latency chain); the
   // EAMs of a block never straddle blocks (wpe divides 16).
   __shared__ unsigned long long zsh[16];
+  pdl_wait();
+  pdl_trigger();
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t it = gw / wpe;
   const uint32_t sub = (uint32_t)(gw - it * wpe);
   const uint32_t slot = wib / wpe;
   if (sub == 0) zsh[slot] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // u8 counts always fit: nothing exceeds the width
+    if (max_count) *max_count = 0;
+    if (init.over_n) *init.over_n = 0;
+  }
   __syncthreads();
   const bool live = it < n;
+  if (live && sub == 0 && lane == 0 && init.T) {
+    init.T[it] = 0x7f7f7f7fu;
+    init.bcnt[it] = 0;
+  }
   const uint32_t ew = E >> 2, nwords = RB >> 2;
   const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src) + it * L * ew;
   uint32_t* d32 = reinterpret_cast<uint32_t*>(dst) + it * L * nwords;
@@ -2141,8 +2165,7 @@ cudaError_t launch_match_t(const CUtensorMap& map, const MatchArgs& a, const Mat
                            cudaStream_t st) {
   cudaError_t e = set_smem_attr<CB, QT, MODE>(g.smem);
   if (e != cudaSuccess) return e;
-  k_match<CB, QT, MODE><<<g.grid, kNT, g.smem, st>>>(map, a);
-  return cudaGetLastError();
+  return launch_pdl(k_match<CB, QT, MODE>, dim3(g.grid), dim3(kNT), g.smem, st, map, a);
 }
 
 template <int MODE>
@@ -2310,7 +2333,7 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
                         uint32_t RB, int cb, uint8_t* dst, float* ia, double* sq, float* ibT,
                         uint64_t ib_cap, uint64_t ib_base, unsigned long long* max_count,
                         __half* nrm, uint32_t Kp, uint64_t* zmask, uint8_t* wide,
-                        cudaStream_t st) {
+                        cudaStream_t st, MatchInit init) {
   if (n == 0) return cudaSuccess;
   const uint32_t threads = 256;
   // u8 -> u8 fast path (8-byte aligned fp16 rows need E % 4 == 0)
@@ -2321,19 +2344,17 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
     while (wpe < 16 && n * wpe < 2048 && wpe * 8 < L) wpe <<= 1;
     const uint32_t pt = 512;
     const uint64_t wblocks = (n * wpe * 32 + pt - 1) / pt;
-    if (E <= 128)
-      k_prep_u8<1><<<(unsigned)wblocks, pt, 0, st>>>(
-          static_cast<const uint8_t*>(src), n, E, L, RB, dst, ia, sq, ibT, ib_cap, ib_base, nrm,
-          Kp, zmask, wide, wpe);
-    else
-      k_prep_u8<2><<<(unsigned)wblocks, pt, 0, st>>>(
-          static_cast<const uint8_t*>(src), n, E, L, RB, dst, ia, sq, ibT, ib_cap, ib_base, nrm,
-          Kp, zmask, wide, wpe);
-    return cudaGetLastError();
+    return launch_pdl(E <= 128 ? k_prep_u8<1> : k_prep_u8<2>, dim3((unsigned)wblocks), dim3(pt),
+                      0, st, static_cast<const uint8_t*>(src), n, E, L, RB, dst, ia, sq, ibT,
+                      ib_cap, ib_base, nrm, Kp, zmask, wide, wpe, max_count, init);
   }
   const uint64_t rows = n * L;
   const uint64_t blocks = (rows * 32 + threads - 1) / threads;
   const uint64_t limit = cb == 1 ? 255ull : 65535ull;
+  if (max_count) {
+    cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+  }
   if (zmask) {
     cudaError_t e = cudaMemsetAsync(zmask, 0, n * sizeof(uint64_t), st);
     if (e != cudaSuccess) return e;
@@ -2342,18 +2363,17 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
     cudaError_t e = cudaMemsetAsync(wide, 0, n, st);
     if (e != cudaSuccess) return e;
   }
-#define MOE_PREP(S)                                                                            \
-  k_prep<S><<<(unsigned)blocks, threads, 0, st>>>(src, rows, E, L, RB, cb, dst, ia, sq, ibT,    \
-                                                  ib_cap, ib_base, max_count, limit, nrm, Kp,  \
-                                                  zmask, wide)
+#define MOE_PREP(S)                                                                          \
+  return launch_pdl(k_prep<S>, dim3((unsigned)blocks), dim3(threads), 0, st, src, rows, E, L, RB, \
+                    cb, dst, ia, sq, ibT, ib_cap, ib_base, max_count, limit, nrm, Kp, zmask,     \
+                    wide, init)
   switch (src_bytes) {
-    case 8: MOE_PREP(8); break;
-    case 2: MOE_PREP(2); break;
-    case 1: MOE_PREP(1); break;
+    case 8: MOE_PREP(8);
+    case 2: MOE_PREP(2);
+    case 1: MOE_PREP(1);
     default: return cudaErrorInvalidValue;
   }
 #undef MOE_PREP
-  return cudaGetLastError();
 }
 
 cudaError_t launch_screen(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
@@ -2396,11 +2416,8 @@ cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork
   r.halt_value = halt_value;
   r.index_base = c.index_base;
   const uint32_t blocks = (pr.Q + kRefineWarps - 1) / kRefineWarps;
-  if (c.cb == 1)
-    k_refine<1><<<blocks, kRefineWarps * 32, 0, st>>>(r);
-  else
-    k_refine<2><<<blocks, kRefineWarps * 32, 0, st>>>(r);
-  return cudaGetLastError();
+  return c.cb == 1 ? launch_pdl(k_refine<1>, dim3(blocks), dim3(kRefineWarps * 32), 0, st, r)
+                   : launch_pdl(k_refine<2>, dim3(blocks), dim3(kRefineWarps * 32), 0, st, r);
 }
 
 cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
@@ -2422,9 +2439,9 @@ cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProb
     if (e != cudaSuccess) return e;
     const uint32_t threads = 256;
     const uint32_t blocks = (uint32_t)(((uint64_t)n * 32 + threads - 1) / threads);
-    k_merge_partials<<<blocks, threads, 0, st>>>(w.partials, g.grid, n, g.n_pt, qlist + off, out,
-                                                 c.index_base, nq_dev, off);
-    e = cudaGetLastError();
+    e = launch_pdl(k_merge_partials, dim3(blocks), dim3(threads), 0, st,
+                   (const moe_match*)w.partials, (uint32_t)g.grid, n, (uint32_t)g.n_pt,
+                   qlist + off, out, (uint64_t)c.index_base, nq_dev, off);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

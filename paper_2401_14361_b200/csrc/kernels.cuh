@@ -70,13 +70,24 @@ bool plan_match(const DevColl& c, int n_sm, int mode, uint32_t QT, MatchGeom* g)
 
 cudaError_t encode_tmap(const DevColl& c, uint32_t G, CUtensorMap* map);
 
+// Matcher state that the probe-prep kernel initialises for the screen pass
+// that follows it (instead of separate memset launches): T[q] = +huge,
+// bcnt[q] = 0, *over_n = 0.  Null members are left alone.
+struct MatchInit {
+  uint32_t* T = nullptr;
+  uint32_t* bcnt = nullptr;
+  uint32_t* over_n = nullptr;
+};
+
 // u64/u16/u8 counts -> packed rows + norms.  rows = n*L.  When ibT != null
 // the row norms are written as collection metadata at slots base..base+n.
+// *max_count (if given) is reset and receives the largest count that does not
+// fit the storage width.
 cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, uint32_t E,
                         uint32_t RB, int cb, uint8_t* dst, float* ia, double* sq, float* ibT,
                         uint64_t ib_cap, uint64_t ib_base, unsigned long long* max_count,
                         __half* nrm, uint32_t Kp, uint64_t* zmask, uint8_t* wide,
-                        cudaStream_t st);
+                        cudaStream_t st, MatchInit init = MatchInit{});
 
 // Tensor-core (tcgen05 kind::f16) screen pass for large probe batches.
 float tc_eps2(uint32_t L, uint32_t E, uint32_t Kp);

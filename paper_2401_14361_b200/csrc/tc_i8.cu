@@ -173,6 +173,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // set-up above overlaps the previous grid's tail
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -306,6 +308,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 // Block-diagonal A: row (q, l) <- probe q's layer-l packed row at K offset l*RB.
 __global__ void k_blockdiag(const uint8_t* packed, uint32_t Q, uint32_t L, uint32_t RB,
                             uint32_t logR, uint32_t Kp, uint32_t rows, uint8_t* A) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t R = 1u << logR;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)rows * Kp / 16;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -350,8 +354,7 @@ cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const I8Args&
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k_tci8_screen<LOGR><<<grid, THREADS, smem, st>>>(ta, tb, a);
-  return cudaGetLastError();
+  return launch_pdl(k_tci8_screen<LOGR>, dim3(grid), dim3(THREADS), smem, st, ta, tb, a);
 }
 
 }  // namespace
@@ -377,9 +380,10 @@ cudaError_t launch_tci8_screen(const DevColl& c, const DevProbes& pr, const Matc
   const uint32_t K = c.L * c.RB;
   const uint32_t Kp = (K + BKB - 1) / BKB * BKB;
   const uint32_t rows = n_m * BM;
-  k_blockdiag<<<std::min<uint32_t>((uint32_t)((uint64_t)rows * Kp / 16 / 256) + 1, 1024), 256, 0,
-                st>>>(pr.packed, pr.Q, c.L, c.RB, logR, Kp, rows, blockdiag);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(
+      k_blockdiag, dim3(std::min<uint32_t>((uint32_t)((uint64_t)rows * Kp / 16 / 256) + 1, 1024)),
+      dim3(256), 0, st, (const uint8_t*)pr.packed, (uint32_t)pr.Q, c.L, c.RB, logR, Kp, rows,
+      blockdiag);
   if (e != cudaSuccess) return e;
   struct MapCache {
     const void* base = nullptr;

@@ -249,6 +249,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // set-up above overlaps the previous grid's tail
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -427,6 +429,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // set-up above overlaps the previous grid's tail
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -613,8 +617,7 @@ cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchW
     }
     const uint32_t tiles = a.n_m * a.n_n;
     const uint32_t clusters = std::min<uint32_t>(tiles, (uint32_t)n_sm / 2);
-    k_tc2_screen<<<clusters * 2, THREADS, smem2, st>>>(ta, cb.map, a);
-    return cudaGetLastError();
+    return launch_pdl(k_tc2_screen, dim3(clusters * 2), dim3(THREADS), smem2, st, ta, cb.map, a);
   }
   if (cb.box != BN) {
     e = encode_2d_f16(c.nrm, c.cap, c.Kp, BN, &cb.map);
@@ -630,8 +633,7 @@ cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchW
   }
   const uint32_t tiles = a.n_m * a.n_n;
   const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)n_sm);
-  k_tc_screen<<<grid, THREADS, smem, st>>>(ta, tb, a);
-  return cudaGetLastError();
+  return launch_pdl(k_tc_screen, dim3(grid), dim3(THREADS), smem, st, ta, tb, a);
 }
 
 }  // namespace moe
