@@ -483,34 +483,54 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
   const uint4* cb4 = reinterpret_cast<const uint4*>(r.counts);
   const uint64_t LC = (uint64_t)r.L * C;
   Acc* part = reinterpret_cast<Acc*>(parts[wib]);
+  const uint32_t L = r.L;
   for (uint32_t g0 = 0; g0 < nc; g0 += G) {
     const uint32_t gn = min(G, nc - g0);
-    const uint32_t pairs = gn * r.L;
+    const uint32_t pairs = gn * L;
     const uint32_t items = pairs * C;
-    // the summing lane's seq load overlaps the row loads below
-    const uint64_t my_seq = lane < gn ? r.seq[cand[wib][g0 + lane]] : 0;
+    const uint32_t* cg = cand[wib] + g0;
+    // Everything the later phases load is issued together with the row loads
+    // (one memory round trip): the summing lane's seq, and the norms of this
+    // lane's first (candidate, layer) pair.
+    const uint64_t my_seq = lane < gn ? r.seq[cg[lane]] : 0;
+    const uint32_t pci0 = lane / L, pl0 = lane - pci0 * L;
+    double sqa0 = 0.0, sqb0 = 0.0;
+    if (lane < pairs) {
+      sqa0 = sqa[pl0];
+      sqb0 = r.sqb[(uint64_t)cg[pci0] * L + pl0];
+    }
+    // (candidate, layer*C + chunk) of item `it`, advanced without divisions
+    uint32_t ci = lane / (uint32_t)LC, lc = lane - ci * (uint32_t)LC;
 #pragma unroll 4
     for (uint32_t it = lane; it < items; it += 32) {
-      const uint32_t ci = it / (uint32_t)LC;
-      const uint32_t lc = it - ci * (uint32_t)LC;  // = l * C + chunk
-      const uint32_t p = cand[wib][g0 + ci];
-      part[it] = Dot<CB>::chunk(__ldg(pa4 + lc), __ldg(cb4 + (uint64_t)p * LC + lc), (Acc)0);
+      part[it] = Dot<CB>::chunk(__ldg(pa4 + lc), __ldg(cb4 + (uint64_t)cg[ci] * LC + lc), (Acc)0);
+      lc += 32;
+      while (lc >= (uint32_t)LC) {
+        lc -= (uint32_t)LC;
+        ++ci;
+      }
     }
     __syncwarp();
+    uint32_t pci = pci0, pl = pl0;
     for (uint32_t pr = lane; pr < pairs; pr += 32) {
-      const uint32_t ci = pr / r.L, l = pr - ci * r.L;
-      const uint32_t p = cand[wib][g0 + ci];
       uint64_t dot = 0;
       for (uint32_t c = 0; c < C; ++c) dot += (uint64_t)part[pr * C + c];
-      rbuf[wib][pr] = row_sim_exact(dot, sqa[l], r.sqb[(uint64_t)p * r.L + l]);
+      const bool first = pr == lane;
+      const double sa = first ? sqa0 : sqa[pl];
+      const double sb = first ? sqb0 : r.sqb[(uint64_t)cg[pci] * L + pl];
+      rbuf[wib][pr] = row_sim_exact(dot, sa, sb);
+      pl += 32;
+      while (pl >= L) {
+        pl -= L;
+        ++pci;
+      }
     }
     __syncwarp();
     if (lane < gn) {
-      const uint32_t p = cand[wib][g0 + lane];
       double sm = 0.0;
-      for (uint32_t l = 0; l < r.L; ++l) sm = __dadd_rn(sm, rbuf[wib][lane * r.L + l]);
-      const double d = finish_distance(sm, r.L);
-      if (better(d, my_seq, b.d, b.seq)) b = Best{d, my_seq, p};
+      for (uint32_t l = 0; l < L; ++l) sm = __dadd_rn(sm, rbuf[wib][lane * L + l]);
+      const double d = finish_distance(sm, L);
+      if (better(d, my_seq, b.d, b.seq)) b = Best{d, my_seq, cg[lane]};
     }
     __syncwarp();
   }
@@ -717,28 +737,46 @@ __global__ void __launch_bounds__(512)
         const uint32_t w = lane + 32 * k, l = l0 + r * wpe;
         wv[r][k] = (l < L && w < ew) ? __ldg(s32 + (uint64_t)l * ew + w) : 0u;
       }
+    // Σc² of the 8 rows (exact integers), then the fp64 scalars of row r on
+    // lane r: one dsqrt/drcp sequence per 8 rows instead of one per row.
+    uint32_t my_ss = 0;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const uint32_t l = l0 + r * wpe;
-      if (l >= L) break;
       uint32_t ss = 0;
 #pragma unroll
       for (int k = 0; k < WPL; ++k) ss = __dp4a(wv[r][k], wv[r][k], ss);
       ss = __reduce_add_sync(0xffffffffu, ss);
-      const uint64_t row = it * L + l;
+      my_ss = (lane & 7) == (uint32_t)r ? ss : my_ss;
+    }
+    {  // zero rows of this group (lane r <-> row l0 + r * wpe)
+      uint32_t zb = __ballot_sync(0xffffffffu, lane < 8 && l0 + lane * wpe < L && my_ss == 0);
+      while (zb) {
+        const uint32_t r = __ffs(zb) - 1;
+        zb &= zb - 1;
+        zbits |= 1ull << ((l0 + r * wpe) & 63);
+      }
+    }
+    const double my_sd = __dsqrt_rn((double)my_ss);
+    const float my_inv = my_ss ? __double2float_rn(__drcp_rn(my_sd)) : 0.f;
+    {
+      const uint32_t l = l0 + lane * wpe;
+      if (lane < 8 && l < L) {
+        const uint64_t row = it * L + l;
+        sq[row] = my_sd;
+        if (ia) ia[row] = my_inv;
+        if (ibT) ibT[(uint64_t)l * ib_cap + ib_base + it] = my_inv;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint32_t l = l0 + r * wpe;
+      if (l >= L) break;
+      const float inv = __shfl_sync(0xffffffffu, my_inv, r);
 #pragma unroll
       for (int k = 0; k < WPL; ++k) {
         const uint32_t w = lane + 32 * k;
         if (w < nwords) d32[(uint64_t)l * nwords + w] = wv[r][k];
       }
-      const double sd = __dsqrt_rn((double)ss);
-      const float inv = ss ? __double2float_rn(__drcp_rn(sd)) : 0.f;
-      if (lane == 0) {
-        sq[row] = sd;
-        if (ia) ia[row] = inv;
-        if (ibT) ibT[(uint64_t)l * ib_cap + ib_base + it] = inv;
-      }
-      if (ss == 0) zbits |= 1ull << (l & 63);
       if (nrm) {
         __half* o = nrm + it * (uint64_t)Kp + (uint64_t)l * E;
 #pragma unroll
