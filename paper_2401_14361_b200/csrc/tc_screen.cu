@@ -131,9 +131,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // Epilogue of one accumulator tile for one probe row and 128 of its 256
 // columns (two warps of the same TMEM lane quarter split the columns).
-// Pass 1 (branch-free): screen distances -> row minimum -> global per-probe
-// threshold.  Pass 2 only runs when the row minimum can still produce a
-// candidate (rare once the threshold has converged) and walks a bitmask.
+// Pass 1 (branch-free): screen distances -> row minimum (and runner-up) ->
+// global per-probe threshold -> the single-candidate push.  Pass 2 re-reads
+// TMEM only for rows with several candidates in the tile.
 __device__ __forceinline__ void epilogue_half(uint32_t tcol, uint32_t col0, uint64_t zq,
                                               const uint64_t* zt, uint32_t q, bool qvalid,
                                               uint32_t p0, const TcArgs& a, float invL) {
@@ -164,34 +164,61 @@ __device__ __forceinline__ void epilogue_half(uint32_t tcol, uint32_t col0, uint
     }
     return;
   }
-  float rmin = __uint_as_float(kFInf);
+  // Pass 1 (branch-free): the row's smallest screen distance d1 (first
+  // column c1 attaining it) and the second smallest d2.  Most rows that can
+  // produce a candidate produce exactly one (d1 <= thr < d2): it is pushed
+  // straight from registers, and the TMEM re-read of pass 2 is needed only by
+  // rows with two or more candidates in this tile (incl. exact ties).
+  // (tcgen05.ld is warp-collective: the loads stay outside the per-row branch)
+  const bool fast = zq == 0 && full_tile;  // no zero rows: minimise d via max sim
+  float s1 = -__uint_as_float(kFInf), s2 = s1;
+  float d1 = __uint_as_float(kFInf), d2 = d1;
+  uint32_t c1 = 0;
 #pragma unroll 1
   for (uint32_t c = 0; c < 4; ++c) {
     tmem_ld32(tcol + c * 32, r);
-    if (zq == 0 && full_tile) {
+    if (fast) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) rmin = fminf(rmin, fmaf(-__uint_as_float(r[j]), invL, 1.0f));
+      for (int j = 0; j < 32; ++j) {
+        const float x = __uint_as_float(r[j]);
+        s2 = fmaxf(s2, fminf(s1, x));
+        c1 = x > s1 ? col0 + c * 32 + j : c1;
+        s1 = fmaxf(s1, x);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const uint32_t col = col0 + c * 32 + j;
         const float sim = __uint_as_float(r[j]) + (float)__popcll(zq & zt[col]);
-        const float d = fmaf(-sim, invL, 1.0f);
-        rmin = (p0 + col < a.P) ? fminf(rmin, d) : rmin;
+        float d = fmaf(-sim, invL, 1.0f);
+        d = (p0 + col < a.P) ? d : __uint_as_float(kFInf);
+        d2 = fminf(d2, fmaxf(d1, d));
+        c1 = d < d1 ? col : c1;
+        d1 = fminf(d1, d);
       }
     }
   }
-  rmin = fmaxf(rmin, 0.0f);
+  if (fast) {  // rounding is monotone: min_j d_j = d(max_j sim_j)
+    d1 = fmaf(-s1, invL, 1.0f);
+    d2 = fmaf(-s2, invL, 1.0f);
+  }
+  d1 = fmaxf(d1, 0.0f);
+  d2 = fmaxf(d2, 0.0f);
   float thr = -1.0f;  // invalid rows never qualify
   if (qvalid) {
-    const uint32_t mb = __float_as_uint(rmin);
+    const uint32_t mb = __float_as_uint(d1);
     uint32_t tv = *reinterpret_cast<volatile uint32_t*>(&a.T[q]);
     if (mb < tv) tv = min(atomicMin(&a.T[q], mb), mb);
     thr = __uint_as_float(tv) + a.eps2;
   }
-  // tcgen05.ld is warp-collective: the (rare) candidate pass is taken by the
-  // whole warp whenever any of its rows can still produce a candidate
-  if (!__any_sync(0xffffffffu, rmin <= thr)) return;
+  const bool multi = d2 <= thr;  // implies d1 <= thr
+  if (d1 <= thr && !multi) {
+    const uint32_t pos = atomicAdd(&a.bcnt[q], 1u);
+    if (pos < a.bcap) a.bucket[(uint64_t)q * a.bcap + pos] = make_uint2(p0 + c1, __float_as_uint(d1));
+  }
+  // tcgen05.ld is warp-collective: the (rarer) full pass is taken by the
+  // whole warp whenever any of its rows has two or more candidates
+  if (!__any_sync(0xffffffffu, multi)) return;
 #pragma unroll 1
   for (uint32_t c = 0; c < 4; ++c) {
     tmem_ld32(tcol + c * 32, r);
@@ -200,7 +227,7 @@ __device__ __forceinline__ void epilogue_half(uint32_t tcol, uint32_t col0, uint
       const uint32_t col = col0 + c * 32 + j;
       const float sim = __uint_as_float(r[j]) + (float)__popcll(zq & zt[col]);
       const float d = fmaxf(fmaf(-sim, invL, 1.0f), 0.0f);
-      if (qvalid && d <= thr && p0 + col < a.P) {
+      if (multi && d <= thr && p0 + col < a.P) {
         const uint32_t pos = atomicAdd(&a.bcnt[q], 1u);
         if (pos < a.bcap)
           a.bucket[(uint64_t)q * a.bcap + pos] = make_uint2(p0 + col, __float_as_uint(d));
