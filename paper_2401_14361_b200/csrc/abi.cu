@@ -348,9 +348,14 @@ moe_status prof_begin(moe_eamc* h) {
 // width; *dmax (device) receives the largest count.  No synchronisation.
 moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t n,
                              cudaStream_t st, DevProbes* pr,
-                             moe::MatchInit init = moe::MatchInit{}) {
+                             moe::MatchInit init = moe::MatchInit{}, bool alias_ok = false) {
   DevColl& c = h->c;
   const uint64_t LR = (uint64_t)c.L * c.RB;
+  // A u8 device source already in the storage layout (RB == E) is used as the
+  // packed probe rows directly (no copy) when the caller keeps it alive for
+  // the whole pipeline; the condition implies launch_prep's u8 fast path.
+  const bool alias = alias_ok && src_bytes == 1 && c.cb == 1 && c.RB == c.E && (c.E & 3) == 0 &&
+                     c.E <= 256 && (reinterpret_cast<uintptr_t>(dsrc) & 15) == 0;
   CK(h->packed.ensure(n * LR + 16));
   CK(h->ia.ensure(n * c.L * sizeof(float)));
   CK(h->sqa.ensure(n * c.L * sizeof(double)));
@@ -370,12 +375,13 @@ moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint6
   }
   CK(h->wide.ensure(n));
   if (h->prof) CK(cudaEventRecord(h->ev[0], st));
-  CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb, h->packed.as<uint8_t>(),
-                      h->ia.as<float>(), h->sqa.as<double>(), nullptr, 0, 0, dmax, nrm, c.Kp, zq,
+  CK(moe::launch_prep(dsrc, src_bytes, n, c.L, c.E, c.RB, c.cb,
+                      alias ? nullptr : h->packed.as<uint8_t>(), h->ia.as<float>(),
+                      h->sqa.as<double>(), nullptr, 0, 0, dmax, nrm, c.Kp, zq,
                       h->wide.as<uint8_t>(), st, init));
   if (h->prof) CK(cudaEventRecord(h->ev[1], st));
   pr->Q = (uint32_t)n;
-  pr->packed = h->packed.as<uint8_t>();
+  pr->packed = alias ? static_cast<uint8_t*>(const_cast<void*>(dsrc)) : h->packed.as<uint8_t>();
   pr->ia = h->ia.as<float>();
   pr->sqa = h->sqa.as<double>();
   pr->nrm = nrm;
@@ -529,7 +535,8 @@ moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bo
     CKS(prof_begin(h));
     MatchWork w;
     CKS(match_work(h, n, &w));
-    CKS(launch_probe_prep(h, dsrc, src_bytes, n, st, pr, moe::MatchInit{w.T, w.bcnt, w.over_n}));
+    CKS(launch_probe_prep(h, dsrc, src_bytes, n, st, pr, moe::MatchInit{w.T, w.bcnt, w.over_n},
+                          /*alias_ok=*/after_prep == nullptr));
     if (after_prep) CK(cudaEventRecord(after_prep, st));  // the source buffer may be reused
     CKS(launch_match(h, *pr, out, st, &w, /*inited=*/true));
     if (async) {

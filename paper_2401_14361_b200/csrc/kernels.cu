@@ -725,18 +725,24 @@ __global__ void __launch_bounds__(512)
     init.bcnt[it] = 0;
   }
   const uint32_t ew = E >> 2, nwords = RB >> 2;
-  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src) + it * L * ew;
-  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst) + it * L * nwords;
+  // Row pointers advance by a fixed stride per row of this warp (64-bit adds
+  // instead of per-row 64-bit multiplies).  dst == null: the caller reads
+  // the packed rows from `src` itself (u8 source already in the storage
+  // layout, RB == E), so no copy is written.
+  const uint32_t* sp = reinterpret_cast<const uint32_t*>(src) + (it * L + sub) * ew + lane;
+  uint32_t* dp = dst ? reinterpret_cast<uint32_t*>(dst) + (it * L + sub) * nwords + lane : nullptr;
+  uint2* np = nrm ? reinterpret_cast<uint2*>(nrm + it * (uint64_t)Kp + (uint64_t)sub * E) + lane
+                  : nullptr;
+  const uint32_t s_stride = wpe * ew, d_stride = wpe * nwords, n_stride = wpe * (E >> 2);
   uint64_t zbits = 0;
   for (uint32_t l0 = sub; live && l0 < L; l0 += 8 * wpe) {
     uint32_t wv[8][WPL];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int k = 0; k < WPL; ++k) {
-        const uint32_t w = lane + 32 * k, l = l0 + r * wpe;
-        wv[r][k] = (l < L && w < ew) ? __ldg(s32 + (uint64_t)l * ew + w) : 0u;
-      }
+      for (int k = 0; k < WPL; ++k)
+        wv[r][k] = (l0 + r * wpe < L && lane + 32 * k < ew) ? __ldg(sp + r * s_stride + 32 * k) : 0u;
+    sp += 8 * s_stride;
     // Σc² of the 8 rows (exact integers), then the fp64 scalars of row r on
     // lane r: one dsqrt/drcp sequence per 8 rows instead of one per row.
     uint32_t my_ss = 0;
@@ -769,20 +775,17 @@ __global__ void __launch_bounds__(512)
     }
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const uint32_t l = l0 + r * wpe;
-      if (l >= L) break;
+      if (l0 + r * wpe >= L) break;
       const float inv = __shfl_sync(0xffffffffu, my_inv, r);
+      if (dp) {
 #pragma unroll
-      for (int k = 0; k < WPL; ++k) {
-        const uint32_t w = lane + 32 * k;
-        if (w < nwords) d32[(uint64_t)l * nwords + w] = wv[r][k];
+        for (int k = 0; k < WPL; ++k)
+          if (lane + 32 * k < nwords) dp[r * d_stride + 32 * k] = wv[r][k];
       }
-      if (nrm) {
-        __half* o = nrm + it * (uint64_t)Kp + (uint64_t)l * E;
+      if (np) {
 #pragma unroll
         for (int k = 0; k < WPL; ++k) {
-          const uint32_t w = lane + 32 * k;
-          if (w < ew) {
+          if (lane + 32 * k < ew) {
             const uint32_t x = wv[r][k];
             const __half2 lo = __floats2half2_rn(__uint2float_rn(x & 0xffu) * inv,
                                                  __uint2float_rn((x >> 8) & 0xffu) * inv);
@@ -791,11 +794,13 @@ __global__ void __launch_bounds__(512)
             uint2 v;
             v.x = *reinterpret_cast<const uint32_t*>(&lo);
             v.y = *reinterpret_cast<const uint32_t*>(&hi);
-            *reinterpret_cast<uint2*>(o + 4 * w) = v;
+            np[r * n_stride + 32 * k] = v;
           }
         }
       }
     }
+    if (dp) dp += 8 * d_stride;
+    if (np) np += 8 * n_stride;
   }
   if (live && lane == 0 && zbits) atomicOr(&zsh[slot], (unsigned long long)zbits);
   __syncthreads();
@@ -2380,7 +2385,8 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
     // warps per EAM: enough warps in flight for small batches
     uint32_t wpe = 1;
     while (wpe < 16 && n * wpe < 2048 && wpe * 8 < L) wpe <<= 1;
-    const uint32_t pt = 512;
+    // small blocks (4 warps, or one EAM's warps) spread evenly over the SMs
+    const uint32_t pt = 32 * std::max<uint32_t>(4, wpe);
     const uint64_t wblocks = (n * wpe * 32 + pt - 1) / pt;
     return launch_pdl(E <= 128 ? k_prep_u8<1> : k_prep_u8<2>, dim3((unsigned)wblocks), dim3(pt),
                       0, st, static_cast<const uint8_t*>(src), n, E, L, RB, dst, ia, sq, ibT,
