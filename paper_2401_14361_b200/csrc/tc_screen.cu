@@ -58,7 +58,31 @@ struct TcArgs {
   uint32_t bcap;
   float* dmat;    // matrix mode: every screen distance -> dmat[q * ldd + p]
   uint32_t ldd;
+  // refine inputs prefetched into L2 during the screen: the collection's
+  // packed rows, fp64 row norms and seqs (pf[i] = bytes [0, pf_bytes[i]))
+  const uint8_t* pf[3];
+  uint64_t pf_bytes[3];
 };
+
+// The exact refine pass after the screen reads its candidates' packed u8 rows,
+// which the screen itself never touches (it streams the fp16 copies).  Each
+// CTA's producer thread prefetches its 1/grid slice of them into L2 with a
+// few bulk prefetches, issued after the CTA's first tile of operand loads.
+__device__ __forceinline__ void prefetch_slice_l2(const TcArgs& a, uint32_t part, uint32_t parts) {
+#pragma unroll 1
+  for (int i = 0; i < 3; ++i) {
+    if (!a.pf[i]) continue;
+    const uint64_t per = ((a.pf_bytes[i] + parts - 1) / parts + 15) & ~15ull;
+    const uint64_t b0 = per * part;
+    const uint64_t end = a.pf_bytes[i] & ~15ull;
+    const uint64_t b1 = b0 + per < end ? b0 + per : end;
+    for (uint64_t o = b0; o < b1; o += 32768) {
+      const uint32_t n = b1 - o < 32768 ? (uint32_t)(b1 - o) : 32768u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf[i] + o), "r"(n)
+                   : "memory");
+    }
+  }
+}
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
@@ -294,6 +318,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             ph ^= 1;
           }
         }
+        if (t == blockIdx.x) prefetch_slice_l2(a, blockIdx.x, gridDim.x);
       }
     }
   } else if (warp == 1) {
@@ -476,6 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             ph ^= 1;
           }
         }
+        if (t == cluster) prefetch_slice_l2(a, blockIdx.x, gridDim.x);
       }
     }
   } else if (warp == 1) {
@@ -622,6 +648,14 @@ cudaError_t launch_tc_screen(const DevColl& c, const DevProbes& pr, const MatchW
   a.bcap = w.bcap;
   a.dmat = dmat;
   a.ldd = ldd;
+  if (!dmat) {  // screen pass (the refine follows): its inputs into L2
+    a.pf[0] = c.counts;
+    a.pf_bytes[0] = (uint64_t)c.size * c.L * c.RB;
+    a.pf[1] = reinterpret_cast<const uint8_t*>(c.sqb);
+    a.pf_bytes[1] = (uint64_t)c.size * c.L * sizeof(double);
+    a.pf[2] = reinterpret_cast<const uint8_t*>(c.seq);
+    a.pf_bytes[2] = (uint64_t)c.size * sizeof(uint64_t);
+  }
   const char* e2 = getenv("MOE_TC2");
   const bool pair = (e2 ? e2[0] != '0' : true) && pr.Q > 128;
   if (pair) {  // 2-CTA pairs: 256-row M tiles, half the B tile per CTA
