@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmoe_eamc.so")
+LIB_PATH = os.environ.get("MOE_LIB") or os.path.join(HERE, "libmoe_eamc.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -403,7 +403,7 @@ __device__ __forceinline__ void refine_rows_per_lane(const RefineArgs& r, const 
 }
 
 template <int CB>
-__global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r) {
+__global__ void __launch_bounds__(kRefineWarps * 32, 7) k_refine(const RefineArgs r) {
   __shared__ double rbuf[kRefineWarps][kRefineBuf];
   __shared__ uint32_t cand[kRefineWarps][256];
   __shared__ uint64_t parts[kRefineWarps][kRefinePartBytes / 8];
@@ -499,15 +499,23 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
       sqa0 = sqa[pl0];
       sqb0 = r.sqb[(uint64_t)cg[pci0] * L + pl0];
     }
-    // (candidate, layer*C + chunk) of item `it`, advanced without divisions
-    uint32_t ci = lane / (uint32_t)LC, lc = lane - ci * (uint32_t)LC;
-#pragma unroll 4
-    for (uint32_t it = lane; it < items; it += 32) {
-      part[it] = Dot<CB>::chunk(__ldg(pa4 + lc), __ldg(cb4 + (uint64_t)cg[ci] * LC + lc), (Acc)0);
-      lc += 32;
-      while (lc >= (uint32_t)LC) {
-        lc -= (uint32_t)LC;
-        ++ci;
+    // Items in batches of 2 per lane: the (candidate, chunk) coordinates are
+    // computed first and the 4 loads of a batch are in flight together.
+    for (uint32_t it0 = lane; it0 < items; it0 += 2 * 32) {
+      uint4 va[2], vb[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t it = it0 + 32u * u;
+        if (it < items) {
+          const uint32_t ci = it / (uint32_t)LC, lc = it - ci * (uint32_t)LC;
+          va[u] = __ldg(pa4 + lc);
+          vb[u] = __ldg(cb4 + (uint64_t)cg[ci] * LC + lc);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t it = it0 + 32u * u;
+        if (it < items) part[it] = Dot<CB>::chunk(va[u], vb[u], (Acc)0);
       }
     }
     __syncwarp();
@@ -527,12 +535,24 @@ __global__ void __launch_bounds__(kRefineWarps * 32) k_refine(const RefineArgs r
     }
     __syncwarp();
     if (lane < gn) {
+      // in-order layer sum (eam.cpp:95-98); shared-memory reads batched ahead
+      const double* rs = rbuf[wib] + lane * L;
       double sm = 0.0;
-      for (uint32_t l = 0; l < L; ++l) sm = __dadd_rn(sm, rbuf[wib][lane * L + l]);
+      uint32_t l = 0;
+      for (; l + 4 <= L; l += 4) {
+        const double x0 = rs[l], x1 = rs[l + 1], x2 = rs[l + 2], x3 = rs[l + 3];
+        sm = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sm, x0), x1), x2), x3);
+      }
+      for (; l < L; ++l) sm = __dadd_rn(sm, rs[l]);
       const double d = finish_distance(sm, L);
       if (better(d, my_seq, b.d, b.seq)) b = Best{d, my_seq, cg[lane]};
     }
     __syncwarp();
+  }
+  if (nc <= 1) {  // a single candidate sits on lane 0: no warp reduction
+    if (lane == 0)
+      r.out[q] = moe_match{b.idx == kNone ? kNone : b.idx + r.index_base, b.seq, b.d};
+    return;
   }
   b = warp_best(b);
   if (lane == 0)
