@@ -1508,16 +1508,17 @@ static bool dec_pass(moe_eamc* h, const uint64_t* probe, uint32_t cur, cudaStrea
     return true;
   const bool prof = h->prof;
   h->prof = false;
-  const moe_status ps = launch_probe_prep(h, h->raw.p, cb, 1, st, pr);
+  unsigned long long* dmin = reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224);
+  moe::MatchInit mi;
+  mi.dmin = dmin;  // reset by the prep kernel (no memset between it and k_dec_dist)
+  const moe_status ps = launch_probe_prep(h, h->raw.p, cb, 1, st, pr, mi);
   h->prof = prof;
   if (ps != MOE_OK) return bad(ps);
-  unsigned long long* dmin = reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224);
   // explicit rows: through the last nonzero probe row and the stored row
   uint32_t hi = n_nz ? nz[n_nz - 1] : 0;
   if (keep < L) hi = std::max(hi, keep);
   if (!n_nz && keep >= L) hi = j0 ? j0 - 1 : 0;  // nothing explicit beyond the cached prefix
-  if (!ck(cudaMemsetAsync(dmin, 0xff, 8, st)) ||
-      !ck(moe::launch_dec_dist(c, pr->packed, pr->sqa,
+  if (!ck(moe::launch_dec_dist(c, pr->packed, pr->sqa,
                                reinterpret_cast<const uint16_t*>(h->raw.as<uint8_t>() + nz_off),
                                nz, n_nz, j0, hi, keep, h->pref.as<double>(), h->dist.as<double>(),
                                dmin, h->agg.as<unsigned long long>(), (uint32_t)cells,

@@ -631,7 +631,10 @@ __global__ void __launch_bounds__(256)
   pdl_trigger();
   const uint64_t row = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  if (row == 0 && lane == 0 && init.over_n) *init.over_n = 0;
+  if (row == 0 && lane == 0) {
+    if (init.over_n) *init.over_n = 0;
+    if (init.dmin) *init.dmin = ~0ull;
+  }
   if (row >= rows) return;
   const uint64_t it = row / L;
   const uint32_t l = (uint32_t)(row - it * L);
@@ -737,6 +740,7 @@ __global__ void __launch_bounds__(512)
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // u8 counts always fit: nothing exceeds the width
     if (max_count) *max_count = 0;
     if (init.over_n) *init.over_n = 0;
+    if (init.dmin) *init.dmin = ~0ull;
   }
   __syncthreads();
   const bool live = it < n;
@@ -1336,6 +1340,8 @@ __global__ void __launch_bounds__(kDecWarps * 32)
                const uint16_t* nz, uint32_t n_nz, uint32_t j0, uint32_t hi, uint32_t keep,
                double* pref, double* dist, unsigned long long* dmin,
                unsigned long long* zero_agg, uint32_t n_agg, uint32_t* zero_cnt) {
+  pdl_wait();
+  pdl_trigger();
   // Rows [j0, hi] are evaluated explicitly (hi >= every nonzero probe row and
   // >= keep when keep < L); rows above hi have zero probe rows, so each adds
   // 1.0 if the entry row is zero and 0.0 otherwise -- adding 0.0 leaves the
@@ -1421,6 +1427,8 @@ __global__ void __launch_bounds__(256)
                  uint64_t nzmask, uint32_t j0, uint32_t hi, uint32_t keep, double* pref,
                  double* dist, unsigned long long* dmin, unsigned long long* zero_agg,
                  uint32_t n_agg, uint32_t* zero_cnt) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
   for (uint32_t i = gtid; i < n_agg; i += gridDim.x * blockDim.x) zero_agg[i] = 0ull;
   if (zero_cnt && gtid == 0) *zero_cnt = 0;
@@ -1496,6 +1504,8 @@ __global__ void __launch_bounds__(1024)
     k_order(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur, int filter,
             moe_candidate* out, uint32_t* n_out, unsigned long long* gkey, uint32_t* gid,
             uint32_t* grank, uint32_t* big) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned long long key[kRankSmall];
   __shared__ uint32_t id[kRankSmall];
   __shared__ unsigned long long rs[256];
@@ -1588,6 +1598,8 @@ __global__ void __launch_bounds__(256)
     k_rank(const unsigned long long* gkey, const uint32_t* gid, const uint32_t* n_dev,
            const uint32_t* big, uint32_t E, uint32_t* grank, uint32_t* done,
            moe_candidate* out) {
+  pdl_wait();
+  pdl_trigger();
   if (*big == 0) return;
   __shared__ unsigned long long tk[1024];
   __shared__ uint32_t ti[1024];
@@ -1647,6 +1659,8 @@ __global__ void __launch_bounds__(256)
 // Window members (dist <= d_min + window, eam.cpp:143) -> compact list.
 __global__ void k_members(const double* dist, const unsigned long long* dmin, double window,
                           uint32_t size, uint32_t* mem, uint32_t* n_mem) {
+  pdl_wait();
+  pdl_trigger();
   const double thr = __dadd_rn(__longlong_as_double((long long)*dmin), window);
   for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < size; p += gridDim.x * blockDim.x)
     if (dist[p] <= thr) mem[atomicAdd(n_mem, 1u)] = p;
@@ -1660,6 +1674,8 @@ __global__ void __launch_bounds__(256)
     k_member_agg(const uint8_t* counts, uint32_t L, uint32_t E, uint32_t RB, uint32_t cur,
                  const uint32_t* mem, const uint32_t* n_mem, uint32_t chunk,
                  unsigned long long* agg) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t rows = L - cur - 1;
   const uint32_t wpr = RB / 4;  // words per row
   const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2756,22 +2772,22 @@ cudaError_t launch_dec_dist(const DevColl& c, const uint8_t* probe, const double
     for (uint32_t i = 0; i < n_nz; ++i) nzmask |= 1ull << nz_host[i];
     const unsigned g = (c.size + 255) / 256;
     if (c.cb == 1)
-      k_dec_dist_t<1><<<g, 256, 0, st>>>(c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB, probe, sqa,
+      launch_pdl(k_dec_dist_t<1>, dim3(g), dim3(256), 0, st, c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB, probe, sqa,
                                          nzmask, j0, hi, keep, pref, dist, dmin, zero_agg, n_agg,
                                          zero_cnt);
     else
-      k_dec_dist_t<2><<<g, 256, 0, st>>>(c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB, probe, sqa,
+      launch_pdl(k_dec_dist_t<2>, dim3(g), dim3(256), 0, st, c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB, probe, sqa,
                                          nzmask, j0, hi, keep, pref, dist, dmin, zero_agg, n_agg,
                                          zero_cnt);
     return cudaGetLastError();
   }
   const unsigned grid = (c.size + kDecWarps - 1) / kDecWarps;
   if (c.cb == 1)
-    k_dec_dist<1><<<grid, kDecWarps * 32, 0, st>>>(c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB,
+    launch_pdl(k_dec_dist<1>, dim3(grid), dim3(kDecWarps * 32), 0, st, c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB,
                                                    probe, sqa, nz, n_nz, j0, hi, keep, pref, dist,
                                                    dmin, zero_agg, n_agg, zero_cnt);
   else
-    k_dec_dist<2><<<grid, kDecWarps * 32, 0, st>>>(c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB,
+    launch_pdl(k_dec_dist<2>, dim3(grid), dim3(kDecWarps * 32), 0, st, c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB,
                                                    probe, sqa, nz, n_nz, j0, hi, keep, pref, dist,
                                                    dmin, zero_agg, n_agg, zero_cnt);
   return cudaGetLastError();
@@ -2786,7 +2802,7 @@ cudaError_t launch_member_agg(const DevColl& c, const double* dist,
     cudaError_t e = cudaMemsetAsync(n_mem, 0, 4, st);
     if (e != cudaSuccess) return e;
   }
-  k_members<<<std::min<uint32_t>((c.size + 255) / 256, (uint32_t)n_sm * 4), 256, 0, st>>>(
+  launch_pdl(k_members, dim3(std::min<uint32_t>((c.size + 255) / 256, (uint32_t)n_sm * 4)), dim3(256), 0, st, 
       dist, dmin, window, c.size, mem, n_mem);
   if (cur + 1 >= c.L) return cudaGetLastError();
   const uint32_t words = (c.L - cur - 1) * (c.RB / 4);
@@ -2796,9 +2812,9 @@ cudaError_t launch_member_agg(const DevColl& c, const double* dist,
   const uint32_t chunk = (c.size + by - 1) / by;
   dim3 grid(bx, by);
   if (c.cb == 1)
-    k_member_agg<1><<<grid, 256, 0, st>>>(c.counts, c.L, c.E, c.RB, cur, mem, n_mem, chunk, agg);
+    launch_pdl(k_member_agg<1>, dim3(grid), dim3(256), 0, st, c.counts, c.L, c.E, c.RB, cur, mem, n_mem, chunk, agg);
   else
-    k_member_agg<2><<<grid, 256, 0, st>>>(c.counts, c.L, c.E, c.RB, cur, mem, n_mem, chunk, agg);
+    launch_pdl(k_member_agg<2>, dim3(grid), dim3(256), 0, st, c.counts, c.L, c.E, c.RB, cur, mem, n_mem, chunk, agg);
   return cudaGetLastError();
 }
 
@@ -2821,10 +2837,10 @@ cudaError_t launch_prefetch_order(const unsigned long long* agg, uint32_t L, uin
         reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 64);
     uint32_t* gid = reinterpret_cast<uint32_t*>(gkey + n);
     uint32_t* grank = gid + n;
-    k_order<<<1, 1024, 0, st>>>(agg, L, E, cur, filter, out, n_dev, gkey, gid, grank, big);
+    launch_pdl(k_order, dim3(1), dim3(1024), 0, st, agg, L, E, cur, filter, out, n_dev, gkey, gid, grank, big);
     if (n > kRankSmall) {
       const dim3 g((n + 255) / 256, (n + 1023) / 1024);
-      k_rank<<<g, 256, 0, st>>>(gkey, gid, n_dev, big, E, grank, done, out);
+      launch_pdl(k_rank, dim3(g), dim3(256), 0, st, gkey, gid, n_dev, big, E, grank, done, out);
     }
     return cudaGetLastError();
   }

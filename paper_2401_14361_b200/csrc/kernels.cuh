@@ -77,6 +77,7 @@ struct MatchInit {
   uint32_t* T = nullptr;
   uint32_t* bcnt = nullptr;
   uint32_t* over_n = nullptr;
+  unsigned long long* dmin = nullptr;  // single-probe exact pass: running minimum <- ~0
 };
 
 // u64/u16/u8 counts -> packed rows + norms.  rows = n*L.  When ibT != null
