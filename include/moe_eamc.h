@@ -179,6 +179,32 @@ moe_status moe_prefetch_priorities(const moe_eamc* h, const uint64_t* cur_eam,
 moe_status moe_decide(const moe_eamc* h, const uint64_t* cur_eam, uint32_t current_layer,
                       const uint64_t* request_eam, const moe_slot_view* slots, uint64_t n_slots,
                       moe_candidate* out, uint64_t cap, uint64_t* n_out, int64_t* victim);
+/* P-sharded prefetch_priorities (policy.cpp:88-126 split at its two
+ * reductions).  Per rank, on the rank's shard:
+ *   1. moe_eamc_window_min_device: exact distances of cur_eam to every entry
+ *      (kept in the handle) and *d_min_bits = bits of the shard's minimum
+ *      distance (+inf for an empty shard) -- the d_min of eam.cpp:132-141.
+ *      Synchronises once (count-width check).
+ *   2. MIN all-reduce of d_min_bits across ranks (non-negative doubles order
+ *      like their bit patterns).
+ *   3. moe_eamc_window_aggregate_device: agg [L][E] u64 (overwritten) = sum of
+ *      the rows > current_layer of the shard's entries with
+ *      d <= d_min + window (eam.cpp:143; policy.cpp:96-104 uses window 0.01,
+ *      policy.hpp:30).  Must follow step 1 on the same handle.
+ *   4. SUM all-reduce of agg.
+ *   5. moe_eamc_prefetch_order_device: priorities, floor filter
+ *      (engine.cpp:663-668) and order from the summed agg; out needs
+ *      (L-current_layer-1)*E slots, *n_out (device) = count.
+ * All pointers except cur_eam are device pointers; work runs on `stream`
+ * (NULL: the handle's stream). */
+moe_status moe_eamc_window_min_device(const moe_eamc* h, const uint64_t* cur_eam,
+                                      uint64_t* d_min_bits, void* stream);
+moe_status moe_eamc_window_aggregate_device(const moe_eamc* h, uint32_t current_layer,
+                                            double window, const uint64_t* d_min_bits,
+                                            uint64_t* agg, void* stream);
+moe_status moe_eamc_prefetch_order_device(const moe_eamc* h, const uint64_t* agg,
+                                          uint32_t current_layer, int apply_floor_filter,
+                                          moe_candidate* out, uint32_t* n_out, void* stream);
 /* cache_priority (policy.cpp:128-141) */
 moe_status moe_cache_priority(const moe_shape* shape, const uint64_t* request_eam,
                               uint32_t layer, uint32_t expert, double* out);

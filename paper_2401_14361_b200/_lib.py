@@ -98,6 +98,9 @@ _sig("moe_eamc_kernel_times", C.c_int, vp, vp, vp)
 _sig("moe_eam_distance", C.c_int, P(moe_shape), vp, vp, P(C.c_double))
 _sig("moe_prefetch_priorities", C.c_int, vp, vp, C.c_uint32, C.c_int, vp, u64, P(u64))
 _sig("moe_decide", C.c_int, vp, vp, C.c_uint32, vp, vp, u64, vp, u64, P(u64), P(C.c_int64))
+_sig("moe_eamc_window_min_device", C.c_int, vp, vp, vp, vp)
+_sig("moe_eamc_window_aggregate_device", C.c_int, vp, C.c_uint32, C.c_double, vp, vp, vp)
+_sig("moe_eamc_prefetch_order_device", C.c_int, vp, vp, C.c_uint32, C.c_int, vp, vp, vp)
 _sig("moe_cache_priority", C.c_int, P(moe_shape), vp, C.c_uint32, C.c_uint32, P(C.c_double))
 _sig("moe_select_eviction_victim", C.c_int, P(moe_shape), vp, vp, u64, P(C.c_int64))
 _sig("moe_eam_trace", C.c_int, P(moe_shape), vp, C.c_int, u64, vp, u64, vp)
@@ -118,6 +121,8 @@ EXPORTS = [
     "moe_eamc_set_index_base", "moe_eamc_set_profiling", "moe_eamc_kernel_times",
     "moe_eam_distance",
     "moe_prefetch_priorities", "moe_decide", "moe_cache_priority",
+    "moe_eamc_window_min_device", "moe_eamc_window_aggregate_device",
+    "moe_eamc_prefetch_order_device",
     "moe_select_eviction_victim", "moe_eam_trace", "moe_eam_trace_device",
     "moe_eamc_capacity_bound", "moe_traces_request_eams", "moe_eamc_build_from_traces",
     "moe_eamc_save", "moe_eamc_load", "moe_gen_bench_family",

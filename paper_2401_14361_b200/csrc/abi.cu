@@ -1647,6 +1647,87 @@ moe_status moe_prefetch_priorities(const moe_eamc* hc, const uint64_t* cur_eam,
                      0, out, cap, n_out, nullptr, nullptr);
 }
 
+// ---- P-sharded decision (K4 window aggregate + K5) -------------
+// prefetch_priorities (policy.cpp:88-126) over a collection sharded by P:
+// (1) every rank's exact distances and local minimum, (2) MIN all-reduce of
+// the minimum's bits, (3) every rank's window members (d <= d_min + window,
+// the fp64 add of eam.cpp:143) aggregated into u64 [L][E] rows > current
+// layer, (4) SUM all-reduce, (5) priorities / floor filter / order from the
+// summed rows.  Integer sums and a min are order-independent, so the result is
+// bit-identical to the unsharded call.
+
+moe_status moe_eamc_window_min_device(const moe_eamc* hc, const uint64_t* cur_eam,
+                                      uint64_t* d_min_bits, void* stream) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || !cur_eam || !d_min_bits) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard dg(h->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->st;
+  CK(h->small.ensure(256));
+  CK(h->pin.ensure(256));
+  if (h->c.size == 0) {  // an empty shard contributes +inf
+    *h->pin.as<uint64_t>() = 0x7ff0000000000000ull;
+    CK(cudaMemcpyAsync(d_min_bits, h->pin.p, 8, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return MOE_OK;
+  }
+  for (;;) {  // the width check needs the host: one synchronisation
+    DevProbes pr;
+    CKS(launch_exact_distances(h, cur_eam, st, &pr));
+    CK(cudaMemcpyAsync(h->pin.p, h->small.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bool ok = false;
+    CKS(check_width(h, *h->pin.as<unsigned long long>(), &ok));
+    if (ok) break;
+  }
+  CK(cudaMemcpyAsync(d_min_bits, h->small.as<uint8_t>() + 224, 8, cudaMemcpyDeviceToDevice, st));
+  return MOE_OK;
+}
+
+moe_status moe_eamc_window_aggregate_device(const moe_eamc* hc, uint32_t current_layer,
+                                            double window, const uint64_t* d_min_bits,
+                                            uint64_t* agg, void* stream) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || !d_min_bits || !agg) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (current_layer >= h->shape.n_layers)
+    return fail(MOE_ERR_OUT_OF_RANGE, "prefetch_priorities: current_layer out of range");
+  DeviceGuard dg(h->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->st;
+  const uint64_t cells = (uint64_t)h->shape.n_layers * h->shape.n_experts_per_layer;
+  CK(cudaMemsetAsync(agg, 0, cells * 8, st));
+  if (h->c.size == 0) return MOE_OK;
+  CK(h->small.ensure(256));
+  CK(h->mem.ensure((size_t)h->c.size * 4));
+  CK(moe::launch_member_agg(h->c, h->dist.as<double>(),
+                            reinterpret_cast<const unsigned long long*>(d_min_bits), window,
+                            current_layer, h->mem.as<uint32_t>(), h->small.as<uint32_t>() + 10,
+                            reinterpret_cast<unsigned long long*>(agg), h->n_sm, st));
+  return MOE_OK;
+}
+
+moe_status moe_eamc_prefetch_order_device(const moe_eamc* hc, const uint64_t* agg,
+                                          uint32_t current_layer, int apply_floor_filter,
+                                          moe_candidate* out, uint32_t* n_out, void* stream) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || !agg || !out || !n_out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  const uint32_t L = h->shape.n_layers, E = h->shape.n_experts_per_layer;
+  if (current_layer >= L)
+    return fail(MOE_ERR_OUT_OF_RANGE, "prefetch_priorities: current_layer out of range");
+  DeviceGuard dg(h->device);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->st;
+  const uint64_t ncand = (uint64_t)(L - current_layer - 1) * E;
+  CK(h->keys.ensure(std::max<uint64_t>(ncand, 1) * 12));
+  const size_t osz = moe::prefetch_order_scratch(L, E);
+  if (h->oscr.n < osz) {
+    CK(h->oscr.ensure(osz));
+    CK(cudaMemsetAsync(h->oscr.p, 0, osz, st));
+  }
+  CK(moe::launch_prefetch_order(reinterpret_cast<const unsigned long long*>(agg), L, E,
+                                current_layer, apply_floor_filter,
+                                h->keys.as<unsigned long long>(), n_out, out, h->n_sm, st,
+                                h->oscr.p));
+  return MOE_OK;
+}
+
 moe_status moe_decide(const moe_eamc* hc, const uint64_t* cur_eam, uint32_t current_layer,
                       const uint64_t* request_eam, const moe_slot_view* slots, uint64_t n_slots,
                       moe_candidate* out, uint64_t cap, uint64_t* n_out, int64_t* victim) {

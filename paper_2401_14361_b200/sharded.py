@@ -59,3 +59,60 @@ class ShardedMatcher:
         dist.all_gather_into_tensor(parts, out, group=self.group)
         check(lib.moe_match_merge_device(parts.data_ptr(), self.world, Q, final.data_ptr(), sp))
         return final
+
+
+class ShardedDecider:
+    """P-sharded prefetch_priorities (SURVEY.md 8e, K4 window aggregate + K5).
+
+    policy.cpp:88-126 over a collection sharded by P, split at its two
+    reductions: each rank computes its shard's exact distances and minimum
+    (`moe_eamc_window_min_device`), the minimum is MIN-all-reduced (the bits of
+    a non-negative double order like the double), each rank aggregates the rows
+    > current_layer of its members d <= d_min + window (eam.cpp:143) into u64
+    [L][E] (`moe_eamc_window_aggregate_device`), the rows are SUM-all-reduced
+    (exact integers, order-independent), and the order is computed from the sum
+    (`moe_eamc_prefetch_order_device`).  The result is bit-identical to
+    `prefetch_order` on the unsharded collection; the exchange is
+    8 + 8*L*E bytes per rank, independent of P.
+    """
+
+    def __init__(self, eamc, group=None, stream=None):
+        import torch
+        from . import _lib
+        self._lib, self.eamc, self.group = _lib, eamc, group
+        self.dev = torch.device("cuda", eamc.device)
+        # one explicit stream for the library calls and the collectives (the
+        # legacy default stream would be read as "the handle's stream")
+        self.stream = stream or torch.cuda.Stream(device=self.dev)
+        L, E = eamc.shape.n_layers, eamc.shape.n_experts_per_layer
+        self.L, self.E = L, E
+        self._dmin = torch.empty(1, dtype=torch.int64, device=self.dev)
+        self._agg = torch.empty(L * E, dtype=torch.int64, device=self.dev)
+        self._out = torch.empty((max(L * E, 1), 2), dtype=torch.float64, device=self.dev)
+        self._n = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
+    def prefetch_order(self, cur_eam_counts: np.ndarray, current_layer: int,
+                       apply_floor_filter: bool = True, window: float = 0.01) -> np.ndarray:
+        import torch
+        import torch.distributed as dist
+        lib, check = self._lib.lib, self._lib.check
+        cur = np.ascontiguousarray(cur_eam_counts, np.uint64).reshape(self.L, self.E)
+        world = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        h = self.eamc._h
+        with torch.cuda.stream(self.stream):
+            sp = C.c_void_p(self.stream.cuda_stream)
+            check(lib.moe_eamc_window_min_device(h, cur.ctypes.data, self._dmin.data_ptr(), sp))
+            if world > 1:
+                dist.all_reduce(self._dmin, op=dist.ReduceOp.MIN, group=self.group)
+            check(lib.moe_eamc_window_aggregate_device(h, current_layer, window,
+                                                       self._dmin.data_ptr(),
+                                                       self._agg.data_ptr(), sp))
+            if world > 1:
+                dist.all_reduce(self._agg, op=dist.ReduceOp.SUM, group=self.group)
+            check(lib.moe_eamc_prefetch_order_device(h, self._agg.data_ptr(), current_layer,
+                                                     int(apply_floor_filter),
+                                                     self._out.data_ptr(),
+                                                     self._n.data_ptr(), sp))
+            n = int(self._n.item())
+            out = self._out[:n].cpu().numpy()
+        return out.view(np.uint8).reshape(n, 16).copy().view(self._lib.CAND_DTYPE)[:, 0]

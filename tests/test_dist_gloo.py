@@ -97,3 +97,63 @@ def test_shard_range_partition():
             assert rs[0][0] == 0 and rs[-1][1] == P
             assert all(rs[i][1] == rs[i + 1][0] for i in range(N - 1))
             assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def _decide_worker(rank, world, port, P, L, E, out_q):
+    """The host logic of sharded.ShardedDecider (SURVEY 8e, K4+K5) with the
+    per-shard device steps restated by the ORACLE: shard distances and
+    minimum -> MIN all-reduce of the double's bits -> members
+    d <= d_min + 0.01 (eam.cpp:143) -> u64 rows > layer -> SUM all-reduce ->
+    order.  Must equal the oracle's unsharded prefetch_priorities."""
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, Workload
+    from paper_2401_14361_b200.sharded import shard_range
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle()
+    w = Workload(L, E, 2, n_groups=6, prompt_len=3, decode_len=4, batch_size=2, seed=77)
+    ents = orc.request_eams(w, P)
+    s, e = shard_range(P, rank, world)
+    ok = True
+    for r, it, layer in [(500, 1, 0), (501, 2, L // 2), (502, 3, L - 2)]:
+        probe = orc.iteration_probe(w, r, it, layer)
+        _, _, d = orc.match_within(ents[s:e], np.arange(s, e, dtype=np.uint64), probe, 2.0)
+        # match_within returns (distance, seq) order; the members are a set
+        dall = np.array([orc.distance(ents[i], probe) for i in range(s, e)])
+        assert np.array_equal(np.sort(d), np.sort(dall))
+        dmin = torch.tensor([np.float64(dall.min()).view(np.int64)], dtype=torch.int64)
+        dist.all_reduce(dmin, op=dist.ReduceOp.MIN)
+        gmin = dmin.numpy().view(np.float64)[0]
+        members = dall <= gmin + 0.01
+        agg = np.zeros((L, E), np.int64)
+        agg[layer + 1:] = ents[s:e][members][:, layer + 1:].astype(np.int64).sum(0)
+        t = torch.from_numpy(agg.reshape(-1).copy())
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        total = t.numpy().reshape(1, L, E).astype(np.uint64)
+        for flt in (True, False):
+            got = orc.prefetch(total, np.zeros(1, np.uint64), probe, layer, flt)
+            want = orc.prefetch(ents, np.arange(P, dtype=np.uint64), probe, layer, flt)
+            ok &= all(np.array_equal(a, b) for a, b in zip(got, want))
+    flags = torch.tensor([int(ok)])
+    dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        out_q.put(bool(flags.item()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_decide_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_decide_worker, args=(r, 2, port, 161, 10, 16, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True

@@ -702,3 +702,62 @@ def test_trace_long_and_empty_requests(m, orc):
     for dt in (np.uint8, np.uint16, np.uint32):
         got = m.trace_requests(s, picks.astype(dt), offs)
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("L,E,P,n_shards", [(59, 160, 240, 3), (24, 128, 301, 2)])
+def test_prefetch_sharded_device_steps(m, orc, L, E, P, n_shards):
+    """The P-sharded decision steps through the C ABI, with the
+    ranks emulated as shard handles on one GPU: local minima -> min,
+    per-shard window aggregates -> sum, order from the sum.  Must equal the
+    oracle's prefetch_priorities over the whole collection, bitwise."""
+    import ctypes as C
+
+    import torch
+    from paper_2401_14361_b200 import _lib
+    from paper_2401_14361_b200.sharded import ShardedDecider, shard_range
+    w = Workload(L, E, min(6, E), n_groups=12, prompt_len=3, decode_len=4, batch_size=2,
+                 seed=31)
+    ents = orc.request_eams(w, P)
+    s = m.ModelShape(L, E, min(6, E))
+    shards = []
+    for r in range(n_shards):
+        a, b = shard_range(P, r, n_shards)
+        e = m.Eamc(s, m.Phase.decode, b - a)
+        e.append(ents[a:b], np.arange(a, b, dtype=np.uint64))
+        shards.append(e)
+    whole = m.Eamc(s, m.Phase.decode, P)
+    whole.build(ents)
+    st = torch.cuda.Stream()
+    sp = C.c_void_p(st.cuda_stream)
+    lib = _lib.lib
+    for r, it, layer in [(900, 1, 0), (901, 2, L // 2), (902, 3, L - 2), (903, 4, L - 1)]:
+        pr = np.ascontiguousarray(orc.iteration_probe(w, r, it, layer), np.uint64)
+        for flt in (True, False):
+            with torch.cuda.stream(st):
+                mins = torch.empty(n_shards, dtype=torch.int64, device="cuda")
+                for k, e in enumerate(shards):
+                    _lib.check(lib.moe_eamc_window_min_device(e._h, pr.ctypes.data,
+                                                              mins[k:].data_ptr(), sp))
+                gmin = mins.min().reshape(1)
+                aggs = torch.empty((n_shards, L * E), dtype=torch.int64, device="cuda")
+                for k, e in enumerate(shards):
+                    _lib.check(lib.moe_eamc_window_aggregate_device(
+                        e._h, layer, 0.01, gmin.data_ptr(), aggs[k].data_ptr(), sp))
+                agg = aggs.sum(0).contiguous()
+                out = torch.empty((max((L - layer - 1) * E, 1), 2), dtype=torch.float64,
+                                  device="cuda")
+                n = torch.zeros(1, dtype=torch.int32, device="cuda")
+                _lib.check(lib.moe_eamc_prefetch_order_device(shards[0]._h, agg.data_ptr(),
+                                                              layer, int(flt), out.data_ptr(),
+                                                              n.data_ptr(), sp))
+                k = int(n.item())
+                got = out[:k].cpu().numpy().view(np.uint8).reshape(k, 16).copy().view(
+                    _lib.CAND_DTYPE)[:, 0]
+            ol, ox, op = orc.prefetch(ents, seqs_of(P), pr, layer, flt)
+            assert np.array_equal(got["layer_idx"], ol)
+            assert np.array_equal(got["expert_idx"], ox)
+            assert np.array_equal(got["priority"], op)
+            # world size 1: the ShardedDecider equals the unsharded call
+            one = ShardedDecider(whole).prefetch_order(pr, layer, flt)
+            ref = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), whole, layer, flt)
+            assert np.array_equal(one, ref)
