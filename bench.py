@@ -37,6 +37,7 @@ L, E, TOPK = 12, 128, 1
 P_PER_GPU, Q = 10_000, 4096
 SEED = 55
 STREAM_P, STREAM_Q = 1 << 20, 8   # SC streaming regime (P >= 1M), north-star HBM target
+BATCH_Q = 65536                  # SC batch regime (BASELINE configs[4]: 65k-query batch)
 
 
 def dist_env():
@@ -530,33 +531,41 @@ def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak,
             _lib.check(_lib.lib.moe_match_merge_device(d_parts.data_ptr(), N, STREAM_Q,
                                                        d_fin.data_ptr(), sp))
 
+    stream = torch.cuda.current_stream()
+
+    def timed(step_fn, steps, profile):
+        if N > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if profile:
+            _lib.check(_lib.lib.moe_eamc_set_profiling(e._h, 1))
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        for i in range(steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step_fn()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        kms = (C.c_double * 3)()
+        kc = (C.c_uint64 * 3)()
+        if profile:
+            _lib.check(_lib.lib.moe_eamc_kernel_times(e._h, kms, kc))
+            _lib.check(_lib.lib.moe_eamc_set_profiling(e._h, 0))
+        t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64,
+                         device=dev)
+        if N > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), kms[1] / max(kc[1], 1)
+
     for _ in range(3):
         step()
-    if N > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     steps = 30
-    _lib.check(_lib.lib.moe_eamc_set_profiling(e._h, 1))
-    stream = torch.cuda.current_stream()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(steps)]
-    for i in range(steps):
-        flush.zero_()
-        evs[i][0].record(stream)
-        step()
-        evs[i][1].record(stream)
-    torch.cuda.synchronize()
-    kms = (C.c_double * 3)()
-    kc = (C.c_uint64 * 3)()
-    _lib.check(_lib.lib.moe_eamc_kernel_times(e._h, kms, kc))
-    t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
-    if N > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_ms = float(t.item())
-    screen_ms = kms[1] / max(kc[1], 1)
+    t_ms, _ = timed(step, steps, False)   # value: no per-kernel events (PDL intact)
+    _, screen_ms = timed(step, steps, True)
     bytes_alg = P * L * E * 1 + STREAM_Q * L * E * 1 + 24 * STREAM_Q
     ach = bytes_alg / (screen_ms / 1e3) / 1e9
-    return {
+    out = {
         "workload": f"SC streaming: P={STREAM_P} (P/GPU={P}), Q={STREAM_Q}, L={L} E={E}, u8",
         "value": P * N * STREAM_Q * steps / (t_ms / 1e3), "unit": "evals/s",
         "ms_per_step": t_ms / steps, "steps": steps,
@@ -568,6 +577,46 @@ def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak,
                      "alg_bytes_per_launch": bytes_alg,
                      "note": f"peak = {peak_kind} HBM copy bandwidth (MEASURED_PEAKS.json)"},
     }
+    if args.no_batch:
+        return out
+    # SC batch regime (BASELINE configs[4]): the same collection, a 65,536-probe batch;
+    # compute-bound by construction, so its roofline is the tensor pipe
+    QB = BATCH_Q
+    pb = torch.from_numpy(m.gen_bench_family(SEED, L, E, QB, skip=STREAM_P + STREAM_Q,
+                                             dtype=np.uint8)).to(dev)
+    b_out = torch.empty((QB, 3), dtype=torch.float64, device=dev)
+    b_parts = torch.empty((N * QB, 3), dtype=torch.float64, device=dev)
+    b_fin = torch.empty((QB, 3), dtype=torch.float64, device=dev)
+
+    def bstep():
+        _lib.check(_lib.lib.moe_eamc_match_device(e._h, pb.data_ptr(), 1, QB, b_out.data_ptr(),
+                                                  sp))
+        if N > 1:
+            dist.all_gather_into_tensor(b_parts, b_out)
+            _lib.check(_lib.lib.moe_match_merge_device(b_parts.data_ptr(), N, QB,
+                                                       b_fin.data_ptr(), sp))
+
+    bstep()
+    bsteps = 3
+    tb_ms, _ = timed(bstep, bsteps, False)
+    _, bscreen_ms = timed(bstep, bsteps, True)
+    ops = 2.0 * L * E * P * QB
+    _, tf_peak, _ = load_peaks()
+    out["batch"] = {
+        "workload": f"SC batch: P={STREAM_P} (P/GPU={P}), Q={QB}, L={L} E={E}, u8",
+        "value": P * N * QB * bsteps / (tb_ms / 1e3), "unit": "evals/s",
+        "ms_per_step": tb_ms / bsteps, "steps": bsteps,
+        "roofline": {"bound": "tensor",
+                     "kernel": "k_tc2_screen (tcgen05.mma.cta_group::2 kind::f16)",
+                     "achieved": ops / (bscreen_ms / 1e3) / 1e12, "peak": tf_peak,
+                     "unit": "TFLOP/s", "frac": ops / (bscreen_ms / 1e3) / 1e12 / tf_peak,
+                     "launch_ms": bscreen_ms, "alg_ops_per_launch": ops,
+                     "frac_of_nominal_2250": ops / (bscreen_ms / 1e3) / 1e12 / 2250.0,
+                     "note": ("ops = 2*L*E*P*Q (SURVEY.md 8d); peak = measured cuBLAS bf16 "
+                              "8192^3 burst (MEASURED_PEAKS.json, taken under the 1000 W cap); "
+                              "frac_of_nominal_2250 = against the nominal dense fp16 peak")},
+    }
+    return out
 
 
 def cpu_baseline(args, probes_u8, gpu_res):
@@ -680,6 +729,7 @@ def main():
     ap.add_argument("--no-streaming", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rows", action="store_true")
+    ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
