@@ -1596,14 +1596,12 @@ __global__ void __launch_bounds__(1024)
 
 __global__ void __launch_bounds__(256)
     k_rank(const unsigned long long* gkey, const uint32_t* gid, const uint32_t* n_dev,
-           const uint32_t* big, uint32_t E, uint32_t* grank, uint32_t* done,
-           moe_candidate* out) {
+           const uint32_t* big, uint32_t* grank) {
   pdl_wait();
   pdl_trigger();
   if (*big == 0) return;
   __shared__ unsigned long long tk[1024];
   __shared__ uint32_t ti[1024];
-  __shared__ bool last;
   const uint32_t ns = *n_dev;
   const uint32_t j0 = blockIdx.y * 1024;
   const uint32_t i = blockIdx.x * 256 + threadIdx.x;
@@ -1622,17 +1620,18 @@ __global__ void __launch_bounds__(256)
       if (r) atomicAdd(&grank[i], r);
     }
   }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (uint32_t q = threadIdx.x; q < ns; q += 256) {
-    const uint32_t r = *reinterpret_cast<volatile const uint32_t*>(&grank[q]);
-    out[r] = make_cand(gkey[q], gid[q], E);
-  }
-  if (threadIdx.x == 0) *done = 0;
+}
+
+// Long survivor lists, second pass: every candidate to its rank (all counts
+// of k_rank are complete: PDL's griddepcontrol.wait orders the two grids).
+__global__ void __launch_bounds__(256)
+    k_rank_scatter(const unsigned long long* gkey, const uint32_t* gid, const uint32_t* n_dev,
+                   const uint32_t* big, uint32_t E, const uint32_t* grank, moe_candidate* out) {
+  pdl_wait();
+  pdl_trigger();
+  if (*big == 0) return;
+  const uint32_t i = blockIdx.x * 256 + threadIdx.x;
+  if (i < *n_dev) out[grank[i]] = make_cand(gkey[i], gid[i], E);
 }
 
 // In-order layer sum (eam.cpp:95-103) -> dist[p]; warp min -> atomicMin(*dmin).
@@ -2832,7 +2831,6 @@ cudaError_t launch_prefetch_order(const unsigned long long* agg, uint32_t L, uin
     // at most 16 candidates per thread
     const uint32_t n = (L - cur - 1) * E;
     uint32_t* big = static_cast<uint32_t*>(scratch);
-    uint32_t* done = big + 1;  // zeroed at allocation, reset by k_rank's last block
     unsigned long long* gkey =
         reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 64);
     uint32_t* gid = reinterpret_cast<uint32_t*>(gkey + n);
@@ -2840,7 +2838,11 @@ cudaError_t launch_prefetch_order(const unsigned long long* agg, uint32_t L, uin
     launch_pdl(k_order, dim3(1), dim3(1024), 0, st, agg, L, E, cur, filter, out, n_dev, gkey, gid, grank, big);
     if (n > kRankSmall) {
       const dim3 g((n + 255) / 256, (n + 1023) / 1024);
-      launch_pdl(k_rank, dim3(g), dim3(256), 0, st, gkey, gid, n_dev, big, E, grank, done, out);
+      launch_pdl(k_rank, dim3(g), dim3(256), 0, st, (const unsigned long long*)gkey,
+                 (const uint32_t*)gid, (const uint32_t*)n_dev, (const uint32_t*)big, grank);
+      launch_pdl(k_rank_scatter, dim3((n + 255) / 256), dim3(256), 0, st,
+                 (const unsigned long long*)gkey, (const uint32_t*)gid, (const uint32_t*)n_dev,
+                 (const uint32_t*)big, E, (const uint32_t*)grank, out);
     }
     return cudaGetLastError();
   }
