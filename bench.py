@@ -260,6 +260,21 @@ def run_ours(args):
     if N > 1:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_val = evals_per_step * e2e_steps / float(t_e2e.item())
+
+    # the same through moe_eamc_match_packed: host probes already narrow (u8,
+    # as traced counts of this workload are), 6.3 MB per step instead of 50 MB
+    h_probes8 = _t.from_numpy(probes_u8).pin_memory()
+
+    def step_e2e_packed():
+        _lib.check(_lib.lib.moe_eamc_match_packed(eamc._h, h_probes8.data_ptr(), 1, Q,
+                                                  h_out.ctypes.data, None))
+
+    for _ in range(min(args.warmup, 3)):
+        step_e2e_packed()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step_e2e_packed()
+    e2e_packed_val = P * Q * e2e_steps / (time.perf_counter() - t0)
     host_threads = int(_lib.lib.moe_host_threads())
 
     # ---- the other SURVEY 8 rows (prefetch decisions, construction, tracing, MIX)
@@ -294,6 +309,10 @@ def run_ours(args):
                             f"narrowed to u8 on {host_threads} host threads inside the call"),
                     "h2d_bytes_per_step": int(Q * L * E * 1),
                     "d2h_bytes_per_step": int(Q * 24)},
+            "e2e_packed_u8": {"value": e2e_packed_val * N, "unit": "evals/s", "steps": e2e_steps,
+                              "api": "moe_eamc_match_packed (host u8 probes, pinned) + D2H results "
+                                     "(per-rank, scaled by N)",
+                              "h2d_bytes_per_step": int(Q * L * E), "d2h_bytes_per_step": int(Q * 24)},
             "gpu_launches": gpu_launches,
             "ms_per_step_profiled": sum(ms_prof) / args.steps,
             "kernel_ms_per_step": {"prep": kms[0] / max(kcalls[0], 1), "screen": screen_ms,

@@ -135,6 +135,11 @@ moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_byt
 /* probes [n][L][E] u64 host; out[n]; found[n] (nullable). */
 moe_status moe_eamc_match(const moe_eamc* h, const uint64_t* probes, uint64_t n_probes,
                           moe_match* out, uint8_t* found);
+/* Same, with host probes already narrow: [n][L][E] of probe_bytes (1, 2 or
+ * 8) bytes per count (e.g. counts traced as u8/u16).  Results are identical
+ * to moe_eamc_match on the widened counts; one H2D of the narrow batch. */
+moe_status moe_eamc_match_packed(const moe_eamc* h, const void* probes, int probe_bytes,
+                                 uint64_t n_probes, moe_match* out, uint8_t* found);
 /* Device variant: probes are device [n][L][E] of probe_bytes (1, 2 or 8)
  * bytes per count, out is device moe_match[n].  stream NULL = the handle's
  * internal stream (NOT the legacy default stream); pass the caller's stream

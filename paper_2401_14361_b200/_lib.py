@@ -89,6 +89,7 @@ _sig("moe_eamc_append", C.c_int, vp, vp, vp, u64)
 _sig("moe_eamc_append_packed", C.c_int, vp, vp, C.c_int, vp, u64)
 _sig("moe_eamc_match", C.c_int, vp, vp, u64, vp, vp)
 _sig("moe_eamc_match_device", C.c_int, vp, vp, C.c_int, u64, vp, vp)
+_sig("moe_eamc_match_packed", C.c_int, vp, vp, C.c_int, u64, vp, vp)
 _sig("moe_eamc_match_within", C.c_int, vp, vp, C.c_double, vp, u64, P(u64))
 _sig("moe_match_merge", C.c_int, vp, u64, u64, vp)
 _sig("moe_match_merge_device", C.c_int, vp, u64, u64, vp, vp)
@@ -117,6 +118,7 @@ EXPORTS = [
     "moe_abi_version", "moe_host_threads", "moe_last_error", "moe_device_info", "moe_device_warmup", "moe_eamc_create",
     "moe_eamc_destroy", "moe_eamc_info", "moe_eamc_clone", "moe_eamc_entry", "moe_eamc_insert", "moe_eamc_build",
     "moe_eamc_append", "moe_eamc_append_packed", "moe_eamc_match", "moe_eamc_match_device",
+    "moe_eamc_match_packed",
     "moe_eamc_match_within", "moe_match_merge", "moe_match_merge_device",
     "moe_eamc_set_index_base", "moe_eamc_set_profiling", "moe_eamc_kernel_times",
     "moe_eam_distance",

@@ -1275,6 +1275,34 @@ moe_status moe_eamc_match_device(const moe_eamc* hc, const void* probes, int pro
   return MOE_OK;
 }
 
+// Host probes already narrow ([n][L][E] of 1 or 2 bytes, e.g. traced
+// counts): one H2D of the narrow batch (a true DMA when the buffer is pinned),
+// the matching pipeline in synchronous mode (width check; widening redo), D2H.
+moe_status moe_eamc_match_packed(const moe_eamc* hc, const void* probes, int probe_bytes,
+                                 uint64_t n_probes, moe_match* out, uint8_t* found) {
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || ((!probes || !out) && n_probes)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (probe_bytes == 8)
+    return moe_eamc_match(hc, static_cast<const uint64_t*>(probes), n_probes, out, found);
+  if (probe_bytes != 1 && probe_bytes != 2)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "probe_bytes must be 1, 2 or 8");
+  if (n_probes == 0) return MOE_OK;
+  if (n_probes > 0xffffffffull) return fail(MOE_ERR_INVALID_ARGUMENT, "too many probes");
+  DeviceGuard dg(h->device);
+  const uint64_t bytes = n_probes * (uint64_t)h->c.L * h->c.E * probe_bytes;
+  CK(h->raw.ensure(bytes + 16));
+  CK(h->outall.ensure(n_probes * sizeof(moe_match)));
+  CK(cudaMemcpyAsync(h->raw.p, probes, bytes, cudaMemcpyHostToDevice, h->st));
+  DevProbes pr;
+  CKS(match_all(h, h->raw.p, probe_bytes, n_probes, true, h->outall.as<moe_match>(), h->st, &pr));
+  CK(cudaMemcpyAsync(out, h->outall.p, n_probes * sizeof(moe_match), cudaMemcpyDeviceToHost,
+                     h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (found)
+    for (uint64_t q = 0; q < n_probes; ++q) found[q] = out[q].index != ~0ull;
+  return MOE_OK;
+}
+
 moe_status moe_eamc_match_within(const moe_eamc* hc, const uint64_t* probe, double window,
                                  moe_match* out, uint64_t cap, uint64_t* n_out) {
   moe_eamc* h = const_cast<moe_eamc*>(hc);

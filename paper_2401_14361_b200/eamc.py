@@ -284,12 +284,17 @@ class Eamc:
     # -- matching ---------------------------------------------------------
     def match_batch(self, probes: np.ndarray) -> np.ndarray:
         """Eamc::match over [Q][L][E] probes -> structured array (index, seq, distance)."""
-        probes = np.ascontiguousarray(probes, np.uint64)
+        narrow = isinstance(probes, np.ndarray) and probes.dtype in (np.uint8, np.uint16)
+        probes = np.ascontiguousarray(probes, probes.dtype if narrow else np.uint64)
         if probes.shape[1:] != (self.shape.n_layers, self.shape.n_experts_per_layer):
             raise ValueError("Eamc: probe shape mismatch")
         Q = probes.shape[0]
         out = np.zeros(max(Q, 1), MATCH_DTYPE)
-        check(lib.moe_eamc_match(self._h, ptr(probes), Q, ptr(out), None))
+        if narrow:  # u8/u16 counts: shipped narrow (moe_eamc_match_packed)
+            check(lib.moe_eamc_match_packed(self._h, ptr(probes), probes.dtype.itemsize, Q,
+                                            ptr(out), None))
+        else:
+            check(lib.moe_eamc_match(self._h, ptr(probes), Q, ptr(out), None))
         return out[:Q]
 
     def match(self, probe: Eam) -> Optional[EamcMatch]:

@@ -761,3 +761,19 @@ def test_prefetch_sharded_device_steps(m, orc, L, E, P, n_shards):
             one = ShardedDecider(whole).prefetch_order(pr, layer, flt)
             ref = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), whole, layer, flt)
             assert np.array_equal(one, ref)
+
+
+def test_match_packed_host_probes(m, orc):
+    """moe_eamc_match_packed: narrow (u8 / u16) host probes give the same
+    results as the u64 reference-API path; u16 counts above 255 widen."""
+    L, E, P = 12, 64, 500
+    fam = m.gen_bench_family(19, L, E, P + 40)
+    e = filled(m, L, E, fam[:P])
+    want = check_match(m, orc, e, fam[:P], seqs_of(P), fam[P:])
+    got8 = e.match_batch(fam[P:].astype(np.uint8))
+    assert np.array_equal(got8, want)
+    wide = (fam[P:] * 20).astype(np.uint16)  # up to 640 > 255
+    got16 = e.match_batch(wide)
+    idx, seq, d, _ = orc.match(fam[:P], seqs_of(P), wide.astype(np.uint64))
+    assert np.array_equal(got16["index"], idx) and np.array_equal(got16["distance"], d)
+    assert e.count_bytes() == 2
