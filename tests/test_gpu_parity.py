@@ -777,3 +777,17 @@ def test_match_packed_host_probes(m, orc):
     idx, seq, d, _ = orc.match(fam[:P], seqs_of(P), wide.astype(np.uint64))
     assert np.array_equal(got16["index"], idx) and np.array_equal(got16["distance"], d)
     assert e.count_bytes() == 2
+
+
+def test_pipeline_without_pdl():
+    """The match / decision pipelines with programmatic dependent launch
+    disabled (plain stream order, MOE_PDL=0): the smoke checks still hold."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MOE_PDL="0")
+    r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"], cwd=root,
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "smoke ok" in r.stdout
