@@ -791,3 +791,23 @@ def test_pipeline_without_pdl():
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "smoke ok" in r.stdout
+
+
+@pytest.mark.parametrize("L,E,P,mult", [(32, 8, 300, 1), (8, 16, 1000, 1), (4, 4, 37, 1),
+                                        (16, 32, 200, 40)])
+def test_prefetch_small_collection(m, orc, L, E, P, mult):
+    """Small collections take the one-launch decision kernel (k_decide_small,
+    P <= 1024, L*E <= 1024); mult > 1 pushes counts past 255 (u16 storage)."""
+    w = Workload(L, E, min(2, E), n_groups=6, prompt_len=3, decode_len=4, batch_size=2, seed=L + P)
+    ents = orc.request_eams(w, P) * mult
+    s = m.ModelShape(L, E, min(2, E))
+    e = m.Eamc(s, m.Phase.decode, P)
+    e.build(ents)
+    for r, it, layer in [(700, 1, 0), (701, 2, L // 2), (702, 3, L - 2), (703, 4, L - 1)]:
+        pr = orc.iteration_probe(w, r, it, layer) * mult
+        for flt in (True, False):
+            ol, ox, op = orc.prefetch(ents, seqs_of(P), pr, layer, flt)
+            out = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), e, layer, flt)
+            assert np.array_equal(out["layer_idx"], ol)
+            assert np.array_equal(out["expert_idx"], ox)
+            assert np.array_equal(out["priority"], op)
