@@ -1534,30 +1534,46 @@ __global__ void __launch_bounds__(1024)
     const uint32_t i = tid + k * blockDim.x;
     av[k] = i < n ? ag[i] : 0ull;
   }
+  // survivors get their slots by one shared atomic per warp (ballot + popc),
+  // not one per candidate on a single shared counter
 #pragma unroll
   for (int u = 0; u < kPre; ++u) {
+    if (u * blockDim.x >= n) break;  // block-uniform: every lane stays for the ballot
     const uint32_t i = tid + u * blockDim.x;
-    if (i >= n) break;
-    const uint32_t li = i / E, e = i - li * E;
-    const uint32_t l = cur + 1 + li;
-    const double prox = px[l];
-    const unsigned long long a = av[u];
-    // a zero count gives priority kEps*prox, which never clears the floor
-    // kEps*prox*(1+1e-9) (rounding is monotone)
-    if (filter && a == 0) continue;
-    const double ratio = rs[l] == 0 ? 0.0 : __ddiv_rn(__ull2double_rn(a), __ull2double_rn(rs[l]));
-    const double pri = __dmul_rn(__dadd_rn(ratio, kEps), prox);
-    if (filter && pri <= __dmul_rn(__dmul_rn(kEps, prox), __dadd_rn(1.0, 1e-9))) continue;
-    const uint32_t pos = atomicAdd(&cnt, 1u);
-    const unsigned long long k = ~(unsigned long long)__double_as_longlong(pri);
-    const uint32_t flat = l * E + e;
-    if (pos < kRankSmall) {
-      key[pos] = k;
-      id[pos] = flat;
+    bool pass = false;
+    unsigned long long k = 0;
+    uint32_t flat = 0;
+    if (i < n) {
+      const uint32_t li = i / E, e = i - li * E;
+      const uint32_t l = cur + 1 + li;
+      const double prox = px[l];
+      const unsigned long long a = av[u];
+      // a zero count gives priority kEps*prox, which never clears the floor
+      // kEps*prox*(1+1e-9) (rounding is monotone)
+      if (!(filter && a == 0)) {
+        const double ratio =
+            rs[l] == 0 ? 0.0 : __ddiv_rn(__ull2double_rn(a), __ull2double_rn(rs[l]));
+        const double pri = __dmul_rn(__dadd_rn(ratio, kEps), prox);
+        pass = !(filter && pri <= __dmul_rn(__dmul_rn(kEps, prox), __dadd_rn(1.0, 1e-9)));
+        k = ~(unsigned long long)__double_as_longlong(pri);
+        flat = l * E + e;
+      }
     }
-    gkey[pos] = k;
-    gid[pos] = flat;
-    grank[pos] = 0;
+    const uint32_t m = __ballot_sync(0xffffffffu, pass);
+    if (m == 0) continue;
+    uint32_t base = 0;
+    if (lane == (uint32_t)(__ffs(m) - 1)) base = atomicAdd(&cnt, (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (pass) {
+      const uint32_t pos = base + __popc(m & ((1u << lane) - 1));
+      if (pos < kRankSmall) {
+        key[pos] = k;
+        id[pos] = flat;
+      }
+      gkey[pos] = k;
+      gid[pos] = flat;
+      grank[pos] = 0;
+    }
   }
   __syncthreads();
   const uint32_t ns = cnt;
