@@ -1496,6 +1496,14 @@ moe_status moe_eam_distance(const moe_shape* shape, const uint64_t* a, const uin
 // (engine.cpp:546, :587) -- are reused from pref (k_dec_dist).  Returns
 // false (nothing launched) when the probe does not fit the storage width;
 // launch errors land in h->last_status.
+static bool zc_ok() {  // MOE_DECIDE_ZC=0: device outputs + copies (A/B runs)
+  static const bool on = [] {
+    const char* e = getenv("MOE_DECIDE_ZC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool dec_pass(moe_eamc* h, const uint64_t* probe, uint32_t cur, cudaStream_t st,
                      DevProbes* pr) {
   h->last_status = MOE_OK;
@@ -1531,15 +1539,22 @@ static bool dec_pass(moe_eamc* h, const uint64_t* probe, uint32_t cur, cudaStrea
     return e == cudaSuccess;
   };
   if (!ck(h->raw.ensure(nz_off + L * 2 + 16)) || !ck(h->pref.ensure((size_t)std::max<uint32_t>(c.size, 1) * 8)) ||
-      !ck(h->dist.ensure((size_t)std::max<uint32_t>(c.size, 1) * 8)) ||
-      !ck(cudaMemcpyAsync(h->raw.p, hb, nz_off + n_nz * 2, cudaMemcpyHostToDevice, st)))
+      !ck(h->dist.ensure((size_t)std::max<uint32_t>(c.size, 1) * 8)))
     return true;
+  // the prep kernel and k_dec_dist read the narrowed probe and its nonzero-row
+  // list straight from pinned host memory (UVA), or from a device copy
+  const uint8_t* src = hb;
+  if (!zc_ok()) {
+    if (!ck(cudaMemcpyAsync(h->raw.p, hb, nz_off + n_nz * 2, cudaMemcpyHostToDevice, st)))
+      return true;
+    src = h->raw.as<uint8_t>();
+  }
   const bool prof = h->prof;
   h->prof = false;
   unsigned long long* dmin = reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224);
   moe::MatchInit mi;
   mi.dmin = dmin;  // reset by the prep kernel (no memset between it and k_dec_dist)
-  const moe_status ps = launch_probe_prep(h, h->raw.p, cb, 1, st, pr, mi);
+  const moe_status ps = launch_probe_prep(h, src, cb, 1, st, pr, mi);
   h->prof = prof;
   if (ps != MOE_OK) return bad(ps);
   // explicit rows: through the last nonzero probe row and the stored row
@@ -1547,7 +1562,7 @@ static bool dec_pass(moe_eamc* h, const uint64_t* probe, uint32_t cur, cudaStrea
   if (keep < L) hi = std::max(hi, keep);
   if (!n_nz && keep >= L) hi = j0 ? j0 - 1 : 0;  // nothing explicit beyond the cached prefix
   if (!ck(moe::launch_dec_dist(c, pr->packed, pr->sqa,
-                               reinterpret_cast<const uint16_t*>(h->raw.as<uint8_t>() + nz_off),
+                               reinterpret_cast<const uint16_t*>(src + nz_off),
                                nz, n_nz, j0, hi, keep, h->pref.as<double>(), h->dist.as<double>(),
                                dmin, h->agg.as<unsigned long long>(), (uint32_t)cells,
                                h->small.as<uint32_t>() + 10, st)))
@@ -1577,6 +1592,12 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
   const uint64_t ncand = prefetch_live && current_layer + 1 < L ? (uint64_t)(L - current_layer - 1) * E : 0;
   CK(h->cand.ensure(std::max<uint64_t>(ncand, 1) * sizeof(moe_candidate)));
   uint32_t* dn = h->small.as<uint32_t>() + 12;
+  // zc: the order kernels write the candidates and their count straight into
+  // pinned host memory (device-visible under UVA) -- no device-to-host copies,
+  // one synchronisation.  Taken on the host-narrowed path (the width check is
+  // then already done on the host) when no eviction output is requested.
+  bool zc = false;
+  uint32_t* dn_host = reinterpret_cast<uint32_t*>(h->pin.as<uint8_t>() + 248);
   if (prefetch_live) {
     // one exact pass over the collection, window membership (kMatchWindow,
     // policy.hpp:30) + u64 aggregation of the members' rows > l, then
@@ -1602,9 +1623,12 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
       CK(h->oscr.ensure(osz));
       CK(cudaMemsetAsync(h->oscr.p, 0, osz, st));
     }
+    zc = fused && !victim && !slot_pri && !request_eam && !n_slots && ncand > 0 && zc_ok();
+    if (zc) CK(h->cpin.ensure(ncand * sizeof(moe_candidate)));
     CK(moe::launch_prefetch_order(agg, L, E, current_layer, filter,
-                                  h->keys.as<unsigned long long>(), dn,
-                                  h->cand.as<moe_candidate>(), h->n_sm, st, h->oscr.p));
+                                  h->keys.as<unsigned long long>(), zc ? dn_host : dn,
+                                  zc ? h->cpin.as<moe_candidate>() : h->cand.as<moe_candidate>(),
+                                  h->n_sm, st, h->oscr.p));
   } else {
     CK(cudaMemsetAsync(h->small.p, 0, 8, st));  // no probe: nothing to width-check
   }
@@ -1628,6 +1652,14 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
   if (victim || slot_pri)
     CK(moe::launch_decide(agg, L, E, current_layer, filter, 0, req, dslots, n_slots, nullptr,
                           nullptr, victim ? dv : nullptr, dpri, st));
+  if (zc) {
+    CK(cudaStreamSynchronize(st));
+    const uint32_t n = *reinterpret_cast<volatile uint32_t*>(dn_host);
+    if (n_out) *n_out = n;
+    if (n && out && cap)
+      std::memcpy(out, h->cpin.p, std::min<uint64_t>(n, cap) * sizeof(moe_candidate));
+    return MOE_OK;
+  }
   CK(cudaMemcpyAsync(h->pin.p, h->small.p, 256, cudaMemcpyDeviceToHost, st));
   // speculative copy of the head of the order with the status words: one
   // round trip for the usual (floor-filtered, short) answer
