@@ -19,9 +19,10 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma.cta_group::1.kind::f16
 //               issuer (M=128, N=256, K=16), double-buffered fp32 accumulators
 //               (2 x 256 TMEM columns), tcgen05.commit -> mbarriers
-//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 (thread = probe row), screen
-//               distance, row min -> global per-probe threshold (atomicMin),
-//               candidate push into the per-probe bucket
+//   warps 2-17  epilogue (EPI_WARPS = 16: four warps per TMEM lane quarter,
+//               64 accumulator columns each): tcgen05.ld 32x32b.x32 (thread =
+//               probe row), screen distance, row min -> global per-probe
+//               threshold (atomicMin), candidate push into the per-probe bucket
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -42,8 +43,16 @@ constexpr uint32_t A_BYTES = BM * BK * 2;  // 16 KB
 constexpr uint32_t B_BYTES = BN * BK * 2;  // 32 KB
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
-constexpr int THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
-constexpr uint32_t EPI_THREADS = 256;
+#ifndef MOE_EPI_WARPS
+#define MOE_EPI_WARPS 16
+#endif
+constexpr int EPI_WARPS = MOE_EPI_WARPS;  // 16: 64 columns per warp (measured best; 8: 128, 4: 256)
+constexpr int THREADS = 64 + 32 * EPI_WARPS;  // warp 0 TMA, warp 1 MMA, then the epilogue
+constexpr uint32_t EPI_THREADS = 32 * EPI_WARPS;
+// epilogue column split: EPI_PARTS warps per TMEM lane quarter, EPI_CH
+// 32-column chunks per warp and call
+constexpr uint32_t EPI_PARTS = EPI_WARPS >= 8 ? EPI_WARPS / 4 : 2;
+constexpr uint32_t EPI_CH = 8 / EPI_PARTS;
 
 struct TcArgs {
   float invL;          // 1/L (fp32)
@@ -162,10 +171,10 @@ __device__ __forceinline__ void epilogue_half(uint32_t tcol, uint32_t col0, uint
                                               const uint64_t* zt, uint32_t q, bool qvalid,
                                               uint32_t p0, const TcArgs& a, float invL) {
   uint32_t r[32];
-  const bool full_tile = p0 + col0 + 128 <= a.P;
+  const bool full_tile = p0 + col0 + 32 * EPI_CH <= a.P;
   if (a.dmat) {  // matrix mode (blocked construction replay): store, no threshold
 #pragma unroll 1
-    for (uint32_t c = 0; c < 4; ++c) {
+    for (uint32_t c = 0; c < EPI_CH; ++c) {
       tmem_ld32(tcol + c * 32, r);
       if (!qvalid) continue;
       float* o = a.dmat + (uint64_t)q * a.ldd + p0 + col0 + c * 32;
@@ -199,7 +208,7 @@ __device__ __forceinline__ void epilogue_half(uint32_t tcol, uint32_t col0, uint
   float d1 = __uint_as_float(kFInf), d2 = d1;
   uint32_t c1 = 0;
 #pragma unroll 1
-  for (uint32_t c = 0; c < 4; ++c) {
+  for (uint32_t c = 0; c < EPI_CH; ++c) {
     tmem_ld32(tcol + c * 32, r);
     if (fast) {
 #pragma unroll
@@ -244,7 +253,7 @@ __device__ __forceinline__ void epilogue_half(uint32_t tcol, uint32_t col0, uint
   // whole warp whenever any of its rows has two or more candidates
   if (!__any_sync(0xffffffffu, multi)) return;
 #pragma unroll 1
-  for (uint32_t c = 0; c < 4; ++c) {
+  for (uint32_t c = 0; c < EPI_CH; ++c) {
     tmem_ld32(tcol + c * 32, r);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {  // rare pass: a branch per column is fine here
@@ -351,7 +360,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // epilogue: 8 warps; warp w serves TMEM lane quarter w%4 (probe rows) and
     // column half (w-2)/4 of the 256-column accumulator
     const uint32_t quarter = warp & 3;
-    const uint32_t half = (warp - 2) >> 2;
+    const uint32_t half0 = EPI_WARPS >= 8 ? (warp - 2) >> 2 : 0;
     const uint32_t row = quarter * 32 + lane;
     const uint32_t et = threadIdx.x - 64;  // 0..255
     uint32_t i = 0;
@@ -360,17 +369,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t m = t % a.n_m, n = t / a.n_m;
       uint64_t* zt = zp_s + acc * BN;
       {
-        const uint32_t p = n * BN + et;
-        zt[et] = p < a.P ? a.zp[p] : 0ull;
+        for (uint32_t j = et; j < BN; j += EPI_THREADS) {
+          const uint32_t p = n * BN + j;
+          zt[j] = p < a.P ? a.zp[p] : 0ull;
+        }
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
       const uint32_t q = m * BM + row;
       const bool qvalid = q < a.Q;
       const uint64_t zq = qvalid ? a.zq[q] : 0ull;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
-      const uint32_t tcol = tmem + ((quarter * 32) << 16) + acc * BN + half * 128;
-      epilogue_half(tcol, half * 128, zq, zt, q, qvalid, n * BN, a, a.invL);
+      for (uint32_t half = half0; half < half0 + (EPI_WARPS >= 8 ? 1u : 2u); ++half) {
+        const uint32_t col0 = half * 32 * EPI_CH;
+        const uint32_t tcol = tmem + ((quarter * 32) << 16) + acc * BN + col0;
+        epilogue_half(tcol, col0, zq, zt, q, qvalid, n * BN, a, a.invL);
+      }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -534,7 +548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // epilogue: 8 warps; warp w serves TMEM lane quarter w%4 (probe rows) and
     // column half (w-2)/4 of the 256-column accumulator
     const uint32_t quarter = warp & 3;
-    const uint32_t half = (warp - 2) >> 2;
+    const uint32_t half0 = EPI_WARPS >= 8 ? (warp - 2) >> 2 : 0;
     const uint32_t row = quarter * 32 + lane;
     const uint32_t et = threadIdx.x - 64;  // 0..255
     uint32_t i = 0;
@@ -543,17 +557,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const uint32_t m = t % a.n_m, n = t / a.n_m;
       uint64_t* zt = zp_s + acc * BN;
       {
-        const uint32_t p = n * BN + et;
-        zt[et] = p < a.P ? a.zp[p] : 0ull;
+        for (uint32_t j = et; j < BN; j += EPI_THREADS) {
+          const uint32_t p = n * BN + j;
+          zt[j] = p < a.P ? a.zp[p] : 0ull;
+        }
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
       const uint32_t q = m * 256 + rank * 128 + row;
       const bool qvalid = q < a.Q;
       const uint64_t zq = qvalid ? a.zq[q] : 0ull;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
-      const uint32_t tcol = tmem + ((quarter * 32) << 16) + acc * BN + half * 128;
-      epilogue_half(tcol, half * 128, zq, zt, q, qvalid, n * BN, a, a.invL);
+      for (uint32_t half = half0; half < half0 + (EPI_WARPS >= 8 ? 1u : 2u); ++half) {
+        const uint32_t col0 = half * 32 * EPI_CH;
+        const uint32_t tcol = tmem + ((quarter * 32) << 16) + acc * BN + col0;
+        epilogue_half(tcol, col0, zq, zt, q, qvalid, n * BN, a, a.invL);
+      }
       tc_fence_before();
       mbar_arrive_leader(&tempty[acc]);
     }
