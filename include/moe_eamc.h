@@ -17,7 +17,11 @@
  *    synchronous.  `_device` variants take device pointers and a
  *    cudaStream_t (passed as void*) and are stream-ordered.
  *  - Threading: one handle per writer.  match/match_within/prefetch are
- *    const readers (eam.hpp:89-94); insert needs exclusivity.
+ *    const readers (eam.hpp:89-94) and may be called from
+ *    several host threads on one handle: the host entry points of a handle
+ *    serialise on its lock (they share its scratch and staging memory).
+ *    `_device` calls on one handle must be ordered on one stream (they share
+ *    device scratch); insert needs exclusivity.
  *  - Errors: the status code, plus a thread-local message from
  *    moe_last_error().
  */

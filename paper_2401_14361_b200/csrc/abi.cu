@@ -119,6 +119,15 @@ moe_status device_ok(int device, int* n_sm) {
   return MOE_OK;
 }
 
+// Lock of a (possibly null) handle for the duration of an entry point.
+struct HandleLock {
+  std::recursive_mutex* m = nullptr;
+  explicit HandleLock(const moe_eamc* h);
+  ~HandleLock() {
+    if (m) m->unlock();
+  }
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int d) {
@@ -146,6 +155,11 @@ uint32_t row_bytes(uint32_t E, int cb) { return (E * cb + 15) / 16 * 16; }
 }  // namespace
 
 struct moe_eamc {
+  // Serialises the host entry points on one handle: the "const reader" calls
+  // (match, match_within, prefetch, ...) share the handle's scratch buffers
+  // and staging memory, so concurrent readers take turns (recursive: some
+  // entry points forward to others).
+  std::recursive_mutex mu;
   int device = 0;
   int n_sm = 148;
   moe_shape shape{};
@@ -207,6 +221,13 @@ struct moe_eamc {
     if (st) cudaStreamDestroy(st);
   }
 };
+
+HandleLock::HandleLock(const moe_eamc* h) {
+  if (h) {
+    m = &const_cast<moe_eamc*>(h)->mu;
+    m->lock();
+  }
+}
 
 namespace {
 
@@ -921,6 +942,7 @@ moe_status moe_eamc_info(const moe_eamc* h, moe_shape* shape, int* phase, uint64
 }
 
 moe_status moe_eamc_entry(const moe_eamc* hc, uint64_t index, uint64_t* counts, uint64_t* seq) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
   if (index >= h->c.size) return fail(MOE_ERR_OUT_OF_RANGE, "entry index out of range");
@@ -930,6 +952,7 @@ moe_status moe_eamc_entry(const moe_eamc* hc, uint64_t index, uint64_t* counts, 
 
 moe_status moe_eamc_insert(moe_eamc* h, const uint64_t* counts, moe_eam_kind kind,
                            moe_phase phase, int64_t* evicted_slot, uint64_t* evicted_counts) {
+  HandleLock hl_(h);
   if (!h || !counts) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   // Eamc::insert validation order (eam.cpp:153-158)
   if (kind != MOE_KIND_REQUEST)
@@ -989,6 +1012,7 @@ static moe_status upload_host_counts(moe_eamc* h, const uint64_t* src, uint64_t 
 
 moe_status moe_eamc_build(moe_eamc* h, const uint64_t* counts, uint64_t n,
                           int64_t* evicted_slots) {
+  HandleLock hl_(h);
   if (!h || (!counts && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   DeviceGuard dg(h->device);
   const uint64_t cells = (uint64_t)h->c.L * h->c.E;
@@ -1034,6 +1058,7 @@ static moe_status append_impl(moe_eamc* h, const void* counts, int cbytes, const
 }
 
 moe_status moe_eamc_append(moe_eamc* h, const uint64_t* counts, const uint64_t* seqs, uint64_t n) {
+  HandleLock hl_(h);
   if (!h || ((!counts || !seqs) && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   DeviceGuard dg(h->device);
   return append_impl(h, counts, 8, seqs, n);
@@ -1041,6 +1066,7 @@ moe_status moe_eamc_append(moe_eamc* h, const uint64_t* counts, const uint64_t* 
 
 moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_bytes,
                                   const uint64_t* seqs, uint64_t n) {
+  HandleLock hl_(h);
   if (!h || ((!counts || !seqs) && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (count_bytes != 1 && count_bytes != 2 && count_bytes != 8)
     return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 1, 2 or 8");
@@ -1175,6 +1201,7 @@ static moe_status match_host_packed(moe_eamc* h, const uint64_t* probes, uint64_
 
 moe_status moe_eamc_match(const moe_eamc* hc, const uint64_t* probes, uint64_t n_probes,
                           moe_match* out, uint8_t* found) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || ((!probes || !out) && n_probes)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (n_probes == 0) return MOE_OK;
@@ -1262,6 +1289,7 @@ moe_status moe_eamc_match(const moe_eamc* hc, const uint64_t* probes, uint64_t n
 
 moe_status moe_eamc_match_device(const moe_eamc* hc, const void* probes, int probe_bytes,
                                  uint64_t n_probes, moe_match* out, void* stream) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || ((!probes || !out) && n_probes)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (probe_bytes != 1 && probe_bytes != 2 && probe_bytes != 8)
@@ -1280,6 +1308,7 @@ moe_status moe_eamc_match_device(const moe_eamc* hc, const void* probes, int pro
 // the matching pipeline in synchronous mode (width check; widening redo), D2H.
 moe_status moe_eamc_match_packed(const moe_eamc* hc, const void* probes, int probe_bytes,
                                  uint64_t n_probes, moe_match* out, uint8_t* found) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || ((!probes || !out) && n_probes)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (probe_bytes == 8)
@@ -1305,6 +1334,7 @@ moe_status moe_eamc_match_packed(const moe_eamc* hc, const void* probes, int pro
 
 moe_status moe_eamc_match_within(const moe_eamc* hc, const uint64_t* probe, double window,
                                  moe_match* out, uint64_t cap, uint64_t* n_out) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !probe || !n_out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   *n_out = 0;
@@ -1367,6 +1397,7 @@ moe_status moe_match_merge_device(const moe_match* parts, uint64_t n_parts, uint
 }
 
 moe_status moe_eamc_clone(const moe_eamc* hc, moe_eamc** out) {
+  HandleLock hl_(hc);
   moe_eamc* src = const_cast<moe_eamc*>(hc);
   if (!src || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   DeviceGuard dg(src->device);
@@ -1390,12 +1421,14 @@ moe_status moe_eamc_clone(const moe_eamc* hc, moe_eamc** out) {
 }
 
 moe_status moe_eamc_set_index_base(moe_eamc* h, uint64_t base) {
+  HandleLock hl_(h);
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
   h->c.index_base = base;
   return MOE_OK;
 }
 
 moe_status moe_eamc_set_profiling(moe_eamc* h, int enable) {
+  HandleLock hl_(h);
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
   DeviceGuard dg(h->device);
   if (h->ring.empty()) {
@@ -1413,6 +1446,7 @@ moe_status moe_eamc_set_profiling(moe_eamc* h, int enable) {
 }
 
 moe_status moe_eamc_kernel_times(const moe_eamc* hc, double* ms, uint64_t* calls) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
   DeviceGuard dg(h->device);
@@ -1695,6 +1729,7 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
 moe_status moe_prefetch_priorities(const moe_eamc* hc, const uint64_t* cur_eam,
                                    uint32_t current_layer, int apply_floor_filter,
                                    moe_candidate* out, uint64_t cap, uint64_t* n_out) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !cur_eam || !n_out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   // policy.cpp:91-93
@@ -1718,6 +1753,7 @@ moe_status moe_prefetch_priorities(const moe_eamc* hc, const uint64_t* cur_eam,
 
 moe_status moe_eamc_window_min_device(const moe_eamc* hc, const uint64_t* cur_eam,
                                       uint64_t* d_min_bits, void* stream) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !cur_eam || !d_min_bits) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   DeviceGuard dg(h->device);
@@ -1746,6 +1782,7 @@ moe_status moe_eamc_window_min_device(const moe_eamc* hc, const uint64_t* cur_ea
 moe_status moe_eamc_window_aggregate_device(const moe_eamc* hc, uint32_t current_layer,
                                             double window, const uint64_t* d_min_bits,
                                             uint64_t* agg, void* stream) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !d_min_bits || !agg) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (current_layer >= h->shape.n_layers)
@@ -1767,6 +1804,7 @@ moe_status moe_eamc_window_aggregate_device(const moe_eamc* hc, uint32_t current
 moe_status moe_eamc_prefetch_order_device(const moe_eamc* hc, const uint64_t* agg,
                                           uint32_t current_layer, int apply_floor_filter,
                                           moe_candidate* out, uint32_t* n_out, void* stream) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !agg || !out || !n_out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   const uint32_t L = h->shape.n_layers, E = h->shape.n_experts_per_layer;
@@ -1791,6 +1829,7 @@ moe_status moe_eamc_prefetch_order_device(const moe_eamc* hc, const uint64_t* ag
 moe_status moe_decide(const moe_eamc* hc, const uint64_t* cur_eam, uint32_t current_layer,
                       const uint64_t* request_eam, const moe_slot_view* slots, uint64_t n_slots,
                       moe_candidate* out, uint64_t cap, uint64_t* n_out, int64_t* victim) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !cur_eam || !request_eam || (!slots && n_slots))
     return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
@@ -2030,6 +2069,7 @@ moe_status moe_traces_request_eams(const char* path, const moe_shape* shape, moe
 }
 
 moe_status moe_eamc_build_from_traces(moe_eamc* h, const char* path, uint64_t* n_inserted) {
+  HandleLock hl_(h);
   if (!h || !path) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   std::vector<uint64_t> c;
   uint64_t n = 0;
@@ -2053,6 +2093,7 @@ moe_status moe_eamc_capacity_bound(const moe_shape* shape, double similarity, ui
 }
 
 moe_status moe_eamc_save(const moe_eamc* hc, const char* path) {
+  HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !path) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   DeviceGuard dg(h->device);

@@ -811,3 +811,32 @@ def test_prefetch_small_collection(m, orc, L, E, P, mult):
             assert np.array_equal(out["layer_idx"], ol)
             assert np.array_equal(out["expert_idx"], ox)
             assert np.array_equal(out["priority"], op)
+
+
+def test_concurrent_readers_one_handle(m, orc):
+    """match / prefetch are const readers (eam.hpp:89-94): concurrent calls on
+    one handle from several host threads give the serial results."""
+    from concurrent.futures import ThreadPoolExecutor
+    L, E, P = 12, 32, 400
+    fam = m.gen_bench_family(23, L, E, P + 64)
+    e = filled(m, L, E, fam[:P])
+    want = e.match_batch(fam[P:])
+    s = m.ModelShape(L, E, 1)
+    probes = [np.ascontiguousarray(fam[P + i]) for i in range(8)]
+    for i, pr in enumerate(probes):
+        pr[i % (L - 1) + 1:] = 0
+    want_pf = [m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), e, i % (L - 1), True)
+               for i, pr in enumerate(probes)]
+
+    def work(k):
+        ok = True
+        for _ in range(5):
+            ok &= bool(np.array_equal(e.match_batch(fam[P:]), want))
+            i = k % len(probes)
+            got = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=probes[i]), e,
+                                   i % (L - 1), True)
+            ok &= bool(np.array_equal(got, want_pf[i]))
+        return ok
+
+    with ThreadPoolExecutor(4) as ex:
+        assert all(ex.map(work, range(8)))
