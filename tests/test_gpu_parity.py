@@ -822,7 +822,7 @@ def test_concurrent_readers_one_handle(m, orc):
     e = filled(m, L, E, fam[:P])
     want = e.match_batch(fam[P:])
     s = m.ModelShape(L, E, 1)
-    probes = [np.ascontiguousarray(fam[P + i]) for i in range(8)]
+    probes = [fam[P + i].copy() for i in range(8)]  # copies: fam itself is matched too
     for i, pr in enumerate(probes):
         pr[i % (L - 1) + 1:] = 0
     want_pf = [m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), e, i % (L - 1), True)
