@@ -840,3 +840,25 @@ def test_concurrent_readers_one_handle(m, orc):
 
     with ThreadPoolExecutor(4) as ex:
         assert all(ex.map(work, range(8)))
+
+
+@pytest.mark.parametrize("E,offset", [(40, 0), (128, 16), (128, 4)])
+def test_match_device_u8_layouts(m, orc, E, offset):
+    """Device u8 probes: rows narrower than the storage row (E % 16 != 0: a
+    packed copy is made), and base pointers at 16- and 4-byte offsets (only a
+    16-byte aligned batch in the storage layout is used in place)."""
+    import ctypes as C
+    import torch
+    from paper_2401_14361_b200 import _lib
+    L, P, Q = 6, 700, 40
+    fam = m.gen_bench_family(41, L, E, P + Q)
+    e = filled(m, L, E, fam[:P])
+    flat = torch.zeros(offset + Q * L * E, dtype=torch.uint8, device="cuda")
+    flat[offset:] = torch.from_numpy(fam[P:].astype(np.uint8).reshape(-1)).cuda()
+    out = torch.zeros((Q, 3), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib.moe_eamc_match_device(e._h, flat.data_ptr() + offset, 1, Q,
+                                              out.data_ptr(), None))
+    torch.cuda.synchronize()
+    res = out.cpu().numpy().view(np.uint8).reshape(Q, 24).copy().view(_lib.MATCH_DTYPE)[:, 0]
+    idx, seq, d, _ = orc.match(fam[:P], seqs_of(P), fam[P:])
+    assert np.array_equal(res["index"], idx) and np.array_equal(res["distance"], d)
