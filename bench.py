@@ -1,14 +1,22 @@
 #!/usr/bin/env python
 """bench.py -- EAM-vs-EAMC distance evals/s on B200 (BASELINE.json `metric`).
 
-Default workload (BASELINE.json configs[1], "SW"): Switch-Transformers-base-128
-shape (L=12, E=128, top-1), an EAMC of P=10,000 entries per GPU matched
-against a 4,096-probe batch.  Inputs are the reference benchmark's own
-synthetic EAM family (bench.cpp:44-54, seed 55): the first P*N EAMs of the
-stream are the collection (rank r owns [r*P, (r+1)*P)), the next Q are the
-probes.  A step = one Eamc::match pass of the probe batch over the whole
-collection; at N>1 the collection is P-sharded and the per-shard argmins are
-merged over NCCL (all_gather + device lexicographic merge): weak scaling.
+Headline workload (BASELINE.json configs[4], "SC", the configuration the
+metric is quoted on): Switch-base-128 shape (L=12, E=128; SURVEY 8 fixes SC's
+unstated shape to the reference benchmark's 12x128), an EAMC of P = 2^20
+entries matched against a 65,536-probe batch.  Inputs are the reference
+benchmark's own synthetic EAM family (bench.cpp:44-54, seed 55): the first P
+EAMs of the stream are the collection, the next 65,536 the probes.  A step =
+one Eamc::match pass of the probe batch over the whole collection
+(eam.cpp:118-129 per probe).  At N > 1 the collection is P-sharded (rank r
+owns slots [r*P/N, (r+1)*P/N)), the probes are replicated and the per-shard
+argmins are merged over NCCL (all_gather + device lexicographic merge):
+total work fixed, i.e. strong scaling.
+
+The line also carries the SC streaming regime (same collection, Q = 8: the
+HBM-bound case the north star's ">= 60% of HBM roofline at P >= 1M" is about)
+as `roofline_streaming`, and the other SURVEY 8 rows under `rows` (SW, DS, NL,
+tracing, MIX), each with the reference CPU path timed beside it.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
@@ -34,10 +42,26 @@ sys.path.insert(0, ROOT)
 
 METRIC = "EAM-vs-EAMC distance evals/sec + % HBM roofline at 1/2/4/8 B200"
 L, E, TOPK = 12, 128, 1
-P_PER_GPU, Q = 10_000, 4096
 SEED = 55
-STREAM_P, STREAM_Q = 1 << 20, 8   # SC streaming regime (P >= 1M), north-star HBM target
-BATCH_Q = 65536                  # SC batch regime (BASELINE configs[4]: 65k-query batch)
+SC_P, SC_Q = 1 << 20, 65536      # BASELINE configs[4]: P = 1M (2^20), 65k-query batch
+STREAM_Q = 8                     # SC streaming regime (HBM-bound), same collection
+SW_P, SW_Q = 10_000, 4096        # BASELINE configs[1] (a row now)
+CPU_SAMPLE_Q = 64                # reference probes timed / parity-checked at SC
+
+
+def sc_config(N):
+    """The `config` of both arms (identical dicts, so the driver can compare)."""
+    return {
+        "workload": (f"SC (BASELINE configs[4]): P={SC_P} EAMs (L={L} E={E}, Switch-base-128 "
+                     f"shape) sharded P/N over N={N} GPU(s), Q={SC_Q}-probe batch, "
+                     "Eamc::match per probe"),
+        "L": L, "E": E, "P_total": SC_P, "P_per_gpu": SC_P // N, "Q": SC_Q, "seed": SEED,
+        "count_bytes": 1,
+        "l2": ("inputs larger than L2 (1.61 GB u8 collection + 3.2 GB fp16 operand copy per "
+               "pass) and a 256 MiB L2 flush between timed steps, outside the events"),
+        "parallelism": (f"P-sharded x{N}, NCCL all_gather + device lexicographic merge"
+                        if N > 1 else "single GPU"),
+    }
 
 
 def dist_env():
@@ -111,6 +135,28 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- ours
+def _events_timed(torch, stream, steps, step_fn, pre=None):
+    """K device-timed steps on `stream` (CUDA events around each step)."""
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for i in range(steps):
+        if pre is not None:
+            pre()
+        evs[i][0].record(stream)
+        step_fn()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def _as_matches(t):
+    """device/host moe_match[Q] tensor (Q x 3 f64 words) -> structured numpy."""
+    from paper_2401_14361_b200 import _lib
+    a = t.cpu().numpy() if hasattr(t, "cpu") else t
+    return np.ascontiguousarray(a).view(np.uint8).reshape(-1, 24).copy().view(
+        _lib.MATCH_DTYPE)[:, 0]
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -136,183 +182,153 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- collection shard + probes (host-generated, reference bench stream)
-    P = P_PER_GPU
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if N > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- SC collection shard (P/N entries per rank) + the replicated probe batch
+    P = SC_P // N
     shard = m.gen_bench_family(SEED, L, E, P, skip=rank * P, dtype=np.uint8)
-    probes_u8 = m.gen_bench_family(SEED, L, E, Q, skip=N * P, dtype=np.uint8)
     eamc = m.Eamc(m.ModelShape(L, E, TOPK), m.Phase.decode, P, device=local)
     eamc.append(shard, np.arange(rank * P, (rank + 1) * P, dtype=np.uint64))
+    del shard
     _lib.check(_lib.lib.moe_eamc_set_index_base(eamc._h, rank * P))
-
+    probes_u8 = m.gen_bench_family(SEED, L, E, SC_Q, skip=SC_P, dtype=np.uint8)
     d_probes = torch.from_numpy(probes_u8).to(dev)
-    d_out = torch.empty((Q, 3), dtype=torch.float64, device=dev)      # moe_match[Q]
-    d_parts = torch.empty((N * Q, 3), dtype=torch.float64, device=dev)
-    d_final = torch.empty((Q, 3), dtype=torch.float64, device=dev)
+    d_out = torch.empty((SC_Q, 3), dtype=torch.float64, device=dev)      # moe_match[Q]
+    d_parts = torch.empty((N * SC_Q, 3), dtype=torch.float64, device=dev)
+    d_final = torch.empty((SC_Q, 3), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step_device():
-        _lib.check(_lib.lib.moe_eamc_match_device(eamc._h, d_probes.data_ptr(), 1, Q,
+        _lib.check(_lib.lib.moe_eamc_match_device(eamc._h, d_probes.data_ptr(), 1, SC_Q,
                                                   d_out.data_ptr(), sp))
         if N > 1:
             dist.all_gather_into_tensor(d_parts, d_out)
-            _lib.check(_lib.lib.moe_match_merge_device(d_parts.data_ptr(), N, Q,
+            _lib.check(_lib.lib.moe_match_merge_device(d_parts.data_ptr(), N, SC_Q,
                                                        d_final.data_ptr(), sp))
             return d_final
         return d_out
 
-    # warmup
     for _ in range(args.warmup):
         step_device()
     barrier()
 
     # ---- timed region: K steps, L2 flushed between steps (outside the events)
-    def timed(profile):
-        if profile:
-            _lib.check(_lib.lib.moe_eamc_set_profiling(eamc._h, 1))
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        barrier()
-        for i in range(args.steps):
-            flush.zero_()
-            evs[i][0].record(stream)
-            step_device()
-            evs[i][1].record(stream)
-        barrier()
-        return [a.elapsed_time(b) for a, b in evs]
-
     clocks = ClockSampler(local)
     time.sleep(0.05)
-    ms_steps = timed(False)
+    barrier()
+    ms_steps = _events_timed(torch, stream, args.steps, step_device, pre=flush.zero_)
+    barrier()
     clk = clocks.stop()
     # Per-kernel times come from a second, identical pass with the library's
     # per-kernel events on: events between the kernels break the programmatic
     # dependent launch overlap, so that pass is not the one `value` is timed on.
-    ms_prof = timed(True)
+    _lib.check(_lib.lib.moe_eamc_set_profiling(eamc._h, 1))
+    barrier()
+    ms_prof = _events_timed(torch, stream, args.steps, step_device, pre=flush.zero_)
     kms = (C.c_double * 3)()
     kcalls = (C.c_uint64 * 3)()
     _lib.check(_lib.lib.moe_eamc_kernel_times(eamc._h, kms, kcalls))
     _lib.check(_lib.lib.moe_eamc_set_profiling(eamc._h, 0))
-    t_total = torch.tensor([sum(ms_steps)], dtype=torch.float64, device=dev)
-    if N > 1:
-        dist.all_reduce(t_total, op=dist.ReduceOp.MAX)
-    t_ms = float(t_total.item())
-    evals_per_step = P * N * Q
+    t_ms = max_over_ranks(sum(ms_steps))
+    evals_per_step = SC_P * SC_Q
     value = evals_per_step * args.steps / (t_ms / 1e3)
     # per step: k_prep_u8, k_tc2_screen, k_refine, and the device-gated exact
     # pass k_match<1,1,1> + k_merge_partials (launched every step, exit at once
     # unless a candidate bucket overflowed); + k_merge for N > 1
     gpu_launches = args.steps * (5 + (1 if N > 1 else 0))
+    res = _as_matches(step_device())  # the result of a timed-config step (parity sample)
 
-    # result of the last step, for the parity sample
-    res = step_device().cpu().numpy().view(np.uint8).reshape(Q, 24).copy().view(
-        _lib.MATCH_DTYPE)[:, 0]
-
-    # ---- roofline of the dominant kernel (screen pass), live CUDA events
+    # ---- roofline of the dominant kernel (the screen), live CUDA events
     hbm_peak, tf_peak, peak_kind = load_peaks()
     screen_ms = kms[1] / max(kcalls[1], 1)
-    ops_alg = 2.0 * L * E * P * Q
-    bytes_alg = P * L * E * 1 + Q * L * E * 1 + 24 * Q
+    ops_alg = 2.0 * L * E * P * SC_Q
+    bytes_alg = P * L * E * 1 + SC_Q * L * E * 1 + 24 * SC_Q
+    ach = ops_alg / (screen_ms / 1e3) / 1e12
     roofline = {
         "bound": "tensor",
         "kernel": "k_tc2_screen (tcgen05.mma.cta_group::2 kind::f16, 256x256 tiles, screen pass)",
-        "achieved": ops_alg / (screen_ms / 1e3) / 1e12, "peak": tf_peak, "unit": "TFLOP/s",
-        "frac": ops_alg / (screen_ms / 1e3) / 1e12 / tf_peak,
-        "traffic": ncu_traffic("sw_screen"),
+        "achieved": ach, "peak": tf_peak, "unit": "TFLOP/s", "frac": ach / tf_peak,
+        "traffic": ncu_traffic("sc_batch_screen"),
         "alg_ops_per_launch": ops_alg, "alg_bytes_per_launch": bytes_alg,
         "launch_ms": screen_ms,
         "share_of_step": screen_ms / (sum(ms_prof) / args.steps),
+        "frac_of_nominal_2250": ach / 2250.0,
         "kernel_times": "per-kernel CUDA events on the launching stream, from a profiled pass of "
                         "the same K steps (ms_per_step_profiled)",
-        "note": (f"peak = {peak_kind} dense bf16 (MEASURED_PEAKS.json); ops = 2*L*E*P*Q "
-                 "(SURVEY.md 8d), executed as one fp16 tensor-core GEMM over unit-normalised "
-                 "rows (K=L*E), fp32 accumulate in TMEM; the operands are the fp16 copies "
-                 "(2 B/count), so ncu traffic is ~2x the u8 algorithmic bytes. HBM view: "
-                 f"{bytes_alg / (screen_ms / 1e3) / 1e9:.1f} GB/s of {hbm_peak:.0f}"),
+        "note": (f"peak = {peak_kind} dense bf16 cuBLAS burst (MEASURED_PEAKS.json); ops = "
+                 "2*L*E*P*Q (SURVEY.md 8d), executed as one fp16 tensor-core GEMM over "
+                 "unit-normalised rows (K=L*E), fp32 accumulate in TMEM, exact integer/fp64 "
+                 "refine of the survivors; the 65k batch is compute-bound by construction "
+                 f"(HBM view: {bytes_alg / (screen_ms / 1e3) / 1e9:.1f} GB/s of {hbm_peak:.0f})"),
     }
 
-    # ---- e2e: public host API, pinned u64 probes in, results out, every step
-    import torch as _t
-    h_probes = _t.from_numpy(probes_u8.astype(np.uint64)).pin_memory()
-    h_out = np.zeros(Q, _lib.MATCH_DTYPE)
-    h_parts = _t.empty((N * Q, 3), dtype=_t.float64, device=dev)
+    # ---- e2e: the reference-facing C ABI call with HOST u64 probes (the
+    # reference's Eam storage, eam.hpp:55) in pinned memory and host results
+    # out, every step (host narrowing, H2D, matching, D2H inside the call)
+    h_probes = torch.from_numpy(probes_u8.astype(np.uint64)).pin_memory()
+    h_out = np.zeros(SC_Q, _lib.MATCH_DTYPE)
+    h_parts = torch.empty((N * SC_Q, 3), dtype=torch.float64, device=dev)
 
     def step_e2e():
-        _lib.check(_lib.lib.moe_eamc_match(eamc._h, h_probes.data_ptr(), Q, h_out.ctypes.data,
+        _lib.check(_lib.lib.moe_eamc_match(eamc._h, h_probes.data_ptr(), SC_Q, h_out.ctypes.data,
                                            None))
         if N > 1:
-            mine = _t.from_numpy(h_out.view(np.float64).reshape(Q, 3)).to(dev)
+            mine = torch.from_numpy(h_out.view(np.float64).reshape(SC_Q, 3)).to(dev)
             dist.all_gather_into_tensor(h_parts, mine)
-            _lib.check(_lib.lib.moe_match_merge_device(h_parts.data_ptr(), N, Q,
+            _lib.check(_lib.lib.moe_match_merge_device(h_parts.data_ptr(), N, SC_Q,
                                                        d_final.data_ptr(), sp))
-            return d_final.cpu()
+            return _as_matches(d_final)
         return h_out
 
-    for _ in range(min(args.warmup, 3)):
+    for _ in range(2):
         step_e2e()
     barrier()
-    e2e_steps = max(3, min(args.steps, 50))
+    e2e_steps = max(3, min(args.steps, 8))
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        step_e2e()
-    if N > 1:
-        dist.barrier()
-    t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-    if N > 1:
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_val = evals_per_step * e2e_steps / float(t_e2e.item())
-
-    # the same through moe_eamc_match_packed: host probes already narrow (u8,
-    # as traced counts of this workload are), 6.3 MB per step instead of 50 MB
-    h_probes8 = _t.from_numpy(probes_u8).pin_memory()
-
-    def step_e2e_packed():
-        _lib.check(_lib.lib.moe_eamc_match_packed(eamc._h, h_probes8.data_ptr(), 1, Q,
-                                                  h_out.ctypes.data, None))
-
-    for _ in range(min(args.warmup, 3)):
-        step_e2e_packed()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        step_e2e_packed()
-    e2e_packed_val = P * Q * e2e_steps / (time.perf_counter() - t0)
+        got_e2e = step_e2e()
+    barrier()
+    t_e2e = max_over_ranks(time.perf_counter() - t0)
+    e2e_val = evals_per_step * e2e_steps / t_e2e
+    e2e_same = bool(np.array_equal(got_e2e, res)) if N == 1 else None
     host_threads = int(_lib.lib.moe_host_threads())
+    del h_probes
 
-    # ---- the other SURVEY 8 rows (prefetch decisions, construction, tracing, MIX)
-    rows = None
-    if N == 1 and not args.no_rows:
-        rows = run_rows(args, m, _lib, torch, dev, sp, stream)
-
-    # ---- streaming regime (north-star target: >= 60% HBM roofline at P >= 1M)
+    # ---- SC streaming regime (north-star target: >= 60% HBM roofline at P >= 1M)
     streaming = None
     if not args.no_streaming:
-        streaming = run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak,
-                                  peak_kind)
+        streaming = run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, eamc,
+                                  hbm_peak, peak_kind)
+
+    # ---- the other SURVEY 8 rows (SW, prefetch decisions, construction, tracing, MIX)
+    rows = None
+    if N == 1 and not args.no_rows:
+        del eamc  # free the SC collection before the rows allocate theirs
+        torch.cuda.empty_cache()
+        rows = run_rows(args, m, _lib, torch, dev, sp, stream, flush)
 
     out = None
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": N,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic: reference bench family F1 (bench.cpp:44-54, seed 55)",
-            "config": {
-                "workload": (f"SW (BASELINE configs[1]): Switch-base-128 shape L={L} E={E} "
-                             f"top-{TOPK}, EAMC P={P} per GPU (P_total={P * N}), Q={Q} probes"),
-                "L": L, "E": E, "P_per_gpu": P, "P_total": P * N, "Q": Q, "count_bytes": 1,
-                "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                "parallelism": (f"P-sharded x{N}, NCCL all_gather + device lexicographic merge"
-                                if N > 1 else "single GPU"),
-            },
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": ("synthetic: reference bench family F1 (bench.cpp:44-54, seed 55); u8 is the "
+                     "count storage width (counts 1..32, lossless), distances are exact fp64"),
+            "config": sc_config(N),
             "roofline": roofline,
             "e2e": {"value": e2e_val, "unit": "evals/s", "steps": e2e_steps,
-                    "api": ("moe_eamc_match (host u64 probes, pinned) + D2H results; u64 "
-                            f"narrowed to u8 on {host_threads} host threads inside the call"),
-                    "h2d_bytes_per_step": int(Q * L * E * 1),
-                    "d2h_bytes_per_step": int(Q * 24)},
-            "e2e_packed_u8": {"value": e2e_packed_val * N, "unit": "evals/s", "steps": e2e_steps,
-                              "api": "moe_eamc_match_packed (host u8 probes, pinned) + D2H results "
-                                     "(per-rank, scaled by N)",
-                              "h2d_bytes_per_step": int(Q * L * E), "d2h_bytes_per_step": int(Q * 24)},
+                    "api": ("moe_eamc_match (host u64 probes [Q][L][E], pinned) + host results, "
+                            f"u64 narrowed to the u8 storage width on {host_threads} host threads "
+                            "inside the call; wall clock"),
+                    "h2d_bytes_per_step": int(SC_Q * L * E * 1),
+                    "d2h_bytes_per_step": int(SC_Q * 24),
+                    "host_input_bytes_per_step": int(SC_Q * L * E * 8),
+                    "same_result_as_device_api": e2e_same},
             "gpu_launches": gpu_launches,
             "ms_per_step_profiled": sum(ms_prof) / args.steps,
             "kernel_ms_per_step": {"prep": kms[0] / max(kcalls[0], 1), "screen": screen_ms,
@@ -320,6 +336,7 @@ def run_ours(args):
             "clocks": clk,
         }
         if streaming:
+            out["roofline_streaming"] = streaming.pop("roofline")
             out["streaming"] = streaming
         if rows:
             out["rows"] = rows
@@ -331,20 +348,99 @@ def run_ours(args):
     return out
 
 
+def run_sw_row(args, m, _lib, torch, dev, sp, stream, flush):
+    """BASELINE configs[1] (SW): P=10k, Q=4096, one B200 -- device-resident
+    value + roofline, e2e through the host API, reference on all host cores
+    over the whole batch with a bitwise check."""
+    shard = m.gen_bench_family(SEED, L, E, SW_P, dtype=np.uint8)
+    probes_u8 = m.gen_bench_family(SEED, L, E, SW_Q, skip=SW_P, dtype=np.uint8)
+    eamc = m.Eamc(m.ModelShape(L, E, TOPK), m.Phase.decode, SW_P, device=dev.index)
+    eamc.append(shard, np.arange(SW_P, dtype=np.uint64))
+    d_probes = torch.from_numpy(probes_u8).to(dev)
+    d_out = torch.empty((SW_Q, 3), dtype=torch.float64, device=dev)
+
+    def step():
+        _lib.check(_lib.lib.moe_eamc_match_device(eamc._h, d_probes.data_ptr(), 1, SW_Q,
+                                                  d_out.data_ptr(), sp))
+
+    for _ in range(max(args.warmup, 5)):
+        step()
+    torch.cuda.synchronize()
+    steps = max(args.steps, 50)
+    ms = _events_timed(torch, stream, steps, step, pre=flush.zero_)
+    _lib.check(_lib.lib.moe_eamc_set_profiling(eamc._h, 1))
+    ms_prof = _events_timed(torch, stream, steps, step, pre=flush.zero_)
+    kms = (C.c_double * 3)()
+    kc = (C.c_uint64 * 3)()
+    _lib.check(_lib.lib.moe_eamc_kernel_times(eamc._h, kms, kc))
+    _lib.check(_lib.lib.moe_eamc_set_profiling(eamc._h, 0))
+    res = _as_matches(d_out)
+    hbm_peak, tf_peak, peak_kind = load_peaks()
+    screen_ms = kms[1] / max(kc[1], 1)
+    ops_alg = 2.0 * L * E * SW_P * SW_Q
+    ach = ops_alg / (screen_ms / 1e3) / 1e12
+    row = {
+        "workload": (f"SW (BASELINE configs[1]): L={L} E={E} top-{TOPK}, EAMC P={SW_P}, "
+                     f"Q={SW_Q} probes, device-resident u8, L2 flushed between steps"),
+        "value": SW_P * SW_Q * steps / (sum(ms) / 1e3), "unit": "evals/s", "steps": steps,
+        "ms_per_step": sum(ms) / steps, "ms_per_step_profiled": sum(ms_prof) / steps,
+        "kernel_ms_per_step": {"prep": kms[0] / max(kc[0], 1), "screen": screen_ms,
+                               "refine": kms[2] / max(kc[2], 1)},
+        "roofline": {"bound": "tensor", "kernel": "k_tc2_screen", "achieved": ach,
+                     "peak": tf_peak, "unit": "TFLOP/s", "frac": ach / tf_peak,
+                     "traffic": ncu_traffic("sw_screen"), "launch_ms": screen_ms,
+                     "alg_ops_per_launch": ops_alg,
+                     "alg_bytes_per_launch": SW_P * L * E + SW_Q * L * E + 24 * SW_Q},
+    }
+    # e2e through the host API (u64 probes, the reference's storage type)
+    h_probes = torch.from_numpy(probes_u8.astype(np.uint64)).pin_memory()
+    h_out = np.zeros(SW_Q, _lib.MATCH_DTYPE)
+    for _ in range(3):
+        _lib.check(_lib.lib.moe_eamc_match(eamc._h, h_probes.data_ptr(), SW_Q, h_out.ctypes.data,
+                                           None))
+    n_e2e = 30
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        _lib.check(_lib.lib.moe_eamc_match(eamc._h, h_probes.data_ptr(), SW_Q, h_out.ctypes.data,
+                                           None))
+    t_e2e = (time.perf_counter() - t0) / n_e2e
+    row["e2e"] = {"value": SW_P * SW_Q / t_e2e, "unit": "evals/s", "ms_per_step": t_e2e * 1e3,
+                  "api": "moe_eamc_match, host u64 probes (pinned) + host results",
+                  "h2d_bytes_per_step": SW_Q * L * E, "d2h_bytes_per_step": SW_Q * 24}
+    ref, _ = _ref_or_none()
+    if ref is not None and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        er = ref.eamc(L, E, TOPK, 1, SW_P)
+        er.fill_bench(SEED, SW_P)
+        pr = ref.gen_bench(SEED, L, E, SW_Q, skip=SW_P)
+        idx, seq, d, f, secs = er.match(pr, threads=cores)
+        row["cpu_baseline"] = {"value": SW_P * SW_Q / secs, "unit": "evals/s", "cores": cores,
+                               "kind": "reference",
+                               "sample": f"all {SW_Q} probes (std::thread over the const matcher)"}
+        row["parity_sample"] = {
+            "probes": SW_Q,
+            "bitwise_equal_index_seq_distance": bool(
+                np.array_equal(idx, res["index"]) and np.array_equal(seq, res["seq"]) and
+                np.array_equal(d, res["distance"]))}
+        row["speedup_vs_reference"] = row["value"] / row["cpu_baseline"]["value"]
+        row["e2e_speedup_vs_reference"] = row["e2e"]["value"] / row["cpu_baseline"]["value"]
+    return row
+
+
 def _ref_or_none():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import REF_SO, Oracle, RefLib
     return (RefLib() if os.path.exists(REF_SO) else None), Oracle()
 
 
-def run_rows(args, m, _lib, torch, dev, sp, stream):
+def run_rows(args, m, _lib, torch, dev, sp, stream, flush):
     """Measured lines for SURVEY 8 rows beyond the headline matcher, each with
     the reference CPU path (oracle/_ref) timed on this box beside it."""
     from concurrent.futures import ThreadPoolExecutor
     hbm_peak, _, peak_kind = load_peaks()
     ref, orc = _ref_or_none()
     cores = os.cpu_count() or 1
-    out = {}
+    out = {"sw_match": run_sw_row(args, m, _lib, torch, dev, sp, stream, flush)}
 
     # -- A10/A11 prefetch decisions, DS shape (L=59, E=160, top-6): one decode
     #    step = 58 prefetch_priorities calls (l = 0..57) + floor filter
@@ -572,16 +668,12 @@ def run_rows(args, m, _lib, torch, dev, sp, stream):
     return out
 
 
-def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak, peak_kind):
+def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, e, hbm_peak, peak_kind):
+    """SC streaming regime: the headline's P = 2^20 collection (sharded P/N),
+    Q = 8 probes -- the HBM-bound case (arithmetic intensity 2Q/s_c)."""
     assert sp.value, "streaming leg must run on the explicit bench stream"
-    """SC streaming regime: P = 2^20 entries (sharded P/N), Q = 8 probes."""
-    P = STREAM_P // N
-    shard = m.gen_bench_family(SEED, L, E, P, skip=rank * P, dtype=np.uint8)
-    probes = m.gen_bench_family(SEED, L, E, STREAM_Q, skip=STREAM_P, dtype=np.uint8)
-    e = m.Eamc(m.ModelShape(L, E, TOPK), m.Phase.decode, P, device=dev.index)
-    e.append(shard, np.arange(rank * P, (rank + 1) * P, dtype=np.uint64))
-    del shard
-    _lib.check(_lib.lib.moe_eamc_set_index_base(e._h, rank * P))
+    P = SC_P // N
+    probes = m.gen_bench_family(SEED, L, E, STREAM_Q, skip=SC_P, dtype=np.uint8)
     d_pr = torch.from_numpy(probes).to(dev)
     d_out = torch.empty((STREAM_Q, 3), dtype=torch.float64, device=dev)
     d_parts = torch.empty((N * STREAM_Q, 3), dtype=torch.float64, device=dev)
@@ -597,27 +689,19 @@ def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak,
 
     stream = torch.cuda.current_stream()
 
-    def timed(step_fn, steps, profile):
+    def timed(steps, profile):
         if N > 1:
             dist.barrier()
         torch.cuda.synchronize()
         if profile:
             _lib.check(_lib.lib.moe_eamc_set_profiling(e._h, 1))
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(steps)]
-        for i in range(steps):
-            flush.zero_()
-            evs[i][0].record(stream)
-            step_fn()
-            evs[i][1].record(stream)
-        torch.cuda.synchronize()
+        ms = _events_timed(torch, stream, steps, step, pre=flush.zero_)
         kms = (C.c_double * 3)()
         kc = (C.c_uint64 * 3)()
         if profile:
             _lib.check(_lib.lib.moe_eamc_kernel_times(e._h, kms, kc))
             _lib.check(_lib.lib.moe_eamc_set_profiling(e._h, 0))
-        t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64,
-                         device=dev)
+        t = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
         if N > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()), kms[1] / max(kc[1], 1)
@@ -625,12 +709,12 @@ def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak,
     for _ in range(3):
         step()
     steps = 30
-    t_ms, _ = timed(step, steps, False)   # value: no per-kernel events (PDL intact)
-    _, screen_ms = timed(step, steps, True)
+    t_ms, _ = timed(steps, False)   # value: no per-kernel events (PDL intact)
+    _, screen_ms = timed(steps, True)
     bytes_alg = P * L * E * 1 + STREAM_Q * L * E * 1 + 24 * STREAM_Q
     ach = bytes_alg / (screen_ms / 1e3) / 1e9
-    out = {
-        "workload": f"SC streaming: P={STREAM_P} (P/GPU={P}), Q={STREAM_Q}, L={L} E={E}, u8",
+    return {
+        "workload": f"SC streaming: P={SC_P} (P/GPU={P}), Q={STREAM_Q}, L={L} E={E}, u8",
         "value": P * N * STREAM_Q * steps / (t_ms / 1e3), "unit": "evals/s",
         "ms_per_step": t_ms / steps, "steps": steps,
         "roofline": {"bound": "hbm",
@@ -639,146 +723,84 @@ def run_streaming(args, m, _lib, torch, dist, rank, N, dev, sp, flush, hbm_peak,
                      "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                      "traffic": ncu_traffic("sc_screen"), "launch_ms": screen_ms,
                      "alg_bytes_per_launch": bytes_alg,
-                     "note": f"peak = {peak_kind} HBM copy bandwidth (MEASURED_PEAKS.json)"},
+                     "note": (f"peak = {peak_kind} HBM copy bandwidth (MEASURED_PEAKS.json); "
+                              "bytes = P*L*E*s_c + Q*L*E*s_q + 24*Q (SURVEY.md 8d)")},
     }
-    if args.no_batch:
-        return out
-    # SC batch regime (BASELINE configs[4]): the same collection, a 65,536-probe batch;
-    # compute-bound by construction, so its roofline is the tensor pipe
-    QB = BATCH_Q
-    pb = torch.from_numpy(m.gen_bench_family(SEED, L, E, QB, skip=STREAM_P + STREAM_Q,
-                                             dtype=np.uint8)).to(dev)
-    b_out = torch.empty((QB, 3), dtype=torch.float64, device=dev)
-    b_parts = torch.empty((N * QB, 3), dtype=torch.float64, device=dev)
-    b_fin = torch.empty((QB, 3), dtype=torch.float64, device=dev)
-
-    def bstep():
-        _lib.check(_lib.lib.moe_eamc_match_device(e._h, pb.data_ptr(), 1, QB, b_out.data_ptr(),
-                                                  sp))
-        if N > 1:
-            dist.all_gather_into_tensor(b_parts, b_out)
-            _lib.check(_lib.lib.moe_match_merge_device(b_parts.data_ptr(), N, QB,
-                                                       b_fin.data_ptr(), sp))
-
-    bstep()
-    bsteps = 3
-    tb_ms, _ = timed(bstep, bsteps, False)
-    _, bscreen_ms = timed(bstep, bsteps, True)
-    ops = 2.0 * L * E * P * QB
-    _, tf_peak, _ = load_peaks()
-    out["batch"] = {
-        "workload": f"SC batch: P={STREAM_P} (P/GPU={P}), Q={QB}, L={L} E={E}, u8",
-        "value": P * N * QB * bsteps / (tb_ms / 1e3), "unit": "evals/s",
-        "ms_per_step": tb_ms / bsteps, "steps": bsteps,
-        "roofline": {"bound": "tensor",
-                     "kernel": "k_tc2_screen (tcgen05.mma.cta_group::2 kind::f16)",
-                     "achieved": ops / (bscreen_ms / 1e3) / 1e12, "peak": tf_peak,
-                     "unit": "TFLOP/s", "frac": ops / (bscreen_ms / 1e3) / 1e12 / tf_peak,
-                     "launch_ms": bscreen_ms, "alg_ops_per_launch": ops,
-                     "frac_of_nominal_2250": ops / (bscreen_ms / 1e3) / 1e12 / 2250.0,
-                     "note": ("ops = 2*L*E*P*Q (SURVEY.md 8d); peak = measured cuBLAS bf16 "
-                              "8192^3 burst (MEASURED_PEAKS.json, taken under the 1000 W cap); "
-                              "frac_of_nominal_2250 = against the nominal dense fp16 peak")},
-    }
-    return out
 
 
 def cpu_baseline(args, probes_u8, gpu_res):
-    """The reference CPU path (oracle/_ref = moesim compiled from its sources) on
-    this box's host cores, bounded sample of the SW workload; also checks the
-    sampled probes against the GPU result bit for bit."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import REF_SO, Oracle, RefLib
-    import paper_2401_14361_b200 as m
-    fam = m.gen_bench_family(SEED, L, E, P_PER_GPU, dtype=np.uint64)
+    """The reference CPU path (oracle/_ref = moesim compiled from its own
+    sources) on this box's host cores, on a bounded sample of the SC workload
+    (the full P = 2^20 collection, CPU_SAMPLE_Q probes spread over the batch);
+    the sampled probes are also checked against the GPU result bit for bit."""
+    ref, orc = _ref_or_none()
     cores = os.cpu_count() or 1
-    if os.path.exists(REF_SO):
-        ref = RefLib()
+    pick = np.linspace(0, SC_Q - 1, CPU_SAMPLE_Q).astype(np.int64)
+    pr = probes_u8[pick].astype(np.uint64)
+    if ref is not None:
         kind = "reference"
-        e = ref.eamc(L, E, TOPK, 1, P_PER_GPU)
-        for x in fam:
-            e.insert(x)
-
-        def run(pr):
-            idx, seq, d, f, secs = e.match(pr, threads=cores)
-            return idx, d, secs
-    else:
-        orc = Oracle()
-        kind = "port"
-        cores = 1
-
-        def run(pr):
-            t0 = time.perf_counter()
-            idx, seq, d, f = orc.match(fam, np.arange(P_PER_GPU, dtype=np.uint64), pr)
-            return idx, d, time.perf_counter() - t0
-    chunk = max(cores * 2, 8)
-    done, secs = 0, 0.0
-    ok = True
-    while done < Q and secs < args.cpu_seconds:
-        pr = probes_u8[done:done + chunk].astype(np.uint64)
-        idx, d, s = run(pr)
-        secs += s
-        ok &= bool(np.array_equal(idx, gpu_res["index"][done:done + chunk]) and
-                   np.array_equal(d, gpu_res["distance"][done:done + chunk]))
-        done += len(pr)
-    val = P_PER_GPU * done / secs
-    return ({"value": val, "unit": "evals/s", "cores": cores, "kind": kind,
-             "sample": (f"{done} of {Q} SW probes vs P={P_PER_GPU} (Eamc::match, "
-                        f"{'std::thread over the const matcher' if cores > 1 else 'one thread'}), "
-                        f"{secs:.1f} s")},
-            {"probes": done, "bitwise_equal_index_and_distance": ok})
+        t0 = time.perf_counter()
+        e = ref.eamc(L, E, TOPK, 1, SC_P)
+        e.fill_bench(SEED, SC_P)          # bench_match's fill loop (bench.cpp:61-62)
+        t_fill = time.perf_counter() - t0
+        idx, seq, d, f, secs = e.match(pr, threads=cores)
+        del e
+    else:  # the reference was not built on this box: the C restatement, one thread
+        kind, cores, t_fill = "port", 1, 0.0
+        fam = orc.bench_family(SEED, L, E, SC_P)
+        t0 = time.perf_counter()
+        idx, seq, d, f = orc.match(fam, np.arange(SC_P, dtype=np.uint64), pr[:4])
+        secs = time.perf_counter() - t0
+        pick, pr = pick[:4], pr[:4]
+    g = gpu_res[pick]
+    ok = bool(np.array_equal(idx, g["index"]) and np.array_equal(seq, g["seq"]) and
+              np.array_equal(d, g["distance"]))
+    return ({"value": SC_P * len(pr) / secs, "unit": "evals/s", "cores": cores, "kind": kind,
+             "sample": (f"{len(pr)} of the {SC_Q} SC probes (every {SC_Q // len(pr)}th) vs the "
+                        f"full P={SC_P} collection, Eamc::match "
+                        f"({'std::thread over the const matcher' if cores > 1 else 'one thread'}),"
+                        f" {secs:.1f} s (+{t_fill:.1f} s collection fill, untimed)")},
+            {"probes": int(len(pr)), "bitwise_equal_index_seq_distance": ok})
 
 
 # --------------------------------------------------------------- reference
 def run_reference(args):
-    """The reference's own CPU implementation (oracle/_ref) on this box's host
-    cores, on our arm's config; rank 0 only."""
+    """The reference's own CPU implementation (oracle/_ref: moesim compiled
+    from its sources) on this box's host cores, on our arm's config (SC:
+    P = 2^20, bench family seed 55); each step is a bounded sample of the batch
+    (one probe per host thread).  Inputs come from the reference's own Rng
+    (ref_shim), so this arm loads nothing from the product package.  Rank 0
+    only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return None
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import REF_SO, Oracle, RefLib
-    import paper_2401_14361_b200 as m
+    from oracle import REF_SO, RefLib
     N = max(world, args.gpus)
-    P = P_PER_GPU * N
-    fam = m.gen_bench_family(SEED, L, E, P + Q, dtype=np.uint64)
     cores = os.cpu_count() or 1
-    if os.path.exists(REF_SO):
-        kind = "reference"
-        e = RefLib().eamc(L, E, TOPK, 1, P)
-        for x in fam[:P]:
-            e.insert(x)
-
-        def run(pr):
-            return e.match(pr, threads=cores)[4]
-    else:
-        kind = "port"
-        orc = Oracle()
-        cores = 1
-
-        def run(pr):
-            t0 = time.perf_counter()
-            orc.match(fam[:P], np.arange(P, dtype=np.uint64), pr)
-            return time.perf_counter() - t0
-    per_step = max(cores, 4)
-    probes = fam[P:]
+    if not os.path.exists(REF_SO):
+        return {"impl": "reference", "unavailable": "oracle/_ref/libmoesim_ref.so was not built"}
+    ref = RefLib()
+    e = ref.eamc(L, E, TOPK, 1, SC_P)
+    e.fill_bench(SEED, SC_P)                      # bench.cpp:61-62
+    per_step = cores
+    n_pr = per_step * (args.steps + args.warmup)
+    probes = ref.gen_bench(SEED, L, E, n_pr, skip=SC_P)  # bench.cpp:64-66
     for i in range(args.warmup):
-        run(probes[:per_step])
+        e.match(probes[i * per_step:(i + 1) * per_step], threads=cores)
     secs = 0.0
-    for i in range(args.steps):
-        s0 = (i * per_step) % (Q - per_step)
-        secs += run(probes[s0:s0 + per_step])
-    val = P * per_step * args.steps / secs
+    for i in range(args.warmup, args.warmup + args.steps):
+        secs += e.match(probes[i * per_step:(i + 1) * per_step], threads=cores)[4]
+    val = SC_P * per_step * args.steps / secs
     return {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "evals/s", "n_gpus": N,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference bench family F1 (bench.cpp:44-54, seed 55)",
-        "config": {"workload": (f"SW (BASELINE configs[1]): L={L} E={E} top-{TOPK}, EAMC "
-                                f"P={P}, Q={Q}; each step a {per_step}-probe sample"),
-                   "L": L, "E": E, "P_total": P, "Q": Q},
-        "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": kind,
-                         "sample": f"{per_step} probes per step x {args.steps} steps"},
+        "config": sc_config(N),
+        "cpu_baseline": {"value": val, "unit": "evals/s", "cores": cores, "kind": "reference",
+                         "sample": (f"{per_step} probes per step (one per host thread) x "
+                                    f"{args.steps} steps vs the full P={SC_P} collection")},
         "e2e": {"value": val, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -793,8 +815,6 @@ def main():
     ap.add_argument("--no-streaming", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rows", action="store_true")
-    ap.add_argument("--no-batch", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

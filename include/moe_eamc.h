@@ -147,7 +147,12 @@ moe_status moe_eamc_match_packed(const moe_eamc* h, const void* probes, int prob
 /* Device variant: probes are device [n][L][E] of probe_bytes (1, 2 or 8)
  * bytes per count, out is device moe_match[n].  stream NULL = the handle's
  * internal stream (NOT the legacy default stream); pass the caller's stream
- * to order the work with the caller's kernels and events. */
+ * to order the work with the caller's kernels and events.  Nothing waits on
+ * the host, so the collection is never widened here: a probe with a count
+ * above the collection's current storage width gets the WIDTH SENTINEL
+ * {index = MOE_MATCH_WIDTH_SENTINEL, seq = UINT64_MAX, distance = NaN}; redo
+ * such probes with moe_eamc_match / moe_eamc_match_packed (which widen). */
+#define MOE_MATCH_WIDTH_SENTINEL 0xFFFFFFFFFFFFFFFEull
 moe_status moe_eamc_match_device(const moe_eamc* h, const void* probes, int probe_bytes,
                                  uint64_t n_probes, moe_match* out, void* stream);
 /* Eamc::match_within (eam.cpp:131-150): every entry within `window` of the
@@ -156,7 +161,9 @@ moe_status moe_eamc_match_device(const moe_eamc* h, const void* probes, int prob
 moe_status moe_eamc_match_within(const moe_eamc* h, const uint64_t* probe, double window,
                                  moe_match* out, uint64_t cap, uint64_t* n_out);
 /* Lexicographic (distance, seq) merge of per-shard results (P-sharded
- * matching): parts is [n_parts][n] -> out[n]. */
+ * matching): parts is [n_parts][n] -> out[n].  A width
+ * sentinel in any part makes the merged result the sentinel (never hidden
+ * behind another shard's answer). */
 moe_status moe_match_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out);
 moe_status moe_match_merge_device(const moe_match* parts, uint64_t n_parts, uint64_t n,
                                   moe_match* out, void* stream);

@@ -302,6 +302,17 @@ class RefLib:
             C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_uint32,
             C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, u64p, C.c_uint32]
 
+        lib.ref_gen_bench.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64,
+                                      C.c_uint64, u64p]
+        lib.ref_eamc_fill_bench.restype = C.c_int
+        lib.ref_eamc_fill_bench.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+
+    def gen_bench(self, seed, L, E, n, skip=0):
+        """bench_match's EAM stream (bench.cpp:44-54) from the reference Rng."""
+        out = np.zeros((n, L, E), np.uint64)
+        self.lib.ref_gen_bench(seed, L, E, skip, n, out)
+        return out
+
     def distance(self, a, b):
         a = np.ascontiguousarray(a, np.uint64)
         b = np.ascontiguousarray(b, np.uint64)
@@ -324,6 +335,12 @@ class RefLib:
 
         def size(self):
             return self.ref.lib.ref_eamc_size(self.h)
+
+        def fill_bench(self, seed, n):
+            """Insert the first n EAMs of the bench stream (bench.cpp:61-62)."""
+            rc = self.ref.lib.ref_eamc_fill_bench(self.h, seed, n)
+            if rc:
+                raise ValueError(f"ref fill error {rc}")
 
         def insert(self, counts, kind=1, phase=None):
             slot = C.c_int64()

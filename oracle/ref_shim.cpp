@@ -256,6 +256,52 @@ uint64_t ref_capacity_bound(uint32_t L, uint32_t E, double similarity) {
   }
 }
 
+// The bench family of bench_match (bench.cpp:44-54, :60-66) drawn from the
+// reference's own Rng: Rng::stream(seed, 0x6265636E), <= 4 set()s per row,
+// counts U[1,32] (random_request_eam is file-local in bench.cpp, so its four
+// lines of generator logic are restated here; every draw is the reference
+// Rng's).  ref_gen_bench skips `skip` EAMs and writes n as u64 [n][L][E];
+// ref_eamc_fill_bench inserts the first n of the stream into an Eamc through
+// Eamc::insert exactly as bench_match's fill loop does (no host copy of the
+// collection is materialised: P = 2^20 at 12x128 is 12.9 GB as Eams).
+namespace {
+Eam bench_eam(const ModelShape& shape, Rng& rng) {
+  Eam eam(shape, EamKind::request, Phase::decode);
+  const uint32_t active = std::min<uint32_t>(4, shape.n_experts_per_layer);
+  for (uint32_t l = 0; l < shape.n_layers; ++l)
+    for (uint32_t k = 0; k < active; ++k) {
+      const auto e = static_cast<uint32_t>(rng.bounded(shape.n_experts_per_layer));
+      eam.set(l, e, rng.bounded(32) + 1);
+    }
+  return eam;
+}
+}  // namespace
+
+void ref_gen_bench(uint64_t seed, uint32_t L, uint32_t E, uint64_t skip, uint64_t n,
+                   uint64_t* out) {
+  const ModelShape s{L, E, 1};
+  Rng rng = Rng::stream(seed, 0x6265636Eull);
+  for (uint64_t i = 0; i < skip; ++i) (void)bench_eam(s, rng);
+  const uint64_t cells = uint64_t{L} * E;
+  for (uint64_t i = 0; i < n; ++i) {
+    const Eam eam = bench_eam(s, rng);
+    const auto c = eam.counts();
+    std::copy(c.begin(), c.end(), out + i * cells);
+  }
+}
+
+int ref_eamc_fill_bench(void* h, uint64_t seed, uint64_t n) {
+  auto* r = static_cast<RefEamc*>(h);
+  try {
+    Rng rng = Rng::stream(seed, 0x6265636Eull);
+    const ModelShape s = r->eamc.shape();
+    for (uint64_t i = 0; i < n; ++i) r->eamc.insert(bench_eam(s, rng));
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
 // bench_match (bench.cpp:58-88): returns the checksum, mean/median us.
 uint64_t ref_bench_match(uint64_t n_entries, uint32_t L, uint32_t E, uint64_t n_queries,
                          uint64_t seed, double* mean_us, double* median_us) {

@@ -568,16 +568,7 @@ class Pool {
       done_.store(n, std::memory_order_release);
       return;
     }
-    fn_ = fn;
-    ctx_ = ctx;
-    n_tasks_ = n;
-    done_.store(0, std::memory_order_relaxed);
-    next_.store(0, std::memory_order_release);
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      gen_.fetch_add(1, std::memory_order_release);
-    }
-    cv_.notify_all();
+    publish(n, fn, ctx);
   }
   void wait() {
     if (async_n_ > 0)
@@ -593,27 +584,45 @@ class Pool {
       for (int i = 0; i < n; ++i) fn(ctx, i);
       return;
     }
-    fn_ = fn;
-    ctx_ = ctx;
-    n_tasks_ = n;
-    done_.store(0, std::memory_order_relaxed);
-    next_.store(0, std::memory_order_release);
-    {
-      std::lock_guard<std::mutex> g(mu_);  // no lost wake-up for a sleeping worker
-      gen_.fetch_add(1, std::memory_order_release);
-    }
-    cv_.notify_all();
+    publish(n, fn, ctx);
     work();
     while (done_.load(std::memory_order_acquire) < n) std::this_thread::yield();
   }
 
  private:
+  // A job is published by one release store of claim_ = (job << 32 | 0)
+  // after fn_/ctx_/n_tasks_ are set.  Tasks are claimed by a CAS on the
+  // whole word, so a worker still leaving the previous job (holding that
+  // job's tag) can never take an index of the next one: its CAS fails once
+  // the tag changes.  The next job is only published after every task of the
+  // previous one has finished (done_ == n), so a successful claim always
+  // reads the fn_/ctx_ of its own job.
+  void publish(int n, void (*fn)(void*, int), void* ctx) {
+    fn_.store(fn, std::memory_order_relaxed);
+    ctx_.store(ctx, std::memory_order_relaxed);
+    n_tasks_.store(n, std::memory_order_relaxed);
+    done_.store(0, std::memory_order_relaxed);
+    ++job_;
+    claim_.store((uint64_t)job_ << 32, std::memory_order_release);
+    {
+      std::lock_guard<std::mutex> g(mu_);  // no lost wake-up for a sleeping worker
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+  }
   void work() {
+    uint64_t c = claim_.load(std::memory_order_acquire);
+    const uint64_t job = c >> 32;
     for (;;) {
-      const int i = next_.fetch_add(1, std::memory_order_acq_rel);
-      if (i >= n_tasks_) return;
-      fn_(ctx_, i);
+      if ((c >> 32) != job) return;
+      const uint32_t i = (uint32_t)c;
+      if ((int)i >= n_tasks_.load(std::memory_order_relaxed)) return;
+      if (!claim_.compare_exchange_weak(c, c + 1, std::memory_order_acq_rel,
+                                        std::memory_order_acquire))
+        continue;  // c reloaded: re-check the tag and the index
+      fn_.load(std::memory_order_relaxed)(ctx_.load(std::memory_order_relaxed), (int)i);
       done_.fetch_add(1, std::memory_order_release);
+      c = claim_.load(std::memory_order_acquire);
     }
   }
   // Workers spin for a while after each job (back-to-back jobs of one call
@@ -643,11 +652,13 @@ class Pool {
   std::condition_variable cv_;
   std::atomic<uint64_t> gen_{0};
   std::atomic<bool> stop_{false};
-  void (*fn_)(void*, int) = nullptr;
-  void* ctx_ = nullptr;
-  int n_tasks_ = 0;
+  std::atomic<void (*)(void*, int)> fn_{nullptr};
+  std::atomic<void*> ctx_{nullptr};
+  std::atomic<int> n_tasks_{0};
   int async_n_ = 0;
-  std::atomic<int> next_{0}, done_{0};
+  uint32_t job_ = 0;                 // written by the (serialised) publisher only
+  std::atomic<uint64_t> claim_{0};   // (job << 32) | next task index
+  std::atomic<int> done_{0};
 };
 
 Pool& pool() {

@@ -591,11 +591,18 @@ __global__ void k_merge_partials(const moe_match* parts, uint32_t grid, uint32_t
 __global__ void k_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out) {
   const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (q >= n) return;
+  // A part holding the width sentinel {UINT64_MAX-1, UINT64_MAX, NaN} (a
+  // probe whose counts exceed that shard's storage width, match_all async
+  // mode) poisons the merged answer: the caller must redo the probe through
+  // the synchronous path, so the sentinel is never hidden by another shard.
   moe_match b = parts[q];
+  bool poisoned = b.index == kNone - 1;
   for (uint64_t k = 1; k < n_parts; ++k) {
     const moe_match m = parts[k * n + q];
+    poisoned |= m.index == kNone - 1;
     if (better(m.distance, m.seq, b.distance, b.seq)) b = m;
   }
+  if (poisoned) b = moe_match{kNone - 1, kNone, __longlong_as_double(0x7ff8000000000000ll)};
   out[q] = b;
 }
 

@@ -346,11 +346,25 @@ def _cands(arr: np.ndarray) -> List[PrefetchCandidate]:
                               float(c["priority"])) for c in arr]
 
 
+def _check_decision_probe(cur_eam: Eam, eamc: Eamc, current_layer: int) -> bool:
+    """policy.cpp:90-95 validation order: current_layer against the probe's
+    own shape (out_of_range), an empty collection answers {} (returns False),
+    then Eamc::check_probe (eam.cpp:113-116, invalid_argument) -- which also
+    keeps the C side from reading a probe of the wrong size."""
+    if current_layer < 0 or current_layer >= cur_eam.shape.n_layers:
+        raise IndexError("prefetch_priorities: current_layer out of range")
+    if eamc.size() == 0:
+        return False
+    if cur_eam.shape != eamc.shape:
+        raise ValueError("Eamc: probe shape mismatch")
+    return True
+
+
 def prefetch_priorities(cur_eam: Eam, eamc: Eamc, current_layer: int,
                         apply_floor_filter: bool = False) -> List[PrefetchCandidate]:
     """policy.cpp:88-126 (+ the engine floor filter, engine.cpp:663-668)."""
-    if current_layer < 0:
-        raise IndexError("prefetch_priorities: current_layer out of range")
+    if not _check_decision_probe(cur_eam, eamc, current_layer):
+        return []
     cap = max(cur_eam.shape.total_experts(), 1)
     out = np.zeros(cap, CAND_DTYPE)
     n = C.c_uint64()
@@ -362,6 +376,8 @@ def prefetch_priorities(cur_eam: Eam, eamc: Eamc, current_layer: int,
 def prefetch_order(cur_eam: Eam, eamc: Eamc, current_layer: int,
                    apply_floor_filter: bool = True) -> np.ndarray:
     """Same as prefetch_priorities, as a structured array (layer, expert, priority)."""
+    if not _check_decision_probe(cur_eam, eamc, current_layer):
+        return np.zeros(0, CAND_DTYPE)
     cap = max(cur_eam.shape.total_experts(), 1)
     out = np.zeros(cap, CAND_DTYPE)
     n = C.c_uint64()
@@ -414,6 +430,13 @@ def select_eviction_victim(slots: Sequence[SlotView], request_eam: Eam) -> Optio
 def decide(cur_eam: Eam, eamc: Eamc, current_layer: int, request_eam: Eam,
            slots: Sequence[SlotView]) -> Tuple[np.ndarray, Optional[int]]:
     """Fused K5+K6: floor-filtered prefetch order and eviction victim in one launch."""
+    if current_layer < 0 or current_layer >= cur_eam.shape.n_layers:
+        raise IndexError("prefetch_priorities: current_layer out of range")
+    if cur_eam.shape != eamc.shape:
+        raise ValueError("Eamc: probe shape mismatch")
+    if (request_eam.shape.n_layers, request_eam.shape.n_experts_per_layer) != (
+            eamc.shape.n_layers, eamc.shape.n_experts_per_layer):
+        raise ValueError("decide: request EAM shape does not match the collection")
     a = _slot_array(slots)
     cap = max(cur_eam.shape.total_experts(), 1)
     out = np.zeros(cap, CAND_DTYPE)

@@ -32,33 +32,108 @@ def gathered_layout(world: int, Q: int):
     return (world * Q, MATCH_WORDS)
 
 
-class ShardedMatcher:
-    """Owns one rank's shard; `match_device` returns the merged global result."""
+WIDTH_SENTINEL = 0xFFFFFFFFFFFFFFFE  # moe_match.index of a probe the device path could not
+                                    # represent at its shard's storage width (moe_eamc.h)
 
-    def __init__(self, eamc, rank: int, world: int, P_total: int, group=None):
+
+class ShardedMatcher:
+    """Owns one rank's shard; `match_device` returns the merged global result.
+
+    `gather(parts, out)` is the exchange (default: NCCL/gloo
+    all_gather_into_tensor over `group`); it is injectable so one process can
+    drive several shards (tests on a single GPU)."""
+
+    def __init__(self, eamc, rank: int, world: int, P_total: int, group=None, gather=None):
         from . import _lib
         self._lib = _lib
         self.eamc, self.rank, self.world, self.group = eamc, rank, world, group
         self.start, self.end = shard_range(P_total, rank, world)
+        self._gather = gather
         _lib.check(_lib.lib.moe_eamc_set_index_base(eamc._h, self.start))
 
-    def load_shard(self, counts: np.ndarray) -> None:
-        """counts = this rank's [end-start][L][E] entries; seqs = global slot numbers."""
-        self.eamc.append(counts, np.arange(self.start, self.end, dtype=np.uint64))
+    def load_shard(self, counts: np.ndarray, seqs: np.ndarray) -> None:
+        """counts = this rank's [end-start][L][E] entries in slot order; seqs =
+        their GLOBAL insertion numbers (Eamc::entry_seq, or a snapshot's
+        "seq" fields).  Slot order is not seq order once entries have been
+        replaced (eam.cpp:164-177), and the (distance, seq) tie-break of
+        eam.cpp:123-124 needs the real seqs."""
+        seqs = np.ascontiguousarray(seqs, np.uint64)
+        if seqs.shape != (self.end - self.start,):
+            raise ValueError("load_shard: one global seq per entry of the shard")
+        self.eamc.append(counts, seqs)
+
+    def _exchange(self, parts, out):
+        if self._gather is not None:
+            self._gather(parts, out)
+        else:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(parts, out, group=self.group)
 
     def match_device(self, probes, probe_bytes: int, out, parts, final, stream):
-        """probes/out/parts/final are torch CUDA tensors; returns `final` ([Q] moe_match)."""
-        import torch.distributed as dist
+        """probes/out/parts/final are torch CUDA tensors; returns `final` ([Q]
+        moe_match), stream-ordered on `stream` (the collective included).  A
+        probe whose counts exceed some shard's storage width comes back as the
+        width sentinel (index WIDTH_SENTINEL, distance NaN) -- k_merge never
+        hides it behind another shard's answer; `match` resolves it."""
+        import torch
         lib, check = self._lib.lib, self._lib.check
         Q = out.shape[0]
-        sp = C.c_void_p(stream.cuda_stream)
-        check(lib.moe_eamc_match_device(self.eamc._h, probes.data_ptr(), probe_bytes, Q,
-                                        out.data_ptr(), sp))
-        if self.world == 1:
-            return out
-        dist.all_gather_into_tensor(parts, out, group=self.group)
-        check(lib.moe_match_merge_device(parts.data_ptr(), self.world, Q, final.data_ptr(), sp))
+        with torch.cuda.stream(stream):
+            sp = C.c_void_p(stream.cuda_stream)
+            check(lib.moe_eamc_match_device(self.eamc._h, probes.data_ptr(), probe_bytes, Q,
+                                            out.data_ptr(), sp))
+            if self.world == 1:
+                return out
+            self._exchange(parts, out)
+            check(lib.moe_match_merge_device(parts.data_ptr(), self.world, Q, final.data_ptr(),
+                                             sp))
         return final
+
+    def match(self, probes_u64: np.ndarray, stream=None) -> np.ndarray:
+        """Host-level sharded Eamc::match over [Q][L][E] u64 probes: the device
+        pass, then the width-sentinel probes redone through the synchronous
+        host path (which widens this rank's shard) and merged again.  Every
+        rank sees the same merged result, so every rank takes the same redo."""
+        import torch
+        from ._lib import MATCH_DTYPE
+        probes_u64 = np.ascontiguousarray(probes_u64, np.uint64)
+        Q = probes_u64.shape[0]
+        dev = torch.device("cuda", self.eamc.device)
+        stream = stream or torch.cuda.Stream(device=dev)
+        d_pr = torch.from_numpy(probes_u64.view(np.int64)).to(dev)
+        out = torch.empty((Q, MATCH_WORDS), dtype=torch.float64, device=dev)
+        parts = torch.empty(gathered_layout(self.world, Q), dtype=torch.float64, device=dev)
+        final = torch.empty((Q, MATCH_WORDS), dtype=torch.float64, device=dev)
+        res = self.match_device(d_pr, 8, out, parts, final, stream)
+        stream.synchronize()
+        got = _to_matches(res)
+        redo = np.nonzero(got["index"] == WIDTH_SENTINEL)[0]
+        if len(redo):
+            sub = np.ascontiguousarray(probes_u64[redo])
+            mine = np.zeros(len(redo), MATCH_DTYPE)
+            self._lib.check(self._lib.lib.moe_eamc_match(self.eamc._h, sub.ctypes.data,
+                                                         len(redo), mine.ctypes.data, None))
+            if self.world == 1:
+                got[redo] = mine
+            else:
+                o2 = torch.from_numpy(mine.view(np.float64).reshape(-1, MATCH_WORDS)).to(dev)
+                p2 = torch.empty(gathered_layout(self.world, len(redo)), dtype=torch.float64,
+                                 device=dev)
+                f2 = torch.empty_like(o2)
+                with torch.cuda.stream(stream):
+                    self._exchange(p2, o2)
+                    self._lib.check(self._lib.lib.moe_match_merge_device(
+                        p2.data_ptr(), self.world, len(redo), f2.data_ptr(),
+                        C.c_void_p(stream.cuda_stream)))
+                stream.synchronize()
+                got[redo] = _to_matches(f2)
+        return got
+
+
+def _to_matches(t) -> np.ndarray:
+    from ._lib import MATCH_DTYPE
+    a = t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
+    return np.ascontiguousarray(a).view(np.uint8).reshape(-1, 24).copy().view(MATCH_DTYPE)[:, 0]
 
 
 class ShardedDecider:
