@@ -101,9 +101,14 @@ moe_status moe_device_info(int device, int* sm_count, int* cc_major, int* cc_min
 moe_status moe_device_warmup(int device);
 
 /* ---- collection lifecycle: Eamc(ModelShape, Phase, capacity) eam.cpp:106-111 ---- */
-/* count_bytes: storage width of one count on the device, 1 or 2 (0 = 1).
- * The collection widens itself (1 -> 2 bytes) when an inserted EAM or a
- * probe needs it; counts that need more are MOE_ERR_OVERFLOW. */
+/* count_bytes: storage width of one count on the device, 1, 2 or 4 (0 = 1).
+ * The collection widens itself (1 -> 2 -> 4 bytes) when an inserted EAM or
+ * a probe needs it.  Any u64 count the reference answers EXACTLY is
+ * accepted: its fp64 sums (eam.cpp:75-87) are exact integers while every
+ * row's sum of squared counts is below 2^53, and the device computes those
+ * sums exactly in integers.  A row at or past that bound (so also any count
+ * >= 2^27) is MOE_ERR_OVERFLOW: there the reference rounds, and this library
+ * refuses rather than answer differently. */
 moe_status moe_eamc_create(const moe_shape* shape, moe_phase phase, uint64_t capacity,
                            int count_bytes, int device, moe_eamc** out);
 moe_status moe_eamc_destroy(moe_eamc* h);
@@ -131,7 +136,8 @@ moe_status moe_eamc_build(moe_eamc* h, const uint64_t* counts, uint64_t n,
  * insertion number of every entry is assigned by the caller.  Entries are
  * u64 [n][L][E]; next_seq becomes max(next_seq, max(seqs)+1). */
 moe_status moe_eamc_append(moe_eamc* h, const uint64_t* counts, const uint64_t* seqs, uint64_t n);
-/* Same, with counts already narrow on the host ([n][L][E] of count_bytes). */
+/* Same, with counts already narrow on the host ([n][L][E] of count_bytes:
+ * 1, 2, 4 or 8). */
 moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_bytes,
                                   const uint64_t* seqs, uint64_t n);
 
@@ -139,12 +145,12 @@ moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_byt
 /* probes [n][L][E] u64 host; out[n]; found[n] (nullable). */
 moe_status moe_eamc_match(const moe_eamc* h, const uint64_t* probes, uint64_t n_probes,
                           moe_match* out, uint8_t* found);
-/* Same, with host probes already narrow: [n][L][E] of probe_bytes (1, 2 or
- * 8) bytes per count (e.g. counts traced as u8/u16).  Results are identical
+/* Same, with host probes already narrow: [n][L][E] of probe_bytes (1, 2, 4
+ * or 8) bytes per count (e.g. counts traced as u8/u16/u32).  Results are identical
  * to moe_eamc_match on the widened counts; one H2D of the narrow batch. */
 moe_status moe_eamc_match_packed(const moe_eamc* h, const void* probes, int probe_bytes,
                                  uint64_t n_probes, moe_match* out, uint8_t* found);
-/* Device variant: probes are device [n][L][E] of probe_bytes (1, 2 or 8)
+/* Device variant: probes are device [n][L][E] of probe_bytes (1, 2, 4 or 8)
  * bytes per count, out is device moe_match[n].  stream NULL = the handle's
  * internal stream (NOT the legacy default stream); pass the caller's stream
  * to order the work with the caller's kernels and events.  Nothing waits on

@@ -17,20 +17,16 @@
 #include <string>
 #include <vector>
 
-#include "common.cuh"
-#include "host.hpp"
-
 #include <atomic>
-#include "kernels.cuh"
+#include <chrono>
 
-using moe::DevColl;
-using moe::DevProbes;
-using moe::MatchGeom;
-using moe::MatchWork;
+#include "abi_internal.hpp"
+
+namespace moe::abi {
 
 namespace {
-
 thread_local std::string g_err;
+}
 
 moe_status fail(moe_status s, const char* fmt, ...) {
   char buf[512];
@@ -42,187 +38,13 @@ moe_status fail(moe_status s, const char* fmt, ...) {
   return s;
 }
 
-#define CK(expr)                                                                          \
-  do {                                                                                    \
-    cudaError_t e_ = (expr);                                                              \
-    if (e_ != cudaSuccess)                                                                \
-      return fail(e_ == cudaErrorMemoryAllocation ? MOE_ERR_OOM : MOE_ERR_CUDA, "%s: %s (%s:%d)", \
-                  #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                     \
-  } while (0)
-#define CKS(expr)                    \
-  do {                               \
-    moe_status s_ = (expr);          \
-    if (s_ != MOE_OK) return s_;     \
-  } while (0)
+const char* last_error() { return g_err.c_str(); }
 
-struct DevBuf {
-  void* p = nullptr;
-  size_t n = 0;
-  cudaError_t ensure(size_t bytes) {
-    if (bytes <= n) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    const size_t want = std::max<size_t>(bytes, 256);
-    cudaError_t e = cudaMalloc(&p, want);
-    if (e == cudaSuccess) n = want;
-    return e;
-  }
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
-  template <typename T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
+}  // namespace moe::abi
 
-struct PinBuf {
-  void* p = nullptr;
-  size_t n = 0;
-  cudaError_t ensure(size_t bytes) {
-    if (bytes <= n) return cudaSuccess;
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    n = 0;
-    cudaError_t e = cudaMallocHost(&p, std::max<size_t>(bytes, 64));
-    if (e == cudaSuccess) n = std::max<size_t>(bytes, 64);
-    return e;
-  }
-  ~PinBuf() {
-    if (p) cudaFreeHost(p);
-  }
-  template <typename T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
+using namespace moe::abi;
 
-int g_n_sm[64] = {0};
-
-moe_status device_ok(int device, int* n_sm) {
-  int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
-    return fail(MOE_ERR_CUDA, "no CUDA device visible (libmoe_eamc has no CPU fallback)");
-  if (device < 0 || device >= n) return fail(MOE_ERR_INVALID_ARGUMENT, "bad device %d", device);
-  if (device < 64 && g_n_sm[device]) {
-    *n_sm = g_n_sm[device];
-    return MOE_OK;
-  }
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, device));
-  if (prop.major != 10)
-    return fail(MOE_ERR_CUDA, "device %d is sm_%d%d; libmoe_eamc is built for sm_100a only", device,
-                prop.major, prop.minor);
-  if (device < 64) g_n_sm[device] = prop.multiProcessorCount;
-  *n_sm = prop.multiProcessorCount;
-  return MOE_OK;
-}
-
-// Lock of a (possibly null) handle for the duration of an entry point.
-struct HandleLock {
-  std::recursive_mutex* m = nullptr;
-  explicit HandleLock(const moe_eamc* h);
-  ~HandleLock() {
-    if (m) m->unlock();
-  }
-};
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int d) {
-    cudaGetDevice(&prev);
-    if (prev != d) cudaSetDevice(d);
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-moe_status check_shape(const moe_shape* s) {
-  // ModelShape::validate (model.cpp:13-19)
-  if (!s) return fail(MOE_ERR_INVALID_ARGUMENT, "null shape");
-  if (s->n_layers < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "ModelShape: n_layers must be >= 1");
-  if (s->n_experts_per_layer < 1)
-    return fail(MOE_ERR_INVALID_ARGUMENT, "ModelShape: n_experts_per_layer must be >= 1");
-  if (s->top_k < 1 || s->top_k > s->n_experts_per_layer)
-    return fail(MOE_ERR_INVALID_ARGUMENT, "ModelShape: top_k must be in [1, n_experts_per_layer]");
-  return MOE_OK;
-}
-
-uint32_t row_bytes(uint32_t E, int cb) { return (E * cb + 15) / 16 * 16; }
-
-}  // namespace
-
-struct moe_eamc {
-  // Serialises the host entry points on one handle: the "const reader" calls
-  // (match, match_within, prefetch, ...) share the handle's scratch buffers
-  // and staging memory, so concurrent readers take turns (recursive: some
-  // entry points forward to others).
-  std::recursive_mutex mu;
-  int device = 0;
-  int n_sm = 148;
-  moe_shape shape{};
-  int phase = 1;
-  uint64_t capacity = 0;
-  uint64_t next_seq = 0;
-  DevColl c;
-  cudaStream_t st = nullptr;
-  // workspace
-  DevBuf raw, packed, ia, sqa, nrm, zq, T, bcnt, bucket, over_list, small, out, partials, wl,
-      agg, cand, slots, req, dist, rsim, keys, mem, bdiag;
-  PinBuf pin;
-  // instrumentation (moe_eamc_set_profiling): a ring of event sets so the
-  // asynchronous device path can be timed without synchronising per call
-  struct EvSet {
-    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    bool pending = false;
-  };
-  bool prof = false;
-  std::vector<EvSet> ring;
-  size_t ring_i = 0;
-  cudaEvent_t* ev = nullptr;  // events of the call in flight
-  double ms[3] = {0, 0, 0};
-  uint64_t calls[3] = {0, 0, 0};
-  DevBuf wide;
-  // pipelined host matching: copy stream, double-buffered u64 staging
-  cudaStream_t st2 = nullptr;
-  DevBuf raw2[2], outall;
-  PinBuf hpack;  // host-narrowed probes (moe_eamc_match, match_host_packed)
-  // collection version: bumped by every mutation (insert/build/append/widen)
-  uint64_t version = 0;
-  // decision-path layer-prefix cache (decide_impl / k_dec_dist): pref[p] =
-  // the in-order layer sum of rows [0, dec_keep] for the probe rows dec_rows
-  PinBuf dpin, cpin;
-  DevBuf pref, oscr;
-  DevBuf rdc, rdx, rocc;  // blocked construction replay: screen matrices, slot occupants
-  std::vector<uint8_t> dec_rows;
-  int64_t dec_keep = -1;
-  uint64_t dec_version = ~0ull;
-  int dec_cb = 0;
-  moe_status last_status = MOE_OK;
-  cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
-
-  ~moe_eamc() {
-    if (c.counts) cudaFree(c.counts);
-    if (c.ibT) cudaFree(c.ibT);
-    if (c.sqb) cudaFree(c.sqb);
-    if (c.seq) cudaFree(c.seq);
-    if (c.nrm) cudaFree(c.nrm);
-    if (c.zmask) cudaFree(c.zmask);
-    for (EvSet& es : ring)
-      for (cudaEvent_t e : es.ev)
-        if (e) cudaEventDestroy(e);
-    for (int i = 0; i < 2; ++i) {
-      if (ev_copy[i]) cudaEventDestroy(ev_copy[i]);
-      if (ev_free[i]) cudaEventDestroy(ev_free[i]);
-    }
-    if (st2) cudaStreamDestroy(st2);
-    if (st) cudaStreamDestroy(st);
-  }
-};
-
-HandleLock::HandleLock(const moe_eamc* h) {
+moe::abi::HandleLock::HandleLock(const moe_eamc* h) {
   if (h) {
     m = &const_cast<moe_eamc*>(h)->mu;
     m->lock();
@@ -287,28 +109,43 @@ moe_status ensure_alloc(moe_eamc* h, uint64_t need) {
   return MOE_OK;
 }
 
-// Re-encode the collection with 2-byte counts.
-moe_status widen(moe_eamc* h) {
+uint64_t width_max(int cb) { return cb == 1 ? 255ull : cb == 2 ? 65535ull : 0xffffffffull; }
+
+// Re-encode the collection with cb_new-byte counts (2 or 4).
+moe_status widen(moe_eamc* h, int cb_new) {
   DevColl& c = h->c;
   ++h->version;
-  if (c.cb == 2) return fail(MOE_ERR_OVERFLOW, "count exceeds 65535 (2-byte storage limit)");
-  const uint32_t RB2 = row_bytes(c.E, 2);
+  if (cb_new <= c.cb) return MOE_OK;
+  const uint32_t RB2 = row_bytes(c.E, cb_new);
   const uint64_t rows = c.cap ? (c.cap + moe::kNT) * c.L : 0;
   if (c.counts) {
     uint8_t* nc = nullptr;
     CK(cudaMalloc(&nc, rows * RB2));
-    CK(moe::launch_widen(c.counts, nc, rows, c.RB, RB2, h->st));
+    CK(moe::launch_widen(c.counts, nc, rows, c.RB, RB2, c.cb, cb_new, h->st));
     CK(cudaStreamSynchronize(h->st));
     cudaFree(c.counts);
     c.counts = nc;
   }
-  c.cb = 2;
+  c.cb = cb_new;
   c.RB = RB2;
   c.C = RB2 / 16;
   return MOE_OK;
 }
 
-uint64_t width_max(int cb) { return cb == 1 ? 255ull : 65535ull; }
+// The outcome of a packing pass whose largest unrepresentable count (or ~0 for
+// a row with sum c^2 >= 2^53, see k_prep) is mx: widen the collection to the
+// width mx needs, or MOE_ERR_OVERFLOW when no width represents it exactly --
+// the reference's fp64 sums are exact only while every row's sum of squares
+// is below 2^53 (eam.cpp:75-87), and past that bound this library refuses
+// rather than answer differently.
+moe_status widen_for(moe_eamc* h, uint64_t mx) {
+  if (mx > 0xffffffffull)
+    return fail(MOE_ERR_OVERFLOW,
+                "count %s: a row's sum of squared counts reaches 2^53, beyond the range where "
+                "the reference's fp64 arithmetic (eam.cpp:75-87) is exact",
+                mx == ~0ull ? "too large" : "exceeds 2^32-1");
+  return widen(h, mx <= 65535ull ? 2 : 4);
+}
 
 // Exact-integer tensor-core screen for small batches (MOE_I8=0 disables,
 // MOE_I8=1 forces it for any batch size it supports).
@@ -333,7 +170,11 @@ bool use_tc(const moe_eamc* h, uint64_t Q) {
     if (e[0] == '0') return false;
     if (e[0] == '1') return true;
   }
-  return !use_i8(h, Q) && Q >= 8;
+  if (use_i8(h, Q)) return false;
+  if (Q >= 8) return true;
+  // small batches take the SIMT screen unless its tiles do not fit the shape
+  MatchGeom g;
+  return !moe::plan_match(h->c, h->n_sm, 0, 1, &g);
 }
 
 // Fold a completed event set into the per-kernel totals.
@@ -416,10 +257,7 @@ moe_status launch_probe_prep(moe_eamc* h, const void* dsrc, int src_bytes, uint6
 moe_status check_width(moe_eamc* h, uint64_t mx, bool* ok) {
   *ok = mx <= width_max(h->c.cb);
   if (*ok) return MOE_OK;
-  if (mx > 65535ull)
-    return fail(MOE_ERR_OVERFLOW, "count %llu exceeds the 2-byte device storage of this build",
-                (unsigned long long)mx);
-  return widen(h);
+  return widen_for(h, mx);
 }
 
 const void* stage_source(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bool src_device,
@@ -498,6 +336,28 @@ moe_status match_work(moe_eamc* h, uint64_t Q, MatchWork* wout) {
   return MOE_OK;
 }
 
+// Exact argmin for the probes in qlist[0..n) (or *nq_dev of them): the TMA
+// matcher in exact mode where the shape fits its shared-memory tiles, else the
+// warp-per-entry kernel.  chunk = probes per partials pass.
+moe_status exact_pass(moe_eamc* h, const DevProbes& pr, const MatchWork& w0, const uint32_t* qlist,
+                      uint32_t n, const uint32_t* T, moe_match* out, cudaStream_t st,
+                      uint32_t chunk, const uint32_t* nq_dev = nullptr) {
+  MatchWork w = w0;
+  Plan pe;
+  if (moe::plan_match(h->c, h->n_sm, 1, 1, &pe.g)) {
+    CK(moe::encode_tmap(h->c, pe.g.G, &pe.map));
+    w.part_chunk = chunk;
+    CK(h->partials.ensure((size_t)chunk * pe.g.grid * sizeof(moe_match)));
+    w.partials = h->partials.as<moe_match>();
+    CK(moe::launch_exact(pe.map, h->c, pr, pe.g, w, qlist, n, T, out, st, nq_dev));
+    return MOE_OK;
+  }
+  CK(h->partials.ensure((size_t)chunk * moe::exact_warp_blocks(h->n_sm) * sizeof(moe_match)));
+  CK(moe::launch_exact_warp(h->c, pr, qlist, n, out, h->partials.as<moe_match>(), chunk, h->n_sm,
+                            st, nq_dev));
+  return MOE_OK;
+}
+
 // Screen + refine launches for packed probes (no synchronisation).  `inited`:
 // the probe prep already initialised w's threshold / bucket counters
 // (MatchInit); otherwise they are reset here.
@@ -525,8 +385,12 @@ moe_status launch_match(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaSt
       CK(h->bdiag.ensure(moe::i8_blockdiag_bytes(c, (uint32_t)Q)));
       CK(moe::launch_tci8_screen(c, pr, w, h->bdiag.as<uint8_t>(), h->n_sm, st));
     } else {
+      // the largest probe tile whose shared-memory layout fits this shape
+      uint32_t qt = pick_qt(Q);
+      MatchGeom g;
+      while (qt > 1 && !moe::plan_match(c, h->n_sm, 0, qt, &g)) qt >>= 1;
       Plan p;
-      CKS(make_plan(h, 0, pick_qt(Q), &p));
+      CKS(make_plan(h, 0, qt, &p));
       CK(moe::launch_screen(p.map, c, pr, p.g, w, st));
     }
   }
@@ -561,15 +425,9 @@ moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bo
     if (after_prep) CK(cudaEventRecord(after_prep, st));  // the source buffer may be reused
     CKS(launch_match(h, *pr, out, st, &w, /*inited=*/true));
     if (async) {
-      if (h->c.size) {
-        Plan pe;
-        CKS(make_plan(h, 1, 1, &pe));
-        w.part_chunk = (uint32_t)std::min<uint64_t>(n, 8192);
-        CK(h->partials.ensure((size_t)w.part_chunk * pe.g.grid * sizeof(moe_match)));
-        w.partials = h->partials.as<moe_match>();
-        CK(moe::launch_exact(pe.map, h->c, *pr, pe.g, w, w.over_list, (uint32_t)n, w.T, out, st,
-                             w.over_n));
-      }
+      if (h->c.size)
+        CKS(exact_pass(h, *pr, w, w.over_list, (uint32_t)n, w.T, out, st,
+                       (uint32_t)std::min<uint64_t>(n, 8192), w.over_n));
       return MOE_OK;
     }
     CK(cudaMemcpyAsync(h->pin.p, h->small.p, 32, cudaMemcpyDeviceToHost, st));
@@ -579,14 +437,7 @@ moe_status match_all(moe_eamc* h, const void* src, int src_bytes, uint64_t n, bo
     CKS(check_width(h, *h->pin.as<unsigned long long>(), &ok));
     if (!ok) continue;  // collection widened: redo with the wider packing
     const uint32_t n_over = h->pin.as<uint32_t>()[4];  // w.over_n = small + 16 B
-    if (n_over) {
-      Plan pe;
-      CKS(make_plan(h, 1, 1, &pe));
-      w.part_chunk = 1024;
-      CK(h->partials.ensure((size_t)w.part_chunk * pe.g.grid * sizeof(moe_match)));
-      w.partials = h->partials.as<moe_match>();
-      CK(moe::launch_exact(pe.map, h->c, *pr, pe.g, w, w.over_list, n_over, w.T, out, st));
-    }
+    if (n_over) CKS(exact_pass(h, *pr, w, w.over_list, n_over, w.T, out, st, 1024));
     return MOE_OK;
   }
 }
@@ -626,15 +477,14 @@ moe_status match_packed(moe_eamc* h, const DevProbes& pr, moe_match* out, cudaSt
   CK(cudaMemcpyAsync(h->pin.p, h->small.p, 32, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const uint32_t n_over = h->pin.as<uint32_t>()[4];  // w.over_n = small + 16 B
-  if (n_over) {
-    Plan pe;
-    CKS(make_plan(h, 1, 1, &pe));
-    w.part_chunk = 1024;
-    CK(h->partials.ensure((size_t)w.part_chunk * pe.g.grid * sizeof(moe_match)));
-    w.partials = h->partials.as<moe_match>();
-    CK(moe::launch_exact(pe.map, h->c, pr, pe.g, w, w.over_list, n_over, w.T, out, st));
-  }
+  if (n_over) CKS(exact_pass(h, pr, w, w.over_list, n_over, w.T, out, st, 1024));
   return MOE_OK;
+}
+
+inline uint64_t unpack_count(const uint8_t* row, uint32_t e, int cb) {
+  return cb == 1 ? row[e]
+         : cb == 2 ? reinterpret_cast<const uint16_t*>(row)[e]
+                   : reinterpret_cast<const uint32_t*>(row)[e];
 }
 
 // Unpack one device entry to host u64 counts.
@@ -646,9 +496,7 @@ moe_status read_entry(moe_eamc* h, uint64_t slot, uint64_t* counts, uint64_t* se
     CK(cudaMemcpy(row.data(), c.counts + slot * LR, LR, cudaMemcpyDeviceToHost));
     for (uint32_t l = 0; l < c.L; ++l)
       for (uint32_t e = 0; e < c.E; ++e)
-        counts[(uint64_t)l * c.E + e] =
-            c.cb == 1 ? row[l * c.RB + e]
-                      : reinterpret_cast<const uint16_t*>(row.data() + (size_t)l * c.RB)[e];
+        counts[(uint64_t)l * c.E + e] = unpack_count(row.data() + (size_t)l * c.RB, e, c.cb);
   }
   if (seq) CK(cudaMemcpy(seq, c.seq + slot, 8, cudaMemcpyDeviceToHost));
   return MOE_OK;
@@ -682,10 +530,7 @@ moe_status stage_entries(moe_eamc* h, const void* dsrc, int src_bytes, uint64_t 
     CK(cudaStreamSynchronize(h->st));
     const uint64_t mx = *h->pin.as<unsigned long long>();
     if (mx <= width_max(c.cb)) break;
-    if (mx > 65535ull)
-      return fail(MOE_ERR_OVERFLOW, "count %llu exceeds the 2-byte device storage of this build",
-                  (unsigned long long)mx);
-    CKS(widen(h));
+    CKS(widen_for(h, mx));
   }
   s->pr.Q = (uint32_t)n;
   s->pr.packed = s->packed.as<uint8_t>();
@@ -831,16 +676,10 @@ moe_status replay_staged(moe_eamc* h, Staged& s, int64_t* evicted_slots) {
     CK(cudaMemsetAsync(w.T, 0x7f, 4, h->st));
     CK(cudaMemsetAsync(w.bcnt, 0, 4, h->st));
     CK(moe::launch_screen(p.map, c, one, p.g, w, h->st));
-    Plan pe;
-    CKS(make_plan(h, 1, 1, &pe));
-    MatchWork we = w;
-    we.part_chunk = 1;
-    CK(h->partials.ensure((size_t)pe.g.grid * sizeof(moe_match)));
-    we.partials = h->partials.as<moe_match>();
     uint32_t* q0 = h->small.as<uint32_t>() + 32;
     CK(cudaMemsetAsync(q0, 0, 4, h->st));
     // exact argmin for probe 0 of `one`, written to vic[j0]
-    CK(moe::launch_exact(pe.map, c, one, pe.g, we, q0, 1, w.T, vic + j0 - 0, h->st));
+    CKS(exact_pass(h, one, w, q0, 1, w.T, vic + j0 - 0, h->st, 1));
     CK(moe::launch_replace(c, s.pr, j0, vic + j0, h->next_seq + (j0 - i), halt, h->st));
     CK(cudaStreamSynchronize(h->st));
     k = j0 + 1;
@@ -857,11 +696,62 @@ moe_status replay_staged(moe_eamc* h, Staged& s, int64_t* evicted_slots) {
 
 }  // namespace
 
+// ---- shard-level internals used by the sharded facade (sharded.cu) --------
+namespace moe::abi {
+
+moe_status replace_slot(moe_eamc* h, const uint64_t* counts, uint64_t slot, uint64_t seq) {
+  HandleLock hl_(h);
+  DeviceGuard dg(h->device);
+  if (slot >= h->c.size) return fail(MOE_ERR_OUT_OF_RANGE, "replace_slot: slot out of range");
+  const uint64_t cells = (uint64_t)h->c.L * h->c.E;
+  Staged s;
+  CK(h->raw.ensure(cells * 8));
+  CK(cudaMemcpyAsync(h->raw.p, counts, cells * 8, cudaMemcpyHostToDevice, h->st));
+  CKS(stage_entries(h, h->raw.p, 8, 1, &s));
+  CK(h->pin.ensure(256));
+  moe_match* v = reinterpret_cast<moe_match*>(h->pin.as<uint8_t>() + 128);
+  *v = moe_match{h->c.index_base + slot, 0, 0.0};
+  CK(h->out.ensure(sizeof(moe_match)));
+  CK(cudaMemcpyAsync(h->out.p, v, sizeof(moe_match), cudaMemcpyHostToDevice, h->st));
+  ++h->version;
+  CK(moe::launch_replace(h->c, s.pr, 0, h->out.as<moe_match>(), seq, nullptr, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return MOE_OK;
+}
+
+moe_status window_list(moe_eamc* h, uint64_t dmin_bits, double window,
+                       std::vector<moe::WinEntry>* v) {
+  HandleLock hl_(h);
+  DeviceGuard dg(h->device);
+  v->clear();
+  if (h->c.size == 0) return MOE_OK;
+  CK(h->pin.ensure(256));
+  CK(h->small.ensure(256));
+  CK(h->wl.ensure((size_t)h->c.size * sizeof(moe::WinEntry)));
+  uint64_t* hp = h->pin.as<uint64_t>();
+  hp[0] = dmin_bits;
+  hp[1] = 0;
+  unsigned long long* dm = reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 232);
+  uint32_t* wl_n = h->small.as<uint32_t>() + 60;
+  CK(cudaMemcpyAsync(dm, hp, 16, cudaMemcpyHostToDevice, h->st));  // dmin and wl_n = 0
+  CK(moe::launch_window_list(h->c, h->dist.as<double>(), dm, window, h->wl.as<moe::WinEntry>(),
+                             wl_n, h->st));
+  CK(cudaMemcpyAsync(hp + 4, wl_n, 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  const uint32_t n = *reinterpret_cast<uint32_t*>(hp + 4);
+  v->resize(n);
+  if (n) CK(cudaMemcpy(v->data(), h->wl.p, n * sizeof(moe::WinEntry), cudaMemcpyDeviceToHost));
+  for (auto& w : *v) w.p += h->c.index_base;
+  return MOE_OK;
+}
+
+}  // namespace moe::abi
+
 extern "C" {
 
 int moe_abi_version(void) { return MOE_EAMC_ABI_VERSION; }
 
-const char* moe_last_error(void) { return g_err.c_str(); }
+const char* moe_last_error(void) { return last_error(); }
 
 int moe_host_threads(void) { return moe::host::pool_threads(); }
 
@@ -896,8 +786,8 @@ moe_status moe_eamc_create(const moe_shape* shape, moe_phase phase, uint64_t cap
   if (phase != MOE_PHASE_PREFILL && phase != MOE_PHASE_DECODE)
     return fail(MOE_ERR_INVALID_ARGUMENT, "bad phase");
   if (count_bytes == 0) count_bytes = 1;
-  if (count_bytes != 1 && count_bytes != 2)
-    return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 0, 1 or 2");
+  if (count_bytes != 1 && count_bytes != 2 && count_bytes != 4)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 0, 1, 2 or 4");
   int n_sm = 0;
   CKS(device_ok(device, &n_sm));
   DeviceGuard dg(device);
@@ -1068,8 +958,8 @@ moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_byt
                                   const uint64_t* seqs, uint64_t n) {
   HandleLock hl_(h);
   if (!h || ((!counts || !seqs) && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
-  if (count_bytes != 1 && count_bytes != 2 && count_bytes != 8)
-    return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 1, 2 or 8");
+  if (count_bytes != 1 && count_bytes != 2 && count_bytes != 4 && count_bytes != 8)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 1, 2, 4 or 8");
   DeviceGuard dg(h->device);
   return append_impl(h, counts, count_bytes, seqs, n);
 }
@@ -1213,6 +1103,16 @@ moe_status moe_eamc_match(const moe_eamc* hc, const uint64_t* probes, uint64_t n
     bool done = false;
     CKS(match_host_packed(h, probes, n_probes, out, &done));
     if (done) {
+      // probes the device pass could not represent (a row's sum of squares
+      // past 2^53) come back as width sentinels: the synchronous path below
+      // reports them (MOE_ERR_OVERFLOW)
+      for (uint64_t q = 0; q < n_probes; ++q)
+        if (out[q].index == ~0ull - 1) {
+          DevProbes pr;
+          CK(h->out.ensure(sizeof(moe_match)));
+          CKS(match_all(h, probes + q * cells, 8, 1, false, h->out.as<moe_match>(), h->st, &pr));
+          CK(cudaMemcpy(out + q, h->out.p, sizeof(moe_match), cudaMemcpyDeviceToHost));
+        }
       if (found)
         for (uint64_t q = 0; q < n_probes; ++q) found[q] = out[q].index != ~0ull;
       return MOE_OK;
@@ -1292,8 +1192,8 @@ moe_status moe_eamc_match_device(const moe_eamc* hc, const void* probes, int pro
   HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || ((!probes || !out) && n_probes)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
-  if (probe_bytes != 1 && probe_bytes != 2 && probe_bytes != 8)
-    return fail(MOE_ERR_INVALID_ARGUMENT, "probe_bytes must be 1, 2 or 8");
+  if (probe_bytes != 1 && probe_bytes != 2 && probe_bytes != 4 && probe_bytes != 8)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "probe_bytes must be 1, 2, 4 or 8");
   if (n_probes == 0) return MOE_OK;
   if (n_probes > 0xffffffffull) return fail(MOE_ERR_INVALID_ARGUMENT, "too many probes");
   DeviceGuard dg(h->device);
@@ -1313,8 +1213,8 @@ moe_status moe_eamc_match_packed(const moe_eamc* hc, const void* probes, int pro
   if (!h || ((!probes || !out) && n_probes)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (probe_bytes == 8)
     return moe_eamc_match(hc, static_cast<const uint64_t*>(probes), n_probes, out, found);
-  if (probe_bytes != 1 && probe_bytes != 2)
-    return fail(MOE_ERR_INVALID_ARGUMENT, "probe_bytes must be 1, 2 or 8");
+  if (probe_bytes != 1 && probe_bytes != 2 && probe_bytes != 4)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "probe_bytes must be 1, 2, 4 or 8");
   if (n_probes == 0) return MOE_OK;
   if (n_probes > 0xffffffffull) return fail(MOE_ERR_INVALID_ARGUMENT, "too many probes");
   DeviceGuard dg(h->device);
@@ -1522,92 +1422,239 @@ moe_status moe_eam_distance(const moe_shape* shape, const uint64_t* a, const uin
   return MOE_OK;
 }
 
-// Decision-path distance pass over a host probe (prefetch_priorities /
-// decide): the probe is narrowed to the storage width on the host (one
-// small pinned upload instead of an 8-byte-per-count copy), and the per-entry
-// layer sums of the rows it shares with the previous call's probe -- the
-// engine calls once per layer with the iteration EAM growing by one row
-// (engine.cpp:546, :587) -- are reused from pref (k_dec_dist).  Returns
-// false (nothing launched) when the probe does not fit the storage width;
-// launch errors land in h->last_status.
-static bool zc_ok() {  // MOE_DECIDE_ZC=0: device outputs + copies (A/B runs)
+// ---- decision path (K4 + K5 [+ K6]): one cooperative launch (decide.cu) ---
+// MOE_DEC_TIMING=1: host-side launch / completion latency of the decision
+// kernel on stderr (diagnostics).
+static bool dec_timing() {
   static const bool on = [] {
-    const char* e = getenv("MOE_DECIDE_ZC");
-    return !(e && e[0] == '0');
+    const char* e = getenv("MOE_DEC_TIMING");
+    return e && e[0] == '1';
   }();
   return on;
 }
 
-static bool dec_pass(moe_eamc* h, const uint64_t* probe, uint32_t cur, cudaStream_t st,
-                     DevProbes* pr) {
-  h->last_status = MOE_OK;
+// Device scratch of the fused decision kernel, grown on demand.
+static moe_status dec_scratch(moe_eamc* h, uint64_t n_slots) {
+  const DevColl& c = h->c;
+  const uint64_t cells = (uint64_t)c.L * c.E;
+  const size_t n = std::max<uint32_t>(c.size, 1);
+  if (h->pref.n < n * 8) {
+    CK(h->pref.ensure(n * 8));
+    h->dec_keep = -1;  // the layer-prefix sums did not survive the reallocation
+  }
+  CK(h->dist.ensure(n * 8));
+  CK(h->agg.ensure(cells * 8));
+  CK(h->dkey.ensure(cells * 8));
+  CK(h->did.ensure(cells * 4));
+  CK(h->drank.ensure(cells * 4));
+  CK(h->dseg.ensure((size_t)c.L * 4));
+  if (!h->dstate.p) {  // dmin2[2] = ~0 (then self-cleaning by call parity), barrier = 0
+    CK(h->dstate.ensure(64));
+    CK(cudaMemsetAsync(h->dstate.p, 0xff, 16, h->st));
+    CK(cudaMemsetAsync(h->dstate.as<uint8_t>() + 16, 0, 16, h->st));
+    h->bar_base = h->bar_base2 = 0;
+  }
+  CK(h->cpin.ensure(std::max<uint64_t>(cells, 1) * sizeof(moe_candidate)));
+  CK(h->fpin.ensure(64));
+  if (n_slots) {
+    CK(h->req.ensure(cells * 8));
+    CK(h->slots.ensure(n_slots * (sizeof(moe_slot_view) + 8)));
+  }
+  return MOE_OK;
+}
+
+// Common launch + result copy of a DecisionArgs set up by the callers below.
+static moe_status run_decision(moe_eamc* h, moe::DecisionArgs& a, size_t stage_rows,
+                               const uint64_t* request_eam, const moe_slot_view* slots,
+                               uint64_t n_slots, moe_candidate* out, uint64_t cap, uint64_t* n_out,
+                               int64_t* victim) {
+  const DevColl& c = h->c;
+  cudaStream_t st = h->st;
+  const uint64_t cells = (uint64_t)c.L * c.E;
+  a.counts = c.counts;
+  a.sqb = c.sqb;
+  a.zm = c.L <= 64 ? c.zmask : nullptr;
+  a.size = c.size;
+  a.L = c.L;
+  a.E = c.E;
+  a.RB = c.RB;
+  a.pref = h->pref.as<double>();
+  a.dist = h->dist.as<double>();
+  a.window = 0.01;  // kMatchWindow (policy.hpp:30)
+  a.dmin2 = h->dstate.as<unsigned long long>();
+  a.agg = h->agg.as<unsigned long long>();
+  a.ckey = h->dkey.as<unsigned long long>();
+  a.cid = h->did.as<uint32_t>();
+  a.crank = h->drank.as<uint32_t>();
+  a.nseg = h->dseg.as<uint32_t>();
+  a.parity = (uint32_t)(h->dec_calls++ & 1);
+  // results straight into pinned host memory (device-visible under UVA)
+  a.out = h->cpin.as<moe_candidate>();
+  a.n_out = h->fpin.as<uint32_t>();
+  long long* vpin = reinterpret_cast<long long*>(h->fpin.as<uint8_t>() + 8);
+  if (n_slots && request_eam) {
+    CK(cudaMemcpyAsync(h->req.p, request_eam, cells * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(h->slots.p, slots, n_slots * sizeof(moe_slot_view), cudaMemcpyHostToDevice,
+                       st));
+    a.req = h->req.as<unsigned long long>();
+    a.slots = h->slots.as<moe_slot_view>();
+    a.n_slots = (uint32_t)n_slots;
+    a.slot_pri = reinterpret_cast<double*>(h->slots.as<moe_slot_view>() + n_slots);
+    a.victim = vpin;
+    *vpin = -1;
+  }
+  if (c.L - a.cur > moe::kDecMaxLayers || c.E > moe::kDecMaxExperts)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "decision: shape %ux%u exceeds the order phases' limits",
+                c.L, c.E);
+  const int grid = moe::decision_grid(h->n_sm, c.size, c.L, a.cur);
+  const size_t smem = std::max(stage_rows, moe::decision_smem(c.L, c.E, c.RB, 0, a.cur, grid));
+  if (smem > 220 * 1024)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "decision: shape %ux%u needs %zu B of shared memory",
+                c.L, c.E, smem);
+  a.tprobe = nullptr;
+  if (dec_timing()) {
+    CK(h->tprobe.ensure(64));
+    a.tprobe = h->tprobe.as<unsigned long long>();
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  a.bar = reinterpret_cast<uint32_t*>(h->dstate.as<uint8_t>() + 16);
+  a.bar_base = h->bar_base;
+  CK(moe::launch_decision(a, c.cb, grid, smem, st));
+  h->bar_base += moe::kDecBarriers * (uint32_t)grid;
+  const auto t1 = std::chrono::steady_clock::now();
+  CK(cudaStreamSynchronize(st));
+  const auto t2 = std::chrono::steady_clock::now();
+  if (dec_timing()) {
+    static double acc[9] = {0};
+    static uint64_t cnt = 0;
+    unsigned long long ts[8];
+    CK(cudaMemcpy(ts, h->tprobe.p, sizeof ts, cudaMemcpyDeviceToHost));
+    acc[0] += std::chrono::duration<double, std::micro>(t1 - t0).count();
+    acc[1] += std::chrono::duration<double, std::micro>(t2 - t1).count();
+    for (int i = 1; i < 8; ++i) acc[1 + i] += (ts[i] - ts[i - 1]) * 1e-3;
+    if (++cnt % 58 == 0)
+      fprintf(stderr,
+              "decision (avg of %llu): launch %.1f us, launch->done %.1f us | A %.1f sync %.1f "
+              "B %.1f sync %.1f C1 %.1f sync %.1f C2 %.1f\n",
+              (unsigned long long)cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
+              acc[4] / cnt, acc[5] / cnt, acc[6] / cnt, acc[7] / cnt, acc[8] / cnt);
+  }
+  const uint32_t n = *reinterpret_cast<volatile uint32_t*>(a.n_out);
+  if (n_out) *n_out = n;
+  if (n && out && cap) std::memcpy(out, a.out, std::min<uint64_t>(n, cap) * sizeof(moe_candidate));
+  if (victim) *victim = n_slots ? *reinterpret_cast<volatile long long*>(vpin) : -1;
+  return MOE_OK;
+}
+
+// The engine's decision on a host probe.  The probe is narrowed to the
+// storage width on the host (padded rows, so the explicit rows ship inside
+// the launch parameters), and the per-entry layer sums over the rows it
+// shares with the previous call's probe are reused from pref (k_decision
+// phase A).  *handled = false: the probe has more explicit rows than the
+// kernel stages; decide_impl then takes the row-parallel distance pass.
+static moe_status decide_fused(moe_eamc* h, const uint64_t* probe, uint32_t cur, int filter,
+                               const uint64_t* request_eam, const moe_slot_view* slots,
+                               uint64_t n_slots, moe_candidate* out, uint64_t cap,
+                               uint64_t* n_out, int64_t* victim, bool* handled) {
+  *handled = false;
   DevColl& c = h->c;
-  const int cb = c.cb;
   const uint32_t L = c.L, E = c.E;
-  const uint64_t row_b = (uint64_t)E * cb, cells = (uint64_t)L * E;
-  const uint64_t nz_off = (cells * cb + 15) & ~15ull;
-  auto bad = [&](moe_status st_) {
-    h->last_status = st_;
-    return true;
-  };
-  if (h->dpin.ensure(nz_off + L * 2 + 16) != cudaSuccess) return bad(fail(MOE_ERR_CUDA, "pinned alloc"));
-  uint8_t* hb = h->dpin.as<uint8_t>();
-  if (moe::host::pack_counts_serial(probe, cells, cb, hb) > width_max(cb)) return false;
-  // reuse the layer-prefix sums when rows [0, dec_keep] are unchanged
+  const uint64_t cells = (uint64_t)L * E;
+  uint8_t* hb = nullptr;
+  for (;;) {  // narrow at the storage width; widen and redo when a count needs it
+    CK(h->dpin.ensure((size_t)L * c.RB + 64));
+    hb = h->dpin.as<uint8_t>();
+    uint64_t o = 0;
+    const uint64_t row_b = (uint64_t)E * c.cb;
+    for (uint32_t l = 0; l < L; ++l) {
+      o |= moe::host::pack_counts_serial(probe + (uint64_t)l * E, E, c.cb, hb + (size_t)l * c.RB);
+      std::memset(hb + (size_t)l * c.RB + row_b, 0, c.RB - row_b);
+    }
+    if (o > width_max(c.cb)) {
+      const uint64_t mx = *std::max_element(probe, probe + cells);
+      if (mx > width_max(c.cb)) {
+        CKS(widen_for(h, mx));
+        continue;
+      }
+    }
+    // the reference's fp64 sums are exact only while sum c^2 < 2^53 per row
+    if ((double)o * (double)o * (double)E >= 9007199254740992.0)
+      for (uint32_t l = 0; l < L; ++l) {
+        uint64_t ss = 0;
+        for (uint32_t e = 0; e < E; ++e) {
+          const uint64_t v = probe[(uint64_t)l * E + e];
+          ss = v >= (1ull << 27) ? (1ull << 53) : std::min<uint64_t>(ss + v * v, 1ull << 53);
+        }
+        if (ss >= (1ull << 53)) CKS(widen_for(h, ~0ull));  // MOE_ERR_OVERFLOW
+      }
+    break;
+  }
+  CKS(dec_scratch(h, n_slots));
+  const uint32_t RB = c.RB;
+  // layer-prefix reuse: rows [0, dec_keep] unchanged, same collection contents
   uint32_t j0 = 0;
-  if (h->dec_keep >= 0 && h->dec_version == h->version && h->dec_cb == cb &&
-      std::memcmp(hb, h->dec_rows.data(), (size_t)(h->dec_keep + 1) * row_b) == 0)
+  if (h->dec_keep >= 0 && h->dec_version == h->version && h->dec_cb == c.cb &&
+      std::memcmp(hb, h->dec_rows.data(), (size_t)(h->dec_keep + 1) * RB) == 0)
     j0 = (uint32_t)h->dec_keep + 1;
   const bool store = (int64_t)cur > h->dec_keep || j0 == 0;
   const uint32_t keep = store ? cur : L;  // L: leave pref as it is
-  uint16_t* nz = reinterpret_cast<uint16_t*>(hb + nz_off);
-  uint32_t n_nz = 0;
+  std::vector<uint16_t>& nz = h->dec_nz;
+  nz.clear();
   for (uint32_t l = j0; l < L; ++l) {
-    const uint8_t* r = hb + l * row_b;
+    const uint64_t* r = reinterpret_cast<const uint64_t*>(hb + (size_t)l * RB);
     bool any = false;
-    for (uint64_t b = 0; b < row_b && !any; ++b) any = r[b] != 0;
-    if (any) nz[n_nz++] = (uint16_t)l;
+    for (uint32_t w = 0; w < RB / 8 && !any; ++w) any = r[w] != 0;
+    if (any) nz.push_back((uint16_t)l);
   }
-  auto ck = [&](cudaError_t e) {
-    if (e != cudaSuccess) h->last_status = fail(MOE_ERR_CUDA, "%s", cudaGetErrorString(e));
-    return e == cudaSuccess;
-  };
-  if (!ck(h->raw.ensure(nz_off + L * 2 + 16)) || !ck(h->pref.ensure((size_t)std::max<uint32_t>(c.size, 1) * 8)) ||
-      !ck(h->dist.ensure((size_t)std::max<uint32_t>(c.size, 1) * 8)))
-    return true;
-  // the prep kernel and k_dec_dist read the narrowed probe and its nonzero-row
-  // list straight from pinned host memory (UVA), or from a device copy
-  const uint8_t* src = hb;
-  if (!zc_ok()) {
-    if (!ck(cudaMemcpyAsync(h->raw.p, hb, nz_off + n_nz * 2, cudaMemcpyHostToDevice, st)))
-      return true;
-    src = h->raw.as<uint8_t>();
-  }
-  const bool prof = h->prof;
-  h->prof = false;
-  unsigned long long* dmin = reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224);
-  moe::MatchInit mi;
-  mi.dmin = dmin;  // reset by the prep kernel (no memset between it and k_dec_dist)
-  const moe_status ps = launch_probe_prep(h, src, cb, 1, st, pr, mi);
-  h->prof = prof;
-  if (ps != MOE_OK) return bad(ps);
+  const uint32_t n_nz = (uint32_t)nz.size();
+  if (n_nz > moe::kDecMaxNz || L > 65535) return MOE_OK;  // decide_impl's general path
   // explicit rows: through the last nonzero probe row and the stored row
-  uint32_t hi = n_nz ? nz[n_nz - 1] : 0;
+  uint32_t hi = n_nz ? nz.back() : 0;
   if (keep < L) hi = std::max(hi, keep);
   if (!n_nz && keep >= L) hi = j0 ? j0 - 1 : 0;  // nothing explicit beyond the cached prefix
-  if (!ck(moe::launch_dec_dist(c, pr->packed, pr->sqa,
-                               reinterpret_cast<const uint16_t*>(src + nz_off),
-                               nz, n_nz, j0, hi, keep, h->pref.as<double>(), h->dist.as<double>(),
-                               dmin, h->agg.as<unsigned long long>(), (uint32_t)cells,
-                               h->small.as<uint32_t>() + 10, st)))
-    return true;
+  moe::DecisionArgs& a = h->dargs;
+  a.do_dist = 1;
+  a.do_agg = 1;
+  a.dmin_ext = nullptr;
+  a.n_nz = n_nz;
+  a.j0 = j0;
+  a.hi = hi;
+  a.keep = keep;
+  a.cur = cur;
+  a.filter = filter;
+  a.req = nullptr;
+  a.slots = nullptr;
+  a.n_slots = 0;
+  a.slot_pri = nullptr;
+  a.victim = nullptr;
+  a.rows_inline = n_nz <= moe::kDecInlineNz && (size_t)n_nz * RB <= moe::kDecInlineBytes;
+  if (a.rows_inline) {
+    for (uint32_t i = 0; i < n_nz; ++i) {
+      a.inline_nz[i] = nz[i];
+      std::memcpy(a.inline_rows + (size_t)i * RB, hb + (size_t)nz[i] * RB, RB);
+    }
+    a.rows = nullptr;
+    a.nz = nullptr;
+  } else {  // one DMA of the explicit rows and their list
+    const size_t rows_b = (size_t)n_nz * RB, nz_b = ((size_t)n_nz * 2 + 15) & ~(size_t)15;
+    CK(h->xpin.ensure(rows_b + nz_b));
+    CK(h->xdev.ensure(rows_b + nz_b));
+    for (uint32_t i = 0; i < n_nz; ++i)
+      std::memcpy(h->xpin.as<uint8_t>() + (size_t)i * RB, hb + (size_t)nz[i] * RB, RB);
+    std::memcpy(h->xpin.as<uint8_t>() + rows_b, nz.data(), (size_t)n_nz * 2);
+    CK(cudaMemcpyAsync(h->xdev.p, h->xpin.p, rows_b + nz_b, cudaMemcpyHostToDevice, h->st));
+    a.rows = h->xdev.as<uint8_t>();
+    a.nz = reinterpret_cast<const uint16_t*>(h->xdev.as<uint8_t>() + rows_b);
+  }
+  CKS(run_decision(h, a, (size_t)n_nz * RB, request_eam, slots, n_slots, out, cap, n_out, victim));
   if (store) {
-    h->dec_rows.assign(hb, hb + (size_t)(cur + 1) * row_b);
+    h->dec_rows.assign(hb, hb + (size_t)(cur + 1) * RB);
     h->dec_keep = cur;
     h->dec_version = h->version;
-    h->dec_cb = cb;
+    h->dec_cb = c.cb;
   }
-  return true;
+  *handled = true;
+  return MOE_OK;
 }
 
 static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_t* cur_eam,
@@ -1618,55 +1665,46 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
   const uint32_t L = shape->n_layers, E = shape->n_experts_per_layer;
   const uint64_t cells = (uint64_t)L * E;
   cudaStream_t st = h->st;
-  CK(h->agg.ensure(cells * 8));
   CK(h->small.ensure(256));
   CK(h->pin.ensure(256));
-  unsigned long long* agg = h->agg.as<unsigned long long>();
-  const bool prefetch_live = do_prefetch && h->c.size > 0;
-  const uint64_t ncand = prefetch_live && current_layer + 1 < L ? (uint64_t)(L - current_layer - 1) * E : 0;
-  CK(h->cand.ensure(std::max<uint64_t>(ncand, 1) * sizeof(moe_candidate)));
-  uint32_t* dn = h->small.as<uint32_t>() + 12;
-  // zc: the order kernels write the candidates and their count straight into
-  // pinned host memory (device-visible under UVA) -- no device-to-host copies,
-  // one synchronisation.  Taken on the host-narrowed path (the width check is
-  // then already done on the host) when no eviction output is requested.
-  bool zc = false;
-  uint32_t* dn_host = reinterpret_cast<uint32_t*>(h->pin.as<uint8_t>() + 248);
-  if (prefetch_live) {
-    // one exact pass over the collection, window membership (kMatchWindow,
-    // policy.hpp:30) + u64 aggregation of the members' rows > l, then
-    // priorities / floor filter / order
-    DevProbes pr;
-    bool fused = false;  // k_dec_dist zeroed agg and the members count
-    if (!h->c.L || h->c.L > 256 || !dec_pass(h, cur_eam, current_layer, st, &pr)) {
-      CK(cudaMemsetAsync(agg, 0, cells * 8, st));
+  if (do_prefetch && h->c.size > 0 && !slot_pri) {
+    bool handled = false;
+    CKS(decide_fused(h, cur_eam, current_layer, filter, request_eam, slots, n_slots, out, cap,
+                     n_out, victim, &handled));
+    if (handled) return MOE_OK;
+    // more explicit probe rows than the fused kernel stages: row-parallel
+    // exact distances + minimum, then the fused kernel's aggregation + order
+    for (;;) {
+      DevProbes pr;
       CKS(launch_exact_distances(h, cur_eam, st, &pr));
-    } else if (h->last_status != MOE_OK) {
-      return h->last_status;
-    } else {
-      fused = true;
+      CK(cudaMemcpyAsync(h->pin.p, h->small.p, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      bool ok = false;
+      CKS(check_width(h, *h->pin.as<unsigned long long>(), &ok));
+      if (ok) break;
     }
-    CK(h->mem.ensure((size_t)h->c.size * 4));
-    CK(moe::launch_member_agg(h->c, h->dist.as<double>(),
-                              reinterpret_cast<unsigned long long*>(h->small.as<uint8_t>() + 224),
-                              0.01, current_layer, h->mem.as<uint32_t>(),
-                              h->small.as<uint32_t>() + 10, agg, h->n_sm, st, fused));
-    CK(h->keys.ensure(std::max<uint64_t>(ncand, 1) * 12));
-    const size_t osz = moe::prefetch_order_scratch(L, E);
-    if (h->oscr.n < osz) {
-      CK(h->oscr.ensure(osz));
-      CK(cudaMemsetAsync(h->oscr.p, 0, osz, st));
-    }
-    zc = fused && !victim && !slot_pri && !request_eam && !n_slots && ncand > 0 && zc_ok();
-    if (zc) CK(h->cpin.ensure(ncand * sizeof(moe_candidate)));
-    CK(moe::launch_prefetch_order(agg, L, E, current_layer, filter,
-                                  h->keys.as<unsigned long long>(), zc ? dn_host : dn,
-                                  zc ? h->cpin.as<moe_candidate>() : h->cand.as<moe_candidate>(),
-                                  h->n_sm, st, h->oscr.p));
-  } else {
-    CK(cudaMemsetAsync(h->small.p, 0, 8, st));  // no probe: nothing to width-check
+    CKS(dec_scratch(h, n_slots));
+    moe::DecisionArgs& a = h->dargs;
+    a.do_dist = 0;
+    a.do_agg = 1;
+    a.dmin_ext = reinterpret_cast<const unsigned long long*>(h->small.as<uint8_t>() + 224);
+    a.n_nz = 0;
+    a.rows_inline = 1;
+    a.j0 = 0;
+    a.hi = 0;
+    a.keep = L;
+    a.cur = current_layer;
+    a.filter = filter;
+    a.req = nullptr;
+    a.slots = nullptr;
+    a.n_slots = 0;
+    a.slot_pri = nullptr;
+    a.victim = nullptr;
+    return run_decision(h, a, 0, request_eam, slots, n_slots, out, cap, n_out, victim);
   }
-  if (!prefetch_live || current_layer + 1 >= L) CK(cudaMemsetAsync(dn, 0, 4, st));
+  // eviction scoring only (cache_priority / select_eviction_victim), or an
+  // empty collection: k_decide over the slot views
+  if (n_out) *n_out = 0;
   unsigned long long* req = nullptr;
   if (request_eam) {
     CK(h->req.ensure(cells * 8));
@@ -1684,44 +1722,11 @@ static moe_status decide_impl(moe_eamc* h, const moe_shape* shape, const uint64_
   }
   long long* dv = reinterpret_cast<long long*>(h->small.as<uint8_t>() + 192);
   if (victim || slot_pri)
-    CK(moe::launch_decide(agg, L, E, current_layer, filter, 0, req, dslots, n_slots, nullptr,
-                          nullptr, victim ? dv : nullptr, dpri, st));
-  if (zc) {
-    CK(cudaStreamSynchronize(st));
-    const uint32_t n = *reinterpret_cast<volatile uint32_t*>(dn_host);
-    if (n_out) *n_out = n;
-    if (n && out && cap)
-      std::memcpy(out, h->cpin.p, std::min<uint64_t>(n, cap) * sizeof(moe_candidate));
-    return MOE_OK;
-  }
+    CK(moe::launch_decide(h->agg.as<unsigned long long>(), L, E, current_layer, filter, 0, req,
+                          dslots, n_slots, nullptr, nullptr, victim ? dv : nullptr, dpri, st));
   CK(cudaMemcpyAsync(h->pin.p, h->small.p, 256, cudaMemcpyDeviceToHost, st));
-  // speculative copy of the head of the order with the status words: one
-  // round trip for the usual (floor-filtered, short) answer
-  const uint64_t head = prefetch_live && out ? std::min<uint64_t>({cap, ncand, 1024}) : 0;
-  if (head) {
-    CK(h->cpin.ensure(head * sizeof(moe_candidate)));
-    CK(cudaMemcpyAsync(h->cpin.p, h->cand.p, head * sizeof(moe_candidate), cudaMemcpyDeviceToHost,
-                       st));
-  }
   CK(cudaStreamSynchronize(st));
-  if (prefetch_live) {
-    bool ok = false;
-    CKS(check_width(h, *h->pin.as<unsigned long long>(), &ok));
-    if (!ok)  // collection widened for this probe: decide again at the new width
-      return decide_impl(h, shape, cur_eam, current_layer, filter, do_prefetch, request_eam, slots,
-                         n_slots, out, cap, n_out, victim, slot_pri);
-  }
-  const uint32_t n = h->pin.as<uint32_t>()[12];
-  const long long v = *reinterpret_cast<const long long*>(h->pin.as<uint8_t>() + 192);
-  if (n_out) *n_out = prefetch_live ? n : 0;
-  if (prefetch_live && n && out && cap) {
-    const uint64_t want = std::min<uint64_t>(n, cap);
-    std::memcpy(out, h->cpin.p, std::min(want, head) * sizeof(moe_candidate));
-    if (want > head)
-      CK(cudaMemcpy(out + head, h->cand.as<moe_candidate>() + head,
-                    (want - head) * sizeof(moe_candidate), cudaMemcpyDeviceToHost));
-  }
-  if (victim) *victim = v;
+  if (victim) *victim = *reinterpret_cast<const long long*>(h->pin.as<uint8_t>() + 192);
   if (slot_pri && n_slots) CK(cudaMemcpy(slot_pri, dpri, n_slots * 8, cudaMemcpyDeviceToHost));
   return MOE_OK;
 }
@@ -1812,17 +1817,42 @@ moe_status moe_eamc_prefetch_order_device(const moe_eamc* hc, const uint64_t* ag
     return fail(MOE_ERR_OUT_OF_RANGE, "prefetch_priorities: current_layer out of range");
   DeviceGuard dg(h->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->st;
-  const uint64_t ncand = (uint64_t)(L - current_layer - 1) * E;
-  CK(h->keys.ensure(std::max<uint64_t>(ncand, 1) * 12));
-  const size_t osz = moe::prefetch_order_scratch(L, E);
-  if (h->oscr.n < osz) {
-    CK(h->oscr.ensure(osz));
-    CK(cudaMemsetAsync(h->oscr.p, 0, osz, st));
-  }
-  CK(moe::launch_prefetch_order(reinterpret_cast<const unsigned long long*>(agg), L, E,
-                                current_layer, apply_floor_filter,
-                                h->keys.as<unsigned long long>(), n_out, out, h->n_sm, st,
-                                h->oscr.p));
+  CKS(dec_scratch(h, 0));
+  // the fused decision kernel's order phases on the caller's aggregate
+  moe::DecisionArgs& a = h->dargs;
+  a = moe::DecisionArgs{};
+  a.do_dist = 0;
+  a.do_agg = 0;
+  a.rows_inline = 1;
+  a.keep = L;
+  a.cur = current_layer;
+  a.filter = apply_floor_filter;
+  a.L = L;
+  a.E = E;
+  a.RB = h->c.RB;
+  a.size = 0;
+  a.agg = const_cast<unsigned long long*>(reinterpret_cast<const unsigned long long*>(agg));
+  a.dmin2 = h->dstate.as<unsigned long long>();
+  a.ckey = h->dkey.as<unsigned long long>();
+  a.cid = h->did.as<uint32_t>();
+  a.crank = h->drank.as<uint32_t>();
+  a.nseg = h->dseg.as<uint32_t>();
+  a.parity = (uint32_t)(h->dec_calls++ & 1);
+  a.out = out;
+  a.n_out = n_out;
+  if (L - current_layer > moe::kDecMaxLayers || E > moe::kDecMaxExperts)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "decision: shape %ux%u exceeds the order phases' limits",
+                L, E);
+  const int grid = moe::decision_grid(h->n_sm, 0, L, current_layer);
+  const size_t smem = moe::decision_smem(L, E, h->c.RB, 0, current_layer, grid);
+  if (smem > 220 * 1024)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "decision: shape %ux%u needs %zu B of shared memory", L,
+                E, smem);
+  // its own barrier counter: this launch runs on the caller's stream
+  a.bar = reinterpret_cast<uint32_t*>(h->dstate.as<uint8_t>() + 20);
+  a.bar_base = h->bar_base2;
+  CK(moe::launch_decision(a, h->c.cb, grid, smem, st));
+  h->bar_base2 += moe::kDecBarriers * (uint32_t)grid;
   return MOE_OK;
 }
 
@@ -2118,8 +2148,7 @@ moe_status moe_eamc_save(const moe_eamc* hc, const char* path) {
     for (uint32_t l = 0; l < c.L; ++l)
       for (uint32_t e = 0; e < c.E; ++e) {
         const uint8_t* r = rows.data() + i * LR + (uint64_t)l * c.RB;
-        snap.counts[(i * c.L + l) * c.E + e] =
-            c.cb == 1 ? r[e] : reinterpret_cast<const uint16_t*>(r)[e];
+        snap.counts[(i * c.L + l) * c.E + e] = unpack_count(r, e, c.cb);
       }
   std::string err;
   if (!moe::host::save_snapshot(path, snap, &err)) return fail(MOE_ERR_SNAPSHOT, "%s", err.c_str());
@@ -2133,7 +2162,7 @@ moe_status moe_eamc_load(const char* path, const moe_shape* expected, int device
   std::string err;
   if (!moe::host::load_snapshot(path, &snap, &err)) return fail(MOE_ERR_SNAPSHOT, "%s", err.c_str());
   const moe_shape s{snap.L, snap.E, snap.top_k};
-  if (check_shape(&s) != MOE_OK) return fail(MOE_ERR_SNAPSHOT, "corrupt snapshot: %s", g_err.c_str());
+  if (check_shape(&s) != MOE_OK) return fail(MOE_ERR_SNAPSHOT, "corrupt snapshot: %s", std::string(last_error()).c_str());
   if (snap.capacity < 1) return fail(MOE_ERR_SNAPSHOT, "corrupt snapshot: capacity must be >= 1");
   if (snap.seqs.size() > snap.capacity)
     return fail(MOE_ERR_SNAPSHOT, "snapshot holds more entries than its capacity");
@@ -2148,7 +2177,7 @@ moe_status moe_eamc_load(const char* path, const moe_shape* expected, int device
     st = moe_eamc_append(h, snap.counts.data(), snap.seqs.data(), snap.seqs.size());
   if (st != MOE_OK) {
     moe_eamc_destroy(h);
-    return st == MOE_ERR_OVERFLOW ? fail(MOE_ERR_SNAPSHOT, "snapshot counts: %s", g_err.c_str()) : st;
+    return st == MOE_ERR_OVERFLOW ? fail(MOE_ERR_SNAPSHOT, "snapshot counts: %s", std::string(last_error()).c_str()) : st;
   }
   h->next_seq = snap.next_seq;  // eam.cpp:244
   *out = h;

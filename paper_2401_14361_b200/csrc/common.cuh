@@ -122,6 +122,23 @@ struct Dot<2> {
   }
 };
 
+//  CB=4: 4 u32 counts, u64 products accumulated in u64.  Exact because every
+//        stored row has sum c^2 < 2^53 (the reference's own exactness bound,
+//        checked when rows are packed), so by Cauchy-Schwarz each dot and each
+//        partial sum is < 2^53 as well.
+template <>
+struct Dot<4> {
+  using Acc = uint64_t;
+  __device__ __forceinline__ static Acc chunk(const uint4& a, const uint4& b, Acc acc) {
+    return acc + (uint64_t)a.x * b.x + (uint64_t)a.y * b.y + (uint64_t)a.z * b.z +
+           (uint64_t)a.w * b.w;
+  }
+};
+
+// Storage-width dispatch: f<1>, f<2> or f<4> by the collection's bytes per count.
+#define MOE_CB_DISPATCH(cb, F, ...) \
+  ((cb) == 1 ? F<1>(__VA_ARGS__) : (cb) == 2 ? F<2>(__VA_ARGS__) : F<4>(__VA_ARGS__))
+
 // Reference row_similarity epilogue (eam.cpp:84-86) on exact integer sums:
 // both rows zero -> 1, one zero -> 0, else dot / (sqrt(na) * sqrt(nb)),
 // every operation IEEE round-to-nearest, no contraction.

@@ -1,0 +1,537 @@
+// decide.cu -- the fused single-probe decision kernel (K4 + K5, optional K6).
+//
+// One cooperative launch per engine decision (prefetch_priorities,
+// policy.cpp:88-126, + the engine's floor filter, engine.cpp:663-668; with
+// slot views also select_eviction_victim, policy.cpp:143-159):
+//
+//  phase A  distances of the probe to every entry (eam.cpp:91-104), thread
+//           per entry.  The per-entry in-order layer sum over the probe rows
+//           shared with the previous call is reused from pref[] (the engine
+//           calls once per layer with the iteration EAM growing by one row,
+//           engine.cpp:546, :587); only the probe's new nonzero rows need
+//           integer dots, every other row adds 1.0 or 0.0 from the entry's
+//           zero-row flag.  Block min -> atomicMin(d_min).
+//  -- grid barrier --
+//  phase B  window membership d <= d_min + window (the fp64 add of
+//           eam.cpp:143, window = kMatchWindow, policy.hpp:30) and the u64
+//           aggregation of the members' rows above the current layer
+//           (policy.cpp:97-104): members compacted per CTA, their row words
+//           spread over the CTA, one atomic per nonzero cell.
+//  -- grid barrier --
+//  phase C1 per layer i > l (CTA per layer): row sum, priorities in the
+//           reference operation order (policy.cpp:108-120), floor filter,
+//           survivors appended to a compact (key = ~bits(priority), flat
+//           ExpertId) list.  K6: cache priorities of the slot views.
+//  -- grid barrier --
+//  phase C2 every survivor's output position = the number of (key, id)
+//           pairs below it (ascending key = descending priority, ties by
+//           ExpertId: the reference's std::sort order, policy.cpp:121-124,
+//           since the pairs are unique); survivors are split over the CTAs,
+//           the list is streamed through shared memory in tiles.  K6: the
+//           victim argmin.
+//
+// Scratch state is self-cleaning: the running minimum and the survivor
+// counter are double-buffered by call parity and the kernel resets the other
+// half for the next call, so a decision is exactly one launch.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace moe {
+
+namespace {
+
+constexpr uint32_t kDecThreads = 256;
+constexpr uint32_t kDecWarpsPerCta = kDecThreads / 32;
+
+__device__ __forceinline__ bool pair_lt(unsigned long long ka, uint32_t ia, unsigned long long kb,
+                                        uint32_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Entry row zero?  zm (L <= 64) holds one bit per row; otherwise the row norm.
+__device__ __forceinline__ bool entry_row_zero(const DecisionArgs& a, uint64_t zv, uint32_t p,
+                                               uint32_t l) {
+  return a.zm ? ((zv >> l) & 1ull) != 0 : a.sqb[(uint64_t)p * a.L + l] == 0.0;
+}
+
+// Grid barrier without a cooperative launch: every CTA of the (co-resident,
+// one CTA per SM) grid adds 1 to a monotonically increasing counter and waits
+// until it reaches base + k*G for the k-th barrier of this launch.  The host
+// passes `base` (the arrivals of all earlier launches, unsigned wrap-around
+// arithmetic), so the counter is never reset and an aborted launch cannot
+// leave a half-reset state behind.  acq_rel/acquire at gpu scope order the
+// phases' global writes and reads (and invalidate stale L1 lines).
+__device__ __forceinline__ void grid_barrier(const DecisionArgs& a, uint32_t k) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(a.bar) : "memory");
+    const uint32_t target = a.bar_base + k * gridDim.x;
+    uint32_t v = old + 1;
+    while ((int32_t)(v - target) < 0) {
+      __nanosleep(20);
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void stamp(const DecisionArgs& a, int i) {
+  if (a.tprobe && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.tprobe[i] = t;
+  }
+}
+
+template <int CB>
+__global__ void __launch_bounds__(kDecThreads, 1) k_decision(const __grid_constant__ DecisionArgs a) {
+  using Acc = typename Dot<CB>::Acc;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ uint16_t nz_s[kDecMaxNz];
+  __shared__ double sqa_s[kDecMaxNz];
+  __shared__ unsigned long long wmin[kDecWarpsPerCta];
+  __shared__ uint32_t mem_s[kDecThreads];
+  __shared__ uint32_t n_mem;
+  __shared__ unsigned long long red_s[kDecWarpsPerCta];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t b = blockIdx.x, G = gridDim.x;
+  const uint32_t L = a.L, E = a.E, RB = a.RB, C = RB / 16;
+  const uint64_t LR = (uint64_t)L * RB;
+  const uint32_t par = a.parity & 1u;
+  const uint32_t rows_above = a.cur + 1 < L ? L - a.cur - 1 : 0;
+  const uint64_t n_cells = (uint64_t)rows_above * E;
+
+  // ---- phase A: distances -------------------------------------------------
+  stamp(a, 0);
+  if (b == 0 && tid == 0) a.dmin2[par ^ 1u] = ~0ull;  // the next call's running minimum
+  if (a.do_agg)
+    for (uint64_t i = (uint64_t)b * kDecThreads + tid; i < n_cells; i += (uint64_t)G * kDecThreads)
+      a.agg[(uint64_t)(a.cur + 1) * E + i] = 0ull;  // used after the first barrier
+  if (a.do_dist) {
+  // explicit probe rows -> shared memory (from the launch parameters when
+  // they fit there, else from the host-narrowed buffer), their norms
+  const uint32_t n_nz = a.n_nz;
+  const uint8_t* rows_src = a.rows_inline ? a.inline_rows : a.rows;
+  const uint16_t* nz_src = a.rows_inline ? a.inline_nz : a.nz;
+  for (uint32_t i = tid; i < n_nz; i += kDecThreads) nz_s[i] = nz_src[i];
+  uint4* prow_s = reinterpret_cast<uint4*>(dsm);
+  for (uint32_t i = tid; i < n_nz * C; i += kDecThreads)
+    prow_s[i] = reinterpret_cast<const uint4*>(rows_src)[i];
+  __syncthreads();
+  for (uint32_t r = wid; r < n_nz; r += kDecWarpsPerCta) {
+    uint64_t ss = 0;
+    const uint8_t* row = reinterpret_cast<const uint8_t*>(prow_s) + (size_t)r * RB;
+    for (uint32_t e = lane; e < E; e += 32) {
+      const uint64_t c = CB == 1 ? row[e]
+                         : CB == 2 ? reinterpret_cast<const uint16_t*>(row)[e]
+                                   : reinterpret_cast<const uint32_t*>(row)[e];
+      ss += c * c;  // exact: the host checked sum c^2 < 2^53 for every probe row
+    }
+    ss = warp_sum_u64(ss);
+    if (lane == 0) sqa_s[r] = __dsqrt_rn(__ull2double_rn(ss));  // as k_prep
+  }
+  __syncthreads();
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  double dloc = kInf;
+  const uint32_t chunk = (a.size + G - 1) / G;  // entries [b*chunk, (b+1)*chunk) per CTA
+  const uint32_t p0 = min(a.size, b * chunk), p1 = min(a.size, p0 + chunk);
+  for (uint32_t p = p0 + tid; p < p1; p += kDecThreads) {
+    const uint64_t zv = a.zm ? a.zm[p] : 0ull;
+    const double* sb = a.sqb + (uint64_t)p * L;
+    const uint4* eb = reinterpret_cast<const uint4*>(a.counts + (uint64_t)p * LR);
+    double sm = a.j0 ? a.pref[p] : 0.0;
+    uint32_t k = 0;
+    for (uint32_t l = a.j0; l <= a.hi && l < L; ++l) {
+      double r;
+      if (k < n_nz && nz_s[k] == l) {
+        Acc acc = 0;
+        const uint4* pr = prow_s + (size_t)k * C;
+        const uint4* er = eb + (size_t)l * C;
+        for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(pr[c], __ldg(er + c), acc);
+        r = row_sim_exact((uint64_t)acc, sqa_s[k], sb[l]);
+        ++k;
+      } else {
+        r = entry_row_zero(a, zv, p, l) ? 1.0 : 0.0;
+      }
+      sm = __dadd_rn(sm, r);  // layer order (eam.cpp:95-98)
+      if (l == a.keep) a.pref[p] = sm;
+    }
+    // rows above hi: zero probe rows, +1.0 per zero entry row (adding 0.0 is exact)
+    if (a.zm) {
+      uint64_t bits = a.hi + 1 < 64 ? zv & ~((2ull << a.hi) - 1ull) : 0ull;
+      if (L < 64) bits &= (1ull << L) - 1ull;
+      for (; bits; bits &= bits - 1) sm = __dadd_rn(sm, 1.0);
+    } else {
+      for (uint32_t l = a.hi + 1; l < L; ++l)
+        if (sb[l] == 0.0) sm = __dadd_rn(sm, 1.0);
+    }
+    const double d = finish_distance(sm, L);
+    a.dist[p] = d;
+    dloc = d < dloc ? d : dloc;
+  }
+  {
+    unsigned long long m = (unsigned long long)__double_as_longlong(dloc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o);
+      m = x < m ? x : m;
+    }
+    if (lane == 0) wmin[wid] = m;
+    __syncthreads();
+    if (tid == 0) {
+      for (uint32_t w = 1; w < kDecWarpsPerCta; ++w) m = wmin[w] < m ? wmin[w] : m;
+      m = wmin[0] < m ? wmin[0] : m;
+      if (m != 0x7ff0000000000000ull) atomicMin(&a.dmin2[par], m);  // non-negative doubles
+    }
+  }
+  }  // do_dist
+  stamp(a, 1);
+  grid_barrier(a, 1);
+  stamp(a, 2);
+
+  // ---- phase B: window members, u64 aggregation of their rows > cur --------
+  if (a.do_agg && rows_above) {
+    const unsigned long long dmb = a.do_dist ? a.dmin2[par] : *a.dmin_ext;
+    const double thr = __dadd_rn(__longlong_as_double((long long)dmb), a.window);
+    const uint32_t wpr = RB / 4;
+    const uint32_t per = 4 / CB;
+    const uint32_t chunk = (a.size + G - 1) / G;
+    const uint32_t p0 = min(a.size, b * chunk), p1 = min(a.size, p0 + chunk);
+    for (uint32_t base = p0; base < p1; base += kDecThreads) {
+      if (tid == 0) n_mem = 0;
+      __syncthreads();
+      const uint32_t p = base + tid;
+      if (p < p1 && a.dist[p] <= thr) mem_s[atomicAdd(&n_mem, 1u)] = p;
+      __syncthreads();
+      const uint32_t nm = n_mem;
+      const uint32_t per_mem = rows_above * wpr;
+      for (uint32_t it = tid; it < nm * per_mem; it += kDecThreads) {
+        const uint32_t mi = it / per_mem, rem = it - mi * per_mem;
+        const uint32_t r = rem / wpr, w = rem - r * wpr;
+        const uint32_t l = a.cur + 1 + r;
+        const uint32_t word = __ldg(reinterpret_cast<const uint32_t*>(
+            a.counts + (uint64_t)mem_s[mi] * LR + (uint64_t)l * RB + 4ull * w));
+        if (!word) continue;
+#pragma unroll
+        for (uint32_t j = 0; j < per; ++j) {
+          const uint32_t e = w * per + j;
+          const uint32_t c = CB == 1 ? (word >> (8 * j)) & 0xffu
+                             : CB == 2 ? (word >> (16 * j)) & 0xffffu
+                                       : word;
+          if (c && e < E) atomicAdd(&a.agg[(uint64_t)l * E + e], (unsigned long long)c);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  stamp(a, 3);
+  grid_barrier(a, 2);
+  stamp(a, 4);
+
+  // ---- phase C1: per layer i > l: priorities, floor filter, sorted segment --
+  // One CTA per layer: keys (~bits(priority): ascending = priority desc) of the
+  // layer's survivors, bitonic-sorted with their flat ExpertId as tie-break,
+  // written to the layer's segment seg[li*E ...) with its length nseg[li].
+  // Within a layer the order is the reference order restricted to that layer.
+  const double kEps = 1e-4;  // policy.hpp:22
+  {
+    uint32_t np = 1;
+    while (np < E) np <<= 1;
+    unsigned long long* sk = reinterpret_cast<unsigned long long*>(dsm);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sk + np);
+    __shared__ uint32_t n_pass;
+    for (uint32_t li = b; li < rows_above; li += G) {
+      const uint32_t l = a.cur + 1 + li;
+      const unsigned long long* ag = a.agg + (uint64_t)l * E;
+      unsigned long long sacc = 0;
+      for (uint32_t e = tid; e < E; e += kDecThreads) sacc += ag[e];
+      sacc = warp_sum_u64(sacc);
+      if (lane == 0) red_s[wid] = sacc;
+      if (tid == 0) n_pass = 0;
+      __syncthreads();
+      unsigned long long rsum = 0;
+      for (uint32_t w = 0; w < kDecWarpsPerCta; ++w) rsum += red_s[w];
+      const double prox = __dsub_rn(1.0, __ddiv_rn((double)(l - a.cur), (double)L));  // policy.cpp:110
+      const double floor_p = __dmul_rn(__dmul_rn(kEps, prox), __dadd_rn(1.0, 1e-9));   // engine.cpp:666
+      for (uint32_t e0 = 0; e0 < np; e0 += kDecThreads) {  // warp-uniform trip count (ballot)
+        const uint32_t e = e0 + tid;
+        unsigned long long key = ~0ull;
+        uint32_t id = 0xffffffffu;
+        if (e < E) {
+          const unsigned long long av = ag[e];
+          // a zero count gives priority kEps*prox, which never clears the floor
+          if (!(a.filter && av == 0)) {
+            const double ratio =
+                rsum == 0 ? 0.0 : __ddiv_rn(__ull2double_rn(av), __ull2double_rn(rsum));
+            const double pri = __dmul_rn(__dadd_rn(ratio, kEps), prox);
+            if (!(a.filter && pri <= floor_p)) {
+              key = ~(unsigned long long)__double_as_longlong(pri);
+              id = l * E + e;
+            }
+          }
+        }
+        if (e < np) {
+          sk[e] = key;
+          si[e] = id;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, key != ~0ull);
+        if (lane == 0 && m) atomicAdd(&n_pass, (uint32_t)__popc(m));
+      }
+      __syncthreads();
+      const uint32_t np_l = n_pass;
+      if (np <= 512) {
+        // small layers: each survivor's in-layer position = the number of
+        // (key, id) pairs below it (broadcast reads), one scatter
+        uint32_t pos[2] = {0, 0};
+        for (uint32_t u = 0; u < 2; ++u) {
+          const uint32_t i = tid + u * kDecThreads;
+          if (i < np && sk[i] != ~0ull)
+            for (uint32_t j = 0; j < np; ++j) pos[u] += pair_lt(sk[j], si[j], sk[i], si[i]);
+        }
+        for (uint32_t u = 0; u < 2; ++u) {
+          const uint32_t i = tid + u * kDecThreads;
+          if (i < np && sk[i] != ~0ull) {
+            a.ckey[(uint64_t)li * E + pos[u]] = sk[i];
+            a.cid[(uint64_t)li * E + pos[u]] = si[i];
+            a.crank[(uint64_t)li * E + pos[u]] = pos[u];
+          }
+        }
+        if (tid == 0) a.nseg[li] = np_l;
+        __syncthreads();
+        continue;
+      }
+      for (uint32_t k = 2; k <= np; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint32_t i = tid; i < np; i += kDecThreads) {
+            const uint32_t ixj = i ^ j;
+            if (ixj > i) {
+              const unsigned long long ki = sk[i], kj = sk[ixj];
+              const uint32_t vi = si[i], vj = si[ixj];
+              if (pair_lt(kj, vj, ki, vi) == ((i & k) == 0)) {
+                sk[i] = kj;
+                sk[ixj] = ki;
+                si[i] = vj;
+                si[ixj] = vi;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      for (uint32_t i = tid; i < np_l; i += kDecThreads) {
+        a.ckey[(uint64_t)li * E + i] = sk[i];
+        a.cid[(uint64_t)li * E + i] = si[i];
+        a.crank[(uint64_t)li * E + i] = i;  // its position inside its own layer
+      }
+      if (tid == 0) a.nseg[li] = np_l;
+      __syncthreads();
+    }
+  }
+  if (a.n_slots) {  // cache_priority of every slot view (policy.cpp:128-141)
+    for (uint32_t s = b * kDecWarpsPerCta + wid; s < a.n_slots; s += G * kDecWarpsPerCta) {
+      const moe_slot_view v = a.slots[s];
+      unsigned long long rq = 0;
+      for (uint32_t e = lane; e < E; e += 32) rq += a.req[(uint64_t)v.layer_idx * E + e];
+      rq = warp_sum_u64(rq);
+      if (lane == 0) {
+        const double ratio =
+            rq == 0 ? 0.0
+                    : __ddiv_rn(__ull2double_rn(a.req[(uint64_t)v.layer_idx * E + v.expert_idx]),
+                                __ull2double_rn(rq));
+        const double w = __dsub_rn(1.0, __ddiv_rn((double)v.layer_idx, (double)L));
+        a.slot_pri[s] = __dmul_rn(__dadd_rn(ratio, kEps), w);
+      }
+    }
+  }
+  stamp(a, 5);
+  grid_barrier(a, 3);
+  stamp(a, 6);
+
+  // ---- phase C2: cross-layer ranks -----------------------------------------
+  // A survivor's output position = its position in its own layer + for every
+  // other layer j the number of j's (key, id) pairs below it (ascending key =
+  // descending priority, ties by ExpertId: the reference's std::sort order,
+  // policy.cpp:121-124; the pairs are unique).  The CTA holding layer j in
+  // shared memory binary-searches every other survivor in it and adds the
+  // count to that survivor's rank.
+  __shared__ uint32_t offs[kDecMaxLayers + 1];
+  if (rows_above > kDecMaxLayers) __trap();  // host checks the bound
+  if (tid == 0) {
+    uint32_t o = 0;
+    for (uint32_t i = 0; i < rows_above; ++i) {
+      offs[i] = o;
+      o += a.nseg[i];
+    }
+    offs[rows_above] = o;
+  }
+  __syncthreads();
+  const uint32_t S = offs[rows_above];
+  if (b == 0 && tid == 0) *a.n_out = S;
+  {
+    unsigned long long* tk = reinterpret_cast<unsigned long long*>(dsm);
+    uint32_t* ti = reinterpret_cast<uint32_t*>(tk + E);
+    for (uint32_t lj = b; lj < rows_above; lj += G) {
+      const uint32_t nj = a.nseg[lj];
+      __syncthreads();
+      for (uint32_t i = tid; i < nj; i += kDecThreads) {
+        tk[i] = a.ckey[(uint64_t)lj * E + i];
+        ti[i] = a.cid[(uint64_t)lj * E + i];
+      }
+      __syncthreads();
+      if (nj == 0) continue;
+      // flat survivors t = offs[li] + pos, four per thread per round with their
+      // loads issued together
+      for (uint32_t t0 = 0; t0 < S; t0 += 4 * kDecThreads) {
+        uint64_t slot[4];
+        unsigned long long kx[4];
+        uint32_t ix[4];
+        bool act[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t t = t0 + u * kDecThreads + tid;
+          uint32_t li = 0, hi2 = rows_above;  // segment of t: offs[li] <= t < offs[li+1]
+          while (hi2 - li > 1) {
+            const uint32_t mid = (li + hi2) >> 1;
+            if (offs[mid] <= t) li = mid; else hi2 = mid;
+          }
+          act[u] = t < S && li != lj;
+          slot[u] = (uint64_t)li * E + (t - offs[li]);
+          if (act[u]) {
+            kx[u] = a.ckey[slot[u]];
+            ix[u] = a.cid[slot[u]];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (!act[u]) continue;
+          uint32_t lo = 0, hb = nj;  // count of (tk, ti) < (kx, ix)
+          while (lo < hb) {
+            const uint32_t mid = (lo + hb) >> 1;
+            if (pair_lt(tk[mid], ti[mid], kx[u], ix[u])) lo = mid + 1; else hb = mid;
+          }
+          if (lo) atomicAdd(&a.crank[slot[u]], lo);
+        }
+      }
+    }
+  }
+  stamp(a, 7);
+  grid_barrier(a, 4);
+
+  // ---- phase C3: scatter to the output positions ----------------------------
+  for (uint32_t li = b; li < rows_above; li += G)
+  for (uint32_t pos = tid; pos < offs[li + 1] - offs[li]; pos += kDecThreads) {
+    const uint64_t slot = (uint64_t)li * E + pos;
+    const unsigned long long key = a.ckey[slot];
+    const uint32_t id = a.cid[slot];
+    moe_candidate o;
+    o.layer_idx = id / E;
+    o.expert_idx = id - o.layer_idx * E;
+    o.priority = __longlong_as_double((long long)~key);
+    a.out[a.crank[slot]] = o;
+  }
+
+  if (a.n_slots && a.victim && b == G - 1) {
+    // select_eviction_victim: argmin (cache_priority, ExpertId) over slots
+    // neither prefetch-protected nor pinned (policy.cpp:143-159)
+    double bp = 0.0;
+    uint64_t bk = ~0ull;
+    long long bs = -1;
+    for (uint32_t i = tid; i < a.n_slots; i += kDecThreads) {
+      const moe_slot_view v = a.slots[i];
+      if (v.prefetch_protected || v.pinned) continue;
+      const double p = a.slot_pri[i];
+      const uint64_t k = ((uint64_t)v.layer_idx << 32) | v.expert_idx;
+      if (bs < 0 || p < bp || (p == bp && k < bk)) {
+        bp = p;
+        bk = k;
+        bs = (long long)v.slot;
+      }
+    }
+    __shared__ double vp[kDecWarpsPerCta];
+    __shared__ uint64_t vk[kDecWarpsPerCta];
+    __shared__ long long vs[kDecWarpsPerCta];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const long long os = __shfl_xor_sync(0xffffffffu, bs, o);
+      if (os >= 0 && (bs < 0 || op < bp || (op == bp && ok < bk))) {
+        bp = op;
+        bk = ok;
+        bs = os;
+      }
+    }
+    if (lane == 0) {
+      vp[wid] = bp;
+      vk[wid] = bk;
+      vs[wid] = bs;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (uint32_t w = 1; w < kDecWarpsPerCta; ++w)
+        if (vs[w] >= 0 && (bs < 0 || vp[w] < bp || (vp[w] == bp && vk[w] < bk))) {
+          bp = vp[w];
+          bk = vk[w];
+          bs = vs[w];
+        }
+      *a.victim = bs;
+    }
+  }
+}
+
+}  // namespace
+
+size_t decision_smem(uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz, uint32_t cur,
+                     uint32_t grid) {
+  (void)L;
+  (void)cur;
+  (void)grid;
+  uint32_t np = 1;
+  while (np < E) np <<= 1;
+  return std::max((size_t)n_nz * RB, (size_t)np * 12);  // staged probe rows | a layer's segment
+}
+
+int decision_grid(int n_sm, uint32_t size, uint32_t L, uint32_t cur) {
+  const uint32_t rows = cur + 1 < L ? L - cur - 1 : 0;
+  uint32_t g = std::max<uint32_t>({(size + 63) / 64, rows, 8u});
+  return (int)std::min<uint32_t>(g, (uint32_t)n_sm);
+}
+
+cudaError_t launch_decision(const DecisionArgs& a, int cb, int grid, size_t smem,
+                            cudaStream_t st) {
+  void (*kern)(DecisionArgs) = cb == 1 ? k_decision<1> : cb == 2 ? k_decision<2> : k_decision<4>;
+  // opt in once to the largest dynamic size the callers use (static + dynamic
+  // shared memory above 48 KB needs it, and the co-residency check of a
+  // cooperative launch counts both)
+  static size_t max_dyn[3] = {0, 0, 0};
+  const int slot = cb == 1 ? 0 : cb == 2 ? 1 : 2;
+  if (!max_dyn[slot]) {
+    int dev = 0, optin = 0;
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess)
+      e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kern);
+    const size_t lim = (size_t)optin - fa.sharedSizeBytes;
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+    if (e != cudaSuccess) return e;
+    max_dyn[slot] = lim;
+  }
+  if (smem > max_dyn[slot]) return cudaErrorInvalidValue;
+  // grid <= SMs and one CTA per SM (launch bounds, shared memory): all CTAs
+  // are co-resident once scheduled, which the software barrier relies on
+  kern<<<(unsigned)grid, kDecThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace moe

@@ -716,15 +716,17 @@ void pack_task(void* vc, int t) {
   // 64-element aligned piece boundaries
   const uint64_t a = (c->n * t / c->parts) & ~63ull;
   const uint64_t b = t + 1 == c->parts ? c->n : (c->n * (t + 1) / c->parts) & ~63ull;
-  c->ors[t] = c->cb == 1 ? pack_range(c->src + a, static_cast<uint8_t*>(c->dst) + a, b - a)
-                         : pack_range(c->src + a, static_cast<uint16_t*>(c->dst) + a, b - a);
+  c->ors[t] = c->cb == 1   ? pack_range(c->src + a, static_cast<uint8_t*>(c->dst) + a, b - a)
+              : c->cb == 2 ? pack_range(c->src + a, static_cast<uint16_t*>(c->dst) + a, b - a)
+                           : pack_range(c->src + a, static_cast<uint32_t*>(c->dst) + a, b - a);
 }
 
 }  // namespace
 
 uint64_t pack_counts_serial(const uint64_t* src, uint64_t n, int cb, void* dst) {
-  return cb == 1 ? pack_range(src, static_cast<uint8_t*>(dst), n)
-                 : pack_range(src, static_cast<uint16_t*>(dst), n);
+  return cb == 1   ? pack_range(src, static_cast<uint8_t*>(dst), n)
+         : cb == 2 ? pack_range(src, static_cast<uint16_t*>(dst), n)
+                   : pack_range(src, static_cast<uint32_t*>(dst), n);
 }
 
 int pool_threads() { return pool().size(); }

@@ -55,7 +55,7 @@ void pool_run(int n, void (*fn)(void*, int), void* ctx);
 void pool_submit(int n, void (*fn)(void*, int), void* ctx);
 void pool_wait();
 
-// Narrow n u64 counts to cb (1 or 2) bytes, in parallel on the pool.
+// Narrow n u64 counts to cb (1, 2 or 4) bytes, in parallel on the pool.
 // Returns the bitwise OR of all inputs: the caller's width check is
 // `or > width_max(cb)` (exactly "some count exceeds the width").
 uint64_t pack_counts(const uint64_t* src, uint64_t n, int cb, void* dst);

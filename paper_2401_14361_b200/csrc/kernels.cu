@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <map>
 #include <tuple>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -588,6 +589,66 @@ __global__ void k_merge_partials(const moe_match* parts, uint32_t grid, uint32_t
     out[qlist[qi]] = moe_match{b.idx == kNone ? kNone : b.idx + index_base, b.seq, b.d};
 }
 
+// Exact argmin without the TMA pipeline (shapes whose rows do not fit the
+// matcher's shared-memory tiles, e.g. wide u32 rows): warp per (listed probe,
+// entry), warp_exact_distance in the reference operation order, block argmin
+// -> parts[qi][blockIdx.x]; k_merge_blocks folds the blocks.
+template <int CB>
+__global__ void __launch_bounds__(256)
+    k_exact_warp(const uint8_t* counts, const double* sqb, const uint64_t* seq, uint32_t size,
+                 uint32_t L, uint32_t C, uint32_t RB, const uint8_t* probes, const double* sqa,
+                 const uint32_t* qlist, uint32_t nq_list, const uint32_t* nq_dev, uint32_t q_off,
+                 moe_match* parts) {
+  pdl_wait();
+  pdl_trigger();
+  uint32_t nq = nq_list;
+  if (nq_dev) {
+    const uint32_t tot = *nq_dev;
+    nq = tot > q_off ? min(tot - q_off, nq_list) : 0u;
+  }
+  const uint32_t qi = blockIdx.y;
+  if (qi >= nq) return;
+  const uint32_t q = qlist[qi];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint64_t LR = (uint64_t)L * RB;
+  Best b{__longlong_as_double(0x7ff0000000000000ll), kNone, kNone};
+  for (uint32_t p = blockIdx.x * nw + wib; p < size; p += gridDim.x * nw) {
+    const double d = warp_exact_distance<CB>(probes + (uint64_t)q * LR, sqa + (uint64_t)q * L,
+                                             counts + (uint64_t)p * LR, sqb + (uint64_t)p * L, L,
+                                             C, RB);
+    const uint64_t sq = seq[p];
+    if (better(d, sq, b.d, b.seq)) b = Best{d, sq, p};
+  }
+  __shared__ Best wb[8];
+  if (lane == 0) wb[wib] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < nw; ++w)
+      if (better(wb[w].d, wb[w].seq, b.d, b.seq)) b = wb[w];
+    parts[(uint64_t)qi * gridDim.x + blockIdx.x] = moe_match{b.idx, b.seq, b.d};
+  }
+}
+
+__global__ void k_merge_blocks(const moe_match* parts, uint32_t nb, const uint32_t* qlist,
+                               uint32_t nq_list, const uint32_t* nq_dev, uint32_t q_off,
+                               moe_match* out, uint64_t index_base) {
+  pdl_wait();
+  pdl_trigger();
+  uint32_t nq = nq_list;
+  if (nq_dev) {
+    const uint32_t tot = *nq_dev;
+    nq = tot > q_off ? min(tot - q_off, nq_list) : 0u;
+  }
+  const uint32_t qi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= nq) return;
+  moe_match b = parts[(uint64_t)qi * nb];
+  for (uint32_t k = 1; k < nb; ++k) {
+    const moe_match m = parts[(uint64_t)qi * nb + k];
+    if (better(m.distance, m.seq, b.distance, b.seq)) b = m;
+  }
+  out[qlist[qi]] = moe_match{b.index == kNone ? kNone : b.index + index_base, b.seq, b.distance};
+}
+
 __global__ void k_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out) {
   const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (q >= n) return;
@@ -615,10 +676,14 @@ __global__ void k_pair_distance(const uint8_t* a, const double* sqa, const uint8
 }
 
 // u64 / u16 / u8 counts -> packed rows of cb-byte counts + sqrt(sum c^2)
-// and fp32 1/sqrt(sum c^2); one warp per row.
+// and fp32 1/sqrt(sum c^2); one warp per row.  Rows with sum c^2 >= 2^53
+// (where the reference's own fp64 sums stop being exact, eam.cpp:75-87)
+// report ~0 as their max count: MOE_ERR_OVERFLOW on the host.
+constexpr uint64_t kNormLimit = 1ull << 53;
 template <int SRC>
 __device__ __forceinline__ uint64_t load_count(const void* src, uint64_t i) {
   if (SRC == 8) return reinterpret_cast<const uint64_t*>(src)[i];
+  if (SRC == 4) return reinterpret_cast<const uint32_t*>(src)[i];
   if (SRC == 2) return reinterpret_cast<const uint16_t*>(src)[i];
   return reinterpret_cast<const uint8_t*>(src)[i];
 }
@@ -671,8 +736,10 @@ __global__ void __launch_bounds__(256)
         if (e < E) {
           const uint64_t c = load_count<SRC>(src, sbase + e);
           mx = c > mx ? c : mx;
-          ss += c * c;  // exact: counts above 65535 are rejected by the caller
-          const uint64_t cc = cb == 1 ? (c & 0xffu) : (c & 0xffffu);
+          // saturating at 2^53: a row at or above it is outside the range the
+          // reference's fp64 sums are exact in (flagged below)
+          ss = c >= (1ull << 27) ? kNormLimit : min(ss + c * c, kNormLimit);
+          const uint64_t cc = cb == 1 ? (c & 0xffu) : cb == 2 ? (c & 0xffffu) : (c & 0xffffffffu);
           word |= (uint32_t)cc << (8 * cb * j);
         }
       }
@@ -681,7 +748,8 @@ __global__ void __launch_bounds__(256)
     if (k < kWords) words[k] = word;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);  // < 2^58
+  if (ss >= kNormLimit) mx = ~0ull;  // sum c^2 >= 2^53: no storage width represents it exactly
   if (mx > width_limit) {
     if (max_count) atomicMax(max_count, (unsigned long long)mx);
     if (wide) wide[it] = 1;  // this EAM does not fit the storage width
@@ -703,8 +771,9 @@ __global__ void __launch_bounds__(256)
         for (uint32_t j = 0; j < per_word; ++j) {
           const uint32_t e = w * per_word + j;
           if (e < E) {
-            const uint32_t c =
-                cb == 1 ? (word >> (8 * j)) & 0xffu : (word >> (16 * j)) & 0xffffu;
+            const uint32_t c = cb == 1 ? (word >> (8 * j)) & 0xffu
+                               : cb == 2 ? (word >> (16 * j)) & 0xffffu
+                                         : word;
             o[e] = __float2half_rn(__uint2float_rn(c) * inv);
           }
         }
@@ -1283,14 +1352,23 @@ __global__ void k_append_staged(uint8_t* counts, float* ibT, double* sqb, uint64
   }
 }
 
+// Re-encode rows of cb_old-byte counts as cb_new-byte counts (padding zero).
 __global__ void k_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32_t RB_old,
-                        uint32_t RB_new) {
-  for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < rows * (RB_new / 2);
+                        uint32_t RB_new, int cb_old, int cb_new) {
+  const uint32_t n_old = RB_old / cb_old, n_new = RB_new / cb_new;
+  for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < rows * n_new;
        o += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t r = o / (RB_new / 2);
-    const uint32_t e = (uint32_t)(o % (RB_new / 2));
-    const uint16_t v = e < RB_old ? src[r * RB_old + e] : 0;
-    reinterpret_cast<uint16_t*>(dst + r * RB_new)[e] = v;
+    const uint64_t r = o / n_new;
+    const uint32_t e = (uint32_t)(o % n_new);
+    uint32_t v = 0;
+    if (e < n_old) {
+      const uint8_t* so = src + r * RB_old;
+      v = cb_old == 1 ? so[e] : cb_old == 2 ? reinterpret_cast<const uint16_t*>(so)[e]
+                                            : reinterpret_cast<const uint32_t*>(so)[e];
+    }
+    uint8_t* d = dst + r * RB_new;
+    if (cb_new == 2) reinterpret_cast<uint16_t*>(d)[e] = (uint16_t)v;
+    else reinterpret_cast<uint32_t*>(d)[e] = v;
   }
 }
 
@@ -1324,337 +1402,6 @@ __global__ void __launch_bounds__(256)
     for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(ra[c], __ldg(&rb[c]), acc);
     r[p * L + l] = row_sim_exact((uint64_t)acc, sqa[l], sqb[p * L + l]);
   }
-}
-
-// Decision-path distances of ONE probe to every entry (the window pass of
-// match_within / prefetch_priorities, eam.cpp:131-150), warp per entry.
-// The per-entry layer sum S is carried over from the previous call through
-// pref[p] for rows [0, j0) (the caller guarantees the probe's rows [0, j0)
-// equal those of the probe that produced pref, and that the collection did
-// not change), so only rows j0..L-1 are evaluated: the probe rows listed in
-// nz (its nonzero rows >= j0) by exact integer dots + the fp64 row
-// similarity, the others from the entry's zero-row flag alone (sqb == 0:
-// both zero -> 1, else 0; eam.cpp:82-83).  S is then summed in layer order
-// (eam.cpp:95-98) and stored at row `keep` for the next call.  Block min ->
-// atomicMin(*dmin) on the distance bits.
-constexpr uint32_t kDecWarps = 4;
-constexpr uint32_t kDecParts = 256;  // per-warp partial-dot scratch (u32 or u64 entries)
-
-template <int CB>
-__global__ void __launch_bounds__(kDecWarps * 32)
-    k_dec_dist(const uint8_t* counts, const double* sqb, const uint64_t* zm, uint32_t size,
-               uint32_t L, uint32_t C, uint32_t RB, const uint8_t* probe, const double* sqa,
-               const uint16_t* nz, uint32_t n_nz, uint32_t j0, uint32_t hi, uint32_t keep,
-               double* pref, double* dist, unsigned long long* dmin,
-               unsigned long long* zero_agg, uint32_t n_agg, uint32_t* zero_cnt) {
-  pdl_wait();
-  pdl_trigger();
-  // Rows [j0, hi] are evaluated explicitly (hi >= every nonzero probe row and
-  // >= keep when keep < L); rows above hi have zero probe rows, so each adds
-  // 1.0 if the entry row is zero and 0.0 otherwise -- adding 0.0 leaves the
-  // sum unchanged, so with the entry's zero-row mask (zm, L <= 64) the tail
-  // is one in-order "+1.0" per zero row instead of a walk over every row.
-  using Acc = typename Dot<CB>::Acc;
-  __shared__ Acc part[kDecWarps][kDecParts];
-  __shared__ double rbuf[kDecWarps][256];
-  __shared__ unsigned long long bmin[kDecWarps];
-  const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t p = blockIdx.x * kDecWarps + wib;
-  // the follow-up kernels' accumulators (members count, u64 aggregate)
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_agg; i += gridDim.x * blockDim.x)
-    zero_agg[i] = 0ull;
-  if (zero_cnt && blockIdx.x == 0 && threadIdx.x == 0) *zero_cnt = 0;
-  double d = __longlong_as_double(0x7ff0000000000000ll);
-  if (p < size) {
-    const uint64_t LR = (uint64_t)L * RB;
-    const uint4* eb = reinterpret_cast<const uint4*>(counts + p * LR);
-    const uint4* pb = reinterpret_cast<const uint4*>(probe);
-    const double* sb = sqb + (uint64_t)p * L;
-    const uint64_t zv = zm ? zm[p] : 0ull;
-    const double s0 = j0 ? pref[p] : 0.0;
-    for (uint32_t l = j0 + lane; l <= hi && l < L; l += 32)
-      rbuf[wib][l] = (zm ? ((zv >> l) & 1ull) != 0 : sb[l] == 0.0) ? 1.0 : 0.0;
-    const uint32_t rows_per = max(1u, kDecParts / C);
-    for (uint32_t r0 = 0; r0 < n_nz; r0 += rows_per) {
-      const uint32_t nr = min(rows_per, n_nz - r0);
-      const uint32_t items = nr * C;
-      __syncwarp();
-#pragma unroll 4
-      for (uint32_t it = lane; it < items; it += 32) {
-        const uint32_t ri = it / C, c = it - ri * C;
-        const uint32_t l = nz[r0 + ri];
-        const uint32_t off = l * (RB / 16) + c;
-        part[wib][it] = Dot<CB>::chunk(__ldg(pb + off), __ldg(eb + off), (Acc)0);
-      }
-      __syncwarp();
-      for (uint32_t ri = lane; ri < nr; ri += 32) {
-        const uint32_t l = nz[r0 + ri];
-        uint64_t dot = 0;
-        for (uint32_t c = 0; c < C; ++c) dot += (uint64_t)part[wib][ri * C + c];
-        rbuf[wib][l] = row_sim_exact(dot, sqa[l], sb[l]);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      double sm = s0;
-      for (uint32_t l = j0; l <= hi && l < L; ++l) {
-        sm = __dadd_rn(sm, rbuf[wib][l]);
-        if (l == keep) pref[p] = sm;
-      }
-      if (zm) {
-        uint64_t bits = hi + 1 < 64 ? zv & ~((2ull << hi) - 1ull) : 0ull;
-        if (L < 64) bits &= (1ull << L) - 1ull;
-        for (; bits; bits &= bits - 1) sm = __dadd_rn(sm, 1.0);
-      } else {
-        for (uint32_t l = hi + 1; l < L; ++l)
-          if (sb[l] == 0.0) sm = __dadd_rn(sm, 1.0);
-      }
-      d = finish_distance(sm, L);
-      dist[p] = d;
-    }
-  }
-  if (lane == 0) bmin[wib] = (unsigned long long)__double_as_longlong(d);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long b = bmin[0];
-    for (uint32_t w = 1; w < kDecWarps; ++w) b = bmin[w] < b ? bmin[w] : b;
-    if (b != 0x7ff0000000000000ull) atomicMin(dmin, b);
-  }
-}
-
-// Thread-per-entry variant of k_dec_dist for the engine's common case: at
-// most a few explicit rows (the probe's new row, L <= 64, entry zero-row
-// masks available).  One thread walks rows [j0, hi] of its entry (dots only
-// for the rows in nzmask) and the zero-row tail; no shared memory, no
-// per-warp fixed cost.  Same arithmetic and order as k_dec_dist.
-template <int CB>
-__global__ void __launch_bounds__(256)
-    k_dec_dist_t(const uint8_t* counts, const double* sqb, const uint64_t* zm, uint32_t size,
-                 uint32_t L, uint32_t C, uint32_t RB, const uint8_t* probe, const double* sqa,
-                 uint64_t nzmask, uint32_t j0, uint32_t hi, uint32_t keep, double* pref,
-                 double* dist, unsigned long long* dmin, unsigned long long* zero_agg,
-                 uint32_t n_agg, uint32_t* zero_cnt) {
-  pdl_wait();
-  pdl_trigger();
-  const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  for (uint32_t i = gtid; i < n_agg; i += gridDim.x * blockDim.x) zero_agg[i] = 0ull;
-  if (zero_cnt && gtid == 0) *zero_cnt = 0;
-  const uint32_t p = gtid;
-  double d = __longlong_as_double(0x7ff0000000000000ll);
-  if (p < size) {
-    const uint64_t LR = (uint64_t)L * RB;
-    const uint64_t zv = zm[p];
-    double sm = j0 ? pref[p] : 0.0;
-    for (uint32_t l = j0; l <= hi && l < L; ++l) {
-      double r;
-      if ((nzmask >> l) & 1ull) {
-        const uint4* ra = reinterpret_cast<const uint4*>(probe + (uint64_t)l * RB);
-        const uint4* rb = reinterpret_cast<const uint4*>(counts + p * LR + (uint64_t)l * RB);
-        typename Dot<CB>::Acc acc = 0;
-        for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(__ldg(ra + c), __ldg(rb + c), acc);
-        r = row_sim_exact((uint64_t)acc, sqa[l], sqb[(uint64_t)p * L + l]);
-      } else {
-        r = ((zv >> l) & 1ull) ? 1.0 : 0.0;
-      }
-      sm = __dadd_rn(sm, r);
-      if (l == keep) pref[p] = sm;
-    }
-    uint64_t bits = hi + 1 < 64 ? zv & ~((2ull << hi) - 1ull) : 0ull;
-    if (L < 64) bits &= (1ull << L) - 1ull;
-    for (; bits; bits &= bits - 1) sm = __dadd_rn(sm, 1.0);
-    d = finish_distance(sm, L);
-    dist[p] = d;
-  }
-  unsigned long long b = (unsigned long long)__double_as_longlong(d);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long x = __shfl_xor_sync(0xffffffffu, b, o);
-    b = x < b ? x : b;
-  }
-  __shared__ unsigned long long wmin[8];
-  if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = b;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (uint32_t w = 1; w < (blockDim.x >> 5); ++w) b = wmin[w] < b ? wmin[w] : b;
-    b = wmin[0] < b ? wmin[0] : b;
-    if (b != 0x7ff0000000000000ull) atomicMin(dmin, b);
-  }
-}
-
-// Priorities, floor filter and the full (priority desc, ExpertId asc) order
-// of the candidates of layers cur+1..L-1 (policy.cpp:106-124,
-// engine.cpp:663-668).  k_order (one block): per-layer row sums, priorities
-// in the reference's operation order, surviving candidates compacted to
-// (key = ~bits(priority), flat ExpertId) -- ascending (key, id) is the
-// reference order and the pairs are unique, so a candidate's output position
-// is the number of pairs below it.  Up to kRankSmall survivors are ranked in
-// the same block (every thread scans the shared-memory list; the reads are
-// broadcasts); more are ranked by k_rank over a 2-D grid of (candidate tile,
-// key tile) blocks, the last block scattering the result.
-constexpr uint32_t kRankSmall = 1024;
-
-__device__ __forceinline__ bool pair_less(unsigned long long ka, uint32_t ia,
-                                          unsigned long long kb, uint32_t ib) {
-  return ka < kb || (ka == kb && ia < ib);
-}
-
-__device__ __forceinline__ moe_candidate make_cand(unsigned long long key, uint32_t id,
-                                                   uint32_t E) {
-  moe_candidate c;
-  c.layer_idx = id / E;
-  c.expert_idx = id - c.layer_idx * E;
-  c.priority = __longlong_as_double((long long)~key);
-  return c;
-}
-
-__global__ void __launch_bounds__(1024)
-    k_order(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur, int filter,
-            moe_candidate* out, uint32_t* n_out, unsigned long long* gkey, uint32_t* gid,
-            uint32_t* grank, uint32_t* big) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ unsigned long long key[kRankSmall];
-  __shared__ uint32_t id[kRankSmall];
-  __shared__ unsigned long long rs[256];
-  __shared__ double px[256];
-  __shared__ uint32_t cnt;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  const double kEps = 1e-4;  // policy.hpp:22
-  if (tid == 0) cnt = 0;
-  for (uint32_t l = cur + 1 + wid; l < L; l += nw) {
-    unsigned long long a = 0;
-    for (uint32_t e = lane; e < E; e += 32) a += agg[(uint64_t)l * E + e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) {
-      rs[l] = a;
-      px[l] = __dsub_rn(1.0, __ddiv_rn((double)(l - cur), (double)L));  // policy.cpp:110
-    }
-  }
-  __syncthreads();
-  const uint32_t n = (L - cur - 1) * E;
-  const unsigned long long* ag = agg + (uint64_t)(cur + 1) * E;  // candidate i <-> ag[i]
-  constexpr int kPre = 16;  // all loads of a thread in flight at once (n <= 16 * 1024)
-  unsigned long long av[kPre];
-#pragma unroll
-  for (int k = 0; k < kPre; ++k) {
-    const uint32_t i = tid + k * blockDim.x;
-    av[k] = i < n ? ag[i] : 0ull;
-  }
-  // survivors get their slots by one shared atomic per warp (ballot + popc),
-  // not one per candidate on a single shared counter
-#pragma unroll
-  for (int u = 0; u < kPre; ++u) {
-    if (u * blockDim.x >= n) break;  // block-uniform: every lane stays for the ballot
-    const uint32_t i = tid + u * blockDim.x;
-    bool pass = false;
-    unsigned long long k = 0;
-    uint32_t flat = 0;
-    if (i < n) {
-      const uint32_t li = i / E, e = i - li * E;
-      const uint32_t l = cur + 1 + li;
-      const double prox = px[l];
-      const unsigned long long a = av[u];
-      // a zero count gives priority kEps*prox, which never clears the floor
-      // kEps*prox*(1+1e-9) (rounding is monotone)
-      if (!(filter && a == 0)) {
-        const double ratio =
-            rs[l] == 0 ? 0.0 : __ddiv_rn(__ull2double_rn(a), __ull2double_rn(rs[l]));
-        const double pri = __dmul_rn(__dadd_rn(ratio, kEps), prox);
-        pass = !(filter && pri <= __dmul_rn(__dmul_rn(kEps, prox), __dadd_rn(1.0, 1e-9)));
-        k = ~(unsigned long long)__double_as_longlong(pri);
-        flat = l * E + e;
-      }
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, pass);
-    if (m == 0) continue;
-    uint32_t base = 0;
-    if (lane == (uint32_t)(__ffs(m) - 1)) base = atomicAdd(&cnt, (uint32_t)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-    if (pass) {
-      const uint32_t pos = base + __popc(m & ((1u << lane) - 1));
-      if (pos < kRankSmall) {
-        key[pos] = k;
-        id[pos] = flat;
-      }
-      gkey[pos] = k;
-      gid[pos] = flat;
-      grank[pos] = 0;
-    }
-  }
-  __syncthreads();
-  const uint32_t ns = cnt;
-  if (tid == 0) {
-    *n_out = ns;
-    *big = ns > kRankSmall;
-  }
-  if (ns > kRankSmall) return;
-  // bitonic sort of the (key, id) pairs in shared memory (np <= 1024: one
-  // compare-exchange per thread per stage)
-  uint32_t np = 1;
-  while (np < ns) np <<= 1;
-  if (tid >= ns && tid < np) {
-    key[tid] = ~0ull;
-    id[tid] = 0xffffffffu;
-  }
-  __syncthreads();
-  for (uint32_t k = 2; k <= np; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      const uint32_t i = tid, ixj = i ^ j;
-      if (i < np && ixj > i) {
-        const bool up = (i & k) == 0;
-        const unsigned long long ki = key[i], kj = key[ixj];
-        const uint32_t vi = id[i], vj = id[ixj];
-        if (pair_less(kj, vj, ki, vi) == up) {
-          key[i] = kj;
-          key[ixj] = ki;
-          id[i] = vj;
-          id[ixj] = vi;
-        }
-      }
-      __syncthreads();
-    }
-  if (tid < ns) out[tid] = make_cand(key[tid], id[tid], E);
-}
-
-__global__ void __launch_bounds__(256)
-    k_rank(const unsigned long long* gkey, const uint32_t* gid, const uint32_t* n_dev,
-           const uint32_t* big, uint32_t* grank) {
-  pdl_wait();
-  pdl_trigger();
-  if (*big == 0) return;
-  __shared__ unsigned long long tk[1024];
-  __shared__ uint32_t ti[1024];
-  const uint32_t ns = *n_dev;
-  const uint32_t j0 = blockIdx.y * 1024;
-  const uint32_t i = blockIdx.x * 256 + threadIdx.x;
-  if (blockIdx.x * 256 < ns && j0 < ns) {
-    const uint32_t nj = min(1024u, ns - j0);
-    for (uint32_t j = threadIdx.x; j < nj; j += 256) {
-      tk[j] = gkey[j0 + j];
-      ti[j] = gid[j0 + j];
-    }
-    __syncthreads();
-    if (i < ns) {
-      const unsigned long long k = gkey[i];
-      const uint32_t v = gid[i];
-      uint32_t r = 0;
-      for (uint32_t j = 0; j < nj; ++j) r += pair_less(tk[j], ti[j], k, v);
-      if (r) atomicAdd(&grank[i], r);
-    }
-  }
-}
-
-// Long survivor lists, second pass: every candidate to its rank (all counts
-// of k_rank are complete: PDL's griddepcontrol.wait orders the two grids).
-__global__ void __launch_bounds__(256)
-    k_rank_scatter(const unsigned long long* gkey, const uint32_t* gid, const uint32_t* n_dev,
-                   const uint32_t* big, uint32_t E, const uint32_t* grank, moe_candidate* out) {
-  pdl_wait();
-  pdl_trigger();
-  if (*big == 0) return;
-  const uint32_t i = blockIdx.x * 256 + threadIdx.x;
-  if (i < *n_dev) out[grank[i]] = make_cand(gkey[i], gid[i], E);
 }
 
 // In-order layer sum (eam.cpp:95-103) -> dist[p]; warp min -> atomicMin(*dmin).
@@ -1708,7 +1455,9 @@ __global__ void __launch_bounds__(256)
   const uint32_t r = w / wpr, wi = w - r * wpr;
   const uint64_t off = (uint64_t)(cur + 1 + r) * RB + 4ull * wi;
   const uint64_t LR = (uint64_t)L * RB;
-  uint32_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;  // per-cell partial sums (<= chunk * 65535)
+  // per-cell partial sums (u32 for 1-2 byte counts: <= chunk * 65535; u64 for u32 counts)
+  using Sum = typename std::conditional<CB == 4, uint64_t, uint32_t>::type;
+  Sum s0 = 0, s1 = 0, s2 = 0, s3 = 0;
   uint32_t m = m0;
   for (; m + 4 <= m1; m += 4) {
     uint32_t v[4];
@@ -1722,9 +1471,11 @@ __global__ void __launch_bounds__(256)
         s1 += (v[k] >> 8) & 0xffu;
         s2 += (v[k] >> 16) & 0xffu;
         s3 += v[k] >> 24;
-      } else {
+      } else if (CB == 2) {
         s0 += v[k] & 0xffffu;
         s1 += v[k] >> 16;
+      } else {
+        s0 += v[k];
       }
     }
   }
@@ -1735,126 +1486,19 @@ __global__ void __launch_bounds__(256)
       s1 += (v >> 8) & 0xffu;
       s2 += (v >> 16) & 0xffu;
       s3 += v >> 24;
-    } else {
+    } else if (CB == 2) {
       s0 += v & 0xffffu;
       s1 += v >> 16;
+    } else {
+      s0 += v;
     }
   }
   const uint32_t per = 4 / CB;
   const uint32_t e0 = wi * per;
   const uint64_t base = (uint64_t)(cur + 1 + r) * E;
-  const uint32_t sums[4] = {s0, s1, s2, s3};
+  const Sum sums[4] = {s0, s1, s2, s3};
   for (uint32_t k = 0; k < per; ++k)
     if (e0 + k < E && sums[k]) atomicAdd(&agg[base + e0 + k], (unsigned long long)sums[k]);
-}
-
-// Priorities (policy.cpp:106-120) + floor filter (engine.cpp:663-668) of
-// every expert of layer cur+1+blockIdx.x; the block then sorts its layer by
-// (priority desc, expert asc) -- within one layer priority is monotone in the
-// aggregated count -- and writes the sorted keys (filtered-out experts get
-// the max key) to the layer's segment.  Keys are ~bits(priority): ascending
-// key = descending priority; priorities are > 0 so no real key is ~0.
-__global__ void __launch_bounds__(1024)
-    k_layer_sort(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur, int filter,
-                 unsigned long long* keys, uint32_t* n_out) {
-  extern __shared__ unsigned long long sk[];  // [np] keys, then [np] u32 expert ids
-  uint32_t np = 1;
-  while (np < E) np <<= 1;
-  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + np);
-  __shared__ unsigned long long rsum;
-  __shared__ uint32_t cnt;
-  const uint32_t l = cur + 1 + blockIdx.x;
-  const double kEps = 1e-4;  // policy.hpp:22
-  if (threadIdx.x == 0) {
-    rsum = 0;
-    cnt = 0;
-  }
-  __syncthreads();
-  unsigned long long part = 0;
-  for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) part += agg[(uint64_t)l * E + e];
-  if (part) atomicAdd(&rsum, part);
-  __syncthreads();
-  const double prox = __dsub_rn(1.0, __ddiv_rn((double)(l - cur), (double)L));
-  for (uint32_t e = threadIdx.x; e < np; e += blockDim.x) {
-    unsigned long long key = ~0ull;
-    if (e < E) {
-      const double ratio =
-          rsum == 0 ? 0.0
-                    : __ddiv_rn(__ull2double_rn(agg[(uint64_t)l * E + e]), __ull2double_rn(rsum));
-      const double pri = __dmul_rn(__dadd_rn(ratio, kEps), prox);
-      if (!(filter && pri <= __dmul_rn(__dmul_rn(kEps, prox), __dadd_rn(1.0, 1e-9)))) {
-        key = ~(unsigned long long)__double_as_longlong(pri);
-        atomicAdd(&cnt, 1u);
-      }
-    }
-    sk[e] = key;
-    sv[e] = e;
-  }
-  __syncthreads();
-  for (uint32_t k = 2; k <= np; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
-        const uint32_t ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k) == 0;
-          const unsigned long long ki = sk[i], kj = sk[ixj];
-          const uint32_t vi = sv[i], vj = sv[ixj];
-          if ((ki > kj || (ki == kj && vi > vj)) == up) {
-            sk[i] = kj;
-            sk[ixj] = ki;
-            sv[i] = vj;
-            sv[ixj] = vi;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  unsigned long long* out = keys + (uint64_t)blockIdx.x * E;
-  uint32_t* ids = reinterpret_cast<uint32_t*>(keys + (uint64_t)(L - cur - 1) * E) +
-                  (uint64_t)blockIdx.x * E;
-  for (uint32_t e = threadIdx.x; e < E; e += blockDim.x) {
-    out[e] = sk[e];
-    ids[e] = sv[e];
-  }
-  if (threadIdx.x == 0) atomicAdd(n_out, cnt);
-}
-
-// Merge-rank of the per-layer sorted segments: a candidate's output position
-// is its position in its own layer plus, for every other layer, the number
-// of that layer's candidates that precede it (binary search).  Keys tie only
-// across layers (ids are unique), where the lower layer -- the smaller
-// ExpertId -- goes first.
-__global__ void __launch_bounds__(256)
-    k_merge_rank(const unsigned long long* keys, uint32_t L, uint32_t E, uint32_t cur,
-                 moe_candidate* out) {
-  extern __shared__ unsigned long long kss[];  // all sorted segments (binary searches stay on chip)
-  const uint32_t nl = L - cur - 1;
-  const uint32_t n = nl * E;
-  for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) kss[j] = keys[j];
-  __syncthreads();
-  const uint32_t* ids = reinterpret_cast<const uint32_t*>(keys + (uint64_t)n);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const unsigned long long k = kss[i];
-    if (k == ~0ull) continue;
-    const uint32_t li = i / E;
-    uint32_t rank = i - li * E;
-    for (uint32_t lj = 0; lj < nl; ++lj) {
-      if (lj == li) continue;
-      const unsigned long long* seg = kss + (uint64_t)lj * E;
-      uint32_t lo = 0, hi = E;  // count of seg < k (lj > li) or <= k (lj < li)
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        const bool before = lj < li ? seg[mid] <= k : seg[mid] < k;
-        if (before) lo = mid + 1; else hi = mid;
-      }
-      rank += lo;
-    }
-    moe_candidate c;
-    c.layer_idx = cur + 1 + li;
-    c.expert_idx = ids[i];
-    c.priority = __longlong_as_double((long long)~k);
-    out[rank] = c;
-  }
 }
 
 // K5+K6 fused decision kernel (one block).
@@ -2273,13 +1917,15 @@ template <int MODE>
 cudaError_t dispatch_match(int cb, uint32_t QT, const CUtensorMap& map, const MatchArgs& a,
                            const MatchGeom& g, cudaStream_t st) {
   if (MODE != 0) {
-    return cb == 1 ? launch_match_t<1, 1, MODE>(map, a, g, st)
-                   : launch_match_t<2, 1, MODE>(map, a, g, st);
+    return cb == 1   ? launch_match_t<1, 1, MODE>(map, a, g, st)
+           : cb == 2 ? launch_match_t<2, 1, MODE>(map, a, g, st)
+                     : launch_match_t<4, 1, MODE>(map, a, g, st);
   }
 #define MOE_QT_CASE(q)                                                      \
   case q:                                                                   \
-    return cb == 1 ? launch_match_t<1, q, 0>(map, a, g, st)                 \
-                   : launch_match_t<2, q, 0>(map, a, g, st);
+    return cb == 1   ? launch_match_t<1, q, 0>(map, a, g, st)               \
+           : cb == 2 ? launch_match_t<2, q, 0>(map, a, g, st)               \
+                     : launch_match_t<4, q, 0>(map, a, g, st);
   switch (QT) {
     MOE_QT_CASE(1)
     MOE_QT_CASE(2)
@@ -2335,13 +1981,16 @@ int occ_blocks_t(size_t smem) {
   return n;
 }
 int occ_blocks(int cb, uint32_t QT, int mode, size_t smem) {
-  if (mode == 1) return cb == 1 ? occ_blocks_t<1, 1, 1>(smem) : occ_blocks_t<2, 1, 1>(smem);
+#define MOE_OCC(q, md) \
+  (cb == 1 ? occ_blocks_t<1, q, md>(smem) \
+           : cb == 2 ? occ_blocks_t<2, q, md>(smem) : occ_blocks_t<4, q, md>(smem))
+  if (mode == 1) return MOE_OCC(1, 1);
   switch (QT) {
-    case 1: return cb == 1 ? occ_blocks_t<1, 1, 0>(smem) : occ_blocks_t<2, 1, 0>(smem);
-    case 2: return cb == 1 ? occ_blocks_t<1, 2, 0>(smem) : occ_blocks_t<2, 2, 0>(smem);
-    case 4: return cb == 1 ? occ_blocks_t<1, 4, 0>(smem) : occ_blocks_t<2, 4, 0>(smem);
-    case 8: return cb == 1 ? occ_blocks_t<1, 8, 0>(smem) : occ_blocks_t<2, 8, 0>(smem);
-    case 16: return cb == 1 ? occ_blocks_t<1, 16, 0>(smem) : occ_blocks_t<2, 16, 0>(smem);
+    case 1: return MOE_OCC(1, 0);
+    case 2: return MOE_OCC(2, 0);
+    case 4: return MOE_OCC(4, 0);
+    case 8: return MOE_OCC(8, 0);
+    case 16: return MOE_OCC(16, 0);
   }
   return 0;
 }
@@ -2452,7 +2101,7 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
   }
   const uint64_t rows = n * L;
   const uint64_t blocks = (rows * 32 + threads - 1) / threads;
-  const uint64_t limit = cb == 1 ? 255ull : 65535ull;
+  const uint64_t limit = cb == 1 ? 255ull : cb == 2 ? 65535ull : 0xffffffffull;
   if (max_count) {
     cudaError_t e = cudaMemsetAsync(max_count, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
@@ -2471,6 +2120,7 @@ cudaError_t launch_prep(const void* src, int src_bytes, uint64_t n, uint32_t L, 
                     wide, init)
   switch (src_bytes) {
     case 8: MOE_PREP(8);
+    case 4: MOE_PREP(4);
     case 2: MOE_PREP(2);
     case 1: MOE_PREP(1);
     default: return cudaErrorInvalidValue;
@@ -2518,8 +2168,9 @@ cudaError_t launch_refine(const DevColl& c, const DevProbes& pr, const MatchWork
   r.halt_value = halt_value;
   r.index_base = c.index_base;
   const uint32_t blocks = (pr.Q + kRefineWarps - 1) / kRefineWarps;
-  return c.cb == 1 ? launch_pdl(k_refine<1>, dim3(blocks), dim3(kRefineWarps * 32), 0, st, r)
-                   : launch_pdl(k_refine<2>, dim3(blocks), dim3(kRefineWarps * 32), 0, st, r);
+  return c.cb == 1   ? launch_pdl(k_refine<1>, dim3(blocks), dim3(kRefineWarps * 32), 0, st, r)
+         : c.cb == 2 ? launch_pdl(k_refine<2>, dim3(blocks), dim3(kRefineWarps * 32), 0, st, r)
+                     : launch_pdl(k_refine<4>, dim3(blocks), dim3(kRefineWarps * 32), 0, st, r);
 }
 
 cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProbes& pr,
@@ -2549,6 +2200,28 @@ cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProb
   return cudaSuccess;
 }
 
+uint32_t exact_warp_blocks(int n_sm) { return (uint32_t)n_sm * 2; }
+
+cudaError_t launch_exact_warp(const DevColl& c, const DevProbes& pr, const uint32_t* qlist,
+                              uint32_t qlist_n, moe_match* out, moe_match* parts,
+                              uint32_t chunk, int n_sm, cudaStream_t st, const uint32_t* nq_dev) {
+  const uint32_t nb = exact_warp_blocks(n_sm);
+  for (uint32_t off = 0; off < qlist_n; off += chunk) {
+    const uint32_t n = std::min(chunk, qlist_n - off);
+    auto kern = c.cb == 1 ? k_exact_warp<1> : c.cb == 2 ? k_exact_warp<2> : k_exact_warp<4>;
+    cudaError_t e = launch_pdl(kern, dim3(nb, n), dim3(256), 0, st, (const uint8_t*)c.counts,
+                               (const double*)c.sqb, (const uint64_t*)c.seq, c.size, c.L, c.C,
+                               c.RB, (const uint8_t*)pr.packed, (const double*)pr.sqa,
+                               qlist + off, n, nq_dev, off, parts);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(k_merge_blocks, dim3((n + 255) / 256), dim3(256), 0, st,
+                   (const moe_match*)parts, nb, qlist + off, n, nq_dev, off, out,
+                   (uint64_t)c.index_base);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out,
                          cudaStream_t st) {
   if (n == 0) return cudaSuccess;
@@ -2561,8 +2234,10 @@ cudaError_t launch_pair_distance(const uint8_t* a, const double* sqa, const uint
                                  double* out, cudaStream_t st) {
   if (cb == 1)
     k_pair_distance<1><<<1, 32, 0, st>>>(a, sqa, b, sqb, L, C, RB, out);
-  else
+  else if (cb == 2)
     k_pair_distance<2><<<1, 32, 0, st>>>(a, sqa, b, sqb, L, C, RB, out);
+  else
+    k_pair_distance<4><<<1, 32, 0, st>>>(a, sqa, b, sqb, L, C, RB, out);
   return cudaGetLastError();
 }
 
@@ -2622,13 +2297,18 @@ cudaError_t launch_replay_block(const DevColl& c, const DevProbes& staged, uint3
     if (e1 == cudaSuccess)
       e1 = cudaFuncSetAttribute(k_replay_block<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem);
+    if (e1 == cudaSuccess)
+      e1 = cudaFuncSetAttribute(k_replay_block<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
     if (e1 != cudaSuccess) return e1;
     set = smem;
   }
   if (c.cb == 1)
     k_replay_block<1><<<1, kReplayThreads, smem, st>>>(a);
-  else
+  else if (c.cb == 2)
     k_replay_block<2><<<1, kReplayThreads, smem, st>>>(a);
+  else
+    k_replay_block<4><<<1, kReplayThreads, smem, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_apply_block<<<nb, 256, 0, st>>>(c.counts, c.ibT, c.sqb, c.seq, c.cap, c.L, c.RB,
@@ -2649,9 +2329,9 @@ cudaError_t launch_append_staged(const DevColl& c, const DevProbes& staged, uint
 }
 
 cudaError_t launch_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32_t RB_old,
-                         uint32_t RB_new, cudaStream_t st) {
+                         uint32_t RB_new, int cb_old, int cb_new, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  k_widen<<<1024, 256, 0, st>>>(src, dst, rows, RB_old, RB_new);
+  k_widen<<<1024, 256, 0, st>>>(src, dst, rows, RB_old, RB_new, cb_old, cb_new);
   return cudaGetLastError();
 }
 
@@ -2769,49 +2449,11 @@ cudaError_t launch_exact_rows(const DevColl& c, const DevProbes& pr, uint32_t q0
   const uint64_t n = (uint64_t)c.size * (l1 - l0);
   if (n) {
     const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)n_sm * 16);
-    if (c.cb == 1)
-      k_rowsim<1><<<grid, 256, 0, st>>>(c.counts, c.sqb, c.size, c.L, c.C, c.RB,
-                                        pr.packed + q0 * LR, pr.sqa + (uint64_t)q0 * c.L, l0, l1, r);
-    else
-      k_rowsim<2><<<grid, 256, 0, st>>>(c.counts, c.sqb, c.size, c.L, c.C, c.RB,
-                                        pr.packed + q0 * LR, pr.sqa + (uint64_t)q0 * c.L, l0, l1, r);
+    auto kern = c.cb == 1 ? k_rowsim<1> : c.cb == 2 ? k_rowsim<2> : k_rowsim<4>;
+    kern<<<grid, 256, 0, st>>>(c.counts, c.sqb, c.size, c.L, c.C, c.RB, pr.packed + q0 * LR,
+                               pr.sqa + (uint64_t)q0 * c.L, l0, l1, r);
   }
   k_rowsum<<<(c.size + 255) / 256, 256, 0, st>>>(r, c.size, c.L, dist, dmin);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_dec_dist(const DevColl& c, const uint8_t* probe, const double* sqa,
-                            const uint16_t* nz, const uint16_t* nz_host, uint32_t n_nz,
-                            uint32_t j0, uint32_t hi,
-                            uint32_t keep, double* pref, double* dist, unsigned long long* dmin,
-                            unsigned long long* zero_agg, uint32_t n_agg, uint32_t* zero_cnt,
-                            cudaStream_t st) {
-  if (c.size == 0) return cudaSuccess;
-  if (c.L > 256) return cudaErrorInvalidValue;
-  const uint64_t* zm = c.L <= 64 ? c.zmask : nullptr;
-  if (zm && n_nz <= 4 && hi + 1 - j0 <= 8) {  // few explicit rows: thread per entry
-    uint64_t nzmask = 0;
-    for (uint32_t i = 0; i < n_nz; ++i) nzmask |= 1ull << nz_host[i];
-    const unsigned g = (c.size + 255) / 256;
-    if (c.cb == 1)
-      launch_pdl(k_dec_dist_t<1>, dim3(g), dim3(256), 0, st, c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB, probe, sqa,
-                                         nzmask, j0, hi, keep, pref, dist, dmin, zero_agg, n_agg,
-                                         zero_cnt);
-    else
-      launch_pdl(k_dec_dist_t<2>, dim3(g), dim3(256), 0, st, c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB, probe, sqa,
-                                         nzmask, j0, hi, keep, pref, dist, dmin, zero_agg, n_agg,
-                                         zero_cnt);
-    return cudaGetLastError();
-  }
-  const unsigned grid = (c.size + kDecWarps - 1) / kDecWarps;
-  if (c.cb == 1)
-    launch_pdl(k_dec_dist<1>, dim3(grid), dim3(kDecWarps * 32), 0, st, c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB,
-                                                   probe, sqa, nz, n_nz, j0, hi, keep, pref, dist,
-                                                   dmin, zero_agg, n_agg, zero_cnt);
-  else
-    launch_pdl(k_dec_dist<2>, dim3(grid), dim3(kDecWarps * 32), 0, st, c.counts, c.sqb, zm, c.size, c.L, c.C, c.RB,
-                                                   probe, sqa, nz, n_nz, j0, hi, keep, pref, dist,
-                                                   dmin, zero_agg, n_agg, zero_cnt);
   return cudaGetLastError();
 }
 
@@ -2833,62 +2475,9 @@ cudaError_t launch_member_agg(const DevColl& c, const double* dist,
                                                                (c.size + 31) / 32));
   const uint32_t chunk = (c.size + by - 1) / by;
   dim3 grid(bx, by);
-  if (c.cb == 1)
-    launch_pdl(k_member_agg<1>, dim3(grid), dim3(256), 0, st, c.counts, c.L, c.E, c.RB, cur, mem, n_mem, chunk, agg);
-  else
-    launch_pdl(k_member_agg<2>, dim3(grid), dim3(256), 0, st, c.counts, c.L, c.E, c.RB, cur, mem, n_mem, chunk, agg);
-  return cudaGetLastError();
-}
-
-size_t prefetch_order_scratch(uint32_t L, uint32_t E) {
-  return (size_t)L * E * 16 + 64;
-}
-
-cudaError_t launch_prefetch_order(const unsigned long long* agg, uint32_t L, uint32_t E,
-                                  uint32_t cur, int filter, unsigned long long* keys,
-                                  uint32_t* n_dev, moe_candidate* out, int n_sm,
-                                  cudaStream_t st, void* scratch) {
-  if (cur + 1 >= L) return cudaMemsetAsync(n_dev, 0, 4, st);
-  if (L <= 256 && scratch && (uint64_t)(L - cur - 1) * E <= 16u * 1024u) {
-    // k_order (+ k_rank for long survivor lists); k_order's loads assume
-    // at most 16 candidates per thread
-    const uint32_t n = (L - cur - 1) * E;
-    uint32_t* big = static_cast<uint32_t*>(scratch);
-    unsigned long long* gkey =
-        reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) + 64);
-    uint32_t* gid = reinterpret_cast<uint32_t*>(gkey + n);
-    uint32_t* grank = gid + n;
-    launch_pdl(k_order, dim3(1), dim3(1024), 0, st, agg, L, E, cur, filter, out, n_dev, gkey, gid, grank, big);
-    if (n > kRankSmall) {
-      const dim3 g((n + 255) / 256, (n + 1023) / 1024);
-      launch_pdl(k_rank, dim3(g), dim3(256), 0, st, (const unsigned long long*)gkey,
-                 (const uint32_t*)gid, (const uint32_t*)n_dev, (const uint32_t*)big, grank);
-      launch_pdl(k_rank_scatter, dim3((n + 255) / 256), dim3(256), 0, st,
-                 (const unsigned long long*)gkey, (const uint32_t*)gid, (const uint32_t*)n_dev,
-                 (const uint32_t*)big, E, (const uint32_t*)grank, out);
-    }
-    return cudaGetLastError();
-  }
-  cudaError_t e = cudaMemsetAsync(n_dev, 0, 4, st);
-  if (e != cudaSuccess) return e;
-  if (E > 4096) return cudaErrorInvalidValue;
-  uint32_t np = 1;
-  while (np < E) np <<= 1;
-  const size_t smem = (size_t)np * 12;
-  const uint32_t nl = L - cur - 1;
-  k_layer_sort<<<nl, std::min<uint32_t>(1024, np), smem, st>>>(agg, L, E, cur, filter, keys,
-                                                                n_dev);
-  const uint32_t n = nl * E;
-  const size_t ksmem = (size_t)n * 8;
-  if (ksmem > 220 * 1024) return cudaErrorInvalidValue;
-  static size_t kset = 0;
-  if (ksmem > kset) {
-    e = cudaFuncSetAttribute(k_merge_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksmem);
-    if (e != cudaSuccess) return e;
-    kset = ksmem;
-  }
-  k_merge_rank<<<std::min<uint32_t>((n + 255) / 256, (uint32_t)n_sm), 256, ksmem, st>>>(
-      keys, L, E, cur, out);
+  auto kern = c.cb == 1 ? k_member_agg<1> : c.cb == 2 ? k_member_agg<2> : k_member_agg<4>;
+  launch_pdl(kern, dim3(grid), dim3(256), 0, st, c.counts, c.L, c.E, c.RB, cur, mem, n_mem, chunk,
+             agg);
   return cudaGetLastError();
 }
 

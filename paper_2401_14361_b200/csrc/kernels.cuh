@@ -13,7 +13,7 @@ namespace moe {
 // Device-resident collection (AoS counts [cap][L][RB], SoA metadata).
 struct DevColl {
   uint32_t L = 0, E = 0, RB = 0, C = 0;
-  int cb = 1;              // bytes per stored count
+  int cb = 1;              // bytes per stored count (1, 2 or 4)
   uint64_t cap = 0;
   uint32_t size = 0;
   uint64_t index_base = 0;    // reported index = index_base + slot (P-sharding)
@@ -126,6 +126,13 @@ cudaError_t launch_exact(const CUtensorMap& map, const DevColl& c, const DevProb
                          const MatchGeom& g, const MatchWork& w, const uint32_t* qlist,
                          uint32_t qlist_n, const uint32_t* T, moe_match* out, cudaStream_t st,
                          const uint32_t* nq_dev = nullptr);
+// Exact argmin for listed probes without the TMA pipeline (any shape); parts
+// is scratch of chunk * exact_warp_blocks(n_sm) moe_match.
+uint32_t exact_warp_blocks(int n_sm);
+cudaError_t launch_exact_warp(const DevColl& c, const DevProbes& pr, const uint32_t* qlist,
+                              uint32_t qlist_n, moe_match* out, moe_match* parts,
+                              uint32_t chunk, int n_sm, cudaStream_t st,
+                              const uint32_t* nq_dev = nullptr);
 cudaError_t launch_window_list(const DevColl& c, const double* dist,
                                const unsigned long long* dmin, double window, WinEntry* wl,
                                uint32_t* wl_n, cudaStream_t st);
@@ -137,26 +144,69 @@ cudaError_t launch_exact_rows(const DevColl& c, const DevProbes& pr, uint32_t q0
                               int n_sm, cudaStream_t st);
 // Window members (dist <= d_min + window) -> mem list; agg[L][E] += their
 // rows > cur (u64).
-// One probe vs every entry, incremental over layers (see k_dec_dist).
-cudaError_t launch_dec_dist(const DevColl& c, const uint8_t* probe, const double* sqa,
-                            const uint16_t* nz, const uint16_t* nz_host, uint32_t n_nz,
-                            uint32_t j0, uint32_t hi,
-                            uint32_t keep, double* pref, double* dist, unsigned long long* dmin,
-                            unsigned long long* zero_agg, uint32_t n_agg, uint32_t* zero_cnt,
-                            cudaStream_t st);
 cudaError_t launch_member_agg(const DevColl& c, const double* dist,
                               const unsigned long long* dmin, double window, uint32_t cur,
                               uint32_t* mem, uint32_t* n_mem, unsigned long long* agg, int n_sm,
                               cudaStream_t st, bool n_mem_zeroed = false);
-// Priorities + floor filter + order of the experts in layers > cur; keys is
-// scratch of (L-cur-1)*E*12 bytes, *n_dev = number of candidates emitted.
-// scratch: prefetch_order_scratch(L, E) bytes, zeroed once at allocation
-// (null: the per-layer sort + merge-rank kernels).
-size_t prefetch_order_scratch(uint32_t L, uint32_t E);
-cudaError_t launch_prefetch_order(const unsigned long long* agg, uint32_t L, uint32_t E,
-                                  uint32_t cur, int filter, unsigned long long* keys,
-                                  uint32_t* n_dev, moe_candidate* out, int n_sm,
-                                  cudaStream_t st, void* scratch);
+// ---- fused single-probe decision (decide.cu, K4 + K5 [+ K6]) -------------
+constexpr uint32_t kDecMaxNz = 1024;        // explicit probe rows per call (else the old path)
+constexpr uint32_t kDecInlineBytes = 512;   // explicit rows passed inside the launch parameters
+constexpr uint32_t kDecInlineNz = 32;
+constexpr uint32_t kDecBarriers = 4;        // grid barriers per decision launch
+constexpr uint32_t kDecMaxLayers = 2048;    // layers above the current one (order phases)
+constexpr uint32_t kDecMaxExperts = 8192;   // experts per layer (a layer's segment in shared memory)
+
+struct DecisionArgs {
+  // phases: do_dist = distances + minimum (else dist[] and *dmin_ext are
+  // given); do_agg = window aggregation (else agg[] is given); the order is
+  // always computed
+  int do_dist, do_agg;
+  const unsigned long long* dmin_ext;
+  // collection
+  const uint8_t* counts;
+  const double* sqb;
+  const uint64_t* zm;  // zero-row bitmasks (L <= 64) or null
+  uint32_t size, L, E, RB;
+  // the probe's explicit rows (its nonzero rows in [j0, hi], ascending), at
+  // the storage width, RB bytes each: inline below or at `rows`/`nz`
+  uint32_t n_nz, j0, hi, keep;
+  int rows_inline;
+  const uint8_t* rows;
+  const uint16_t* nz;
+  double* pref;  // [size] in-order layer sum through row `keep` (reused when j0 > 0)
+  double* dist;  // [size]
+  // window + aggregation
+  uint32_t cur;
+  double window;
+  unsigned long long* dmin2;  // [2] by call parity, ~0 before first use
+  unsigned long long* agg;    // [L*E]
+  // order
+  int filter;
+  unsigned long long* ckey;  // [(L-cur-1)*E] per-layer sorted survivor keys (~bits(priority))
+  uint32_t* cid;             // [(L-cur-1)*E] their flat ExpertIds
+  uint32_t* crank;           // [(L-cur-1)*E] their output positions
+  uint32_t* nseg;            // [L-cur-1] survivors per layer
+  uint32_t parity;
+  moe_candidate* out;  // [(L-cur-1)*E] (host-mapped or device)
+  uint32_t* n_out;
+  // eviction (optional)
+  const unsigned long long* req;  // request EAM [L*E]
+  const moe_slot_view* slots;
+  uint32_t n_slots;
+  double* slot_pri;  // [n_slots] scratch
+  long long* victim;
+  unsigned long long* tprobe;  // optional [8] phase timestamps of CTA 0 (MOE_DEC_TIMING)
+  uint32_t* bar;      // grid-barrier arrival counter (never reset)
+  uint32_t bar_base;  // arrivals before this launch (kDecBarriers * grid per launch)
+  alignas(16) uint8_t inline_rows[kDecInlineBytes];
+  uint16_t inline_nz[kDecInlineNz];
+};
+size_t decision_smem(uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz, uint32_t cur,
+                     uint32_t grid);
+int decision_grid(int n_sm, uint32_t size, uint32_t L, uint32_t cur);
+// One cooperative launch (grid <= co-resident CTAs; decision_grid picks it).
+cudaError_t launch_decision(const DecisionArgs& a, int cb, int grid, size_t smem,
+                            cudaStream_t st);
 
 cudaError_t launch_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out,
                          cudaStream_t st);
@@ -174,7 +224,8 @@ cudaError_t launch_append_staged(const DevColl& c, const DevProbes& staged, uint
                                  uint32_t n, uint64_t base, cudaStream_t st);
 
 // Eviction scoring (K6): cache priorities and the victim over slot views; the
-// prefetch half of this kernel is superseded by launch_prefetch_order.
+// prefetch half of this kernel is superseded by the fused decision kernel
+// (launch_decision); it serves cache_priority / select_eviction_victim.
 cudaError_t launch_decide(const unsigned long long* agg, uint32_t L, uint32_t E, uint32_t cur,
                           int filter, int do_prefetch, const unsigned long long* req,
                           const moe_slot_view* slots, uint64_t n_slots, moe_candidate* out,
@@ -193,6 +244,6 @@ cudaError_t launch_trace_commit64(const uint32_t* scratch, uint64_t n, const int
                                   unsigned long long* counts, cudaStream_t st);
 
 cudaError_t launch_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32_t RB_old,
-                         uint32_t RB_new, cudaStream_t st);
+                         uint32_t RB_new, int cb_old, int cb_new, cudaStream_t st);
 
 }  // namespace moe

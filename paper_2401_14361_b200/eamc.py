@@ -284,13 +284,14 @@ class Eamc:
     # -- matching ---------------------------------------------------------
     def match_batch(self, probes: np.ndarray) -> np.ndarray:
         """Eamc::match over [Q][L][E] probes -> structured array (index, seq, distance)."""
-        narrow = isinstance(probes, np.ndarray) and probes.dtype in (np.uint8, np.uint16)
+        narrow = isinstance(probes, np.ndarray) and probes.dtype in (np.uint8, np.uint16,
+                                                                     np.uint32)
         probes = np.ascontiguousarray(probes, probes.dtype if narrow else np.uint64)
         if probes.shape[1:] != (self.shape.n_layers, self.shape.n_experts_per_layer):
             raise ValueError("Eamc: probe shape mismatch")
         Q = probes.shape[0]
         out = np.zeros(max(Q, 1), MATCH_DTYPE)
-        if narrow:  # u8/u16 counts: shipped narrow (moe_eamc_match_packed)
+        if narrow:  # u8/u16/u32 counts: shipped narrow (moe_eamc_match_packed)
             check(lib.moe_eamc_match_packed(self._h, ptr(probes), probes.dtype.itemsize, Q,
                                             ptr(out), None))
         else:

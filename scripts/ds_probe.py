@@ -1,6 +1,7 @@
-"""DS decision-path timing breakdown: 58 prefetch_priorities calls of one
-decode step (L=59, E=160, P=10k) through the C ABI, with per-call wall time
-and the kernel list for ncu."""
+"""DS decision-path timing: the 58 prefetch_priorities calls of one decode
+step (L=59, E=160, P=10k; DS_P / DS_L / DS_E override) through the C ABI,
+wall time per call (MOE_DEC_TIMING=1 adds the library's launch/completion
+split on stderr)."""
 import ctypes as C
 import os
 import sys
@@ -14,9 +15,11 @@ import torch  # noqa: E402,F401
 import paper_2401_14361_b200 as m  # noqa: E402
 from paper_2401_14361_b200 import _lib  # noqa: E402
 
-L, E, P = 59, 160, int(os.environ.get("DS_P", "10000"))
+L = int(os.environ.get("DS_L", "59"))
+E = int(os.environ.get("DS_E", "160"))
+P = int(os.environ.get("DS_P", "10000"))
 fam = m.gen_bench_family(55, L, E, P + 1, dtype=np.uint8)
-e = m.Eamc(m.ModelShape(L, E, 6), m.Phase.decode, P)
+e = m.Eamc(m.ModelShape(L, E, 2), m.Phase.decode, P)
 e.append(fam[:P], np.arange(P, dtype=np.uint64))
 base = fam[P].astype(np.uint64)
 probes = []
@@ -39,4 +42,5 @@ for _ in range(reps):
         _lib.check(_lib.lib.moe_prefetch_priorities(e._h, probes[l].ctypes.data, l, 1,
                                                     out.ctypes.data, cap, C.byref(n)))
     ts.append(time.perf_counter() - t0)
-print(f"C-ABI decode step: {min(ts)*1e3:.3f} ms ({min(ts)/(L-1)*1e6:.1f} us/call)")
+print(f"L={L} E={E} P={P}: C-ABI decode step {min(ts)*1e3:.3f} ms "
+      f"({min(ts)/(L-1)*1e6:.1f} us/call)", flush=True)

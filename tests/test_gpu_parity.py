@@ -163,8 +163,12 @@ def test_match_wide_counts(m, orc):
     big[::7] *= 1500
     e2 = filled(m, L, E, big)
     check_match(m, orc, e2, big, seqs_of(P), fam[P:])
+    # 70,000 > 65,535: 4-byte storage, still exact (sum c^2 < 2^53)
+    check_match(m, orc, e2, big, seqs_of(P), fam[P:P + 3] * 70000)
+    assert e2.count_bytes() == 4
+    # a row with sum c^2 >= 2^53 is outside the reference's exact range
     with pytest.raises(m.CountOverflowError):
-        e2.match_batch(fam[P:P + 1] * 70000)
+        e2.match_batch(fam[P:P + 1] * 100_000_000)
 
 
 def test_match_long_wide_eams(m, orc):
@@ -796,8 +800,8 @@ def test_pipeline_without_pdl():
 @pytest.mark.parametrize("L,E,P,mult", [(32, 8, 300, 1), (8, 16, 1000, 1), (4, 4, 37, 1),
                                         (16, 32, 200, 40)])
 def test_prefetch_small_collection(m, orc, L, E, P, mult):
-    """Small collections take the one-launch decision kernel (k_decide_small,
-    P <= 1024, L*E <= 1024); mult > 1 pushes counts past 255 (u16 storage)."""
+    """Small collections (one or a few CTAs of the fused decision kernel,
+    decide.cu); mult > 1 pushes counts past 255 (u16 storage)."""
     w = Workload(L, E, min(2, E), n_groups=6, prompt_len=3, decode_len=4, batch_size=2, seed=L + P)
     ents = orc.request_eams(w, P) * mult
     s = m.ModelShape(L, E, min(2, E))

@@ -231,3 +231,144 @@ def test_prefetch_large_candidate_sets(m, orc, L, E, P, layer, filt):
     assert len(got) == len(ol)
     assert np.array_equal(got["layer_idx"], ol) and np.array_equal(got["expert_idx"], oe)
     assert np.array_equal(got["priority"], op)
+
+
+# ------------------------------------------- count envelope: u32 storage (A1)
+def _ds_request_eams(n, L=59, E=160, k=6, tokens=1_000_000, seed=7):
+    """Request-level EAMs of 1M-token DeepSeek-V2 requests (hard
+    part 5): every row sums to tokens*k, the hot experts far above 65,535."""
+    rng = np.random.default_rng(seed)
+    out = np.zeros((n, L, E), np.uint64)
+    for i in range(n):
+        p = rng.dirichlet(np.full(E, 0.3), size=L)
+        out[i] = np.stack([rng.multinomial(tokens * k, p[l]) for l in range(L)])
+    return out
+
+
+def test_u32_counts_match_within_prefetch_bitwise(m, orc):
+    """1M-token DS request EAMs (counts up to ~10^6) stored as u32: match,
+    match_within and prefetch order against the oracle, bitwise; the
+    collection widens 1 -> 4 bytes by itself."""
+    L, E, P = 59, 160, 40
+    ents = _ds_request_eams(P + 4)
+    assert ents.max() > 65535 and ents.max() < (1 << 27)
+    e = m.Eamc(m.ModelShape(L, E, 6), m.Phase.decode, P)
+    e.append(ents[:P], np.arange(P, dtype=np.uint64))
+    assert e.count_bytes() == 4
+    probes = np.concatenate([ents[P:], ents[:2]])
+    got = e.match_batch(probes)
+    idx, seq, d, _ = orc.match(ents[:P], np.arange(P, dtype=np.uint64), probes)
+    assert np.array_equal(got["index"], idx) and np.array_equal(got["distance"], d)
+    # the same probes as u32 arrays ship narrow (probe_bytes 4)
+    got32 = e.match_batch(probes.astype(np.uint32))
+    assert np.array_equal(got32, got)
+    s = m.ModelShape(L, E, 6)
+    w = e.match_within(m.Eam(s, counts=probes[0]), 0.01)
+    wi, ws, wd = orc.match_within(ents[:P], np.arange(P, dtype=np.uint64), probes[0], 0.01)
+    assert [x.index for x in w] == list(wi) and [x.distance for x in w] == list(wd)
+    for layer in (0, 30, 57):
+        cur = probes[1].copy()
+        cur[layer + 1:] = 0
+        o = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=cur), e, layer, True)
+        ol, oe, op = orc.prefetch(ents[:P], np.arange(P, dtype=np.uint64), cur, layer, True)
+        assert np.array_equal(o["layer_idx"], ol) and np.array_equal(o["expert_idx"], oe)
+        assert np.array_equal(o["priority"], op)
+
+
+def test_u32_counts_construction_and_snapshot(m, orc, tmp_path):
+    """Construction replay on a u32 collection (blocked replay, 4-byte rows)
+    and a JSON v1 snapshot holding counts > 65,535 round-trips."""
+    L, E, cap, n = 12, 128, 60, 260
+    fam = m.gen_bench_family(91, L, E, n).copy()
+    fam[::4] *= 9000  # up to 288,000 per cell: 4-byte storage
+    e = m.Eamc(m.ModelShape(L, E), m.Phase.decode, cap)
+    slots = e.build(fam)
+    assert e.count_bytes() == 4
+    ent, sq, want = orc.insert_replay(L, E, cap, fam)
+    assert np.array_equal(slots, want)
+    p = tmp_path / "big.json"
+    e.save(str(p))
+    e2 = m.Eamc.load(str(p))
+    assert e2.count_bytes() == 4 and e2.size() == cap
+    for i in (0, cap // 2, cap - 1):
+        assert np.array_equal(e2.entry(i).counts, ent[i]) and e2.entry_seq(i) == sq[i]
+    probes = fam[:5] * 3
+    got = e2.match_batch(probes)
+    idx, seq, d, _ = orc.match(ent, sq, probes)
+    assert np.array_equal(got["index"], idx) and np.array_equal(got["distance"], d)
+
+
+def test_overflow_only_past_the_exact_range(m, orc):
+    """MOE_ERR_OVERFLOW exactly when a row's sum of squares reaches 2^53
+    (where the reference's fp64 sums stop being exact), not before."""
+    L, E = 2, 4
+    s = m.ModelShape(L, E)
+    ok_row = np.array([[67_108_863, 0, 0, 0], [1, 2, 3, 4]], np.uint64)  # (2^26-1)^2 < 2^53
+    bad_row = np.array([[94_906_266, 0, 0, 0], [1, 0, 0, 0]], np.uint64)  # > 2^53
+    e = m.Eamc(s, m.Phase.decode, 4)
+    e.append(np.stack([ok_row, ok_row // 3]), np.arange(2, dtype=np.uint64))
+    got = e.match_batch(ok_row[None])
+    idx, seq, d, _ = orc.match(np.stack([ok_row, ok_row // 3]), np.arange(2, dtype=np.uint64),
+                               ok_row[None])
+    assert got["index"][0] == idx[0] and got["distance"][0] == d[0]
+    with pytest.raises(m.CountOverflowError):
+        e.match_batch(bad_row[None])
+    with pytest.raises(m.CountOverflowError):
+        e.insert(m.Eam(s, counts=bad_row))
+    assert m.eam_distance(m.Eam(s, counts=ok_row), m.Eam(s, counts=ok_row // 3)) == \
+        orc.distance(ok_row, ok_row // 3)
+
+
+# ------------------------------------------ fused decision kernel (K4+K5+K6)
+def test_fused_decision_sequence_with_victims(m, orc):
+    """moe_decide = ONE cooperative launch (decide.cu): the engine's per-layer
+    call sequence (the iteration EAM grows by one row per call, so phase A
+    reuses the layer-prefix sums), each call's floor-filtered order and the
+    eviction victim over slot views, against the oracle; then an unrelated
+    probe (prefix cache miss) and the last layer (no candidates)."""
+    from oracle import Workload
+    L, E, P = 24, 64, 700
+    w = Workload(L, E, 2, n_groups=10, prompt_len=3, decode_len=4, batch_size=2, seed=77)
+    ents = orc.request_eams(w, P)
+    s = m.ModelShape(L, E, 2)
+    e = m.Eamc(s, m.Phase.decode, P)
+    e.build(ents)
+    req = orc.request_eams(w, 1, start=901)[0]
+    slots = [m.SlotView(i, m.ExpertId(i % L, (11 * i) % E), i % 6 == 0, i % 9 == 0)
+             for i in range(61)]
+    want_v = orc.select_victim(req, [v.slot for v in slots],
+                               [v.occupant.layer_idx for v in slots],
+                               [v.occupant.expert_idx for v in slots],
+                               [int(v.prefetch_protected) for v in slots],
+                               [int(v.pinned) for v in slots])
+    full = orc.iteration_probe(w, 950, 2, L - 1)
+    for layer in list(range(L)) + [5, L - 1]:
+        pr = full.copy()
+        pr[layer + 1:] = 0
+        if layer == 5:
+            pr = orc.iteration_probe(w, 951, 3, 5)  # unrelated probe: prefix cache miss
+        order, victim = m.decide(m.Eam(s, m.EamKind.iteration, counts=pr), e, layer,
+                                 m.Eam(s, counts=req), slots)
+        ol, ox, op = orc.prefetch(ents, np.arange(P, dtype=np.uint64), pr, layer, True)
+        assert np.array_equal(order["layer_idx"], ol) and np.array_equal(order["expert_idx"], ox)
+        assert np.array_equal(order["priority"], op)
+        assert (victim if victim is not None else -1) == want_v
+    assert len(ol) == 0  # last layer: nothing above it
+
+
+def test_decision_many_explicit_rows_fallback(m, orc):
+    """More explicit probe rows than the fused kernel stages (L = 1,100 > 1,024):
+    the row-parallel exact distance pass feeds the kernel's aggregation and
+    order phases; same order as the reference."""
+    L, E, P = 1100, 4, 50
+    fam = m.gen_bench_family(19, L, E, P + 1).copy()
+    e = m.Eamc(m.ModelShape(L, E), m.Phase.decode, P)
+    e.append(fam[:P], np.arange(P, dtype=np.uint64))
+    for layer, flt in [(1050, True), (1050, False), (3, True)]:
+        cur = fam[P].copy()
+        cur[layer + 1:] = 0
+        got = m.prefetch_order(m.Eam(m.ModelShape(L, E), m.EamKind.iteration, counts=cur), e,
+                               layer, flt)
+        ol, oe, op = orc.prefetch(fam[:P], np.arange(P, dtype=np.uint64), cur, layer, flt)
+        assert np.array_equal(got["layer_idx"], ol) and np.array_equal(got["expert_idx"], oe)
+        assert np.array_equal(got["priority"], op)
