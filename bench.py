@@ -538,7 +538,7 @@ def run_rows(args, m, _lib, torch, dev, sp, stream, flush):
     out["construction"] = row
 
     # -- A2/K1 tracing, DS shape: T = 1M router tokens x 59 layers x top-6 ids
-    #    (u8, resident) -> R = 1000 per-request count matrices
+    #    (u8, resident) -> R = 1000 per-request count matrices (u32), accumulated
     L4, E4, k4, T4 = 59, 160, 6, 1_000_000
     R4 = T4 // 1000
     rng = np.random.default_rng(1001)
@@ -561,14 +561,18 @@ def run_rows(args, m, _lib, torch, dev, sp, stream, flush):
     for _ in range(3):
         trace_dev()
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(10)]
-    for a, b in evs:
-        a.record(stream)
-        trace_dev()
-        b.record(stream)
+    d_counts.zero_()
     torch.cuda.synchronize()
-    t_dev = sum(a.elapsed_time(b) for a, b in evs) / len(evs) / 1e3
+    n_ev = 10
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n_ev)]
+    for a_, b_ in evs:
+        a_.record(stream)
+        trace_dev()  # the whole call: k_trace_own + gated long-request pass + gated rollbacks
+        b_.record(stream)
+    torch.cuda.synchronize()
+    t_dev = sum(a_.elapsed_time(b_) for a_, b_ in evs) / n_ev / 1e3
+    dev_counts = d_counts.cpu().numpy().astype(np.uint64) // n_ev  # n_ev accumulations
     bytes_alg = T4 * L4 * k4 * 1 + R4 * L4 * E4 * 4 + 8 * (R4 + 1)
     host_counts = m.trace_requests(s4, picks, offs)  # warm-up (buffers) + parity result
     acc = np.zeros_like(host_counts)
@@ -579,22 +583,36 @@ def run_rows(args, m, _lib, torch, dev, sp, stream, flush):
     t_e2e = (time.perf_counter() - t0) / reps4
     row = {"workload": f"DS tracing: T={T4} tokens x L={L4} x top-{k4} u8 ids, R={R4} requests",
            "gpu_ms": t_dev * 1e3, "picks_per_s": T4 * L4 * k4 / t_dev,
-           "roofline": {"bound": "hbm", "achieved": bytes_alg / t_dev / 1e9, "peak": hbm_peak,
+           "roofline": {"bound": "hbm", "kernel": "k_trace_own (+ gated passes), whole call",
+                        "achieved": bytes_alg / t_dev / 1e9, "peak": hbm_peak,
                         "unit": "GB/s", "frac": bytes_alg / t_dev / 1e9 / hbm_peak,
-                        "alg_bytes": bytes_alg, "note": f"peak = {peak_kind} HBM"},
+                        "traffic": ncu_traffic("k_trace_own"),
+                        "alg_bytes": bytes_alg, "note": f"peak = {peak_kind} HBM; bytes = "
+                        "T*L*k ids + R*L*E*4 counts + 8*(R+1) offsets (SURVEY 8d)"},
            "e2e_ms": t_e2e * 1e3,
            "e2e_api": ("moe_eam_trace (host u8 ids + host u64 counts accumulated; transfers "
                        "through pinned staging inside the call)")}
-    ns = 20_000
-    t0 = time.perf_counter()
-    rc, ref_counts = orc.trace(L4, E4, k4, picks[:ns].astype(np.uint32),
-                               np.arange(0, ns + 1, 1000, dtype=np.uint64))
-    t_cpu = time.perf_counter() - t0
-    row.update({"cpu_picks_per_s": ns * L4 * k4 / t_cpu, "cpu_cores": 1, "cpu_kind": "port",
-                "cpu_sample": f"{ns} tokens (oracle restatement of workload.cpp:166-181 + "
-                              "Eam::record)",
-                "parity_sample": bool(rc == 0 and np.array_equal(host_counts[:ns // 1000],
-                                                                 ref_counts))})
+    if ref is not None:  # the reference's Eam::record on all host cores, full workload
+        ncpu = os.cpu_count() or 1
+        sec, ref_counts = ref.trace_mt(L4, E4, k4, picks, offs, ncpu)
+        row.update({"cpu_picks_per_s": T4 * L4 * k4 / sec, "cpu_cores": ncpu,
+                    "cpu_kind": "reference",
+                    "cpu_sample": f"all {T4} tokens (reference Eam::record, one RoutingEvent per "
+                                  "request and layer as workload.cpp:166-181; std::thread over "
+                                  "requests)",
+                    "speedup": (T4 * L4 * k4 / t_dev) / (T4 * L4 * k4 / sec),
+                    "parity_full": bool(np.array_equal(host_counts, ref_counts)
+                                        and np.array_equal(dev_counts, ref_counts))})
+    else:
+        ns = 20_000
+        t0 = time.perf_counter()
+        rc, ref_counts = orc.trace(L4, E4, k4, picks[:ns].astype(np.uint32),
+                                   np.arange(0, ns + 1, 1000, dtype=np.uint64))
+        t_cpu = time.perf_counter() - t0
+        row.update({"cpu_picks_per_s": ns * L4 * k4 / t_cpu, "cpu_cores": 1, "cpu_kind": "port",
+                    "cpu_sample": f"{ns} tokens (oracle restatement)",
+                    "parity_sample": bool(rc == 0 and np.array_equal(host_counts[:ns // 1000],
+                                                                     ref_counts))})
     out["tracing"] = row
     del d_picks, d_counts
 

@@ -291,6 +291,9 @@ class RefLib:
         lib.ref_eam_record.restype = C.c_int
         lib.ref_eam_record.argtypes = [C.c_uint32, C.c_uint32, u64p, C.c_uint32, u32p, u64p,
                                        C.c_uint64]
+        lib.ref_trace_mt.restype = C.c_double
+        lib.ref_trace_mt.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, u8p, u64p, C.c_uint64,
+                                     u64p, C.c_int]
         lib.ref_capacity_bound.restype = C.c_uint64
         lib.ref_capacity_bound.argtypes = [C.c_uint32, C.c_uint32, C.c_double]
         lib.ref_bench_match.restype = C.c_uint64
@@ -306,6 +309,16 @@ class RefLib:
                                       C.c_uint64, u64p]
         lib.ref_eamc_fill_bench.restype = C.c_int
         lib.ref_eamc_fill_bench.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+
+    def trace_mt(self, L, E, k, topk_u8, offsets, n_threads):
+        """Per-request EAMs from u8 router ids through the reference's Eam::record
+        (RoutingEvent per layer, workload.cpp:166-181); returns (seconds, counts)."""
+        topk_u8 = np.ascontiguousarray(topk_u8, np.uint8)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        R = len(offsets) - 1
+        out = np.zeros((R, L, E), np.uint64)
+        sec = self.lib.ref_trace_mt(L, E, k, topk_u8, offsets, R, out, n_threads)
+        return sec, out
 
     def gen_bench(self, seed, L, E, n, skip=0):
         """bench_match's EAM stream (bench.cpp:44-54) from the reference Rng."""

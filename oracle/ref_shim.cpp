@@ -248,6 +248,51 @@ int ref_eam_record(uint32_t L, uint32_t E, uint64_t* counts, uint32_t layer,
   }
 }
 
+// Router top-k ids [T][L][k] (u8) -> per-request request-level EAMs with the
+// reference's own types: per request and layer, the per-expert token counts
+// are gathered as workload.cpp:166-181 does and handed to Eam::record as one
+// RoutingEvent per layer.  Requests are split over n_threads std::threads
+// (independent Eams).  Returns wall seconds, or -1 on a record error.
+double ref_trace_mt(uint32_t L, uint32_t E, uint32_t k, const uint8_t* topk,
+                    const uint64_t* offsets, uint64_t R, uint64_t* out, int n_threads) {
+  if (n_threads < 1) n_threads = 1;
+  const ModelShape shape{L, E, k};
+  std::vector<int> err(n_threads, 0);
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int th = 0; th < n_threads; ++th)
+    pool.emplace_back([&, th] {
+      std::vector<uint64_t> c(E);
+      try {
+        for (uint64_t r = th; r < R; r += n_threads) {
+          Eam eam(shape, EamKind::request, Phase::decode);
+          for (uint32_t l = 0; l < L; ++l) {
+            std::fill(c.begin(), c.end(), 0);
+            for (uint64_t t = offsets[r]; t < offsets[r + 1]; ++t)
+              for (uint32_t j = 0; j < k; ++j) {
+                const uint32_t e = topk[(t * L + l) * k + j];
+                if (e < E) ++c[e]; else throw std::out_of_range("expert");
+              }
+            RoutingEvent ev;
+            ev.layer_idx = l;
+            for (uint32_t e = 0; e < E; ++e)
+              if (c[e]) ev.assignments.push_back({e, c[e]});
+            if (!ev.assignments.empty()) eam.record(ev);
+          }
+          auto cnt = eam.counts();
+          std::copy(cnt.begin(), cnt.end(), out + r * uint64_t{L} * E);
+        }
+      } catch (...) {
+        err[th] = 1;
+      }
+    });
+  for (auto& t : pool) t.join();
+  const auto t1 = std::chrono::steady_clock::now();
+  for (int e : err)
+    if (e) return -1.0;
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
 uint64_t ref_capacity_bound(uint32_t L, uint32_t E, double similarity) {
   try {
     return eamc_capacity_bound(ModelShape{L, E, 1}, similarity);

@@ -1922,19 +1922,11 @@ moe_status moe_eam_trace_device(const moe_shape* shape, const void* topk_idx, in
   int dev = 0, n_sm = 0;
   cudaGetDevice(&dev);
   CKS(device_ok(dev, &n_sm));
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const uint64_t cells = (uint64_t)shape->n_layers * shape->n_experts_per_layer;
-  // persistent per-device scratch (a stream-ordered pool allocation would be
-  // unmapped and remapped around every synchronisation)
-  static std::mutex mu;
-  static DevBuf scratch_buf[64];
-  std::lock_guard<std::mutex> lock(mu);
-  CK(scratch_buf[dev & 63].ensure(std::max<uint64_t>(1, n_requests * cells) * 4));
-  uint32_t* scratch = scratch_buf[dev & 63].as<uint32_t>();
-  // k_trace writes (or zeroes) every request's rows itself
+  // no scratch: the kernels accumulate into counts_u32 directly and roll their
+  // additions back on an out-of-range id (trace.cu)
   CK(moe::launch_trace(topk_idx, idx_bytes, n_tokens, shape->n_layers, shape->n_experts_per_layer,
-                       shape->top_k, offsets, n_requests, scratch, bad_index_flag, n_sm, st));
-  CK(moe::launch_trace_commit(scratch, n_requests * cells, bad_index_flag, counts_u32, st));
+                       shape->top_k, offsets, n_requests, counts_u32, 4, bad_index_flag, n_sm,
+                       static_cast<cudaStream_t>(stream)));
   return MOE_OK;
 }
 
@@ -2048,7 +2040,7 @@ moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_b
   // persistent per-device state: stream, buffers, pinned staging ring
   struct TraceState {
     cudaStream_t st = nullptr;
-    DevBuf din, doff, dscr, dcnt, dbad;
+    DevBuf din, doff, dcnt, dbad;
     PinBuf hbad;
     StagingRing ring;
   };
@@ -2060,7 +2052,6 @@ moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_b
   cudaStream_t st = S.st;
   CK(S.din.ensure(std::max<uint64_t>(in_bytes, 16)));
   CK(S.doff.ensure((n_requests + 1) * 8));
-  CK(S.dscr.ensure(n_requests * cells * 4));
   CK(S.dcnt.ensure(n_requests * cells * 8));
   CK(S.dbad.ensure(4));
   CK(S.hbad.ensure(4));
@@ -2070,9 +2061,7 @@ moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_b
   CK(cudaMemsetAsync(S.dbad.p, 0, 4, st));
   CK(moe::launch_trace(S.din.p, idx_bytes, n_tokens, shape->n_layers,
                        shape->n_experts_per_layer, shape->top_k, S.doff.as<uint64_t>(),
-                       n_requests, S.dscr.as<uint32_t>(), S.dbad.as<int>(), n_sm, st));
-  CK(moe::launch_trace_commit64(S.dscr.as<uint32_t>(), n_requests * cells, S.dbad.as<int>(),
-                                S.dcnt.as<unsigned long long>(), st));
+                       n_requests, S.dcnt.p, 8, S.dbad.as<int>(), n_sm, st));
   CK(cudaMemcpyAsync(S.hbad.p, S.dbad.p, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (*S.hbad.as<int>())  // all-or-nothing (eam.cpp:42-47): the caller's counts untouched

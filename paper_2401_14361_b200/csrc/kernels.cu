@@ -19,8 +19,7 @@
 //  K5+K6 k_decide         prefetch priorities + floor filter + order
 //                         (policy.cpp:106-125, engine.cpp:663-668) and the
 //                         eviction victim (policy.cpp:128-159), one block.
-//  K1  k_trace            router top-k ids -> per-request L x E histograms
-//                         (eam.cpp:41-52 semantics, all-or-nothing).
+//  (K1 tracing lives in trace.cu.)
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -1646,255 +1645,6 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
-// K1: top-k ids -> per-request histograms in shared memory.
-template <int IB>
-__device__ __forceinline__ uint32_t load_idx(const void* p, uint64_t i) {
-  if (IB == 1) return reinterpret_cast<const uint8_t*>(p)[i];
-  if (IB == 2) return reinterpret_cast<const uint16_t*>(p)[i];
-  return reinterpret_cast<const uint32_t*>(p)[i];
-}
-
-// Histogram of the ids of tokens [s0, s1) into the shared histogram (odd row
-// stride ES), position-major: a token's L*k ids are "positions"; thread
-// (phase, pi) owns position pair pi (2 consecutive ids when L*k is even, so
-// one 16-bit load) of tokens phase, phase+phases, ...  Its histogram row
-// offsets are loop-invariant registers; per id: extract, range check, add,
-// shared-memory reduction.  Lanes of a warp read consecutive bytes of a
-// token (coalesced) and hit distinct rows (banks).  Out-of-range ids raise *bad.
-template <int IB>
-__device__ __forceinline__ void trace_tokens(const void* topk, uint64_t s0, uint64_t s1,
-                                             uint32_t L, uint32_t E, uint32_t k, uint32_t ES,
-                                             uint32_t* hist, int* bad) {
-  const uint32_t per_tok = L * k;
-  const uint32_t span = (IB == 1 && (per_tok & 1) == 0) ? 2u : 1u;
-  const uint32_t npos = per_tok / span;
-  const uint32_t phases = npos <= blockDim.x ? blockDim.x / npos : 1u;
-  const uint32_t tid = threadIdx.x;
-  if (tid >= phases * npos && npos <= blockDim.x) return;
-  const uint32_t phase = npos <= blockDim.x ? tid / npos : 0u;
-  for (uint32_t pi = npos <= blockDim.x ? tid - phase * npos : tid; pi < npos;
-       pi += npos <= blockDim.x ? npos : blockDim.x) {
-    const uint32_t pos = pi * span;
-    const uint32_t b0 = (pos / k) * ES, b1 = ((pos + 1) / k) * ES;
-    auto load = [&](uint64_t t) -> uint32_t {
-      const uint64_t i = t * per_tok + pos;
-      return span == 2 ? (uint32_t)reinterpret_cast<const uint16_t*>(topk)[i >> 1]
-                       : load_idx<IB>(topk, i);
-    };
-    auto count = [&](uint32_t w) {
-      if (span == 2) {
-        const uint32_t e0 = w & 0xffu, e1 = w >> 8;
-        if (e0 < E) atomicAdd(&hist[b0 + e0], 1u); else *bad = 1;
-        if (e1 < E) atomicAdd(&hist[b1 + e1], 1u); else *bad = 1;
-      } else {
-        if (w < E) atomicAdd(&hist[b0 + w], 1u); else *bad = 1;
-      }
-    };
-    constexpr int kU = 8;  // loads in flight per thread
-    uint64_t t = s0 + phase;
-    for (; t + (kU - 1) * (uint64_t)phases < s1; t += kU * (uint64_t)phases) {
-      uint32_t w[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) w[u] = load(t + u * (uint64_t)phases);
-#pragma unroll
-      for (int u = 0; u < kU; ++u) count(w[u]);
-    }
-    for (; t < s1; t += phases) count(load(t));
-  }
-}
-
-constexpr uint64_t kTraceOwnedMax = 16384;  // tokens a single block owns outright
-
-// Requests of <= kTraceOwnedMax tokens: one block owns the request and writes
-// its whole L x E histogram with plain stores (no zeroing, no global
-// atomics).  Longer requests only get their scratch rows zeroed here.
-template <int IB>
-__global__ void __launch_bounds__(512)
-    k_trace(const void* topk, uint32_t L, uint32_t E, uint32_t k, const uint64_t* offsets,
-            uint64_t R, uint32_t* scratch, int* bad) {
-  extern __shared__ uint32_t hist[];
-  const uint32_t ES = E | 1;  // odd row stride: rows of the same expert on distinct banks
-  for (uint64_t r = blockIdx.x; r < R; r += gridDim.x) {
-    const uint64_t s0 = offsets[r], s1 = offsets[r + 1];
-    uint32_t* dst = scratch + r * (uint64_t)L * E;
-    if (s1 - s0 > kTraceOwnedMax) {
-      for (uint32_t i = threadIdx.x; i < L * E; i += blockDim.x) dst[i] = 0;
-      continue;
-    }
-    for (uint32_t i = threadIdx.x; i < L * ES; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    trace_tokens<IB>(topk, s0, s1, L, E, k, ES, hist, bad);
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < L * E; i += blockDim.x) {
-      const uint32_t l = i / E;
-      dst[i] = hist[l * ES + (i - l * E)];
-    }
-    __syncthreads();
-  }
-}
-
-// u8 ids (E <= 256), 16-byte aligned: the owned-request kernel with 128-bit
-// loads.  Bytes of the id stream are grouped in 16-byte chunks; since
-// 16*CH = lcm(L*k, 16) (CH = L*k / gcd(L*k, 16)), the token position -- and
-// so the histogram row -- of byte j of chunk i depends only on (i mod CH, j).
-// A block of G*CH threads walks the request's chunks with stride G*CH, so
-// thread t always sees chunk phase t mod CH and keeps its 16 row offsets in
-// registers; per id the work is one byte extract, one add and one shared
-// atomic, the range check is a 4-way byte max per word.  Chunks straddling
-// the request boundary take a per-byte masked path.
-template <int U>
-__device__ __forceinline__ void trace_chunks_u8(const uint4* src, int64_t i, int64_t first,
-                                                int64_t last, uint64_t b0, uint64_t b1,
-                                                uint32_t stride, const uint32_t (&rowb)[16],
-                                                uint32_t E, int* bad) {
-  uint4 w[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t c = i + (int64_t)u * stride;
-    w[u] = (c >= first && c <= last) ? __ldg(src + c) : make_uint4(0u, 0u, 0u, 0u);
-  }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t c = i + (int64_t)u * stride;
-    if (c < first || c > last) continue;
-    const uint32_t v[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-    const uint32_t mx = __vmaxu4(__vmaxu4(v[0], v[1]), __vmaxu4(v[2], v[3]));
-    const uint32_t m2 = __vmaxu4(mx, mx >> 16);
-    const bool in_range = max(m2 & 0xffu, (m2 >> 8) & 0xffu) < E;
-    if (c == first || c == last || !in_range) {  // boundary chunk / bad id: per-byte tests
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint64_t B = (uint64_t)c * 16 + j;
-        if (B < b0 || B >= b1) continue;
-        const uint32_t e = __byte_perm(v[j >> 2], 0u, 0x4440u | (j & 3));
-        if (e < E)
-          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(rowb[j] + 4u * e));
-        else
-          *bad = 1;
-      }
-      continue;
-    }
-    // hot path: PRMT + LEA + RED per id
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t e = __byte_perm(v[j >> 2], 0u, 0x4440u | (j & 3));
-      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(rowb[j] + 4u * e));
-    }
-  }
-}
-
-__global__ void __launch_bounds__(512)
-    k_trace_u8(const uint8_t* topk, uint32_t L, uint32_t E, uint32_t k, uint32_t CH,
-               const uint64_t* offsets, uint64_t R, uint32_t* scratch, int* bad) {
-  extern __shared__ uint32_t hist[];
-  const uint32_t ES = E | 1;
-  const uint32_t Lk = L * k;
-  const uint32_t stride = blockDim.x;  // a multiple of CH
-  const uint32_t t = threadIdx.x;
-  uint32_t rowb[16];  // shared-window byte address of the histogram row of each byte
-  {
-    const uint32_t ph = t % CH;
-    const uint32_t hb = (uint32_t)__cvta_generic_to_shared(hist);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) rowb[j] = hb + 4u * ((((16u * ph + j) % Lk) / k) * ES);
-  }
-  const uint4* src = reinterpret_cast<const uint4*>(topk);
-  for (uint64_t r = blockIdx.x; r < R; r += gridDim.x) {
-    const uint64_t s0 = offsets[r], s1 = offsets[r + 1];
-    uint32_t* dst = scratch + r * (uint64_t)L * E;
-    if (s1 - s0 > kTraceOwnedMax) {
-      for (uint32_t i = t; i < L * E; i += blockDim.x) dst[i] = 0;
-      continue;
-    }
-    for (uint32_t i = t; i < L * ES; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    if (s1 > s0) {
-      const uint64_t b0 = s0 * Lk, b1 = s1 * Lk;
-      const int64_t first = (int64_t)(b0 / 16), last = (int64_t)((b1 - 1) / 16);
-      const int64_t base = first - first % CH;  // chunk phase of thread t = t mod CH
-      constexpr int U = 4;
-      int64_t i = base + t;
-      for (; i + (int64_t)(U - 1) * stride <= last; i += (int64_t)U * stride)
-        trace_chunks_u8<U>(src, i, first, last, b0, b1, stride, rowb, E, bad);
-      for (; i <= last; i += stride)
-        trace_chunks_u8<1>(src, i, first, last, b0, b1, stride, rowb, E, bad);
-    }
-    __syncthreads();
-    for (uint32_t i = t; i < L * E; i += blockDim.x) {
-      const uint32_t l = i / E;
-      dst[i] = hist[l * ES + (i - l * E)];
-    }
-    __syncthreads();
-  }
-}
-
-// Requests longer than kTraceOwnedMax: split into token chunks across blocks,
-// flushed with global atomics (runs after k_trace, which zeroed their rows).
-template <int IB>
-__global__ void __launch_bounds__(512)
-    k_trace_long(const void* topk, uint64_t T, uint32_t L, uint32_t E, uint32_t k,
-                 const uint64_t* offsets, uint64_t R, uint32_t* scratch, int* bad) {
-  extern __shared__ uint32_t hist[];
-  const uint32_t ES = E | 1;
-  const uint64_t n_chunks = (T + kTraceOwnedMax - 1) / kTraceOwnedMax;
-  for (uint64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    const uint64_t t0 = ch * kTraceOwnedMax, t1 = min(T, t0 + kTraceOwnedMax);
-    uint64_t lo = 0, hi = R;  // first request whose range ends after t0
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) / 2;
-      if (offsets[mid + 1] <= t0) lo = mid + 1; else hi = mid;
-    }
-    for (uint64_t r = lo; r < R && offsets[r] < t1; ++r) {
-      if (offsets[r + 1] - offsets[r] <= kTraceOwnedMax) continue;  // owned by k_trace
-      const uint64_t s0 = max(t0, offsets[r]), s1 = min(t1, offsets[r + 1]);
-      if (s0 >= s1) continue;
-      for (uint32_t i = threadIdx.x; i < L * ES; i += blockDim.x) hist[i] = 0;
-      __syncthreads();
-      trace_tokens<IB>(topk, s0, s1, L, E, k, ES, hist, bad);
-      __syncthreads();
-      uint32_t* dst = scratch + r * (uint64_t)L * E;
-      for (uint32_t i = threadIdx.x; i < L * E; i += blockDim.x) {
-        const uint32_t l = i / E;
-        const uint32_t v = hist[l * ES + (i - l * E)];
-        if (v) atomicAdd(&dst[i], v);
-      }
-      __syncthreads();
-    }
-  }
-}
-
-__global__ void k_trace_commit(const uint32_t* scratch, uint64_t n, const int* bad,
-                               uint32_t* counts) {
-  if (*bad) return;
-  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-  if (((reinterpret_cast<uintptr_t>(scratch) | reinterpret_cast<uintptr_t>(counts)) & 15) == 0) {
-    const uint64_t n4 = n / 4;
-    const uint4* s4 = reinterpret_cast<const uint4*>(scratch);
-    uint4* c4 = reinterpret_cast<uint4*>(counts);
-    for (uint64_t i = tid; i < n4; i += nth) {
-      const uint4 a = s4[i];
-      uint4 b = c4[i];
-      b.x += a.x;
-      b.y += a.y;
-      b.z += a.z;
-      b.w += a.w;
-      c4[i] = b;
-    }
-    for (uint64_t i = n4 * 4 + tid; i < n; i += nth) counts[i] += scratch[i];
-    return;
-  }
-  for (uint64_t i = tid; i < n; i += nth) counts[i] += scratch[i];
-}
-
-__global__ void k_trace_commit64(const uint32_t* scratch, uint64_t n, const int* bad,
-                                 unsigned long long* counts) {
-  if (*bad) return;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    counts[i] += scratch[i];
-}
-
 template <int CB, int QT, int MODE>
 cudaError_t set_smem_attr(size_t smem) {
   static size_t set = 0;  // cudaFuncSetAttribute only when the requirement grows
@@ -2354,82 +2104,6 @@ cudaError_t launch_decide(const unsigned long long* agg, uint32_t L, uint32_t E,
   }
   k_decide<<<1, 1024, smem, st>>>(agg, L, E, cur, filter, do_prefetch && cur + 1 < L, req, slots,
                                   n_slots, out, n_out, victim, slot_pri, np);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_trace(const void* topk, int idx_bytes, uint64_t T, uint32_t L, uint32_t E,
-                         uint32_t k, const uint64_t* offsets, uint64_t R, uint32_t* scratch,
-                         int* bad, int n_sm, cudaStream_t st) {
-  if (T == 0 || R == 0) return cudaSuccess;
-  const size_t smem = (size_t)L * (E | 1) * 4;
-  if (smem > 220 * 1024) return cudaErrorInvalidValue;
-  const unsigned grid = (unsigned)std::min<uint64_t>(R, (uint64_t)n_sm * 4);
-  const unsigned grid_long =
-      (unsigned)std::min<uint64_t>((T + kTraceOwnedMax - 1) / kTraceOwnedMax, (uint64_t)n_sm * 4);
-#define MOE_TRACE(IB)                                                                          \
-  {                                                                                            \
-    static size_t set = 0;                                                                     \
-    if (smem > set) {                                                                          \
-      cudaError_t e =                                                                          \
-          cudaFuncSetAttribute(k_trace<IB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      if (e == cudaSuccess)                                                                    \
-        e = cudaFuncSetAttribute(k_trace_long<IB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 (int)smem);                                                   \
-      if (e != cudaSuccess) return e;                                                          \
-      set = smem;                                                                              \
-    }                                                                                          \
-    k_trace<IB><<<grid, 512, smem, st>>>(topk, L, E, k, offsets, R, scratch, bad);             \
-    k_trace_long<IB><<<grid_long, 512, smem, st>>>(topk, T, L, E, k, offsets, R, scratch, bad); \
-  }
-  const uint32_t Lk = L * k;
-  uint32_t g16 = 16;
-  while (Lk % g16) g16 >>= 1;
-  const uint32_t CH = Lk / g16;
-  if (idx_bytes == 1 && E <= 256 && CH <= 512 && (reinterpret_cast<uintptr_t>(topk) & 15) == 0) {
-    static size_t set = 0;
-    if (smem > set) {
-      cudaError_t e =
-          cudaFuncSetAttribute(k_trace_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_trace_long<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-      if (e != cudaSuccess) return e;
-      set = smem;
-    }
-    const uint32_t threads = (512 / CH) * CH;
-    // blocks resident per SM by shared memory (the histogram) and threads
-    const uint32_t per_sm = std::max<uint32_t>(
-        1, std::min<uint32_t>((uint32_t)((220u * 1024u) / std::max<size_t>(smem, 1)),
-                              2048u / threads));
-    const unsigned g = (unsigned)std::min<uint64_t>(R, (uint64_t)n_sm * per_sm);
-    k_trace_u8<<<g, threads, smem, st>>>(static_cast<const uint8_t*>(topk), L, E, k, CH, offsets,
-                                         R, scratch, bad);
-    k_trace_long<1><<<grid_long, 512, smem, st>>>(topk, T, L, E, k, offsets, R, scratch, bad);
-    return cudaGetLastError();
-  }
-  switch (idx_bytes) {
-    case 1: MOE_TRACE(1) break;
-    case 2: MOE_TRACE(2) break;
-    case 4: MOE_TRACE(4) break;
-    default: return cudaErrorInvalidValue;
-  }
-#undef MOE_TRACE
-  return cudaGetLastError();
-}
-
-cudaError_t launch_trace_commit(const uint32_t* scratch, uint64_t n, const int* bad,
-                                uint32_t* counts, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  k_trace_commit<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
-      scratch, n, bad, counts);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_trace_commit64(const uint32_t* scratch, uint64_t n, const int* bad,
-                                  unsigned long long* counts, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  k_trace_commit64<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, st>>>(
-      scratch, n, bad, counts);
   return cudaGetLastError();
 }
 

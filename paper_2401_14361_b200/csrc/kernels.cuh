@@ -232,16 +232,12 @@ cudaError_t launch_decide(const unsigned long long* agg, uint32_t L, uint32_t E,
                           uint32_t* n_out, long long* victim, double* slot_pri,
                           cudaStream_t st);
 
-// K1 tracing: scratch[R][L][E] (u32, zeroed) += histogram; *bad |= 1 on
-// an out-of-range index.
+// K1 tracing (trace.cu): counts[R][L][E] (count_bytes 4 = u32, 8 = u64) +=
+// the per-request histograms of the ids; an out-of-range id sets *bad and
+// the call's additions are rolled back on the device (all-or-nothing).
 cudaError_t launch_trace(const void* topk, int idx_bytes, uint64_t T, uint32_t L, uint32_t E,
-                         uint32_t k, const uint64_t* offsets, uint64_t R, uint32_t* scratch,
-                         int* bad, int n_sm, cudaStream_t st);
-cudaError_t launch_trace_commit(const uint32_t* scratch, uint64_t n, const int* bad,
-                                uint32_t* counts, cudaStream_t st);
-
-cudaError_t launch_trace_commit64(const uint32_t* scratch, uint64_t n, const int* bad,
-                                  unsigned long long* counts, cudaStream_t st);
+                         uint32_t k, const uint64_t* offsets, uint64_t R, void* counts,
+                         int count_bytes, int* bad, int n_sm, cudaStream_t st);
 
 cudaError_t launch_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32_t RB_old,
                          uint32_t RB_new, int cb_old, int cb_new, cudaStream_t st);

@@ -18,7 +18,7 @@ d_b = torch.zeros(1, dtype=torch.int32, device="cuda")
 sh = m.ModelShape(L, E, k).c()
 st = torch.cuda.Stream(); torch.cuda.set_stream(st)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-for it in range(4):
+for it in range(int(os.environ.get("TRACE_ITERS", "8"))):
     ev[0].record(st)
     _lib.check(_lib.lib.moe_eam_trace_device(C.byref(sh), d_p.data_ptr(), 1, T, d_o.data_ptr(), R,
                                              d_c.data_ptr(), d_b.data_ptr(), C.c_void_p(st.cuda_stream)))
