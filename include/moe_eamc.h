@@ -178,6 +178,34 @@ moe_status moe_match_merge_device(const moe_match* parts, uint64_t n_parts, uint
  * per-shard outputs merge into global slot numbers. */
 moe_status moe_eamc_set_index_base(moe_eamc* h, uint64_t base);
 
+/* A P-sharded Eamc(ModelShape, Phase, capacity) (eam.cpp:106-111; SURVEY.md
+ * 8e) behind the same handle type: n_shards shards, shard s on device
+ * device_ids[s] (ids may repeat: shards sharing one GPU), owning the
+ * contiguous global slot range of its share of the capacity.  Every entry
+ * point of this header that takes host pointers (insert, build, append,
+ * match, match_packed, match_within, prefetch_priorities, decide, entry,
+ * info, clone, save, destroy, build_from_traces) works on it with exactly the
+ * unsharded semantics and results: matching = per-shard matcher + all-gather
+ * of the per-shard {index, seq, distance} (24 B per probe per shard) + the
+ * lexicographic (distance, seq) merge; prefetch = per-shard exact distances,
+ * MIN all-reduce, per-shard u64 window aggregates, SUM all-reduce, order on
+ * shard 0; insert at capacity = the sharded match of the incoming EAM picks
+ * the victim.  With every shard on its own device the collectives are NCCL
+ * (libnccl.so.2, loaded at run time; failures are MOE_ERR_NCCL); shards that
+ * share a device (or MOE_SHARD_NCCL=0) use stream-ordered device copies and
+ * reduction kernels.  The `_device` entry points and set_index_base apply to
+ * single-device handles only (MOE_ERR_INVALID_ARGUMENT here). */
+moe_status moe_eamc_create_sharded(const moe_shape* shape, moe_phase phase, uint64_t capacity,
+                                   int count_bytes, int n_shards, const int* device_ids,
+                                   moe_eamc** out);
+/* Eamc::load (eam.cpp:207-256) into a sharded collection (same snapshot
+ * semantics as moe_eamc_load; a snapshot whose capacity is below n_shards
+ * loads as a single-device collection on device_ids[0]). */
+moe_status moe_eamc_load_sharded(const char* path, const moe_shape* expected, int n_shards,
+                                 const int* device_ids, moe_eamc** out);
+/* n_shards (1 for a single-device handle) and whether NCCL carries its collectives. */
+moe_status moe_eamc_shard_layout(const moe_eamc* h, int* n_shards, int* uses_nccl);
+
 /* Instrumentation: when enabled, matching records CUDA events around its
  * kernels on the launching stream; ms[0..2] = accumulated device time of
  * probe packing, the screen pass and the refine pass, calls[0..2] their

@@ -719,6 +719,13 @@ moe_status replace_slot(moe_eamc* h, const uint64_t* counts, uint64_t slot, uint
   return MOE_OK;
 }
 
+moe_status ensure_width(moe_eamc* h, uint64_t mx) {
+  HandleLock hl_(h);
+  DeviceGuard dg(h->device);
+  if (mx <= width_max(h->c.cb)) return MOE_OK;
+  return widen_for(h, mx);
+}
+
 moe_status window_list(moe_eamc* h, uint64_t dmin_bits, double window,
                        std::vector<moe::WinEntry>* v) {
   HandleLock hl_(h);
@@ -811,8 +818,56 @@ moe_status moe_eamc_create(const moe_shape* shape, moe_phase phase, uint64_t cap
   return MOE_OK;
 }
 
+moe_status moe_eamc_create_sharded(const moe_shape* shape, moe_phase phase, uint64_t capacity,
+                                   int count_bytes, int n_shards, const int* device_ids,
+                                   moe_eamc** out) {
+  if (phase != MOE_PHASE_PREFILL && phase != MOE_PHASE_DECODE)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "bad phase");
+  if (count_bytes != 0 && count_bytes != 1 && count_bytes != 2 && count_bytes != 4)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 0, 1, 2 or 4");
+  return moe::abi::sh_create(shape, phase, capacity, count_bytes, n_shards, device_ids, out);
+}
+
+moe_status moe_eamc_load_sharded(const char* path, const moe_shape* expected, int n_shards,
+                                 const int* device_ids, moe_eamc** out) {
+  if (!out || !device_ids || n_shards < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "bad argument");
+  moe_eamc* one = nullptr;
+  CKS(moe_eamc_load(path, expected, device_ids[0], &one));
+  if (one->capacity < (uint64_t)n_shards || n_shards == 1) {
+    *out = one;
+    return MOE_OK;
+  }
+  moe_eamc* h = nullptr;
+  moe_status st = moe::abi::sh_create(&one->shape, (moe_phase)one->phase, one->capacity,
+                                      one->c.cb, n_shards, device_ids, &h);
+  const uint64_t cells = (uint64_t)one->c.L * one->c.E, n = one->c.size;
+  std::vector<uint64_t> counts(n * cells), seqs(n);
+  for (uint64_t i = 0; i < n && st == MOE_OK; ++i)
+    st = moe_eamc_entry(one, i, counts.data() + i * cells, &seqs[i]);
+  if (st == MOE_OK && n) st = moe_eamc_append(h, counts.data(), seqs.data(), n);
+  if (st == MOE_OK) h->next_seq = one->next_seq;
+  moe_eamc_destroy(one);
+  if (st != MOE_OK) {
+    moe_eamc_destroy(h);
+    return st;
+  }
+  *out = h;
+  return MOE_OK;
+}
+
+moe_status moe_eamc_shard_layout(const moe_eamc* h, int* n_shards, int* uses_nccl) {
+  if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  if (!h->sh) {
+    if (n_shards) *n_shards = 1;
+    if (uses_nccl) *uses_nccl = 0;
+    return MOE_OK;
+  }
+  return moe::abi::sh_layout(h, n_shards, uses_nccl);
+}
+
 moe_status moe_eamc_destroy(moe_eamc* h) {
   if (!h) return MOE_OK;
+  if (h->sh) return moe::abi::sh_destroy(h);
   DeviceGuard dg(h->device);
   cudaStreamSynchronize(h->st);
   delete h;
@@ -828,6 +883,7 @@ moe_status moe_eamc_info(const moe_eamc* h, moe_shape* shape, int* phase, uint64
   if (size) *size = h->c.size;
   if (next_seq) *next_seq = h->next_seq;
   if (count_bytes) *count_bytes = h->c.cb;
+  if (h->sh) return moe::abi::sh_info(h, size, count_bytes);
   return MOE_OK;
 }
 
@@ -835,6 +891,7 @@ moe_status moe_eamc_entry(const moe_eamc* hc, uint64_t index, uint64_t* counts, 
   HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  if (h->sh) return moe::abi::sh_entry(h, index, counts, seq);
   if (index >= h->c.size) return fail(MOE_ERR_OUT_OF_RANGE, "entry index out of range");
   DeviceGuard dg(h->device);
   return read_entry(h, index, counts, seq);
@@ -848,6 +905,7 @@ moe_status moe_eamc_insert(moe_eamc* h, const uint64_t* counts, moe_eam_kind kin
   if (kind != MOE_KIND_REQUEST)
     return fail(MOE_ERR_INVALID_ARGUMENT, "Eamc::insert: only request-level EAMs are stored");
   if ((int)phase != h->phase) return fail(MOE_ERR_INVALID_ARGUMENT, "Eamc::insert: phase mismatch");
+  if (h->sh) return moe::abi::sh_insert(h, counts, evicted_slot, evicted_counts);
   DeviceGuard dg(h->device);
   const uint64_t cells = (uint64_t)h->c.L * h->c.E;
   Staged s;
@@ -904,6 +962,7 @@ moe_status moe_eamc_build(moe_eamc* h, const uint64_t* counts, uint64_t n,
                           int64_t* evicted_slots) {
   HandleLock hl_(h);
   if (!h || (!counts && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->sh) return moe::abi::sh_build(h, counts, n, evicted_slots);
   DeviceGuard dg(h->device);
   const uint64_t cells = (uint64_t)h->c.L * h->c.E;
   const uint64_t chunk = std::max<uint64_t>(1, (256ull << 20) / (cells * 8));
@@ -950,6 +1009,7 @@ static moe_status append_impl(moe_eamc* h, const void* counts, int cbytes, const
 moe_status moe_eamc_append(moe_eamc* h, const uint64_t* counts, const uint64_t* seqs, uint64_t n) {
   HandleLock hl_(h);
   if (!h || ((!counts || !seqs) && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->sh) return moe::abi::sh_append(h, counts, 8, seqs, n);
   DeviceGuard dg(h->device);
   return append_impl(h, counts, 8, seqs, n);
 }
@@ -960,6 +1020,7 @@ moe_status moe_eamc_append_packed(moe_eamc* h, const void* counts, int count_byt
   if (!h || ((!counts || !seqs) && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (count_bytes != 1 && count_bytes != 2 && count_bytes != 4 && count_bytes != 8)
     return fail(MOE_ERR_INVALID_ARGUMENT, "count_bytes must be 1, 2, 4 or 8");
+  if (h->sh) return moe::abi::sh_append(h, counts, count_bytes, seqs, n);
   DeviceGuard dg(h->device);
   return append_impl(h, counts, count_bytes, seqs, n);
 }
@@ -1095,6 +1156,12 @@ moe_status moe_eamc_match(const moe_eamc* hc, const uint64_t* probes, uint64_t n
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || ((!probes || !out) && n_probes)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   if (n_probes == 0) return MOE_OK;
+  if (h->sh) {
+    CKS(moe::abi::sh_match(h, probes, n_probes, out));
+    if (found)
+      for (uint64_t q = 0; q < n_probes; ++q) found[q] = out[q].index != ~0ull;
+    return MOE_OK;
+  }
   DeviceGuard dg(h->device);
   const uint64_t cells = (uint64_t)h->c.L * h->c.E;
   const uint64_t bytes = n_probes * cells * 8;
@@ -1196,6 +1263,9 @@ moe_status moe_eamc_match_device(const moe_eamc* hc, const void* probes, int pro
     return fail(MOE_ERR_INVALID_ARGUMENT, "probe_bytes must be 1, 2, 4 or 8");
   if (n_probes == 0) return MOE_OK;
   if (n_probes > 0xffffffffull) return fail(MOE_ERR_INVALID_ARGUMENT, "too many probes");
+  if (h->sh)
+    return fail(MOE_ERR_INVALID_ARGUMENT,
+                "moe_eamc_match_device: a sharded collection spans devices; use moe_eamc_match");
   DeviceGuard dg(h->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->st;
   DevProbes pr;
@@ -1217,6 +1287,15 @@ moe_status moe_eamc_match_packed(const moe_eamc* hc, const void* probes, int pro
     return fail(MOE_ERR_INVALID_ARGUMENT, "probe_bytes must be 1, 2, 4 or 8");
   if (n_probes == 0) return MOE_OK;
   if (n_probes > 0xffffffffull) return fail(MOE_ERR_INVALID_ARGUMENT, "too many probes");
+  if (h->sh) {  // the sharded matcher packs u64 probes itself
+    const uint64_t m = n_probes * (uint64_t)h->c.L * h->c.E;
+    std::vector<uint64_t> wide(m);
+    for (uint64_t i = 0; i < m; ++i)
+      wide[i] = probe_bytes == 1 ? static_cast<const uint8_t*>(probes)[i]
+                : probe_bytes == 2 ? static_cast<const uint16_t*>(probes)[i]
+                                   : static_cast<const uint32_t*>(probes)[i];
+    return moe_eamc_match(hc, wide.data(), n_probes, out, found);
+  }
   DeviceGuard dg(h->device);
   const uint64_t bytes = n_probes * (uint64_t)h->c.L * h->c.E * probe_bytes;
   CK(h->raw.ensure(bytes + 16));
@@ -1238,6 +1317,7 @@ moe_status moe_eamc_match_within(const moe_eamc* hc, const uint64_t* probe, doub
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !probe || !n_out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   *n_out = 0;
+  if (h->sh) return moe::abi::sh_match_within(h, probe, window, out, cap, n_out);
   if (h->c.size == 0) return MOE_OK;
   DeviceGuard dg(h->device);
   cudaStream_t st = h->st;
@@ -1300,6 +1380,7 @@ moe_status moe_eamc_clone(const moe_eamc* hc, moe_eamc** out) {
   HandleLock hl_(hc);
   moe_eamc* src = const_cast<moe_eamc*>(hc);
   if (!src || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (src->sh) return moe::abi::sh_clone(src, out);
   DeviceGuard dg(src->device);
   const uint64_t cells = (uint64_t)src->c.L * src->c.E, n = src->c.size;
   std::vector<uint64_t> counts(n * cells), seqs(n);
@@ -1321,6 +1402,8 @@ moe_status moe_eamc_clone(const moe_eamc* hc, moe_eamc** out) {
 }
 
 moe_status moe_eamc_set_index_base(moe_eamc* h, uint64_t base) {
+  if (h && h->sh)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "a sharded collection sets its shards' index bases");
   HandleLock hl_(h);
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
   h->c.index_base = base;
@@ -1330,6 +1413,7 @@ moe_status moe_eamc_set_index_base(moe_eamc* h, uint64_t base) {
 moe_status moe_eamc_set_profiling(moe_eamc* h, int enable) {
   HandleLock hl_(h);
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  if (h->sh) return fail(MOE_ERR_INVALID_ARGUMENT, "profiling is per shard handle");
   DeviceGuard dg(h->device);
   if (h->ring.empty()) {
     h->ring.resize(256);
@@ -1741,6 +1825,8 @@ moe_status moe_prefetch_priorities(const moe_eamc* hc, const uint64_t* cur_eam,
   if (current_layer >= h->shape.n_layers)
     return fail(MOE_ERR_OUT_OF_RANGE, "prefetch_priorities: current_layer out of range");
   *n_out = 0;
+  if (h->sh)
+    return moe::abi::sh_prefetch(h, cur_eam, current_layer, apply_floor_filter, out, cap, n_out);
   if (h->c.size == 0) return MOE_OK;
   DeviceGuard dg(h->device);
   return decide_impl(h, &h->shape, cur_eam, current_layer, apply_floor_filter, 1, nullptr, nullptr,
@@ -1761,6 +1847,7 @@ moe_status moe_eamc_window_min_device(const moe_eamc* hc, const uint64_t* cur_ea
   HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !cur_eam || !d_min_bits) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->sh) return fail(MOE_ERR_INVALID_ARGUMENT, "device decision steps are per shard handle");
   DeviceGuard dg(h->device);
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->st;
   CK(h->small.ensure(256));
@@ -1790,6 +1877,7 @@ moe_status moe_eamc_window_aggregate_device(const moe_eamc* hc, uint32_t current
   HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !d_min_bits || !agg) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->sh) return fail(MOE_ERR_INVALID_ARGUMENT, "device decision steps are per shard handle");
   if (current_layer >= h->shape.n_layers)
     return fail(MOE_ERR_OUT_OF_RANGE, "prefetch_priorities: current_layer out of range");
   DeviceGuard dg(h->device);
@@ -1812,6 +1900,7 @@ moe_status moe_eamc_prefetch_order_device(const moe_eamc* hc, const uint64_t* ag
   HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !agg || !out || !n_out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->sh) return fail(MOE_ERR_INVALID_ARGUMENT, "device decision steps are per shard handle");
   const uint32_t L = h->shape.n_layers, E = h->shape.n_experts_per_layer;
   if (current_layer >= L)
     return fail(MOE_ERR_OUT_OF_RANGE, "prefetch_priorities: current_layer out of range");
@@ -1869,6 +1958,13 @@ moe_status moe_decide(const moe_eamc* hc, const uint64_t* cur_eam, uint32_t curr
     if (slots[i].layer_idx >= h->shape.n_layers ||
         slots[i].expert_idx >= h->shape.n_experts_per_layer)
       return fail(MOE_ERR_OUT_OF_RANGE, "cache_priority: expert out of range");
+  if (h->sh) {  // the sharded prefetch order, then the (unsharded) eviction scoring
+    uint64_t n = 0;
+    CKS(moe::abi::sh_prefetch(h, cur_eam, current_layer, 1, out, cap, &n));
+    if (n_out) *n_out = n;
+    if (victim) CKS(moe_select_eviction_victim(&h->shape, request_eam, slots, n_slots, victim));
+    return MOE_OK;
+  }
   DeviceGuard dg(h->device);
   return decide_impl(h, &h->shape, cur_eam, current_layer, 1, 1, request_eam, slots, n_slots, out,
                      cap, n_out, victim, nullptr);
@@ -2115,6 +2211,7 @@ moe_status moe_eamc_save(const moe_eamc* hc, const char* path) {
   HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !path) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->sh) return moe::abi::sh_save(h, path);
   DeviceGuard dg(h->device);
   const DevColl& c = h->c;
   const uint64_t LR = (uint64_t)c.L * c.RB;

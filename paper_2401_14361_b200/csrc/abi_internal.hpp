@@ -230,8 +230,16 @@ moe_status replace_slot(moe_eamc* h, const uint64_t* counts, uint64_t slot, uint
 // distances the last moe_eamc_window_min_device on `h` left; global indices.
 moe_status window_list(moe_eamc* h, uint64_t dmin_bits, double window,
                        std::vector<moe::WinEntry>* v);
+// Widen the collection so counts up to mx are representable (MOE_ERR_OVERFLOW
+// past 2^32 - 1).
+moe_status ensure_width(moe_eamc* h, uint64_t mx);
 // Sharded facade entry points (sharded.cu), called by the public C ABI when
 // h->sh is set.
+moe_status sh_create(const moe_shape* shape, moe_phase phase, uint64_t capacity, int count_bytes,
+                     int n_shards, const int* device_ids, moe_eamc** out);
+moe_status sh_layout(const moe_eamc* h, int* n_shards, int* use_nccl);
+moe_status sh_clone(const moe_eamc* h, moe_eamc** out);
+moe_status sh_save(const moe_eamc* h, const char* path);
 moe_status sh_destroy(moe_eamc* h);
 moe_status sh_info(const moe_eamc* h, uint64_t* size, int* count_bytes);
 moe_status sh_entry(moe_eamc* h, uint64_t index, uint64_t* counts, uint64_t* seq);

@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "moe_eamc.h"
 #include "moesim/eam.hpp"
@@ -35,6 +36,24 @@ inline moe_shape to_c(const ModelShape& s) {
 inline int device() {
   const char* v = std::getenv("MOE_EAMC_DEVICE");
   return v ? std::atoi(v) : 0;
+}
+
+/// P-sharded collections: $MOE_EAMC_SHARDS = comma-separated
+/// device ids, one shard each (repeats allowed), e.g. "0,1,2,3,4,5,6,7"; empty
+/// or unset = one single-device collection.
+inline std::vector<int> shard_devices() {
+  std::vector<int> ids;
+  const char* v = std::getenv("MOE_EAMC_SHARDS");
+  if (!v) return ids;
+  std::string s(v);
+  size_t i = 0;
+  while (i < s.size()) {
+    size_t j = s.find(',', i);
+    if (j == std::string::npos) j = s.size();
+    if (j > i) ids.push_back(std::atoi(s.substr(i, j - i).c_str()));
+    i = j + 1;
+  }
+  return ids;
 }
 
 }  // namespace moesim::dropin

@@ -89,8 +89,12 @@ Eamc::Eamc(ModelShape shape, Phase phase, std::size_t capacity)
   shape_.validate();
   if (capacity_ < 1) throw std::invalid_argument("Eamc: capacity must be >= 1");
   const moe_shape s = to_c(shape_);
-  check(moe_eamc_create(&s, phase == Phase::prefill ? MOE_PHASE_PREFILL : MOE_PHASE_DECODE,
-                        capacity_, 0, dropin::device(), &h_));
+  const moe_phase ph = phase == Phase::prefill ? MOE_PHASE_PREFILL : MOE_PHASE_DECODE;
+  const std::vector<int> shards = dropin::shard_devices();
+  if (shards.size() > 1 && capacity_ >= shards.size())
+    check(moe_eamc_create_sharded(&s, ph, capacity_, 0, (int)shards.size(), shards.data(), &h_));
+  else
+    check(moe_eamc_create(&s, ph, capacity_, 0, dropin::device(), &h_));
 }
 
 Eamc::Eamc(moe_eamc* h) : h_(h) {
@@ -202,17 +206,24 @@ void Eamc::save(const std::filesystem::path& path) const {
   check(moe_eamc_save(h_, path.string().c_str()));
 }
 
-Eamc Eamc::load(const std::filesystem::path& path) {
+namespace {
+moe_eamc* load_handle(const std::filesystem::path& path, const moe_shape* expected) {
   moe_eamc* h = nullptr;
-  check(moe_eamc_load(path.string().c_str(), nullptr, dropin::device(), &h));
-  return Eamc(h);
+  const std::vector<int> shards = dropin::shard_devices();
+  if (shards.size() > 1)
+    check(moe_eamc_load_sharded(path.string().c_str(), expected, (int)shards.size(),
+                                shards.data(), &h));
+  else
+    check(moe_eamc_load(path.string().c_str(), expected, dropin::device(), &h));
+  return h;
 }
+}  // namespace
+
+Eamc Eamc::load(const std::filesystem::path& path) { return Eamc(load_handle(path, nullptr)); }
 
 Eamc Eamc::load(const std::filesystem::path& path, const ModelShape& expected) {
   const moe_shape s = to_c(expected);
-  moe_eamc* h = nullptr;
-  check(moe_eamc_load(path.string().c_str(), &s, dropin::device(), &h));
-  return Eamc(h);
+  return Eamc(load_handle(path, &s));
 }
 
 std::uint64_t eamc_capacity_bound(const ModelShape& shape, double similarity) {

@@ -183,6 +183,26 @@ class Eamc:
                                       C.byref(self._h)))
         self.device = device
 
+    @classmethod
+    def sharded(cls, shape: ModelShape, phase: Phase = Phase.decode, capacity: int = 1,
+                device_ids: Sequence[int] = (0,), count_bytes: int = 0) -> "Eamc":
+        """A P-sharded collection with the unsharded Eamc semantics:
+        shard s on device_ids[s] (ids may repeat), contiguous global slot ranges,
+        NCCL collectives when every shard has its own GPU
+        (moe_eamc_create_sharded)."""
+        h = C.c_void_p()
+        ids = (C.c_int * len(device_ids))(*device_ids)
+        sh = shape.c()
+        check(lib.moe_eamc_create_sharded(C.byref(sh), int(phase), capacity, count_bytes,
+                                          len(device_ids), ids, C.byref(h)))
+        return cls(shape, phase, capacity, device=device_ids[0], _handle=h)
+
+    def shard_layout(self) -> Tuple[int, bool]:
+        """(number of shards, whether NCCL carries the collectives)."""
+        n, nccl = C.c_int(), C.c_int()
+        check(lib.moe_eamc_shard_layout(self._h, C.byref(n), C.byref(nccl)))
+        return n.value, bool(nccl.value)
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:

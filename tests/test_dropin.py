@@ -87,3 +87,37 @@ def test_reference_acceptance_suite_on_gpu():
             continue
         assert g.rstrip() == w.rstrip(), (g, w)
         assert g.startswith("[PASS]"), g
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shards", ["0,0,0"])
+def test_reference_path_unit_tests_on_sharded_gpu_collections(shards):
+    """The same 56 reference cases with every Eamc the reference code creates
+    (or loads) P-sharded over 3 shards (MOE_EAMC_SHARDS; they share GPU 0
+    here): the drop-in builds sharded collections through the C ABI and the
+    reference's own assertions hold unchanged."""
+    _need(TESTS_GPU)
+    env = dict(os.environ, MOE_EAMC_SHARDS=shards)
+    r = subprocess.run([TESTS_GPU], capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout + r.stderr
+    m = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed", r.stdout)
+    assert m and int(m.group(3)) == 0 and int(m.group(1)) >= 56, r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_on_sharded_gpu_collections():
+    """acceptance_main.cpp with 3-way sharded collections: every criterion's
+    numbers equal the reference CPU build's (criterion 9: absolute bound)."""
+    _need(ACC_GPU)
+    env = dict(os.environ, MOE_EAMC_SHARDS="0,0,0")
+    r = subprocess.run([ACC_GPU], capture_output=True, text=True, timeout=1500, env=env)
+    got = [re.sub(r"\([ 0-9.]*s\)", "", ln) for ln in r.stdout.splitlines() if "criterion" in ln
+           and "failed" not in ln]
+    want = [ln.rstrip("\n") for ln in open(GOLDEN) if "failed" not in ln]
+    assert len(got) == len(want) == 11, r.stdout
+    for g, w in zip(got, want):
+        if "criterion  9" in w:
+            m = re.search(r"mean 1K=([0-9.]+)us", g)
+            assert m and float(m.group(1)) < 5000.0, g
+            continue
+        assert g.rstrip() == w.rstrip(), (g, w)
