@@ -191,3 +191,106 @@ class ShardedDecider:
             n = int(self._n.item())
             out = self._out[:n].cpu().numpy()
         return out.view(np.uint8).reshape(n, 16).copy().view(self._lib.CAND_DTYPE)[:, 0]
+
+
+# ---------------------------------------------------------------- K1 tracing
+def request_split(offsets: np.ndarray, rank: int, world: int) -> Tuple[int, int]:
+    """Request-owned split of K1: rank r takes the contiguous
+    requests [r0, r1) whose token ranges start in its 1/world share of the
+    token stream (balanced by tokens, not by request count).  Each rank traces
+    its own requests; no collective."""
+    offsets = np.asarray(offsets, np.uint64)
+    T0, T1 = int(offsets[0]), int(offsets[-1])
+    R = len(offsets) - 1
+
+    def cut(k):
+        t = T0 + (T1 - T0) * k // world
+        return int(np.searchsorted(offsets[:R], t, side="left")) if k < world else R
+    return cut(rank), cut(rank + 1)
+
+
+def token_split(n_tokens: int, offsets: np.ndarray, rank: int, world: int):
+    """Token-sharded split of K1: rank r takes tokens [t0, t1) of the stream;
+    returns (t0, t1, local_offsets) with every request's range clipped to the
+    rank's tokens (requests outside it become empty), so the rank's partial
+    histograms sum over ranks to Eam::record over the whole request."""
+    base, rem = divmod(n_tokens, world)
+    t0 = rank * base + min(rank, rem)
+    t1 = t0 + base + (1 if rank < rem else 0)
+    off = np.asarray(offsets, np.uint64).astype(np.int64)
+    local = np.clip(off - t0, 0, t1 - t0).astype(np.uint64)
+    return t0, t1, local
+
+
+class ShardedTracer:
+    """Token-sharded K1 (Eam::record, eam.cpp:41-52, over router top-k ids):
+    each rank histograms its token range of every request it intersects into a
+    zeroed partial [R][L][E] u32 (moe_eam_trace_device), the out-of-range flag
+    is MAX-all-reduced and the partials SUM-all-reduced (exact, order-free
+    integer sums; NCCL over NVLink in production), and the sum is added to the
+    caller's counts on every rank.  All-or-nothing across ranks (eam.cpp:42-47):
+    an out-of-range id on any rank raises IndexError on every rank with the
+    counts untouched.  The exchange is R*L*E*4 bytes, independent of T.
+
+    `local`/`allreduce` are injectable so one process can drive several
+    ranks' device steps (single-GPU tests) and CPU tests can stand an oracle in
+    for the device step."""
+
+    def __init__(self, shape, rank: int, world: int, group=None, local=None, allreduce=None):
+        self.shape, self.rank, self.world, self.group = shape, rank, world, group
+        self._local = local or self._device_local
+        self._allreduce = allreduce or self._dist_allreduce
+
+    def _device_local(self, topk_local, local_offsets, partial, bad, stream):
+        """This rank's device step: partial += histograms of its tokens."""
+        import torch
+        from . import _lib
+        sh = self.shape.c()
+        with torch.cuda.stream(stream):
+            d_off = torch.from_numpy(np.ascontiguousarray(local_offsets).view(np.int64)).to(
+                partial.device, non_blocking=False)
+            _lib.check(_lib.lib.moe_eam_trace_device(
+                C.byref(sh), C.c_void_p(topk_local.data_ptr()), topk_local.element_size(),
+                C.c_uint64(topk_local.shape[0]), C.c_void_p(d_off.data_ptr()),
+                C.c_uint64(len(local_offsets) - 1), C.c_void_p(partial.data_ptr()),
+                C.c_void_p(bad.data_ptr()), C.c_void_p(stream.cuda_stream)))
+        return d_off  # kept alive until the stream has used it
+
+    def _dist_allreduce(self, t, op):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM,
+                            group=self.group)
+
+    def trace(self, topk_local, n_tokens: int, offsets: np.ndarray, counts, stream=None):
+        """topk_local: this rank's ids [t1-t0][L][k] (token_split); offsets:
+        the GLOBAL request offsets; counts: [R][L][E] int32 tensor, accumulated."""
+        import torch
+        t0, t1, local = token_split(n_tokens, offsets, self.rank, self.world)
+        if topk_local.shape[0] != t1 - t0:
+            raise ValueError("trace: topk_local must hold this rank's token range")
+        stream = stream or (torch.cuda.current_stream(counts.device)
+                            if counts.is_cuda else None)
+        if counts.is_cuda:  # inputs made on the caller's current stream
+            stream.wait_stream(torch.cuda.current_stream(counts.device))
+        ctx = torch.cuda.stream(stream) if counts.is_cuda else _null()
+        with ctx:
+            partial = torch.zeros_like(counts)
+            bad = torch.zeros(1, dtype=torch.int32, device=counts.device)
+        keep = self._local(topk_local, local, partial, bad, stream)
+        with ctx:
+            self._allreduce(bad, "max")
+            if int(bad.item()):  # some rank saw an id >= E: nobody's counts move
+                raise IndexError("Eam::record: expert index out of range")
+            self._allreduce(partial, "sum")
+            counts += partial
+        del keep
+        return counts
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False

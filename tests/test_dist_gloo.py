@@ -157,3 +157,104 @@ def test_sharded_decide_gloo_world2():
         p.join(timeout=240)
         assert p.exitcode == 0
     assert q.get(timeout=10) is True
+
+
+def _trace_worker(rank, world, port, bad_rank, out_q):
+    """sharded.ShardedTracer (token-sharded K1) over gloo, the ORACLE standing
+    in for each rank's device step on its clipped token range: MAX all-reduce
+    of the range flag, SUM all-reduce of the partials, accumulate.  Must equal
+    the oracle's Eam::record over the whole requests; with an out-of-range id
+    on one rank, every rank raises and nobody's counts move."""
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, Workload
+    from paper_2401_14361_b200.eamc import ModelShape
+    from paper_2401_14361_b200.sharded import ShardedTracer, request_split, token_split
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle()
+    L, E, k = 12, 32, 2
+    w = Workload(L, E, k, n_groups=6, prompt_len=5, decode_len=7, batch_size=3, seed=13)
+    picks, offs = [], [0]
+    for r in range(9):
+        _, pk = orc.trace_picks(w, r)
+        picks.append(pk)
+        offs.append(offs[-1] + pk.shape[0])
+    picks = np.concatenate(picks).astype(np.uint32)
+    offs = np.array(offs, np.uint64)
+    offs[4] = offs[3]  # an empty request
+    T = picks.shape[0]
+    if bad_rank >= 0:
+        t0b, t1b, _ = token_split(T, offs, bad_rank, world)
+        picks[(t0b + t1b) // 2, 3, 1] = E
+    rc_all, want = orc.trace(L, E, k, picks, offs)
+
+    def local(topk_local, local_offsets, partial, bad, stream):
+        rc, part = orc.trace(L, E, k, np.ascontiguousarray(topk_local), local_offsets)
+        if rc != 0:
+            bad[0] = 1
+        else:
+            partial += torch.from_numpy(part.astype(np.int32))
+
+    t0, t1, _ = token_split(T, offs, rank, world)
+    tr = ShardedTracer(ModelShape(L, E, k), rank, world, local=local)
+    base = torch.full((len(offs) - 1, L, E), 3, dtype=torch.int32)
+    counts = base.clone()
+    raised = False
+    try:
+        tr.trace(picks[t0:t1], T, offs, counts)
+    except IndexError:
+        raised = True
+    ok = True
+    if bad_rank >= 0:
+        ok &= raised and torch.equal(counts, base) and rc_all != 0
+    else:
+        ok &= (not raised) and np.array_equal(counts.numpy().astype(np.uint64) - 3, want)
+        # request-owned split: each rank traces its own requests, no collective
+        r0, r1 = request_split(offs, rank, world)
+        a, b = int(offs[r0]), int(offs[r1])
+        rc, mine = orc.trace(L, E, k, picks[a:b], offs[r0:r1 + 1] - offs[r0])
+        ok &= rc == 0 and np.array_equal(mine, want[r0:r1])
+        spans = [torch.tensor([r0, r1])]
+        gathered = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(gathered, spans[0])
+        cov = sorted((int(g[0]), int(g[1])) for g in gathered)
+        ok &= cov[0][0] == 0 and cov[-1][1] == len(offs) - 1 and all(
+            cov[i][1] == cov[i + 1][0] for i in range(world - 1))
+    flags = torch.tensor([int(bool(ok))])
+    dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        out_q.put(bool(flags.item()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("bad_rank", [-1, 1])
+def test_sharded_trace_gloo_world2(bad_rank):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_trace_worker, args=(r, 2, port, bad_rank, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
+
+
+def test_trace_splits_partition():
+    from paper_2401_14361_b200.sharded import request_split, token_split
+    offs = np.array([0, 10, 10, 250, 251, 900, 1000], np.uint64)
+    for N in (1, 2, 3, 8):
+        rs = [request_split(offs, r, N) for r in range(N)]
+        assert rs[0][0] == 0 and rs[-1][1] == 6
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(N - 1))
+        tot = np.zeros(6, np.int64)
+        for r in range(N):
+            t0, t1, loc = token_split(1000, offs, r, N)
+            assert np.all(np.diff(loc.astype(np.int64)) >= 0) and loc[-1] <= t1 - t0
+            tot += np.diff(loc.astype(np.int64))
+        assert np.array_equal(tot, np.diff(offs.astype(np.int64)))

@@ -177,3 +177,28 @@ def test_trace_wide_shape(m, orc):
     for dt in (np.uint16, np.uint32):
         got = m.trace_requests(m.ModelShape(L, E, k), picks.astype(dt), offs)
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_tracer_device_steps(m, orc, world):
+    """Token-sharded K1 (sharded.ShardedTracer) with the real device step: the
+    ranks are emulated one after another on this GPU, each adding its partial
+    (the SUM all-reduce's result is the sum of the partials); the total equals
+    the oracle's Eam::record over the whole requests, with requests cut by the
+    rank boundaries."""
+    import torch
+    from paper_2401_14361_b200.sharded import ShardedTracer, token_split
+    L, E, k, T = 59, 160, 6, 50_000
+    rng = np.random.default_rng(21)
+    picks = _picks(rng, T, L, E, k).astype(np.uint8)
+    offs = _ragged_offsets(rng, T, 23)
+    want = _oracle_trace(orc, L, E, k, picks, offs)
+    counts = torch.zeros((len(offs) - 1, L, E), dtype=torch.int32, device="cuda")
+    st = torch.cuda.Stream()
+    for rank in range(world):
+        t0, t1, _ = token_split(T, offs, rank, world)
+        tr = ShardedTracer(m.ModelShape(L, E, k), rank, world, allreduce=lambda t, op: None)
+        tr.trace(torch.from_numpy(np.ascontiguousarray(picks[t0:t1])).cuda(), T, offs, counts,
+                 stream=st)
+    st.synchronize()
+    assert np.array_equal(counts.cpu().numpy().astype(np.uint64), want)
