@@ -43,6 +43,7 @@ namespace moe {
 namespace {
 
 constexpr uint32_t kDecThreads = 256;
+
 constexpr uint32_t kDecWarpsPerCta = kDecThreads / 32;
 
 __device__ __forceinline__ bool pair_lt(unsigned long long ka, uint32_t ia, unsigned long long kb,
@@ -290,21 +291,43 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decision(const __grid_consta
       __syncthreads();
       const uint32_t np_l = n_pass;
       if (np <= 512) {
-        // small layers: each survivor's in-layer position = the number of
+        // small layers: survivors compacted (ballot prefix, in expert order),
+        // then each survivor's in-layer position = the number of survivor
         // (key, id) pairs below it (broadcast reads), one scatter
-        uint32_t pos[2] = {0, 0};
-        for (uint32_t u = 0; u < 2; ++u) {
-          const uint32_t i = tid + u * kDecThreads;
-          if (i < np && sk[i] != ~0ull)
-            for (uint32_t j = 0; j < np; ++j) pos[u] += pair_lt(sk[j], si[j], sk[i], si[i]);
-        }
-        for (uint32_t u = 0; u < 2; ++u) {
-          const uint32_t i = tid + u * kDecThreads;
-          if (i < np && sk[i] != ~0ull) {
-            a.ckey[(uint64_t)li * E + pos[u]] = sk[i];
-            a.cid[(uint64_t)li * E + pos[u]] = si[i];
-            a.crank[(uint64_t)li * E + pos[u]] = pos[u];
+        unsigned long long* ck = sk + 2 * np;  // compact copies behind the slots
+        uint32_t* ci = reinterpret_cast<uint32_t*>(ck + np);
+        __shared__ uint32_t wofs[kDecWarpsPerCta + 1];
+        for (uint32_t e0 = 0; e0 < np; e0 += kDecThreads) {
+          const uint32_t e = e0 + tid;
+          const bool sv = e < np && sk[e] != ~0ull;
+          const uint32_t m = __ballot_sync(0xffffffffu, sv);
+          if (lane == 0) wofs[wid] = __popc(m);
+          __syncthreads();
+          if (tid == 0) {
+            uint32_t o = e0 == 0 ? 0u : wofs[kDecWarpsPerCta];
+            for (uint32_t w = 0; w < kDecWarpsPerCta; ++w) {
+              const uint32_t c = wofs[w];
+              wofs[w] = o;
+              o += c;
+            }
+            wofs[kDecWarpsPerCta] = o;
           }
+          __syncthreads();
+          if (sv) {
+            const uint32_t q = wofs[wid] + __popc(m & ((1u << lane) - 1u));
+            ck[q] = sk[e];
+            ci[q] = si[e];
+          }
+          __syncthreads();
+        }
+        for (uint32_t i = tid; i < np_l; i += kDecThreads) {
+          const unsigned long long ki = ck[i];
+          const uint32_t ii = ci[i];
+          uint32_t pos = 0;
+          for (uint32_t j = 0; j < np_l; ++j) pos += pair_lt(ck[j], ci[j], ki, ii);
+          a.ckey[(uint64_t)li * E + pos] = ki;
+          a.cid[(uint64_t)li * E + pos] = ii;
+          a.crank[(uint64_t)li * E + pos] = pos;
         }
         if (tid == 0) a.nseg[li] = np_l;
         __syncthreads();
@@ -365,13 +388,17 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decision(const __grid_consta
   // count to that survivor's rank.
   __shared__ uint32_t offs[kDecMaxLayers + 1];
   if (rows_above > kDecMaxLayers) __trap();  // host checks the bound
+  // segment offsets: all lengths loaded at once, then a serial prefix over
+  // shared memory (a serial loop over global loads costs a latency per layer)
+  for (uint32_t i = tid; i < rows_above; i += kDecThreads) offs[i + 1] = a.nseg[i];
+  __syncthreads();
   if (tid == 0) {
     uint32_t o = 0;
+    offs[0] = 0;
     for (uint32_t i = 0; i < rows_above; ++i) {
-      offs[i] = o;
-      o += a.nseg[i];
+      o += offs[i + 1];
+      offs[i + 1] = o;
     }
-    offs[rows_above] = o;
   }
   __syncthreads();
   const uint32_t S = offs[rows_above];
@@ -497,7 +524,8 @@ size_t decision_smem(uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz, uint32_
   (void)grid;
   uint32_t np = 1;
   while (np < E) np <<= 1;
-  return std::max((size_t)n_nz * RB, (size_t)np * 12);  // staged probe rows | a layer's segment
+  // staged probe rows | a layer's slots + its compacted survivors
+  return std::max((size_t)n_nz * RB, (size_t)np * 28);
 }
 
 int decision_grid(int n_sm, uint32_t size, uint32_t L, uint32_t cur) {

@@ -1,0 +1,59 @@
+// Launch-overhead probe: host time of <<<>>> for kernels with small / ~800 B
+// parameter blocks and large dynamic shared memory, then launch->complete.
+#include <chrono>
+#include <cstdio>
+#include <cuda_runtime.h>
+struct Big { char b[800]; };
+struct Big1k { alignas(16) char b[1100]; };
+__global__ void __launch_bounds__(256, 1) k_gc(const __grid_constant__ Big1k a, int* p) {
+  extern __shared__ int s[];
+  __shared__ int st[4000];
+  st[threadIdx.x] = a.b[threadIdx.x % 1000];
+  s[threadIdx.x] = st[threadIdx.x ^ 1];
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x == 0 && p) *p = s[3];
+}
+__global__ void k_small(int* p) { if (threadIdx.x == 0 && blockIdx.x == 0 && p) *p = 1; }
+__global__ void k_big(Big a, int* p) { if (threadIdx.x == 0 && blockIdx.x == 0 && p) *p = a.b[5]; }
+__global__ void k_smem(Big a, int* p) {
+  extern __shared__ int s[];
+  s[threadIdx.x] = a.b[threadIdx.x % 800];
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x == 0 && p) *p = s[3];
+}
+template <class F> void timeit(const char* name, F f, cudaStream_t st) {
+  double tl = 0, tt = 0;
+  const int n = 200;
+  for (int i = 0; i < n + 10; ++i) {
+    auto t0 = std::chrono::steady_clock::now();
+    f();
+    auto t1 = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(st);
+    auto t2 = std::chrono::steady_clock::now();
+    if (i >= 10) {
+      tl += std::chrono::duration<double, std::micro>(t1 - t0).count();
+      tt += std::chrono::duration<double, std::micro>(t2 - t0).count();
+    }
+  }
+  printf("%-28s launch %.2f us  launch+sync %.2f us\n", name, tl / n, tt / n);
+}
+int main() {
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  int* d;
+  cudaMalloc(&d, 4);
+  Big b = {};
+  cudaFuncSetAttribute(k_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  timeit("small, 1 block", [&] { k_small<<<1, 32, 0, st>>>(d); }, st);
+  timeit("small, 148 blocks x 256", [&] { k_small<<<148, 256, 0, st>>>(d); }, st);
+  timeit("800B params, 148x256", [&] { k_big<<<148, 256, 0, st>>>(b, d); }, st);
+  timeit("800B + 40KB smem 148x256", [&] { k_smem<<<148, 256, 40 * 1024, st>>>(b, d); }, st);
+  timeit("800B + 200KB smem attr", [&] { k_smem<<<148, 256, 4 * 1024, st>>>(b, d); }, st);
+  Big1k b1 = {};
+  cudaFuncSetAttribute(k_gc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  timeit("1.1KB grid_constant 31x256", [&] { k_gc<<<31, 256, 4 * 1024, st>>>(b1, d); }, st);
+  timeit("1.1KB gc + 110KB dyn smem", [&] { k_gc<<<58, 256, 110 * 1024, st>>>(b1, d); }, st);
+  int* hp; cudaMallocHost(&hp, 64);
+  timeit("1.1KB gc, host-mapped out", [&] { k_gc<<<31, 256, 4 * 1024, st>>>(b1, hp); }, st);
+  return 0;
+}
