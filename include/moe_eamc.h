@@ -293,6 +293,11 @@ moe_status moe_eamc_capacity_bound(const moe_shape* shape, double similarity, ui
 
 /* ---- snapshots: Eamc::save / Eamc::load (eam.cpp:184-256), JSON v1 ---- */
 moe_status moe_eamc_save(const moe_eamc* h, const char* path);
+/* Binary fast path (same contents: slot order, seqs, next_seq): a 64-byte
+ * header, seq[size] u64 and the counts at the storage width, written from one
+ * D2H copy (layout in abi.cu).  moe_eamc_load reads either format (by its
+ * magic "MOEEAMCB"). */
+moe_status moe_eamc_save_binary(const moe_eamc* h, const char* path);
 /* expected may be NULL (load(path)) or the configured shape (load(path, shape)). */
 moe_status moe_eamc_load(const char* path, const moe_shape* expected, int device,
                          moe_eamc** out);

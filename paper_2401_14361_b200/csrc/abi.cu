@@ -2211,7 +2211,7 @@ moe_status moe_eamc_save(const moe_eamc* hc, const char* path) {
   HandleLock hl_(hc);
   moe_eamc* h = const_cast<moe_eamc*>(hc);
   if (!h || !path) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
-  if (h->sh) return moe::abi::sh_save(h, path);
+  if (h->sh) return moe::abi::sh_save(h, path, false);
   DeviceGuard dg(h->device);
   const DevColl& c = h->c;
   const uint64_t LR = (uint64_t)c.L * c.RB;
@@ -2241,9 +2241,147 @@ moe_status moe_eamc_save(const moe_eamc* hc, const char* path) {
   return MOE_OK;
 }
 
+// ---- binary snapshots: the fast path next to JSON v1 ----------------------
+// Layout (little-endian): 64-byte header {char magic[8] = "MOEEAMCB"; u32
+// version = 1; u32 n_layers, n_experts_per_layer, top_k, phase (0 prefill,
+// 1 decode), count_bytes (1, 2, 4); u64 capacity, size, next_seq; 8 bytes
+// zero}, then seq[size] u64, then counts [size][L][E] of count_bytes each
+// (the device storage width, unpadded).  Slot order, seqs and next_seq are
+// those of Eamc::save (eam.cpp:184-205); the counts move as one D2H / H2D of
+// the storage-width rows instead of a decimal JSON text.
+namespace {
+struct BinHeader {
+  char magic[8];
+  uint32_t version, L, E, top_k, phase, cb;
+  uint64_t capacity, size, next_seq, zero;
+};
+static_assert(sizeof(BinHeader) == 64, "binary snapshot header");
+constexpr char kBinMagic[8] = {'M', 'O', 'E', 'E', 'A', 'M', 'C', 'B'};
+
+struct StripJob {
+  const uint8_t* rows;  // [n][L][RB]
+  uint8_t* dst;         // [n][L][E*cb]
+  uint64_t n;
+  uint32_t L, RB, rb;
+  int parts;
+};
+void strip_task(void* vj, int t) {
+  StripJob* j = static_cast<StripJob*>(vj);
+  const uint64_t a = j->n * t / j->parts, b = j->n * (t + 1) / j->parts;
+  for (uint64_t i = a; i < b; ++i)
+    for (uint32_t l = 0; l < j->L; ++l)
+      std::memcpy(j->dst + (i * j->L + l) * j->rb, j->rows + (i * j->L + l) * j->RB, j->rb);
+}
+}  // namespace
+
+moe_status moe_eamc_save_binary(const moe_eamc* hc, const char* path) {
+  HandleLock hl_(hc);
+  moe_eamc* h = const_cast<moe_eamc*>(hc);
+  if (!h || !path) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->sh) return moe::abi::sh_save(h, path, true);
+  DeviceGuard dg(h->device);
+  const DevColl& c = h->c;
+  const uint32_t rb = c.E * (uint32_t)c.cb;
+  BinHeader hd{};
+  std::memcpy(hd.magic, kBinMagic, 8);
+  hd.version = 1;
+  hd.L = c.L;
+  hd.E = c.E;
+  hd.top_k = h->shape.top_k;
+  hd.phase = (uint32_t)h->phase;
+  hd.cb = (uint32_t)c.cb;
+  hd.capacity = h->capacity;
+  hd.size = c.size;
+  hd.next_seq = h->next_seq;
+  std::vector<uint8_t> buf(sizeof hd + (size_t)c.size * 8 + (size_t)c.size * c.L * rb);
+  std::memcpy(buf.data(), &hd, sizeof hd);
+  if (c.size) {
+    CK(cudaMemcpy(buf.data() + sizeof hd, c.seq, (size_t)c.size * 8, cudaMemcpyDeviceToHost));
+    const uint64_t LR = (uint64_t)c.L * c.RB;
+    PinBuf rows;
+    CK(rows.ensure((size_t)c.size * LR));
+    CK(cudaMemcpy(rows.p, c.counts, (size_t)c.size * LR, cudaMemcpyDeviceToHost));
+    StripJob j{rows.as<uint8_t>(), buf.data() + sizeof hd + (size_t)c.size * 8, c.size, c.L,
+               c.RB, rb,
+               (int)std::max<uint64_t>(1, std::min<uint64_t>(moe::host::pool_threads(),
+                                                             c.size / 1024 + 1))};
+    moe::host::pool_run(j.parts, strip_task, &j);
+  }
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(MOE_ERR_SNAPSHOT, "cannot open for writing: %s", path);
+  const bool ok = std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+  if (std::fclose(f) != 0 || !ok) return fail(MOE_ERR_SNAPSHOT, "write failed: %s", path);
+  return MOE_OK;
+}
+
+static moe_status load_binary(const char* path, const moe_shape* expected, int device,
+                              moe_eamc** out) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(MOE_ERR_SNAPSHOT, "cannot open for reading: %s", path);
+  std::fseek(f, 0, SEEK_END);
+  const long flen = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  BinHeader hd{};
+  if (flen < (long)sizeof hd || std::fread(&hd, 1, sizeof hd, f) != sizeof hd) {
+    std::fclose(f);
+    return fail(MOE_ERR_SNAPSHOT, "corrupt snapshot: truncated header");
+  }
+  const moe_shape s{hd.L, hd.E, hd.top_k};
+  auto bad = [&](const char* why) {
+    std::fclose(f);
+    return fail(MOE_ERR_SNAPSHOT, "corrupt snapshot: %s", why);
+  };
+  if (hd.version != 1) {
+    std::fclose(f);
+    return fail(MOE_ERR_SNAPSHOT, "unsupported snapshot version");
+  }
+  if (check_shape(&s) != MOE_OK) return bad("bad shape");
+  if (hd.phase > 1) return bad("unknown phase");
+  if (hd.cb != 1 && hd.cb != 2 && hd.cb != 4) return bad("bad count width");
+  if (hd.capacity < 1) return bad("capacity must be >= 1");
+  if (hd.size > hd.capacity) {
+    std::fclose(f);
+    return fail(MOE_ERR_SNAPSHOT, "snapshot holds more entries than its capacity");
+  }
+  const uint64_t body = hd.size * 8 + hd.size * (uint64_t)hd.L * hd.E * hd.cb;
+  if ((uint64_t)flen != sizeof hd + body) return bad("file length does not match its header");
+  if (expected && (expected->n_layers != s.n_layers ||
+                   expected->n_experts_per_layer != s.n_experts_per_layer ||
+                   expected->top_k != s.top_k)) {
+    std::fclose(f);
+    return fail(MOE_ERR_SNAPSHOT, "snapshot shape does not match the configured model shape");
+  }
+  PinBuf data;
+  CK(data.ensure(std::max<uint64_t>(body, 64)));
+  const bool rd = std::fread(data.p, 1, body, f) == body;
+  std::fclose(f);
+  if (!rd) return fail(MOE_ERR_SNAPSHOT, "corrupt snapshot: truncated body");
+  moe_eamc* h = nullptr;
+  CKS(moe_eamc_create(&s, (moe_phase)hd.phase, hd.capacity, (int)hd.cb, device, &h));
+  moe_status st = MOE_OK;
+  if (hd.size) {
+    const uint64_t* seqs = data.as<uint64_t>();
+    st = moe_eamc_append_packed(h, data.as<uint8_t>() + hd.size * 8, (int)hd.cb, seqs, hd.size);
+  }
+  if (st != MOE_OK) {
+    moe_eamc_destroy(h);
+    return st;
+  }
+  h->next_seq = hd.next_seq;
+  *out = h;
+  return MOE_OK;
+}
+
 moe_status moe_eamc_load(const char* path, const moe_shape* expected, int device, moe_eamc** out) {
   if (!path || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
+  {  // format by magic: the binary fast path, else JSON v1
+    FILE* f = std::fopen(path, "rb");
+    char m[8] = {0};
+    const bool bin = f && std::fread(m, 1, 8, f) == 8 && std::memcmp(m, kBinMagic, 8) == 0;
+    if (f) std::fclose(f);
+    if (bin) return load_binary(path, expected, device, out);
+  }
   moe::host::Snapshot snap;
   std::string err;
   if (!moe::host::load_snapshot(path, &snap, &err)) return fail(MOE_ERR_SNAPSHOT, "%s", err.c_str());

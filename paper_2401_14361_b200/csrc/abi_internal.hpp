@@ -239,7 +239,7 @@ moe_status sh_create(const moe_shape* shape, moe_phase phase, uint64_t capacity,
                      int n_shards, const int* device_ids, moe_eamc** out);
 moe_status sh_layout(const moe_eamc* h, int* n_shards, int* use_nccl);
 moe_status sh_clone(const moe_eamc* h, moe_eamc** out);
-moe_status sh_save(const moe_eamc* h, const char* path);
+moe_status sh_save(const moe_eamc* h, const char* path, bool binary);
 moe_status sh_destroy(moe_eamc* h);
 moe_status sh_info(const moe_eamc* h, uint64_t* size, int* count_bytes);
 moe_status sh_entry(moe_eamc* h, uint64_t index, uint64_t* counts, uint64_t* seq);

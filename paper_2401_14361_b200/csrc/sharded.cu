@@ -574,7 +574,7 @@ moe_status sh_clone(const moe_eamc* h, moe_eamc** out) {
   return MOE_OK;
 }
 
-moe_status sh_save(const moe_eamc* h, const char* path) {
+moe_status sh_save(const moe_eamc* h, const char* path, bool binary) {
   // the snapshot of the equivalent single collection: entries in global slot
   // order with their seqs and next_seq (JSON v1, eam.cpp:184-205)
   const Shards& S = *h->sh;
@@ -595,7 +595,7 @@ moe_status sh_save(const moe_eamc* h, const char* path) {
   }
   if (st == MOE_OK) {
     one->next_seq = h->next_seq;
-    st = moe_eamc_save(one, path);
+    st = binary ? moe_eamc_save_binary(one, path) : moe_eamc_save(one, path);
   }
   moe_eamc_destroy(one);
   return st;

@@ -343,6 +343,10 @@ class Eamc:
     def save(self, path: str) -> None:
         check(lib.moe_eamc_save(self._h, str(path).encode()))
 
+    def save_binary(self, path: str) -> None:
+        """The binary snapshot fast path (load() reads either format)."""
+        check(lib.moe_eamc_save_binary(self._h, str(path).encode()))
+
     @staticmethod
     def load(path: str, expected: Optional[ModelShape] = None, device: int = 0) -> "Eamc":
         h = C.c_void_p()
