@@ -131,6 +131,23 @@ moe_status moe_eamc_insert(moe_eamc* h, const uint64_t* counts, moe_eam_kind kin
  * moesim_main.cpp:212-216).  evicted_slots[n] (nullable). */
 moe_status moe_eamc_build(moe_eamc* h, const uint64_t* counts, uint64_t n,
                           int64_t* evicted_slots);
+/* Clustering construction (north-star item 3; OPT-IN and PARITY-UNPINNED:
+ * the reference defers clustering).  Picks
+ * capacity representatives from the n request EAMs: iteration 0 is exactly
+ * moe_eamc_build (n ordered Eamc::insert calls); each further iteration
+ * assigns every EAM to its nearest representative (the exact matcher),
+ * proposes per cluster the member closest to the u64 sum of the cluster's
+ * counts, and replaces the representative when the cluster's total exact
+ * distance to the proposal is strictly lower -- so representatives stay
+ * real request EAMs and the objective sum_i min_p d(eam_i, rep_p) never
+ * increases.  Stops after `iterations` or when nothing changes.  The
+ * collection must start empty.  objective[iterations+1] (nullable): the
+ * objective after each iteration (index 0 = the reference construction);
+ * rep_index[capacity] (nullable): the input index of every slot's EAM, which
+ * is also its seq; *iterations_run (nullable): refinement iterations done. */
+moe_status moe_eamc_build_clustered(moe_eamc* h, const uint64_t* counts, uint64_t n,
+                                    uint32_t iterations, double* objective, uint64_t* rep_index,
+                                    uint32_t* iterations_run);
 /* Bulk append with caller-given seqs (Eamc::load semantics, eam.cpp:229-244);
  * used for snapshots and for P-sharded collections where the global
  * insertion number of every entry is assigned by the caller.  Entries are

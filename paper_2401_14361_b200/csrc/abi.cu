@@ -1006,6 +1006,100 @@ static moe_status append_impl(moe_eamc* h, const void* counts, int cbytes, const
   return MOE_OK;
 }
 
+// Clustering construction (cluster.cu has the kernels and the method).
+moe_status moe_eamc_build_clustered(moe_eamc* h, const uint64_t* counts, uint64_t n,
+                                    uint32_t iterations, double* objective, uint64_t* rep_index,
+                                    uint32_t* iterations_run) {
+  HandleLock hl_(h);
+  if (!h || (!counts && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->sh) return fail(MOE_ERR_INVALID_ARGUMENT, "clustering builds a single-device collection");
+  if (h->c.size != 0)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "build_clustered: the collection must start empty");
+  if (iterations_run) *iterations_run = 0;
+  if (n == 0) return MOE_OK;
+  DeviceGuard dg(h->device);
+  // iteration 0: the reference construction (n ordered Eamc::insert calls)
+  std::vector<int64_t> ev(n);
+  CKS(moe_eamc_build(h, counts, n, ev.data()));
+  DevColl& c = h->c;
+  const uint64_t P = c.size, cells = (uint64_t)c.L * c.E;
+  std::vector<uint64_t> rep(P);  // input index of each slot's trace (= its seq here)
+  {
+    uint64_t appended = 0;
+    for (uint64_t k = 0; k < n; ++k) rep[ev[k] < 0 ? appended++ : (uint64_t)ev[k]] = k;
+  }
+  // every trace once on the device: narrow rows for the matcher, staged rows
+  // (packed, norms) for the exact distances and the replacements
+  DevBuf tr;
+  Staged S;
+  {
+    int sb = 8;
+    CKS(upload_host_counts(h, counts, n, &sb));
+    CK(tr.ensure(n * cells * sb + 16));
+    CK(cudaMemcpyAsync(tr.p, h->raw.p, n * cells * sb, cudaMemcpyDeviceToDevice, h->st));
+    CKS(stage_entries(h, tr.p, sb, n, &S));
+    if (sb != c.cb) {  // the staging widened the collection: matcher probes at its width
+      std::vector<uint8_t> hp(n * cells * c.cb);
+      moe::host::pack_counts(counts, n * cells, c.cb, hp.data());
+      CK(tr.ensure(hp.size() + 16));
+      CK(cudaMemcpy(tr.p, hp.data(), hp.size(), cudaMemcpyHostToDevice));
+    }
+  }
+  DevBuf dm, cent, dc, cmin, cidx, tcur, tcand, vic;
+  CK(dm.ensure(n * sizeof(moe_match)));
+  CK(cent.ensure(P * cells * 8));
+  CK(dc.ensure(n * 8));
+  CK(cmin.ensure(P * 8));
+  CK(cidx.ensure(P * 8));
+  CK(tcur.ensure(P * 8));
+  CK(tcand.ensure(P * 8));
+  CK(vic.ensure(P * sizeof(moe_match)));
+  std::vector<moe_match> hm(n);
+  std::vector<uint64_t> hidx(P), hcur(P), hcand(P);
+  uint32_t t = 0;
+  for (;; ++t) {
+    CKS(moe_eamc_match_device(h, tr.p, c.cb, n, dm.as<moe_match>(), h->st));
+    CK(cudaMemcpyAsync(hm.data(), dm.p, n * sizeof(moe_match), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    double obj = 0.0;
+    for (uint64_t i = 0; i < n; ++i) obj += hm[i].distance;  // input order: deterministic
+    if (objective) objective[t] = obj;
+    if (t == iterations) break;
+    CK(moe::launch_cluster_step(S.pr.packed, S.pr.sqa, n, c.L, c.E, c.RB, c.cb, dm.as<moe_match>(),
+                                c.index_base, P, cent.as<unsigned long long>(), dc.as<double>(),
+                                cmin.as<unsigned long long>(), cidx.as<unsigned long long>(),
+                                tcur.as<unsigned long long>(), tcand.as<unsigned long long>(),
+                                h->st));
+    CK(cudaMemcpyAsync(hidx.data(), cidx.p, P * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(hcur.data(), tcur.p, P * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(hcand.data(), tcand.p, P * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    std::vector<moe_match> acc;
+    std::vector<uint64_t> acc_i;
+    for (uint64_t p = 0; p < P; ++p)
+      if (hidx[p] != ~0ull && hidx[p] != rep[p] && hcand[p] < hcur[p]) {
+        acc.push_back(moe_match{c.index_base + p, 0, 0.0});
+        acc_i.push_back(hidx[p]);
+        rep[p] = hidx[p];
+      }
+    if (acc.empty()) {  // converged: later iterations would repeat this one
+      for (uint32_t u = t + 1; objective && u <= iterations; ++u) objective[u] = obj;
+      break;
+    }
+    ++h->version;
+    CK(cudaMemcpyAsync(vic.p, acc.data(), acc.size() * sizeof(moe_match), cudaMemcpyHostToDevice,
+                       h->st));
+    for (size_t k = 0; k < acc.size(); ++k)  // seq = the trace's input index (unique)
+      CK(moe::launch_replace(c, S.pr, (uint32_t)acc_i[k], vic.as<moe_match>() + k, acc_i[k],
+                             nullptr, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  }
+  h->next_seq = std::max<uint64_t>(h->next_seq, n);
+  if (rep_index) std::copy(rep.begin(), rep.end(), rep_index);
+  if (iterations_run) *iterations_run = t;
+  return MOE_OK;
+}
+
 moe_status moe_eamc_append(moe_eamc* h, const uint64_t* counts, const uint64_t* seqs, uint64_t n) {
   HandleLock hl_(h);
   if (!h || ((!counts || !seqs) && n)) return fail(MOE_ERR_INVALID_ARGUMENT, "null argument");

@@ -311,28 +311,6 @@ __global__ void __launch_bounds__(kNT, 1)
   if (MODE == 1 && cur_qi >= 0) flush_best((uint32_t)cur_qi);
 }
 
-// Exact distance of packed probe row-set `pa` vs entry `pb`, warp-cooperative
-// (lane = layer), reference operation order (eam.cpp:95-103).
-template <int CB>
-__device__ double warp_exact_distance(const uint8_t* pa, const double* sqa, const uint8_t* pb,
-                                      const double* sqb, uint32_t L, uint32_t C, uint32_t RB) {
-  const uint32_t lane = threadIdx.x & 31;
-  double sim = 0.0;
-  for (uint32_t l0 = 0; l0 < L; l0 += 32) {
-    const uint32_t l = l0 + lane;
-    double r = 0.0;
-    if (l < L) {
-      typename Dot<CB>::Acc acc = 0;
-      const uint4* ra = reinterpret_cast<const uint4*>(pa + (uint64_t)l * RB);
-      const uint4* rb = reinterpret_cast<const uint4*>(pb + (uint64_t)l * RB);
-      for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(ra[c], rb[c], acc);
-      r = row_sim_exact((uint64_t)acc, sqa[l], sqb[l]);
-    }
-    const uint32_t n = min(32u, L - l0);
-    for (uint32_t i = 0; i < n; ++i) sim = __dadd_rn(sim, __shfl_sync(0xffffffffu, r, i));
-  }
-  return finish_distance(sim, L);
-}
 
 struct RefineArgs {
   const uint8_t* counts;

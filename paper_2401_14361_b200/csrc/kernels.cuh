@@ -239,6 +239,16 @@ cudaError_t launch_trace(const void* topk, int idx_bytes, uint64_t T, uint32_t L
                          uint32_t k, const uint64_t* offsets, uint64_t R, void* counts,
                          int count_bytes, int* bad, int n_sm, cudaStream_t st);
 
+// Clustering construction (cluster.cu): one refinement step's device work --
+// centroids of the assignment m, per-cluster proposals cidx (trace index),
+// fixed-point totals of the current and proposed representatives' distances.
+cudaError_t launch_cluster_step(const uint8_t* packed, const double* sq, uint64_t n, uint32_t L,
+                                uint32_t E, uint32_t RB, int cb, const moe_match* m,
+                                uint64_t base, uint64_t P, unsigned long long* cent, double* dc,
+                                unsigned long long* cmin, unsigned long long* cidx,
+                                unsigned long long* tot_cur, unsigned long long* tot_cand,
+                                cudaStream_t st);
+
 cudaError_t launch_widen(const uint8_t* src, uint8_t* dst, uint64_t rows, uint32_t RB_old,
                          uint32_t RB_new, int cb_old, int cb_new, cudaStream_t st);
 

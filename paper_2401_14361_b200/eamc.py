@@ -283,6 +283,19 @@ class Eamc:
         check(lib.moe_eamc_build(self._h, ptr(counts), n, ptr(slots)))
         return slots[:n]
 
+    def build_clustered(self, counts: np.ndarray, iterations: int = 5):
+        """Clustering construction (opt-in, parity-unpinned; moe_eamc_build_clustered):
+        iteration 0 = build(counts), then k-medoids-style refinement.  Returns
+        (objective per iteration, input index of every slot's EAM, iterations run)."""
+        counts = np.ascontiguousarray(counts, np.uint64)
+        n = counts.shape[0]
+        obj = np.zeros(iterations + 1, np.float64)
+        rep = np.zeros(max(self.capacity(), 1), np.uint64)
+        it = C.c_uint32()
+        check(lib.moe_eamc_build_clustered(self._h, ptr(counts), n, iterations, ptr(obj), ptr(rep),
+                                           C.byref(it)))
+        return obj, rep[:self.size()], it.value
+
     def build_from_traces(self, trace_path: str) -> int:
         """`moesim eamc save` minus the write (moesim_main.cpp:203-221): the request
         EAMs of this collection's phase, from a JSONL trace file, inserted in file
