@@ -288,7 +288,11 @@ moe_status moe_select_eviction_victim(const moe_shape* shape, const uint64_t* re
 moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_bytes,
                          uint64_t n_tokens, const uint64_t* offsets, uint64_t n_requests,
                          uint64_t* counts);
-/* Device variant: all pointers device; counts_u32 [R][L][E] accumulated. */
+/* Device variant: all pointers device, stream-ordered on `stream`; counts_u32
+ * [R][L][E] accumulated.  *bad_index_flag must be 0 on entry; an index >= E
+ * leaves it 1 and counts_u32 as it was (the call's additions are rolled back
+ * on the device).  Calls on different streams share no scratch memory.
+ * Request offsets must lie within [0, n_tokens]. */
 moe_status moe_eam_trace_device(const moe_shape* shape, const void* topk_idx, int idx_bytes,
                                 uint64_t n_tokens, const uint64_t* offsets, uint64_t n_requests,
                                 uint32_t* counts_u32, int* bad_index_flag, void* stream);
