@@ -223,6 +223,15 @@ moe_status moe_eamc_load_sharded(const char* path, const moe_shape* expected, in
 /* n_shards (1 for a single-device handle) and whether NCCL carries its collectives. */
 moe_status moe_eamc_shard_layout(const moe_eamc* h, int* n_shards, int* uses_nccl);
 
+/* Persistent decision server (0 = off, the default: one kernel launch per
+ * decision).  With n_ctas > 0 (capped at half the SMs), prefetch_priorities
+ * on this handle is served by a decision kernel resident on n_ctas SMs and
+ * fed through a pinned-memory mailbox: no launch and no stream
+ * synchronisation per call.  It exits after 50 ms without requests and is
+ * relaunched on the next one.  While enabled, other decision launches in the
+ * process size their grids to the remaining SMs. */
+moe_status moe_eamc_set_decision_server(moe_eamc* h, int n_ctas);
+
 /* Instrumentation: when enabled, matching records CUDA events around its
  * kernels on the launching stream; ms[0..2] = accumulated device time of
  * probe packing, the screen pass and the refine pass, calls[0..2] their

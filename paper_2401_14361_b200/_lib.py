@@ -83,6 +83,7 @@ _sig("moe_eamc_create_sharded", C.c_int, P(moe_shape), C.c_int, u64, C.c_int, C.
      P(C.c_int), P(vp))
 _sig("moe_eamc_shard_layout", C.c_int, vp, P(C.c_int), P(C.c_int))
 _sig("moe_eamc_save_binary", C.c_int, vp, C.c_char_p)
+_sig("moe_eamc_set_decision_server", C.c_int, vp, C.c_int)
 _sig("moe_eamc_build_clustered", C.c_int, vp, vp, u64, C.c_uint32, vp, vp, P(C.c_uint32))
 _sig("moe_eamc_load_sharded", C.c_int, C.c_char_p, P(moe_shape), C.c_int, P(C.c_int), P(vp))
 _sig("moe_eamc_info", C.c_int, vp, P(moe_shape), P(C.c_int), P(u64), P(u64), P(u64),
@@ -123,7 +124,7 @@ _sig("moe_gen_bench_family", C.c_int, u64, C.c_uint32, C.c_uint32, u64, u64, C.c
 EXPORTS = [
     "moe_abi_version", "moe_host_threads", "moe_last_error", "moe_device_info", "moe_device_warmup", "moe_eamc_create",
     "moe_eamc_create_sharded", "moe_eamc_shard_layout", "moe_eamc_load_sharded",
-    "moe_eamc_save_binary", "moe_eamc_build_clustered",
+    "moe_eamc_save_binary", "moe_eamc_build_clustered", "moe_eamc_set_decision_server",
     "moe_eamc_destroy", "moe_eamc_info", "moe_eamc_clone", "moe_eamc_entry", "moe_eamc_insert", "moe_eamc_build",
     "moe_eamc_append", "moe_eamc_append_packed", "moe_eamc_match", "moe_eamc_match_device",
     "moe_eamc_match_packed",

@@ -754,7 +754,12 @@ moe_status window_list(moe_eamc* h, uint64_t dmin_bits, double window,
 
 }  // namespace moe::abi
 
+// SMs held by resident decision servers per device (see server_run).
+static std::atomic<int> g_srv_sms[64];
+
 extern "C" {
+
+static moe_status server_stop(moe_eamc* h);
 
 int moe_abi_version(void) { return MOE_EAMC_ABI_VERSION; }
 
@@ -870,6 +875,7 @@ moe_status moe_eamc_destroy(moe_eamc* h) {
   if (h->sh) return moe::abi::sh_destroy(h);
   DeviceGuard dg(h->device);
   cudaStreamSynchronize(h->st);
+  if (h->srv.G) g_srv_sms[h->device & 63] -= h->srv.G;
   delete h;
   return MOE_OK;
 }
@@ -1504,6 +1510,20 @@ moe_status moe_eamc_set_index_base(moe_eamc* h, uint64_t base) {
   return MOE_OK;
 }
 
+moe_status moe_eamc_set_decision_server(moe_eamc* h, int n_ctas) {
+  HandleLock hl_(h);
+  if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
+  if (h->sh) return fail(MOE_ERR_INVALID_ARGUMENT, "the decision server is per shard handle");
+  if (n_ctas < 0) return fail(MOE_ERR_INVALID_ARGUMENT, "n_ctas must be >= 0");
+  DeviceGuard dg(h->device);
+  const int want = std::min(n_ctas, h->n_sm / 2);
+  if (want == h->srv.G) return MOE_OK;
+  CKS(server_stop(h));
+  g_srv_sms[h->device & 63] += want - h->srv.G;
+  h->srv.G = want;
+  return MOE_OK;
+}
+
 moe_status moe_eamc_set_profiling(moe_eamc* h, int enable) {
   HandleLock hl_(h);
   if (!h) return fail(MOE_ERR_INVALID_ARGUMENT, "null handle");
@@ -1641,6 +1661,92 @@ static moe_status dec_scratch(moe_eamc* h, uint64_t n_slots) {
   return MOE_OK;
 }
 
+// ---- persistent decision server --------------------------------------------
+// SMs held by resident decision servers per device: other software-grid-
+// barrier launches (k_decision) must stay co-resident, so they size their grid
+// to the SMs that remain.
+static int decision_sms(const moe_eamc* h) {
+  return std::max(8, h->n_sm - g_srv_sms[h->device & 63].load());
+}
+
+static bool server_takes(const moe_eamc* h, uint64_t n_slots) {
+  return h->srv.G > 0 && n_slots == 0 && !dec_timing();
+}
+
+static moe_status server_stop(moe_eamc* h) {
+  auto& v = h->srv;
+  if (!v.st) return MOE_OK;
+  reinterpret_cast<volatile int*>(&v.ctl.as<moe::DecServerCtl>()->stop)[0] = 1;
+  CK(cudaStreamSynchronize(v.st));
+  reinterpret_cast<volatile int*>(&v.ctl.as<moe::DecServerCtl>()->stop)[0] = 0;
+  v.launched = false;
+  return MOE_OK;
+}
+
+static moe_status server_launch(moe_eamc* h) {
+  auto& v = h->srv;
+  const DevColl& c = h->c;
+  uint32_t np = 1;
+  while (np < c.E) np <<= 1;
+  v.smem = std::max<size_t>((size_t)c.L * c.RB, (size_t)np * 28);
+  CK(v.drows.ensure((size_t)c.L * c.RB + 2 * c.L + 32));
+  v.cb = c.cb;
+  auto* ctl = v.ctl.as<moe::DecServerCtl>();
+  // seq0 = the last request completed: a pending request (seq_req > seq0) is served
+  CK(moe::launch_decision_server(ctl, v.dargs.as<moe::DecisionArgs>(), v.drows.as<uint8_t>(),
+                                 v.state.as<uint32_t>(), v.state.as<uint32_t>() + 1,
+                                 v.state.as<uint32_t>() + 2,
+                                 reinterpret_cast<volatile uint64_t*>(&ctl->seq_done)[0], v.k,
+                                 50'000'000ull, ++v.gen, c.cb, v.G, v.smem, v.st));
+  v.launched = true;
+  return MOE_OK;
+}
+
+// One request through the server: post the arguments in the pinned mailbox,
+// wait for seq_done (relaunching an idled-out server).
+static moe_status server_run(moe_eamc* h, const moe::DecisionArgs& a) {
+  auto& v = h->srv;
+  if (!v.st) {
+    CK(cudaStreamCreateWithFlags(&v.st, cudaStreamNonBlocking));
+    CK(v.ctl.ensure(sizeof(moe::DecServerCtl)));
+    std::memset(v.ctl.p, 0, sizeof(moe::DecServerCtl));
+    CK(v.dargs.ensure(sizeof(moe::DecisionArgs)));
+    CK(v.state.ensure(64));
+    CK(cudaMemset(v.state.p, 0, 64));
+    v.seq = 0;
+    v.k = 0;
+  }
+  if (v.launched && v.cb != h->c.cb) CKS(server_stop(h));  // widened: relaunch at the new width
+  auto* ctl = v.ctl.as<moe::DecServerCtl>();
+  std::memcpy(&ctl->args, &a, sizeof a);
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  const uint64_t seq = ++v.seq;
+  reinterpret_cast<volatile uint64_t*>(&ctl->seq_req)[0] = seq;
+  if (!v.launched) CKS(server_launch(h));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t spin = 1;; ++spin) {
+    if (reinterpret_cast<volatile uint64_t*>(&ctl->seq_done)[0] == seq) break;
+    if ((spin & 1023) == 0) {
+      const cudaError_t q = cudaStreamQuery(v.st);
+      if (q == cudaSuccess) {  // the server idled out before seeing the request
+        if (reinterpret_cast<volatile uint64_t*>(&ctl->seq_done)[0] == seq) break;
+        v.launched = false;
+        CKS(server_launch(h));
+      } else if (q != cudaErrorNotReady) {
+        CK(q);
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10)) {
+        reinterpret_cast<volatile int*>(&ctl->stop)[0] = 1;
+        return fail(MOE_ERR_CUDA, "decision server: request %llu not served within 10 s",
+                    (unsigned long long)seq);
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  ++v.k;
+  return MOE_OK;
+}
+
 // Common launch + result copy of a DecisionArgs set up by the callers below.
 static moe_status run_decision(moe_eamc* h, moe::DecisionArgs& a, size_t stage_rows,
                                const uint64_t* request_eam, const moe_slot_view* slots,
@@ -1684,7 +1790,15 @@ static moe_status run_decision(moe_eamc* h, moe::DecisionArgs& a, size_t stage_r
   if (c.L - a.cur > moe::kDecMaxLayers || c.E > moe::kDecMaxExperts)
     return fail(MOE_ERR_INVALID_ARGUMENT, "decision: shape %ux%u exceeds the order phases' limits",
                 c.L, c.E);
-  const int grid = moe::decision_grid(h->n_sm, c.size, c.L, a.cur);
+  if (server_takes(h, n_slots)) {
+    CKS(server_run(h, a));
+    const uint32_t n = *reinterpret_cast<volatile uint32_t*>(a.n_out);
+    if (n_out) *n_out = n;
+    if (n && out && cap) std::memcpy(out, a.out, std::min<uint64_t>(n, cap) * sizeof(moe_candidate));
+    if (victim) *victim = -1;
+    return MOE_OK;
+  }
+  const int grid = moe::decision_grid(decision_sms(h), c.size, c.L, a.cur);
   const size_t smem = std::max(stage_rows, moe::decision_smem(c.L, c.E, c.RB, 0, a.cur, grid));
   if (smem > 220 * 1024)
     return fail(MOE_ERR_INVALID_ARGUMENT, "decision: shape %ux%u needs %zu B of shared memory",
@@ -1820,9 +1934,14 @@ static moe_status decide_fused(moe_eamc* h, const uint64_t* probe, uint32_t cur,
     for (uint32_t i = 0; i < n_nz; ++i)
       std::memcpy(h->xpin.as<uint8_t>() + (size_t)i * RB, hb + (size_t)nz[i] * RB, RB);
     std::memcpy(h->xpin.as<uint8_t>() + rows_b, nz.data(), (size_t)n_nz * 2);
-    CK(cudaMemcpyAsync(h->xdev.p, h->xpin.p, rows_b + nz_b, cudaMemcpyHostToDevice, h->st));
-    a.rows = h->xdev.as<uint8_t>();
-    a.nz = reinterpret_cast<const uint16_t*>(h->xdev.as<uint8_t>() + rows_b);
+    if (server_takes(h, n_slots)) {  // the server copies them from pinned memory itself
+      a.rows = h->xpin.as<uint8_t>();
+      a.nz = reinterpret_cast<const uint16_t*>(h->xpin.as<uint8_t>() + rows_b);
+    } else {
+      CK(cudaMemcpyAsync(h->xdev.p, h->xpin.p, rows_b + nz_b, cudaMemcpyHostToDevice, h->st));
+      a.rows = h->xdev.as<uint8_t>();
+      a.nz = reinterpret_cast<const uint16_t*>(h->xdev.as<uint8_t>() + rows_b);
+    }
   }
   CKS(run_decision(h, a, (size_t)n_nz * RB, request_eam, slots, n_slots, out, cap, n_out, victim));
   if (store) {
@@ -2026,7 +2145,7 @@ moe_status moe_eamc_prefetch_order_device(const moe_eamc* hc, const uint64_t* ag
   if (L - current_layer > moe::kDecMaxLayers || E > moe::kDecMaxExperts)
     return fail(MOE_ERR_INVALID_ARGUMENT, "decision: shape %ux%u exceeds the order phases' limits",
                 L, E);
-  const int grid = moe::decision_grid(h->n_sm, 0, L, current_layer);
+  const int grid = moe::decision_grid(decision_sms(h), 0, L, current_layer);
   const size_t smem = moe::decision_smem(L, E, h->c.RB, 0, current_layer, grid);
   if (smem > 220 * 1024)
     return fail(MOE_ERR_INVALID_ARGUMENT, "decision: shape %ux%u needs %zu B of shared memory", L,

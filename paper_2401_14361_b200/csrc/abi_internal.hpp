@@ -197,12 +197,30 @@ struct moe_eamc {
   uint64_t dec_version = ~0ull;
   int dec_cb = 0;
   moe_status last_status = MOE_OK;
+  // persistent decision server (moe_eamc_set_decision_server; decide.cu)
+  struct DecServer {
+    int G = 0;             // CTAs (0 = off: a launch per decision)
+    int cb = 0;            // storage width it was launched for
+    bool launched = false;
+    cudaStream_t st = nullptr;
+    moe::abi::PinBuf ctl;  // moe::DecServerCtl, device-mapped
+    moe::abi::DevBuf dargs, drows, state;  // state: go, done, barrier counter
+    uint64_t seq = 0;      // last request posted
+    uint32_t k = 0;        // requests completed
+    uint32_t gen = 0;      // server launches (tags each launch's exit word)
+    size_t smem = 0;
+  } srv;
   // P-sharded facade (sharded.cu): when set, this handle owns no collection
   // itself and every entry point forwards to the shards
   moe::abi::Shards* sh = nullptr;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
 
   ~moe_eamc() {
+    if (srv.st) {  // ask a resident decision server to exit, then wait for it
+      if (srv.ctl.p) reinterpret_cast<volatile int*>(&srv.ctl.as<moe::DecServerCtl>()->stop)[0] = 1;
+      cudaStreamSynchronize(srv.st);
+      cudaStreamDestroy(srv.st);
+    }
     if (c.counts) cudaFree(c.counts);
     if (c.ibT) cudaFree(c.ibT);
     if (c.sqb) cudaFree(c.sqb);

@@ -94,8 +94,16 @@ __device__ __forceinline__ void stamp(const DecisionArgs& a, int i) {
   }
 }
 
-template <int CB>
-__global__ void __launch_bounds__(kDecThreads, 1) k_decision(const __grid_constant__ DecisionArgs a) {
+// Read-only collection loads: the non-coherent path in a launch; L2 (ld.cg)
+// in the persistent server, whose lifetime spans collection updates.
+template <bool PS, typename T>
+__device__ __forceinline__ T ld_ro(const T* p) {
+  if constexpr (PS) return __ldcg(p);
+  else return __ldg(p);
+}
+
+template <int CB, bool PS>
+__device__ __forceinline__ void decision_body(const DecisionArgs& a) {
   using Acc = typename Dot<CB>::Acc;
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ uint16_t nz_s[kDecMaxNz];
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decision(const __grid_consta
         Acc acc = 0;
         const uint4* pr = prow_s + (size_t)k * C;
         const uint4* er = eb + (size_t)l * C;
-        for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(pr[c], __ldg(er + c), acc);
+        for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(pr[c], ld_ro<PS>(er + c), acc);
         r = row_sim_exact((uint64_t)acc, sqa_s[k], sb[l]);
         ++k;
       } else {
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decision(const __grid_consta
         const uint32_t mi = it / per_mem, rem = it - mi * per_mem;
         const uint32_t r = rem / wpr, w = rem - r * wpr;
         const uint32_t l = a.cur + 1 + r;
-        const uint32_t word = __ldg(reinterpret_cast<const uint32_t*>(
+        const uint32_t word = ld_ro<PS>(reinterpret_cast<const uint32_t*>(
             a.counts + (uint64_t)mem_s[mi] * LR + (uint64_t)l * RB + 4ull * w));
         if (!word) continue;
 #pragma unroll
@@ -515,6 +523,124 @@ __global__ void __launch_bounds__(kDecThreads, 1) k_decision(const __grid_consta
   }
 }
 
+template <int CB>
+__global__ void __launch_bounds__(kDecThreads, 1) k_decision(const __grid_constant__ DecisionArgs a) {
+  decision_body<CB, false>(a);
+}
+
+// Persistent decision server (moe_eamc_set_decision_server): the same phases,
+// resident on `gridDim.x` SMs, fed through a pinned-memory mailbox instead of
+// a launch per decision.  CTA 0's thread 0 polls the host mailbox; on a new
+// request CTA 0 copies the arguments (and the probe's explicit rows, when they
+// do not ride inline) from pinned host memory to the device, then releases the
+// request to the other CTAs through a device word (every CTA follows CTA 0's
+// decision, so all of them run a request or all exit).  After the phases each
+// CTA makes its writes visible system-wide and counts itself done; the last one
+// publishes seq_done to the host.  Idle for idle_ns (or asked to stop), the
+// server exits; the host relaunches it on the next request.
+template <int CB>
+__global__ void __launch_bounds__(kDecThreads, 1)
+    k_decision_server(DecServerCtl* ctl, DecisionArgs* dargs, uint8_t* drows, uint32_t* go,
+                      uint32_t* done, uint32_t* bar, uint64_t seq0, uint32_t k0, uint64_t idle_ns,
+                      uint32_t gen) {
+  __shared__ DecisionArgs sa;
+  __shared__ uint64_t sh_seq;
+  const uint32_t tid = threadIdx.x, b = blockIdx.x, G = gridDim.x;
+  // exit word of THIS launch (an earlier server's exit word carries its own
+  // generation, so a relaunch does not see it as its own)
+  const uint32_t kExit = 0x80000000u | (gen & 0x7fffffffu);
+  uint64_t last = seq0;
+  uint32_t k = k0;  // requests served by earlier servers on this state
+  for (;;) {
+    if (b == 0) {
+      if (tid == 0) {
+        uint64_t t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        uint64_t sq = 0;
+        for (;;) {
+          asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(sq) : "l"(&ctl->seq_req));
+          if (sq != last) break;
+          int stop;
+          asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(stop) : "l"(&ctl->stop));
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          if (stop || t - t0 > idle_ns) {
+            sq = ~0ull;
+            break;
+          }
+          __nanosleep(100);
+        }
+        sh_seq = sq;
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+      }
+      __syncthreads();
+      if (sh_seq != ~0ull) {
+        // arguments and explicit probe rows: pinned host memory -> device
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(&ctl->args);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(dargs);
+        for (uint32_t i = tid; i < sizeof(DecisionArgs) / 4; i += kDecThreads)
+          dst[i] = *reinterpret_cast<const volatile uint32_t*>(src + i);
+        __syncthreads();
+        if (!dargs->rows_inline && dargs->n_nz) {
+          const uint32_t rows_b = dargs->n_nz * dargs->RB;
+          const uint32_t nz_b = (dargs->n_nz * 2 + 15) & ~15u;
+          const uint4* rs = reinterpret_cast<const uint4*>(dargs->rows);
+          for (uint32_t i = tid; i < (rows_b + nz_b) / 16; i += kDecThreads)
+            reinterpret_cast<uint4*>(drows)[i] = rs[i];  // rows then the row list (host layout)
+          __syncthreads();
+          if (tid == 0) {
+            dargs->rows = drows;
+            dargs->nz = reinterpret_cast<const uint16_t*>(drows + rows_b);
+          }
+        }
+        if (tid == 0) {
+          dargs->bar = bar;
+          dargs->bar_base = k * kDecBarriers * G;
+          dargs->out = ctl->args.out;
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(go), "r"(k + 1) : "memory");
+      } else if (tid == 0) {
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(go), "r"(kExit) : "memory");
+      }
+    }
+    // every CTA (CTA 0 included): wait for the release, acquire (fresh L1)
+    __shared__ uint32_t sh_go;
+    if (tid == 0) {
+      uint32_t v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(go) : "memory");
+        if (v == k + 1 || v == kExit) break;
+        __nanosleep(64);
+      }
+      sh_go = v;
+    }
+    __syncthreads();
+    if (sh_go == kExit) return;
+    {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(dargs);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(&sa);
+      for (uint32_t i = tid; i < sizeof(DecisionArgs) / 4; i += kDecThreads) dst[i] = __ldcg(src + i);
+    }
+    __syncthreads();
+    decision_body<CB, true>(sa);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      const uint32_t old = atomicAdd(done, 1u);
+      if (old + 1 == (k + 1) * G) {  // the last CTA of this request
+        __threadfence_system();
+        uint64_t sq;
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(sq) : "l"(&ctl->seq_req));
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&ctl->seq_done), "l"(sq) : "memory");
+      }
+    }
+    ++k;
+    if (b == 0) last = sh_seq;
+    __syncthreads();  // sh_seq is rewritten by the next poll
+  }
+}
+
 }  // namespace
 
 size_t decision_smem(uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz, uint32_t cur,
@@ -532,6 +658,26 @@ int decision_grid(int n_sm, uint32_t size, uint32_t L, uint32_t cur) {
   const uint32_t rows = cur + 1 < L ? L - cur - 1 : 0;
   uint32_t g = std::max<uint32_t>({(size + 63) / 64, rows, 8u});
   return (int)std::min<uint32_t>(g, (uint32_t)n_sm);
+}
+
+cudaError_t launch_decision_server(DecServerCtl* ctl, DecisionArgs* dargs, uint8_t* drows,
+                                   uint32_t* go, uint32_t* done, uint32_t* bar, uint64_t seq0,
+                                   uint32_t k0, uint64_t idle_ns, uint32_t gen, int cb, int grid,
+                                   size_t smem, cudaStream_t st) {
+  void (*kern)(DecServerCtl*, DecisionArgs*, uint8_t*, uint32_t*, uint32_t*, uint32_t*, uint64_t,
+               uint32_t, uint64_t, uint32_t) =
+      cb == 1 ? k_decision_server<1> : cb == 2 ? k_decision_server<2> : k_decision_server<4>;
+  static size_t set[3] = {0, 0, 0};
+  const int slot = cb == 1 ? 0 : cb == 2 ? 1 : 2;
+  if (smem > set[slot]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set[slot] = smem;
+  }
+  kern<<<(unsigned)grid, kDecThreads, smem, st>>>(ctl, dargs, drows, go, done, bar, seq0, k0,
+                                                  idle_ns, gen);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_decision(const DecisionArgs& a, int cb, int grid, size_t smem,

@@ -207,6 +207,18 @@ int decision_grid(int n_sm, uint32_t size, uint32_t L, uint32_t cur);
 // One cooperative launch (grid <= co-resident CTAs; decision_grid picks it).
 cudaError_t launch_decision(const DecisionArgs& a, int cb, int grid, size_t smem,
                             cudaStream_t st);
+// The persistent decision server's mailbox (pinned host memory, device-mapped).
+struct DecServerCtl {
+  uint64_t seq_req;   // host: the request number being posted
+  uint64_t seq_done;  // device: the last request completed
+  int stop;           // host: ask the server to exit
+  int pad_;
+  DecisionArgs args;  // the request (host-side pointers for rows/nz when not inline)
+};
+cudaError_t launch_decision_server(DecServerCtl* ctl, DecisionArgs* dargs, uint8_t* drows,
+                                   uint32_t* go, uint32_t* done, uint32_t* bar, uint64_t seq0,
+                                   uint32_t k0, uint64_t idle_ns, uint32_t gen, int cb, int grid,
+                                   size_t smem, cudaStream_t st);
 
 cudaError_t launch_merge(const moe_match* parts, uint64_t n_parts, uint64_t n, moe_match* out,
                          cudaStream_t st);

@@ -19,8 +19,11 @@ L = int(os.environ.get("DS_L", "59"))
 E = int(os.environ.get("DS_E", "160"))
 P = int(os.environ.get("DS_P", "10000"))
 fam = m.gen_bench_family(55, L, E, P + 1, dtype=np.uint8)
+SRV = int(os.environ.get("DS_SERVER", "0"))
 e = m.Eamc(m.ModelShape(L, E, 2), m.Phase.decode, P)
 e.append(fam[:P], np.arange(P, dtype=np.uint64))
+if SRV:
+    _lib.check(_lib.lib.moe_eamc_set_decision_server(e._h, SRV))
 base = fam[P].astype(np.uint64)
 probes = []
 for l in range(L - 1):
@@ -42,5 +45,5 @@ for _ in range(reps):
         _lib.check(_lib.lib.moe_prefetch_priorities(e._h, probes[l].ctypes.data, l, 1,
                                                     out.ctypes.data, cap, C.byref(n)))
     ts.append(time.perf_counter() - t0)
-print(f"L={L} E={E} P={P}: C-ABI decode step {min(ts)*1e3:.3f} ms "
+print(f"server={SRV} L={L} E={E} P={P}: C-ABI decode step {min(ts)*1e3:.3f} ms "
       f"({min(ts)/(L-1)*1e6:.1f} us/call)", flush=True)
