@@ -23,6 +23,9 @@
 //               64 accumulator columns each): tcgen05.ld 32x32b.x32 (thread =
 //               probe row), screen distance, row min -> global per-probe
 //               threshold (atomicMin), candidate push into the per-probe bucket
+#ifndef TC_GROUP_M
+#define TC_GROUP_M 64
+#endif
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -111,6 +114,30 @@ __device__ __forceinline__ void tc_fence_before() {
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Output tile t -> (probe tile m, entry tile n), grouped: GM consecutive
+// probe tiles sweep all entry tiles together, so the clusters running side by
+// side share entry tiles (each read once from HBM per group) while the group's
+// probe tiles stay in L2.  With m fastest over all probe tiles (the previous
+// order) a large probe batch cycled more probe-tile bytes than L2 holds and
+// re-read them from HBM for every entry tile: 391 GB of DRAM reads per SC
+// batch launch for 1.7 GB of algorithmic bytes.  Small batches (n_m <= GM) keep
+// the plain order.
+constexpr uint32_t kTileGroupM = TC_GROUP_M;
+__device__ __forceinline__ void tile_mn(uint32_t t, uint32_t n_m, uint32_t n_n, uint32_t* m,
+                                        uint32_t* n) {
+  if (n_m <= kTileGroupM) {
+    *m = t % n_m;
+    *n = t / n_m;
+    return;
+  }
+  const uint32_t per = kTileGroupM * n_n;
+  const uint32_t g = t / per, first = g * kTileGroupM;
+  const uint32_t gsz = min(kTileGroupM, n_m - first);
+  const uint32_t r = t - g * per;
+  *m = first + r % gsz;
+  *n = r / gsz;
 }
 
 // K-major operand tile, 128-byte swizzle: 8-row atoms of 128 B, atoms 1024 B
@@ -316,7 +343,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       uint32_t s = 0, ph = 0;
       for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const uint32_t m = t % a.n_m, n = t / a.n_m;
+        uint32_t m, n;
+        tile_mn(t, a.n_m, a.n_n, &m, &n);
         for (uint32_t kb = 0; kb < a.n_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
@@ -366,7 +394,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t i = 0;
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
       const uint32_t acc = i & 1;
-      const uint32_t m = t % a.n_m, n = t / a.n_m;
+      uint32_t m, n;
+        tile_mn(t, a.n_m, a.n_n, &m, &n);
       uint64_t* zt = zp_s + acc * BN;
       {
         for (uint32_t j = et; j < BN; j += EPI_THREADS) {
@@ -502,7 +531,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       uint32_t s = 0, ph = 0;
       for (uint32_t t = cluster; t < n_tiles; t += n_clusters) {
-        const uint32_t m = t % a.n_m, n = t / a.n_m;
+        uint32_t m, n;
+        tile_mn(t, a.n_m, a.n_n, &m, &n);
         for (uint32_t kb = 0; kb < a.n_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE2);
@@ -554,7 +584,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint32_t i = 0;
     for (uint32_t t = cluster; t < n_tiles; t += n_clusters, ++i) {
       const uint32_t acc = i & 1;
-      const uint32_t m = t % a.n_m, n = t / a.n_m;
+      uint32_t m, n;
+        tile_mn(t, a.n_m, a.n_n, &m, &n);
       uint64_t* zt = zp_s + acc * BN;
       {
         for (uint32_t j = et; j < BN; j += EPI_THREADS) {
