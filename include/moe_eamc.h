@@ -289,6 +289,49 @@ moe_status moe_select_eviction_victim(const moe_shape* shape, const uint64_t* re
                                       const moe_slot_view* slots, uint64_t n_slots,
                                       int64_t* victim);
 
+/* ---- expert weights: the host consumer of the prefetch order ----
+ * A pool of n_slots GPU expert slots filled from host expert weights
+ * ([L][E][expert_bytes], page-locked here unless already) by chunked
+ * cudaMemcpyAsync, driven by the engine's rules for the reference's simulated
+ * transfers: TransferQueue (policy.cpp:43-86), one transfer in flight cut at
+ * chunk boundaries (memsim.cpp:73-84), slot acquisition -- free slot, else the
+ * select_eviction_victim victim priced by cache_priority of the request EAM,
+ * displaced by a speculative prefetch only when it outranks it -- and
+ * on-demand fetches at +inf priority that preempt speculative transfers and
+ * displace the least valuable protected prefetch when nothing else is free
+ * (engine.cpp:306-357, :429-529), execution resets protection
+ * (policy.cpp:161-167). */
+typedef struct moe_expert_cache moe_expert_cache;
+typedef struct moe_expert_cache_stats {
+  uint64_t transfers_started, transfers_completed, transfers_cancelled, preemptions, evictions;
+  uint64_t hits, misses, bytes_moved, queued, in_flight;
+} moe_expert_cache_stats;
+moe_status moe_expert_cache_create(const moe_shape* shape, uint64_t expert_bytes, uint32_t n_slots,
+                                   uint64_t chunk_bytes, const void* host_weights, int device,
+                                   moe_expert_cache** out);
+moe_status moe_expert_cache_destroy(moe_expert_cache* c);
+/* The request's cross-phase EAM [L][E] that prices cache_priority (engine.cpp:563). */
+moe_status moe_expert_cache_set_request_eam(moe_expert_cache* c, const uint64_t* request_eam);
+/* recompute_prefetch (engine.cpp:656-678): cancel_all, submit the order (e.g. the
+ * output of moe_prefetch_priorities with the floor filter), start transfers. */
+moe_status moe_expert_cache_submit(moe_expert_cache* c, const moe_candidate* order, uint64_t n);
+/* Retire finished chunks/transfers and start the next ones; wait_idle: until
+ * nothing is in flight and nothing startable remains. */
+moe_status moe_expert_cache_progress(moe_expert_cache* c, int wait_idle);
+/* execute_layer's fetch (engine.cpp:681-712): the expert's device weights,
+ * on demand when not resident (blocks until resident); marks it executing. */
+moe_status moe_expert_cache_acquire(moe_expert_cache* c, uint32_t layer, uint32_t expert,
+                                    void** device_ptr, int* was_resident);
+/* Execution done: not executing, protection cleared, repriced (policy.cpp:161-167). */
+moe_status moe_expert_cache_release(moe_expert_cache* c, uint32_t layer, uint32_t expert);
+/* Slot state: occupant (flat layer*E+expert, -1 empty), residency (0 empty,
+ * 1 transferring, 2 resident), protection, cache priority. */
+moe_status moe_expert_cache_slot(const moe_expert_cache* c, uint32_t slot, int64_t* expert_flat,
+                                 int* residency, int* prefetch_protected, double* priority);
+moe_status moe_expert_cache_stats_get(const moe_expert_cache* c, moe_expert_cache_stats* out);
+/* The bytes a slot holds (D2H; for verification). */
+moe_status moe_expert_cache_read_slot(const moe_expert_cache* c, uint32_t slot, void* host_dst);
+
 /* ---- tracing: Eam::record (eam.cpp:41-52) from router top-k ids ---- */
 /* topk_idx [n_tokens][L][top_k] with idx_bytes in {1,2,4}; request r owns
  * tokens [offsets[r], offsets[r+1]).  counts [R][L][E] u64 are ACCUMULATED

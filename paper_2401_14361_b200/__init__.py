@@ -6,14 +6,14 @@ reference's C++ API.  Importing it fails loudly if the library is missing.
 """
 from ._lib import (CountOverflowError, CudaError, EamcSnapshotError, gen_bench_family,  # noqa
                    LIB_PATH, TraceIngestError)
-from .eamc import (Eam, EamKind, Eamc, EamcMatch, ExpertId, ModelShape, Phase,  # noqa: F401
+from .eamc import (Eam, EamKind, Eamc, EamcMatch, ExpertCache, ExpertId, ModelShape, Phase,  # noqa
                    PrefetchCandidate, RoutingEvent, SlotView, TransferQueue, cache_priority,
                    decide, eam_distance, eamc_capacity_bound, eamc_save_from_traces,
                    ingest_request_eams, kEpsilon, kMatchWindow, kMaxPriority, prefetch_order,
                    prefetch_priorities, select_eviction_victim, trace_requests)
 
 __all__ = [
-    "Eam", "EamKind", "Eamc", "EamcMatch", "ExpertId", "ModelShape", "Phase",
+    "Eam", "EamKind", "Eamc", "EamcMatch", "ExpertCache", "ExpertId", "ModelShape", "Phase",
     "PrefetchCandidate", "RoutingEvent", "SlotView", "TransferQueue", "cache_priority", "decide",
     "eam_distance", "eamc_capacity_bound", "prefetch_order", "prefetch_priorities",
     "select_eviction_victim", "trace_requests", "gen_bench_family", "CudaError",

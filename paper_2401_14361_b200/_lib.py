@@ -84,6 +84,25 @@ _sig("moe_eamc_create_sharded", C.c_int, P(moe_shape), C.c_int, u64, C.c_int, C.
 _sig("moe_eamc_shard_layout", C.c_int, vp, P(C.c_int), P(C.c_int))
 _sig("moe_eamc_save_binary", C.c_int, vp, C.c_char_p)
 _sig("moe_eamc_set_decision_server", C.c_int, vp, C.c_int)
+
+
+class moe_expert_cache_stats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "transfers_started", "transfers_completed", "transfers_cancelled", "preemptions",
+        "evictions", "hits", "misses", "bytes_moved", "queued", "in_flight")]
+
+
+_sig("moe_expert_cache_create", C.c_int, P(moe_shape), u64, C.c_uint32, u64, vp, C.c_int, P(vp))
+_sig("moe_expert_cache_destroy", C.c_int, vp)
+_sig("moe_expert_cache_set_request_eam", C.c_int, vp, vp)
+_sig("moe_expert_cache_submit", C.c_int, vp, vp, u64)
+_sig("moe_expert_cache_progress", C.c_int, vp, C.c_int)
+_sig("moe_expert_cache_acquire", C.c_int, vp, C.c_uint32, C.c_uint32, P(vp), P(C.c_int))
+_sig("moe_expert_cache_release", C.c_int, vp, C.c_uint32, C.c_uint32)
+_sig("moe_expert_cache_slot", C.c_int, vp, C.c_uint32, P(C.c_int64), P(C.c_int), P(C.c_int),
+     P(C.c_double))
+_sig("moe_expert_cache_stats_get", C.c_int, vp, P(moe_expert_cache_stats))
+_sig("moe_expert_cache_read_slot", C.c_int, vp, C.c_uint32, vp)
 _sig("moe_eamc_build_clustered", C.c_int, vp, vp, u64, C.c_uint32, vp, vp, P(C.c_uint32))
 _sig("moe_eamc_load_sharded", C.c_int, C.c_char_p, P(moe_shape), C.c_int, P(C.c_int), P(vp))
 _sig("moe_eamc_info", C.c_int, vp, P(moe_shape), P(C.c_int), P(u64), P(u64), P(u64),
@@ -125,6 +144,10 @@ EXPORTS = [
     "moe_abi_version", "moe_host_threads", "moe_last_error", "moe_device_info", "moe_device_warmup", "moe_eamc_create",
     "moe_eamc_create_sharded", "moe_eamc_shard_layout", "moe_eamc_load_sharded",
     "moe_eamc_save_binary", "moe_eamc_build_clustered", "moe_eamc_set_decision_server",
+    "moe_expert_cache_create", "moe_expert_cache_destroy", "moe_expert_cache_set_request_eam",
+    "moe_expert_cache_submit", "moe_expert_cache_progress", "moe_expert_cache_acquire",
+    "moe_expert_cache_release", "moe_expert_cache_slot", "moe_expert_cache_stats_get",
+    "moe_expert_cache_read_slot",
     "moe_eamc_destroy", "moe_eamc_info", "moe_eamc_clone", "moe_eamc_entry", "moe_eamc_insert", "moe_eamc_build",
     "moe_eamc_append", "moe_eamc_append_packed", "moe_eamc_match", "moe_eamc_match_device",
     "moe_eamc_match_packed",

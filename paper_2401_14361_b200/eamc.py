@@ -583,3 +583,70 @@ def eamc_save_from_traces(trace_path: str, shape: ModelShape, phase: Phase, capa
     e.build_from_traces(trace_path)
     e.save(out_path)
     return e
+
+
+class ExpertCache:
+    """GPU expert-weight slots filled by chunked DMA in the engine's prefetch
+    order (moe_expert_cache_*): the reference's TransferQueue,
+    GpuBuffer and contention rules (engine.cpp:306-357, :429-529) over real
+    cudaMemcpyAsync of host expert weights ([L][E][expert_bytes] uint8)."""
+
+    def __init__(self, shape: ModelShape, host_weights: np.ndarray, n_slots: int,
+                 chunk_bytes: int = 16 << 20, device: int = 0):
+        self.shape = shape
+        self.weights = np.ascontiguousarray(host_weights, np.uint8)
+        L, E = shape.n_layers, shape.n_experts_per_layer
+        if self.weights.ndim != 3 or self.weights.shape[:2] != (L, E):
+            raise ValueError("host_weights must be [L][E][expert_bytes] uint8")
+        self.expert_bytes = self.weights.shape[2]
+        self._h = C.c_void_p()
+        sh = shape.c()
+        check(lib.moe_expert_cache_create(C.byref(sh), self.expert_bytes, n_slots, chunk_bytes,
+                                          ptr(self.weights), device, C.byref(self._h)))
+        self.n_slots = n_slots
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.moe_expert_cache_destroy(h)
+            self._h = C.c_void_p()
+
+    def set_request_eam(self, request_eam: "Eam") -> None:
+        check(lib.moe_expert_cache_set_request_eam(self._h, ptr(request_eam._buf())))
+
+    def submit(self, order: np.ndarray) -> None:
+        """recompute_prefetch: cancel_all, then the (floor-filtered) order."""
+        order = np.ascontiguousarray(order, CAND_DTYPE)
+        check(lib.moe_expert_cache_submit(self._h, ptr(order), len(order)))
+
+    def progress(self, wait_idle: bool = False) -> None:
+        check(lib.moe_expert_cache_progress(self._h, int(wait_idle)))
+
+    def acquire(self, expert: ExpertId) -> Tuple[int, bool]:
+        p = C.c_void_p()
+        hit = C.c_int()
+        check(lib.moe_expert_cache_acquire(self._h, expert.layer_idx, expert.expert_idx,
+                                           C.byref(p), C.byref(hit)))
+        return p.value, bool(hit.value)
+
+    def release(self, expert: ExpertId) -> None:
+        check(lib.moe_expert_cache_release(self._h, expert.layer_idx, expert.expert_idx))
+
+    def slot(self, i: int) -> dict:
+        occ, res, prot, pri = C.c_int64(), C.c_int(), C.c_int(), C.c_double()
+        check(lib.moe_expert_cache_slot(self._h, i, C.byref(occ), C.byref(res), C.byref(prot),
+                                        C.byref(pri)))
+        E = self.shape.n_experts_per_layer
+        ex = None if occ.value < 0 else ExpertId(occ.value // E, occ.value % E)
+        return {"expert": ex, "residency": res.value, "protected": bool(prot.value),
+                "priority": pri.value}
+
+    def read_slot(self, i: int) -> np.ndarray:
+        out = np.zeros(self.expert_bytes, np.uint8)
+        check(lib.moe_expert_cache_read_slot(self._h, i, ptr(out)))
+        return out
+
+    def stats(self) -> dict:
+        s = _lib.moe_expert_cache_stats()
+        check(lib.moe_expert_cache_stats_get(self._h, C.byref(s)))
+        return {n: getattr(s, n) for n, _ in s._fields_}
