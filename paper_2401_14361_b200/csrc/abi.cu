@@ -1669,6 +1669,14 @@ static int decision_sms(const moe_eamc* h) {
   return std::max(8, h->n_sm - g_srv_sms[h->device & 63].load());
 }
 
+static bool small_off() {  // MOE_DEC_SMALL=0: always the multi-CTA kernel (A/B runs)
+  static const bool off = [] {
+    const char* e = getenv("MOE_DEC_SMALL");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 static bool server_takes(const moe_eamc* h, uint64_t n_slots) {
   return h->srv.G > 0 && n_slots == 0 && !dec_timing();
 }
@@ -1797,6 +1805,44 @@ static moe_status run_decision(moe_eamc* h, moe::DecisionArgs& a, size_t stage_r
     if (n && out && cap) std::memcpy(out, a.out, std::min<uint64_t>(n, cap) * sizeof(moe_candidate));
     if (victim) *victim = -1;
     return MOE_OK;
+  }
+  const uint32_t rows_above = a.cur + 1 < c.L ? c.L - a.cur - 1 : 0;
+  if (!n_slots && a.do_dist && a.do_agg && c.size <= moe::kSmallMaxP &&
+      (uint64_t)rows_above * c.E <= moe::kSmallMaxCells && !small_off()) {
+    // small collection: one CTA, no grid barriers
+    const size_t smem = moe::decision_small_smem(c.size, c.L, c.E, c.RB, a.n_nz, a.cur);
+    if (smem <= 200 * 1024) {
+      a.tprobe = nullptr;
+      if (dec_timing()) {
+        CK(h->tprobe.ensure(64));
+        a.tprobe = h->tprobe.as<unsigned long long>();
+      }
+      const auto t0 = std::chrono::steady_clock::now();
+      CK(moe::launch_decision_small(a, c.cb, smem, st));
+      const auto t1 = std::chrono::steady_clock::now();
+      CK(cudaStreamSynchronize(st));
+      if (dec_timing()) {
+        const auto t2 = std::chrono::steady_clock::now();
+        static double acc[5] = {0};
+        static uint64_t cnt = 0;
+        unsigned long long ts[4];
+        CK(cudaMemcpy(ts, h->tprobe.p, sizeof ts, cudaMemcpyDeviceToHost));
+        acc[0] += std::chrono::duration<double, std::micro>(t1 - t0).count();
+        acc[1] += std::chrono::duration<double, std::micro>(t2 - t1).count();
+        for (int i = 1; i < 4; ++i) acc[1 + i] += (ts[i] - ts[i - 1]) * 1e-3;
+        if (++cnt % 58 == 0)
+          fprintf(stderr, "small decision (avg of %llu): launch %.1f us, launch->done %.1f us | "
+                          "A %.1f B %.1f C %.1f\n",
+                  (unsigned long long)cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt,
+                  acc[3] / cnt, acc[4] / cnt);
+      }
+      const uint32_t n = *reinterpret_cast<volatile uint32_t*>(a.n_out);
+      if (n_out) *n_out = n;
+      if (n && out && cap)
+        std::memcpy(out, a.out, std::min<uint64_t>(n, cap) * sizeof(moe_candidate));
+      if (victim) *victim = -1;
+      return MOE_OK;
+    }
   }
   const int grid = moe::decision_grid(decision_sms(h), c.size, c.L, a.cur);
   const size_t smem = std::max(stage_rows, moe::decision_smem(c.L, c.E, c.RB, 0, a.cur, grid));

@@ -523,6 +523,202 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
   }
 }
 
+// Small collections (size <= kSmallMaxP, (L-l-1)*E <= kSmallMaxCells): the
+// whole decision in one CTA -- the same per-entry distance code, the window
+// aggregation with shared-memory u64 atomics, and the order as one bitonic
+// sort of all (~bits(priority), flat ExpertId) pairs in shared memory -- with
+// no grid barriers and no global atomics.  (MIX: P=300, 31 x 8 candidates.)
+constexpr uint32_t kSmallThreads = 512;
+constexpr uint32_t kSmallWarps = kSmallThreads / 32;
+
+template <int CB>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_decision_small(const __grid_constant__ DecisionArgs a) {
+  using Acc = typename Dot<CB>::Acc;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  __shared__ uint16_t nz_s[kDecMaxNz];
+  __shared__ double sqa_s[kDecMaxNz];
+  __shared__ unsigned long long red_s[kSmallWarps];
+  __shared__ uint32_t cnt_s[kSmallWarps + 1];
+  __shared__ unsigned long long dmin_s;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t L = a.L, E = a.E, RB = a.RB, C = RB / 16;
+  const uint64_t LR = (uint64_t)L * RB;
+  const uint32_t rows_above = a.cur + 1 < L ? L - a.cur - 1 : 0;
+  const uint32_t N = rows_above * E;
+  uint32_t N2 = 1;
+  while (N2 < N) N2 <<= 1;
+  // shared layout: probe rows | dist[size] | agg[N] | rowsum[rows] | key[N2] | id[N2] | members
+  const uint32_t n_nz = a.n_nz;
+  uint4* prow_s = reinterpret_cast<uint4*>(dsm);
+  double* dist_s = reinterpret_cast<double*>(dsm + ((n_nz * RB + 15) & ~15u));
+  unsigned long long* agg_s = reinterpret_cast<unsigned long long*>(dist_s + a.size);
+  unsigned long long* rsum_s = agg_s + N;
+  unsigned long long* key_s = rsum_s + rows_above;
+  uint32_t* id_s = reinterpret_cast<uint32_t*>(key_s + N2);
+  uint32_t* mem_s = id_s + N2;
+  stamp(a, 0);
+  // ---- A: distances (the probe rows the prefix cache does not cover)
+  const uint8_t* rows_src = a.rows_inline ? a.inline_rows : a.rows;
+  const uint16_t* nz_src = a.rows_inline ? a.inline_nz : a.nz;
+  for (uint32_t i = tid; i < n_nz; i += kSmallThreads) nz_s[i] = nz_src[i];
+  for (uint32_t i = tid; i < n_nz * C; i += kSmallThreads)
+    prow_s[i] = reinterpret_cast<const uint4*>(rows_src)[i];
+  for (uint32_t i = tid; i < N; i += kSmallThreads) agg_s[i] = 0;
+  if (tid == 0) dmin_s = ~0ull;
+  __syncthreads();
+  for (uint32_t r = wid; r < n_nz; r += kSmallWarps) {
+    uint64_t ss = 0;
+    const uint8_t* row = reinterpret_cast<const uint8_t*>(prow_s) + (size_t)r * RB;
+    for (uint32_t e = lane; e < E; e += 32) {
+      const uint64_t c = CB == 1 ? row[e]
+                         : CB == 2 ? reinterpret_cast<const uint16_t*>(row)[e]
+                                   : reinterpret_cast<const uint32_t*>(row)[e];
+      ss += c * c;
+    }
+    ss = warp_sum_u64(ss);
+    if (lane == 0) sqa_s[r] = __dsqrt_rn(__ull2double_rn(ss));
+  }
+  __syncthreads();
+  unsigned long long mloc = ~0ull;
+  for (uint32_t p = tid; p < a.size; p += kSmallThreads) {
+    const uint64_t zv = a.zm ? a.zm[p] : 0ull;
+    const double* sb = a.sqb + (uint64_t)p * L;
+    const uint4* eb = reinterpret_cast<const uint4*>(a.counts + (uint64_t)p * LR);
+    double sm = a.j0 ? a.pref[p] : 0.0;
+    uint32_t k = 0;
+    for (uint32_t l = a.j0; l <= a.hi && l < L; ++l) {
+      double r;
+      if (k < n_nz && nz_s[k] == l) {
+        Acc acc = 0;
+        const uint4* pr = prow_s + (size_t)k * C;
+        const uint4* er = eb + (size_t)l * C;
+        for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(pr[c], __ldg(er + c), acc);
+        r = row_sim_exact((uint64_t)acc, sqa_s[k], sb[l]);
+        ++k;
+      } else {
+        r = entry_row_zero(a, zv, p, l) ? 1.0 : 0.0;
+      }
+      sm = __dadd_rn(sm, r);  // layer order (eam.cpp:95-98)
+      if (l == a.keep) a.pref[p] = sm;
+    }
+    if (a.zm) {
+      uint64_t bits = a.hi + 1 < 64 ? zv & ~((2ull << a.hi) - 1ull) : 0ull;
+      if (L < 64) bits &= (1ull << L) - 1ull;
+      for (; bits; bits &= bits - 1) sm = __dadd_rn(sm, 1.0);
+    } else {
+      for (uint32_t l = a.hi + 1; l < L; ++l)
+        if (sb[l] == 0.0) sm = __dadd_rn(sm, 1.0);
+    }
+    const double d = finish_distance(sm, L);
+    dist_s[p] = d;
+    const unsigned long long db = (unsigned long long)__double_as_longlong(d);
+    mloc = db < mloc ? db : mloc;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, mloc, o);
+    mloc = x < mloc ? x : mloc;
+  }
+  if (lane == 0) atomicMin(&dmin_s, mloc);
+  __syncthreads();
+  stamp(a, 1);
+  // ---- B: window members (eam.cpp:143) and their rows above cur
+  const double thr = __dadd_rn(__longlong_as_double((long long)dmin_s), a.window);
+  if (tid == 0) cnt_s[kSmallWarps] = 0;
+  __syncthreads();
+  for (uint32_t p = tid; p < a.size; p += kSmallThreads)
+    if (dist_s[p] <= thr) mem_s[atomicAdd(&cnt_s[kSmallWarps], 1u)] = p;
+  __syncthreads();
+  const uint32_t nm = cnt_s[kSmallWarps];
+  if (rows_above) {
+    const uint32_t wpr = RB / 4, per = 4 / CB, per_mem = rows_above * wpr;
+    for (uint32_t it = tid; it < nm * per_mem; it += kSmallThreads) {
+      const uint32_t mi = it / per_mem, rem = it - mi * per_mem;
+      const uint32_t r = rem / wpr, w = rem - r * wpr;
+      const uint32_t l = a.cur + 1 + r;
+      const uint32_t word = __ldg(reinterpret_cast<const uint32_t*>(
+          a.counts + (uint64_t)mem_s[mi] * LR + (uint64_t)l * RB + 4ull * w));
+      if (!word) continue;
+#pragma unroll
+      for (uint32_t j = 0; j < per; ++j) {
+        const uint32_t e = w * per + j;
+        const uint32_t c = CB == 1 ? (word >> (8 * j)) & 0xffu
+                           : CB == 2 ? (word >> (16 * j)) & 0xffffu
+                                     : word;
+        if (c && e < E) atomicAdd(&agg_s[r * E + e], (unsigned long long)c);
+      }
+    }
+  }
+  __syncthreads();
+  stamp(a, 2);
+  // ---- C: priorities (policy.cpp:106-120), floor filter (engine.cpp:663-668), order
+  for (uint32_t r = wid; r < rows_above; r += kSmallWarps) {
+    unsigned long long s = 0;
+    for (uint32_t e = lane; e < E; e += 32) s += agg_s[r * E + e];
+    s = warp_sum_u64(s);
+    if (lane == 0) rsum_s[r] = s;
+  }
+  __syncthreads();
+  const double kEps = 1e-4;
+  for (uint32_t i = tid; i < N2; i += kSmallThreads) {
+    unsigned long long key = ~0ull;
+    uint32_t id = 0xffffffffu;
+    if (i < N) {
+      const uint32_t r = i / E, e = i - r * E, l = a.cur + 1 + r;
+      const unsigned long long av = agg_s[i], rs = rsum_s[r];
+      if (!(a.filter && av == 0)) {
+        const double prox = __dsub_rn(1.0, __ddiv_rn((double)(l - a.cur), (double)L));
+        const double ratio = rs == 0 ? 0.0 : __ddiv_rn(__ull2double_rn(av), __ull2double_rn(rs));
+        const double pri = __dmul_rn(__dadd_rn(ratio, kEps), prox);
+        const double floor_p = __dmul_rn(__dmul_rn(kEps, prox), __dadd_rn(1.0, 1e-9));
+        if (!(a.filter && pri <= floor_p)) {
+          key = ~(unsigned long long)__double_as_longlong(pri);
+          id = l * E + e;
+        }
+      }
+    }
+    key_s[i] = key;
+    id_s[i] = id;
+  }
+  __syncthreads();
+  for (uint32_t k = 2; k <= N2; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = tid; i < N2; i += kSmallThreads) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long ki = key_s[i], kj = key_s[ixj];
+          const uint32_t vi = id_s[i], vj = id_s[ixj];
+          if (pair_lt(kj, vj, ki, vi) == ((i & k) == 0)) {
+            key_s[i] = kj;
+            key_s[ixj] = ki;
+            id_s[i] = vj;
+            id_s[ixj] = vi;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  // survivors first (their keys are below ~0); count and write
+  uint32_t c = 0;
+  for (uint32_t i = tid; i < N2; i += kSmallThreads) c += key_s[i] != ~0ull;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if (lane == 0) cnt_s[wid] = c;
+  __syncthreads();
+  uint32_t S = 0;
+  for (uint32_t w = 0; w < kSmallWarps; ++w) S += cnt_s[w];
+  for (uint32_t i = tid; i < S; i += kSmallThreads) {
+    const uint32_t id = id_s[i];
+    moe_candidate o;
+    o.layer_idx = id / E;
+    o.expert_idx = id - o.layer_idx * E;
+    o.priority = __longlong_as_double((long long)~key_s[i]);
+    a.out[i] = o;
+  }
+  if (tid == 0) *a.n_out = S;
+  stamp(a, 3);
+}
+
 template <int CB>
 __global__ void __launch_bounds__(kDecThreads, 1) k_decision(const __grid_constant__ DecisionArgs a) {
   decision_body<CB, false>(a);
@@ -642,6 +838,30 @@ __global__ void __launch_bounds__(kDecThreads, 1)
 }
 
 }  // namespace
+
+size_t decision_small_smem(uint32_t size, uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz,
+                           uint32_t cur) {
+  const uint32_t rows = cur + 1 < L ? L - cur - 1 : 0, N = rows * E;
+  uint32_t N2 = 1;
+  while (N2 < N) N2 <<= 1;
+  return (((size_t)n_nz * RB + 15) & ~(size_t)15) + (size_t)size * 8 + (size_t)N * 8 +
+         (size_t)rows * 8 + (size_t)N2 * 12 + (size_t)size * 4;
+}
+
+cudaError_t launch_decision_small(const DecisionArgs& a, int cb, size_t smem, cudaStream_t st) {
+  void (*kern)(DecisionArgs) =
+      cb == 1 ? k_decision_small<1> : cb == 2 ? k_decision_small<2> : k_decision_small<4>;
+  static size_t set[3] = {0, 0, 0};
+  const int slot = cb == 1 ? 0 : cb == 2 ? 1 : 2;
+  if (smem > set[slot]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set[slot] = smem;
+  }
+  kern<<<1, kSmallThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
 
 size_t decision_smem(uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz, uint32_t cur,
                      uint32_t grid) {

@@ -207,6 +207,12 @@ int decision_grid(int n_sm, uint32_t size, uint32_t L, uint32_t cur);
 // One cooperative launch (grid <= co-resident CTAs; decision_grid picks it).
 cudaError_t launch_decision(const DecisionArgs& a, int cb, int grid, size_t smem,
                             cudaStream_t st);
+// Small collections: the whole decision in one CTA (decide.cu).
+size_t decision_small_smem(uint32_t size, uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz,
+                           uint32_t cur);
+cudaError_t launch_decision_small(const DecisionArgs& a, int cb, size_t smem, cudaStream_t st);
+constexpr uint32_t kSmallMaxP = 512;        // entries (one per thread)
+constexpr uint32_t kSmallMaxCells = 1024;   // (L - cur - 1) * E candidates
 // The persistent decision server's mailbox (pinned host memory, device-mapped).
 struct DecServerCtl {
   uint64_t seq_req;   // host: the request number being posted

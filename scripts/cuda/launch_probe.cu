@@ -2,6 +2,7 @@
 // parameter blocks and large dynamic shared memory, then launch->complete.
 #include <chrono>
 #include <cstdio>
+#include <vector>
 #include <cuda_runtime.h>
 struct Big { char b[800]; };
 struct Big1k { alignas(16) char b[1100]; };
@@ -54,6 +55,18 @@ int main() {
   timeit("1.1KB grid_constant 31x256", [&] { k_gc<<<31, 256, 4 * 1024, st>>>(b1, d); }, st);
   timeit("1.1KB gc + 110KB dyn smem", [&] { k_gc<<<58, 256, 110 * 1024, st>>>(b1, d); }, st);
   int* hp; cudaMallocHost(&hp, 64);
+  static std::vector<char> junk(4 << 20);
+  timeit("1.1KB gc + 4MB host work between", [&] {
+    for (size_t i = 0; i < junk.size(); i += 64) junk[i]++;
+    auto t = std::chrono::steady_clock::now();
+    k_gc<<<31, 256, 4 * 1024, st>>>(b1, d);
+    (void)t;
+  }, st);
+  static std::vector<char> small(64 << 10);
+  timeit("1.1KB gc + 64KB host work", [&] {
+    for (size_t i = 0; i < small.size(); i += 64) small[i]++;
+    k_gc<<<31, 256, 4 * 1024, st>>>(b1, d);
+  }, st);
   timeit("1.1KB gc, host-mapped out", [&] { k_gc<<<31, 256, 4 * 1024, st>>>(b1, hp); }, st);
   return 0;
 }
