@@ -34,6 +34,9 @@
 // counter are double-buffered by call parity and the kernel resets the other
 // half for the next call, so a decision is exactly one launch.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -660,10 +663,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     if (lane == 0) rsum_s[r] = s;
   }
   __syncthreads();
+  // survivors compacted in flat ExpertId order (ballot prefix), then each
+  // survivor's output position = the number of survivor pairs below it
   const double kEps = 1e-4;
-  for (uint32_t i = tid; i < N2; i += kSmallThreads) {
+  uint32_t base = 0;
+  for (uint32_t i0 = 0; i0 < N; i0 += kSmallThreads) {
+    const uint32_t i = i0 + tid;
     unsigned long long key = ~0ull;
-    uint32_t id = 0xffffffffu;
+    uint32_t id = 0;
     if (i < N) {
       const uint32_t r = i / E, e = i - r * E, l = a.cur + 1 + r;
       const unsigned long long av = agg_s[i], rs = rsum_s[r];
@@ -678,42 +685,33 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
         }
       }
     }
-    key_s[i] = key;
-    id_s[i] = id;
-  }
-  __syncthreads();
-  for (uint32_t k = 2; k <= N2; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = tid; i < N2; i += kSmallThreads) {
-        const uint32_t ixj = i ^ j;
-        if (ixj > i) {
-          const unsigned long long ki = key_s[i], kj = key_s[ixj];
-          const uint32_t vi = id_s[i], vj = id_s[ixj];
-          if (pair_lt(kj, vj, ki, vi) == ((i & k) == 0)) {
-            key_s[i] = kj;
-            key_s[ixj] = ki;
-            id_s[i] = vj;
-            id_s[ixj] = vi;
-          }
-        }
-      }
-      __syncthreads();
+    const bool sv = key != ~0ull;
+    const uint32_t m = __ballot_sync(0xffffffffu, sv);
+    if (lane == 0) cnt_s[wid] = __popc(m);
+    __syncthreads();
+    uint32_t off = base;
+    for (uint32_t w = 0; w < wid; ++w) off += cnt_s[w];
+    if (sv) {
+      const uint32_t q = off + __popc(m & ((1u << lane) - 1u));
+      key_s[q] = key;
+      id_s[q] = id;
     }
-  // survivors first (their keys are below ~0); count and write
-  uint32_t c = 0;
-  for (uint32_t i = tid; i < N2; i += kSmallThreads) c += key_s[i] != ~0ull;
-  c = __reduce_add_sync(0xffffffffu, c);
-  if (lane == 0) cnt_s[wid] = c;
-  __syncthreads();
-  uint32_t S = 0;
-  for (uint32_t w = 0; w < kSmallWarps; ++w) S += cnt_s[w];
+    uint32_t tot = 0;
+    for (uint32_t w = 0; w < kSmallWarps; ++w) tot += cnt_s[w];
+    base += tot;
+    __syncthreads();
+  }
+  const uint32_t S = base;
   for (uint32_t i = tid; i < S; i += kSmallThreads) {
-    const uint32_t id = id_s[i];
+    const unsigned long long ki = key_s[i];
+    const uint32_t ii = id_s[i];
+    uint32_t pos = 0;
+    for (uint32_t j = 0; j < S; ++j) pos += pair_lt(key_s[j], id_s[j], ki, ii);
     moe_candidate o;
-    o.layer_idx = id / E;
-    o.expert_idx = id - o.layer_idx * E;
-    o.priority = __longlong_as_double((long long)~key_s[i]);
-    a.out[i] = o;
+    o.layer_idx = ii / E;
+    o.expert_idx = ii - o.layer_idx * E;
+    o.priority = __longlong_as_double((long long)~ki);
+    a.out[pos] = o;
   }
   if (tid == 0) *a.n_out = S;
   stamp(a, 3);
@@ -859,8 +857,30 @@ cudaError_t launch_decision_small(const DecisionArgs& a, int cb, size_t smem, cu
     if (e != cudaSuccess) return e;
     set[slot] = smem;
   }
-  kern<<<1, kSmallThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  static const bool prof = getenv("MOE_LAUNCH_PROF") != nullptr;
+  if (!prof) {
+    kern<<<1, kSmallThreads, smem, st>>>(a);
+    return cudaGetLastError();
+  }
+  // launch-path instrumentation (MOE_LAUNCH_PROF=1)
+  static double acc[4] = {0, 0, 0, 0};
+  static uint64_t cnt = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaError_t q = cudaStreamQuery(st);
+  const auto t1 = std::chrono::steady_clock::now();
+  void* args[] = {const_cast<DecisionArgs*>(&a)};
+  cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(kern), dim3(1), dim3(kSmallThreads),
+                                   args, smem, st);
+  const auto t2 = std::chrono::steady_clock::now();
+  cudaError_t g = cudaGetLastError();
+  const auto t3 = std::chrono::steady_clock::now();
+  acc[0] += std::chrono::duration<double, std::micro>(t1 - t0).count();
+  acc[1] += std::chrono::duration<double, std::micro>(t2 - t1).count();
+  acc[2] += std::chrono::duration<double, std::micro>(t3 - t2).count();
+  if (++cnt % 100 == 0)
+    fprintf(stderr, "launch path (avg of %llu): streamQuery %.2f us, cudaLaunchKernel %.2f us, getLastError %.2f us (q=%d)\n",
+            (unsigned long long)cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, (int)q);
+  return e != cudaSuccess ? e : g;
 }
 
 size_t decision_smem(uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz, uint32_t cur,
