@@ -556,6 +556,24 @@ def run_rows(args, m, _lib, torch, dev, sp, stream, flush):
                                "block's screen distances come from tcgen05 GEMMs"}
     out["construction"] = row
 
+    # -- the step-wise construction path (one screen + refine + replace per insert;
+    #    taken for single inserts, L > 64 or P > 16,384), timed at P = 20,000
+    P7, n7 = 20_000, 256
+    fam7 = m.gen_bench_family(5, L3, E3, P7 + 32 + n7, dtype=np.uint8)
+    e7 = m.Eamc(m.ModelShape(L3, E3), m.Phase.decode, P7)
+    e7.append(fam7[:P7], np.arange(P7, dtype=np.uint64))
+    st7 = fam7[P7:].astype(np.uint64)
+    e7.build(st7[:32])  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e7.build(st7[32:])
+    t7 = time.perf_counter() - t0
+    out["construction_stepwise"] = {
+        "workload": f"L={L3} E={E3}, capacity P={P7} (> 16,384: the step-wise replay), {n7} "
+                    "at-capacity inserts (moe_eamc_build, host u64 EAMs)",
+        "gpu_us_per_step": t7 / n7 * 1e6, "gpu_evals_per_s": n7 * P7 / t7}
+    del e7
+
     # -- north-star (3): clustering construction, NL config (configs[2]):
     #    N = 100k request EAMs (F2 grouped workload, L=24 E=128 top-2) -> P = 10k.
     #    Iteration 0 = the reference insert replay over all N (the full configs[2]
