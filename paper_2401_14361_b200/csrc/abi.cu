@@ -155,11 +155,13 @@ bool use_i8(const moe_eamc* h, uint64_t Q) {
     if (e[0] == '0') return false;
     if (e[0] == '1') return true;
   }
-  // one 128-row block-diagonal M tile (128/R probes) streams the collection
-  // once; beyond that the fp16 screen is cheaper
+  // one 128-row block-diagonal M tile holds 128/R probes; up to three M
+  // tiles the i8 screen still beats the fp16 one (its M tiles share each
+  // entry tile through L2; measured at P=2^20, L=12: Q=16 0.38 vs 0.73 ms,
+  // Q=24 0.51 vs 0.65 ms, Q=32 0.70 vs 0.63 ms)
   uint32_t R = 1;
   while (R < h->c.L) R <<= 1;
-  return Q <= 128 / R;
+  return Q <= 3 * (128 / R);
 }
 
 // Tensor-core screen for probe batches that fill its 128-row M tile

@@ -31,7 +31,13 @@ namespace moe {
 namespace {
 
 constexpr int BM = 128, BN = 256, BKB = 128;  // BKB = K bytes per stage (one SW128 atom row)
-constexpr int STAGES = 4;
+#ifndef I8_IB_STAGE
+#define I8_IB_STAGE 1
+#endif
+// With the entry norms of a tile staged in shared memory (I8_IB_STAGE), three
+// operand stages leave room for them.
+constexpr int STAGES = I8_IB_STAGE ? 3 : 4;
+constexpr uint32_t IBS = 257;  // staged norm row stride (odd: 16 rows -> 16 banks)
 constexpr uint32_t A_BYTES = BM * BKB;  // 16 KB
 constexpr uint32_t B_BYTES = BN * BKB;  // 32 KB
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -140,7 +146,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* zp_s = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);  // [2][BN]
-  uint64_t* full = zp_s + 2 * BN;
+  float* ib_s = reinterpret_cast<float*>(zp_s + 2 * BN);                 // [2][R][IBS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ib_s + (I8_IB_STAGE ? 2 * (1u << LOGR) * IBS : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -234,6 +241,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t p = n * BN + et;
         zt[et] = p < a.P ? a.zp[p] : 0ull;
       }
+#if I8_IB_STAGE
+      // the tile's entry norms ibT[l][n*BN .. +BN) -> shared (coalesced rows),
+      // read back per (lane = layer, column) without bank conflicts
+      float* ibs = ib_s + acc * R * IBS;
+      for (uint32_t k = et; k < R * BN; k += EPI_THREADS) {
+        const uint32_t r = k / BN, c = k - r * BN;
+        const uint32_t p = n * BN + c;
+        ibs[r * IBS + c] = (r < a.L && p < a.P) ? __ldg(a.ibT + (uint64_t)r * a.cap + p) : 0.f;
+      }
+#endif
       asm volatile("bar.sync 1, 256;" ::: "memory");
       const uint32_t q = m * (BM >> LOGR) + qg;
       const bool qvalid = q < a.Q;
@@ -255,7 +272,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const uint32_t p = p0 + c * 32 + j;
+#if I8_IB_STAGE
+          const float ib = ibs[l * IBS + half * 128 + c * 32 + j];
+          (void)ibl;
+          (void)p;
+#else
           const float ib = (rvalid && p < a.P) ? __ldg(ibl + p) : 0.f;
+#endif
           v[j] = __uint2float_rn(r[j]) * ia * ib;
         }
         group_sum_transpose<LOGR>(v, lane);
@@ -424,7 +447,9 @@ cudaError_t launch_tci8_screen(const DevColl& c, const DevProbes& pr, const Matc
   a.bcnt = w.bcnt;
   a.bucket = w.bucket;
   a.bcap = w.bcap;
-  const size_t smem = (size_t)STAGES * STAGE_BYTES + 2 * BN * 8 + (2 * STAGES + 4) * 8 + 16;
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + 2 * BN * 8 +
+                      (I8_IB_STAGE ? (2 * (size_t)(1u << logR) * IBS) * 4 : 0) +
+                      (2 * STAGES + 4) * 8 + 16;
   const uint32_t grid = std::min<uint32_t>(a.n_m * a.n_n, (uint32_t)n_sm);
   switch (logR) {
     case 0: return launch_t<0>(ca.map, cb.map, a, grid, smem, st);

@@ -866,3 +866,21 @@ def test_match_device_u8_layouts(m, orc, E, offset):
     res = out.cpu().numpy().view(np.uint8).reshape(Q, 24).copy().view(_lib.MATCH_DTYPE)[:, 0]
     idx, seq, d, _ = orc.match(fam[:P], seqs_of(P), fam[P:])
     assert np.array_equal(res["index"], idx) and np.array_equal(res["distance"], d)
+
+
+# ------------------------------------------ i8 streaming screen, 1-3 M tiles
+@pytest.mark.parametrize("L,E,Q", [(12, 128, 8), (12, 128, 16), (12, 128, 24), (32, 8, 12),
+                                   (3, 64, 96), (30, 32, 3)])
+def test_match_i8_screen_m_tiles(m, orc, L, E, Q):
+    """u8 collections with Q up to three 128-row block-diagonal M tiles take
+    the kind::i8 tensor-core screen (its entry norms staged in shared memory):
+    bitwise vs the oracle, incl. exact duplicates (ties) and zero rows."""
+    P = 3000
+    fam = m.gen_bench_family(13, L, E, P + Q).copy()
+    fam[P - 40:P] = fam[:40]            # exact duplicate entries: ties by seq
+    fam[5, :L // 2] = 0                 # zero rows
+    probes = np.concatenate([fam[[0, 7, 2999]], fam[P:P + Q - 3]])
+    e = m.Eamc(m.ModelShape(L, E), m.Phase.decode, P)
+    e.append(fam[:P], np.arange(P, dtype=np.uint64))
+    assert e.count_bytes() == 1
+    check_match(m, orc, e, fam[:P], np.arange(P, dtype=np.uint64), probes)
