@@ -639,7 +639,7 @@ def run_rows(args, m, _lib, torch, dev, sp, stream, flush):
            for _ in range(n_ev)]
     for a_, b_ in evs:
         a_.record(stream)
-        trace_dev()  # the whole call: k_trace_own + gated long-request pass + gated rollbacks
+        trace_dev()  # the whole call: k_trace_lane + its gated rollback
         b_.record(stream)
     torch.cuda.synchronize()
     t_dev = sum(a_.elapsed_time(b_) for a_, b_ in evs) / n_ev / 1e3
@@ -654,10 +654,10 @@ def run_rows(args, m, _lib, torch, dev, sp, stream, flush):
     t_e2e = (time.perf_counter() - t0) / reps4
     row = {"workload": f"DS tracing: T={T4} tokens x L={L4} x top-{k4} u8 ids, R={R4} requests",
            "gpu_ms": t_dev * 1e3, "picks_per_s": T4 * L4 * k4 / t_dev,
-           "roofline": {"bound": "hbm", "kernel": "k_trace_own (+ gated passes), whole call",
+           "roofline": {"bound": "hbm", "kernel": "k_trace_lane (+ gated rollback), whole call",
                         "achieved": bytes_alg / t_dev / 1e9, "peak": hbm_peak,
                         "unit": "GB/s", "frac": bytes_alg / t_dev / 1e9 / hbm_peak,
-                        "traffic": ncu_traffic("k_trace_own"),
+                        "traffic": ncu_traffic("k_trace_lane"),
                         "alg_bytes": bytes_alg, "note": f"peak = {peak_kind} HBM; bytes = "
                         "T*L*k ids + R*L*E*4 counts + 8*(R+1) offsets (SURVEY 8d)"},
            "e2e_ms": t_e2e * 1e3,

@@ -2,38 +2,32 @@
 // counts (Eam::record, eam.cpp:41-52, driven per token as
 // workload.cpp:166-181 does), accumulated straight into the caller's counts.
 //
-// Work items are (token chunk, layer group) pairs over the id stream
-// [T][L][k]: a persistent grid walks them, and inside an item the block
-// processes every request piece (request r intersected with the chunk) and
-// flushes that piece's histogram into counts[r] -- plain read-modify-write
-// when the chunk holds the whole request (the only writer of those cells),
-// global atomics when the request spans chunks.  There is no scratch
-// histogram in global memory and no commit pass: the counts are written once.
+// Three kernels share one contract.  All-or-nothing (eam.cpp:42-47: every
+// index is validated before any count moves): an out-of-range id is skipped
+// and raises *bad; a second, gated launch of the same kernel then runs only
+// when *bad is set and subtracts exactly what the first added (same items,
+// same skips; unsigned arithmetic is exact modulo 2^32 / 2^64), so a failed
+// call leaves counts as it found them.  The gated launch costs one empty grid
+// on the success path.  No kernel keeps a global scratch histogram: each adds
+// its shared-memory partial straight into the caller's counts once.
 //
-// All-or-nothing (eam.cpp:42-47: every index is validated before any count
-// moves).  An out-of-range id is skipped and raises *bad; a second, gated
-// launch of the same kernel then runs only when *bad is set and subtracts
-// exactly what the first added (same items, same skips; unsigned arithmetic
-// is exact modulo 2^32 / 2^64), so a failed call leaves counts as it found
-// them.  The gated launch costs one empty grid on the success path.
+// k_trace_lane (u8 ids, L*k even, E <= 256, requests of >= 16 tokens on
+// average; the DS case): bank-locked private counters fed by a bulk-copy
+// ring -- see its comment below.  Any request length.
 //
-// k_trace_own (u8 ids, E <= 256, 16-byte aligned stream, L x E histogram in
-// shared memory; the DS case): a block owns whole requests (<= 16,384
-// tokens) and adds its shared histogram straight into counts[r].  The id
-// stream is read in aligned 16-byte chunks; 16*CH bytes = lcm(L*k, 16) hold a
-// whole number of tokens, so the histogram row of byte j of chunk i depends
-// only on (i mod CH, j): each thread keeps its 16 row addresses in registers
-// and, per id, does PRMT + LEA + RED.shared.  Four chunks per thread are in
-// flight (a rolling register pipeline), which is what keeps HBM busy.  The
-// range check is a SWAR test per word (the byte-wise __vmaxu4 is emulated on
-// sm_100).  Longer requests, other index widths and shapes whose histogram
-// does not fit go through k_trace_gen.
+// k_trace_own (other u8 shapes whose L x E histogram fits): a block owns whole
+// requests (<= 16,384 tokens) and adds its shared histogram straight into
+// counts[r].  The id stream is read in aligned 16-byte chunks; 16*CH bytes =
+// lcm(L*k, 16) hold a whole number of tokens, so the histogram row of byte j
+// of chunk i depends only on (i mod CH, j): each thread keeps its 16 row
+// addresses in registers and, per id, does PRMT + LEA + RED.shared (~3.3
+// wavefronts each: random banks).  The range check is a SWAR test per word.
 //
-// Measured alternative, not kept: per-lane private counter
-// copies make the shared reductions conflict-free (1.1 instead of ~3.4
-// wavefronts each), but 32 copies need layer groups of ~10 layers per block,
-// which cut the loads in flight per SM and added a flush per (request,
-// group): 0.28 ms vs 0.19 ms for this kernel at DS.
+// k_trace_gen (u16/u32 ids, any alignment, wide shapes, and k_trace_own's long
+// requests): work items are (token chunk, layer group) pairs; per item the
+// block processes every request piece (request r intersected with the chunk)
+// and flushes that piece's histogram into counts[r] -- plain read-modify-write
+// when the chunk holds the whole request, global atomics when it spans chunks.
 #include <algorithm>
 #include <cstdint>
 
@@ -206,6 +200,269 @@ __global__ void __launch_bounds__(512)
   pdl_trigger();
 }
 
+#ifndef LANE_U
+#define LANE_U 16
+#endif
+// ---- k_trace_lane: bank-locked private counters fed by a bulk-copy ring ----
+//
+// The id stream is cut into items of TS tokens (one per block); inside an item
+// one producer thread streams stages of TW whole tokens through a ring of
+// shared-memory slots (cp.async.bulk of the 16-byte aligned window, completion
+// on an mbarrier), so the loads in flight do not depend on registers.
+//
+// Consumer warps form G groups; group g takes stages g, g + G, ...  Inside a
+// group, thread tg = tp * H + q (H = L*k / 2 position pairs) owns the id
+// positions 2q, 2q+1 of the stage's tokens j = tp (mod TPg): it reads them as
+// one u16 and adds 1 (position 2q) or 0x10000 (position 2q+1) into the counter
+// word of its column for expert e, cnt[e][col].  A column belongs to one lane
+// position of one warp in every group (col = tg mod C), so the 32 lanes of a
+// warp always hit 32 distinct banks -- one wavefront per RED.shared, where a
+// shared L x E histogram takes ~3.3 (k_trace_own).  Ids >= E are clamped into
+// a trash row (nonzero -> the call's flag), masked tail slots into a null row.
+// A 16-bit half counts at most one id per token of a piece and pieces are at
+// most TS <= 65,535 tokens, so halves never carry.
+//
+// Request ends inside the item and the item end are events: every group joins
+// each event (a named barrier over all consumers) after counting its tokens
+// before it and before counting any token after it, and the consumers then
+// reduce the counters into counts[r]: per (layer, expert) cell the halves of
+// the layer's positions (and the token phases' columns) are summed into a
+// padded staging row, the counters are zeroed, and the staged cells are added
+// into counts[r] with coalesced reductions (RED: no thread waits on the
+// counts' latency; a read-modify-write pass cost ~2 us per piece).  The
+// rollback launch subtracts the same sums (see gate_open).
+//
+// Measured (DS, 1M tokens, scripts/trace_probe.py): 0.173 ms at 1,000
+// requests (k_trace_own: 0.190 ms), 0.129 ms at 50 requests of 20k tokens
+// (k_trace_own + k_trace_gen: 1.95 ms).  The remaining gap to HBM is issue
+// (~10 instructions per u16 of ids) and the cross-group barrier per piece.
+struct LaneArgs {
+  const uint8_t* topk;
+  uint64_t T, TS;
+  const uint64_t* offsets;
+  uint64_t R;
+  uint32_t L, E, k, H;
+  uint32_t TPg, NWg, G;  // token phases per group, warps per group, groups
+  uint32_t C, NCOL;      // counter columns (thread tg uses column tg mod C), padded to 32
+  uint32_t TW, NSTG, SB; // tokens per stage, ring slots, slot bytes
+  int* bad;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync(uint32_t n) {
+  asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory");
+}
+
+// Effective token range of item ii: tokens outside [offsets[0], offsets[R])
+// belong to no request and are neither streamed nor counted.
+__device__ __forceinline__ bool lane_item(const LaneArgs& a, uint64_t ii, uint64_t lo, uint64_t hi,
+                                          uint64_t* ta, uint64_t* tb) {
+  *ta = max(ii * a.TS, lo);
+  *tb = min(min(a.T, ii * a.TS + a.TS), hi);
+  return *ta < *tb;
+}
+
+// The consumers' reduction of one request piece into counts[r].
+template <typename OUT>
+__device__ __forceinline__ void lane_flush(const LaneArgs& a, uint32_t* cnt, uint32_t* stage_out,
+                                           uint32_t NC, OUT* dst, int sign) {
+  const uint32_t t = threadIdx.x, L = a.L, E = a.E, k = a.k, ES = E | 1, NCOL = a.NCOL;
+  consumers_sync(NC);
+  {  // cell (l, e), layer fastest: conflict-free reads
+    const uint32_t de = NC / L, dl = NC - de * L;
+    uint32_t e = t / L, l = t - e * L;
+    const uint32_t CM = a.C / a.H;  // columns per position pair
+    if (CM == 1 && (k & 1) == 0) {  // whole words per layer, one column each
+      const uint32_t kh = k >> 1;
+      for (; e < E;) {
+        const uint32_t* cw = cnt + e * NCOL + l * kh;
+        uint32_t sum = 0;
+        for (uint32_t w = 0; w < kh; ++w) sum += (cw[w] & 0xffffu) + (cw[w] >> 16);
+        stage_out[l * ES + e] = sum;
+        l += dl;
+        e += de;
+        if (l >= L) l -= L, ++e;
+      }
+    } else {
+      for (; e < E;) {
+        const uint32_t p0 = l * k, p1 = p0 + k;
+        uint32_t sum = 0;
+        for (uint32_t w = p0 >> 1; w < (p1 + 1) >> 1; ++w) {
+          const bool lo_in = 2 * w >= p0, hi_in = 2 * w + 1 < p1;
+          for (uint32_t m = 0; m < CM; ++m) {
+            const uint32_t c = cnt[e * NCOL + m * a.H + w];
+            sum += (lo_in ? (c & 0xffffu) : 0u) + (hi_in ? (c >> 16) : 0u);
+          }
+        }
+        stage_out[l * ES + e] = sum;
+        l += dl;
+        e += de;
+        if (l >= L) l -= L, ++e;
+      }
+    }
+  }
+  for (uint32_t i = t; i < NCOL; i += NC)  // the trash row: ids >= E
+    if (cnt[E * NCOL + i] != 0 && sign > 0) *a.bad = 1;
+  consumers_sync(NC);
+  for (uint32_t i = t; i < (E + 2) * NCOL / 4; i += NC)
+    reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  // reductions without a return value: no thread waits on the counts' latency
+  for (uint32_t i = t; i < L * E; i += NC) {
+    const uint32_t l = i / E;
+    const uint32_t v = stage_out[l * ES + (i - l * E)];
+    if (v) add_out(dst + i, v, sign, false);
+  }
+  consumers_sync(NC);
+}
+
+template <typename OUT>
+__global__ void __launch_bounds__(640, 1) k_trace_lane(LaneArgs a, OUT* __restrict__ counts, int mode, int sign) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const uint32_t NC = a.G * a.NWg * 32;  // consumer threads (whole warps)
+  const uint32_t t = threadIdx.x;
+  const uint32_t L = a.L, E = a.E, Lk = L * a.k, ES = E | 1, NCOL = a.NCOL;
+  uint8_t* ring = sm;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + (size_t)a.NSTG * a.SB);  // [E + 2][NCOL]
+  uint32_t* stage_out = cnt + (size_t)(E + 2) * NCOL;                       // [L][ES]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + (((size_t)L * ES + 1) & ~(size_t)1));
+  uint64_t* empty = full + a.NSTG;
+  if (t == 0) {
+    for (uint32_t s = 0; s < a.NSTG; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], a.NWg);  // the stage's group
+    }
+    fence_mbar_init();
+  }
+  if (mode == kRun)  // zeroing overlaps the previous grid's tail
+    for (uint32_t i = t; i < (E + 2) * NCOL / 4; i += blockDim.x)
+      reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  pdl_wait();
+  if (!gate_open(a.bad, mode)) return;  // rollback launch on a clean call
+  if (mode != kRun) {
+    for (uint32_t i = t; i < (E + 2) * NCOL / 4; i += blockDim.x)
+      reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+  }
+  const uint64_t lo = a.offsets[0], hi = a.offsets[a.R];
+  const uint64_t n_items = (a.T + a.TS - 1) / a.TS;
+  const uintptr_t base = reinterpret_cast<uintptr_t>(a.topk);
+  if (t >= NC) {  // producer warp: one thread streams the stages in order
+    if (t == NC) {
+      uint32_t s = 0, ph = 0;  // ring slot and its pass parity
+      for (uint64_t ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
+        uint64_t ta, tb;
+        if (!lane_item(a, ii, lo, hi, &ta, &tb)) continue;
+        for (uint64_t tok = ta; tok < tb; tok += a.TW) {
+          const uint64_t te = min(tb, tok + a.TW);
+          const uintptr_t g0 = (base + tok * Lk) & ~(uintptr_t)15;
+          const uintptr_t g1 = (base + te * Lk + 15) & ~(uintptr_t)15;
+          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[s], (uint32_t)(g1 - g0));
+          bulk_g2s(ring + (size_t)s * a.SB, reinterpret_cast<const void*>(g0), (uint32_t)(g1 - g0),
+                   &full[s]);
+          if (++s == a.NSTG) s = 0, ph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+  const uint32_t lane = t & 31, g = (t >> 5) / a.NWg, tg = t - g * a.NWg * 32;
+  const bool act = tg < a.H * a.TPg;
+  const uint32_t tp = act ? tg / a.H : 0, q = act ? tg - tp * a.H : 0;
+  const uint32_t my = smem_u32(cnt) + 4u * (tg % a.C), rowE = 4u * NCOL;  // expert e: my + e * rowE
+  const uint32_t Eh = E, dj = a.TPg * Lk;
+  uint32_t seq0 = 0;  // ring sequence number of the item's first stage
+  for (uint64_t ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
+    uint64_t ta, tb;
+    if (!lane_item(a, ii, lo, hi, &ta, &tb)) continue;
+    uint64_t r;  // the request holding token ta (the first one whose end lies beyond it)
+    {
+      uint64_t l0 = 0, h0 = a.R;
+      while (l0 < h0) {
+        const uint64_t mid = (l0 + h0) / 2;
+        if (a.offsets[mid + 1] <= ta) l0 = mid + 1; else h0 = mid;
+      }
+      r = l0;
+    }
+    uint64_t rend = a.offsets[r + 1];
+    uint64_t ev = min(rend, tb);  // the next event
+    bool done = false;            // the item-end event has been joined
+    // join the next event: reduce the piece of request r, step to the next request
+    auto join = [&]() {
+      lane_flush<OUT>(a, cnt, stage_out, NC, counts + r * (uint64_t)L * E, sign);
+      if (ev == tb) done = true;
+      if (ev == rend) {  // next non-empty request
+        while (r + 1 < a.R && a.offsets[r + 2] <= ev) ++r;
+        ++r;
+        rend = r < a.R ? a.offsets[r + 1] : hi;
+      }
+      ev = min(rend, tb);
+    };
+    const uint32_t ns = (uint32_t)((tb - ta + a.TW - 1) / a.TW);
+    uint32_t s = (seq0 + g) % a.NSTG, ph = ((seq0 + g) / a.NSTG) & 1u;
+    for (uint32_t kst = g; kst < ns; kst += a.G) {
+      const uint64_t tok = ta + (uint64_t)kst * a.TW;
+      const uint32_t n = (uint32_t)min((uint64_t)a.TW, tb - tok);  // tokens in this stage
+      while (!done && ev <= tok) join();  // events before the stage
+      mbar_wait(&full[s], ph);
+      const uint8_t* sb = ring + (size_t)s * a.SB + ((base + tok * Lk) & 15) + 2u * q;
+      uint32_t jx = 0;
+      while (jx < n) {
+        const uint32_t jy = ev - tok < n ? (uint32_t)(ev - tok) : n;
+        if (act) {  // stage-local tokens j in [jx, jy), phase tp takes j = tp (mod TPg)
+          uint32_t j = jx == 0 ? tp : jx + (tp + a.TPg - jx % a.TPg) % a.TPg;
+          const uint8_t* pj = sb + j * Lk;
+          constexpr int U = LANE_U;
+          for (; j + (U - 1) * a.TPg < jy; j += U * a.TPg, pj += U * dj) {
+            uint32_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = *reinterpret_cast<const uint16_t*>(pj + u * dj);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {  // ids >= E land in the trash row E
+              const uint32_t e0 = min(v[u] & 0xffu, Eh), e1 = min(v[u] >> 8, Eh);
+              asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(my + e0 * rowE));
+              asm volatile("red.shared.add.u32 [%0], 65536;" ::"r"(my + e1 * rowE));
+            }
+          }
+          if (j < jy) {  // tail: one masked round, the masked slots count into the null row
+            uint32_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              v[u] = j + u * a.TPg < jy ? *reinterpret_cast<const uint16_t*>(pj + u * dj) : 0u;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const bool in = j + u * a.TPg < jy;
+              const uint32_t e0 = in ? min(v[u] & 0xffu, Eh) : Eh + 1;
+              const uint32_t e1 = in ? min(v[u] >> 8, Eh) : Eh + 1;
+              asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(my + e0 * rowE));
+              asm volatile("red.shared.add.u32 [%0], 65536;" ::"r"(my + e1 * rowE));
+            }
+          }
+        }
+        jx = jy;
+        if (!done && tok + jy == ev) join();  // an event inside (or at the end of) the stage
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      s += a.G;
+      if (s >= a.NSTG) s -= a.NSTG, ph ^= 1u;
+    }
+    while (!done) join();  // the events after this group's last stage
+    seq0 += ns;
+  }
+  pdl_trigger();
+}
+
 // Generic kernel (u8/u16/u32 ids, any alignment, any E up to ~51k): work
 // items are (token chunk, layer group) pairs; per item the block processes
 // every request piece (request r intersected with the chunk) into one shared
@@ -299,11 +556,93 @@ uint64_t chunk_tokens(uint64_t T, uint32_t NG, uint64_t slots, uint64_t cap) {
   return std::max<uint64_t>(1, std::min<uint64_t>(ts, cap));
 }
 
+// k_trace_lane's shape: u8 ids, an even number of ids per token, E <= 256 and
+// the private counters in shared memory; requests of at least 16 tokens on
+// average (each piece costs one L x E reduction).  MOE_TRACE_LANE=0 disables
+// it (A/B runs).
+bool lane_config(uint64_t T, uint32_t L, uint32_t E, uint32_t k, uint64_t R, int n_sm, LaneArgs* a,
+                 size_t* smem, unsigned* grid) {
+  static const bool off = [] {
+    const char* e = getenv("MOE_TRACE_LANE");
+    return e && e[0] == '0';
+  }();
+  const uint32_t Lk = L * k;
+  if (off || Lk == 0 || Lk % 2 || E == 0 || E > 256 || T < 16 * R) return false;
+  const size_t kMax = 227u * 1024u;
+  constexpr uint32_t kMaxWarps = 19;  // consumer warps (+ the producer warp: <= 640 threads)
+  const uint32_t H = Lk / 2, ES = E | 1;
+  if (H > kMaxWarps * 32) return false;
+  // a group: the warps holding every position pair once (several token phases
+  // when a warp holds more than H lanes); columns are shared by the groups
+  const uint32_t NWg = (H + 31) / 32, TPg = NWg * 32 / H;
+  const uint32_t C = H >= 32 ? H : H * TPg;
+  const uint32_t NCOL = (C + 31) / 32 * 32;
+  const size_t cnt_b = (size_t)(E + 2) * NCOL * 4;  // + the trash and null rows
+  const size_t out_b = (((size_t)L * ES + 1) & ~(size_t)1) * 4;
+  const size_t fixed = cnt_b + out_b;
+  const uint32_t UT = LANE_U * TPg;  // tokens of one unrolled round of every phase
+  const size_t sb_min = (((size_t)UT * Lk + 32) + 127) & ~(size_t)127;
+  if (fixed + 2 * (sb_min + 16) + 256 > kMax) return false;
+  const size_t ring = kMax - fixed - 256;
+  // groups: as many as the warp budget allows with two ring slots each
+  uint32_t G = std::max<uint32_t>(1, kMaxWarps / NWg);
+  while (G > 1 && 2 * (size_t)G * (sb_min + 16) > ring) --G;
+  // tokens per stage: <= 16 KB, two slots per group
+  const size_t sb_max = std::min<size_t>(16384 + 160, ring / (2 * G) - 16);
+  uint32_t TW = (uint32_t)std::max<size_t>(UT, (sb_max - 160) / Lk / UT * UT);
+  const uint32_t SB = (uint32_t)((((size_t)TW * Lk + 32) + 127) & ~(size_t)127);
+  const uint32_t NSTG = (uint32_t)std::min<size_t>(32, ring / (SB + 16));
+  if (NSTG < G) return false;
+  *smem = (size_t)NSTG * SB + fixed + 16 * (size_t)NSTG;
+  *grid = (unsigned)n_sm;  // one block per SM
+  // one item per block (equal token counts; each piece costs one reduction)
+  uint64_t TS = (T + *grid - 1) / *grid;
+  TS = std::min<uint64_t>(std::max<uint64_t>(TS, TW), 65535);
+  *grid = (unsigned)std::min<uint64_t>(*grid, (T + TS - 1) / TS);
+  a->T = T;
+  a->TS = TS;
+  a->R = R;
+  a->L = L;
+  a->E = E;
+  a->k = k;
+  a->H = H;
+  a->TPg = TPg;
+  a->NWg = NWg;
+  a->G = G;
+  a->C = C;
+  a->NCOL = NCOL;
+  a->TW = TW;
+  a->NSTG = NSTG;
+  a->SB = SB;
+  return true;
+}
+
 template <typename OUT>
 cudaError_t launch_trace_t(const void* topk, int idx_bytes, uint64_t T, uint32_t L, uint32_t E,
                            uint32_t k, const uint64_t* offsets, uint64_t R, OUT* counts, int* bad,
                            int n_sm, cudaStream_t st) {
   if (T == 0 || R == 0) return cudaSuccess;
+  if (idx_bytes == 1) {
+    LaneArgs a;
+    size_t smem;
+    unsigned grid;
+    if (lane_config(T, L, E, k, R, n_sm, &a, &smem, &grid) &&
+        (reinterpret_cast<uintptr_t>(topk) & 1) == 0) {
+      a.topk = static_cast<const uint8_t*>(topk);
+      a.offsets = offsets;
+      a.bad = bad;
+      static size_t set = 0;
+      cudaError_t e = raise_smem(k_trace_lane<OUT>, smem, &set);
+      if (e != cudaSuccess) return e;
+      const unsigned threads = a.G * a.NWg * 32 + 32;
+      e = launch_pdl(k_trace_lane<OUT>, dim3(grid), dim3(threads), smem, st, a, counts, (int)kRun, 1);
+      if (e == cudaSuccess)  // rollback: any grid subtracts the same sums
+        e = launch_pdl(k_trace_lane<OUT>, dim3(std::min<unsigned>(grid, 16)), dim3(threads), smem,
+                       st, a, counts, (int)kIfBad, -1);
+      if (e != cudaSuccess) return e;
+      return cudaGetLastError();
+    }
+  }
   const uint32_t Lk = L * k;
   uint64_t min_len = 0;  // requests the generic kernel leaves to k_trace_own
   void (*own)(const uint8_t*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, const uint64_t*,

@@ -32,7 +32,7 @@ def main():
           "and at ncu's clocks; the bench's CUDA-event times are the timing of record).", ""]
     summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
     keys = {"sc_batch_screen": "sc_batch_screen", "sc_screen": "sc_screen", "sw_screen": "sw_screen",
-            "trace_own": "k_trace_own", "decision": "k_decision"}
+            "trace_lane": "k_trace_lane", "decision": "k_decision"}
     for f, key in keys.items():
         rep = os.path.join(P, f + ".ncu-rep")
         if not os.path.exists(rep):

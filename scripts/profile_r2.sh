@@ -14,8 +14,8 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_tc
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_tci8 -s 3 -c 1 \
   -o $O/sc_screen python scripts/sweep_match.py --qs 8 --reps 2 > /dev/null 2>&1
 # K1 tracing
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_trace_own -s 2 -c 1 \
-  -o $O/trace_own env TRACE_ITERS=2 python scripts/trace_probe.py > /dev/null 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_trace_lane -s 2 -c 1 \
+  -o $O/trace_lane env TRACE_ITERS=2 python scripts/trace_probe.py > /dev/null 2>&1
 # decision kernel (DS P=10k)
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_decision -s 60 -c 3 \
   -o $O/decision env REPS=1 python scripts/ds_probe.py > /dev/null 2>&1
