@@ -281,12 +281,16 @@ __device__ __forceinline__ void lane_flush(const LaneArgs& a, uint32_t* cnt, uin
     const uint32_t de = NC / L, dl = NC - de * L;
     uint32_t e = t / L, l = t - e * L;
     const uint32_t CM = a.C / a.H;  // columns per position pair
-    if (CM == 1 && (k & 1) == 0) {  // whole words per layer, one column each
+    if (CM == 1 && (k & 1) == 0 && k <= 8) {  // whole words per layer, one column each
       const uint32_t kh = k >> 1;
       for (; e < E;) {
         const uint32_t* cw = cnt + e * NCOL + l * kh;
+        uint32_t c[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) c[w] = w < (int)kh ? cw[w] : 0u;
         uint32_t sum = 0;
-        for (uint32_t w = 0; w < kh; ++w) sum += (cw[w] & 0xffffu) + (cw[w] >> 16);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) sum += (c[w] & 0xffffu) + (c[w] >> 16);
         stage_out[l * ES + e] = sum;
         l += dl;
         e += de;
@@ -316,10 +320,16 @@ __device__ __forceinline__ void lane_flush(const LaneArgs& a, uint32_t* cnt, uin
   for (uint32_t i = t; i < (E + 2) * NCOL / 4; i += NC)
     reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
   // reductions without a return value: no thread waits on the counts' latency
-  for (uint32_t i = t; i < L * E; i += NC) {
-    const uint32_t l = i / E;
-    const uint32_t v = stage_out[l * ES + (i - l * E)];
-    if (v) add_out(dst + i, v, sign, false);
+  {
+    const uint32_t dl = NC / E, de = NC - dl * E;
+    uint32_t l = t / E, e = t - l * E;
+    for (uint32_t i = t; i < L * E; i += NC) {
+      const uint32_t v = stage_out[l * ES + e];
+      if (v) add_out(dst + i, v, sign, false);
+      l += dl;
+      e += de;
+      if (e >= E) e -= E, ++l;
+    }
   }
   consumers_sync(NC);
 }
@@ -395,30 +405,32 @@ __global__ void __launch_bounds__(640, 1) k_trace_lane(LaneArgs a, OUT* __restri
       r = l0;
     }
     uint64_t rend = a.offsets[r + 1];
-    uint64_t ev = min(rend, tb);  // the next event
-    bool done = false;            // the item-end event has been joined
+    // item-relative token offsets fit in 32 bits (items hold <= 65,535 tokens)
+    const uint32_t len = (uint32_t)(tb - ta);
+    const uint32_t ib = (uint32_t)(base + ta * Lk);  // low bits of the item's first byte address
+    uint32_t evr = (uint32_t)(min(rend, tb) - ta);   // the next event
+    bool done = false;                                // the item-end event has been joined
     // join the next event: reduce the piece of request r, step to the next request
     auto join = [&]() {
       lane_flush<OUT>(a, cnt, stage_out, NC, counts + r * (uint64_t)L * E, sign);
-      if (ev == tb) done = true;
-      if (ev == rend) {  // next non-empty request
-        while (r + 1 < a.R && a.offsets[r + 2] <= ev) ++r;
+      if (evr == len) done = true;
+      if (ta + evr == rend) {  // next non-empty request
+        while (r + 1 < a.R && a.offsets[r + 2] <= rend) ++r;
         ++r;
         rend = r < a.R ? a.offsets[r + 1] : hi;
       }
-      ev = min(rend, tb);
+      evr = (uint32_t)(min(rend, tb) - ta);
     };
-    const uint32_t ns = (uint32_t)((tb - ta + a.TW - 1) / a.TW);
+    const uint32_t ns = (len + a.TW - 1) / a.TW;
     uint32_t s = (seq0 + g) % a.NSTG, ph = ((seq0 + g) / a.NSTG) & 1u;
-    for (uint32_t kst = g; kst < ns; kst += a.G) {
-      const uint64_t tok = ta + (uint64_t)kst * a.TW;
-      const uint32_t n = (uint32_t)min((uint64_t)a.TW, tb - tok);  // tokens in this stage
-      while (!done && ev <= tok) join();  // events before the stage
+    for (uint32_t kst = g, tr = g * a.TW; kst < ns; kst += a.G, tr += a.G * a.TW) {
+      const uint32_t n = min(a.TW, len - tr);  // tokens in this stage
+      while (!done && evr <= tr) join();      // events before the stage
       mbar_wait(&full[s], ph);
-      const uint8_t* sb = ring + (size_t)s * a.SB + ((base + tok * Lk) & 15) + 2u * q;
+      const uint8_t* sb = ring + s * a.SB + ((ib + tr * Lk) & 15u) + 2u * q;
       uint32_t jx = 0;
       while (jx < n) {
-        const uint32_t jy = ev - tok < n ? (uint32_t)(ev - tok) : n;
+        const uint32_t jy = min(evr - tr, n);
         if (act) {  // stage-local tokens j in [jx, jy), phase tp takes j = tp (mod TPg)
           uint32_t j = jx == 0 ? tp : jx + (tp + a.TPg - jx % a.TPg) % a.TPg;
           const uint8_t* pj = sb + j * Lk;
@@ -450,7 +462,7 @@ __global__ void __launch_bounds__(640, 1) k_trace_lane(LaneArgs a, OUT* __restri
           }
         }
         jx = jy;
-        if (!done && tok + jy == ev) join();  // an event inside (or at the end of) the stage
+        if (!done && tr + jy == evr) join();  // an event inside (or at the end of) the stage
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -586,13 +598,14 @@ bool lane_config(uint64_t T, uint32_t L, uint32_t E, uint32_t k, uint64_t R, int
   const size_t ring = kMax - fixed - 256;
   // groups: as many as the warp budget allows with two ring slots each
   uint32_t G = std::max<uint32_t>(1, kMaxWarps / NWg);
-  while (G > 1 && 2 * (size_t)G * (sb_min + 16) > ring) --G;
-  // tokens per stage: <= 16 KB, two slots per group
-  const size_t sb_max = std::min<size_t>(16384 + 160, ring / (2 * G) - 16);
+  while (G > 1 && (size_t)(G + 1) * (sb_min + 16) > ring) --G;
+  // tokens per stage: <= 24 KB, at least G + 1 slots (measured at DS: 48-token
+  // stages in 4 slots beat 32-token stages in 6 and 16-token stages in 12)
+  const size_t sb_max = std::min<size_t>(24576 + 160, ring / (G + 1) - 16);
   uint32_t TW = (uint32_t)std::max<size_t>(UT, (sb_max - 160) / Lk / UT * UT);
   const uint32_t SB = (uint32_t)((((size_t)TW * Lk + 32) + 127) & ~(size_t)127);
   const uint32_t NSTG = (uint32_t)std::min<size_t>(32, ring / (SB + 16));
-  if (NSTG < G) return false;
+  if (NSTG < G + 1) return false;
   *smem = (size_t)NSTG * SB + fixed + 16 * (size_t)NSTG;
   *grid = (unsigned)n_sm;  // one block per SM
   // one item per block (equal token counts; each piece costs one reduction)
