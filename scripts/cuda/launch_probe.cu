@@ -6,6 +6,13 @@
 #include <cuda_runtime.h>
 struct Big { char b[800]; };
 struct Big1k { alignas(16) char b[1100]; };
+struct Big10k { alignas(16) char b[10240]; };
+__global__ void __launch_bounds__(256, 1) k_gc10(const __grid_constant__ Big10k a, int* p) {
+  __shared__ int st[2560];
+  for (int i = threadIdx.x; i < 2560; i += blockDim.x) st[i] = reinterpret_cast<const int*>(a.b)[i];
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x == 0 && p) *p = st[7];
+}
 __global__ void __launch_bounds__(256, 1) k_gc(const __grid_constant__ Big1k a, int* p) {
   extern __shared__ int s[];
   __shared__ int st[4000];
@@ -68,5 +75,14 @@ int main() {
     k_gc<<<31, 256, 4 * 1024, st>>>(b1, d);
   }, st);
   timeit("1.1KB gc, host-mapped out", [&] { k_gc<<<31, 256, 4 * 1024, st>>>(b1, hp); }, st);
+  static Big10k b10 = {};
+  timeit("10KB gc params 148x256", [&] { k_gc10<<<148, 256, 0, st>>>(b10, d); }, st);
+  char* hpin; cudaMallocHost(&hpin, 16384);
+  char* dbuf; cudaMalloc(&dbuf, 16384);
+  timeit("10KB H2D memcpy + 1.1KB launch", [&] {
+    cudaMemcpyAsync(dbuf, hpin, 9440, cudaMemcpyHostToDevice, st);
+    k_gc<<<148, 256, 4 * 1024, st>>>(b1, d);
+  }, st);
+  timeit("1.1KB gc 148x256 alone", [&] { k_gc<<<148, 256, 4 * 1024, st>>>(b1, d); }, st);
   return 0;
 }
