@@ -600,7 +600,9 @@ bool lane_config(uint64_t T, uint32_t L, uint32_t E, uint32_t k, uint64_t R, int
   uint32_t G = std::max<uint32_t>(1, kMaxWarps / NWg);
   while (G > 1 && (size_t)(G + 1) * (sb_min + 16) > ring) --G;
   // tokens per stage: <= 24 KB, at least G + 1 slots (measured at DS: 48-token
-  // stages in 4 slots beat 32-token stages in 6 and 16-token stages in 12)
+  // stages in 4 slots beat 32-token stages in 6 and 16-token stages in 12; one
+  // group of 18 warps with 3 token phases per stage instead of 3 groups: 0.177
+  // vs 0.153 ms)
   const size_t sb_max = std::min<size_t>(24576 + 160, ring / (G + 1) - 16);
   uint32_t TW = (uint32_t)std::max<size_t>(UT, (sb_max - 160) / Lk / UT * UT);
   const uint32_t SB = (uint32_t)((((size_t)TW * Lk + 32) + 127) & ~(size_t)127);
