@@ -344,7 +344,10 @@ moe_status moe_eam_trace(const moe_shape* shape, const void* topk_idx, int idx_b
  * [R][L][E] accumulated.  *bad_index_flag must be 0 on entry; an index >= E
  * leaves it 1 and counts_u32 as it was (the call's additions are rolled back
  * on the device).  Calls on different streams share no scratch memory.
- * Request offsets must lie within [0, n_tokens]. */
+ * Request offsets must lie within [0, n_tokens].  u8 ids are read in aligned
+ * 16-byte granules, so up to 15 bytes past either end of the id buffer (in
+ * the granules holding its first and last byte, never another page) may be
+ * read; they are never counted. */
 moe_status moe_eam_trace_device(const moe_shape* shape, const void* topk_idx, int idx_bytes,
                                 uint64_t n_tokens, const uint64_t* offsets, uint64_t n_requests,
                                 uint32_t* counts_u32, int* bad_index_flag, void* stream);
