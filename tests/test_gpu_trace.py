@@ -1,5 +1,6 @@
 """K1 tracing (Eam::record, eam.cpp:41-52, per token as workload.cpp:166-181)
-against the oracle at scale: the lane-copy u8 kernel and the generic kernel,
+against the oracle at scale: the lane (bank-locked counters), request-owned
+and generic kernels,
 ragged / empty / multi-chunk requests, counts that overflow the 16-bit lane
 copies within a request, the device rollback that makes a failed call
 all-or-nothing (eam.cpp:42-47), concurrent calls on two streams, and shapes
@@ -61,6 +62,9 @@ def _device_trace(shape, picks_t, offs, counts_t, bad_t, stream):
     (1, 256, 1, 30_000, 3),      # E = 256: every byte is a valid id
     (7, 40, 3, 41_000, 4),       # odd L, L*k = 21
     (3, 5, 5, 9_000, 5),         # k = E, strided picks: duplicate ids inside a (token, layer)
+    (22, 64, 3, 30_000, 9),      # k odd, L*k even: position pairs straddle layers (lane kernel)
+    (4, 256, 2, 20_000, 6),      # E = 256 on the lane kernel (no trash ids)
+    (59, 160, 6, 3_000, 400),    # short requests (< 16 tokens on average): k_trace_own
 ])
 def test_trace_ragged_vs_oracle(m, orc, L, E, k, T, R):
     rng = np.random.default_rng(L * 1000 + E)
@@ -201,4 +205,28 @@ def test_sharded_tracer_device_steps(m, orc, world):
         tr.trace(torch.from_numpy(np.ascontiguousarray(picks[t0:t1])).cuda(), T, offs, counts,
                  stream=st)
     st.synchronize()
+    assert np.array_equal(counts.cpu().numpy().astype(np.uint64), want)
+
+
+def test_trace_unaligned_ids(m, orc):
+    """A u8 id stream starting at an odd address (the lane kernel needs 2-byte
+    alignment, k_trace_own 16): the generic kernel takes it, results exact."""
+    import torch
+    L, E, k, T = 59, 160, 6, 20_000
+    rng = np.random.default_rng(8)
+    picks = _picks(rng, T, L, E, k).astype(np.uint8)
+    offs = np.linspace(0, T, 9).astype(np.uint64)
+    rc, want = orc.trace(L, E, k, picks.astype(np.uint32), offs)
+    assert rc == 0
+    buf = torch.zeros(picks.size + 1, dtype=torch.uint8, device="cuda")
+    buf[1:] = torch.from_numpy(picks.reshape(-1)).cuda()
+    view = buf[1:].view(T, L, k)
+    assert view.data_ptr() % 2 == 1
+    counts = torch.zeros((len(offs) - 1, L, E), dtype=torch.int32, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = torch.cuda.Stream()
+    keep = _device_trace(m.ModelShape(L, E, k), view, offs, counts, bad, st)
+    st.synchronize()
+    del keep
+    assert int(bad.item()) == 0
     assert np.array_equal(counts.cpu().numpy().astype(np.uint64), want)
