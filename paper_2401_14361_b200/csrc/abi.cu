@@ -1648,10 +1648,12 @@ static moe_status dec_scratch(moe_eamc* h, uint64_t n_slots) {
   CK(h->did.ensure(cells * 4));
   CK(h->drank.ensure(cells * 4));
   CK(h->dseg.ensure((size_t)c.L * 4));
-  if (!h->dstate.p) {  // dmin2[2] = ~0 (then self-cleaning by call parity), barrier = 0
-    CK(h->dstate.ensure(64));
-    CK(cudaMemsetAsync(h->dstate.p, 0xff, 16, h->st));
-    CK(cudaMemsetAsync(h->dstate.as<uint8_t>() + 16, 0, 16, h->st));
+  CK(h->dmlist.ensure(n * 4));
+  if (!h->dstate.p) {  // dmin2[2] = ~0 (then self-cleaning by call parity), barriers and
+                       // listed-member counts = 0
+    CK(h->dstate.ensure(64));  // synchronous: device-step calls run on the caller's stream
+    CK(cudaMemset(h->dstate.p, 0xff, 16));
+    CK(cudaMemset(h->dstate.as<uint8_t>() + 16, 0, 48));
     h->bar_base = h->bar_base2 = 0;
   }
   CK(h->cpin.ensure(std::max<uint64_t>(cells, 1) * sizeof(moe_candidate)));
@@ -1698,7 +1700,7 @@ static moe_status server_launch(moe_eamc* h) {
   const DevColl& c = h->c;
   uint32_t np = 1;
   while (np < c.E) np <<= 1;
-  v.smem = std::max<size_t>((size_t)c.L * c.RB, (size_t)np * 28);
+  v.smem = std::max({(size_t)c.L * c.RB, (size_t)np * 28, moe::decision_smem(c.L, c.E, c.RB, 0, 0, 1)});
   CK(v.drows.ensure((size_t)c.L * c.RB + 2 * c.L + 32));
   v.cb = c.cb;
   auto* ctl = v.ctl.as<moe::DecServerCtl>();
@@ -1777,6 +1779,8 @@ static moe_status run_decision(moe_eamc* h, moe::DecisionArgs& a, size_t stage_r
   a.window = 0.01;  // kMatchWindow (policy.hpp:30)
   a.dmin2 = h->dstate.as<unsigned long long>();
   a.agg = h->agg.as<unsigned long long>();
+  a.mcount = reinterpret_cast<uint32_t*>(h->dstate.as<uint8_t>() + 24);
+  a.mlist = h->dmlist.as<uint32_t>();
   a.ckey = h->dkey.as<unsigned long long>();
   a.cid = h->did.as<uint32_t>();
   a.crank = h->drank.as<uint32_t>();

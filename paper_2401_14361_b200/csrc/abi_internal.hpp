@@ -188,7 +188,7 @@ struct moe_eamc {
   moe::abi::DevBuf rdc, rdx, rocc;  // blocked construction replay: screen matrices, slot occupants
   std::vector<uint8_t> dec_rows;
   std::vector<uint16_t> dec_nz;
-  moe::abi::DevBuf dkey, did, drank, dseg, dstate, xdev, tprobe;  // fused decision: survivor list, parity state, explicit rows
+  moe::abi::DevBuf dkey, did, drank, dseg, dstate, xdev, tprobe, dmlist;  // fused decision: survivor list, parity state, explicit rows
   moe::abi::PinBuf fpin, xpin;               // n_out / victim (host-mapped), explicit-row staging
   moe::DecisionArgs dargs{};
   uint64_t dec_calls = 0;

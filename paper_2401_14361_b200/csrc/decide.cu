@@ -89,6 +89,14 @@ __device__ __forceinline__ void grid_barrier(const DecisionArgs& a, uint32_t k) 
   __syncthreads();
 }
 
+// Arrival without the wait: a barrier index every CTA passes but whose
+// condition (no listed window members) needs no rendezvous; the arrival keeps
+// the counter's targets base + k*G of the later barriers.
+__device__ __forceinline__ void grid_arrive(const DecisionArgs& a) {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
+}
+
 __device__ __forceinline__ void stamp(const DecisionArgs& a, int i) {
   if (a.tprobe && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
@@ -103,6 +111,110 @@ template <bool PS, typename T>
 __device__ __forceinline__ T ld_ro(const T* p) {
   if constexpr (PS) return __ldcg(p);
   else return __ldg(p);
+}
+
+// Column-split window aggregation over the listed members: CTA b owns the
+// 16-byte chunks [q0, q1) of every member's rows above the current layer;
+// thread (chunk j, member group g) accumulates its group's members (u8 counts
+// in 16-bit SWAR lanes, widened every 256 members; wider counts in u64), the
+// groups are reduced in shared memory (>= 16 KB of dsm) and each nonzero cell
+// is added into agg with one atomic.
+template <int CB, bool PS>
+__device__ __forceinline__ void list_sum(const DecisionArgs& a, uint8_t* red, uint32_t NL,
+                                         uint32_t rows_above) {
+  const uint32_t tid = threadIdx.x, b = blockIdx.x, G = gridDim.x;
+  const uint32_t E = a.E, RB = a.RB;
+  const uint64_t LR = (uint64_t)a.L * RB;
+  const uint32_t W4 = rows_above * (RB / 16);  // 16-byte chunks per member
+  const uint32_t q0 = (uint32_t)((uint64_t)W4 * b / G), q1 = (uint32_t)((uint64_t)W4 * (b + 1) / G);
+  const uint32_t nq = q1 - q0;
+  if (nq == 0) return;
+  constexpr uint32_t NPC = 16 / CB;  // counts per chunk
+  const uint32_t ngr = kDecThreads / nq >= 1 ? kDecThreads / nq : 1;
+  const uint32_t j = tid % nq, g = tid / nq;
+  const bool act = nq <= kDecThreads ? g < ngr : tid < nq;
+  uint64_t tot[NPC];
+#pragma unroll
+  for (uint32_t c = 0; c < NPC; ++c) tot[c] = 0;
+  const uint8_t* rbase = a.counts + (uint64_t)(a.cur + 1) * RB;
+  if (act) {
+    for (uint32_t jj = j; jj < nq; jj += (nq <= kDecThreads ? nq : kDecThreads)) {
+      const uint32_t q = q0 + jj;
+      if (CB == 1) {
+        for (uint32_t m0 = g; m0 < NL; m0 += 256 * ngr) {  // <= 256 members per widening
+          uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          const uint32_t m1 = min(NL, m0 + 256 * ngr);
+          uint32_t m = m0;
+          constexpr int U = 8;  // loads in flight per thread
+          for (; m + (U - 1) * ngr < m1; m += U * ngr) {
+            uint32_t mi[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) mi[u] = __ldcg(a.mlist + m + u * ngr);
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              v[u] = ld_ro<PS>(reinterpret_cast<const uint4*>(rbase + (uint64_t)mi[u] * LR) + q);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                acc[2 * k] += w[k] & 0x00ff00ffu;
+                acc[2 * k + 1] += (w[k] >> 8) & 0x00ff00ffu;
+              }
+            }
+          }
+          for (; m < m1; m += ngr) {
+            const uint4 v = ld_ro<PS>(reinterpret_cast<const uint4*>(rbase + (uint64_t)__ldcg(a.mlist + m) * LR) + q);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              acc[2 * k] += w[k] & 0x00ff00ffu;
+              acc[2 * k + 1] += (w[k] >> 8) & 0x00ff00ffu;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // byte 4k+i of the chunk: lane (i&1) of acc[2k + (i>>1)]
+            tot[4 * k + 0] += acc[2 * k] & 0xffffu;
+            tot[4 * k + 2] += acc[2 * k] >> 16;
+            tot[4 * k + 1] += acc[2 * k + 1] & 0xffffu;
+            tot[4 * k + 3] += acc[2 * k + 1] >> 16;
+          }
+        }
+      } else {
+        for (uint32_t m = g; m < NL; m += ngr) {
+          const uint4 v = ld_ro<PS>(reinterpret_cast<const uint4*>(rbase + (uint64_t)__ldcg(a.mlist + m) * LR) + q);
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (uint32_t c = 0; c < NPC; ++c)
+            tot[c] += CB == 2 ? (w[c >> 1] >> (16 * (c & 1))) & 0xffffu : w[c];
+        }
+      }
+      if (nq > kDecThreads) {  // one thread per chunk: add directly
+#pragma unroll
+        for (uint32_t c = 0; c < NPC; ++c) {
+          const uint32_t off = q * 16 + c * CB, r = off / RB, e = (off - r * RB) / CB;
+          if (tot[c] && e < E) atomicAdd(&a.agg[(uint64_t)(a.cur + 1 + r) * E + e], (unsigned long long)tot[c]);
+          tot[c] = 0;
+        }
+      }
+    }
+  }
+  if (nq > kDecThreads) return;
+  // reduce the member groups: red[g][j][c] (u64), then one thread per cell
+  unsigned long long* rs = reinterpret_cast<unsigned long long*>(red);
+  __syncthreads();
+  if (act)
+#pragma unroll
+    for (uint32_t c = 0; c < NPC; ++c) rs[((uint64_t)g * nq + j) * NPC + c] = tot[c];
+  __syncthreads();
+  for (uint32_t cell = tid; cell < nq * NPC; cell += kDecThreads) {
+    unsigned long long sum = 0;
+    for (uint32_t gg = 0; gg < ngr; ++gg) sum += rs[(uint64_t)gg * nq * NPC + cell];
+    const uint32_t jj = cell / NPC, c = cell - jj * NPC;
+    const uint32_t off = (q0 + jj) * 16 + c * CB, r = off / RB, e = (off - r * RB) / CB;
+    if (sum && e < E) atomicAdd(&a.agg[(uint64_t)(a.cur + 1 + r) * E + e], sum);
+  }
 }
 
 template <int CB, bool PS>
@@ -226,6 +338,16 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
       if (p < p1 && a.dist[p] <= thr) mem_s[atomicAdd(&n_mem, 1u)] = p;
       __syncthreads();
       const uint32_t nm = n_mem;
+      // many members x rows: listed, summed column-split below (one atomic per
+      // nonzero count is cheaper only for a few members)
+      if (a.mcount && (uint64_t)nm * rows_above * wpr > kDecListWords) {
+        __shared__ uint32_t moff;
+        if (tid == 0) moff = atomicAdd(a.mcount, nm);
+        __syncthreads();
+        for (uint32_t i = tid; i < nm; i += kDecThreads) a.mlist[moff + i] = mem_s[i];
+        __syncthreads();
+        continue;
+      }
       const uint32_t per_mem = rows_above * wpr;
       for (uint32_t it = tid; it < nm * per_mem; it += kDecThreads) {
         const uint32_t mi = it / per_mem, rem = it - mi * per_mem;
@@ -246,8 +368,19 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
       __syncthreads();
     }
   }
-  stamp(a, 3);
   grid_barrier(a, 2);
+  stamp(a, 3);
+  // listed members (wide windows, e.g. the first layers of a decode step): CTA
+  // b sums a slice of the rows-above region over every listed member -- its
+  // own cells, coalesced 16-byte loads, no per-count atomics -- and adds its
+  // nonzero cells into agg once
+  const uint32_t NL = (a.do_agg && rows_above && a.mcount) ? __ldcg(a.mcount) : 0u;
+  if (NL) {
+    list_sum<CB, PS>(a, reinterpret_cast<uint8_t*>(dsm), NL, rows_above);
+    grid_barrier(a, 3);
+  } else {
+    grid_arrive(a);
+  }
   stamp(a, 4);
 
   // ---- phase C1: per layer i > l: priorities, floor filter, sorted segment --
@@ -387,7 +520,7 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
     }
   }
   stamp(a, 5);
-  grid_barrier(a, 3);
+  grid_barrier(a, 4);
   stamp(a, 6);
 
   // ---- phase C2: cross-layer ranks -----------------------------------------
@@ -414,7 +547,80 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
   __syncthreads();
   const uint32_t S = offs[rows_above];
   if (b == 0 && tid == 0) *a.n_out = S;
-  {
+  // many survivors (wide windows: every expert scores): every CTA stages the
+  // whole sorted list and ranks its own share of the survivors against every
+  // layer, (survivor, layer) pairs spread over the threads, then writes them
+  // out -- no per-pair global atomics, no C3 pass
+  uint32_t dsm_bytes;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm_bytes));
+  const bool staged = S > kDecStagedMin && (size_t)S * 12 <= dsm_bytes;
+  if (staged) {
+    unsigned long long* tk = reinterpret_cast<unsigned long long*>(dsm);
+    uint32_t* ti = reinterpret_cast<uint32_t*>(tk + S);
+    __shared__ uint32_t rk[kDecThreads];
+    // 12 survivors' loads in flight per thread; CTA b starts at its own offset
+    // so the CTAs do not all request the same lines at once
+    const uint32_t rot = (uint32_t)((uint64_t)S * b / G);
+    for (uint32_t i0 = tid; i0 < S; i0 += 12 * kDecThreads) {
+      unsigned long long kk[12];
+      uint32_t ii[12];
+#pragma unroll
+      for (int u = 0; u < 12; ++u) {
+        const uint32_t j = i0 + u * kDecThreads;
+        if (j >= S) break;
+        const uint32_t i = j + rot < S ? j + rot : j + rot - S;
+        uint32_t li = 0, hi2 = rows_above;  // segment of i
+        while (hi2 - li > 1) {
+          const uint32_t mid = (li + hi2) >> 1;
+          if (offs[mid] <= i) li = mid; else hi2 = mid;
+        }
+        const uint64_t slot = (uint64_t)li * E + (i - offs[li]);
+        kk[u] = __ldcg(a.ckey + slot);
+        ii[u] = __ldcg(a.cid + slot);
+      }
+#pragma unroll
+      for (int u = 0; u < 12; ++u) {
+        const uint32_t j = i0 + u * kDecThreads;
+        if (j >= S) break;
+        const uint32_t i = j + rot < S ? j + rot : j + rot - S;
+        tk[i] = kk[u];
+        ti[i] = ii[u];
+      }
+    }
+    __syncthreads();
+    const uint32_t s0 = (uint32_t)((uint64_t)S * b / G), s1 = (uint32_t)((uint64_t)S * (b + 1) / G);
+    for (uint32_t c0 = s0; c0 < s1; c0 += kDecThreads) {  // chunks of <= kDecThreads survivors
+      const uint32_t nc = min(kDecThreads, s1 - c0);
+      if (tid < nc) {  // own position in its layer
+        const uint32_t t = c0 + tid;
+        uint32_t li = 0, hi2 = rows_above;
+        while (hi2 - li > 1) {
+          const uint32_t mid = (li + hi2) >> 1;
+          if (offs[mid] <= t) li = mid; else hi2 = mid;
+        }
+        rk[tid] = t - offs[li];
+      }
+      __syncthreads();
+      // layer-major pairs: the lanes of a warp search one segment (broadcast
+      // reads) for different survivors (distinct rank counters)
+      for (uint32_t pr = tid; pr < nc * rows_above; pr += kDecThreads) {
+        const uint32_t lj = pr / nc, u = pr - lj * nc;
+        const uint32_t t = c0 + u;
+        if (t >= offs[lj] && t < offs[lj + 1]) continue;  // its own layer
+        const unsigned long long kx = tk[t];
+        const uint32_t ix = ti[t];
+        uint32_t lo = offs[lj], hb = offs[lj + 1];  // count of (tk, ti) < (kx, ix)
+        while (lo < hb) {
+          const uint32_t mid = (lo + hb) >> 1;
+          if (pair_lt(tk[mid], ti[mid], kx, ix)) lo = mid + 1; else hb = mid;
+        }
+        if (lo > offs[lj]) atomicAdd(&rk[u], lo - offs[lj]);
+      }
+      __syncthreads();
+      if (tid < nc) a.crank[rk[tid]] = c0 + tid;  // the inverse: output position -> survivor
+      __syncthreads();
+    }
+  } else {
     unsigned long long* tk = reinterpret_cast<unsigned long long*>(dsm);
     uint32_t* ti = reinterpret_cast<uint32_t*>(tk + E);
     for (uint32_t lj = b; lj < rows_above; lj += G) {
@@ -462,9 +668,27 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
     }
   }
   stamp(a, 7);
-  grid_barrier(a, 4);
+  grid_barrier(a, 5);
+  // every CTA has read the listed-member count (barrier 3 < 5): clean it for
+  // the next call, whatever path that takes
+  if (b == 0 && tid == 0 && a.mcount) *a.mcount = 0u;
 
-  // ---- phase C3: scatter to the output positions ----------------------------
+  // ---- phase C3: the output ------------------------------------------------
+  // staged: CTA b writes output positions [b*S/G, (b+1)*S/G) in order from its
+  // staged copy (contiguous stores: whole bursts to host-mapped memory)
+  if (staged) {
+    const unsigned long long* tk = reinterpret_cast<const unsigned long long*>(dsm);
+    const uint32_t* ti = reinterpret_cast<const uint32_t*>(tk + S);
+    const uint32_t r0 = (uint32_t)((uint64_t)S * b / G), r1 = (uint32_t)((uint64_t)S * (b + 1) / G);
+    for (uint32_t r = r0 + tid; r < r1; r += kDecThreads) {
+      const uint32_t t = __ldcg(a.crank + r), id = ti[t];
+      moe_candidate o;
+      o.layer_idx = id / E;
+      o.expert_idx = id - o.layer_idx * E;
+      o.priority = __longlong_as_double((long long)~tk[t]);
+      a.out[r] = o;
+    }
+  } else
   for (uint32_t li = b; li < rows_above; li += G)
   for (uint32_t pos = tid; pos < offs[li + 1] - offs[li]; pos += kDecThreads) {
     const uint64_t slot = (uint64_t)li * E + pos;
@@ -885,13 +1109,15 @@ cudaError_t launch_decision_small(const DecisionArgs& a, int cb, size_t smem, cu
 
 size_t decision_smem(uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz, uint32_t cur,
                      uint32_t grid) {
-  (void)L;
-  (void)cur;
   (void)grid;
   uint32_t np = 1;
   while (np < E) np <<= 1;
-  // staged probe rows | a layer's slots + its compacted survivors
-  return std::max((size_t)n_nz * RB, (size_t)np * 28);
+  // staged probe rows | a layer's slots + its compacted survivors | the listed
+  // members' group reduction (one u64 per count of a 16-byte chunk per thread)
+  // | the staged survivor list (12 bytes per candidate, C2 with many survivors)
+  const size_t rows = cur + 1 < L ? L - cur - 1 : 0;
+  return std::max({(size_t)n_nz * RB, (size_t)np * 28, (size_t)kDecThreads * 16 * 8,
+                   std::min<size_t>(rows * E * 12, 160 * 1024)});
 }
 
 int decision_grid(int n_sm, uint32_t size, uint32_t L, uint32_t cur) {

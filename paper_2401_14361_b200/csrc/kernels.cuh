@@ -152,7 +152,9 @@ cudaError_t launch_member_agg(const DevColl& c, const double* dist,
 constexpr uint32_t kDecMaxNz = 1024;        // explicit probe rows per call (else the old path)
 constexpr uint32_t kDecInlineBytes = 512;   // explicit rows passed inside the launch parameters
 constexpr uint32_t kDecInlineNz = 32;
-constexpr uint32_t kDecBarriers = 4;        // grid barriers per decision launch
+constexpr uint32_t kDecBarriers = 5;        // grid barriers per decision launch
+constexpr uint32_t kDecListWords = 4096;    // member row words of a 256-entry batch above which members are listed
+constexpr uint32_t kDecStagedMin = 2048;    // survivors above which every CTA stages the whole list (C2)
 constexpr uint32_t kDecMaxLayers = 2048;    // layers above the current one (order phases)
 constexpr uint32_t kDecMaxExperts = 8192;   // experts per layer (a layer's segment in shared memory)
 
@@ -180,6 +182,8 @@ struct DecisionArgs {
   double window;
   unsigned long long* dmin2;  // [2] by call parity, ~0 before first use
   unsigned long long* agg;    // [L*E]
+  uint32_t* mcount;           // listed window members (0 between calls; null: never list)
+  uint32_t* mlist;            // [size] listed window members (wide windows)
   // order
   int filter;
   unsigned long long* ckey;  // [(L-cur-1)*E] per-layer sorted survivor keys (~bits(priority))
