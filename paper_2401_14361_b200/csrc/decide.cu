@@ -217,6 +217,20 @@ __device__ __forceinline__ void list_sum(const DecisionArgs& a, uint8_t* red, ui
   }
 }
 
+// The staged survivors' flat ExpertIds (C2 with many survivors): u16 when
+// L*E <= 65,536 (10 bytes per survivor with the u64 key), else u32.
+struct StagedIds {
+  void* p;
+  bool h;
+  __device__ __forceinline__ uint32_t operator[](uint32_t i) const {
+    return h ? static_cast<const uint16_t*>(p)[i] : static_cast<const uint32_t*>(p)[i];
+  }
+  __device__ __forceinline__ void set(uint32_t i, uint32_t v) const {
+    if (h) static_cast<uint16_t*>(p)[i] = (uint16_t)v;
+    else static_cast<uint32_t*>(p)[i] = v;
+  }
+};
+
 template <int CB, bool PS>
 __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
   using Acc = typename Dot<CB>::Acc;
@@ -553,10 +567,12 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
   // out -- no per-pair global atomics, no C3 pass
   uint32_t dsm_bytes;
   asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm_bytes));
-  const bool staged = S > kDecStagedMin && (size_t)S * 12 <= dsm_bytes;
+  // flat ExpertIds as u16 when L*E <= 65,536: 10 bytes per staged survivor
+  const bool id16 = (uint64_t)L * E <= 65536u;
+  const bool staged = S > kDecStagedMin && (size_t)S * (id16 ? 10 : 12) <= dsm_bytes;
   if (staged) {
     unsigned long long* tk = reinterpret_cast<unsigned long long*>(dsm);
-    uint32_t* ti = reinterpret_cast<uint32_t*>(tk + S);
+    StagedIds ti{tk + S, id16};
     __shared__ uint32_t rk[kDecThreads];
     // 12 survivors' loads in flight per thread; CTA b starts at its own offset
     // so the CTAs do not all request the same lines at once
@@ -584,7 +600,7 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
         if (j >= S) break;
         const uint32_t i = j + rot < S ? j + rot : j + rot - S;
         tk[i] = kk[u];
-        ti[i] = ii[u];
+        ti.set(i, ii[u]);
       }
     }
     __syncthreads();
@@ -677,8 +693,8 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
   // staged: CTA b writes output positions [b*S/G, (b+1)*S/G) in order from its
   // staged copy (contiguous stores: whole bursts to host-mapped memory)
   if (staged) {
-    const unsigned long long* tk = reinterpret_cast<const unsigned long long*>(dsm);
-    const uint32_t* ti = reinterpret_cast<const uint32_t*>(tk + S);
+    unsigned long long* tk = reinterpret_cast<unsigned long long*>(dsm);
+    const StagedIds ti{tk + S, id16};
     const uint32_t r0 = (uint32_t)((uint64_t)S * b / G), r1 = (uint32_t)((uint64_t)S * (b + 1) / G);
     for (uint32_t r = r0 + tid; r < r1; r += kDecThreads) {
       const uint32_t t = __ldcg(a.crank + r), id = ti[t];
@@ -1114,10 +1130,13 @@ size_t decision_smem(uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz, uint32_
   while (np < E) np <<= 1;
   // staged probe rows | a layer's slots + its compacted survivors | the listed
   // members' group reduction (one u64 per count of a 16-byte chunk per thread)
-  // | the staged survivor list (12 bytes per candidate, C2 with many survivors)
+  // | the staged survivor list (12 bytes per candidate, C2 with many survivors),
+  // capped so that two decision CTAs still fit one SM: two launches in flight
+  // on different streams (two handles, two host threads) must stay co-resident
+  // for their software grid barriers
   const size_t rows = cur + 1 < L ? L - cur - 1 : 0;
   return std::max({(size_t)n_nz * RB, (size_t)np * 28, (size_t)kDecThreads * 16 * 8,
-                   std::min<size_t>(rows * E * 12, 160 * 1024)});
+                   std::min<size_t>(rows * E * ((uint64_t)L * E <= 65536u ? 10 : 12), kDecStageCap)});
 }
 
 int decision_grid(int n_sm, uint32_t size, uint32_t L, uint32_t cur) {

@@ -155,6 +155,7 @@ constexpr uint32_t kDecInlineNz = 32;
 constexpr uint32_t kDecBarriers = 5;        // grid barriers per decision launch
 constexpr uint32_t kDecListWords = 4096;    // member row words of a 256-entry batch above which members are listed
 constexpr uint32_t kDecStagedMin = 2048;    // survivors above which every CTA stages the whole list (C2)
+constexpr size_t kDecStageCap = 92 * 1024;  // its shared memory bound (two CTAs per SM)
 constexpr uint32_t kDecMaxLayers = 2048;    // layers above the current one (order phases)
 constexpr uint32_t kDecMaxExperts = 8192;   // experts per layer (a layer's segment in shared memory)
 

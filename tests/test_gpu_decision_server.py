@@ -81,3 +81,42 @@ def test_server_width_change_idle_and_destroy(m, orc):
     e3 = m.Eamc(s, m.Phase.decode, P)  # decisions on another handle still co-reside
     e3.append(ents, seqs)
     _check(m, orc, e3, ents, seqs, probe, 4, s)
+
+
+@pytest.mark.timeout(300)
+def test_concurrent_decisions_two_handles(m, orc):
+    """Two handles deciding at once from two host threads (two streams): the
+    software-grid-barrier kernels must stay co-resident (two CTAs per SM by
+    their shared-memory bound), including the wide-window path (layer 0: listed
+    members, staged ranking).  Results equal the sequential ones."""
+    import threading
+    L, E, k, P = 59, 160, 6, 2000
+    w = Workload(L, E, k, seed=13)
+    hs, probes = [], []
+    for i in range(2):
+        ents = orc.request_eams(w, P, start=5000 * i)
+        e = m.Eamc(m.ModelShape(L, E, k), m.Phase.decode, P)
+        e.append(ents, np.arange(P, dtype=np.uint64))
+        hs.append(e)
+        probes.append([orc.iteration_probe(w, 700 + 10 * i + j, 2, j % (L - 1)) for j in range(24)])
+    s = m.ModelShape(L, E, k)
+
+    def run(i, res):
+        for j, pr in enumerate(probes[i]):
+            cur = m.Eam(s, m.EamKind.iteration, counts=pr)
+            res.append(m.prefetch_order(cur, hs[i], j % (L - 1), True))
+
+    want = [[], []]
+    for i in range(2):
+        run(i, want[i])
+    for _ in range(3):
+        got = [[], []]
+        ts = [threading.Thread(target=run, args=(i, got[i])) for i in range(2)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(timeout=120)
+            assert not t.is_alive(), "concurrent decisions did not finish"
+        for i in range(2):
+            for a, b in zip(got[i], want[i]):
+                assert np.array_equal(a, b)
