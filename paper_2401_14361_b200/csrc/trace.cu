@@ -236,6 +236,8 @@ __global__ void __launch_bounds__(512)
 // requests (k_trace_own: 0.190 ms), 0.129 ms at 50 requests of 20k tokens
 // (k_trace_own + k_trace_gen: 1.95 ms).  The remaining gap to HBM is issue
 // (~10 instructions per u16 of ids) and the cross-group barrier per piece.
+constexpr uint32_t kLaneMaxGroups = 19;  // consumer warps at most (one per group when H <= 32)
+
 struct LaneArgs {
   const uint8_t* topk;
   uint64_t T, TS;
@@ -269,6 +271,48 @@ __device__ __forceinline__ bool lane_item(const LaneArgs& a, uint64_t ii, uint64
   *ta = max(ii * a.TS, lo);
   *tb = min(min(a.T, ii * a.TS + a.TS), hi);
   return *ta < *tb;
+}
+
+// The request holding token ta (the first one whose end lies beyond it).
+__device__ __forceinline__ uint64_t lane_first_request(const LaneArgs& a, uint64_t ta) {
+  uint64_t l0 = 0, h0 = a.R;
+  while (l0 < h0) {
+    const uint64_t mid = (l0 + h0) / 2;
+    if (a.offsets[mid + 1] <= ta) l0 = mid + 1; else h0 = mid;
+  }
+  return l0;
+}
+// The next non-empty request after r, which ended at token pe.
+__device__ __forceinline__ uint64_t lane_next_request(const LaneArgs& a, uint64_t r, uint64_t pe) {
+  while (r + 1 < a.R && a.offsets[r + 2] <= pe) ++r;
+  return r + 1;
+}
+
+// Stages of a piece of n tokens: full stages of TW tokens, then the last G of
+// equal size (all of them, G at most, when the piece holds <= G*TW tokens), so
+// that the G groups, which take every G-th stage, reach the piece's end
+// together.
+__device__ __forceinline__ uint32_t piece_stages(uint32_t n, uint32_t TW, uint32_t G) {
+  const uint32_t full = (n + TW - 1) / TW;
+  return full <= G ? min(G, n) : full;
+}
+__device__ __forceinline__ void piece_stage(uint32_t n, uint32_t TW, uint32_t G, uint32_t j,
+                                            uint32_t* st, uint32_t* en) {
+  const uint32_t full = (n + TW - 1) / TW;
+  if (full <= G) {
+    const uint32_t m = min(G, n);
+    *st = n * j / m;
+    *en = n * (j + 1) / m;
+    return;
+  }
+  const uint32_t head = full - G, t0 = head * TW, tail = n - t0;
+  if (j < head) {
+    *st = j * TW;
+    *en = *st + TW;
+  } else {
+    *st = t0 + tail * (j - head) / G;
+    *en = t0 + tail * (j - head + 1) / G;
+  }
 }
 
 // The consumers' reduction of one request piece into counts[r].
@@ -368,19 +412,34 @@ __global__ void __launch_bounds__(640, 1) k_trace_lane(LaneArgs a, OUT* __restri
   const uintptr_t base = reinterpret_cast<uintptr_t>(a.topk);
   if (t >= NC) {  // producer warp: one thread streams the stages in order
     if (t == NC) {
-      uint32_t s = 0, ph = 0;  // ring slot and its pass parity
+      // group g owns slots g, g + G, ...: each slot has one consumer group, so
+      // a group's wait for the n-th use of its slot cannot alias an earlier,
+      // still incomplete use (mbarrier parity) however far other groups lag
+      uint32_t used[kLaneMaxGroups];  // stages issued per group so far
+      for (uint32_t i = 0; i < a.G; ++i) used[i] = 0;
+      const uint32_t D = a.NSTG / a.G;  // slots per group
       for (uint64_t ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
         uint64_t ta, tb;
         if (!lane_item(a, ii, lo, hi, &ta, &tb)) continue;
-        for (uint64_t tok = ta; tok < tb; tok += a.TW) {
-          const uint64_t te = min(tb, tok + a.TW);
-          const uintptr_t g0 = (base + tok * Lk) & ~(uintptr_t)15;
-          const uintptr_t g1 = (base + te * Lk + 15) & ~(uintptr_t)15;
-          mbar_wait(&empty[s], ph ^ 1u);
-          mbar_arrive_expect_tx(&full[s], (uint32_t)(g1 - g0));
-          bulk_g2s(ring + (size_t)s * a.SB, reinterpret_cast<const void*>(g0), (uint32_t)(g1 - g0),
-                   &full[s]);
-          if (++s == a.NSTG) s = 0, ph ^= 1u;
+        uint64_t r = lane_first_request(a, ta), ps = ta;
+        uint32_t k = 0;
+        while (ps < tb) {  // pieces: request r intersected with the item
+          const uint64_t rend = a.offsets[r + 1], pe = min(rend, tb);
+          const uint32_t n = (uint32_t)(pe - ps), m = piece_stages(n, a.TW, a.G);
+          for (uint32_t j = 0; j < m; ++j, ++k) {
+            uint32_t st, en;
+            piece_stage(n, a.TW, a.G, j, &st, &en);
+            const uintptr_t g0 = (base + (ps + st) * Lk) & ~(uintptr_t)15;
+            const uintptr_t g1 = (base + (ps + en) * Lk + 15) & ~(uintptr_t)15;
+            const uint32_t gg = k % a.G, u = used[gg]++;
+            const uint32_t s = gg + a.G * (u % D), ph = (u / D) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            mbar_arrive_expect_tx(&full[s], (uint32_t)(g1 - g0));
+            bulk_g2s(ring + (size_t)s * a.SB, reinterpret_cast<const void*>(g0),
+                     (uint32_t)(g1 - g0), &full[s]);
+          }
+          ps = pe;
+          if (pe == rend) r = lane_next_request(a, r, pe);
         }
       }
     }
@@ -391,51 +450,29 @@ __global__ void __launch_bounds__(640, 1) k_trace_lane(LaneArgs a, OUT* __restri
   const uint32_t tp = act ? tg / a.H : 0, q = act ? tg - tp * a.H : 0;
   const uint32_t my = smem_u32(cnt) + 4u * (tg % a.C), rowE = 4u * NCOL;  // expert e: my + e * rowE
   const uint32_t Eh = E, dj = a.TPg * Lk;
-  uint32_t seq0 = 0;  // ring sequence number of the item's first stage
+  const uint32_t D = a.NSTG / a.G;  // this group's slots: g, g + G, ... (see the producer)
+  uint32_t used = 0;                // stages this group has taken so far
   for (uint64_t ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
     uint64_t ta, tb;
     if (!lane_item(a, ii, lo, hi, &ta, &tb)) continue;
-    uint64_t r;  // the request holding token ta (the first one whose end lies beyond it)
-    {
-      uint64_t l0 = 0, h0 = a.R;
-      while (l0 < h0) {
-        const uint64_t mid = (l0 + h0) / 2;
-        if (a.offsets[mid + 1] <= ta) l0 = mid + 1; else h0 = mid;
-      }
-      r = l0;
-    }
-    uint64_t rend = a.offsets[r + 1];
-    // item-relative token offsets fit in 32 bits (items hold <= 65,535 tokens)
-    const uint32_t len = (uint32_t)(tb - ta);
-    const uint32_t ib = (uint32_t)(base + ta * Lk);  // low bits of the item's first byte address
-    uint32_t evr = (uint32_t)(min(rend, tb) - ta);   // the next event
-    bool done = false;                                // the item-end event has been joined
-    // join the next event: reduce the piece of request r, step to the next request
-    auto join = [&]() {
-      lane_flush<OUT>(a, cnt, stage_out, NC, counts + r * (uint64_t)L * E, sign);
-      if (evr == len) done = true;
-      if (ta + evr == rend) {  // next non-empty request
-        while (r + 1 < a.R && a.offsets[r + 2] <= rend) ++r;
-        ++r;
-        rend = r < a.R ? a.offsets[r + 1] : hi;
-      }
-      evr = (uint32_t)(min(rend, tb) - ta);
-    };
-    const uint32_t ns = (len + a.TW - 1) / a.TW;
-    uint32_t s = (seq0 + g) % a.NSTG, ph = ((seq0 + g) / a.NSTG) & 1u;
-    for (uint32_t kst = g, tr = g * a.TW; kst < ns; kst += a.G, tr += a.G * a.TW) {
-      const uint32_t n = min(a.TW, len - tr);  // tokens in this stage
-      while (!done && evr <= tr) join();      // events before the stage
-      mbar_wait(&full[s], ph);
-      const uint8_t* sb = ring + s * a.SB + ((ib + tr * Lk) & 15u) + 2u * q;
-      uint32_t jx = 0;
-      while (jx < n) {
-        const uint32_t jy = min(evr - tr, n);
-        if (act) {  // stage-local tokens j in [jx, jy), phase tp takes j = tp (mod TPg)
-          uint32_t j = jx == 0 ? tp : jx + (tp + a.TPg - jx % a.TPg) % a.TPg;
-          const uint8_t* pj = sb + j * Lk;
+    uint64_t r = lane_first_request(a, ta), ps = ta;
+    uint32_t k = 0;  // stages of the item so far; group g takes k = g (mod G)
+    while (ps < tb) {
+      const uint64_t rend = a.offsets[r + 1], pe = min(rend, tb);
+      const uint32_t n = (uint32_t)(pe - ps), m = piece_stages(n, a.TW, a.G);
+      for (uint32_t j = (g + a.G - k % a.G) % a.G; j < m; j += a.G) {
+        const uint32_t s = g + a.G * (used % D), ph = (used / D) & 1u;
+        ++used;
+        uint32_t st, en;
+        piece_stage(n, a.TW, a.G, j, &st, &en);
+        mbar_wait(&full[s], ph);
+        if (act) {  // the stage's tokens jj in [0, en - st), phase tp takes jj = tp (mod TPg)
+          const uint32_t jy = en - st;
+          const uint8_t* pj = ring + s * a.SB + ((uint32_t)(base + (ps + st) * Lk) & 15u) + 2u * q +
+                              tp * Lk;
+          uint32_t jj = tp;
           constexpr int U = LANE_U;
-          for (; j + (U - 1) * a.TPg < jy; j += U * a.TPg, pj += U * dj) {
+          for (; jj + (U - 1) * a.TPg < jy; jj += U * a.TPg, pj += U * dj) {
             uint32_t v[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) v[u] = *reinterpret_cast<const uint16_t*>(pj + u * dj);
@@ -446,14 +483,14 @@ __global__ void __launch_bounds__(640, 1) k_trace_lane(LaneArgs a, OUT* __restri
               asm volatile("red.shared.add.u32 [%0], 65536;" ::"r"(my + e1 * rowE));
             }
           }
-          if (j < jy) {  // tail: one masked round, the masked slots count into the null row
+          if (jj < jy) {  // tail: one masked round, the masked slots count into the null row
             uint32_t v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-              v[u] = j + u * a.TPg < jy ? *reinterpret_cast<const uint16_t*>(pj + u * dj) : 0u;
+            for (int u = 0; u < U; ++u)  // masked slots re-read the first slot (inside the stage)
+              v[u] = *reinterpret_cast<const uint16_t*>(jj + u * a.TPg < jy ? pj + u * dj : pj);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              const bool in = j + u * a.TPg < jy;
+              const bool in = jj + u * a.TPg < jy;
               const uint32_t e0 = in ? min(v[u] & 0xffu, Eh) : Eh + 1;
               const uint32_t e1 = in ? min(v[u] >> 8, Eh) : Eh + 1;
               asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(my + e0 * rowE));
@@ -461,16 +498,15 @@ __global__ void __launch_bounds__(640, 1) k_trace_lane(LaneArgs a, OUT* __restri
             }
           }
         }
-        jx = jy;
-        if (!done && tr + jy == evr) join();  // an event inside (or at the end of) the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      s += a.G;
-      if (s >= a.NSTG) s -= a.NSTG, ph ^= 1u;
+      k += m;
+      // the piece's end: every group has counted its stages of it
+      lane_flush<OUT>(a, cnt, stage_out, NC, counts + r * (uint64_t)L * E, sign);
+      ps = pe;
+      if (pe == rend) r = lane_next_request(a, r, pe);
     }
-    while (!done) join();  // the events after this group's last stage
-    seq0 += ns;
   }
   pdl_trigger();
 }
@@ -581,7 +617,7 @@ bool lane_config(uint64_t T, uint32_t L, uint32_t E, uint32_t k, uint64_t R, int
   const uint32_t Lk = L * k;
   if (off || Lk == 0 || Lk % 2 || E == 0 || E > 256 || T < 16 * R) return false;
   const size_t kMax = 227u * 1024u;
-  constexpr uint32_t kMaxWarps = 19;  // consumer warps (+ the producer warp: <= 640 threads)
+  constexpr uint32_t kMaxWarps = kLaneMaxGroups;  // consumer warps (+ the producer warp: <= 640 threads)
   const uint32_t H = Lk / 2, ES = E | 1;
   if (H > kMaxWarps * 32) return false;
   // a group: the warps holding every position pair once (several token phases
@@ -598,16 +634,16 @@ bool lane_config(uint64_t T, uint32_t L, uint32_t E, uint32_t k, uint64_t R, int
   const size_t ring = kMax - fixed - 256;
   // groups: as many as the warp budget allows with two ring slots each
   uint32_t G = std::max<uint32_t>(1, kMaxWarps / NWg);
-  while (G > 1 && (size_t)(G + 1) * (sb_min + 16) > ring) --G;
-  // tokens per stage: <= 24 KB, at least G + 1 slots (measured at DS: 48-token
-  // stages in 4 slots beat 32-token stages in 6 and 16-token stages in 12; one
-  // group of 18 warps with 3 token phases per stage instead of 3 groups: 0.177
-  // vs 0.153 ms)
-  const size_t sb_max = std::min<size_t>(24576 + 160, ring / (G + 1) - 16);
+  while (G > 1 && (size_t)(2 * G) * (sb_min + 16) > ring) --G;
+  // tokens per stage: <= 24 KB, two slots per group (slots belong to groups;
+  // one group of 18 warps with 3 token phases per stage instead of 3 groups
+  // measured 0.177 vs 0.153 ms at DS)
+  const size_t sb_max = std::min<size_t>(24576 + 160, ring / (2 * G) - 16);
   uint32_t TW = (uint32_t)std::max<size_t>(UT, (sb_max - 160) / Lk / UT * UT);
   const uint32_t SB = (uint32_t)((((size_t)TW * Lk + 32) + 127) & ~(size_t)127);
-  const uint32_t NSTG = (uint32_t)std::min<size_t>(32, ring / (SB + 16));
-  if (NSTG < G + 1) return false;
+  const uint32_t D = (uint32_t)std::min<size_t>(64 / G, ring / (SB + 16) / G);  // slots per group
+  if (D < 2) return false;
+  const uint32_t NSTG = D * G;
   *smem = (size_t)NSTG * SB + fixed + 16 * (size_t)NSTG;
   *grid = (unsigned)n_sm;  // one block per SM
   // one item per block (equal token counts; each piece costs one reduction)
