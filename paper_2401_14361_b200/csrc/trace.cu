@@ -200,42 +200,44 @@ __global__ void __launch_bounds__(512)
   pdl_trigger();
 }
 
-#ifndef LANE_U
-#define LANE_U 16
-#endif
 // ---- k_trace_lane: bank-locked private counters fed by a bulk-copy ring ----
 //
-// The id stream is cut into items of TS tokens (one per block); inside an item
-// one producer thread streams stages of TW whole tokens through a ring of
-// shared-memory slots (cp.async.bulk of the 16-byte aligned window, completion
-// on an mbarrier), so the loads in flight do not depend on registers.
+// The id stream is cut into items of TS tokens (one per block), an item into
+// pieces (request r intersected with the item) and a piece into stages of at
+// most TW whole tokens; the last G stages of a piece are of equal size.  One
+// producer thread streams the stages through shared-memory ring slots
+// (cp.async.bulk of the 16-byte aligned window, completion on an mbarrier), so
+// the loads in flight do not depend on registers.
 //
-// Consumer warps form G groups; group g takes stages g, g + G, ...  Inside a
-// group, thread tg = tp * H + q (H = L*k / 2 position pairs) owns the id
-// positions 2q, 2q+1 of the stage's tokens j = tp (mod TPg): it reads them as
-// one u16 and adds 1 (position 2q) or 0x10000 (position 2q+1) into the counter
-// word of its column for expert e, cnt[e][col].  A column belongs to one lane
-// position of one warp in every group (col = tg mod C), so the 32 lanes of a
-// warp always hit 32 distinct banks -- one wavefront per RED.shared, where a
-// shared L x E histogram takes ~3.3 (k_trace_own).  Ids >= E are clamped into
-// a trash row (nonzero -> the call's flag), masked tail slots into a null row.
-// A 16-bit half counts at most one id per token of a piece and pieces are at
-// most TS <= 65,535 tokens, so halves never carry.
+// Consumer warps form G groups; group g takes every G-th stage of the item and
+// owns the ring slots g, g + G, ... (one consumer group per slot: a group's
+// wait for the n-th use of a slot cannot alias an earlier use by mbarrier
+// parity, however far the groups drift apart).  Inside a group, thread
+// tg = tp * H + q (H = L*k / 2 position pairs) owns the id positions 2q, 2q+1
+// of the stage's tokens j = tp (mod TPg): it reads them as one u16 and adds 1
+// (position 2q) or 0x10000 (position 2q+1) into the counter word of its column
+// for expert e, cnt[e][col].  A column belongs to one lane position of one
+// warp in every group (col = tg mod C), so the 32 lanes of a warp always hit
+// 32 distinct banks -- one wavefront per RED.shared, where a shared L x E
+// histogram takes ~3.3 (k_trace_own).  Ids >= E are clamped into a trash row
+// (nonzero -> the call's flag), masked tail slots into a null row.  A 16-bit
+// half counts at most one id per token of a piece and pieces are at most
+// TS <= 65,535 tokens, so halves never carry.
 //
-// Request ends inside the item and the item end are events: every group joins
-// each event (a named barrier over all consumers) after counting its tokens
-// before it and before counting any token after it, and the consumers then
-// reduce the counters into counts[r]: per (layer, expert) cell the halves of
-// the layer's positions (and the token phases' columns) are summed into a
-// padded staging row, the counters are zeroed, and the staged cells are added
-// into counts[r] with coalesced reductions (RED: no thread waits on the
-// counts' latency; a read-modify-write pass cost ~2 us per piece).  The
-// rollback launch subtracts the same sums (see gate_open).
+// At a piece's end (every group has counted its stages of it: a named barrier
+// over all consumers) the consumers reduce the counters into counts[r]: per
+// (layer, expert) cell the halves of the layer's positions (and the token
+// phases' columns) are summed into a padded staging row, the counters are
+// zeroed, and the staged cells are added into counts[r] with coalesced
+// reductions (RED: no thread waits on the counts' latency; a read-modify-write
+// pass cost ~2 us per piece).  The rollback launch subtracts the same sums
+// (see gate_open).
 //
-// Measured (DS, 1M tokens, scripts/trace_probe.py): 0.173 ms at 1,000
-// requests (k_trace_own: 0.190 ms), 0.129 ms at 50 requests of 20k tokens
+// Measured (DS, 1M tokens, scripts/trace_probe.py): ~0.15 ms at 1,000
+// requests (k_trace_own: 0.190 ms), ~0.12 ms at 50 requests of 20k tokens
 // (k_trace_own + k_trace_gen: 1.95 ms).  The remaining gap to HBM is issue
-// (~10 instructions per u16 of ids) and the cross-group barrier per piece.
+// (~10 instructions per u16 of ids) and the per-piece reduction.
+constexpr int kLaneU = 16;  // tokens per thread and unrolled round
 constexpr uint32_t kLaneMaxGroups = 19;  // consumer warps at most (one per group when H <= 32)
 
 struct LaneArgs {
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(640, 1) k_trace_lane(LaneArgs a, OUT* __restri
           const uint8_t* pj = ring + s * a.SB + ((uint32_t)(base + (ps + st) * Lk) & 15u) + 2u * q +
                               tp * Lk;
           uint32_t jj = tp;
-          constexpr int U = LANE_U;
+          constexpr int U = kLaneU;
           for (; jj + (U - 1) * a.TPg < jy; jj += U * a.TPg, pj += U * dj) {
             uint32_t v[U];
 #pragma unroll
@@ -628,7 +630,7 @@ bool lane_config(uint64_t T, uint32_t L, uint32_t E, uint32_t k, uint64_t R, int
   const size_t cnt_b = (size_t)(E + 2) * NCOL * 4;  // + the trash and null rows
   const size_t out_b = (((size_t)L * ES + 1) & ~(size_t)1) * 4;
   const size_t fixed = cnt_b + out_b;
-  const uint32_t UT = LANE_U * TPg;  // tokens of one unrolled round of every phase
+  const uint32_t UT = kLaneU * TPg;  // tokens of one unrolled round of every phase
   const size_t sb_min = (((size_t)UT * Lk + 32) + 127) & ~(size_t)127;
   if (fixed + 2 * (sb_min + 16) + 256 > kMax) return false;
   const size_t ring = kMax - fixed - 256;
