@@ -1901,6 +1901,7 @@ static moe_status decide_fused(moe_eamc* h, const uint64_t* probe, uint32_t cur,
                                uint64_t n_slots, moe_candidate* out, uint64_t cap,
                                uint64_t* n_out, int64_t* victim, bool* handled) {
   *handled = false;
+  const auto th0 = std::chrono::steady_clock::now();
   DevColl& c = h->c;
   const uint32_t L = c.L, E = c.E;
   const uint64_t cells = (uint64_t)L * E;
@@ -1995,7 +1996,15 @@ static moe_status decide_fused(moe_eamc* h, const uint64_t* probe, uint32_t cur,
       a.nz = reinterpret_cast<const uint16_t*>(h->xdev.as<uint8_t>() + rows_b);
     }
   }
+  const auto th1 = std::chrono::steady_clock::now();
   CKS(run_decision(h, a, (size_t)n_nz * RB, request_eam, slots, n_slots, out, cap, n_out, victim));
+  if (dec_timing()) {
+    static double acc = 0;
+    static uint64_t cnt = 0;
+    acc += std::chrono::duration<double, std::micro>(th1 - th0).count();
+    if (++cnt % 58 == 0)
+      fprintf(stderr, "decision host prep (avg of %llu): %.1f us\n", (unsigned long long)cnt, acc / cnt);
+  }
   if (store) {
     h->dec_rows.assign(hb, hb + (size_t)(cur + 1) * RB);
     h->dec_keep = cur;
