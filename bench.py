@@ -769,9 +769,27 @@ def run_rows(args, m, _lib, torch, dev, sp, stream, flush):
         fn5(h5, pq[q], q % (L5 - 1), 1, op5, cap5, pn5)
     t5p = time.perf_counter() - t0
     _lib.check(fn5(h5, pq[0], 0, 1, op5, cap5, pn5))
+    # the same through the opt-in persistent decision server (one resident CTA
+    # for a small collection, fed through a pinned mailbox instead of a launch)
+    _lib.check(_lib.lib.moe_eamc_set_decision_server(h5, 8))
+    for q in range(20):
+        _lib.check(fn5(h5, pq[q], q % (L5 - 1), 1, op5, cap5, pn5))
+    srv_same = True
+    for q in range(64):
+        _lib.check(fn5(h5, pq[q], q % (L5 - 1), 1, op5, cap5, pn5))
+        srv_same &= bool(np.array_equal(o5p[:n5.value], got[q]))
+    t0 = time.perf_counter()
+    for q in range(Q5):
+        fn5(h5, pq[q], q % (L5 - 1), 1, op5, cap5, pn5)
+    t5s = time.perf_counter() - t0
+    _lib.check(_lib.lib.moe_eamc_set_decision_server(h5, 0))
     row = {"workload": f"MIX prefetch: L={L5} E={E5}, EAMC P={P5}, {Q5} prefetch_priorities "
                        "calls (l = q mod (L-1)) + floor filter, C ABI with host buffers",
-           "us_per_decision": t5p / Q5 * 1e6, "decisions_per_s": Q5 / t5p}
+           "us_per_decision": t5p / Q5 * 1e6, "decisions_per_s": Q5 / t5p,
+           "us_per_decision_server": t5s / Q5 * 1e6,
+           "server_note": "opt-in moe_eamc_set_decision_server: one resident CTA polls a pinned "
+                          "mailbox (no launch per decision); results equal the launched path's",
+           "server_same_orders": srv_same}
     if ref is not None:
         t0 = time.perf_counter()
         ok = True

@@ -1695,9 +1695,20 @@ static moe_status server_stop(moe_eamc* h) {
   return MOE_OK;
 }
 
-static moe_status server_launch(moe_eamc* h) {
+static moe_status server_launch(moe_eamc* h, bool small) {
   auto& v = h->srv;
   const DevColl& c = h->c;
+  if (small) {  // one CTA, shared memory for the largest small-path request
+    auto* ctl = v.ctl.as<moe::DecServerCtl>();
+    v.cb = c.cb;
+    v.small = true;
+    CK(moe::launch_decision_small_server(
+        ctl, reinterpret_cast<volatile uint64_t*>(&ctl->seq_done)[0], 50'000'000ull, c.cb,
+        moe::decision_small_smem_max(c.L, c.RB), v.st));
+    v.launched = true;
+    return MOE_OK;
+  }
+  v.small = false;
   uint32_t np = 1;
   while (np < c.E) np <<= 1;
   v.smem = std::max({(size_t)c.L * c.RB, (size_t)np * 28, moe::decision_smem(c.L, c.E, c.RB, 0, 0, 1)});
@@ -1716,7 +1727,7 @@ static moe_status server_launch(moe_eamc* h) {
 
 // One request through the server: post the arguments in the pinned mailbox,
 // wait for seq_done (relaunching an idled-out server).
-static moe_status server_run(moe_eamc* h, const moe::DecisionArgs& a) {
+static moe_status server_run(moe_eamc* h, const moe::DecisionArgs& a, bool small) {
   auto& v = h->srv;
   if (!v.st) {
     CK(cudaStreamCreateWithFlags(&v.st, cudaStreamNonBlocking));
@@ -1728,13 +1739,19 @@ static moe_status server_run(moe_eamc* h, const moe::DecisionArgs& a) {
     v.seq = 0;
     v.k = 0;
   }
-  if (v.launched && v.cb != h->c.cb) CKS(server_stop(h));  // widened: relaunch at the new width
+  // widened, or the other server kind: relaunch
+  if (v.launched && (v.cb != h->c.cb || v.small != small)) CKS(server_stop(h));
+  // collection updates queued on the handle's stream complete before the
+  // resident kernel reads the collection
+  const cudaError_t q = cudaStreamQuery(h->st);
+  if (q == cudaErrorNotReady) CK(cudaStreamSynchronize(h->st));
+  else CK(q);
   auto* ctl = v.ctl.as<moe::DecServerCtl>();
   std::memcpy(&ctl->args, &a, sizeof a);
   std::atomic_thread_fence(std::memory_order_seq_cst);
   const uint64_t seq = ++v.seq;
   reinterpret_cast<volatile uint64_t*>(&ctl->seq_req)[0] = seq;
-  if (!v.launched) CKS(server_launch(h));
+  if (!v.launched) CKS(server_launch(h, small));
   const auto t0 = std::chrono::steady_clock::now();
   for (uint64_t spin = 1;; ++spin) {
     if (reinterpret_cast<volatile uint64_t*>(&ctl->seq_done)[0] == seq) break;
@@ -1743,7 +1760,7 @@ static moe_status server_run(moe_eamc* h, const moe::DecisionArgs& a) {
       if (q == cudaSuccess) {  // the server idled out before seeing the request
         if (reinterpret_cast<volatile uint64_t*>(&ctl->seq_done)[0] == seq) break;
         v.launched = false;
-        CKS(server_launch(h));
+        CKS(server_launch(h, small));
       } else if (q != cudaErrorNotReady) {
         CK(q);
       }
@@ -1755,7 +1772,7 @@ static moe_status server_run(moe_eamc* h, const moe::DecisionArgs& a) {
     }
   }
   std::atomic_thread_fence(std::memory_order_seq_cst);
-  ++v.k;
+  if (!small) ++v.k;  // the multi-CTA server's barrier and completion counters
   return MOE_OK;
 }
 
@@ -1804,17 +1821,20 @@ static moe_status run_decision(moe_eamc* h, moe::DecisionArgs& a, size_t stage_r
   if (c.L - a.cur > moe::kDecMaxLayers || c.E > moe::kDecMaxExperts)
     return fail(MOE_ERR_INVALID_ARGUMENT, "decision: shape %ux%u exceeds the order phases' limits",
                 c.L, c.E);
+  const uint32_t rows_above = a.cur + 1 < c.L ? c.L - a.cur - 1 : 0;
+  const bool small_ok = !n_slots && a.do_dist && a.do_agg && c.size <= moe::kSmallMaxP &&
+                        (uint64_t)rows_above * c.E <= moe::kSmallMaxCells && !small_off() &&
+                        moe::decision_small_smem_max(c.L, c.RB) <= 200 * 1024;
   if (server_takes(h, n_slots)) {
-    CKS(server_run(h, a));
+    a.tprobe = nullptr;
+    CKS(server_run(h, a, small_ok));
     const uint32_t n = *reinterpret_cast<volatile uint32_t*>(a.n_out);
     if (n_out) *n_out = n;
     if (n && out && cap) std::memcpy(out, a.out, std::min<uint64_t>(n, cap) * sizeof(moe_candidate));
     if (victim) *victim = -1;
     return MOE_OK;
   }
-  const uint32_t rows_above = a.cur + 1 < c.L ? c.L - a.cur - 1 : 0;
-  if (!n_slots && a.do_dist && a.do_agg && c.size <= moe::kSmallMaxP &&
-      (uint64_t)rows_above * c.E <= moe::kSmallMaxCells && !small_off()) {
+  if (small_ok) {
     // small collection: one CTA, no grid barriers
     const size_t smem = moe::decision_small_smem(c.size, c.L, c.E, c.RB, a.n_nz, a.cur);
     if (smem <= 200 * 1024) {

@@ -202,6 +202,7 @@ struct moe_eamc {
     int G = 0;             // CTAs (0 = off: a launch per decision)
     int cb = 0;            // storage width it was launched for
     bool launched = false;
+    bool small = false;    // the launched server is the one-CTA small-collection kernel
     cudaStream_t st = nullptr;
     moe::abi::PinBuf ctl;  // moe::DecServerCtl, device-mapped
     moe::abi::DevBuf dargs, drows, state;  // state: go, done, barrier counter

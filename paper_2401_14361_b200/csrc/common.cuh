@@ -145,6 +145,7 @@ struct Dot<4> {
 __device__ __forceinline__ double row_sim_exact(uint64_t dot, double sa, double sb) {
   if (sa == 0.0 && sb == 0.0) return 1.0;
   if (sa == 0.0 || sb == 0.0) return 0.0;
+  if (dot == 0) return 0.0;  // +0.0 / positive: the division's exact result
   return __ddiv_rn(__ull2double_rn(dot), __dmul_rn(sa, sb));
 }
 // d = 1 - sim / L, clamped to [0, 1] (eam.cpp:99-103)

@@ -112,6 +112,15 @@ __device__ __forceinline__ T ld_ro(const T* p) {
   if constexpr (PS) return __ldcg(p);
   else return __ldg(p);
 }
+// The one-CTA server's collection reads: L1-cached plain loads.  Collection
+// updates complete before a request is posted (the host drains the handle's
+// stream), and the request's system-scope acquire fence (thread 0, then
+// bar.sync) orders every later load of the CTA after them.
+template <int MODE, typename T>
+__device__ __forceinline__ T ld_col(const T* p) {
+  if constexpr (MODE == 2) return *p;
+  else return ld_ro<MODE == 1>(p);
+}
 
 // Column-split window aggregation over the listed members: CTA b owns the
 // 16-byte chunks [q0, q1) of every member's rows above the current layer;
@@ -774,9 +783,8 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
 constexpr uint32_t kSmallThreads = 512;
 constexpr uint32_t kSmallWarps = kSmallThreads / 32;
 
-template <int CB>
-__global__ void __launch_bounds__(kSmallThreads, 1)
-    k_decision_small(const __grid_constant__ DecisionArgs a) {
+template <int CB, int MODE>
+__device__ __forceinline__ void small_body(const DecisionArgs& a) {
   using Acc = typename Dot<CB>::Acc;
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ uint16_t nz_s[kDecMaxNz];
@@ -823,35 +831,77 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     if (lane == 0) sqa_s[r] = __dsqrt_rn(__ull2double_rn(ss));
   }
   __syncthreads();
+  // the arguments this loop reads, in registers (the server passes them in
+  // shared memory)
+  const uint64_t* const zm = a.zm;
+  const double* const sqb = a.sqb;
+  const uint8_t* const counts = a.counts;
+  double* const pref = a.pref;
+  const uint32_t j0 = a.j0, hi = a.hi, keep = a.keep, size = a.size;
+  const auto row_zero = [&](uint64_t zv, uint32_t p, uint32_t l) {
+    return zm ? ((zv >> l) & 1ull) != 0 : ld_col<MODE>(sqb + (uint64_t)p * L + l) == 0.0;
+  };
   unsigned long long mloc = ~0ull;
-  for (uint32_t p = tid; p < a.size; p += kSmallThreads) {
-    const uint64_t zv = a.zm ? a.zm[p] : 0ull;
-    const double* sb = a.sqb + (uint64_t)p * L;
-    const uint4* eb = reinterpret_cast<const uint4*>(a.counts + (uint64_t)p * LR);
-    double sm = a.j0 ? a.pref[p] : 0.0;
+  for (uint32_t p = tid; p < size; p += kSmallThreads) {
+    const uint64_t zv = zm ? ld_col<MODE>(zm + p) : 0ull;
+    const double* sb = sqb + (uint64_t)p * L;
+    const uint4* eb = reinterpret_cast<const uint4*>(counts + (uint64_t)p * LR);
+    double sm = j0 ? (MODE == 1 ? __ldcg(pref + p) : pref[p]) : 0.0;
     uint32_t k = 0;
-    for (uint32_t l = a.j0; l <= a.hi && l < L; ++l) {
+    uint32_t l = j0;
+    if (C == 1) {  // one 16-byte chunk per row: four rows' loads in flight per round
+      const uint32_t lend = min(hi + 1, L);
+      for (; l + 4 <= lend; l += 4) {
+        uint4 ev[4];
+        double sv[4];
+        uint32_t kk[4];
+        bool ex[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ex[u] = k < n_nz && nz_s[k] == l + u;
+          kk[u] = k;
+          if (ex[u]) {
+            ev[u] = ld_col<MODE>(eb + l + u);
+            sv[u] = ld_col<MODE>(sb + l + u);
+            ++k;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double r;
+          if (ex[u]) {
+            const Acc acc = Dot<CB>::chunk(prow_s[kk[u]], ev[u], (Acc)0);
+            r = row_sim_exact((uint64_t)acc, sqa_s[kk[u]], sv[u]);
+          } else {
+            r = row_zero(zv, p, l + u) ? 1.0 : 0.0;
+          }
+          sm = __dadd_rn(sm, r);  // layer order (eam.cpp:95-98)
+          if (l + u == keep) pref[p] = sm;
+        }
+      }
+    }
+    for (; l <= hi && l < L; ++l) {
       double r;
       if (k < n_nz && nz_s[k] == l) {
         Acc acc = 0;
         const uint4* pr = prow_s + (size_t)k * C;
         const uint4* er = eb + (size_t)l * C;
-        for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(pr[c], __ldg(er + c), acc);
-        r = row_sim_exact((uint64_t)acc, sqa_s[k], sb[l]);
+        for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(pr[c], ld_col<MODE>(er + c), acc);
+        r = row_sim_exact((uint64_t)acc, sqa_s[k], ld_col<MODE>(sb + l));
         ++k;
       } else {
-        r = entry_row_zero(a, zv, p, l) ? 1.0 : 0.0;
+        r = row_zero(zv, p, l) ? 1.0 : 0.0;
       }
       sm = __dadd_rn(sm, r);  // layer order (eam.cpp:95-98)
-      if (l == a.keep) a.pref[p] = sm;
+      if (l == keep) pref[p] = sm;
     }
-    if (a.zm) {
-      uint64_t bits = a.hi + 1 < 64 ? zv & ~((2ull << a.hi) - 1ull) : 0ull;
+    if (zm) {
+      uint64_t bits = hi + 1 < 64 ? zv & ~((2ull << hi) - 1ull) : 0ull;
       if (L < 64) bits &= (1ull << L) - 1ull;
       for (; bits; bits &= bits - 1) sm = __dadd_rn(sm, 1.0);
     } else {
-      for (uint32_t l = a.hi + 1; l < L; ++l)
-        if (sb[l] == 0.0) sm = __dadd_rn(sm, 1.0);
+      for (uint32_t l = hi + 1; l < L; ++l)
+        if (ld_col<MODE>(sb + l) == 0.0) sm = __dadd_rn(sm, 1.0);
     }
     const double d = finish_distance(sm, L);
     dist_s[p] = d;
@@ -880,7 +930,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
       const uint32_t mi = it / per_mem, rem = it - mi * per_mem;
       const uint32_t r = rem / wpr, w = rem - r * wpr;
       const uint32_t l = a.cur + 1 + r;
-      const uint32_t word = __ldg(reinterpret_cast<const uint32_t*>(
+      const uint32_t word = ld_col<MODE>(reinterpret_cast<const uint32_t*>(
           a.counts + (uint64_t)mem_s[mi] * LR + (uint64_t)l * RB + 4ull * w));
       if (!word) continue;
 #pragma unroll
@@ -955,6 +1005,65 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   }
   if (tid == 0) *a.n_out = S;
   stamp(a, 3);
+}
+
+template <int CB>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_decision_small(const __grid_constant__ DecisionArgs a) {
+  small_body<CB, 0>(a);
+}
+
+// One-CTA persistent server for small collections (the k_decision_small
+// phases; moe_eamc_set_decision_server): thread 0 polls the pinned mailbox,
+// the CTA copies the arguments from host memory into shared memory, runs the
+// decision (results straight into pinned host memory, as launched) and
+// publishes seq_done.  Collection reads are L1-cached plain loads ordered by
+// the request's acquire fence (ld_col).  Idle for idle_ns or asked to stop,
+// it exits.
+template <int CB>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_decision_small_server(DecServerCtl* ctl, uint64_t seq0, uint64_t idle_ns) {
+  __shared__ DecisionArgs sa;
+  __shared__ uint64_t sh_seq;
+  const uint32_t tid = threadIdx.x;
+  uint64_t last = seq0;
+  for (;;) {
+    if (tid == 0) {
+      uint64_t t0, t, sq = 0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (;;) {
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(sq) : "l"(&ctl->seq_req));
+        if (sq != last) break;
+        int stop;
+        asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(stop) : "l"(&ctl->stop));
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (stop || t - t0 > idle_ns) {
+          sq = ~0ull;
+          break;
+        }
+        __nanosleep(32);
+      }
+      sh_seq = sq;
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+    }
+    __syncthreads();
+    if (sh_seq == ~0ull) return;
+    {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(&ctl->args);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(&sa);
+      for (uint32_t i = tid; i < sizeof(DecisionArgs) / 4; i += kSmallThreads)
+        dst[i] = *reinterpret_cast<const volatile uint32_t*>(src + i);
+    }
+    __syncthreads();
+    small_body<CB, 2>(sa);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&ctl->seq_done), "l"(sh_seq) : "memory");
+    }
+    last = sh_seq;
+    __syncthreads();  // sh_seq is rewritten by the next poll
+  }
 }
 
 template <int CB>
@@ -1076,6 +1185,21 @@ __global__ void __launch_bounds__(kDecThreads, 1)
 }
 
 }  // namespace
+
+size_t decision_small_smem_max(uint32_t L, uint32_t RB) {
+  return (((size_t)L * RB + 15) & ~(size_t)15) + (size_t)kSmallMaxP * 8 + (size_t)kSmallMaxCells * 8 +
+         (size_t)L * 8 + (size_t)kSmallMaxCells * 12 + (size_t)kSmallMaxP * 4;
+}
+
+cudaError_t launch_decision_small_server(DecServerCtl* ctl, uint64_t seq0, uint64_t idle_ns, int cb,
+                                        size_t smem, cudaStream_t st) {
+  void (*kern)(DecServerCtl*, uint64_t, uint64_t) =
+      cb == 1 ? k_decision_small_server<1> : cb == 2 ? k_decision_small_server<2> : k_decision_small_server<4>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<1, kSmallThreads, smem, st>>>(ctl, seq0, idle_ns);
+  return cudaGetLastError();
+}
 
 size_t decision_small_smem(uint32_t size, uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz,
                            uint32_t cur) {

@@ -216,6 +216,9 @@ cudaError_t launch_decision(const DecisionArgs& a, int cb, int grid, size_t smem
 size_t decision_small_smem(uint32_t size, uint32_t L, uint32_t E, uint32_t RB, uint32_t n_nz,
                            uint32_t cur);
 cudaError_t launch_decision_small(const DecisionArgs& a, int cb, size_t smem, cudaStream_t st);
+// Shared memory of the small-path kernel for any request it takes (size <= kSmallMaxP,
+// rows above x E <= kSmallMaxCells, all L probe rows explicit).
+size_t decision_small_smem_max(uint32_t L, uint32_t RB);
 constexpr uint32_t kSmallMaxP = 512;        // entries (one per thread)
 constexpr uint32_t kSmallMaxCells = 1024;   // (L - cur - 1) * E candidates
 // The persistent decision server's mailbox (pinned host memory, device-mapped).
@@ -226,6 +229,9 @@ struct DecServerCtl {
   int pad_;
   DecisionArgs args;  // the request (host-side pointers for rows/nz when not inline)
 };
+// One-CTA persistent server for small collections (moe_eamc_set_decision_server).
+cudaError_t launch_decision_small_server(DecServerCtl* ctl, uint64_t seq0, uint64_t idle_ns, int cb,
+                                        size_t smem, cudaStream_t st);
 cudaError_t launch_decision_server(DecServerCtl* ctl, DecisionArgs* dargs, uint8_t* drows,
                                    uint32_t* go, uint32_t* done, uint32_t* bar, uint64_t seq0,
                                    uint32_t k0, uint64_t idle_ns, uint32_t gen, int cb, int grid,

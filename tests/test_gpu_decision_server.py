@@ -83,6 +83,44 @@ def test_server_width_change_idle_and_destroy(m, orc):
     _check(m, orc, e3, ents, seqs, probe, 4, s)
 
 
+def test_small_server_switches_kinds(m, orc):
+    """A small collection is served by the one-CTA server (the k_decision_small
+    phases); when it grows past the small path's bound the multi-CTA server
+    takes over, and back -- orders bitwise equal to the oracle throughout,
+    including collection updates seen by the resident kernel."""
+    L, E, k = 32, 8, 2
+    w = Workload(L, E, k, seed=23)
+    ents = orc.request_eams(w, 900)
+    s = m.ModelShape(L, E, k)
+    e = m.Eamc(s, m.Phase.decode, 900)
+    e.append(ents[:300], np.arange(300, dtype=np.uint64))
+    _server(m, e, 8)
+    base = orc.iteration_probe(w, 777, 2, L - 1)
+    for P in (300, 400, 900, 900):
+        if P > e.size():
+            e.append(ents[e.size():P], np.arange(e.size(), P, dtype=np.uint64))
+        seqs = np.arange(P, dtype=np.uint64)
+        for layer in (0, 3, L // 2, L - 2):
+            pr = base.copy()
+            pr[layer + 1:] = 0
+            _check(m, orc, e, ents[:P], seqs, pr, layer, s)
+    small = m.Eamc(s, m.Phase.decode, 300)
+    small.append(ents[:300], np.arange(300, dtype=np.uint64))
+    _server(m, small, 8)
+    for j in range(40):  # unrelated probes, every layer: no prefix reuse
+        pr = orc.iteration_probe(w, 5000 + j, 2, j % (L - 1))
+        _check(m, orc, small, ents[:300], np.arange(300, dtype=np.uint64), pr, j % (L - 1), s)
+    # entries replaced in place (at-capacity inserts) while the server is
+    # resident and has read them: the next decisions see the new contents
+    small.build(ents[300:420])
+    want_ent, want_seqs, _ = orc.insert_replay(L, E, 300, ents[:420])
+    for j in range(12):
+        pr = orc.iteration_probe(w, 6000 + j, 2, j % (L - 1))
+        _check(m, orc, small, want_ent, want_seqs, pr, j % (L - 1), s)
+    _server(m, small, 0)
+    _server(m, e, 0)
+
+
 @pytest.mark.timeout(300)
 def test_concurrent_decisions_two_handles(m, orc):
     """Two handles deciding at once from two host threads (two streams): the
