@@ -1313,8 +1313,30 @@ cudaError_t launch_decision(const DecisionArgs& a, int cb, int grid, size_t smem
   if (smem > max_dyn[slot]) return cudaErrorInvalidValue;
   // grid <= SMs and one CTA per SM (launch bounds, shared memory): all CTAs
   // are co-resident once scheduled, which the software barrier relies on
+  static const bool prof = getenv("MOE_LAUNCH_PROF") != nullptr;
+  if (!prof) {
+    kern<<<(unsigned)grid, kDecThreads, smem, st>>>(a);
+    return cudaGetLastError();
+  }
+  // launch-path instrumentation (MOE_LAUNCH_PROF=1)
+  static double acc[3] = {0, 0, 0};
+  static uint64_t cnt = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaError_t q = cudaStreamQuery(st);
+  const auto t1 = std::chrono::steady_clock::now();
   kern<<<(unsigned)grid, kDecThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  const auto t2 = std::chrono::steady_clock::now();
+  cudaError_t e = cudaGetLastError();
+  const auto t3 = std::chrono::steady_clock::now();
+  acc[0] += std::chrono::duration<double, std::micro>(t1 - t0).count();
+  acc[1] += std::chrono::duration<double, std::micro>(t2 - t1).count();
+  acc[2] += std::chrono::duration<double, std::micro>(t3 - t2).count();
+  if (++cnt % 58 == 0)
+    fprintf(stderr, "k_decision launch (avg of %llu, grid %d, smem %zu, params %zu B): query %.1f us "
+                    "(%d), <<<>>> %.1f us, getlasterror %.1f us\n",
+            (unsigned long long)cnt, grid, smem, sizeof(DecisionArgs), acc[0] / cnt, (int)q,
+            acc[1] / cnt, acc[2] / cnt);
+  return e;
 }
 
 }  // namespace moe

@@ -323,17 +323,23 @@ __device__ __forceinline__ void lane_flush(const LaneArgs& a, uint32_t* cnt, uin
                                            uint32_t NC, OUT* dst, int sign) {
   const uint32_t t = threadIdx.x, L = a.L, E = a.E, k = a.k, ES = E | 1, NCOL = a.NCOL;
   consumers_sync(NC);
+  const uint32_t CM = a.C / a.H;  // columns per position pair
+  // whole words per layer, one column each: a cell's words belong to it alone,
+  // so the reader zeroes them (no separate zeroing pass, one barrier less)
+  const bool own = CM == 1 && (k & 1) == 0 && k <= 8;
   {  // cell (l, e), layer fastest: conflict-free reads
     const uint32_t de = NC / L, dl = NC - de * L;
     uint32_t e = t / L, l = t - e * L;
-    const uint32_t CM = a.C / a.H;  // columns per position pair
-    if (CM == 1 && (k & 1) == 0 && k <= 8) {  // whole words per layer, one column each
+    if (own) {
       const uint32_t kh = k >> 1;
       for (; e < E;) {
-        const uint32_t* cw = cnt + e * NCOL + l * kh;
+        uint32_t* cw = cnt + e * NCOL + l * kh;
         uint32_t c[4];
 #pragma unroll
         for (int w = 0; w < 4; ++w) c[w] = w < (int)kh ? cw[w] : 0u;
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (w < (int)kh) cw[w] = 0u;
         uint32_t sum = 0;
 #pragma unroll
         for (int w = 0; w < 4; ++w) sum += (c[w] & 0xffffu) + (c[w] >> 16);
@@ -360,11 +366,19 @@ __device__ __forceinline__ void lane_flush(const LaneArgs& a, uint32_t* cnt, uin
       }
     }
   }
-  for (uint32_t i = t; i < NCOL; i += NC)  // the trash row: ids >= E
-    if (cnt[E * NCOL + i] != 0 && sign > 0) *a.bad = 1;
-  consumers_sync(NC);
-  for (uint32_t i = t; i < (E + 2) * NCOL / 4; i += NC)
-    reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  if (own) {  // the trash row (ids >= E) and the null row (masked slots)
+    for (uint32_t i = t; i < 2 * NCOL; i += NC) {
+      if (i < NCOL && cnt[E * NCOL + i] != 0 && sign > 0) *a.bad = 1;
+      cnt[E * NCOL + i] = 0u;
+    }
+    consumers_sync(NC);
+  } else {
+    for (uint32_t i = t; i < NCOL; i += NC)  // the trash row: ids >= E
+      if (cnt[E * NCOL + i] != 0 && sign > 0) *a.bad = 1;
+    consumers_sync(NC);
+    for (uint32_t i = t; i < (E + 2) * NCOL / 4; i += NC)
+      reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
+  }
   // reductions without a return value: no thread waits on the counts' latency
   {
     const uint32_t dl = NC / E, de = NC - dl * E;
@@ -377,7 +391,9 @@ __device__ __forceinline__ void lane_flush(const LaneArgs& a, uint32_t* cnt, uin
       if (e >= E) e -= E, ++l;
     }
   }
-  consumers_sync(NC);
+  // with own: the counters are zero since the barrier above, and the staging
+  // row is rewritten only after the next flush's first barrier
+  if (!own) consumers_sync(NC);
 }
 
 template <typename OUT>
