@@ -38,6 +38,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -780,6 +782,21 @@ __device__ __forceinline__ void decision_body(const DecisionArgs& a) {
 // aggregation with shared-memory u64 atomics, and the order as one bitonic
 // sort of all (~bits(priority), flat ExpertId) pairs in shared memory -- with
 // no grid barriers and no global atomics.  (MIX: P=300, 31 x 8 candidates.)
+#ifndef SMALL_ROWS_U
+#define SMALL_ROWS_U 4
+#endif
+constexpr int kSmallRowsU = SMALL_ROWS_U;
+constexpr uint32_t kSmallMaxCluster = 16;
+
+// Byte offset of the staged row similarities r[entries][n_nz] of the cluster
+// launch (after the members list; the layout of small_body's shared memory,
+// see decision_small_smem).
+__host__ __device__ __forceinline__ size_t small_rsim_offset(uint32_t n_nz, uint32_t RB, uint32_t size,
+                                                             uint32_t N, uint32_t rows, uint32_t N2) {
+  const size_t b = (((size_t)n_nz * RB + 15) & ~(size_t)15) + (size_t)size * 8 + (size_t)N * 8 +
+                   (size_t)rows * 8 + (size_t)N2 * 12 + (size_t)size * 4;
+  return (b + 15) & ~(size_t)15;
+}  // rows per round of the per-entry loop (A/B builds)
 constexpr uint32_t kSmallThreads = 512;
 constexpr uint32_t kSmallWarps = kSmallThreads / 32;
 
@@ -791,7 +808,8 @@ __device__ __forceinline__ void small_body(const DecisionArgs& a) {
   __shared__ double sqa_s[kDecMaxNz];
   __shared__ unsigned long long red_s[kSmallWarps];
   __shared__ uint32_t cnt_s[kSmallWarps + 1];
-  __shared__ unsigned long long dmin_s;
+  __shared__ unsigned long long dmin_s, exm_s;
+  __shared__ unsigned long long cmin_s[kSmallMaxCluster];  // per-CTA minima (cluster launch)
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t L = a.L, E = a.E, RB = a.RB, C = RB / 16;
   const uint64_t LR = (uint64_t)L * RB;
@@ -830,7 +848,15 @@ __device__ __forceinline__ void small_body(const DecisionArgs& a) {
     ss = warp_sum_u64(ss);
     if (lane == 0) sqa_s[r] = __dsqrt_rn(__ull2double_rn(ss));
   }
+  if (wid == 0 && L <= 64) {  // the explicit rows as a bit mask (no smem chain in the loop)
+    unsigned long long m = 0;
+    for (uint32_t i = lane; i < n_nz; i += 32) m |= 1ull << nz_s[i];
+    const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)m);
+    const uint32_t hi2 = __reduce_or_sync(0xffffffffu, (uint32_t)(m >> 32));
+    if (lane == 0) exm_s = (unsigned long long)lo | ((unsigned long long)hi2 << 32);
+  }
   __syncthreads();
+  stamp(a, 4);
   // the arguments this loop reads, in registers (the server passes them in
   // shared memory)
   const uint64_t* const zm = a.zm;
@@ -842,22 +868,160 @@ __device__ __forceinline__ void small_body(const DecisionArgs& a) {
     return zm ? ((zv >> l) & 1ull) != 0 : ld_col<MODE>(sqb + (uint64_t)p * L + l) == 0.0;
   };
   unsigned long long mloc = ~0ull;
-  for (uint32_t p = tid; p < size; p += kSmallThreads) {
+  uint32_t crank = 0, csize = 1;  // a plain launch is a cluster of one
+  if (MODE == 0) {
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+  }
+  if (csize > 1) {
+    // Cluster launch: the fp64 row similarities (a correctly rounded division
+    // each; one SM's FP64 pipe bounded the one-CTA loop) are spread over the
+    // cluster.  CTA c takes the entries p = c (mod csize); its (entry,
+    // explicit row) items are independent, staged as r[j][k] in its shared
+    // memory, then summed per entry in layer order (eam.cpp:95-98).  The
+    // distances and per-CTA minima go to CTA 0's shared memory (DSMEM), which
+    // runs phases B and C alone after the cluster barrier.
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t nloc = size > crank ? (size - crank + csize - 1) / csize : 0;
+    const uint32_t items = nloc * n_nz;
+    double* r_s = reinterpret_cast<double*>(
+        dsm + small_rsim_offset(n_nz, RB, size, N, rows_above, N2));
+    if (C == 1) {  // two items per thread and round: both rows' loads in flight
+      for (uint32_t i0 = tid; i0 < items; i0 += 2 * kSmallThreads) {
+        uint4 ev[2];
+        double sv[2];
+        uint32_t kk[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t i = i0 + u * kSmallThreads;
+          kk[u] = 0;
+          if (i < items) {
+            const uint32_t j = i / n_nz, k = i - j * n_nz, p = crank + csize * j, l = nz_s[k];
+            kk[u] = k;
+            ev[u] = ld_col<MODE>(reinterpret_cast<const uint4*>(counts + (uint64_t)p * LR + (uint64_t)l * RB));
+            sv[u] = ld_col<MODE>(sqb + (uint64_t)p * L + l);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t i = i0 + u * kSmallThreads;
+          if (i < items) {
+            const Acc acc = Dot<CB>::chunk(prow_s[kk[u]], ev[u], (Acc)0);
+            r_s[i] = row_sim_exact((uint64_t)acc, sqa_s[kk[u]], sv[u]);
+          }
+        }
+      }
+    } else {
+      for (uint32_t i = tid; i < items; i += kSmallThreads) {
+        const uint32_t j = i / n_nz, k = i - j * n_nz, p = crank + csize * j, l = nz_s[k];
+        const uint4* er = reinterpret_cast<const uint4*>(counts + (uint64_t)p * LR + (uint64_t)l * RB);
+        const uint4* pr = prow_s + (size_t)k * C;
+        Acc acc = 0;
+        for (uint32_t c = 0; c < C; ++c) acc = Dot<CB>::chunk(pr[c], ld_col<MODE>(er + c), acc);
+        r_s[i] = row_sim_exact((uint64_t)acc, sqa_s[k], ld_col<MODE>(sqb + (uint64_t)p * L + l));
+      }
+    }
+    __syncthreads();
+    double* dist0 = cl.map_shared_rank(dist_s, 0);
+    for (uint32_t j = tid; j < nloc; j += kSmallThreads) {
+      const uint32_t p = crank + csize * j;
+      const uint64_t zv = zm ? ld_col<MODE>(zm + p) : 0ull;
+      double sm = j0 ? pref[p] : 0.0;
+      const double* rp = r_s + (size_t)j * n_nz;
+      uint32_t k = 0;
+      for (uint32_t l = j0; l <= hi && l < L; ++l) {
+        double r;
+        if (k < n_nz && nz_s[k] == l) r = rp[k++];
+        else r = row_zero(zv, p, l) ? 1.0 : 0.0;
+        sm = __dadd_rn(sm, r);  // layer order (eam.cpp:95-98)
+        if (l == keep) pref[p] = sm;
+      }
+      if (zm) {
+        uint64_t bits = hi + 1 < 64 ? zv & ~((2ull << hi) - 1ull) : 0ull;
+        if (L < 64) bits &= (1ull << L) - 1ull;
+        for (; bits; bits &= bits - 1) sm = __dadd_rn(sm, 1.0);
+      } else {
+        for (uint32_t l = hi + 1; l < L; ++l)
+          if (ld_col<MODE>(sqb + (uint64_t)p * L + l) == 0.0) sm = __dadd_rn(sm, 1.0);
+      }
+      const double d = finish_distance(sm, L);
+      dist0[p] = d;
+      const unsigned long long db = (unsigned long long)__double_as_longlong(d);
+      mloc = db < mloc ? db : mloc;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, mloc, o);
+      mloc = x < mloc ? x : mloc;
+    }
+    if (lane == 0) red_s[wid] = mloc;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long m = ~0ull;
+      for (uint32_t w = 0; w < kSmallWarps; ++w) m = red_s[w] < m ? red_s[w] : m;
+      cl.map_shared_rank(cmin_s, 0)[crank] = m;
+    }
+    cl.sync();  // release/acquire: CTA 0 sees every distance and minimum
+    if (crank != 0) return;
+    if (tid == 0) {
+      unsigned long long m = ~0ull;
+      for (uint32_t c = 0; c < csize; ++c) m = cmin_s[c] < m ? cmin_s[c] : m;
+      dmin_s = m;
+    }
+    __syncthreads();
+  }
+  for (uint32_t p = tid; p < size && csize == 1; p += kSmallThreads) {
     const uint64_t zv = zm ? ld_col<MODE>(zm + p) : 0ull;
     const double* sb = sqb + (uint64_t)p * L;
     const uint4* eb = reinterpret_cast<const uint4*>(counts + (uint64_t)p * LR);
     double sm = j0 ? (MODE == 1 ? __ldcg(pref + p) : pref[p]) : 0.0;
     uint32_t k = 0;
     uint32_t l = j0;
-    if (C == 1) {  // one 16-byte chunk per row: four rows' loads in flight per round
+    if (C == 1 && L <= 64) {
+      // one 16-byte chunk per row; the explicit rows and their probe-row index
+      // come from the mask, so a round's loads issue without waiting on
+      // shared memory
+      constexpr int U = kSmallRowsU;
+      const uint64_t exm = exm_s;
       const uint32_t lend = min(hi + 1, L);
-      for (; l + 4 <= lend; l += 4) {
-        uint4 ev[4];
-        double sv[4];
-        uint32_t kk[4];
-        bool ex[4];
+      for (; l + U <= lend; l += U) {
+        uint4 ev[U];
+        double sv[U];
+        bool ex[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
+          ex[u] = (exm >> (l + u)) & 1ull;
+          if (ex[u]) {
+            ev[u] = ld_col<MODE>(eb + l + u);
+            sv[u] = ld_col<MODE>(sb + l + u);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          double r;
+          if (ex[u]) {
+            const uint32_t kq = __popcll(exm & ((1ull << (l + u)) - 1ull));
+            const Acc acc = Dot<CB>::chunk(prow_s[kq], ev[u], (Acc)0);
+            r = row_sim_exact((uint64_t)acc, sqa_s[kq], sv[u]);
+          } else {
+            r = row_zero(zv, p, l + u) ? 1.0 : 0.0;
+          }
+          sm = __dadd_rn(sm, r);  // layer order (eam.cpp:95-98)
+          if (l + u == keep) pref[p] = sm;
+        }
+      }
+      k = l >= 64 ? (uint32_t)__popcll(exm) : (uint32_t)__popcll(exm & ((1ull << l) - 1ull));
+    } else if (C == 1) {  // one 16-byte chunk per row: kSmallRowsU rows' loads in flight per round
+      constexpr int U = kSmallRowsU;
+      const uint32_t lend = min(hi + 1, L);
+      for (; l + U <= lend; l += U) {
+        uint4 ev[U];
+        double sv[U];
+        uint32_t kk[U];
+        bool ex[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
           ex[u] = k < n_nz && nz_s[k] == l + u;
           kk[u] = k;
           if (ex[u]) {
@@ -867,7 +1031,7 @@ __device__ __forceinline__ void small_body(const DecisionArgs& a) {
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           double r;
           if (ex[u]) {
             const Acc acc = Dot<CB>::chunk(prow_s[kk[u]], ev[u], (Acc)0);
@@ -908,13 +1072,16 @@ __device__ __forceinline__ void small_body(const DecisionArgs& a) {
     const unsigned long long db = (unsigned long long)__double_as_longlong(d);
     mloc = db < mloc ? db : mloc;
   }
+  stamp(a, 5);
+  if (csize == 1) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long x = __shfl_xor_sync(0xffffffffu, mloc, o);
-    mloc = x < mloc ? x : mloc;
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long x = __shfl_xor_sync(0xffffffffu, mloc, o);
+      mloc = x < mloc ? x : mloc;
+    }
+    if (lane == 0) atomicMin(&dmin_s, mloc);
+    __syncthreads();
   }
-  if (lane == 0) atomicMin(&dmin_s, mloc);
-  __syncthreads();
   stamp(a, 1);
   // ---- B: window members (eam.cpp:143) and their rows above cur
   const double thr = __dadd_rn(__longlong_as_double((long long)dmin_s), a.window);
@@ -1210,6 +1377,19 @@ size_t decision_small_smem(uint32_t size, uint32_t L, uint32_t E, uint32_t RB, u
          (size_t)rows * 8 + (size_t)N2 * 12 + (size_t)size * 4;
 }
 
+// Cluster size of a small-path launch: the row similarities of enough
+// (entry, explicit row) pairs are spread over a cluster (MOE_DEC_CLUSTER=<n>
+// overrides, 1 = the one-CTA kernel; A/B runs).
+static uint32_t small_cluster(uint32_t size, uint32_t n_nz) {
+  static const int env = [] {
+    const char* e = getenv("MOE_DEC_CLUSTER");
+    return e ? atoi(e) : -1;
+  }();
+  uint32_t n = env >= 1 ? (uint32_t)std::min<int>(env, (int)kSmallMaxCluster) : 8u;
+  if (env < 1 && (uint64_t)size * n_nz < 1024) n = 1;
+  return n;
+}
+
 cudaError_t launch_decision_small(const DecisionArgs& a, int cb, size_t smem, cudaStream_t st) {
   void (*kern)(DecisionArgs) =
       cb == 1 ? k_decision_small<1> : cb == 2 ? k_decision_small<2> : k_decision_small<4>;
@@ -1222,6 +1402,42 @@ cudaError_t launch_decision_small(const DecisionArgs& a, int cb, size_t smem, cu
     set[slot] = smem;
   }
   static const bool prof = getenv("MOE_LAUNCH_PROF") != nullptr;
+  const uint32_t ncl = small_cluster(a.size, a.n_nz);
+  if (ncl > 1) {
+    // the cluster's CTAs also stage their entries' row similarities
+    const uint32_t rows = a.cur + 1 < a.L ? a.L - a.cur - 1 : 0, N = rows * a.E;
+    uint32_t N2 = 1;
+    while (N2 < N) N2 <<= 1;
+    const size_t need = small_rsim_offset(a.n_nz, a.RB, a.size, N, rows, N2) +
+                        (size_t)((a.size + ncl - 1) / ncl) * a.n_nz * 8;
+    smem = std::max(smem, need);
+    if (smem > set[slot]) {
+      cudaError_t e =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      set[slot] = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncl);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ncl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static bool nonportable[3] = {false, false, false};
+    if (ncl > 8 && !nonportable[slot]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      nonportable[slot] = true;
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   if (!prof) {
     kern<<<1, kSmallThreads, smem, st>>>(a);
     return cudaGetLastError();
