@@ -817,6 +817,48 @@ def test_prefetch_small_collection(m, orc, L, E, P, mult):
             assert np.array_equal(out["priority"], op)
 
 
+@pytest.mark.parametrize("L,E,P,mult", [(72, 8, 150, 1), (32, 8, 509, 1), (20, 8, 64, 70000),
+                                        (12, 8, 9, 1)])
+def test_prefetch_small_cluster_shapes(m, orc, L, E, P, mult):
+    """The small-path decision kernel launched as a thread-block cluster
+    (size x explicit rows >= 1,024; decide.cu small_body): L > 64 (no
+    zero-row mask), entry counts not a multiple of the cluster size, u32
+    storage (counts of 70,000), and a collection small enough for one CTA."""
+    w = Workload(L, E, 2, n_groups=5, prompt_len=3, decode_len=4, batch_size=2, seed=L * 7 + P)
+    ents = orc.request_eams(w, P) * mult
+    s = m.ModelShape(L, E, 2)
+    e = m.Eamc(s, m.Phase.decode, P)
+    e.build(ents)
+    for r, it, layer in [(800, 1, 0), (801, 2, L // 3), (802, 3, (2 * L) // 3), (803, 4, L - 2)]:
+        pr = orc.iteration_probe(w, r, it, layer) * mult
+        ol, ox, op = orc.prefetch(ents, seqs_of(P), pr, layer, True)
+        out = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), e, layer, True)
+        assert np.array_equal(out["layer_idx"], ol)
+        assert np.array_equal(out["expert_idx"], ox)
+        assert np.array_equal(out["priority"], op)
+
+
+def test_prefetch_small_cluster_decode_sequence(m, orc):
+    """One decode step on a small collection: the iteration EAM grows by one
+    row per call, so the cluster path reuses the stored layer-prefix sums
+    (j0 > 0) -- every call's order equals the oracle's."""
+    L, E, P = 32, 8, 300
+    w = Workload(L, E, 2, n_groups=6, prompt_len=3, decode_len=4, batch_size=2, seed=4242)
+    ents = orc.request_eams(w, P)
+    s = m.ModelShape(L, E, 2)
+    e = m.Eamc(s, m.Phase.decode, P)
+    e.build(ents)
+    full = orc.iteration_probe(w, 900, 2, L - 1)
+    for layer in range(L - 1):
+        pr = full.copy()
+        pr[layer + 1:] = 0
+        ol, ox, op = orc.prefetch(ents, seqs_of(P), pr, layer, True)
+        out = m.prefetch_order(m.Eam(s, m.EamKind.iteration, counts=pr), e, layer, True)
+        assert np.array_equal(out["layer_idx"], ol), layer
+        assert np.array_equal(out["expert_idx"], ox), layer
+        assert np.array_equal(out["priority"], op), layer
+
+
 def test_concurrent_readers_one_handle(m, orc):
     """match / prefetch are const readers (eam.hpp:89-94): concurrent calls on
     one handle from several host threads give the serial results."""
