@@ -1849,9 +1849,9 @@ static moe_status run_decision(moe_eamc* h, moe::DecisionArgs& a, size_t stage_r
       CK(cudaStreamSynchronize(st));
       if (dec_timing()) {
         const auto t2 = std::chrono::steady_clock::now();
-        static double acc[8] = {0};
+        static double acc[11] = {0};
         static uint64_t cnt = 0;
-        unsigned long long ts[6];
+        unsigned long long ts[8];
         CK(cudaMemcpy(ts, h->tprobe.p, sizeof ts, cudaMemcpyDeviceToHost));
         acc[0] += std::chrono::duration<double, std::micro>(t1 - t0).count();
         acc[1] += std::chrono::duration<double, std::micro>(t2 - t1).count();
@@ -1860,11 +1860,17 @@ static moe_status run_decision(moe_eamc* h, moe::DecisionArgs& a, size_t stage_r
         acc[5] += (ts[4] - ts[0]) * 1e-3;
         acc[6] += (ts[5] - ts[4]) * 1e-3;
         acc[7] += (ts[1] - ts[5]) * 1e-3;
+        // phase C split: row sums (2..6), priorities + compaction (6..7), rank + output (7..3)
+        acc[8] += (ts[6] - ts[2]) * 1e-3;
+        acc[9] += (ts[7] - ts[6]) * 1e-3;
+        acc[10] += (ts[3] - ts[7]) * 1e-3;
         if (++cnt % 58 == 0)
           fprintf(stderr, "small decision (avg of %llu): launch %.1f us, launch->done %.1f us | "
-                          "A %.1f (rows %.1f, entries %.1f, min %.1f) B %.1f C %.1f\n",
+                          "A %.1f (rows %.1f, entries %.1f, min %.1f) B %.1f C %.1f (rowsum %.1f, "
+                          "priorities %.1f, rank %.1f)\n",
                   (unsigned long long)cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[5] / cnt,
-                  acc[6] / cnt, acc[7] / cnt, acc[3] / cnt, acc[4] / cnt);
+                  acc[6] / cnt, acc[7] / cnt, acc[3] / cnt, acc[4] / cnt, acc[8] / cnt,
+                  acc[9] / cnt, acc[10] / cnt);
       }
       const uint32_t n = *reinterpret_cast<volatile uint32_t*>(a.n_out);
       if (n_out) *n_out = n;

@@ -1120,6 +1120,7 @@ __device__ __forceinline__ void small_body(const DecisionArgs& a) {
     if (lane == 0) rsum_s[r] = s;
   }
   __syncthreads();
+  stamp(a, 6);
   // survivors compacted in flat ExpertId order (ballot prefix), then each
   // survivor's output position = the number of survivor pairs below it
   const double kEps = 1e-4;
@@ -1159,6 +1160,7 @@ __device__ __forceinline__ void small_body(const DecisionArgs& a) {
     __syncthreads();
   }
   const uint32_t S = base;
+  stamp(a, 7);
   for (uint32_t i = tid; i < S; i += kSmallThreads) {
     const unsigned long long ki = key_s[i];
     const uint32_t ii = id_s[i];
