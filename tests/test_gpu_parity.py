@@ -859,6 +859,24 @@ def test_prefetch_small_cluster_decode_sequence(m, orc):
         assert np.array_equal(out["priority"], op), layer
 
 
+@pytest.mark.parametrize("n", ["1", "2"])
+def test_prefetch_small_cluster_sizes(n):
+    """The small-collection parity cases with other cluster sizes
+    (MOE_DEC_CLUSTER: 1 = the one-CTA kernel, 2 = a two-CTA cluster; the
+    default is 8), in a subprocess since the switch is read once."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MOE_DEC_CLUSTER=n)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        "tests/test_gpu_parity.py", "-k",
+                        "small_cluster_shapes or small_cluster_decode or small_collection"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert " passed" in r.stdout
+
+
 def test_concurrent_readers_one_handle(m, orc):
     """match / prefetch are const readers (eam.hpp:89-94): concurrent calls on
     one handle from several host threads give the serial results."""
