@@ -929,13 +929,23 @@ __device__ __forceinline__ void small_body(const DecisionArgs& a) {
       const uint64_t zv = zm ? ld_col<MODE>(zm + p) : 0ull;
       double sm = j0 ? pref[p] : 0.0;
       const double* rp = r_s + (size_t)j * n_nz;
-      uint32_t k = 0;
-      for (uint32_t l = j0; l <= hi && l < L; ++l) {
-        double r;
-        if (k < n_nz && nz_s[k] == l) r = rp[k++];
-        else r = row_zero(zv, p, l) ? 1.0 : 0.0;
-        sm = __dadd_rn(sm, r);  // layer order (eam.cpp:95-98)
-        if (l == keep) pref[p] = sm;
+      if (L <= 64) {  // explicit rows from the mask: the loads do not wait on a chain
+        const uint64_t exm = exm_s;
+        for (uint32_t l = j0; l <= hi && l < L; ++l) {
+          const double r = (exm >> l) & 1ull ? rp[__popcll(exm & ((1ull << l) - 1ull))]
+                           : row_zero(zv, p, l) ? 1.0 : 0.0;
+          sm = __dadd_rn(sm, r);  // layer order (eam.cpp:95-98)
+          if (l == keep) pref[p] = sm;
+        }
+      } else {
+        uint32_t k = 0;
+        for (uint32_t l = j0; l <= hi && l < L; ++l) {
+          double r;
+          if (k < n_nz && nz_s[k] == l) r = rp[k++];
+          else r = row_zero(zv, p, l) ? 1.0 : 0.0;
+          sm = __dadd_rn(sm, r);  // layer order (eam.cpp:95-98)
+          if (l == keep) pref[p] = sm;
+        }
       }
       if (zm) {
         uint64_t bits = hi + 1 < 64 ? zv & ~((2ull << hi) - 1ull) : 0ull;
